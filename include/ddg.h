@@ -1,0 +1,175 @@
+/*
+ * ddg.h — C ABI of libddg, the B200-native DDG-preconditioned CG solver.
+ *
+ * Method: Edwards & Bridson, "The Discretely-Discontinuous Galerkin Coarse
+ * Grid for Domain Decomposition", arXiv:1504.00907.  Conjugate
+ * gradient (§7) on a sparse SPD system A u = f
+ * (Table 1), preconditioned by the two-level symmetric
+ * multiplicative overlapping Schwarz method (§6) whose
+ * coarse level is the DDG space: each generating vector (column of F,
+ * PAPER.md:239-241) restricted to each non-overlapping part Omega_I and
+ * orthonormalised per part is one basis function; the
+ * coarse matrix is the Galerkin projection A_c = P^T A P (PAPER.md:266,
+ * written A_0 = R_0 A R_0^T there; P = R_0^T).
+ *
+ * Everything below runs on one CUDA device per context.  All numerics are
+ * IEEE fp64.  There is no CPU fallback: with no usable device every entry
+ * point returns DDG_E_CUDA.
+ *
+ * Ownership: every input pointer is BORROWED for the duration of the call and
+ * copied; the context owns all device memory it allocates; outputs go into
+ * caller-allocated buffers.  A context is not thread-safe; one context per
+ * GPU / rank; a context can be reused for any number of solves.
+ *
+ * Errors: every int-returning call returns a ddg_status.  On error a
+ * stage-labelled, thread-local message is available from ddg_last_error().
+ */
+#ifndef DDG_H
+#define DDG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DDG_OK = 0,
+    DDG_E_ARG = 1,         /* null pointer, bad size (message carries sizes)          */
+    DDG_E_DIM = 2,         /* dimension mismatch / non-canonical CSR                  */
+    DDG_E_PART = 3,        /* empty part or part id out of range                      */
+    DDG_E_ZERO_BLOCK = 4,  /* F restricted to a part is entirely zero   */
+    DDG_E_NOT_SPD = 5,     /* non-positive pivot in a local or the coarse factor
+                              (SPEC.md:73); message names stage, block and pivot      */
+    DDG_E_COLOURING = 6,   /* internal colouring check failed                         */
+    DDG_E_BREAKDOWN = 7,   /* p^T A p <= 0 or r^T z <= 0 inside PCG     */
+    DDG_E_CUDA = 8,        /* CUDA runtime error or no device                         */
+    DDG_E_NCCL = 9,        /* communicator error                                      */
+    DDG_E_OOM = 10         /* device allocation failed                                */
+} ddg_status;
+
+typedef struct ddg_ctx ddg_ctx;
+
+/* Stopping rule readings of "a 10^-9 reduction in residual after the first
+ * application of the preconditioner"; reading R1. */
+enum { DDG_STOP_RES0 = 0,      /* ||r_k||_2 <= rtol ||r_0||_2 (default)              */
+       DDG_STOP_RES1 = 1,      /* ||r_k||_2 <= rtol ||r_1||_2           */
+       DDG_STOP_PREC = 2 };    /* sqrt(r_k^T z_k) <= rtol sqrt(r_0^T z_0)             */
+
+typedef struct {
+    int overlap;          /* Delta: graph distance in the pattern of A. default 1 */
+    double rank_tol;      /* keep column j of a part iff |R_jj| >= rank_tol * max_j ||F_I e_j||
+                             (reading R7). default 1e-8            */
+    int stop_mode;        /* DDG_STOP_*, default DDG_STOP_RES0                                   */
+    int max_iter;         /* default 1000                                         */
+    int device;           /* CUDA device ordinal; default 0                                       */
+    void* stream;         /* cudaStream_t to run on, or NULL: the context creates its own stream   */
+    int use_graphs;       /* 1 (default): capture the preconditioner in a CUDA graph               */
+    int verbose;          /* 0 (default): quiet; 1: setup timings on stderr                        */
+} ddg_opts;
+
+typedef struct {
+    int converged;        /* 1 if the stopping rule was met                                     */
+    int iters;            /* number of A p products (reading R16)              */
+    double res0;          /* ||r_0||_2 = ||f||_2                                                 */
+    double res_final;     /* last recurrence residual ||r_k||_2                                  */
+    double t_setup;       /* seconds spent in ddg_setup (host clock around device work)          */
+    double t_solve;       /* seconds of the last solve (CUDA events on the context stream)       */
+    double frac_iters;    /* fractional iteration count                       */
+} ddg_report;
+
+typedef struct {
+    int64_t n;            /* fine unknowns                                                      */
+    int64_t n_c;          /* coarse unknowns after rank pruning                                 */
+    int32_t nparts;       /* number of parts Omega_I = number of overlapping subdomains         */
+    int32_t ncolours;     /* colours of the multiplicative sweep                                */
+    int32_t m_min, m_max; /* min / max |Omega~_i|                                               */
+    int32_t k;            /* generating vectors per part before pruning                          */
+    int32_t dropped;      /* total columns dropped by the rank test                              */
+    double min_rank_ratio;          /* min over parts and kept j of |R_jj| / max_j ||F_I e_j||  */
+    int64_t local_factor_bytes;     /* bytes of the stored local operators (device)            */
+    int64_t coarse_factor_bytes;    /* bytes of the stored coarse operator (device)            */
+    int32_t coarse_variant;         /* 1 dense packed inverse, 2 sparse supernodal             */
+    int32_t pad;
+} ddg_info;
+
+/* Fills *o with the defaults listed above. */
+void ddg_default_opts(ddg_opts* o);
+
+/*
+ * ddg_setup — build the preconditioner for A.
+ *   n                 fine unknowns (>= 1)
+ *   row_ptr[n+1]      int64 CSR row offsets, row_ptr[0] = 0            (host)
+ *   col[nnz]          int32 column indices, strictly increasing per row (host)
+ *   val[nnz]          fp64 values; A must be symmetric positive definite (host)
+ *   F[n*k]            fp64 generating vectors, column-major n x k       (host)
+ *   k                 number of generating vectors (1..64)
+ *   part[n]           int32 part id of every unknown, 0..nparts-1; every part non-empty
+ *   nparts            number of parts
+ *   opts              NULL for defaults
+ *   out               receives the new context
+ * Errors: DDG_E_ARG, DDG_E_DIM, DDG_E_PART, DDG_E_ZERO_BLOCK, DDG_E_NOT_SPD,
+ *         DDG_E_CUDA, DDG_E_OOM.  On error *out is NULL.
+ */
+int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+              const double* F, int k, const int32_t* part, int32_t nparts,
+              const ddg_opts* opts, ddg_ctx** out);
+
+/*
+ * ddg_pcg_solve — solve A u = f from u_0 = 0 by PCG with the
+ * DDG two-level preconditioner.  HOST buffers: f is copied to the device,
+ * u and the residual history are copied back (the end-to-end path).
+ *   f[n]              right-hand side (host)
+ *   rtol              relative tolerance (> 0)
+ *   max_iter          <= 0 means opts.max_iter
+ *   u[n]              solution (host, out)
+ *   iters             number of A p products (out, may be NULL)
+ *   res_hist[cap]     ||r_j||_2 for j = 0..iters (out, may be NULL); entries past
+ *                     cap are dropped
+ *   rep               report (out, may be NULL)
+ * Hitting max_iter is not an error: rep->converged = 0.
+ * Errors: DDG_E_ARG, DDG_E_BREAKDOWN, DDG_E_CUDA.
+ */
+int ddg_pcg_solve(ddg_ctx* ctx, const double* f, double rtol, int max_iter, double* u,
+                  int* iters, double* res_hist, int res_hist_cap, ddg_report* rep);
+
+/* Same as ddg_pcg_solve with f and u DEVICE pointers on the context's device
+ * (e.g. torch tensors); res_hist stays a host buffer.  No host<->device copy of
+ * vectors happens inside. */
+int ddg_pcg_solve_device(ddg_ctx* ctx, const double* d_f, double rtol, int max_iter,
+                         double* d_u, int* iters, double* res_hist, int res_hist_cap,
+                         ddg_report* rep);
+
+/* z = M r, the full two-level symmetric preconditioner;
+ * host buffers of length n.  Test hook: symmetry, positivity, linearity. */
+int ddg_apply_precond(ddg_ctx* ctx, const double* r, double* z);
+
+/* z = P A_c^{-1} P^T r, the coarse correction alone; host buffers. */
+int ddg_coarse_correct(ddg_ctx* ctx, const double* r, double* z);
+
+/* y = A x on the device (test hook for the SpMV kernel); host buffers. */
+int ddg_spmv(ddg_ctx* ctx, const double* x, double* y);
+
+/* Size and diagnostics of a built context. */
+int ddg_get_info(ddg_ctx* ctx, ddg_info* info);
+
+/* colour[nparts]: colour of every subdomain in the multiplicative sweep (host, out). */
+int ddg_get_colours(ddg_ctx* ctx, int32_t* colour);
+
+/* m[nparts]: |Omega~_i| of every subdomain (host, out). */
+int ddg_get_subdomain_sizes(ddg_ctx* ctx, int32_t* m);
+
+/* Number of kernel launches the context issued since the last reset (its own
+ * kernels only); `reset` != 0 zeroes the counter after reading. */
+int64_t ddg_launch_count(ddg_ctx* ctx, int reset);
+
+/* Release every resource of the context (NULL is a no-op). */
+void ddg_destroy(ddg_ctx* ctx);
+
+const char* ddg_status_string(int status);
+const char* ddg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDG_H */

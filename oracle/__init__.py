@@ -1,0 +1,187 @@
+"""CPU oracle for the DDG-preconditioned CG path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+`--impl reference` legs may import this package.  The product
+(paper_1504_00907_b200/) never imports it and shares no code with it.
+
+The arithmetic lives in oracle.c (plain single-threaded C, fp64, citing
+PAPER.md step by step); this module only builds it with gcc and marshals
+numpy arrays through ctypes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+STOP_RES0, STOP_RES1, STOP_PREC = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (single-threaded, -O2, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-Wall", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        i64, i32, f64, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
+        L.or_setup.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64,
+                               C.POINTER(vp)]
+        L.or_setup.restype = C.c_int
+        for name in ("or_apply_precond", "or_forward_sweep", "or_coarse_correct", "or_spmv"):
+            getattr(L, name).argtypes = [vp, vp, vp]
+            getattr(L, name).restype = C.c_int
+        L.or_pcg.argtypes = [vp, vp, f64, C.c_int, C.c_int, vp, C.POINTER(C.c_int), vp,
+                             C.POINTER(C.c_int)]
+        L.or_pcg.restype = C.c_int
+        L.or_info.argtypes = [vp, vp]
+        L.or_info.restype = None
+        L.or_min_rank_ratio.argtypes = [vp]
+        L.or_min_rank_ratio.restype = f64
+        L.or_get_colours.argtypes = [vp, vp]
+        L.or_get_overlap.argtypes = [vp, i32, vp]
+        L.or_get_overlap.restype = i64
+        L.or_get_P_dense.argtypes = [vp, vp]
+        L.or_get_Ac_dense.argtypes = [vp, vp]
+        L.or_get_coarse_offsets.argtypes = [vp, vp]
+        L.or_destroy.argtypes = [vp]
+        L.or_destroy.restype = None
+        L.or_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"oracle error {code}: {msg}")
+        self.code = code
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Oracle:
+    """Plain CPU implementation of setup + M r + PCG (see oracle.c)."""
+
+    def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8):
+        L = lib()
+        self._keep = [np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
+                      np.ascontiguousarray(val, np.float64),
+                      np.asfortranarray(F, dtype=np.float64),
+                      np.ascontiguousarray(part, np.int32)]
+        rp, ci, va, Ff, pa = self._keep
+        self.n = int(n)
+        self.k = int(Ff.shape[1])
+        h = C.c_void_p()
+        st = L.or_setup(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
+                        int(overlap), float(rank_tol), C.byref(h))
+        if st != 0:
+            raise OracleError(st, L.or_last_error().decode())
+        self._h = h
+        self._keep = None
+        info = np.zeros(10, np.int64)
+        L.or_info(self._h, _p(info))
+        (self.n, self.nc, self.nparts, self.ncolours, self.m_min, self.m_max, _, self.dropped,
+         _, _) = [int(x) for x in info]
+
+    @classmethod
+    def from_problem(cls, pr, overlap=None, rank_tol=1e-8):
+        return cls(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts,
+                   pr.overlap if overlap is None else overlap, rank_tol)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().or_destroy(h)
+            self._h = None
+
+    def _vec(self, name, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty(self.n)
+        st = getattr(lib(), name)(self._h, _p(r), _p(z))
+        if st:
+            raise OracleError(st, lib().or_last_error().decode())
+        return z
+
+    def apply_precond(self, r):
+        return self._vec("or_apply_precond", r)
+
+    def forward_sweep(self, r):
+        return self._vec("or_forward_sweep", r)
+
+    def coarse_correct(self, r):
+        return self._vec("or_coarse_correct", r)
+
+    def spmv(self, x):
+        return self._vec("or_spmv", x)
+
+    def pcg(self, f, rtol=1e-8, max_iter=1000, stop_mode=STOP_RES0):
+        f = np.ascontiguousarray(f, np.float64)
+        u = np.empty(self.n)
+        hist = np.zeros(max_iter + 1)
+        it = C.c_int(0)
+        conv = C.c_int(0)
+        st = lib().or_pcg(self._h, _p(f), float(rtol), int(max_iter), int(stop_mode), _p(u),
+                          C.byref(it), _p(hist), C.byref(conv))
+        if st:
+            raise OracleError(st, lib().or_last_error().decode())
+        return u, it.value, hist[: it.value + 1].copy(), bool(conv.value)
+
+    def colours(self):
+        c = np.empty(self.nparts, np.int32)
+        lib().or_get_colours(self._h, _p(c))
+        return c
+
+    def overlap_set(self, i):
+        m = lib().or_get_overlap(self._h, int(i), None)
+        idx = np.empty(m, np.int32)
+        lib().or_get_overlap(self._h, int(i), _p(idx))
+        return idx
+
+    def P_dense(self):
+        P = np.zeros((self.nc, self.n))
+        lib().or_get_P_dense(self._h, _p(P))
+        return P.T.copy()
+
+    def Ac_dense(self):
+        A = np.zeros((self.nc, self.nc))
+        lib().or_get_Ac_dense(self._h, _p(A))
+        return A
+
+    def coarse_offsets(self):
+        c = np.empty(self.nparts + 1, np.int32)
+        lib().or_get_coarse_offsets(self._h, _p(c))
+        return c
+
+    def min_rank_ratio(self):
+        return float(lib().or_min_rank_ratio(self._h))
+
+
+def fractional_iterations(hist, tol_abs):
+    """Fractional iteration count: the real k* where the
+    linear interpolation of (k, log10 hist[k]) meets log10(tol_abs)."""
+    h = np.asarray(hist, float)
+    lt = np.log10(tol_abs)
+    for k in range(len(h)):
+        if h[k] <= tol_abs:
+            if k == 0:
+                return 0.0
+            a, b = np.log10(h[k - 1]), np.log10(h[k])
+            return (k - 1) + (a - lt) / (a - b)
+    return float("inf")

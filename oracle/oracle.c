@@ -1,0 +1,799 @@
+/*
+ * oracle.c — CPU ORACLE (TEST INFRASTRUCTURE ONLY; see oracle.h).
+ *
+ * A plain, slow, single-threaded fp64 implementation of the DDG two-level
+ * symmetric multiplicative Schwarz preconditioner and of PCG, following
+ * PAPER.md (arXiv:1504.00907) step by step.  No blocking, fusion, colouring
+ * parallelism or reordering beyond what the paper's algorithm states.
+ * Where the paper is silent the DESIGN.md reading is named (R1..R18).
+ *
+ *   setup (or_setup)
+ *     1. parts Omega_I from the partition
+ *     2. overlap Omega~_i: graph distance <= Delta in A
+ *     3. colours + sweep order (reading R3/R6)
+ *     4. local matrices A_i = R~_i A R~_i^T, Cholesky
+ *     5. coarse basis: F restricted to Omega_I,
+ *        orthonormalised per part (double-double MGS, R6c),
+ *        rank-deficient columns discarded (R7)
+ *     6. A_0 = R_0 A R_0^T  (A_c = P^T A P)
+ *     7. Cholesky of A_0 in envelope storage
+ *   apply (or_apply_precond)
+ *   pcg (or_pcg)
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_*.py
+ * (see DESIGN.md "Oracle pins"); none is "parity unpinned".
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+static char g_err[512];
+const char* or_last_error(void) { return g_err; }
+static int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+struct or_ctx {
+    int64_t n;
+    int64_t* rp;
+    int32_t* ci;
+    double* va;
+    int k, nparts, overlap;
+    double rank_tol;
+    int32_t* part;
+    /* parts Omega_I: sorted node lists */
+    int64_t* bptr;
+    int32_t* bidx;
+    int32_t* bpos; /* position of node v inside its part's list */
+    /* overlapping subdomains Omega~_i: sorted node lists */
+    int64_t* optr;
+    int32_t* oidx;
+    /* colours and sweep order */
+    int32_t* colour;
+    int ncolours;
+    int32_t* order;
+    /* local Cholesky factors, packed lower, row-major: L[a][b] at a(a+1)/2 + b */
+    int64_t* loff;
+    double* L;
+    /* coarse basis */
+    int32_t* cptr;  /* coarse offset of part I (nparts+1) */
+    int64_t* qoff;  /* offset of Q_I (|Omega_I| x r_I column-major) in Q */
+    double* Q;
+    int dropped;
+    double min_ratio;
+    int64_t nc;
+    /* coarse matrix, envelope lower storage: row i holds columns efirst[i]..i */
+    int64_t* efirst;
+    int64_t* eptr;
+    double* ea;  /* A_0 (unfactored copy) */
+    double* el;  /* its Cholesky factor */
+};
+
+#define ALLOC(p, cnt)                                                        \
+    do {                                                                     \
+        (p) = calloc((size_t)(cnt) > 0 ? (size_t)(cnt) : 1, sizeof(*(p)));   \
+        if (!(p)) return fail(OR_E_OOM, "out of memory (%lld items)", (long long)(cnt)); \
+    } while (0)
+
+/* ---------------------------------------------------------------------------
+ * double-double arithmetic (reading R6c: orthonormalisation accumulated in
+ * double-double so the span of F restricted to a part is resolved to fp64
+ * rounding even for ill-conditioned blocks).  Dekker / Knuth error-free
+ * transformations.  Compiled with -ffp-contract=off.
+ * ------------------------------------------------------------------------- */
+typedef struct { double hi, lo; } dd;
+static dd two_sum(double a, double b) {
+    dd r; double s = a + b, bb = s - a;
+    r.hi = s; r.lo = (a - (s - bb)) + (b - bb); return r;
+}
+static dd quick_two_sum(double a, double b) {
+    dd r; double s = a + b; r.hi = s; r.lo = b - (s - a); return r;
+}
+static dd dd_add(dd x, dd y) {
+    dd s = two_sum(x.hi, y.hi), t = two_sum(x.lo, y.lo);
+    s.lo += t.hi; s = quick_two_sum(s.hi, s.lo);
+    s.lo += t.lo; return quick_two_sum(s.hi, s.lo);
+}
+static dd dd_neg(dd x) { x.hi = -x.hi; x.lo = -x.lo; return x; }
+static dd dd_mul(dd x, dd y) {
+    double p = x.hi * y.hi;
+    double e = fma(x.hi, y.hi, -p);
+    e += x.hi * y.lo + x.lo * y.hi;
+    return quick_two_sum(p, e);
+}
+static dd dd_div(dd x, dd y) {
+    double q1 = x.hi / y.hi;
+    dd r = dd_add(x, dd_neg(dd_mul((dd){q1, 0.0}, y)));
+    double q2 = r.hi / y.hi;
+    r = dd_add(r, dd_neg(dd_mul((dd){q2, 0.0}, y)));
+    double q3 = r.hi / y.hi;
+    dd q = quick_two_sum(q1, q2);
+    return dd_add(q, (dd){q3, 0.0});
+}
+static dd dd_sqrt(dd a) {
+    if (a.hi <= 0.0) return (dd){0.0, 0.0};
+    double x = sqrt(a.hi);
+    dd x2 = dd_mul((dd){x, 0.0}, (dd){x, 0.0});
+    dd r = dd_add(a, dd_neg(x2));
+    return dd_add((dd){x, 0.0}, (dd){r.hi / (2.0 * x), 0.0});
+}
+
+/* ---------------------------------------------------------------------------
+ * y = A x  (plain CSR row dot products)
+ * ------------------------------------------------------------------------- */
+int or_spmv(or_ctx* c, const double* x, double* y) {
+    for (int64_t i = 0; i < c->n; i++) {
+        double s = 0.0;
+        for (int64_t e = c->rp[i]; e < c->rp[i + 1]; e++) s += c->va[e] * x[c->ci[e]];
+        y[i] = s;
+    }
+    return OR_OK;
+}
+
+static double dot(int64_t n, const double* a, const double* b) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
+    return s;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 2: overlap.  "expanding the partition to include nodes within graph
+ * distance Delta in the graph defined by A".  Breadth-first
+ * level sets over the off-diagonal pattern of A; result sorted.
+ * ------------------------------------------------------------------------- */
+static int cmp_i32(const void* a, const void* b) {
+    int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+    return (x > y) - (x < y);
+}
+
+static int build_overlap(or_ctx* c) {
+    int64_t n = c->n;
+    int32_t* mark;   /* mark[v] = 1 + id of last subdomain that took v */
+    int32_t* list;
+    ALLOC(mark, n);
+    ALLOC(list, n);
+    /* first pass: sizes, second pass: fill */
+    ALLOC(c->optr, c->nparts + 1);
+    int64_t total = 0;
+    int32_t** lists = calloc((size_t)c->nparts, sizeof(int32_t*));
+    int64_t* sizes = calloc((size_t)c->nparts, sizeof(int64_t));
+    if (!lists || !sizes) return fail(OR_E_OOM, "oom overlap");
+    for (int32_t I = 0; I < c->nparts; I++) {
+        int64_t cnt = 0;
+        for (int64_t a = c->bptr[I]; a < c->bptr[I + 1]; a++) {
+            list[cnt++] = c->bidx[a];
+            mark[c->bidx[a]] = I + 1;
+        }
+        int64_t lev_begin = 0, lev_end = cnt;
+        for (int d = 0; d < c->overlap; d++) {
+            for (int64_t a = lev_begin; a < lev_end; a++) {
+                int32_t v = list[a];
+                for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
+                    int32_t u = c->ci[e];
+                    if (u == v || mark[u] == I + 1) continue;
+                    mark[u] = I + 1;
+                    list[cnt++] = u;
+                }
+            }
+            lev_begin = lev_end;
+            lev_end = cnt;
+        }
+        qsort(list, (size_t)cnt, sizeof(int32_t), cmp_i32);
+        lists[I] = malloc((size_t)cnt * sizeof(int32_t));
+        if (!lists[I]) return fail(OR_E_OOM, "oom overlap list");
+        memcpy(lists[I], list, (size_t)cnt * sizeof(int32_t));
+        sizes[I] = cnt;
+        total += cnt;
+    }
+    ALLOC(c->oidx, total);
+    c->optr[0] = 0;
+    for (int32_t I = 0; I < c->nparts; I++) {
+        c->optr[I + 1] = c->optr[I] + sizes[I];
+        memcpy(c->oidx + c->optr[I], lists[I], (size_t)sizes[I] * sizeof(int32_t));
+        free(lists[I]);
+    }
+    free(lists); free(sizes); free(mark); free(list);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 3: colours and sweep order (reading R3).  The paper iterates "over all
+ * subdomains" one at a time.  The order used is: subdomains
+ * sorted by (colour, id), colours from greedy first-fit over increasing id,
+ * where i and j conflict iff Omega~_i intersects Omega~_j or its neighbourhood
+ * N(Omega~_j).  The oracle still processes this order strictly sequentially.
+ * ------------------------------------------------------------------------- */
+static int build_colours(or_ctx* c) {
+    int64_t n = c->n;
+    int np = c->nparts;
+    /* cover lists: subdomains containing node v */
+    int64_t* cptr_;
+    int32_t* cidx;
+    ALLOC(cptr_, n + 1);
+    for (int64_t a = 0; a < c->optr[np]; a++) cptr_[c->oidx[a] + 1]++;
+    for (int64_t v = 0; v < n; v++) cptr_[v + 1] += cptr_[v];
+    ALLOC(cidx, c->optr[np]);
+    int64_t* fill;
+    ALLOC(fill, n);
+    for (int32_t i = 0; i < np; i++)
+        for (int64_t a = c->optr[i]; a < c->optr[i + 1]; a++) {
+            int32_t v = c->oidx[a];
+            cidx[cptr_[v] + fill[v]++] = i;
+        }
+    ALLOC(c->colour, np);
+    for (int32_t i = 0; i < np; i++) c->colour[i] = -1;
+    int32_t* vmark;
+    ALLOC(vmark, n);
+    int maxc = 0;
+    int cap = 64;
+    char* used = calloc((size_t)cap, 1);
+    for (int32_t i = 0; i < np; i++) {
+        memset(used, 0, (size_t)cap);
+        /* nodes of Omega~_i and their neighbours */
+        for (int64_t a = c->optr[i]; a < c->optr[i + 1]; a++) {
+            int32_t v = c->oidx[a];
+            for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
+                int32_t u = c->ci[e];
+                if (vmark[u] == i + 1) continue;
+                vmark[u] = i + 1;
+                for (int64_t t = cptr_[u]; t < cptr_[u + 1]; t++) {
+                    int32_t j = cidx[t];
+                    if (j != i && c->colour[j] >= 0) {
+                        if (c->colour[j] >= cap) {
+                            int ncap = 2 * c->colour[j] + 2;
+                            used = realloc(used, (size_t)ncap);
+                            memset(used + cap, 0, (size_t)(ncap - cap));
+                            cap = ncap;
+                        }
+                        used[c->colour[j]] = 1;
+                    }
+                }
+            }
+        }
+        int col = 0;
+        while (col < cap && used[col]) col++;
+        c->colour[i] = col;
+        if (col + 1 > maxc) maxc = col + 1;
+        if (maxc >= cap) {
+            used = realloc(used, (size_t)(2 * cap));
+            memset(used + cap, 0, (size_t)cap);
+            cap *= 2;
+        }
+    }
+    c->ncolours = maxc;
+    ALLOC(c->order, np);
+    int64_t pos = 0;
+    for (int col = 0; col < maxc; col++)
+        for (int32_t i = 0; i < np; i++)
+            if (c->colour[i] == col) c->order[pos++] = i;
+    free(used); free(vmark); free(cptr_); free(cidx); free(fill);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 4: local matrices A_i = R~_i A R~_i^T, exact solves via
+ * dense Cholesky A_i = L_i L_i^T (Cholesky-Banachiewicz, row by row).
+ * ------------------------------------------------------------------------- */
+static int chol_packed(double* L, int64_t m, int32_t blk) {
+    for (int64_t i = 0; i < m; i++) {
+        double* Li = L + i * (i + 1) / 2;
+        for (int64_t j = 0; j <= i; j++) {
+            double* Lj = L + j * (j + 1) / 2;
+            double s = Li[j];
+            for (int64_t t = 0; t < j; t++) s -= Li[t] * Lj[t];
+            if (i == j) {
+                if (!(s > 0.0))
+                    return fail(OR_E_NOT_SPD,
+                                "local factor: subdomain %d not positive definite at pivot %lld (%.3e)",
+                                blk, (long long)i, s);
+                Li[i] = sqrt(s);
+            } else {
+                Li[j] = s / Lj[j];
+            }
+        }
+    }
+    return OR_OK;
+}
+
+static void chol_solve_packed(const double* L, int64_t m, double* x) {
+    for (int64_t i = 0; i < m; i++) { /* L y = b */
+        const double* Li = L + i * (i + 1) / 2;
+        double s = x[i];
+        for (int64_t t = 0; t < i; t++) s -= Li[t] * x[t];
+        x[i] = s / Li[i];
+    }
+    for (int64_t i = m - 1; i >= 0; i--) { /* L^T x = y */
+        const double* Li = L + i * (i + 1) / 2;
+        x[i] /= Li[i];
+        for (int64_t t = 0; t < i; t++) x[t] -= Li[t] * x[i];
+    }
+}
+
+static int build_local(or_ctx* c) {
+    int np = c->nparts;
+    ALLOC(c->loff, np + 1);
+    for (int32_t i = 0; i < np; i++) {
+        int64_t m = c->optr[i + 1] - c->optr[i];
+        c->loff[i + 1] = c->loff[i] + m * (m + 1) / 2;
+    }
+    ALLOC(c->L, c->loff[np]);
+    int32_t* pos;
+    ALLOC(pos, c->n);
+    for (int64_t v = 0; v < c->n; v++) pos[v] = -1;
+    for (int32_t i = 0; i < np; i++) {
+        int64_t m = c->optr[i + 1] - c->optr[i];
+        const int32_t* idx = c->oidx + c->optr[i];
+        for (int64_t a = 0; a < m; a++) pos[idx[a]] = (int32_t)a;
+        double* L = c->L + c->loff[i];
+        for (int64_t a = 0; a < m; a++) {
+            int32_t v = idx[a];
+            for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
+                int32_t b = pos[c->ci[e]];
+                if (b >= 0 && b <= a) L[a * (a + 1) / 2 + b] = c->va[e];
+            }
+        }
+        int st = chol_packed(L, m, i);
+        for (int64_t a = 0; a < m; a++) pos[idx[a]] = -1;
+        if (st) { free(pos); return st; }
+    }
+    free(pos);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 5: coarse basis.  phi_I = R_I^T R_I F: F restricted
+ * to part I; orthogonalised per part; columns for which
+ * phi_I is not of full rank discarded.  Modified
+ * Gram-Schmidt in double-double over the columns in their given (graded-lex)
+ * order; column j kept iff ||v_j|| >= rank_tol * max_j ||F_I e_j||  (R7).
+ * ------------------------------------------------------------------------- */
+static int build_basis(or_ctx* c, const double* F) {
+    int np = c->nparts, k = c->k;
+    ALLOC(c->cptr, np + 1);
+    ALLOC(c->qoff, np + 1);
+    int64_t qtotal = 0;
+    for (int32_t I = 0; I < np; I++) qtotal += (c->bptr[I + 1] - c->bptr[I]) * (int64_t)k;
+    ALLOC(c->Q, qtotal);
+    int64_t mmax = 0;
+    for (int32_t I = 0; I < np; I++)
+        if (c->bptr[I + 1] - c->bptr[I] > mmax) mmax = c->bptr[I + 1] - c->bptr[I];
+    dd* V;  /* kept q vectors of this part, dd, column-major mI x k */
+    dd* v;
+    ALLOC(V, mmax * k);
+    ALLOC(v, mmax);
+    c->dropped = 0;
+    c->min_ratio = INFINITY;
+    int64_t qpos = 0;
+    for (int32_t I = 0; I < np; I++) {
+        int64_t mI = c->bptr[I + 1] - c->bptr[I];
+        const int32_t* rows = c->bidx + c->bptr[I];
+        double ref = 0.0;
+        for (int j = 0; j < k; j++) {
+            dd s = {0.0, 0.0};
+            for (int64_t a = 0; a < mI; a++) {
+                double x = F[(int64_t)j * c->n + rows[a]];
+                s = dd_add(s, dd_mul((dd){x, 0.0}, (dd){x, 0.0}));
+            }
+            double nrm = dd_sqrt(s).hi;
+            if (nrm > ref) ref = nrm;
+        }
+        if (!(ref > 0.0))
+            return fail(OR_E_ZERO_BLOCK, "coarse basis: F restricted to part %d is zero", I);
+        int r = 0;
+        for (int j = 0; j < k; j++) {
+            for (int64_t a = 0; a < mI; a++) v[a] = (dd){F[(int64_t)j * c->n + rows[a]], 0.0};
+            for (int t = 0; t < r; t++) { /* MGS: v -= (q_t^T v) q_t */
+                dd* q = V + (int64_t)t * mI;
+                dd s = {0.0, 0.0};
+                for (int64_t a = 0; a < mI; a++) s = dd_add(s, dd_mul(q[a], v[a]));
+                for (int64_t a = 0; a < mI; a++) v[a] = dd_add(v[a], dd_neg(dd_mul(s, q[a])));
+            }
+            dd s = {0.0, 0.0};
+            for (int64_t a = 0; a < mI; a++) s = dd_add(s, dd_mul(v[a], v[a]));
+            dd nrm = dd_sqrt(s);
+            double ratio = nrm.hi / ref;
+            if (ratio >= c->rank_tol && nrm.hi > 0.0) {
+                dd* q = V + (int64_t)r * mI;
+                for (int64_t a = 0; a < mI; a++) q[a] = dd_div(v[a], nrm);
+                if (ratio < c->min_ratio) c->min_ratio = ratio;
+                r++;
+            } else {
+                c->dropped++;
+            }
+        }
+        c->qoff[I] = qpos;
+        for (int t = 0; t < r; t++)
+            for (int64_t a = 0; a < mI; a++) c->Q[qpos + (int64_t)t * mI + a] = V[(int64_t)t * mI + a].hi;
+        qpos += (int64_t)r * mI;
+        c->cptr[I + 1] = c->cptr[I] + r;
+    }
+    c->qoff[np] = qpos;
+    c->nc = c->cptr[np];
+    free(V); free(v);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 6: A_0 = R_0 A R_0^T.  Column (J,j) of A_0 is
+ * P^T (A p_{J,j}); (A p)[u] = sum_c A[u,c] p[c] evaluated for every row u that
+ * can be non-zero (rows in Omega_J and its neighbours).  Stored as the lower
+ * triangle in envelope form (A_0 is symmetric; only rows >= columns kept).
+ * ------------------------------------------------------------------------- */
+static int build_coarse(or_ctx* c) {
+    int np = c->nparts;
+    int64_t n = c->n, nc = c->nc;
+    /* envelope: first column of each coarse row = first coarse index of the
+       lowest-numbered part adjacent to (or equal to) its part */
+    int32_t* minadj;
+    ALLOC(minadj, np);
+    for (int32_t I = 0; I < np; I++) minadj[I] = I;
+    for (int64_t v = 0; v < n; v++)
+        for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
+            int32_t I = c->part[v], J = c->part[c->ci[e]];
+            if (J < minadj[I]) minadj[I] = J;
+        }
+    ALLOC(c->efirst, nc);
+    ALLOC(c->eptr, nc + 1);
+    for (int32_t I = 0; I < np; I++)
+        for (int32_t i = c->cptr[I]; i < c->cptr[I + 1]; i++) c->efirst[i] = c->cptr[minadj[I]];
+    for (int64_t i = 0; i < nc; i++) c->eptr[i + 1] = c->eptr[i] + (i - c->efirst[i] + 1);
+    ALLOC(c->ea, c->eptr[nc]);
+    double* w;
+    double* p;
+    int32_t* touched;
+    char* tmark;
+    ALLOC(w, n);
+    ALLOC(p, n);
+    ALLOC(touched, n);
+    ALLOC(tmark, n);
+    for (int32_t J = 0; J < np; J++) {
+        int64_t mJ = c->bptr[J + 1] - c->bptr[J];
+        const int32_t* rowsJ = c->bidx + c->bptr[J];
+        /* rows where A p can be non-zero */
+        int64_t nt = 0;
+        for (int64_t a = 0; a < mJ; a++) {
+            int32_t v = rowsJ[a];
+            for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
+                int32_t u = c->ci[e];
+                if (!tmark[u]) { tmark[u] = 1; touched[nt++] = u; }
+            }
+        }
+        for (int32_t j = 0; j < c->cptr[J + 1] - c->cptr[J]; j++) {
+            int64_t cj = c->cptr[J] + j;
+            const double* qJ = c->Q + c->qoff[J] + (int64_t)j * mJ;
+            for (int64_t a = 0; a < mJ; a++) p[rowsJ[a]] = qJ[a];
+            for (int64_t t = 0; t < nt; t++) {
+                int32_t u = touched[t];
+                double s = 0.0;
+                for (int64_t e = c->rp[u]; e < c->rp[u + 1]; e++) s += c->va[e] * p[c->ci[e]];
+                w[u] = s;
+            }
+            /* A_0[(I,i),(J,j)] = Q_I[:,i]^T w[Omega_I] for parts I touched */
+            for (int64_t t = 0; t < nt; t++) {
+                int32_t u = touched[t];
+                int32_t I = c->part[u];
+                if (I < 0) continue;
+                int64_t mI = c->bptr[I + 1] - c->bptr[I];
+                for (int32_t i = 0; i < c->cptr[I + 1] - c->cptr[I]; i++) {
+                    int64_t ci_ = c->cptr[I] + i;
+                    if (ci_ < cj) continue;
+                    double qv = c->Q[c->qoff[I] + (int64_t)i * mI + c->bpos[u]];
+                    c->ea[c->eptr[ci_] + (cj - c->efirst[ci_])] += qv * w[u];
+                }
+            }
+            for (int64_t a = 0; a < mJ; a++) p[rowsJ[a]] = 0.0;
+        }
+        for (int64_t t = 0; t < nt; t++) tmark[touched[t]] = 0;
+    }
+    free(w); free(p); free(touched); free(tmark); free(minadj);
+    /* Step 7: Cholesky of A_0 within its envelope (exact: no fill outside it) */
+    ALLOC(c->el, c->eptr[nc]);
+    memcpy(c->el, c->ea, (size_t)c->eptr[nc] * sizeof(double));
+    for (int64_t i = 0; i < nc; i++) {
+        double* Li = c->el + c->eptr[i] - c->efirst[i]; /* Li[j] valid for j >= efirst[i] */
+        for (int64_t j = c->efirst[i]; j <= i; j++) {
+            double* Lj = c->el + c->eptr[j] - c->efirst[j];
+            int64_t t0 = c->efirst[i] > c->efirst[j] ? c->efirst[i] : c->efirst[j];
+            double s = Li[j];
+            for (int64_t t = t0; t < j; t++) s -= Li[t] * Lj[t];
+            if (i == j) {
+                if (!(s > 0.0))
+                    return fail(OR_E_NOT_SPD, "coarse factor: A_0 not positive definite at pivot %lld (%.3e)",
+                                (long long)i, s);
+                Li[i] = sqrt(s);
+            } else {
+                Li[j] = s / Lj[j];
+            }
+        }
+    }
+    return OR_OK;
+}
+
+static void coarse_solve(or_ctx* c, double* x) {
+    int64_t nc = c->nc;
+    for (int64_t i = 0; i < nc; i++) {
+        const double* Li = c->el + c->eptr[i] - c->efirst[i];
+        double s = x[i];
+        for (int64_t t = c->efirst[i]; t < i; t++) s -= Li[t] * x[t];
+        x[i] = s / Li[i];
+    }
+    for (int64_t i = nc - 1; i >= 0; i--) {
+        const double* Li = c->el + c->eptr[i] - c->efirst[i];
+        x[i] /= Li[i];
+        for (int64_t t = c->efirst[i]; t < i; t++) x[t] -= Li[t] * x[i];
+    }
+}
+
+/* ---------------------------------------------------------------------------
+ * setup
+ * ------------------------------------------------------------------------- */
+int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+             const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+             double rank_tol, or_ctx** out) {
+    *out = NULL;
+    g_err[0] = 0;
+    if (n < 1 || !row_ptr || !col || !val || !F || !part || k < 1 || nparts < 1 || overlap < 0)
+        return fail(OR_E_ARG, "bad argument (n=%lld k=%d nparts=%d overlap=%d)", (long long)n, k,
+                    nparts, overlap);
+    if (row_ptr[0] != 0) return fail(OR_E_DIM, "row_ptr[0] != 0");
+    for (int64_t i = 0; i < n; i++) {
+        if (row_ptr[i + 1] < row_ptr[i]) return fail(OR_E_DIM, "row_ptr decreasing at %lld", (long long)i);
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; e++) {
+            if (col[e] < 0 || col[e] >= n) return fail(OR_E_DIM, "column out of range in row %lld", (long long)i);
+            if (e > row_ptr[i] && col[e] <= col[e - 1])
+                return fail(OR_E_DIM, "columns not strictly increasing in row %lld", (long long)i);
+        }
+    }
+    or_ctx* c = calloc(1, sizeof(or_ctx));
+    if (!c) return fail(OR_E_OOM, "oom");
+    int st;
+    c->n = n; c->k = k; c->nparts = nparts; c->overlap = overlap; c->rank_tol = rank_tol;
+    int64_t nnz = row_ptr[n];
+    c->rp = malloc((size_t)(n + 1) * sizeof(int64_t));
+    c->ci = malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
+    c->va = malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(double));
+    c->part = malloc((size_t)n * sizeof(int32_t));
+    if (!c->rp || !c->ci || !c->va || !c->part) { or_destroy(c); return fail(OR_E_OOM, "oom"); }
+    memcpy(c->rp, row_ptr, (size_t)(n + 1) * sizeof(int64_t));
+    memcpy(c->ci, col, (size_t)nnz * sizeof(int32_t));
+    memcpy(c->va, val, (size_t)nnz * sizeof(double));
+    memcpy(c->part, part, (size_t)n * sizeof(int32_t));
+    /* Step 1: parts Omega_I (sorted node lists) */
+    c->bptr = calloc((size_t)nparts + 1, sizeof(int64_t));
+    c->bidx = malloc((size_t)n * sizeof(int32_t));
+    c->bpos = malloc((size_t)n * sizeof(int32_t));
+    if (!c->bptr || !c->bidx || !c->bpos) { or_destroy(c); return fail(OR_E_OOM, "oom"); }
+    for (int64_t v = 0; v < n; v++) {
+        if (part[v] < 0 || part[v] >= nparts) {
+            or_destroy(c);
+            return fail(OR_E_PART, "part id %d of node %lld out of range [0,%d)", part[v], (long long)v, nparts);
+        }
+        c->bptr[part[v] + 1]++;
+    }
+    for (int32_t I = 0; I < nparts; I++) {
+        if (c->bptr[I + 1] == 0) { or_destroy(c); return fail(OR_E_PART, "part %d is empty", I); }
+        c->bptr[I + 1] += c->bptr[I];
+    }
+    {
+        int64_t* fillp = calloc((size_t)nparts, sizeof(int64_t));
+        for (int64_t v = 0; v < n; v++) {
+            int32_t I = part[v];
+            c->bpos[v] = (int32_t)fillp[I];
+            c->bidx[c->bptr[I] + fillp[I]++] = (int32_t)v;
+        }
+        free(fillp);
+    }
+    if ((st = build_overlap(c)) || (st = build_colours(c)) || (st = build_local(c)) ||
+        (st = build_basis(c, F)) || (st = build_coarse(c))) {
+        or_destroy(c);
+        return st;
+    }
+    *out = c;
+    return OR_OK;
+}
+
+void or_destroy(or_ctx* c) {
+    if (!c) return;
+    free(c->rp); free(c->ci); free(c->va); free(c->part);
+    free(c->bptr); free(c->bidx); free(c->bpos);
+    free(c->optr); free(c->oidx); free(c->colour); free(c->order);
+    free(c->loff); free(c->L);
+    free(c->cptr); free(c->qoff); free(c->Q);
+    free(c->efirst); free(c->eptr); free(c->ea); free(c->el);
+    free(c);
+}
+
+/* ---------------------------------------------------------------------------
+ * Subdomain update:  u <- u + R~_i^T A_i^{-1} R~_i (f - A u),
+ * the residual restricted to Omega~_i recomputed from the current iterate.
+ * ------------------------------------------------------------------------- */
+static void subdomain_update(or_ctx* c, int32_t i, const double* r, double* z, double* s) {
+    int64_t m = c->optr[i + 1] - c->optr[i];
+    const int32_t* idx = c->oidx + c->optr[i];
+    for (int64_t a = 0; a < m; a++) {
+        int32_t v = idx[a];
+        double az = 0.0;
+        for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) az += c->va[e] * z[c->ci[e]];
+        s[a] = r[v] - az;
+    }
+    chol_solve_packed(c->L + c->loff[i], m, s);
+    for (int64_t a = 0; a < m; a++) z[idx[a]] += s[a];
+}
+
+static int64_t max_m(or_ctx* c) {
+    int64_t mm = 0;
+    for (int32_t i = 0; i < c->nparts; i++)
+        if (c->optr[i + 1] - c->optr[i] > mm) mm = c->optr[i + 1] - c->optr[i];
+    return mm;
+}
+
+/* one forward pass of one-level multiplicative Schwarz from z = 0 (test hook) */
+int or_forward_sweep(or_ctx* c, const double* r, double* z) {
+    double* s = malloc((size_t)max_m(c) * sizeof(double));
+    if (!s) return fail(OR_E_OOM, "oom");
+    memset(z, 0, (size_t)c->n * sizeof(double));
+    for (int32_t t = 0; t < c->nparts; t++) subdomain_update(c, c->order[t], r, z, s);
+    free(s);
+    return OR_OK;
+}
+
+/* coarse correction R_0^T A_0^{-1} R_0 r added into z */
+static void coarse_add(or_ctx* c, const double* res, double* z) {
+    double* b = malloc((size_t)(c->nc > 0 ? c->nc : 1) * sizeof(double));
+    for (int32_t I = 0; I < c->nparts; I++) {
+        int64_t mI = c->bptr[I + 1] - c->bptr[I];
+        const int32_t* rows = c->bidx + c->bptr[I];
+        for (int32_t i = 0; i < c->cptr[I + 1] - c->cptr[I]; i++) {
+            const double* q = c->Q + c->qoff[I] + (int64_t)i * mI;
+            double s = 0.0;
+            for (int64_t a = 0; a < mI; a++) s += q[a] * res[rows[a]];
+            b[c->cptr[I] + i] = s;
+        }
+    }
+    coarse_solve(c, b);
+    for (int32_t I = 0; I < c->nparts; I++) {
+        int64_t mI = c->bptr[I + 1] - c->bptr[I];
+        const int32_t* rows = c->bidx + c->bptr[I];
+        for (int32_t i = 0; i < c->cptr[I + 1] - c->cptr[I]; i++) {
+            const double* q = c->Q + c->qoff[I] + (int64_t)i * mI;
+            double y = b[c->cptr[I] + i];
+            for (int64_t a = 0; a < mI; a++) z[rows[a]] += q[a] * y;
+        }
+    }
+    free(b);
+}
+
+int or_coarse_correct(or_ctx* c, const double* r, double* z) {
+    memset(z, 0, (size_t)c->n * sizeof(double));
+    coarse_add(c, r, z);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Two-level symmetric multiplicative preconditioner z = M r:
+ * zero initial guess; one pass over the subdomains (pre-smoother); the coarse
+ * problem solution on the current residual; another pass in reverse order.
+ * ------------------------------------------------------------------------- */
+int or_apply_precond(or_ctx* c, const double* r, double* z) {
+    int64_t n = c->n;
+    double* s = malloc((size_t)max_m(c) * sizeof(double));
+    double* res = malloc((size_t)n * sizeof(double));
+    if (!s || !res) { free(s); free(res); return fail(OR_E_OOM, "oom"); }
+    memset(z, 0, (size_t)n * sizeof(double));
+    for (int32_t t = 0; t < c->nparts; t++) subdomain_update(c, c->order[t], r, z, s);
+    or_spmv(c, z, res);
+    for (int64_t v = 0; v < n; v++) res[v] = r[v] - res[v];
+    coarse_add(c, res, z);
+    for (int32_t t = c->nparts - 1; t >= 0; t--) subdomain_update(c, c->order[t], r, z, s);
+    free(s); free(res);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Preconditioned CG (Hestenes-Stiefel) from u_0 = 0.
+ * hist[j] = ||r_j||_2 (recurrence residual, reading R2); iterations = number of
+ * A p products (R16).  stop_mode: 0 ||r_k|| <= rtol ||r_0||; 1 <= rtol ||r_1||
+ * (SPEC.md:398); 2 sqrt(r_k^T z_k) <= rtol sqrt(r_0^T z_0)  (reading R1).
+ * ------------------------------------------------------------------------- */
+int or_pcg(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode, double* u,
+           int* iters, double* hist, int* converged) {
+    int64_t n = c->n;
+    double *r = malloc(n * sizeof(double)), *z = malloc(n * sizeof(double)),
+           *p = malloc(n * sizeof(double)), *q = malloc(n * sizeof(double));
+    if (!r || !z || !p || !q) return fail(OR_E_OOM, "oom");
+    int st = OR_OK;
+    *converged = 0;
+    *iters = 0;
+    memset(u, 0, (size_t)n * sizeof(double));
+    memcpy(r, f, (size_t)n * sizeof(double));
+    double res0 = sqrt(dot(n, r, r));
+    hist[0] = res0;
+    if (res0 == 0.0) { *converged = 1; goto done; }
+    or_apply_precond(c, r, z);
+    memcpy(p, z, (size_t)n * sizeof(double));
+    double rho = dot(n, r, z);
+    if (!(rho > 0.0)) { st = fail(OR_E_BREAKDOWN, "r^T z <= 0 at iteration 0"); goto done; }
+    double pres0 = sqrt(rho), ref = res0;
+    for (int it = 0; it < max_iter; it++) {
+        or_spmv(c, p, q);
+        double sigma = dot(n, p, q);
+        if (!(sigma > 0.0)) { st = fail(OR_E_BREAKDOWN, "p^T A p <= 0 at iteration %d", it); goto done; }
+        double alpha = rho / sigma;
+        for (int64_t v = 0; v < n; v++) { u[v] += alpha * p[v]; r[v] -= alpha * q[v]; }
+        double res = sqrt(dot(n, r, r));
+        hist[it + 1] = res;
+        *iters = it + 1;
+        if (stop_mode == 1 && it == 0) ref = res;
+        if (stop_mode != 2 && res <= rtol * ref && !(stop_mode == 1 && it == 0)) { *converged = 1; break; }
+        if (res == 0.0) { *converged = 1; break; }
+        or_apply_precond(c, r, z);
+        double rho1 = dot(n, r, z);
+        if (stop_mode == 2 && sqrt(fabs(rho1)) <= rtol * pres0) { *converged = 1; break; }
+        if (!(rho1 > 0.0)) { st = fail(OR_E_BREAKDOWN, "r^T z <= 0 at iteration %d", it + 1); goto done; }
+        double beta = rho1 / rho;
+        rho = rho1;
+        for (int64_t v = 0; v < n; v++) p[v] = z[v] + beta * p[v];
+    }
+done:
+    free(r); free(z); free(p); free(q);
+    return st;
+}
+
+/* ---------------------------------------------------------------------------
+ * accessors for tests
+ * ------------------------------------------------------------------------- */
+void or_info(or_ctx* c, int64_t* info) {
+    int64_t mmin = INT64_MAX, mmax = 0;
+    for (int32_t i = 0; i < c->nparts; i++) {
+        int64_t m = c->optr[i + 1] - c->optr[i];
+        if (m < mmin) mmin = m;
+        if (m > mmax) mmax = m;
+    }
+    info[0] = c->n; info[1] = c->nc; info[2] = c->nparts; info[3] = c->ncolours;
+    info[4] = mmin; info[5] = mmax; info[6] = c->k; info[7] = c->dropped; info[8] = 0; info[9] = 0;
+}
+double or_min_rank_ratio(or_ctx* c) { return c->min_ratio; }
+int or_get_colours(or_ctx* c, int32_t* colour) {
+    memcpy(colour, c->colour, (size_t)c->nparts * sizeof(int32_t));
+    return OR_OK;
+}
+int64_t or_get_overlap(or_ctx* c, int32_t i, int32_t* idx) {
+    if (i < 0 || i >= c->nparts) return -1;
+    int64_t m = c->optr[i + 1] - c->optr[i];
+    if (idx) memcpy(idx, c->oidx + c->optr[i], (size_t)m * sizeof(int32_t));
+    return m;
+}
+int or_get_P_dense(or_ctx* c, double* P) {
+    memset(P, 0, (size_t)(c->n * c->nc) * sizeof(double));
+    for (int32_t I = 0; I < c->nparts; I++) {
+        int64_t mI = c->bptr[I + 1] - c->bptr[I];
+        for (int32_t i = 0; i < c->cptr[I + 1] - c->cptr[I]; i++)
+            for (int64_t a = 0; a < mI; a++)
+                P[(int64_t)(c->cptr[I] + i) * c->n + c->bidx[c->bptr[I] + a]] =
+                    c->Q[c->qoff[I] + (int64_t)i * mI + a];
+    }
+    return OR_OK;
+}
+int or_get_Ac_dense(or_ctx* c, double* Ac) {
+    int64_t nc = c->nc;
+    memset(Ac, 0, (size_t)(nc * nc) * sizeof(double));
+    for (int64_t i = 0; i < nc; i++)
+        for (int64_t j = c->efirst[i]; j <= i; j++) {
+            double v = c->ea[c->eptr[i] + (j - c->efirst[i])];
+            Ac[i * nc + j] = v;
+            Ac[j * nc + i] = v;
+        }
+    return OR_OK;
+}
+int or_get_coarse_offsets(or_ctx* c, int32_t* cptr) {
+    memcpy(cptr, c->cptr, (size_t)(c->nparts + 1) * sizeof(int32_t));
+    return OR_OK;
+}

@@ -1,0 +1,48 @@
+/*
+ * oracle.h — CPU ORACLE for the DDG-preconditioned CG path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This code is the slow, plain, single-threaded
+ * fp64 definition of what the CUDA path computes, written from PAPER.md
+ * (arXiv:1504.00907).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it.  It shares no code,
+ * header or helper with the product (paper_1504_00907_b200/, include/ddg.h).
+ *
+ * Parity pins: see tests/test_oracle_*.py and DESIGN.md §"Oracle pins".
+ */
+#ifndef DDG_ORACLE_H
+#define DDG_ORACLE_H
+#include <stdint.h>
+
+typedef struct or_ctx or_ctx;
+
+/* return codes (own numbering, mirrors the meaning of the product's statuses) */
+#define OR_OK 0
+#define OR_E_ARG 1
+#define OR_E_DIM 2
+#define OR_E_PART 3
+#define OR_E_ZERO_BLOCK 4
+#define OR_E_NOT_SPD 5
+#define OR_E_BREAKDOWN 7
+#define OR_E_OOM 10
+
+int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+             const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+             double rank_tol, or_ctx** out);
+int or_apply_precond(or_ctx* c, const double* r, double* z);
+int or_forward_sweep(or_ctx* c, const double* r, double* z);
+int or_coarse_correct(or_ctx* c, const double* r, double* z);
+int or_spmv(or_ctx* c, const double* x, double* y);
+int or_pcg(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode,
+           double* u, int* iters, double* hist, int* converged);
+/* info[0..9] = n, n_c, nparts, ncolours, m_min, m_max, k, dropped, (unused), (unused) */
+void or_info(or_ctx* c, int64_t* info);
+double or_min_rank_ratio(or_ctx* c);
+int or_get_colours(or_ctx* c, int32_t* colour);
+int64_t or_get_overlap(or_ctx* c, int32_t i, int32_t* idx);  /* returns |Omega~_i|, fills idx if non-NULL */
+int or_get_P_dense(or_ctx* c, double* P);        /* n x n_c column-major (tiny problems) */
+int or_get_Ac_dense(or_ctx* c, double* Ac);      /* n_c x n_c, full symmetric (tiny problems) */
+int or_get_coarse_offsets(or_ctx* c, int32_t* cptr); /* nparts+1 */
+void or_destroy(or_ctx* c);
+const char* or_last_error(void);
+
+#endif
