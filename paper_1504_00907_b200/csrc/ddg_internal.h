@@ -1,0 +1,129 @@
+// ddg_internal.h — internal types shared by the host setup (setup.cpp) and the
+// sm_100a kernels (kernels.cu) of libddg.  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace ddg {
+
+constexpr int TILE = 32;                 // rows/cols per tile = warp width
+constexpr int TILE_ELEMS = TILE * TILE;  // 1024 doubles = 8 KB per tile
+constexpr int SYMV_WARPS = 8;            // consumer warps per SYMV CTA
+constexpr int MAX_BT = 16;               // max tiles per item side (smem partial sizing)
+
+// One dense symmetric operator applied by the tiled SYMV kernel: a local
+// inverse A_i^{-1} or the dense coarse inverse A_c^{-1}.
+// Its lower-triangle tiles are stored item after item, each tile column-major
+// (element (i,j) of tile at j*32+i), padded rows/cols zero.
+struct OpDesc {
+    int32_t m;        // true size
+    int32_t mp;       // padded to a multiple of TILE
+    int32_t nT;       // tiles per side
+    int32_t BT;       // tiles per item-block side
+    int32_t nblk;     // item-block rows = ceil(nT / BT)
+    int32_t item_base;
+    int32_t nitems;   // nblk * (nblk + 1) / 2
+    int32_t out_mode; // 0: z[idx[r]] += y[r]; 1: y_out[r] = y[r] (identity, coarse)
+    int64_t tile_off; // first double of its tiles
+    int64_t idx_off;  // offset of its index list Omega~_i in d_oidx (out_mode 0)
+    int64_t s_off;    // offset of its right-hand side (mp entries) in d_s
+    int64_t part_off; // offset of its partial segments (multi-item only)
+};
+
+// A work item: the tiles of item-block (bi, bj), bj <= bi, of one operator.
+struct ItemDesc {
+    int32_t op;       // index into OpDesc array
+    int32_t I0, I1;   // tile rows [I0, I1)
+    int32_t J0, J1;   // tile cols [J0, J1)
+    int32_t tri;      // 1: diagonal block (lower triangle incl. diagonal tiles)
+    int32_t ntiles;
+    int64_t tile_off; // first double of this item's tiles
+    int64_t part_off; // its partial slot (2 * BT * TILE doubles), -1 if single-item op
+};
+
+// Reduction task for multi-item operators: row block b of operator op.
+struct RedDesc {
+    int32_t op;
+    int32_t b;
+};
+
+// Device-side PCG scalars (one struct in device memory).
+struct Scalars {
+    double rho, sigma, alpha, beta, gamma;
+    double res0, ref, pres0, res;
+    double rtol;
+    int32_t iter, done, status, max_iter;
+    int32_t stop_mode, converged, pad0, pad1;
+};
+
+// Reduction scratch: per-block partial sums + a ticket counter.
+constexpr int RED_BLOCKS = 148 * 4;
+constexpr int VEC_THREADS = 256;
+
+struct DevCSR {
+    int64_t n;
+    int64_t nnz;
+    const int32_t* rp;   // int32 row offsets (nnz < 2^31 checked)
+    const int32_t* col;
+    const double* val;
+};
+
+struct ColourPlan {
+    int32_t sub_begin, sub_end;     // sweep positions [begin, end)
+    int32_t item_begin, item_end;   // items of this colour
+    int32_t red_begin, red_end;     // reduction tasks of multi-item ops
+    int32_t max_rows;               // max m over the colour's subdomains
+};
+
+// ---- kernel launchers (kernels.cu) ----------------------------------------
+void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, const int32_t* oidx,
+                   DevCSR A, const double* r, const double* z, double* s, bool z_is_zero,
+                   const int32_t* done);
+void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
+                 int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
+                 double* y_out, double* partials, const int32_t* done);
+void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
+                        const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
+                        const double* partials, double* z, double* y_out, const int32_t* done);
+void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
+                            const int32_t* cptr, const int64_t* qoff, const double* Q, DevCSR A,
+                            const double* r, const double* z, double* bc, int maxmI,
+                            const int32_t* done);
+void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
+                    const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc,
+                    double* z, const int32_t* done);
+void launch_fill(cudaStream_t st, double* x, int64_t n, double v, const int32_t* done);
+void launch_spmv(cudaStream_t st, DevCSR A, const double* x, double* y);
+
+// PCG pieces (all read/write the device Scalars; all exit early once done != 0)
+void launch_pcg_init(cudaStream_t st, int64_t n, const double* f, double* r, double* u,
+                     Scalars* sc, double* hist, double* red, unsigned* ticket);
+void launch_pcg_rz_first(cudaStream_t st, int64_t n, const double* r, const double* z, double* p,
+                         Scalars* sc, double* red, unsigned* ticket);
+void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, Scalars* sc,
+                         double* red, unsigned* ticket);
+void launch_pcg_update(cudaStream_t st, int64_t n, const double* p, const double* q, double* u,
+                       double* r, Scalars* sc, double* hist, double* red, unsigned* ticket);
+void launch_pcg_rz(cudaStream_t st, int64_t n, const double* r, const double* z, Scalars* sc,
+                   double* red, unsigned* ticket);
+void launch_pcg_direction(cudaStream_t st, int64_t n, const double* z, double* p, Scalars* sc);
+
+// setup kernels
+void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
+                          const int32_t* oidx, DevCSR A, double* scratch,
+                          const int64_t* scratch_off);
+void launch_gj_batched(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
+                       double* scratch, const int64_t* scratch_off, int32_t* err);
+void launch_gj_big(cudaStream_t st, int nT, double* M, int32_t* err);
+void launch_scatter_coarse(cudaStream_t st, int64_t nent, const int32_t* row, const int32_t* col,
+                           const double* val, int nT, int n_c, double* M);
+void launch_pack(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
+                 const ItemDesc* items, const double* scratch, const int64_t* scratch_off,
+                 double* tiles);
+
+int num_sms();
+
+}  // namespace ddg

@@ -1,0 +1,814 @@
+// kernels.cu — sm_100a kernels of libddg.
+//
+// Hot path, one PCG iteration:
+//   a1 pcg_spmv_dot      q = A p, sigma = p^T q, alpha = rho / sigma
+//   a2 pcg_update        u += alpha p, r -= alpha q, gamma = r^T r, history, stop test
+//   a4 gather + symv     per colour: s_i = R~_i (r - A z); z[Omega~_i] += A_i^{-1} s_i
+//   a5 coarse_restrict   b_c = P^T (r - A z)
+//   a6 symv (coarse op)  y_c = A_c^{-1} b_c (dense packed inverse, small n_c)
+//   a7 prolong           z += P y_c
+//   a8 gather + symv     reverse colour order
+//   a9 pcg_rz, direction rho' = r^T z, beta, p = z + beta p
+// Setup: extract_local, Gauss-Jordan block inversion (batched / big), pack.
+//
+// Every reduction is deterministic (fixed partition, fixed order, last-block
+// finalisation with a ticket; no floating-point atomics), so runs are bitwise
+// repeatable.  Every PCG kernel exits immediately once the device flag
+// `done` is set, so the host can enqueue several iterations without syncing.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ddg_internal.h"
+
+namespace ddg {
+
+#define FULL 0xffffffffu
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// block-wide sum; result valid in every thread. blockDim.x multiple of 32, <= 1024
+__device__ double block_sum(double v) {
+    __shared__ double ws[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) ws[w] = v;
+    __syncthreads();
+    double t = (threadIdx.x < nw) ? ws[threadIdx.x] : 0.0;
+    if (w == 0) t = warp_sum(t);
+    if (threadIdx.x == 0) ws[0] = t;
+    __syncthreads();
+    return ws[0];
+}
+
+// Grid reduction: every block contributes v; the last block to arrive sums
+// the block partials in index order and calls fin(total) in thread 0.
+template <typename Fin>
+__device__ void grid_reduce(double v, double* red, unsigned* ticket, Fin fin) {
+    __shared__ bool last;
+    double b = block_sum(v);
+    if (threadIdx.x == 0) {
+        red[blockIdx.x] = b;
+        __threadfence();
+        unsigned t = atomicAdd(ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double s = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(red + i);
+        s = block_sum(s);
+        if (threadIdx.x == 0) {
+            fin(s);
+            *ticket = 0u;
+        }
+    }
+}
+
+// =============================================================================
+// PCG vector kernels
+// =============================================================================
+
+__global__ void k_pcg_init(int64_t n, const double* __restrict__ f, double* __restrict__ r,
+                           double* __restrict__ u, Scalars* sc, double* hist, double* red,
+                           unsigned* ticket) {
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double v = f[i];
+        r[i] = v;
+        u[i] = 0.0;
+        acc += v * v;
+    }
+    grid_reduce(acc, red, ticket, [&](double s) {
+        double r0 = sqrt(s);
+        sc->res0 = r0;
+        sc->ref = r0;
+        sc->res = r0;
+        hist[0] = r0;
+        sc->iter = 0;
+        sc->status = 0;
+        sc->converged = (r0 == 0.0);
+        sc->done = (r0 == 0.0);
+    });
+}
+
+// rho = r^T z ; p = z  (first direction)
+__global__ void k_pcg_rz_first(int64_t n, const double* __restrict__ r, const double* __restrict__ z,
+                               double* __restrict__ p, Scalars* sc, double* red, unsigned* ticket) {
+    if (sc->done) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double zi = z[i];
+        p[i] = zi;
+        acc += r[i] * zi;
+    }
+    grid_reduce(acc, red, ticket, [&](double s) {
+        if (!(s > 0.0)) {
+            sc->status = 7;  // DDG_E_BREAKDOWN
+            sc->done = 1;
+        } else {
+            sc->rho = s;
+            sc->pres0 = sqrt(s);
+        }
+    });
+}
+
+// q = A p ; sigma = p^T q ; alpha = rho / sigma
+__global__ void k_pcg_spmv_dot(DevCSR A, const double* __restrict__ p, double* __restrict__ q,
+                               Scalars* sc, double* red, unsigned* ticket) {
+    if (sc->done) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int e = A.rp[i]; e < A.rp[i + 1]; e++) s += A.val[e] * p[A.col[e]];
+        q[i] = s;
+        acc += p[i] * s;
+    }
+    grid_reduce(acc, red, ticket, [&](double s) {
+        sc->sigma = s;
+        if (!(s > 0.0)) {
+            sc->status = 7;
+            sc->done = 1;
+        } else {
+            sc->alpha = sc->rho / s;
+        }
+    });
+}
+
+// u += alpha p ; r -= alpha q ; ||r|| ; history ; stopping rule (reading R1)
+__global__ void k_pcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ q,
+                             double* __restrict__ u, double* __restrict__ r, Scalars* sc,
+                             double* hist, double* red, unsigned* ticket) {
+    if (sc->done) return;
+    const double alpha = sc->alpha;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u[i] += alpha * p[i];
+        double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        acc += ri * ri;
+    }
+    grid_reduce(acc, red, ticket, [&](double s) {
+        double res = sqrt(s);
+        int it = sc->iter + 1;
+        sc->iter = it;
+        sc->res = res;
+        hist[it] = res;
+        if (sc->stop_mode == 1 && it == 1) sc->ref = res;
+        bool conv = false;
+        if (sc->stop_mode == 0) conv = res <= sc->rtol * sc->ref;
+        if (sc->stop_mode == 1) conv = (it > 1) && res <= sc->rtol * sc->ref;
+        if (res == 0.0) conv = true;
+        if (conv) {
+            sc->converged = 1;
+            sc->done = 1;
+        } else if (it >= sc->max_iter) {
+            sc->done = 1;
+        }
+    });
+}
+
+// rho' = r^T z ; beta = rho' / rho
+__global__ void k_pcg_rz(int64_t n, const double* __restrict__ r, const double* __restrict__ z,
+                         Scalars* sc, double* red, unsigned* ticket) {
+    if (sc->done) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc += r[i] * z[i];
+    grid_reduce(acc, red, ticket, [&](double s) {
+        if (sc->stop_mode == 2 && sqrt(fabs(s)) <= sc->rtol * sc->pres0) {
+            sc->converged = 1;
+            sc->done = 1;
+        } else if (!(s > 0.0)) {
+            sc->status = 7;
+            sc->done = 1;
+        } else {
+            sc->beta = s / sc->rho;
+            sc->rho = s;
+        }
+    });
+}
+
+// p = z + beta p
+__global__ void k_pcg_direction(int64_t n, const double* __restrict__ z, double* __restrict__ p,
+                                const Scalars* sc) {
+    if (sc->done) return;
+    const double beta = sc->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = z[i] + beta * p[i];
+}
+
+__global__ void k_fill(double* x, int64_t n, double v, const int32_t* done) {
+    if (done && *done) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void k_spmv(DevCSR A, const double* __restrict__ x, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int e = A.rp[i]; e < A.rp[i + 1]; e++) s += A.val[e] * x[A.col[e]];
+        y[i] = s;
+    }
+}
+
+// =============================================================================
+// Multiplicative Schwarz colour step
+// =============================================================================
+
+// s_i = R~_i (r - A z) for every subdomain i of one colour (pull form, reading R5)
+__global__ void k_gather(const OpDesc* __restrict__ ops, int sub_begin, const int32_t* __restrict__ oidx,
+                         DevCSR A, const double* __restrict__ r, const double* __restrict__ z,
+                         double* __restrict__ s, int z_is_zero, const int32_t* done) {
+    if (*done) return;
+    const OpDesc op = ops[sub_begin + blockIdx.x];
+    const int32_t* idx = oidx + op.idx_off;
+    double* so = s + op.s_off;
+    for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
+        const int v = idx[a];
+        double az = 0.0;
+        if (!z_is_zero)
+            for (int e = A.rp[v]; e < A.rp[v + 1]; e++) az += A.val[e] * z[A.col[e]];
+        so[a] = r[v] - az;
+    }
+}
+
+__device__ __forceinline__ void item_tile(const ItemDesc& it, int l, int& I, int& J) {
+    if (!it.tri) {
+        const int wJ = it.J1 - it.J0;
+        I = it.I0 + l / wJ;
+        J = it.J0 + l % wJ;
+    } else {
+        int rr = (int)((sqrtf(8.0f * (float)l + 1.0f) - 1.0f) * 0.5f);
+        while ((rr + 1) * (rr + 2) / 2 <= l) rr++;
+        while (rr * (rr + 1) / 2 > l) rr--;
+        I = it.I0 + rr;
+        J = it.J0 + (l - rr * (rr + 1) / 2);
+    }
+}
+
+// butterfly reduce-scatter of 32 per-lane values: afterwards v[0] of lane l
+// holds sum over lanes of the original v[l].
+template <int OFF>
+__device__ __forceinline__ void rs_stage(double* v, int lane) {
+    const bool upper = (lane & OFF) != 0;
+#pragma unroll
+    for (int j = 0; j < OFF; ++j) {
+        double send = upper ? v[j] : v[j + OFF];
+        double keep = upper ? v[j + OFF] : v[j];
+        v[j] = keep + __shfl_xor_sync(FULL, send, OFF);
+    }
+}
+
+// Tiled symmetric matrix-vector product y = S s over one item-block of a
+// packed symmetric operator.  Warp w handles tiles w, w+W, ...; lane i owns
+// row i of each tile: direct part y_I += S_IJ s_J by per-lane dot products,
+// transposed part y_J += S_IJ^T s_I by a butterfly reduce-scatter.  Per-warp
+// partials in shared memory are summed in warp order (deterministic).
+__global__ void __launch_bounds__(SYMV_WARPS * 32)
+k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
+       const double* __restrict__ tiles, const double* __restrict__ s,
+       const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
+       double* __restrict__ partials, const int32_t* done) {
+    if (*done) return;
+    extern __shared__ double sm[];
+    const ItemDesc it = items[item_begin + blockIdx.x];
+    const OpDesc op = ops[it.op];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int rows_r = (it.I1 - it.I0) * TILE;
+    const int rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+    const int rows_t = rows_r + rows_c;
+    double* s_sm = sm;                          // [rows_t]: s over row block, then col block
+    double* part = sm + rows_t;                 // [SYMV_WARPS][rows_t]
+    const double* sop = s + op.s_off;
+    for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
+        int g = x < rows_r ? it.I0 * TILE + x : it.J0 * TILE + (x - rows_r);
+        s_sm[x] = sop[g];
+    }
+    for (int x = threadIdx.x; x < SYMV_WARPS * rows_t; x += blockDim.x) part[x] = 0.0;
+    __syncthreads();
+    double* pw = part + w * rows_t;
+    const double* tbase = tiles + it.tile_off;
+    for (int l = w; l < it.ntiles; l += SYMV_WARPS) {
+        int I, J;
+        item_tile(it, l, I, J);
+        const double* T = tbase + (int64_t)l * TILE_ELEMS;
+        double a[TILE];
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) a[j] = __ldcs(T + j * TILE + lane);
+        const int ri = (I - it.I0) * TILE;                           // row offset in s_sm / pw
+        const int cj = it.tri ? (J - it.I0) * TILE : rows_r + (J - it.J0) * TILE;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) acc += a[j] * s_sm[cj + j];
+        pw[ri + lane] += acc;
+        if (I != J) {
+            const double si = s_sm[ri + lane];
+#pragma unroll
+            for (int j = 0; j < TILE; ++j) a[j] *= si;
+            rs_stage<16>(a, lane);
+            rs_stage<8>(a, lane);
+            rs_stage<4>(a, lane);
+            rs_stage<2>(a, lane);
+            rs_stage<1>(a, lane);
+            pw[cj + lane] += a[0];
+        }
+    }
+    __syncthreads();
+    const bool single = it.part_off < 0;
+    for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
+        double y = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < SYMV_WARPS; ++ww) y += part[ww * rows_t + x];
+        if (single) {
+            const int g = it.I0 * TILE + x;     // single-item op: one triangle from 0
+            if (g < op.m) {
+                if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+                else y_out[g] = y;
+            }
+        } else {
+            partials[it.part_off + x] = y;
+        }
+    }
+}
+
+// Sum the partial segments of multi-item operators for one row block, in
+// fixed item order, and apply the result.
+__global__ void k_symv_reduce(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
+                              const RedDesc* __restrict__ red, int red_begin,
+                              const int32_t* __restrict__ oidx, const double* __restrict__ partials,
+                              double* __restrict__ z, double* __restrict__ y_out,
+                              const int32_t* done) {
+    if (*done) return;
+    const RedDesc rd = red[red_begin + blockIdx.x];
+    const OpDesc op = ops[rd.op];
+    const int b = rd.b;
+    const int rows_b = (min(op.nT, (b + 1) * op.BT) - b * op.BT) * TILE;
+    for (int x = threadIdx.x; x < rows_b; x += blockDim.x) {
+        const int g = b * op.BT * TILE + x;
+        double y = 0.0;
+        for (int j = 0; j <= b; ++j) {                       // items (b, j): row segments
+            const ItemDesc& it = items[op.item_base + b * (b + 1) / 2 + j];
+            y += partials[it.part_off + x];
+        }
+        for (int i = b + 1; i < op.nblk; ++i) {              // items (i, b): col segments
+            const ItemDesc& it = items[op.item_base + i * (i + 1) / 2 + b];
+            y += partials[it.part_off + (it.I1 - it.I0) * TILE + x];
+        }
+        if (g < op.m) {
+            if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+            else y_out[g] = y;
+        }
+    }
+}
+
+// =============================================================================
+// Coarse correction
+// =============================================================================
+
+// b_c[I,:] = Q_I^T (r - A z)[Omega_I]
+__global__ void k_coarse_restrict(const int64_t* __restrict__ bptr, const int32_t* __restrict__ bidx,
+                                  const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff,
+                                  const double* __restrict__ Q, DevCSR A, const double* __restrict__ r,
+                                  const double* __restrict__ z, double* __restrict__ bc,
+                                  const int32_t* done) {
+    if (*done) return;
+    extern __shared__ double res[];
+    const int I = blockIdx.x;
+    const int64_t b0 = bptr[I];
+    const int mI = (int)(bptr[I + 1] - b0);
+    for (int a = threadIdx.x; a < mI; a += blockDim.x) {
+        const int v = bidx[b0 + a];
+        double az = 0.0;
+        for (int e = A.rp[v]; e < A.rp[v + 1]; e++) az += A.val[e] * z[A.col[e]];
+        res[a] = r[v] - az;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int ncI = cptr[I + 1] - cptr[I];
+    const double* QI = Q + qoff[I];
+    for (int i = w; i < ncI; i += nw) {
+        double acc = 0.0;
+        for (int a = lane; a < mI; a += 32) acc += QI[(int64_t)i * mI + a] * res[a];
+        acc = warp_sum(acc);
+        if (lane == 0) bc[cptr[I] + i] = acc;
+    }
+}
+
+// z[Omega_I] += Q_I y_c[I,:]
+__global__ void k_prolong(const int64_t* __restrict__ bptr, const int32_t* __restrict__ bidx,
+                          const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff,
+                          const double* __restrict__ Q, const double* __restrict__ yc,
+                          double* __restrict__ z, const int32_t* done) {
+    if (*done) return;
+    __shared__ double ys[64];
+    const int I = blockIdx.x;
+    const int64_t b0 = bptr[I];
+    const int mI = (int)(bptr[I + 1] - b0);
+    const int ncI = cptr[I + 1] - cptr[I];
+    if (threadIdx.x < ncI) ys[threadIdx.x] = yc[cptr[I] + threadIdx.x];
+    __syncthreads();
+    const double* QI = Q + qoff[I];
+    for (int a = threadIdx.x; a < mI; a += blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < ncI; i++) acc += QI[(int64_t)i * mI + a] * ys[i];
+        z[bidx[b0 + a]] += acc;
+    }
+}
+
+// =============================================================================
+// Setup: local matrices and their explicit inverses
+// =============================================================================
+
+// element (R, C) of a tiled dense mp x mp matrix (tile (I,J) at (J*nT+I)*1024)
+__device__ __forceinline__ int64_t tix(int nT, int R, int C) {
+    return ((int64_t)(C / TILE) * nT + R / TILE) * TILE_ELEMS + (C % TILE) * TILE + (R % TILE);
+}
+
+__global__ void k_extract_local(const int32_t* __restrict__ op_ids, const OpDesc* __restrict__ ops,
+                                const int32_t* __restrict__ oidx, DevCSR A, double* scratch,
+                                const int64_t* __restrict__ scratch_off) {
+    const OpDesc op = ops[op_ids[blockIdx.x]];
+    double* M = scratch + scratch_off[blockIdx.x];
+    const int64_t tot = (int64_t)op.mp * op.mp;
+    for (int64_t x = threadIdx.x; x < tot; x += blockDim.x) M[x] = 0.0;
+    __syncthreads();
+    const int32_t* idx = oidx + op.idx_off;
+    for (int a = threadIdx.x; a < op.mp; a += blockDim.x) {
+        if (a >= op.m) {
+            M[tix(op.nT, a, a)] = 1.0;   // identity on the padding keeps the matrix SPD
+            continue;
+        }
+        const int v = idx[a];
+        for (int e = A.rp[v]; e < A.rp[v + 1]; e++) {
+            const int c = A.col[e];
+            int lo = 0, hi = op.m;       // binary search in the sorted Omega~_i
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (idx[mid] < c) lo = mid + 1; else hi = mid;
+            }
+            if (lo < op.m && idx[lo] == c) M[tix(op.nT, a, lo)] = A.val[e];
+        }
+    }
+}
+
+// ---- Gauss-Jordan exchange inversion, tile level ------------------------------
+// For pivot tile k (PAPER.md's exact local solves realised as A_i^{-1}):
+//   P = A_kk^{-1};  A_kj <- -P A_kj;  A_ij <- A_ij + A_ik A_kj;  A_ik <- A_ik P.
+// After all k the matrix holds its inverse.  SPD input => all pivots > 0.
+
+// invert the 32x32 tile in shared memory by scalar exchange (256 threads)
+__device__ void tile_exchange_inverse(double* P, int32_t* err, int op_id, int kbase) {
+    for (int p = 0; p < TILE; ++p) {
+        const double d = P[p * TILE + p];
+        double rowp[4], colp[4], old[4];
+        const double inv = 1.0 / d;
+        for (int q = 0; q < 4; ++q) {
+            int e = threadIdx.x + q * 256;
+            int i = e % TILE, j = e / TILE;   // element (i, j) at j*32+i
+            old[q] = P[e];
+            colp[q] = P[p * TILE + i];        // (i, p)
+            rowp[q] = P[j * TILE + p];        // (p, j)
+        }
+        if (threadIdx.x == 0 && !(d > 0.0) && err) {
+            if (atomicCAS(err, -1, op_id) == -1) err[1] = kbase + p;
+        }
+        __syncthreads();
+        for (int q = 0; q < 4; ++q) {
+            int e = threadIdx.x + q * 256;
+            int i = e % TILE, j = e / TILE;
+            double nv;
+            if (i == p && j == p) nv = inv;
+            else if (i == p) nv = -rowp[q] * inv;
+            else if (j == p) nv = colp[q] * inv;
+            else nv = old[q] - colp[q] * rowp[q] * inv;
+            P[e] = nv;
+        }
+        __syncthreads();
+    }
+}
+
+// warp: C (32x32 tile, global) = alpha * Ps(smem) * B (global tile), lane = row
+__device__ __forceinline__ void warp_left_mul(const double* Ps, const double* B, double* C,
+                                              double* Bs, double alpha) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (int j = 0; j < TILE; ++j) Bs[j * TILE + lane] = B[j * TILE + lane];
+    __syncwarp();
+    double prow[TILE];
+#pragma unroll
+    for (int t = 0; t < TILE; ++t) prow[t] = Ps[t * TILE + lane];
+    for (int j = 0; j < TILE; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) acc += prow[t] * Bs[j * TILE + t];
+        C[j * TILE + lane] = alpha * acc;
+    }
+    __syncwarp();
+}
+
+// warp: C += Arow-tile(global) * Bs(smem), lane = row
+__device__ __forceinline__ void warp_gemm_acc(const double* Ag, const double* Bs, double* C) {
+    const int lane = threadIdx.x & 31;
+    double arow[TILE];
+#pragma unroll
+    for (int t = 0; t < TILE; ++t) arow[t] = Ag[t * TILE + lane];
+    for (int j = 0; j < TILE; ++j) {
+        double acc = C[j * TILE + lane];
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) acc += arow[t] * Bs[j * TILE + t];
+        C[j * TILE + lane] = acc;
+    }
+}
+
+// warp: C = C * Ps  (C global tile, right-multiplied in place), lane = row
+__device__ __forceinline__ void warp_right_mul(double* C, const double* Ps) {
+    const int lane = threadIdx.x & 31;
+    double crow[TILE];
+#pragma unroll
+    for (int t = 0; t < TILE; ++t) crow[t] = C[t * TILE + lane];
+    for (int j = 0; j < TILE; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) acc += crow[t] * Ps[j * TILE + t];
+        C[j * TILE + lane] = acc;
+    }
+}
+
+// one CTA (8 warps) inverts one tiled dense matrix in place
+__global__ void __launch_bounds__(256)
+k_gj_batched(const int32_t* __restrict__ op_ids, const OpDesc* __restrict__ ops, double* scratch,
+             const int64_t* __restrict__ scratch_off, int32_t* err) {
+    extern __shared__ double gjsm[];
+    double* Ps = gjsm;
+    double (*Bs)[TILE_ELEMS] = reinterpret_cast<double (*)[TILE_ELEMS]>(gjsm + TILE_ELEMS);
+    const int opid = op_ids[blockIdx.x];
+    const int nT = ops[opid].nT;
+    double* M = scratch + scratch_off[blockIdx.x];
+    const int w = threadIdx.x >> 5;
+    auto tile = [&](int I, int J) { return M + ((int64_t)J * nT + I) * TILE_ELEMS; };
+    for (int k = 0; k < nT; ++k) {
+        for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = tile(k, k)[e];
+        __syncthreads();
+        tile_exchange_inverse(Ps, err, opid, k * TILE);
+        for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) tile(k, k)[e] = Ps[e];
+        // row panel: A_kj <- -P A_kj
+        for (int j = w; j < nT; j += 8)
+            if (j != k) warp_left_mul(Ps, tile(k, j), tile(k, j), Bs[w], -1.0);
+        __syncthreads();
+        // trailing update: A_ij += A_ik A_kj  (i, j != k)
+        for (int j = w; j < nT; j += 8) {
+            if (j == k) continue;
+            const double* B = tile(k, j);
+            const int lane = threadIdx.x & 31;
+            for (int c = 0; c < TILE; ++c) Bs[w][c * TILE + lane] = B[c * TILE + lane];
+            __syncwarp();
+            for (int i = 0; i < nT; ++i)
+                if (i != k) warp_gemm_acc(tile(i, k), Bs[w], tile(i, j));
+            __syncwarp();
+        }
+        __syncthreads();
+        // column panel: A_ik <- A_ik P
+        for (int i = w; i < nT; i += 8)
+            if (i != k) warp_right_mul(tile(i, k), Ps);
+        __syncthreads();
+    }
+}
+
+// ---- the same exchange for one big matrix, one launch per phase ---------------
+__global__ void k_gj_pivot(double* M, int nT, int k, int32_t* err) {
+    __shared__ double Ps[TILE_ELEMS];
+    double* T = M + ((int64_t)k * nT + k) * TILE_ELEMS;
+    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = T[e];
+    __syncthreads();
+    tile_exchange_inverse(Ps, err, 0, k * TILE);
+    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) T[e] = Ps[e];
+}
+
+__global__ void __launch_bounds__(256) k_gj_rowpanel(double* M, int nT, int k) {
+    extern __shared__ double gjsm[];
+    double* Ps = gjsm;
+    double (*Bs)[TILE_ELEMS] = reinterpret_cast<double (*)[TILE_ELEMS]>(gjsm + TILE_ELEMS);
+    const double* P = M + ((int64_t)k * nT + k) * TILE_ELEMS;
+    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = P[e];
+    __syncthreads();
+    const int w = threadIdx.x >> 5;
+    const int j = blockIdx.x * 8 + w;
+    if (j < nT && j != k) {
+        double* T = M + ((int64_t)j * nT + k) * TILE_ELEMS;
+        warp_left_mul(Ps, T, T, Bs[w], -1.0);
+    }
+}
+
+// grid (nT, ceil(nT/8)): CTA stages B_kj once; warp w updates tile (i, j)
+__global__ void __launch_bounds__(256) k_gj_update(double* M, int nT, int k) {
+    __shared__ double Bs[TILE_ELEMS];
+    const int j = blockIdx.x;
+    if (j == k) return;
+    const double* B = M + ((int64_t)j * nT + k) * TILE_ELEMS;
+    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Bs[e] = B[e];
+    __syncthreads();
+    const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (i >= nT || i == k) return;
+    warp_gemm_acc(M + ((int64_t)k * nT + i) * TILE_ELEMS, Bs, M + ((int64_t)j * nT + i) * TILE_ELEMS);
+}
+
+__global__ void __launch_bounds__(256) k_gj_colpanel(double* M, int nT, int k) {
+    __shared__ double Ps[TILE_ELEMS];
+    const double* P = M + ((int64_t)k * nT + k) * TILE_ELEMS;
+    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = P[e];
+    __syncthreads();
+    const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i < nT && i != k) warp_right_mul(M + ((int64_t)k * nT + i) * TILE_ELEMS, Ps);
+}
+
+// Dense tiled A_c from its lower-triangle entries (mirrored => exactly symmetric,
+// reading R9); identity on the padding.
+__global__ void k_scatter_coarse(int64_t nent, const int32_t* __restrict__ row,
+                                 const int32_t* __restrict__ col, const double* __restrict__ val,
+                                 int nT, int n_c, double* M) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nent;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int R = row[e], C = col[e];
+        M[tix(nT, R, C)] = val[e];
+        M[tix(nT, C, R)] = val[e];
+    }
+    for (int64_t a = n_c + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < (int64_t)nT * TILE;
+         a += (int64_t)gridDim.x * blockDim.x)
+        M[tix(nT, (int)a, (int)a)] = 1.0;
+}
+
+// Pack the lower-triangle tiles of the inverse into item order; diagonal
+// tiles symmetrised, padding rows/cols zeroed.
+__global__ void k_pack(const int32_t* __restrict__ op_ids, const OpDesc* __restrict__ ops,
+                       const ItemDesc* __restrict__ items, const double* __restrict__ scratch,
+                       const int64_t* __restrict__ scratch_off, double* __restrict__ tiles) {
+    const int opid = op_ids[blockIdx.y];
+    const OpDesc op = ops[opid];
+    const double* M = scratch + scratch_off[blockIdx.y];
+    for (int itx = blockIdx.x; itx < op.nitems; itx += gridDim.x) {
+        const ItemDesc it = items[op.item_base + itx];
+        for (int l = 0; l < it.ntiles; ++l) {
+            int I, J;
+            item_tile(it, l, I, J);
+            const double* src = M + ((int64_t)J * op.nT + I) * TILE_ELEMS;
+            double* dst = tiles + it.tile_off + (int64_t)l * TILE_ELEMS;
+            for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
+                const int i = e % TILE, j = e / TILE;
+                double v = src[e];
+                if (I == J) v = 0.5 * (v + src[i * TILE + j]);
+                if (I * TILE + i >= op.m || J * TILE + j >= op.m) v = 0.0;
+                dst[e] = v;
+            }
+        }
+    }
+}
+
+// =============================================================================
+// launchers
+// =============================================================================
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+static inline int vec_grid(int64_t n) {
+    int64_t g = (n + VEC_THREADS - 1) / VEC_THREADS;
+    return (int)(g < RED_BLOCKS ? (g > 0 ? g : 1) : RED_BLOCKS);
+}
+
+void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, const int32_t* oidx,
+                   DevCSR A, const double* r, const double* z, double* s, bool z_is_zero,
+                   const int32_t* done) {
+    if (nsub <= 0) return;
+    k_gather<<<nsub, 128, 0, st>>>(ops, sub_begin, oidx, A, r, z, s, z_is_zero ? 1 : 0, done);
+}
+
+static size_t symv_smem(int max_rows_t) {
+    return (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
+}
+
+void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
+                 int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
+                 double* y_out, double* partials, const int32_t* done) {
+    if (nitems <= 0) return;
+    const size_t smem = symv_smem(2 * MAX_BT * TILE);
+    cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_symv<<<nitems, SYMV_WARPS * 32, smem, st>>>(ops, items, item_begin, tiles, s, oidx, z, y_out,
+                                                  partials, done);
+}
+
+void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
+                        const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
+                        const double* partials, double* z, double* y_out, const int32_t* done) {
+    if (nred <= 0) return;
+    k_symv_reduce<<<nred, 256, 0, st>>>(ops, items, red, red_begin, oidx, partials, z, y_out, done);
+}
+
+void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
+                            const int32_t* cptr, const int64_t* qoff, const double* Q, DevCSR A,
+                            const double* r, const double* z, double* bc, int maxmI,
+                            const int32_t* done) {
+    const size_t smem = (size_t)maxmI * sizeof(double);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_coarse_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_coarse_restrict<<<nparts, 256, smem, st>>>(bptr, bidx, cptr, qoff, Q, A, r, z, bc, done);
+}
+
+void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
+                    const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc,
+                    double* z, const int32_t* done) {
+    k_prolong<<<nparts, 128, 0, st>>>(bptr, bidx, cptr, qoff, Q, yc, z, done);
+}
+
+void launch_fill(cudaStream_t st, double* x, int64_t n, double v, const int32_t* done) {
+    k_fill<<<vec_grid(n), VEC_THREADS, 0, st>>>(x, n, v, done);
+}
+
+void launch_spmv(cudaStream_t st, DevCSR A, const double* x, double* y) {
+    k_spmv<<<vec_grid(A.n), VEC_THREADS, 0, st>>>(A, x, y);
+}
+
+void launch_pcg_init(cudaStream_t st, int64_t n, const double* f, double* r, double* u,
+                     Scalars* sc, double* hist, double* red, unsigned* ticket) {
+    k_pcg_init<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, f, r, u, sc, hist, red, ticket);
+}
+void launch_pcg_rz_first(cudaStream_t st, int64_t n, const double* r, const double* z, double* p,
+                         Scalars* sc, double* red, unsigned* ticket) {
+    k_pcg_rz_first<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, r, z, p, sc, red, ticket);
+}
+void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, Scalars* sc,
+                         double* red, unsigned* ticket) {
+    k_pcg_spmv_dot<<<vec_grid(A.n), VEC_THREADS, 0, st>>>(A, p, q, sc, red, ticket);
+}
+void launch_pcg_update(cudaStream_t st, int64_t n, const double* p, const double* q, double* u,
+                       double* r, Scalars* sc, double* hist, double* red, unsigned* ticket) {
+    k_pcg_update<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, p, q, u, r, sc, hist, red, ticket);
+}
+void launch_pcg_rz(cudaStream_t st, int64_t n, const double* r, const double* z, Scalars* sc,
+                   double* red, unsigned* ticket) {
+    k_pcg_rz<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, r, z, sc, red, ticket);
+}
+void launch_pcg_direction(cudaStream_t st, int64_t n, const double* z, double* p, Scalars* sc) {
+    k_pcg_direction<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, z, p, sc);
+}
+
+void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
+                          const int32_t* oidx, DevCSR A, double* scratch,
+                          const int64_t* scratch_off) {
+    if (nops <= 0) return;
+    k_extract_local<<<nops, 256, 0, st>>>(op_ids, ops, oidx, A, scratch, scratch_off);
+}
+
+void launch_gj_batched(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
+                       double* scratch, const int64_t* scratch_off, int32_t* err) {
+    if (nops <= 0) return;
+    const int smem = 9 * TILE_ELEMS * sizeof(double);
+    cudaFuncSetAttribute(k_gj_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_gj_batched<<<nops, 256, smem, st>>>(op_ids, ops, scratch, scratch_off, err);
+}
+
+void launch_gj_big(cudaStream_t st, int nT, double* M, int32_t* err) {
+    const int smem = 9 * TILE_ELEMS * sizeof(double);
+    cudaFuncSetAttribute(k_gj_rowpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int k = 0; k < nT; ++k) {
+        k_gj_pivot<<<1, 256, 0, st>>>(M, nT, k, err);
+        k_gj_rowpanel<<<(nT + 7) / 8, 256, smem, st>>>(M, nT, k);
+        k_gj_update<<<dim3(nT, (nT + 7) / 8), 256, 0, st>>>(M, nT, k);
+        k_gj_colpanel<<<(nT + 7) / 8, 256, 0, st>>>(M, nT, k);
+    }
+}
+
+void launch_scatter_coarse(cudaStream_t st, int64_t nent, const int32_t* row, const int32_t* col,
+                           const double* val, int nT, int n_c, double* M) {
+    k_scatter_coarse<<<RED_BLOCKS, 256, 0, st>>>(nent, row, col, val, nT, n_c, M);
+}
+
+void launch_pack(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
+                 const ItemDesc* items, const double* scratch, const int64_t* scratch_off,
+                 double* tiles) {
+    if (nops <= 0) return;
+    k_pack<<<dim3(8, nops), 256, 0, st>>>(op_ids, ops, items, scratch, scratch_off, tiles);
+}
+
+}  // namespace ddg

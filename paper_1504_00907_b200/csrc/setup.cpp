@@ -1,0 +1,1051 @@
+// setup.cpp — host side of libddg: the C ABI (include/ddg.h), the setup
+// pipeline, and the PCG driver that enqueues the sm_100a kernels.
+//
+// Setup, SURVEY.md §3 call stack (1):
+//   parts Omega_I -> overlap Omega~_i (BFS, Delta) -> colours + sweep order
+//   -> per-part double-double MGS basis (R6c, R7) -> Galerkin A_c = P^T A P
+//   (host, threaded) -> device: local inverses A_i^{-1} (extract + batched
+//   Gauss-Jordan + pack) and the coarse inverse A_c^{-1}.
+// Solve: PCG whose every vector operation and every
+// preconditioner step runs in kernels.cu; the host only enqueues (one CUDA
+// graph per iteration) and polls the device `done` flag every few iterations.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <functional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/ddg.h"
+#include "ddg_internal.h"
+
+using namespace ddg;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+static int set_err(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            return set_err(_e == cudaErrorMemoryAllocation ? DDG_E_OOM : DDG_E_CUDA,     \
+                           "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+extern "C" const char* ddg_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char* ddg_status_string(int s) {
+    switch (s) {
+        case DDG_OK: return "ok";
+        case DDG_E_ARG: return "invalid argument";
+        case DDG_E_DIM: return "dimension mismatch / non-canonical CSR";
+        case DDG_E_PART: return "invalid partition";
+        case DDG_E_ZERO_BLOCK: return "generating vectors vanish on a part";
+        case DDG_E_NOT_SPD: return "matrix not positive definite";
+        case DDG_E_COLOURING: return "colouring conflict";
+        case DDG_E_BREAKDOWN: return "CG breakdown";
+        case DDG_E_CUDA: return "CUDA error";
+        case DDG_E_NCCL: return "NCCL error";
+        case DDG_E_OOM: return "out of device memory";
+        default: return "unknown status";
+    }
+}
+
+extern "C" void ddg_default_opts(ddg_opts* o) {
+    memset(o, 0, sizeof *o);
+    o->overlap = 1;
+    o->rank_tol = 1e-8;
+    o->stop_mode = DDG_STOP_RES0;
+    o->max_iter = 1000;
+    o->device = 0;
+    o->stream = nullptr;
+    o->use_graphs = 1;
+    o->verbose = 0;
+}
+
+// ---------------------------------------------------------------------------
+// small host helpers
+// ---------------------------------------------------------------------------
+static void parallel_for(int64_t n, const std::function<void(int64_t, int64_t, int)>& fn) {
+    int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 32);
+    if (n < 64 || nt == 1) { fn(0, n, 0); return; }
+    nt = (int)std::min<int64_t>(nt, n);
+    std::vector<std::thread> th;
+    std::atomic<int64_t> next{0};
+    const int64_t chunk = std::max<int64_t>(1, n / (nt * 16));
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (;;) {
+                int64_t b = next.fetch_add(chunk);
+                if (b >= n) break;
+                fn(b, std::min(n, b + chunk), t);
+            }
+        });
+    for (auto& x : th) x.join();
+}
+
+static int hw_threads() {
+    return (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
+}
+
+// double-double numbers for the per-part orthonormalisation (reading R6c)
+struct DD {
+    double hi, lo;
+};
+static inline DD dd_two_sum(double a, double b) {
+    double s = a + b, v = s - a;
+    return {s, (a - (s - v)) + (b - v)};
+}
+static inline DD dd_fast(double a, double b) {
+    double s = a + b;
+    return {s, b - (s - a)};
+}
+static inline DD operator+(DD x, DD y) {
+    DD s = dd_two_sum(x.hi, y.hi), t = dd_two_sum(x.lo, y.lo);
+    s.lo += t.hi;
+    s = dd_fast(s.hi, s.lo);
+    s.lo += t.lo;
+    return dd_fast(s.hi, s.lo);
+}
+static inline DD operator-(DD x) { return {-x.hi, -x.lo}; }
+static inline DD operator*(DD x, DD y) {
+    double p = x.hi * y.hi;
+    double e = fma(x.hi, y.hi, -p) + (x.hi * y.lo + x.lo * y.hi);
+    return dd_fast(p, e);
+}
+static inline DD dd_div(DD x, DD y) {
+    double q1 = x.hi / y.hi;
+    DD r = x + -(DD{q1, 0} * y);
+    double q2 = r.hi / y.hi;
+    r = r + -(DD{q2, 0} * y);
+    double q3 = r.hi / y.hi;
+    return dd_fast(q1, q2) + DD{q3, 0};
+}
+static inline DD dd_sqrt(DD a) {
+    if (a.hi <= 0) return {0, 0};
+    double x = sqrt(a.hi);
+    DD r = a + -(DD{x, 0} * DD{x, 0});
+    return DD{x, 0} + DD{r.hi / (2 * x), 0};
+}
+
+// ---------------------------------------------------------------------------
+// the context
+// ---------------------------------------------------------------------------
+template <typename T>
+static int dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    if (e != cudaSuccess)
+        return set_err(DDG_E_OOM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
+                       cudaGetErrorString(e));
+    return DDG_OK;
+}
+
+struct ddg_ctx {
+    ddg_opts opts{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t n = 0, nnz = 0;
+    int k = 0, nparts = 0;
+    // host structures
+    std::vector<int64_t> bptr;
+    std::vector<int32_t> bidx, bpos, part;
+    std::vector<int64_t> optr;
+    std::vector<int32_t> oidx;
+    std::vector<int32_t> colour, order;
+    int ncolours = 0;
+    std::vector<ColourPlan> plans;
+    std::vector<int32_t> cptr;
+    std::vector<int64_t> qoff;
+    std::vector<double> Q;
+    int64_t nc = 0;
+    int dropped = 0;
+    double min_ratio = INFINITY;
+    std::vector<OpDesc> ops;
+    std::vector<ItemDesc> items;
+    std::vector<RedDesc> red;
+    int coarse_op = -1;
+    int coarse_item_begin = 0, coarse_item_end = 0, coarse_red_begin = 0, coarse_red_end = 0;
+    int maxmI = 0;
+    int64_t tiles_doubles = 0, s_doubles = 0, part_doubles = 0;
+    // device
+    DevCSR A{};
+    int32_t *d_rp = nullptr, *d_col = nullptr;
+    double* d_val = nullptr;
+    int32_t* d_oidx = nullptr;
+    OpDesc* d_ops = nullptr;
+    ItemDesc* d_items = nullptr;
+    RedDesc* d_red = nullptr;
+    double *d_tiles = nullptr, *d_s = nullptr, *d_partials = nullptr;
+    int64_t* d_bptr = nullptr;
+    int32_t *d_bidx = nullptr, *d_cptr = nullptr;
+    int64_t* d_qoff = nullptr;
+    double *d_Q = nullptr, *d_yc = nullptr;
+    double *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_f = nullptr,
+           *d_u = nullptr, *d_x = nullptr;
+    Scalars* d_sc = nullptr;
+    double* d_hist = nullptr;
+    int hist_cap = 0;
+    double* d_redbuf = nullptr;
+    unsigned* d_ticket = nullptr;
+    int32_t* d_zero = nullptr;  // a device int that stays 0 (`done` for test hooks)
+    Scalars* h_sc = nullptr;    // pinned mirror
+    cudaGraph_t g_iter = nullptr;
+    cudaGraphExec_t ge_iter = nullptr;
+    const double* g_iter_u = nullptr;  // u pointer baked into the captured graph
+    int64_t launches = 0;
+    int64_t launches_per_iter = 0;
+    int64_t local_bytes = 0, coarse_bytes = 0;
+    double t_setup = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+static void free_ctx(ddg_ctx* c) {
+    if (!c) return;
+    if (c->device >= 0) cudaSetDevice(c->device);
+    if (c->ge_iter) cudaGraphExecDestroy(c->ge_iter);
+    if (c->g_iter) cudaGraphDestroy(c->g_iter);
+    void* ptrs[] = {c->d_rp, c->d_col, c->d_val, c->d_oidx, c->d_ops, c->d_items, c->d_red,
+                    c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
+                    c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
+                    c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_sc) cudaFreeHost(c->h_sc);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+extern "C" void ddg_destroy(ddg_ctx* c) { free_ctx(c); }
+
+// ---------------------------------------------------------------------------
+// setup steps (host)
+// ---------------------------------------------------------------------------
+
+// Omega~_i: nodes within graph distance Delta of Omega_i, sorted
+static void build_overlap(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
+    const int np = c->nparts;
+    std::vector<std::vector<int32_t>> lists(np);
+    const int nt = hw_threads();
+    std::vector<std::vector<int32_t>> marks(nt);
+    parallel_for(np, [&](int64_t b, int64_t e, int t) {
+        auto& mark = marks[t];
+        if (mark.empty()) mark.assign(c->n, -1);
+        for (int64_t I = b; I < e; ++I) {
+            auto& L = lists[I];
+            for (int64_t a = c->bptr[I]; a < c->bptr[I + 1]; ++a) {
+                L.push_back(c->bidx[a]);
+                mark[c->bidx[a]] = (int32_t)I;
+            }
+            size_t lb = 0, le = L.size();
+            for (int d = 0; d < c->opts.overlap; ++d) {
+                for (size_t a = lb; a < le; ++a) {
+                    const int32_t v = L[a];
+                    for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
+                        const int32_t u = col[x];
+                        if (u != v && mark[u] != (int32_t)I) {
+                            mark[u] = (int32_t)I;
+                            L.push_back(u);
+                        }
+                    }
+                }
+                lb = le;
+                le = L.size();
+            }
+            std::sort(L.begin(), L.end());
+        }
+    });
+    c->optr.assign(np + 1, 0);
+    for (int I = 0; I < np; ++I) c->optr[I + 1] = c->optr[I] + (int64_t)lists[I].size();
+    c->oidx.resize(c->optr[np]);
+    for (int I = 0; I < np; ++I)
+        std::copy(lists[I].begin(), lists[I].end(), c->oidx.begin() + c->optr[I]);
+}
+
+// Greedy first-fit colours over increasing id; i, j conflict iff Omega~_i meets
+// Omega~_j or its neighbourhood (the pull-form residual of j reads there).
+// Sweep order: (colour, id).  Reading R3.
+static int build_colours(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
+    const int64_t n = c->n;
+    const int np = c->nparts;
+    std::vector<int64_t> cp(n + 1, 0);
+    for (int32_t v : c->oidx) cp[v + 1]++;
+    for (int64_t v = 0; v < n; ++v) cp[v + 1] += cp[v];
+    std::vector<int32_t> cov(cp[n]);
+    {
+        std::vector<int64_t> fill(cp.begin(), cp.end() - 1);
+        for (int i = 0; i < np; ++i)
+            for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) cov[fill[c->oidx[a]]++] = i;
+    }
+    c->colour.assign(np, -1);
+    std::vector<int32_t> vmark(n, -1);
+    std::vector<char> used;
+    int maxc = 0;
+    for (int i = 0; i < np; ++i) {
+        used.assign(maxc + 1, 0);
+        for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) {
+            const int32_t v = c->oidx[a];
+            for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
+                const int32_t u = col[x];
+                if (vmark[u] == i) continue;
+                vmark[u] = i;
+                for (int64_t t = cp[u]; t < cp[u + 1]; ++t) {
+                    const int j = cov[t];
+                    if (j != i && c->colour[j] >= 0) used[c->colour[j]] = 1;
+                }
+            }
+        }
+        int cc = 0;
+        while (cc <= maxc && used[cc]) ++cc;
+        c->colour[i] = cc;
+        maxc = std::max(maxc, cc + 1);
+    }
+    c->ncolours = maxc;
+    c->order.clear();
+    for (int cc = 0; cc < maxc; ++cc)
+        for (int i = 0; i < np; ++i)
+            if (c->colour[i] == cc) c->order.push_back(i);
+    return DDG_OK;
+}
+
+// Per-part orthonormal basis of F[Omega_I,:]: modified
+// Gram-Schmidt in double-double, columns in their given order, column j kept
+// iff ||v_j|| >= rank_tol * max_j ||F_I e_j|| (reading R7).
+static int build_basis(ddg_ctx* c, const double* F) {
+    const int np = c->nparts, k = c->k;
+    const int64_t n = c->n;
+    std::vector<int> rank(np, 0);
+    std::vector<std::vector<double>> QI(np);
+    std::vector<double> ratio(np, INFINITY);
+    std::atomic<int> bad{-1};
+    parallel_for(np, [&](int64_t b, int64_t e, int) {
+        std::vector<DD> V, v;
+        for (int64_t I = b; I < e; ++I) {
+            const int64_t mI = c->bptr[I + 1] - c->bptr[I];
+            const int32_t* rows = c->bidx.data() + c->bptr[I];
+            double ref = 0;
+            for (int j = 0; j < k; ++j) {
+                DD s{0, 0};
+                for (int64_t a = 0; a < mI; ++a) {
+                    double x = F[(int64_t)j * n + rows[a]];
+                    s = s + DD{x, 0} * DD{x, 0};
+                }
+                ref = std::max(ref, dd_sqrt(s).hi);
+            }
+            if (!(ref > 0)) {
+                int expect = -1;
+                bad.compare_exchange_strong(expect, (int)I);
+                continue;
+            }
+            V.assign((size_t)mI * k, DD{0, 0});
+            v.resize(mI);
+            int r = 0;
+            for (int j = 0; j < k; ++j) {
+                for (int64_t a = 0; a < mI; ++a) v[a] = DD{F[(int64_t)j * n + rows[a]], 0};
+                for (int t = 0; t < r; ++t) {
+                    const DD* q = V.data() + (size_t)t * mI;
+                    DD s{0, 0};
+                    for (int64_t a = 0; a < mI; ++a) s = s + q[a] * v[a];
+                    for (int64_t a = 0; a < mI; ++a) v[a] = v[a] + -(s * q[a]);
+                }
+                DD s{0, 0};
+                for (int64_t a = 0; a < mI; ++a) s = s + v[a] * v[a];
+                DD nrm = dd_sqrt(s);
+                const double rt = nrm.hi / ref;
+                if (rt >= c->opts.rank_tol && nrm.hi > 0) {
+                    DD* q = V.data() + (size_t)r * mI;
+                    for (int64_t a = 0; a < mI; ++a) q[a] = dd_div(v[a], nrm);
+                    ratio[I] = std::min(ratio[I], rt);
+                    ++r;
+                }
+            }
+            rank[I] = r;
+            QI[I].resize((size_t)r * mI);
+            for (size_t x = 0; x < (size_t)r * mI; ++x) QI[I][x] = V[x].hi;
+        }
+    });
+    if (bad.load() >= 0)
+        return set_err(DDG_E_ZERO_BLOCK, "coarse basis: F restricted to part %d is zero", bad.load());
+    c->cptr.assign(np + 1, 0);
+    c->qoff.assign(np + 1, 0);
+    c->dropped = 0;
+    for (int I = 0; I < np; ++I) {
+        c->cptr[I + 1] = c->cptr[I] + rank[I];
+        c->qoff[I + 1] = c->qoff[I] + (int64_t)QI[I].size();
+        c->dropped += k - rank[I];
+        c->min_ratio = std::min(c->min_ratio, ratio[I]);
+    }
+    c->nc = c->cptr[np];
+    c->Q.resize(c->qoff[np]);
+    for (int I = 0; I < np; ++I) std::copy(QI[I].begin(), QI[I].end(), c->Q.begin() + c->qoff[I]);
+    return DDG_OK;
+}
+
+// Galerkin product A_c = P^T A P: for every part J and kept
+// column j, w = A p_{J,j} on the rows where it can be non-zero, then
+// A_c[(I,i),(J,j)] = Q_I[:,i]^T w[Omega_I]; only coarse row >= coarse col kept.
+static void build_galerkin(ddg_ctx* c, const int64_t* rp, const int32_t* col, const double* val,
+                           std::vector<int32_t>& er, std::vector<int32_t>& ec,
+                           std::vector<double>& ev) {
+    const int np = c->nparts;
+    const int nt = hw_threads();
+    std::vector<std::vector<int32_t>> tr(np), tc(np);
+    std::vector<std::vector<double>> tv(np);
+    std::vector<std::vector<int32_t>> marks(nt);
+    parallel_for(np, [&](int64_t b, int64_t e, int t) {
+        auto& mark = marks[t];
+        if (mark.empty()) mark.assign(c->n, -1);
+        std::vector<int32_t> touched;
+        std::vector<double> w;
+        std::vector<int32_t> partsI;
+        std::vector<double> acc;
+        for (int64_t J = b; J < e; ++J) {
+            const int64_t mJ = c->bptr[J + 1] - c->bptr[J];
+            const int32_t* rowsJ = c->bidx.data() + c->bptr[J];
+            touched.clear();
+            for (int64_t a = 0; a < mJ; ++a) {
+                const int32_t v = rowsJ[a];
+                for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
+                    const int32_t u = col[x];
+                    if (mark[u] != (int32_t)J) {
+                        mark[u] = (int32_t)J;
+                        touched.push_back(u);
+                    }
+                }
+            }
+            std::sort(touched.begin(), touched.end());
+            partsI.clear();
+            for (int32_t u : touched) partsI.push_back(c->part[u]);
+            std::sort(partsI.begin(), partsI.end());
+            partsI.erase(std::unique(partsI.begin(), partsI.end()), partsI.end());
+            const int ncJ = c->cptr[J + 1] - c->cptr[J];
+            w.resize(touched.size());
+            for (int j = 0; j < ncJ; ++j) {
+                const double* qJ = c->Q.data() + c->qoff[J] + (int64_t)j * mJ;
+                for (size_t t2 = 0; t2 < touched.size(); ++t2) {
+                    const int32_t u = touched[t2];
+                    double s = 0;
+                    for (int64_t x = rp[u]; x < rp[u + 1]; ++x) {
+                        const int32_t cc = col[x];
+                        if (c->part[cc] == (int32_t)J) s += val[x] * qJ[c->bpos[cc]];
+                    }
+                    w[t2] = s;
+                }
+                const int64_t cj = c->cptr[J] + j;
+                for (int32_t I : partsI) {
+                    const int ncI = c->cptr[I + 1] - c->cptr[I];
+                    const int64_t mI = c->bptr[I + 1] - c->bptr[I];
+                    acc.assign(ncI, 0.0);
+                    for (size_t t2 = 0; t2 < touched.size(); ++t2) {
+                        const int32_t u = touched[t2];
+                        if (c->part[u] != I) continue;
+                        const double wu = w[t2];
+                        for (int i = 0; i < ncI; ++i)
+                            acc[i] += c->Q[c->qoff[I] + (int64_t)i * mI + c->bpos[u]] * wu;
+                    }
+                    for (int i = 0; i < ncI; ++i) {
+                        const int64_t ci = c->cptr[I] + i;
+                        if (ci < cj) continue;
+                        tr[J].push_back((int32_t)ci);
+                        tc[J].push_back((int32_t)cj);
+                        tv[J].push_back(acc[i]);
+                    }
+                }
+            }
+        }
+    });
+    size_t tot = 0;
+    for (int J = 0; J < np; ++J) tot += tv[J].size();
+    er.reserve(tot);
+    ec.reserve(tot);
+    ev.reserve(tot);
+    for (int J = 0; J < np; ++J) {
+        er.insert(er.end(), tr[J].begin(), tr[J].end());
+        ec.insert(ec.end(), tc[J].begin(), tc[J].end());
+        ev.insert(ev.end(), tv[J].begin(), tv[J].end());
+    }
+}
+
+// Operator descriptors, work items and reduction tasks for the tiled SYMV.
+static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool allow_single) {
+    OpDesc op{};
+    op.m = m;
+    op.mp = ((m + TILE - 1) / TILE) * TILE;
+    op.nT = op.mp / TILE;
+    if (allow_single && op.nT <= MAX_BT) op.BT = op.nT;
+    else op.BT = (op.nT > 512) ? MAX_BT : 8;
+    if (op.BT > op.nT) op.BT = op.nT;
+    op.nblk = (op.nT + op.BT - 1) / op.BT;
+    op.item_base = (int32_t)c->items.size();
+    op.nitems = op.nblk * (op.nblk + 1) / 2;
+    op.out_mode = out_mode;
+    op.tile_off = c->tiles_doubles;
+    op.idx_off = idx_off;
+    op.s_off = c->s_doubles;
+    op.part_off = -1;
+    const int opi = (int)c->ops.size();
+    for (int bi = 0; bi < op.nblk; ++bi)
+        for (int bj = 0; bj <= bi; ++bj) {
+            ItemDesc it{};
+            it.op = opi;
+            it.I0 = bi * op.BT;
+            it.I1 = std::min(op.nT, (bi + 1) * op.BT);
+            it.J0 = bj * op.BT;
+            it.J1 = std::min(op.nT, (bj + 1) * op.BT);
+            it.tri = (bi == bj);
+            const int h = it.I1 - it.I0, wd = it.J1 - it.J0;
+            it.ntiles = it.tri ? h * (h + 1) / 2 : h * wd;
+            it.tile_off = c->tiles_doubles;
+            c->tiles_doubles += (int64_t)it.ntiles * TILE_ELEMS;
+            if (op.nitems > 1) {
+                it.part_off = c->part_doubles;
+                c->part_doubles += (int64_t)(h + (it.tri ? 0 : wd)) * TILE;
+            } else {
+                it.part_off = -1;
+            }
+            c->items.push_back(it);
+        }
+    if (op.nitems > 1)
+        for (int b = 0; b < op.nblk; ++b) c->red.push_back(RedDesc{opi, b});
+    c->s_doubles += op.mp;
+    c->ops.push_back(op);
+}
+
+static int build_plans(ddg_ctx* c) {
+    c->ops.clear();
+    c->items.clear();
+    c->red.clear();
+    c->plans.assign(c->ncolours, ColourPlan{});
+    // subdomain operators in sweep order; the index lists are stored in that order
+    std::vector<int32_t> sorted_idx;
+    sorted_idx.reserve(c->oidx.size());
+    int pos = 0;
+    for (int cc = 0; cc < c->ncolours; ++cc) {
+        ColourPlan& pl = c->plans[cc];
+        pl.sub_begin = pos;
+        pl.item_begin = (int)c->items.size();
+        pl.red_begin = (int)c->red.size();
+        pl.max_rows = 0;
+        while (pos < c->nparts && c->colour[c->order[pos]] == cc) {
+            const int i = c->order[pos];
+            const int64_t m = c->optr[i + 1] - c->optr[i];
+            const int64_t off = (int64_t)sorted_idx.size();
+            sorted_idx.insert(sorted_idx.end(), c->oidx.begin() + c->optr[i],
+                              c->oidx.begin() + c->optr[i + 1]);
+            add_op(c, (int32_t)m, 0, off, true);
+            pl.max_rows = std::max<int>(pl.max_rows, (int)m);
+            ++pos;
+        }
+        pl.sub_end = pos;
+        pl.item_end = (int)c->items.size();
+        pl.red_end = (int)c->red.size();
+    }
+    c->oidx.swap(sorted_idx);  // now in sweep order; optr no longer valid for oidx
+    // dense coarse inverse
+    c->coarse_op = (int)c->ops.size();
+    c->coarse_item_begin = (int)c->items.size();
+    c->coarse_red_begin = (int)c->red.size();
+    add_op(c, (int32_t)c->nc, 1, -1, true);
+    c->coarse_item_end = (int)c->items.size();
+    c->coarse_red_end = (int)c->red.size();
+    return DDG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device setup: local inverses and the coarse inverse
+// ---------------------------------------------------------------------------
+static int invert_locals(ddg_ctx* c) {
+    const int np = c->nparts;
+    size_t freeb = 0, totb = 0;
+    CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
+    int64_t budget = std::min<int64_t>((int64_t)freeb / 4, (int64_t)8 << 30);
+    budget = std::max<int64_t>(budget, (int64_t)64 << 20);
+    double* scratch = nullptr;
+    int64_t max_single = 0;
+    for (int q = 0; q < np; ++q) max_single = std::max<int64_t>(max_single, (int64_t)c->ops[q].mp * c->ops[q].mp);
+    const int64_t cap = std::max<int64_t>(budget / 8, max_single);
+    int st = dalloc(&scratch, cap);
+    if (st) return st;
+    int32_t *d_ids = nullptr, *d_err = nullptr;
+    int64_t* d_soff = nullptr;
+    if ((st = dalloc(&d_ids, np)) || (st = dalloc(&d_soff, np)) || (st = dalloc(&d_err, 2))) {
+        cudaFree(scratch);
+        return st;
+    }
+    int32_t herr[2] = {-1, -1};
+    CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
+    std::vector<int32_t> ids;
+    std::vector<int64_t> soff;
+    int q = 0;
+    while (q < np) {
+        ids.clear();
+        soff.clear();
+        int64_t used = 0;
+        while (q < np && (ids.empty() || used + (int64_t)c->ops[q].mp * c->ops[q].mp <= cap)) {
+            ids.push_back(q);
+            soff.push_back(used);
+            used += (int64_t)c->ops[q].mp * c->ops[q].mp;
+            ++q;
+        }
+        CUDA_TRY(cudaMemcpyAsync(d_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_soff, soff.data(), soff.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        launch_extract_local(c->stream, (int)ids.size(), d_ids, c->d_ops, c->d_oidx, c->A, scratch, d_soff);
+        launch_gj_batched(c->stream, (int)ids.size(), d_ids, c->d_ops, scratch, d_soff, d_err);
+        launch_pack(c->stream, (int)ids.size(), d_ids, c->d_ops, c->d_items, scratch, d_soff, c->d_tiles);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+    CUDA_TRY(cudaMemcpy(herr, d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    cudaFree(scratch);
+    cudaFree(d_ids);
+    cudaFree(d_soff);
+    cudaFree(d_err);
+    if (herr[0] >= 0)
+        return set_err(DDG_E_NOT_SPD,
+                       "local inverse: subdomain %d (sweep position %d) not positive definite at pivot %d",
+                       c->order[herr[0]], herr[0], herr[1]);
+    return DDG_OK;
+}
+
+static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::vector<int32_t>& ec,
+                         const std::vector<double>& ev) {
+    const OpDesc& op = c->ops[c->coarse_op];
+    const int64_t tot = (int64_t)op.mp * op.mp;
+    double* M = nullptr;
+    int32_t *d_r = nullptr, *d_c = nullptr, *d_err = nullptr, *d_ids = nullptr;
+    double* d_v = nullptr;
+    int64_t* d_soff = nullptr;
+    int st;
+    if ((st = dalloc(&M, tot)) || (st = dalloc(&d_r, er.size())) || (st = dalloc(&d_c, ec.size())) ||
+        (st = dalloc(&d_v, ev.size())) || (st = dalloc(&d_err, 2)) || (st = dalloc(&d_ids, 1)) ||
+        (st = dalloc(&d_soff, 1)))
+        return st;
+    int32_t herr[2] = {-1, -1};
+    int32_t id = c->coarse_op;
+    int64_t zero = 0;
+    CUDA_TRY(cudaMemsetAsync(M, 0, tot * sizeof(double), c->stream));
+    CUDA_TRY(cudaMemcpy(d_r, er.data(), er.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_c, ec.data(), ec.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_v, ev.data(), ev.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_ids, &id, 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_soff, &zero, 8, cudaMemcpyHostToDevice));
+    launch_scatter_coarse(c->stream, (int64_t)ev.size(), d_r, d_c, d_v, op.nT, op.m, M);
+    if (op.nT <= 64) launch_gj_batched(c->stream, 1, d_ids, c->d_ops, M, d_soff, d_err);
+    else launch_gj_big(c->stream, op.nT, M, d_err);
+    launch_pack(c->stream, 1, d_ids, c->d_ops, c->d_items, M, d_soff, c->d_tiles);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(herr, d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    cudaFree(M); cudaFree(d_r); cudaFree(d_c); cudaFree(d_v); cudaFree(d_err); cudaFree(d_ids); cudaFree(d_soff);
+    if (herr[0] >= 0)
+        return set_err(DDG_E_NOT_SPD, "coarse inverse: A_c not positive definite at pivot %d", herr[1]);
+    return DDG_OK;
+}
+
+template <typename T>
+static int upload(T** d, const std::vector<T>& h) {
+    int st = dalloc(d, h.size());
+    if (st) return st;
+    if (!h.empty()) CUDA_TRY(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return DDG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ddg_setup
+// ---------------------------------------------------------------------------
+extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                         const double* F, int k, const int32_t* part, int32_t nparts,
+                         const ddg_opts* opts, ddg_ctx** out) {
+    if (!out) return set_err(DDG_E_ARG, "out is NULL");
+    *out = nullptr;
+    g_last_error.clear();
+    if (n < 1 || !row_ptr || !col || !val || !F || !part || k < 1 || k > 64 || nparts < 1)
+        return set_err(DDG_E_ARG, "bad argument (n=%lld k=%d nparts=%d)", (long long)n, k, nparts);
+    if (n >= (int64_t)INT32_MAX) return set_err(DDG_E_ARG, "n=%lld too large for int32 indices", (long long)n);
+    auto t0 = std::chrono::steady_clock::now();
+    ddg_ctx* c = new ddg_ctx();
+    if (opts) c->opts = *opts;
+    else ddg_default_opts(&c->opts);
+    if (c->opts.overlap < 0) { free_ctx(c); return set_err(DDG_E_ARG, "overlap < 0"); }
+    if (c->opts.max_iter <= 0) c->opts.max_iter = 1000;
+    c->n = n;
+    c->k = k;
+    c->nparts = nparts;
+    c->nnz = row_ptr[n];
+    if (row_ptr[0] != 0 || c->nnz < n) { free_ctx(c); return set_err(DDG_E_DIM, "row_ptr[0] != 0 or nnz < n"); }
+    if (c->nnz >= (int64_t)INT32_MAX) { free_ctx(c); return set_err(DDG_E_ARG, "nnz too large"); }
+    for (int64_t i = 0; i < n; ++i) {
+        if (row_ptr[i + 1] < row_ptr[i]) { free_ctx(c); return set_err(DDG_E_DIM, "row_ptr decreasing at row %lld", (long long)i); }
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            if (col[e] < 0 || col[e] >= n) { free_ctx(c); return set_err(DDG_E_DIM, "column %d out of range in row %lld", col[e], (long long)i); }
+            if (e > row_ptr[i] && col[e] <= col[e - 1]) { free_ctx(c); return set_err(DDG_E_DIM, "columns not strictly increasing in row %lld", (long long)i); }
+        }
+    }
+    // parts Omega_I
+    c->part.assign(part, part + n);
+    c->bptr.assign(nparts + 1, 0);
+    for (int64_t v = 0; v < n; ++v) {
+        if (part[v] < 0 || part[v] >= nparts) {
+            int pv = part[v];
+            free_ctx(c);
+            return set_err(DDG_E_PART, "part id %d of unknown %lld outside [0,%d)", pv, (long long)v, nparts);
+        }
+        c->bptr[part[v] + 1]++;
+    }
+    for (int I = 0; I < nparts; ++I) {
+        if (c->bptr[I + 1] == 0) { free_ctx(c); return set_err(DDG_E_PART, "part %d is empty", I); }
+        c->bptr[I + 1] += c->bptr[I];
+    }
+    c->bidx.resize(n);
+    c->bpos.resize(n);
+    {
+        std::vector<int64_t> fill(c->bptr.begin(), c->bptr.end() - 1);
+        for (int64_t v = 0; v < n; ++v) {
+            const int I = part[v];
+            c->bpos[v] = (int32_t)(fill[I] - c->bptr[I]);
+            c->bidx[fill[I]++] = (int32_t)v;
+        }
+    }
+    int st;
+    // device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        free_ctx(c);
+        return set_err(DDG_E_CUDA, "no CUDA device available (libddg has no CPU fallback)");
+    }
+    c->device = c->opts.device;
+    if (cudaSetDevice(c->device) != cudaSuccess) {
+        free_ctx(c);
+        return set_err(DDG_E_CUDA, "cudaSetDevice(%d) failed", c->opts.device);
+    }
+    if (c->opts.stream) {
+        c->stream = (cudaStream_t)c->opts.stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            free_ctx(c);
+            return set_err(DDG_E_CUDA, "stream creation failed");
+        }
+        c->own_stream = true;
+    }
+    auto tick = [&](const char* what) {
+        if (c->opts.verbose) {
+            double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            fprintf(stderr, "[ddg_setup] %-28s %8.3f s\n", what, s);
+        }
+    };
+    build_overlap(c, row_ptr, col);
+    tick("overlap");
+    build_colours(c, row_ptr, col);
+    tick("colours");
+    if ((st = build_basis(c, F))) { free_ctx(c); return st; }
+    tick("basis (dd-MGS)");
+    std::vector<int32_t> er, ec;
+    std::vector<double> ev;
+    build_galerkin(c, row_ptr, col, val, er, ec, ev);
+    tick("galerkin");
+    if (c->nc > 131072) {
+        int64_t nc = c->nc;
+        free_ctx(c);
+        return set_err(DDG_E_ARG, "n_c = %lld: the dense coarse inverse is limited to 131072 unknowns",
+                       (long long)nc);
+    }
+    build_plans(c);
+    // uploads
+    std::vector<int32_t> rp32(n + 1);
+    for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
+    if ((st = upload(&c->d_rp, rp32)) || (st = dalloc(&c->d_col, c->nnz)) || (st = dalloc(&c->d_val, c->nnz))) {
+        free_ctx(c);
+        return st;
+    }
+    if (cudaMemcpy(c->d_col, col, c->nnz * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_val, val, c->nnz * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+        free_ctx(c);
+        return set_err(DDG_E_CUDA, "upload of A failed");
+    }
+    c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val};
+    if ((st = upload(&c->d_oidx, c->oidx)) || (st = upload(&c->d_ops, c->ops)) ||
+        (st = upload(&c->d_items, c->items)) || (st = upload(&c->d_red, c->red)) ||
+        (st = dalloc(&c->d_tiles, c->tiles_doubles)) || (st = dalloc(&c->d_s, c->s_doubles)) ||
+        (st = dalloc(&c->d_partials, c->part_doubles)) || (st = upload(&c->d_bptr, c->bptr)) ||
+        (st = upload(&c->d_bidx, c->bidx)) || (st = upload(&c->d_cptr, c->cptr)) ||
+        (st = upload(&c->d_qoff, c->qoff)) || (st = upload(&c->d_Q, c->Q)) ||
+        (st = dalloc(&c->d_yc, c->nc)) || (st = dalloc(&c->d_r, n)) || (st = dalloc(&c->d_z, n)) ||
+        (st = dalloc(&c->d_p, n)) || (st = dalloc(&c->d_q, n)) || (st = dalloc(&c->d_f, n)) ||
+        (st = dalloc(&c->d_u, n)) || (st = dalloc(&c->d_x, n)) || (st = dalloc(&c->d_sc, 1)) ||
+        (st = dalloc(&c->d_redbuf, RED_BLOCKS)) || (st = dalloc(&c->d_ticket, 1)) ||
+        (st = dalloc(&c->d_zero, 1))) {
+        free_ctx(c);
+        return st;
+    }
+    if (cudaMemset(c->d_s, 0, c->s_doubles * 8) != cudaSuccess ||
+        cudaMemset(c->d_ticket, 0, sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(c->d_zero, 0, sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(c->d_sc, 0, sizeof(Scalars)) != cudaSuccess ||
+        cudaMallocHost(&c->h_sc, sizeof(Scalars)) != cudaSuccess ||
+        cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+        free_ctx(c);
+        return set_err(DDG_E_CUDA, "device initialisation failed");
+    }
+    c->maxmI = 0;
+    for (int I = 0; I < nparts; ++I) c->maxmI = std::max<int>(c->maxmI, (int)(c->bptr[I + 1] - c->bptr[I]));
+    tick("upload");
+    if ((st = invert_locals(c))) { free_ctx(c); return st; }
+    tick("local inverses (GPU)");
+    if ((st = invert_coarse(c, er, ec, ev))) { free_ctx(c); return st; }
+    tick("coarse inverse (GPU)");
+    c->local_bytes = 0;
+    for (int q = 0; q < nparts; ++q) {
+        const OpDesc& op = c->ops[q];
+        for (int t = 0; t < op.nitems; ++t) c->local_bytes += (int64_t)c->items[op.item_base + t].ntiles * TILE_ELEMS * 8;
+    }
+    c->coarse_bytes = (c->tiles_doubles * 8) - c->local_bytes;
+    c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = c;
+    return DDG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// preconditioner and PCG enqueue
+// ---------------------------------------------------------------------------
+static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
+    const ColourPlan& pl = c->plans[cc];
+    launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, c->d_oidx, c->A, r, z,
+                  c->d_s, z_zero, done);
+    launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
+                c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done);
+    launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, pl.red_begin,
+                       pl.red_end - pl.red_begin, c->d_oidx, c->d_partials, z, nullptr, done);
+    c->launches += 2 + (pl.red_end > pl.red_begin);
+}
+
+static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
+    const OpDesc& op = c->ops[c->coarse_op];
+    launch_coarse_restrict(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
+                           c->A, r, z, c->d_s + op.s_off, c->maxmI, done);
+    launch_symv(c->stream, c->d_ops, c->d_items, c->coarse_item_begin,
+                c->coarse_item_end - c->coarse_item_begin, c->d_tiles, c->d_s, c->d_oidx, nullptr,
+                c->d_yc, c->d_partials, done);
+    launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, c->coarse_red_begin,
+                       c->coarse_red_end - c->coarse_red_begin, c->d_oidx, c->d_partials, nullptr,
+                       c->d_yc, done);
+    launch_prolong(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc, z, done);
+    c->launches += 3 + (c->coarse_red_end > c->coarse_red_begin);
+}
+
+// z = M r: zero guess, forward sweep, coarse, reverse sweep
+static void enqueue_precond(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
+    launch_fill(c->stream, z, c->n, 0.0, done);
+    c->launches += 1;
+    for (int cc = 0; cc < c->ncolours; ++cc) colour_step(c, cc, r, z, cc == 0, done);
+    coarse_add(c, r, z, done);
+    for (int cc = c->ncolours - 1; cc >= 0; --cc) colour_step(c, cc, r, z, false, done);
+}
+
+static void enqueue_iteration(ddg_ctx* c, double* u) {
+    Scalars* sc = c->d_sc;
+    const int32_t* done = &sc->done;
+    launch_pcg_spmv_dot(c->stream, c->A, c->d_p, c->d_q, sc, c->d_redbuf, c->d_ticket);
+    launch_pcg_update(c->stream, c->n, c->d_p, c->d_q, u, c->d_r, sc, c->d_hist, c->d_redbuf, c->d_ticket);
+    enqueue_precond(c, c->d_r, c->d_z, done);
+    launch_pcg_rz(c->stream, c->n, c->d_r, c->d_z, sc, c->d_redbuf, c->d_ticket);
+    launch_pcg_direction(c->stream, c->n, c->d_z, c->d_p, sc);
+    c->launches += 4;
+}
+
+static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int max_iter,
+                   int* iters, double* res_hist, int cap, ddg_report* rep) {
+    if (!(rtol > 0)) return set_err(DDG_E_ARG, "rtol must be > 0");
+    if (max_iter <= 0) max_iter = c->opts.max_iter;
+    if (max_iter + 1 > c->hist_cap) {
+        if (c->d_hist) cudaFree(c->d_hist);
+        c->d_hist = nullptr;
+        int st = dalloc(&c->d_hist, max_iter + 1);
+        if (st) return st;
+        c->hist_cap = max_iter + 1;
+    }
+    Scalars init{};
+    init.rtol = rtol;
+    init.max_iter = max_iter;
+    init.stop_mode = c->opts.stop_mode;
+    *c->h_sc = init;
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_sc, c->h_sc, sizeof(Scalars), cudaMemcpyHostToDevice, c->stream));
+    launch_pcg_init(c->stream, c->n, d_f, c->d_r, d_u, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket);
+    enqueue_precond(c, c->d_r, c->d_z, &c->d_sc->done);
+    launch_pcg_rz_first(c->stream, c->n, c->d_r, c->d_z, c->d_p, c->d_sc, c->d_redbuf, c->d_ticket);
+    c->launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    // iteration graph (captured once per u pointer)
+    bool use_graph = c->opts.use_graphs != 0;
+    if (use_graph && (!c->ge_iter || c->g_iter_u != d_u)) {
+        if (c->ge_iter) cudaGraphExecDestroy(c->ge_iter);
+        if (c->g_iter) cudaGraphDestroy(c->g_iter);
+        c->ge_iter = nullptr;
+        c->g_iter = nullptr;
+        int64_t l0 = c->launches;
+        CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_iteration(c, d_u);
+        cudaError_t e = cudaStreamEndCapture(c->stream, &c->g_iter);
+        if (e != cudaSuccess) return set_err(DDG_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        CUDA_TRY(cudaGraphInstantiate(&c->ge_iter, c->g_iter, 0));
+        c->launches_per_iter = c->launches - l0;
+        c->launches = l0;
+        c->g_iter_u = d_u;
+    }
+    int done_iters = 0;
+    int chunk = 2;
+    while (done_iters < max_iter) {
+        const int todo = std::min(chunk, max_iter - done_iters);
+        for (int t = 0; t < todo; ++t) {
+            if (use_graph) {
+                CUDA_TRY(cudaGraphLaunch(c->ge_iter, c->stream));
+                c->launches += c->launches_per_iter;
+            } else {
+                enqueue_iteration(c, d_u);
+            }
+        }
+        done_iters += todo;
+        CUDA_TRY(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (c->h_sc->done) break;
+        chunk = std::min(chunk * 2, 8);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+    CUDA_TRY(cudaEventSynchronize(c->ev1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    const Scalars s = *c->h_sc;
+    const int it = s.iter;
+    if (iters) *iters = it;
+    if (res_hist && cap > 0) {
+        int cnt = std::min(cap, it + 1);
+        CUDA_TRY(cudaMemcpy(res_hist, c->d_hist, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (rep) {
+        rep->converged = s.converged;
+        rep->iters = it;
+        rep->res0 = s.res0;
+        rep->res_final = s.res;
+        rep->t_setup = c->t_setup;
+        rep->t_solve = ms * 1e-3;
+        rep->frac_iters = (double)it;
+        if (it >= 1 && s.converged && s.res > 0) {
+            std::vector<double> h(it + 1);
+            if (cudaMemcpy(h.data(), c->d_hist, (it + 1) * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess) {
+                double tol = s.rtol * s.ref;
+                double a = log10(h[it - 1]), b = log10(h[it]), lt = log10(tol);
+                if (a != b) rep->frac_iters = (it - 1) + (a - lt) / (a - b);
+            }
+        }
+    }
+    if (s.status) return set_err(s.status, "PCG breakdown (p^T A p <= 0 or r^T z <= 0) at iteration %d", it);
+    return DDG_OK;
+}
+
+extern "C" int ddg_pcg_solve_device(ddg_ctx* c, const double* d_f, double rtol, int max_iter, double* d_u,
+                                    int* iters, double* res_hist, int res_hist_cap, ddg_report* rep) {
+    if (!c || !d_f || !d_u) return set_err(DDG_E_ARG, "null argument");
+    if (cudaSetDevice(c->device) != cudaSuccess) return set_err(DDG_E_CUDA, "cudaSetDevice failed");
+    return run_pcg(c, d_f, d_u, rtol, max_iter, iters, res_hist, res_hist_cap, rep);
+}
+
+extern "C" int ddg_pcg_solve(ddg_ctx* c, const double* f, double rtol, int max_iter, double* u,
+                             int* iters, double* res_hist, int res_hist_cap, ddg_report* rep) {
+    if (!c || !f || !u) return set_err(DDG_E_ARG, "null argument");
+    if (cudaSetDevice(c->device) != cudaSuccess) return set_err(DDG_E_CUDA, "cudaSetDevice failed");
+    CUDA_TRY(cudaMemcpyAsync(c->d_f, f, c->n * 8, cudaMemcpyHostToDevice, c->stream));
+    int st = run_pcg(c, c->d_f, c->d_u, rtol, max_iter, iters, res_hist, res_hist_cap, rep);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpyAsync(u, c->d_u, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return DDG_OK;
+}
+
+static int host_vec_op(ddg_ctx* c, const double* in, double* out, int which) {
+    if (!c || !in || !out) return set_err(DDG_E_ARG, "null argument");
+    if (cudaSetDevice(c->device) != cudaSuccess) return set_err(DDG_E_CUDA, "cudaSetDevice failed");
+    CUDA_TRY(cudaMemcpyAsync(c->d_x, in, c->n * 8, cudaMemcpyHostToDevice, c->stream));
+    if (which == 0) {
+        enqueue_precond(c, c->d_x, c->d_z, c->d_zero);
+    } else if (which == 1) {
+        launch_fill(c->stream, c->d_z, c->n, 0.0, nullptr);
+        coarse_add(c, c->d_x, c->d_z, c->d_zero);
+    } else {
+        launch_spmv(c->stream, c->A, c->d_x, c->d_z);
+        c->launches += 1;
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, c->d_z, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return DDG_OK;
+}
+
+extern "C" int ddg_apply_precond(ddg_ctx* c, const double* r, double* z) { return host_vec_op(c, r, z, 0); }
+extern "C" int ddg_coarse_correct(ddg_ctx* c, const double* r, double* z) { return host_vec_op(c, r, z, 1); }
+extern "C" int ddg_spmv(ddg_ctx* c, const double* x, double* y) { return host_vec_op(c, x, y, 2); }
+
+extern "C" int ddg_get_info(ddg_ctx* c, ddg_info* info) {
+    if (!c || !info) return set_err(DDG_E_ARG, "null argument");
+    memset(info, 0, sizeof *info);
+    info->n = c->n;
+    info->n_c = c->nc;
+    info->nparts = c->nparts;
+    info->ncolours = c->ncolours;
+    int mmin = INT32_MAX, mmax = 0;
+    for (int q = 0; q < c->nparts; ++q) {
+        mmin = std::min(mmin, c->ops[q].m);
+        mmax = std::max(mmax, c->ops[q].m);
+    }
+    info->m_min = mmin;
+    info->m_max = mmax;
+    info->k = c->k;
+    info->dropped = c->dropped;
+    info->min_rank_ratio = c->min_ratio;
+    info->local_factor_bytes = c->local_bytes;
+    info->coarse_factor_bytes = c->coarse_bytes;
+    info->coarse_variant = 1;
+    return DDG_OK;
+}
+
+extern "C" int ddg_get_colours(ddg_ctx* c, int32_t* colour) {
+    if (!c || !colour) return set_err(DDG_E_ARG, "null argument");
+    std::copy(c->colour.begin(), c->colour.end(), colour);
+    return DDG_OK;
+}
+
+extern "C" int ddg_get_subdomain_sizes(ddg_ctx* c, int32_t* m) {
+    if (!c || !m) return set_err(DDG_E_ARG, "null argument");
+    for (int q = 0; q < c->nparts; ++q) m[c->order[q]] = c->ops[q].m;
+    return DDG_OK;
+}
+
+extern "C" int64_t ddg_launch_count(ddg_ctx* c, int reset) {
+    if (!c) return -1;
+    int64_t v = c->launches;
+    if (reset) c->launches = 0;
+    return v;
+}

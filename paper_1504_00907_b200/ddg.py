@@ -1,0 +1,210 @@
+"""Thin ctypes binding of libddg (include/ddg.h) — argument marshalling only.
+
+Every step of setup and of the PCG hot path runs inside libddg.so (host C++
+setup + sm_100a kernels).  There is no CPU fallback: if the library is missing
+or no CUDA device is visible, every call raises DDGError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libddg.so")
+_lib = None
+
+DDG_OK = 0
+STATUS = {0: "DDG_OK", 1: "DDG_E_ARG", 2: "DDG_E_DIM", 3: "DDG_E_PART", 4: "DDG_E_ZERO_BLOCK",
+          5: "DDG_E_NOT_SPD", 6: "DDG_E_COLOURING", 7: "DDG_E_BREAKDOWN", 8: "DDG_E_CUDA",
+          9: "DDG_E_NCCL", 10: "DDG_E_OOM"}
+STOP_RES0, STOP_RES1, STOP_PREC = 0, 1, 2
+
+# symbols declared in include/ddg.h (checked by tests/test_abi.py)
+EXPORTS = ["ddg_default_opts", "ddg_setup", "ddg_pcg_solve", "ddg_pcg_solve_device",
+           "ddg_apply_precond", "ddg_coarse_correct", "ddg_spmv", "ddg_get_info",
+           "ddg_get_colours", "ddg_get_subdomain_sizes", "ddg_launch_count", "ddg_destroy",
+           "ddg_status_string", "ddg_last_error"]
+
+
+class ddg_opts(C.Structure):
+    _fields_ = [("overlap", C.c_int), ("rank_tol", C.c_double), ("stop_mode", C.c_int),
+                ("max_iter", C.c_int), ("device", C.c_int), ("stream", C.c_void_p),
+                ("use_graphs", C.c_int), ("verbose", C.c_int)]
+
+
+class ddg_report(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iters", C.c_int), ("res0", C.c_double),
+                ("res_final", C.c_double), ("t_setup", C.c_double), ("t_solve", C.c_double),
+                ("frac_iters", C.c_double)]
+
+
+class ddg_info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_c", C.c_int64), ("nparts", C.c_int32),
+                ("ncolours", C.c_int32), ("m_min", C.c_int32), ("m_max", C.c_int32),
+                ("k", C.c_int32), ("dropped", C.c_int32), ("min_rank_ratio", C.c_double),
+                ("local_factor_bytes", C.c_int64), ("coarse_factor_bytes", C.c_int64),
+                ("coarse_variant", C.c_int32), ("pad", C.c_int32)]
+
+
+class DDGError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def load(path: str = LIB_PATH):
+    """Load libddg.so (build it first with paper_1504_00907_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise DDGError(8, f"{path} not built (run __graft_entry__.build()); no CPU fallback")
+    L = C.CDLL(path)
+    vp, i64, i32, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    L.ddg_default_opts.argtypes = [C.POINTER(ddg_opts)]
+    L.ddg_default_opts.restype = None
+    L.ddg_setup.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.POINTER(ddg_opts),
+                            C.POINTER(vp)]
+    L.ddg_setup.restype = C.c_int
+    for name in ("ddg_pcg_solve", "ddg_pcg_solve_device"):
+        f = getattr(L, name)
+        f.argtypes = [vp, vp, dbl, C.c_int, vp, C.POINTER(C.c_int), vp, C.c_int,
+                      C.POINTER(ddg_report)]
+        f.restype = C.c_int
+    for name in ("ddg_apply_precond", "ddg_coarse_correct", "ddg_spmv"):
+        getattr(L, name).argtypes = [vp, vp, vp]
+        getattr(L, name).restype = C.c_int
+    L.ddg_get_info.argtypes = [vp, C.POINTER(ddg_info)]
+    L.ddg_get_info.restype = C.c_int
+    L.ddg_get_colours.argtypes = [vp, vp]
+    L.ddg_get_subdomain_sizes.argtypes = [vp, vp]
+    L.ddg_launch_count.argtypes = [vp, C.c_int]
+    L.ddg_launch_count.restype = i64
+    L.ddg_destroy.argtypes = [vp]
+    L.ddg_destroy.restype = None
+    L.ddg_status_string.argtypes = [C.c_int]
+    L.ddg_status_string.restype = C.c_char_p
+    L.ddg_last_error.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _check(st):
+    if st != DDG_OK:
+        raise DDGError(st, load().ddg_last_error().decode())
+
+
+def default_opts() -> ddg_opts:
+    o = ddg_opts()
+    load().ddg_default_opts(C.byref(o))
+    return o
+
+
+class Solver:
+    """ddg_setup(A, F, partition, overlap) -> ddg_pcg_solve(f, rtol) (include/ddg.h)."""
+
+    def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
+                 stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
+                 verbose=False):
+        L = load()
+        o = default_opts()
+        o.overlap, o.rank_tol, o.stop_mode, o.max_iter = overlap, rank_tol, stop_mode, max_iter
+        o.device = device
+        o.stream = stream
+        o.use_graphs = 1 if use_graphs else 0
+        o.verbose = 1 if verbose else 0
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        ci = np.ascontiguousarray(col, np.int32)
+        va = np.ascontiguousarray(val, np.float64)
+        Ff = np.asfortranarray(F, dtype=np.float64)
+        pa = np.ascontiguousarray(part, np.int32)
+        self.n = int(n)
+        h = C.c_void_p()
+        st = L.ddg_setup(self.n, _p(rp), _p(ci), _p(va), _p(Ff), int(Ff.shape[1]), _p(pa),
+                         int(nparts), C.byref(o), C.byref(h))
+        _check(st)
+        self._h = h
+        self.max_iter = max_iter
+        self.info = ddg_info()
+        _check(L.ddg_get_info(self._h, C.byref(self.info)))
+
+    @classmethod
+    def from_problem(cls, pr, **kw):
+        kw.setdefault("overlap", pr.overlap)
+        return cls(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts, **kw)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            load().ddg_destroy(h)
+            self._h = None
+
+    __del__ = close
+
+    def solve(self, f, rtol=1e-8, max_iter=None):
+        """Host buffers in, host buffers out (end-to-end path)."""
+        max_iter = self.max_iter if max_iter is None else max_iter
+        f = np.ascontiguousarray(f, np.float64)
+        u = np.empty(self.n)
+        hist = np.zeros(max_iter + 1)
+        it = C.c_int(0)
+        rep = ddg_report()
+        _check(load().ddg_pcg_solve(self._h, _p(f), float(rtol), int(max_iter), _p(u),
+                                    C.byref(it), _p(hist), len(hist), C.byref(rep)))
+        return u, it.value, hist[: it.value + 1].copy(), rep
+
+    def solve_device(self, f_ptr, u_ptr, rtol=1e-8, max_iter=None):
+        """f and u are device pointers (e.g. torch tensor data_ptr())."""
+        max_iter = self.max_iter if max_iter is None else max_iter
+        hist = np.zeros(max_iter + 1)
+        it = C.c_int(0)
+        rep = ddg_report()
+        _check(load().ddg_pcg_solve_device(self._h, C.c_void_p(f_ptr), float(rtol), int(max_iter),
+                                           C.c_void_p(u_ptr), C.byref(it), _p(hist), len(hist),
+                                           C.byref(rep)))
+        return it.value, hist[: it.value + 1].copy(), rep
+
+    def solve_host_ptr(self, f_ptr, u_ptr, rtol=1e-8, max_iter=None):
+        """f and u are (pinned) HOST pointers; the H2D/D2H copies happen inside."""
+        max_iter = self.max_iter if max_iter is None else max_iter
+        hist = np.zeros(max_iter + 1)
+        it = C.c_int(0)
+        rep = ddg_report()
+        _check(load().ddg_pcg_solve(self._h, C.c_void_p(f_ptr), float(rtol), int(max_iter),
+                                    C.c_void_p(u_ptr), C.byref(it), _p(hist), len(hist),
+                                    C.byref(rep)))
+        return it.value, hist[: it.value + 1].copy(), rep
+
+    def _vec(self, name, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty(self.n)
+        _check(getattr(load(), name)(self._h, _p(x), _p(y)))
+        return y
+
+    def apply_precond(self, r):
+        return self._vec("ddg_apply_precond", r)
+
+    def coarse_correct(self, r):
+        return self._vec("ddg_coarse_correct", r)
+
+    def spmv(self, x):
+        return self._vec("ddg_spmv", x)
+
+    def colours(self):
+        c = np.empty(self.info.nparts, np.int32)
+        _check(load().ddg_get_colours(self._h, _p(c)))
+        return c
+
+    def subdomain_sizes(self):
+        m = np.empty(self.info.nparts, np.int32)
+        _check(load().ddg_get_subdomain_sizes(self._h, _p(m)))
+        return m
+
+    def launch_count(self, reset=False):
+        return int(load().ddg_launch_count(self._h, 1 if reset else 0))

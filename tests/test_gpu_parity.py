@@ -1,0 +1,163 @@
+"""GPU parity: libddg (sm_100a, through the C ABI) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): solution within 1e-10 relative 2-norm,
+iteration count within +-1, every residual-history entry within 1e-8
+relative.  Integer/index work (colours, subdomain sizes) bit-exact.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from ddg_gen import problems as P
+
+pytestmark = pytest.mark.gpu
+
+U_TOL, H_TOL = 1e-10, 1e-8
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1504_00907_b200 import build
+    build.build()
+
+
+def _solver(pr, **kw):
+    from paper_1504_00907_b200 import Solver
+    return Solver.from_problem(pr, **kw)
+
+
+def compare_solve(pr, rtol=1e-8, stop_mode=0, max_iter=1000):
+    s = _solver(pr, stop_mode=stop_mode, max_iter=max_iter)
+    o = oracle.Oracle.from_problem(pr)
+    u, it, hist, rep = s.solve(pr.f, rtol)
+    uo, ito, histo, conv = o.pcg(pr.f, rtol, max_iter, stop_mode)
+    assert bool(rep.converged) == conv
+    assert abs(it - ito) <= 1, (it, ito)
+    m = min(len(hist), len(histo))
+    hr = np.abs(hist[:m] - histo[:m]) / histo[:m]
+    assert hr.max() <= H_TOL, hr
+    ur = np.linalg.norm(u - uo) / np.linalg.norm(uo)
+    assert ur <= U_TOL, ur
+    assert np.array_equal(s.colours(), o.colours())
+    return s, o, it, ur
+
+
+CASES = {
+    "C1": lambda: P.poisson2d(64, 8, 1, 1001),                 # BASELINE configs[0], full size
+    "poisson3d_24_b8_p2": lambda: P.poisson3d(24, 8, 2, 1002),  # C2 shape: m ~ 700-1000, multi-item ops
+    "lognormal_16_b4": lambda: P.lognormal3d(16, 4, 1, 1003),  # C3 shape
+    "elasticity_8_be4": lambda: P.elasticity3d(8, 4, 1004),     # C4 shape (m up to 1500)
+    "biharm_64_b16_p3": lambda: P.biharmonic2d(64, 16, 3, 1005),  # C5 shape (m = 321..388)
+    "poisson2d_ragged": lambda: P.poisson2d(37, 6, 2, 7),      # ragged blocks and tails
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_pcg_parity(name):
+    compare_solve(CASES[name]())
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_stop_modes(mode):
+    compare_solve(P.poisson2d(48, 8, 1, 11), stop_mode=mode)
+
+
+@pytest.mark.parametrize("name", ["C1", "poisson3d_24_b8_p2", "biharm_64_b16_p3", "elasticity_8_be4"])
+def test_apply_coarse_spmv_parity(name):
+    pr = CASES[name]()
+    s = _solver(pr)
+    o = oracle.Oracle.from_problem(pr)
+    r = np.random.default_rng(0).standard_normal(pr.n)
+    for g, ref in ((s.spmv(r), o.spmv(r)), (s.coarse_correct(r), o.coarse_correct(r)),
+                   (s.apply_precond(r), o.apply_precond(r))):
+        assert np.linalg.norm(g - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert s.info.n_c == o.nc and s.info.ncolours == o.ncolours
+    sizes = np.array([len(o.overlap_set(i)) for i in range(pr.nparts)])
+    assert np.array_equal(s.subdomain_sizes(), sizes)
+
+
+def test_preconditioner_symmetric_on_gpu():
+    pr = P.biharmonic2d(64, 16, 3, 5)
+    s = _solver(pr)
+    rs = np.random.default_rng(1)
+    x, y = rs.standard_normal(pr.n), rs.standard_normal(pr.n)
+    Mx, My = s.apply_precond(x), s.apply_precond(y)
+    assert abs(x @ My - y @ Mx) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(My)
+    assert x @ Mx > 0
+
+
+def test_bitwise_repeatable():
+    pr = P.poisson3d(24, 8, 2, 3)
+    s = _solver(pr)
+    u1, it1, h1, _ = s.solve(pr.f)
+    u2, it2, h2, _ = s.solve(pr.f)
+    assert it1 == it2 and np.array_equal(u1, u2) and np.array_equal(h1, h2)
+
+
+def test_edge_cases():
+    pr = P.poisson2d(32, 8, 1, 3)
+    s = _solver(pr)
+    u, it, hist, rep = s.solve(np.zeros(pr.n))
+    assert it == 0 and rep.converged and np.all(u == 0)
+    u, it, hist, rep = s.solve(pr.f, 1e-14, max_iter=2)
+    assert it == 2 and not rep.converged
+    # single subdomain: M = A^{-1}, one iteration
+    pr1 = P.poisson2d(12, 12, 1, 3)
+    u, it, hist, rep = _solver(pr1).solve(pr1.f, 1e-10)
+    assert it == 1 and rep.converged
+    # overlap 0 and rank-deficient F (duplicate column dropped on every part)
+    F2 = np.asfortranarray(np.concatenate([pr.F, pr.F[:, 1:2]], axis=1))
+    from paper_1504_00907_b200 import Solver
+    s2 = Solver(pr.n, pr.row_ptr, pr.col, pr.val, F2, pr.part, pr.nparts, overlap=0)
+    o2 = oracle.Oracle(pr.n, pr.row_ptr, pr.col, pr.val, F2, pr.part, pr.nparts, 0)
+    assert s2.info.dropped == pr.nparts == o2.dropped
+    u, it, hist, rep = s2.solve(pr.f)
+    uo, ito, histo, _ = o2.pcg(pr.f)
+    assert abs(it - ito) <= 1 and np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+
+
+def test_error_statuses():
+    from paper_1504_00907_b200 import DDGError, Solver
+    from tests.helpers import csr_from_dense, laplace1d
+    An = laplace1d(40)
+    An[0, 0] = An[-1, -1] = 1                      # singular (all-Neumann)
+    rp, c, v = csr_from_dense(An)
+    part = np.repeat(np.arange(4), 10).astype(np.int32)
+    with pytest.raises(DDGError) as e:
+        Solver(40, rp, c, v, np.ones((40, 1)), part, 4, overlap=1)
+    assert e.value.code == 5
+    F = np.ones((40, 1)); F[10:20] = 0
+    rp, c, v = csr_from_dense(laplace1d(40))
+    with pytest.raises(DDGError) as e:
+        Solver(40, rp, c, v, F, part, 4)
+    assert e.value.code == 4
+
+
+def test_full_c2_properties():
+    """BASELINE configs[1] (C2) at full size, in the configuration bench.py times:
+    properties that hold at any size (the oracle needs minutes there)."""
+    import scipy.sparse as sp
+    pr = P.make("C2")
+    s = _solver(pr)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    A = sp.csr_matrix((pr.val, pr.col, pr.row_ptr), shape=(pr.n, pr.n))
+    assert rep.converged and 2 <= it <= 20
+    assert abs(hist[0] - np.linalg.norm(pr.f)) <= 1e-13 * hist[0]
+    assert hist[-1] <= 1e-8 * hist[0]
+    true_res = np.linalg.norm(pr.f - A @ u) / np.linalg.norm(pr.f)
+    assert true_res <= 1e-7, true_res
+    # polynomial reproduction of the coarse space at full size
+    for j in (0, 4, 9):
+        Fj = pr.F[:, j]
+        z = s.coarse_correct(A @ Fj)
+        assert np.linalg.norm(z - Fj) <= 1e-9 * np.linalg.norm(Fj)
+    # symmetry probe of M at full size
+    rs = np.random.default_rng(2)
+    x, y = rs.standard_normal(pr.n), rs.standard_normal(pr.n)
+    Mx, My = s.apply_precond(x), s.apply_precond(y)
+    assert abs(x @ My - y @ Mx) <= 1e-11 * np.linalg.norm(x) * np.linalg.norm(My)
