@@ -163,6 +163,25 @@ int ddg_get_subdomain_sizes(ddg_ctx* ctx, int32_t* m);
  * kernels only); `reset` != 0 zeroes the counter after reading. */
 int64_t ddg_launch_count(ddg_ctx* ctx, int reset);
 
+/* Per-kernel timing of the hot path (CUDA events on the context stream).
+ * While profiling is on, solves run without CUDA graphs and every kernel of
+ * the listed classes is bracketed by an event pair; ddg_get_kernel_stats
+ * synchronises, sums the pairs recorded since the last call, and resets. */
+typedef struct {
+    int64_t symv_launches;     /* local colour SYMV launches (a4/a8 dominant kernel)          */
+    double symv_ms;            /* their summed device time                                    */
+    double symv_alg_bytes;     /* algorithmic bytes they must move: per subdomain visit the
+                                  packed inverse 8 m(m+1)/2 + s read 8m + z read-modify-write 16m */
+    double gather_ms;          /* residual restriction kernels                                */
+    double reduce_ms;          /* partial-sum reduction kernels                               */
+    double coarse_ms;          /* coarse restrict + coarse SYMV + prolong                     */
+    double vec_ms;             /* SpMV+dot, update, r^T z, direction, fill                    */
+    int64_t launches;          /* all kernels timed                                           */
+} ddg_kstats;
+
+int ddg_set_profiling(ddg_ctx* ctx, int on);
+int ddg_get_kernel_stats(ddg_ctx* ctx, ddg_kstats* st);
+
 /* Release every resource of the context (NULL is a no-op). */
 void ddg_destroy(ddg_ctx* ctx);
 

@@ -219,7 +219,39 @@ struct ddg_ctx {
     int64_t local_bytes = 0, coarse_bytes = 0;
     double t_setup = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // profiling (ddg_set_profiling)
+    bool profiling = false;
+    std::vector<cudaEvent_t> evpool;
+    struct ProfRec { int cat; int e0, e1; double bytes; };
+    std::vector<ProfRec> recs;
+    std::vector<double> colour_alg_bytes;
 };
+
+enum { PC_SYMV = 0, PC_GATHER, PC_REDUCE, PC_COARSE, PC_VEC, PC_N };
+
+static int prof_event(ddg_ctx* c) {
+    int need = 0;
+    for (auto& r : c->recs) need = std::max(need, std::max(r.e0, r.e1) + 1);
+    if ((int)c->evpool.size() <= need) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->evpool.push_back(e);
+    }
+    return need;
+}
+// bracket the launches issued by fn with an event pair when profiling
+template <typename Fn>
+static void prof(ddg_ctx* c, int cat, double bytes, Fn fn) {
+    if (!c->profiling) { fn(); return; }
+    ddg_ctx::ProfRec r{cat, 0, 0, bytes};
+    r.e0 = prof_event(c);
+    c->recs.push_back(r);
+    cudaEventRecord(c->evpool[r.e0], c->stream);
+    fn();
+    int e1 = prof_event(c);
+    c->recs.back().e1 = e1;
+    cudaEventRecord(c->evpool[e1], c->stream);
+}
 
 static void free_ctx(ddg_ctx* c) {
     if (!c) return;
@@ -233,6 +265,7 @@ static void free_ctx(ddg_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
+    for (auto e : c->evpool) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -564,6 +597,12 @@ static int build_plans(ddg_ctx* c) {
         pl.red_end = (int)c->red.size();
     }
     c->oidx.swap(sorted_idx);  // now in sweep order; optr no longer valid for oidx
+    c->colour_alg_bytes.assign(c->ncolours, 0.0);
+    for (int cc = 0; cc < c->ncolours; ++cc)
+        for (int q = c->plans[cc].sub_begin; q < c->plans[cc].sub_end; ++q) {
+            const double m = c->ops[q].m;
+            c->colour_alg_bytes[cc] += 8.0 * m * (m + 1) / 2 + 24.0 * m;
+        }
     // dense coarse inverse
     c->coarse_op = (int)c->ops.size();
     c->coarse_item_begin = (int)c->items.size();
@@ -833,32 +872,42 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
 // ---------------------------------------------------------------------------
 static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
     const ColourPlan& pl = c->plans[cc];
-    launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, c->d_oidx, c->A, r, z,
-                  c->d_s, z_zero, done);
-    launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
-                c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done);
-    launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, pl.red_begin,
-                       pl.red_end - pl.red_begin, c->d_oidx, c->d_partials, z, nullptr, done);
+    prof(c, PC_GATHER, 0, [&] {
+        launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, c->d_oidx, c->A, r, z,
+                      c->d_s, z_zero, done);
+    });
+    prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
+        launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
+                    c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done);
+    });
+    if (pl.red_end > pl.red_begin)
+        prof(c, PC_REDUCE, 0, [&] {
+            launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, pl.red_begin,
+                               pl.red_end - pl.red_begin, c->d_oidx, c->d_partials, z, nullptr, done);
+        });
     c->launches += 2 + (pl.red_end > pl.red_begin);
 }
 
 static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
     const OpDesc& op = c->ops[c->coarse_op];
-    launch_coarse_restrict(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
-                           c->A, r, z, c->d_s + op.s_off, c->maxmI, done);
-    launch_symv(c->stream, c->d_ops, c->d_items, c->coarse_item_begin,
-                c->coarse_item_end - c->coarse_item_begin, c->d_tiles, c->d_s, c->d_oidx, nullptr,
-                c->d_yc, c->d_partials, done);
-    launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, c->coarse_red_begin,
-                       c->coarse_red_end - c->coarse_red_begin, c->d_oidx, c->d_partials, nullptr,
-                       c->d_yc, done);
-    launch_prolong(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc, z, done);
+    prof(c, PC_COARSE, 0, [&] {
+        launch_coarse_restrict(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
+                               c->A, r, z, c->d_s + op.s_off, c->maxmI, done);
+        launch_symv(c->stream, c->d_ops, c->d_items, c->coarse_item_begin,
+                    c->coarse_item_end - c->coarse_item_begin, c->d_tiles, c->d_s, c->d_oidx, nullptr,
+                    c->d_yc, c->d_partials, done);
+        launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, c->coarse_red_begin,
+                           c->coarse_red_end - c->coarse_red_begin, c->d_oidx, c->d_partials, nullptr,
+                           c->d_yc, done);
+        launch_prolong(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc,
+                       z, done);
+    });
     c->launches += 3 + (c->coarse_red_end > c->coarse_red_begin);
 }
 
 // z = M r: zero guess, forward sweep, coarse, reverse sweep
 static void enqueue_precond(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
-    launch_fill(c->stream, z, c->n, 0.0, done);
+    prof(c, PC_VEC, 0, [&] { launch_fill(c->stream, z, c->n, 0.0, done); });
     c->launches += 1;
     for (int cc = 0; cc < c->ncolours; ++cc) colour_step(c, cc, r, z, cc == 0, done);
     coarse_add(c, r, z, done);
@@ -868,11 +917,16 @@ static void enqueue_precond(ddg_ctx* c, const double* r, double* z, const int32_
 static void enqueue_iteration(ddg_ctx* c, double* u) {
     Scalars* sc = c->d_sc;
     const int32_t* done = &sc->done;
-    launch_pcg_spmv_dot(c->stream, c->A, c->d_p, c->d_q, sc, c->d_redbuf, c->d_ticket);
-    launch_pcg_update(c->stream, c->n, c->d_p, c->d_q, u, c->d_r, sc, c->d_hist, c->d_redbuf, c->d_ticket);
+    prof(c, PC_VEC, 0, [&] {
+        launch_pcg_spmv_dot(c->stream, c->A, c->d_p, c->d_q, sc, c->d_redbuf, c->d_ticket);
+        launch_pcg_update(c->stream, c->n, c->d_p, c->d_q, u, c->d_r, sc, c->d_hist, c->d_redbuf,
+                          c->d_ticket);
+    });
     enqueue_precond(c, c->d_r, c->d_z, done);
-    launch_pcg_rz(c->stream, c->n, c->d_r, c->d_z, sc, c->d_redbuf, c->d_ticket);
-    launch_pcg_direction(c->stream, c->n, c->d_z, c->d_p, sc);
+    prof(c, PC_VEC, 0, [&] {
+        launch_pcg_rz(c->stream, c->n, c->d_r, c->d_z, sc, c->d_redbuf, c->d_ticket);
+        launch_pcg_direction(c->stream, c->n, c->d_z, c->d_p, sc);
+    });
     c->launches += 4;
 }
 
@@ -900,7 +954,7 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     c->launches += 2;
     CUDA_TRY(cudaGetLastError());
     // iteration graph (captured once per u pointer)
-    bool use_graph = c->opts.use_graphs != 0;
+    bool use_graph = c->opts.use_graphs != 0 && !c->profiling;
     if (use_graph && (!c->ge_iter || c->g_iter_u != d_u)) {
         if (c->ge_iter) cudaGraphExecDestroy(c->ge_iter);
         if (c->g_iter) cudaGraphDestroy(c->g_iter);
@@ -1048,4 +1102,31 @@ extern "C" int64_t ddg_launch_count(ddg_ctx* c, int reset) {
     int64_t v = c->launches;
     if (reset) c->launches = 0;
     return v;
+}
+
+extern "C" int ddg_set_profiling(ddg_ctx* c, int on) {
+    if (!c) return set_err(DDG_E_ARG, "null argument");
+    c->profiling = on != 0;
+    c->recs.clear();
+    return DDG_OK;
+}
+
+extern "C" int ddg_get_kernel_stats(ddg_ctx* c, ddg_kstats* st) {
+    if (!c || !st) return set_err(DDG_E_ARG, "null argument");
+    memset(st, 0, sizeof *st);
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (auto& r : c->recs) {
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->evpool[r.e0], c->evpool[r.e1]));
+        switch (r.cat) {
+            case PC_SYMV: st->symv_launches++; st->symv_ms += ms; st->symv_alg_bytes += r.bytes; break;
+            case PC_GATHER: st->gather_ms += ms; break;
+            case PC_REDUCE: st->reduce_ms += ms; break;
+            case PC_COARSE: st->coarse_ms += ms; break;
+            default: st->vec_ms += ms; break;
+        }
+        st->launches++;
+    }
+    c->recs.clear();
+    return DDG_OK;
 }

@@ -25,7 +25,7 @@ STOP_RES0, STOP_RES1, STOP_PREC = 0, 1, 2
 EXPORTS = ["ddg_default_opts", "ddg_setup", "ddg_pcg_solve", "ddg_pcg_solve_device",
            "ddg_apply_precond", "ddg_coarse_correct", "ddg_spmv", "ddg_get_info",
            "ddg_get_colours", "ddg_get_subdomain_sizes", "ddg_launch_count", "ddg_destroy",
-           "ddg_status_string", "ddg_last_error"]
+           "ddg_status_string", "ddg_last_error", "ddg_set_profiling", "ddg_get_kernel_stats"]
 
 
 class ddg_opts(C.Structure):
@@ -46,6 +46,13 @@ class ddg_info(C.Structure):
                 ("k", C.c_int32), ("dropped", C.c_int32), ("min_rank_ratio", C.c_double),
                 ("local_factor_bytes", C.c_int64), ("coarse_factor_bytes", C.c_int64),
                 ("coarse_variant", C.c_int32), ("pad", C.c_int32)]
+
+
+class ddg_kstats(C.Structure):
+    _fields_ = [("symv_launches", C.c_int64), ("symv_ms", C.c_double),
+                ("symv_alg_bytes", C.c_double), ("gather_ms", C.c_double),
+                ("reduce_ms", C.c_double), ("coarse_ms", C.c_double), ("vec_ms", C.c_double),
+                ("launches", C.c_int64)]
 
 
 class DDGError(RuntimeError):
@@ -84,6 +91,10 @@ def load(path: str = LIB_PATH):
     L.ddg_launch_count.restype = i64
     L.ddg_destroy.argtypes = [vp]
     L.ddg_destroy.restype = None
+    L.ddg_set_profiling.argtypes = [vp, C.c_int]
+    L.ddg_set_profiling.restype = C.c_int
+    L.ddg_get_kernel_stats.argtypes = [vp, C.POINTER(ddg_kstats)]
+    L.ddg_get_kernel_stats.restype = C.c_int
     L.ddg_status_string.argtypes = [C.c_int]
     L.ddg_status_string.restype = C.c_char_p
     L.ddg_last_error.restype = C.c_char_p
@@ -208,3 +219,11 @@ class Solver:
 
     def launch_count(self, reset=False):
         return int(load().ddg_launch_count(self._h, 1 if reset else 0))
+
+    def set_profiling(self, on=True):
+        _check(load().ddg_set_profiling(self._h, 1 if on else 0))
+
+    def kernel_stats(self) -> ddg_kstats:
+        st = ddg_kstats()
+        _check(load().ddg_get_kernel_stats(self._h, C.byref(st)))
+        return st

@@ -73,9 +73,14 @@ def test_apply_coarse_spmv_parity(name):
     s = _solver(pr)
     o = oracle.Oracle.from_problem(pr)
     r = np.random.default_rng(0).standard_normal(pr.n)
-    for g, ref in ((s.spmv(r), o.spmv(r)), (s.coarse_correct(r), o.coarse_correct(r)),
-                   (s.apply_precond(r), o.apply_precond(r))):
-        assert np.linalg.norm(g - ref) <= 1e-12 * np.linalg.norm(ref)
+    # M applies exact local solves; the GPU uses the explicit inverse A_i^{-1}
+    # (Gauss-Jordan), the oracle Cholesky solves: both are backward stable, so
+    # they agree to ~ eps * cond(A_i).  cond(A_i) <= ~1e3 for the 2nd-order
+    # problems, ~1e6 for the 13-point biharmonic blocks.
+    tol_m = 1e-9 if "biharm" in name else 1e-12
+    for g, ref, tol in ((s.spmv(r), o.spmv(r), 1e-14), (s.coarse_correct(r), o.coarse_correct(r), 1e-11),
+                        (s.apply_precond(r), o.apply_precond(r), tol_m)):
+        assert np.linalg.norm(g - ref) <= tol * np.linalg.norm(ref)
     assert s.info.n_c == o.nc and s.info.ncolours == o.ncolours
     sizes = np.array([len(o.overlap_set(i)) for i in range(pr.nparts)])
     assert np.array_equal(s.subdomain_sizes(), sizes)
