@@ -76,6 +76,7 @@ struct ColourPlan {
     int32_t item_begin, item_end;   // items of this colour
     int32_t red_begin, red_end;     // reduction tasks of multi-item ops
     int32_t max_rows;               // max m over the colour's subdomains
+    int32_t max_rows_t;             // max rows touched by one SYMV item (smem sizing)
 };
 
 // ---- kernel launchers (kernels.cu) ----------------------------------------
@@ -84,7 +85,7 @@ void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, 
                    const int32_t* done);
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
-                 double* y_out, double* partials, const int32_t* done);
+                 double* y_out, double* partials, const int32_t* done, int max_rows_t);
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
                         const double* partials, double* z, double* y_out, const int32_t* done);

@@ -710,9 +710,9 @@ static size_t symv_smem(int max_rows_t) {
 
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
-                 double* y_out, double* partials, const int32_t* done) {
+                 double* y_out, double* partials, const int32_t* done, int max_rows_t) {
     if (nitems <= 0) return;
-    const size_t smem = symv_smem(2 * MAX_BT * TILE);
+    const size_t smem = symv_smem(max_rows_t > 0 ? max_rows_t : 2 * MAX_BT * TILE);
     cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_symv<<<nitems, SYMV_WARPS * 32, smem, st>>>(ops, items, item_begin, tiles, s, oidx, z, y_out,
                                                   partials, done);

@@ -76,9 +76,10 @@ def test_apply_coarse_spmv_parity(name):
     # M applies exact local solves; the GPU uses the explicit inverse A_i^{-1}
     # (Gauss-Jordan), the oracle Cholesky solves: both are backward stable, so
     # they agree to ~ eps * cond(A_i).  cond(A_i) <= ~1e3 for the 2nd-order
-    # problems, ~1e6 for the 13-point biharmonic blocks.
+    # problems, ~1e6 for the 13-point biharmonic blocks; cond(A_c) likewise
+    # (1.6e6 at 128^2) for the coarse correction.
     tol_m = 1e-9 if "biharm" in name else 1e-12
-    for g, ref, tol in ((s.spmv(r), o.spmv(r), 1e-14), (s.coarse_correct(r), o.coarse_correct(r), 1e-11),
+    for g, ref, tol in ((s.spmv(r), o.spmv(r), 1e-14), (s.coarse_correct(r), o.coarse_correct(r), tol_m),
                         (s.apply_precond(r), o.apply_precond(r), tol_m)):
         assert np.linalg.norm(g - ref) <= tol * np.linalg.norm(ref)
     assert s.info.n_c == o.nc and s.info.ncolours == o.ncolours
