@@ -66,6 +66,12 @@ typedef struct {
     void* stream;         /* cudaStream_t to run on, or NULL: the context creates its own stream   */
     int use_graphs;       /* 1 (default): capture the preconditioner in a CUDA graph               */
     int verbose;          /* 0 (default): quiet; 1: setup timings on stderr                        */
+    int coarse_variant;   /* 0 auto (dense if n_c <= 8192), 1 dense packed inverse of A_c,
+                             2 sparse: nested dissection + supernodal block elimination         */
+    int block_ndim;       /* 0, or the dimension of block_coords                                    */
+    const int32_t* block_coords; /* optional nparts x block_ndim integer coordinates of the parts
+                             (host, borrowed): geometric nested dissection of the coarse graph;
+                             NULL: BFS level-set bisection                                       */
 } ddg_opts;
 
 typedef struct {

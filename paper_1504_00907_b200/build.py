@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libddg.so")
-SOURCES = ["kernels.cu", "setup.cpp"]
-HEADERS = ["ddg_internal.h", os.path.join("..", "..", "include", "ddg.h")]
+SOURCES = ["kernels.cu", "setup.cpp", "coarse_sparse.cpp"]
+HEADERS = ["ddg_internal.h", "ctx.h", os.path.join("..", "..", "include", "ddg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1,0 +1,679 @@
+// coarse_sparse.cpp — sparse direct solve of the DDG coarse system
+// A_c y = b_c, exploiting its block sparsity: "the same
+// sparsity pattern as the subdomain adjacency matrix, but with each non-zero
+// replaced with a small dense block".
+//
+// Symbolic (host): nested dissection of the part-adjacency graph (geometric
+// bisection when block coordinates are given, BFS level-set bisection
+// otherwise; every cut is verified to separate), supernodes = separators and
+// leaf boxes, boundary sets B_t = ancestor unknowns coupled to the subtree.
+// Numeric (device, level by level from the leaves): each front [S_t | B_t] is
+// assembled from A_c entries and the children's Schur complements
+// (extend-add), then the S_t pivots are eliminated by block Gauss-Jordan
+// exchange, which leaves H_t = A_SS^{-1}, G_t = A_BS A_SS^{-1} and the Schur
+// complement A_BB - A_BS A_SS^{-1} A_SB for the parent.
+// Solve (device): forward w_t = inc_B - G_t b_S (leaves to root), backward
+// x_S = H_t b_S - G_t^T x_B (root to leaves), each level one tiled SYMV launch
+// over the operator K_t = [[H_t, .], [-G_t, 0]] plus gather/reduce launches.
+// Bytes per solve: 2|G| + |H| (H packed lower) -- below the 2|L_c| of
+// Cholesky forward/back substitution.
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <functional>
+#include <numeric>
+
+#include "ctx.h"
+
+namespace {
+
+constexpr int LEAF_UNKNOWNS = 256;
+constexpr int FRONT_BT = 8;
+
+struct NDNode {
+    std::vector<int32_t> sep;  // blocks eliminated at this node
+    int child[2] = {-1, -1};
+    int parent = -1;
+    int height = 0;
+};
+
+}  // namespace
+
+struct SparseCoarse {
+    int nfront = 0, nlevels = 0;
+    std::vector<FrontDesc> fr;
+    std::vector<int32_t> fS, fB, fmap;
+    std::vector<int> lb;                       // fronts of level h: [lb[h], lb[h+1])
+    std::vector<int> g_begin, g_end, h_begin, h_end;
+    std::vector<int> fwd_b, bwd_b;             // task ranges per level (size nlevels+1)
+    std::vector<FRedTask> fwd, bwd;
+    std::vector<int64_t> contrib;
+    std::vector<int32_t> item_front;           // item (relative to item_base) -> front
+    int item_base = 0, item_end = 0;
+    int max_rows_t = 0;
+    int64_t fvec_doubles = 0, w_doubles = 0, ctile_doubles = 0;
+    // triplets per level (front-local row, col, value, front)
+    std::vector<std::vector<int32_t>> tr_r, tr_c, tr_f;
+    std::vector<std::vector<double>> tr_v;
+    // device
+    FrontDesc* d_fr = nullptr;
+    int32_t *d_fS = nullptr, *d_fB = nullptr, *d_fmap = nullptr, *d_item_front = nullptr;
+    FRedTask *d_fwd = nullptr, *d_bwd = nullptr;
+    int64_t* d_contrib = nullptr;
+    double *d_fvec = nullptr, *d_w = nullptr, *d_ctiles = nullptr, *d_bc = nullptr;
+    int64_t factor_bytes = 0;
+};
+
+void sparse_coarse_free(SparseCoarse* s) {
+    if (!s) return;
+    void* p[] = {s->d_fr, s->d_fS, s->d_fB, s->d_fmap, s->d_item_front, s->d_fwd, s->d_bwd,
+                 s->d_contrib, s->d_fvec, s->d_w, s->d_ctiles, s->d_bc};
+    for (void* x : p)
+        if (x) cudaFree(x);
+    delete s;
+}
+
+// --------------------------------------------------------------------------
+// nested dissection of the part-adjacency graph
+// --------------------------------------------------------------------------
+namespace {
+
+struct NDBuilder {
+    const std::vector<std::vector<int32_t>>& adj;
+    const std::vector<int32_t>& rank;
+    const int32_t* coords;
+    int ndim;
+    std::vector<NDNode> nodes;
+    std::vector<int32_t> mark;   // 0 none, 1 L, 2 R, 3 S, 4 in V (scratch)
+    std::vector<int32_t> lev;
+
+    NDBuilder(const std::vector<std::vector<int32_t>>& a, const std::vector<int32_t>& r,
+              const int32_t* co, int nd)
+        : adj(a), rank(r), coords(co), ndim(nd), mark(a.size(), 0), lev(a.size(), -1) {}
+
+    int64_t unknowns(const std::vector<int32_t>& V) const {
+        int64_t s = 0;
+        for (int32_t v : V) s += rank[v];
+        return s;
+    }
+
+    bool split_geom(const std::vector<int32_t>& V, std::vector<int32_t>& L, std::vector<int32_t>& R,
+                    std::vector<int32_t>& S) {
+        if (!coords) return false;
+        int axis = -1;
+        int32_t best = 0;
+        for (int d = 0; d < ndim; ++d) {
+            int32_t lo = INT32_MAX, hi = INT32_MIN;
+            for (int32_t v : V) {
+                lo = std::min(lo, coords[(int64_t)v * ndim + d]);
+                hi = std::max(hi, coords[(int64_t)v * ndim + d]);
+            }
+            if (hi - lo > best) { best = hi - lo; axis = d; }
+        }
+        if (axis < 0) return false;
+        std::vector<int32_t> vals;
+        vals.reserve(V.size());
+        for (int32_t v : V) vals.push_back(coords[(int64_t)v * ndim + axis]);
+        std::nth_element(vals.begin(), vals.begin() + vals.size() / 2, vals.end());
+        const int32_t m = vals[vals.size() / 2];
+        L.clear(); R.clear(); S.clear();
+        for (int32_t v : V) {
+            const int32_t x = coords[(int64_t)v * ndim + axis];
+            if (x < m) L.push_back(v); else if (x > m) R.push_back(v); else S.push_back(v);
+        }
+        if (L.empty() || R.empty()) return false;
+        fix_separation(L, R, S);
+        return true;
+    }
+
+    // move every R endpoint of an L-R edge into S
+    void fix_separation(std::vector<int32_t>& L, std::vector<int32_t>& R, std::vector<int32_t>& S) {
+        for (int32_t v : L) mark[v] = 1;
+        for (int32_t v : R) mark[v] = 2;
+        for (int32_t v : S) mark[v] = 3;
+        for (int32_t v : L)
+            for (int32_t u : adj[v])
+                if (mark[u] == 2) mark[u] = 3;
+        std::vector<int32_t> R2;
+        for (int32_t v : R) {
+            if (mark[v] == 3) S.push_back(v); else R2.push_back(v);
+        }
+        R.swap(R2);
+        for (int32_t v : L) mark[v] = 0;
+        for (int32_t v : R) mark[v] = 0;
+        for (int32_t v : S) mark[v] = 0;
+    }
+
+    // BFS level-structure bisection from a pseudo-peripheral node (induced subgraph)
+    void split_bfs(const std::vector<int32_t>& V, std::vector<int32_t>& L, std::vector<int32_t>& R,
+                   std::vector<int32_t>& S) {
+        for (int32_t v : V) mark[v] = 4;
+        auto bfs = [&](int32_t s, std::vector<int32_t>& order) {
+            order.clear();
+            for (int32_t v : V) lev[v] = -1;
+            lev[s] = 0;
+            order.push_back(s);
+            for (size_t h = 0; h < order.size(); ++h) {
+                int32_t v = order[h];
+                for (int32_t u : adj[v])
+                    if (mark[u] == 4 && lev[u] < 0) { lev[u] = lev[v] + 1; order.push_back(u); }
+            }
+        };
+        std::vector<int32_t> order;
+        bfs(V[0], order);
+        bfs(order.back(), order);
+        const int maxlev = lev[order.back()];
+        std::vector<int64_t> cnt(maxlev + 2, 0);
+        for (int32_t v : order) cnt[lev[v]]++;
+        int64_t cum = 0;
+        int cut = 0;
+        for (int l = 0; l <= maxlev; ++l) {
+            cum += cnt[l];
+            if (cum * 2 > (int64_t)V.size()) { cut = l; break; }
+        }
+        if (cut == 0 && maxlev >= 1) cut = 1;
+        L.clear(); R.clear(); S.clear();
+        for (int32_t v : V) {
+            if (lev[v] < 0) R.push_back(v);          // other components
+            else if (lev[v] < cut) L.push_back(v);
+            else if (lev[v] == cut) S.push_back(v);
+            else R.push_back(v);
+        }
+        for (int32_t v : V) { mark[v] = 0; lev[v] = -1; }
+    }
+
+    int build(std::vector<int32_t> V) {
+        const int id = (int)nodes.size();
+        nodes.emplace_back();
+        if (V.size() <= 1 || unknowns(V) <= LEAF_UNKNOWNS) {
+            std::sort(V.begin(), V.end());
+            nodes[id].sep = std::move(V);
+            return id;
+        }
+        std::vector<int32_t> L, R, S;
+        if (!split_geom(V, L, R, S)) split_bfs(V, L, R, S);
+        if (S.empty() && (L.empty() || R.empty())) {
+            std::sort(V.begin(), V.end());
+            nodes[id].sep = std::move(V);
+            return id;
+        }
+        if (S.empty()) {          // disconnected halves: eliminate one block here
+            S.push_back(R.back());
+            R.pop_back();
+        }
+        std::sort(S.begin(), S.end());
+        nodes[id].sep = S;
+        int k = 0;
+        for (auto* part : {&L, &R}) {
+            if (part->empty()) continue;
+            int ch = build(std::move(*part));
+            nodes[id].child[k++] = ch;
+            nodes[ch].parent = id;
+        }
+        return id;
+    }
+};
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+// symbolic phase: fronts, items, reduction tasks, triplets
+// --------------------------------------------------------------------------
+int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
+                           const std::vector<int32_t>& er, const std::vector<int32_t>& ec,
+                           const std::vector<double>& ev) {
+    const int np = c->nparts;
+    SparseCoarse* sc = new SparseCoarse();
+    c->sparse = sc;
+    // part adjacency
+    std::vector<std::vector<int32_t>> adj(np);
+    for (int I = 0; I < np; ++I) {
+        auto& a = adj[I];
+        for (int64_t x = c->bptr[I]; x < c->bptr[I + 1]; ++x) {
+            const int32_t v = c->bidx[x];
+            for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+                const int32_t J = c->part[col[e]];
+                if (J != I) a.push_back(J);
+            }
+        }
+        std::sort(a.begin(), a.end());
+        a.erase(std::unique(a.begin(), a.end()), a.end());
+    }
+    std::vector<int32_t> rank(np);
+    for (int I = 0; I < np; ++I) rank[I] = c->cptr[I + 1] - c->cptr[I];
+    NDBuilder nd(adj, rank, c->block_coords.empty() ? nullptr : c->block_coords.data(), c->block_ndim);
+    // one tree per connected component of the part graph
+    {
+        std::vector<int32_t> comp(np, -1);
+        std::vector<int32_t> stack;
+        for (int s = 0; s < np; ++s) {
+            if (comp[s] >= 0) continue;
+            std::vector<int32_t> V{s};
+            comp[s] = s;
+            stack.assign(1, s);
+            while (!stack.empty()) {
+                int32_t v = stack.back();
+                stack.pop_back();
+                for (int32_t u : adj[v])
+                    if (comp[u] < 0) { comp[u] = s; V.push_back(u); stack.push_back(u); }
+            }
+            nd.build(std::move(V));
+        }
+    }
+    auto& nodes = nd.nodes;
+    const int nn = (int)nodes.size();
+    // postorder, heights, Euler intervals
+    std::vector<int> post;
+    std::vector<int> tin(nn), tout(nn);
+    {
+        int timer = 0;
+        std::function<void(int)> dfs = [&](int t) {
+            tin[t] = timer++;
+            for (int k = 0; k < 2; ++k)
+                if (nodes[t].child[k] >= 0) dfs(nodes[t].child[k]);
+            int h = 0;
+            for (int k = 0; k < 2; ++k)
+                if (nodes[t].child[k] >= 0) h = std::max(h, nodes[nodes[t].child[k]].height + 1);
+            nodes[t].height = h;
+            post.push_back(t);
+            tout[t] = timer++;
+        };
+        for (int t = 0; t < nn; ++t)
+            if (nodes[t].parent < 0) dfs(t);
+    }
+    std::vector<int> postidx(nn);
+    for (int i = 0; i < nn; ++i) postidx[post[i]] = i;
+    auto is_anc = [&](int a, int b) { return tin[a] <= tin[b] && tout[b] <= tout[a]; };  // a ancestor-or-self of b
+    std::vector<int32_t> snode(np, -1);
+    for (int t = 0; t < nn; ++t)
+        for (int32_t b : nodes[t].sep) snode[b] = t;
+    // boundary block sets, bottom-up
+    std::vector<std::vector<int32_t>> Bblk(nn);
+    for (int t : post) {
+        std::vector<int32_t> cand;
+        for (int32_t b : nodes[t].sep) cand.insert(cand.end(), adj[b].begin(), adj[b].end());
+        for (int k = 0; k < 2; ++k)
+            if (nodes[t].child[k] >= 0) {
+                const auto& cb = Bblk[nodes[t].child[k]];
+                cand.insert(cand.end(), cb.begin(), cb.end());
+            }
+        std::vector<int32_t> keep;
+        for (int32_t u : cand) {
+            const int su = snode[u];
+            if (su != t && is_anc(su, t)) keep.push_back(u);
+        }
+        std::sort(keep.begin(), keep.end(), [&](int32_t a, int32_t b) {
+            return postidx[snode[a]] != postidx[snode[b]] ? postidx[snode[a]] < postidx[snode[b]] : a < b;
+        });
+        keep.erase(std::unique(keep.begin(), keep.end()), keep.end());
+        Bblk[t] = std::move(keep);
+    }
+    // fronts ordered by (height, postorder)
+    std::vector<int> order(nn);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        return nodes[a].height != nodes[b].height ? nodes[a].height < nodes[b].height : postidx[a] < postidx[b];
+    });
+    std::vector<int> fid(nn);
+    for (int i = 0; i < nn; ++i) fid[order[i]] = i;
+    sc->nfront = nn;
+    sc->nlevels = nn ? nodes[order.back()].height + 1 : 0;
+    sc->lb.assign(sc->nlevels + 1, 0);
+    for (int i = 0; i < nn; ++i) sc->lb[nodes[order[i]].height + 1]++;
+    for (int h = 0; h < sc->nlevels; ++h) sc->lb[h + 1] += sc->lb[h];
+    sc->fr.assign(nn, FrontDesc{});
+    for (int i = 0; i < nn; ++i) {
+        const int t = order[i];
+        FrontDesc& f = sc->fr[i];
+        f.parent = nodes[t].parent >= 0 ? fid[nodes[t].parent] : -1;
+        f.child0 = nodes[t].child[0] >= 0 ? fid[nodes[t].child[0]] : -1;
+        f.child1 = nodes[t].child[1] >= 0 ? fid[nodes[t].child[1]] : -1;
+        f.S_off = (int64_t)sc->fS.size();
+        for (int32_t b : nodes[t].sep)
+            for (int32_t q = c->cptr[b]; q < c->cptr[b + 1]; ++q) sc->fS.push_back(q);
+        f.nS = (int32_t)(sc->fS.size() - f.S_off);
+        f.B_off = (int64_t)sc->fB.size();
+        for (int32_t b : Bblk[t])
+            for (int32_t q = c->cptr[b]; q < c->cptr[b + 1]; ++q) sc->fB.push_back(q);
+        f.nB = (int32_t)(sc->fB.size() - f.B_off);
+        f.nSp = ((f.nS + TILE - 1) / TILE) * TILE;
+        const int nBp = ((f.nB + TILE - 1) / TILE) * TILE;
+        f.nK = f.nSp / TILE;
+        f.nT = (f.nSp + nBp) / TILE;
+        f.fvec_off = sc->fvec_doubles;
+        sc->fvec_doubles += (int64_t)f.nT * TILE;
+        f.w_off = sc->w_doubles;
+        sc->w_doubles += f.nB;
+        f.map_off = -1;
+    }
+    // child -> parent position maps
+    std::vector<int32_t> pos(c->nc, -1);
+    for (int i = 0; i < nn; ++i) {
+        FrontDesc& p = sc->fr[i];
+        for (int a = 0; a < p.nS; ++a) pos[sc->fS[p.S_off + a]] = a;
+        for (int j = 0; j < p.nB; ++j) pos[sc->fB[p.B_off + j]] = p.nSp + j;
+        for (int ci : {p.child0, p.child1}) {
+            if (ci < 0) continue;
+            FrontDesc& ch = sc->fr[ci];
+            ch.map_off = (int64_t)sc->fmap.size();
+            for (int j = 0; j < ch.nB; ++j) {
+                const int32_t q = sc->fB[ch.B_off + j];
+                if (pos[q] < 0) {
+                    delete sc;
+                    c->sparse = nullptr;
+                    return set_err(DDG_E_COLOURING, "sparse coarse: boundary unknown %d of front %d not in parent", q, ci);
+                }
+                sc->fmap.push_back(pos[q]);
+            }
+        }
+        for (int a = 0; a < p.nS; ++a) pos[sc->fS[p.S_off + a]] = -1;
+        for (int j = 0; j < p.nB; ++j) pos[sc->fB[p.B_off + j]] = -1;
+    }
+    // A_c entries -> the front eliminated first (the deeper supernode)
+    std::vector<int32_t> cblock(c->nc);
+    for (int I = 0; I < np; ++I)
+        for (int32_t q = c->cptr[I]; q < c->cptr[I + 1]; ++q) cblock[q] = I;
+    std::vector<std::vector<int64_t>> byfront(nn);
+    for (size_t e = 0; e < ev.size(); ++e) {
+        const int tr = snode[cblock[er[e]]], tc = snode[cblock[ec[e]]];
+        const int t = is_anc(tc, tr) ? tr : tc;   // descendant-or-self
+        byfront[fid[t]].push_back((int64_t)e);
+    }
+    sc->tr_r.assign(sc->nlevels, {});
+    sc->tr_c.assign(sc->nlevels, {});
+    sc->tr_f.assign(sc->nlevels, {});
+    sc->tr_v.assign(sc->nlevels, {});
+    for (int i = 0; i < nn; ++i) {
+        const FrontDesc& f = sc->fr[i];
+        const int h = nodes[order[i]].height;
+        for (int a = 0; a < f.nS; ++a) pos[sc->fS[f.S_off + a]] = a;
+        for (int j = 0; j < f.nB; ++j) pos[sc->fB[f.B_off + j]] = f.nSp + j;
+        for (int64_t e : byfront[i]) {
+            const int pr = pos[er[e]], pc = pos[ec[e]];
+            if (pr < 0 || pc < 0) {
+                delete sc;
+                c->sparse = nullptr;
+                return set_err(DDG_E_COLOURING, "sparse coarse: A_c entry (%d,%d) outside front %d", er[e], ec[e], i);
+            }
+            sc->tr_r[h].push_back(pr);
+            sc->tr_c[h].push_back(pc);
+            sc->tr_f[h].push_back(i);
+            sc->tr_v[h].push_back(ev[e]);
+        }
+        for (int a = f.nS; a < f.nSp; ++a) {      // identity on the S padding
+            sc->tr_r[h].push_back(a);
+            sc->tr_c[h].push_back(a);
+            sc->tr_f[h].push_back(i);
+            sc->tr_v[h].push_back(1.0);
+        }
+        for (int a = 0; a < f.nS; ++a) pos[sc->fS[f.S_off + a]] = -1;
+        for (int j = 0; j < f.nB; ++j) pos[sc->fB[f.B_off + j]] = -1;
+    }
+    // solve operators: ops + items (per level: all G items, then all H items)
+    std::vector<std::vector<int>> rowblk(nn);   // row-block starts (tiles) per front
+    for (int i = 0; i < nn; ++i) {
+        FrontDesc& f = sc->fr[i];
+        auto& rb = rowblk[i];
+        for (int t0 = 0; t0 < f.nK; t0 += FRONT_BT) rb.push_back(t0);
+        for (int t0 = f.nK; t0 < f.nT; t0 += FRONT_BT) rb.push_back(t0);
+        rb.push_back(f.nT);
+        OpDesc op{};
+        op.m = f.nS;
+        op.mp = f.nT * TILE;
+        op.nT = f.nT;
+        op.BT = FRONT_BT;
+        op.nblk = (int)rb.size() - 1;
+        op.out_mode = 1;
+        op.idx_off = -1;
+        op.s_off = f.fvec_off;
+        op.part_off = 0;
+        f.op = (int)c->ops.size();
+        c->ops.push_back(op);
+    }
+    sc->item_base = (int)c->items.size();
+    struct PendingItem { int front, bi, bj; };
+    std::vector<std::vector<int>> item_of(nn);   // item index per (bi, bj) pair, row-major over all blocks
+    auto nblkS = [&](int i) {
+        int k = 0;
+        for (size_t b = 0; b + 1 < rowblk[i].size(); ++b)
+            if (rowblk[i][b] < sc->fr[i].nK) ++k;
+        return k;
+    };
+    auto add_item = [&](int i, int bi, int bj) {
+        const FrontDesc& f = sc->fr[i];
+        const auto& rb = rowblk[i];
+        ItemDesc it{};
+        it.op = f.op;
+        it.I0 = rb[bi];
+        it.I1 = rb[bi + 1];
+        it.J0 = rb[bj];
+        it.J1 = rb[bj + 1];
+        it.tri = (bi == bj);
+        const int h = it.I1 - it.I0, wd = it.J1 - it.J0;
+        it.ntiles = it.tri ? h * (h + 1) / 2 : h * wd;
+        it.tile_off = sc->ctile_doubles;
+        sc->ctile_doubles += (int64_t)it.ntiles * TILE_ELEMS;
+        it.part_off = c->part_doubles;
+        c->part_doubles += (int64_t)(h + (it.tri ? 0 : wd)) * TILE;
+        sc->max_rows_t = std::max(sc->max_rows_t, (h + (it.tri ? 0 : wd)) * TILE);
+        item_of[i][bi * (rowblk[i].size() - 1) + bj] = (int)c->items.size();
+        c->items.push_back(it);
+        sc->item_front.push_back(i);
+    };
+    for (int i = 0; i < nn; ++i) item_of[i].assign((rowblk[i].size() - 1) * (rowblk[i].size() - 1), -1);
+    sc->g_begin.assign(sc->nlevels, 0);
+    sc->g_end.assign(sc->nlevels, 0);
+    sc->h_begin.assign(sc->nlevels, 0);
+    sc->h_end.assign(sc->nlevels, 0);
+    for (int h = 0; h < sc->nlevels; ++h) {
+        sc->g_begin[h] = (int)c->items.size();
+        for (int i = sc->lb[h]; i < sc->lb[h + 1]; ++i) {
+            const int nb = (int)rowblk[i].size() - 1, ns = nblkS(i);
+            for (int bi = ns; bi < nb; ++bi)
+                for (int bj = 0; bj < ns; ++bj) add_item(i, bi, bj);
+        }
+        sc->g_end[h] = sc->h_begin[h] = (int)c->items.size();
+        for (int i = sc->lb[h]; i < sc->lb[h + 1]; ++i) {
+            const int ns = nblkS(i);
+            for (int bi = 0; bi < ns; ++bi)
+                for (int bj = 0; bj <= bi; ++bj) add_item(i, bi, bj);
+        }
+        sc->h_end[h] = (int)c->items.size();
+    }
+    sc->item_end = (int)c->items.size();
+    // reduction tasks
+    sc->fwd_b.assign(sc->nlevels + 1, 0);
+    sc->bwd_b.assign(sc->nlevels + 1, 0);
+    for (int h = 0; h < sc->nlevels; ++h) {
+        sc->fwd_b[h] = (int)sc->fwd.size();
+        sc->bwd_b[h] = (int)sc->bwd.size();
+        for (int i = sc->lb[h]; i < sc->lb[h + 1]; ++i) {
+            const auto& rb = rowblk[i];
+            const int nb = (int)rb.size() - 1, ns = nblkS(i);
+            auto idx = [&](int bi, int bj) { return item_of[i][bi * nb + bj]; };
+            for (int bi = ns; bi < nb; ++bi) {       // forward: rows in B
+                FRedTask t{i, 0, rb[bi] * TILE, (rb[bi + 1] - rb[bi]) * TILE, (int)sc->contrib.size(), 0};
+                for (int bj = 0; bj < ns; ++bj) sc->contrib.push_back(c->items[idx(bi, bj)].part_off);
+                t.cend = (int)sc->contrib.size();
+                sc->fwd.push_back(t);
+            }
+            for (int b = 0; b < ns; ++b) {            // backward: rows in S
+                FRedTask t{i, 1, rb[b] * TILE, (rb[b + 1] - rb[b]) * TILE, (int)sc->contrib.size(), 0};
+                for (int bj = 0; bj <= b; ++bj) sc->contrib.push_back(c->items[idx(b, bj)].part_off);
+                for (int bi = b + 1; bi < nb; ++bi) {
+                    const ItemDesc& it = c->items[idx(bi, b)];
+                    sc->contrib.push_back(it.part_off + (int64_t)(it.I1 - it.I0) * TILE);
+                }
+                t.cend = (int)sc->contrib.size();
+                sc->bwd.push_back(t);
+            }
+        }
+    }
+    sc->fwd_b[sc->nlevels] = (int)sc->fwd.size();
+    sc->bwd_b[sc->nlevels] = (int)sc->bwd.size();
+    sc->factor_bytes = sc->ctile_doubles * 8;
+    return DDG_OK;
+}
+
+template <typename T>
+static int up(T** d, const std::vector<T>& h) {
+    int st = dalloc(d, h.size());
+    if (st) return st;
+    if (!h.empty() && cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+        return set_err(DDG_E_CUDA, "sparse coarse upload failed");
+    return DDG_OK;
+}
+
+// --------------------------------------------------------------------------
+// numeric phase (device)
+// --------------------------------------------------------------------------
+int sparse_coarse_numeric(ddg_ctx* c) {
+    SparseCoarse* sc = c->sparse;
+    int st;
+    if ((st = up(&sc->d_fr, sc->fr)) || (st = up(&sc->d_fS, sc->fS)) || (st = up(&sc->d_fB, sc->fB)) ||
+        (st = up(&sc->d_fmap, sc->fmap)) || (st = up(&sc->d_item_front, sc->item_front)) ||
+        (st = up(&sc->d_fwd, sc->fwd)) || (st = up(&sc->d_bwd, sc->bwd)) ||
+        (st = up(&sc->d_contrib, sc->contrib)) || (st = dalloc(&sc->d_fvec, sc->fvec_doubles)) ||
+        (st = dalloc(&sc->d_w, sc->w_doubles)) || (st = dalloc(&sc->d_ctiles, sc->ctile_doubles)) ||
+        (st = dalloc(&sc->d_bc, c->nc)))
+        return st;
+    const int nn = sc->nfront;
+    double** d_fptr = nullptr;
+    int32_t *d_err = nullptr, *d_ids = nullptr, *d_nT = nullptr, *d_nK = nullptr, *d_tasks = nullptr;
+    if ((st = dalloc(&d_fptr, nn)) || (st = dalloc(&d_err, 2)) || (st = dalloc(&d_ids, nn)) ||
+        (st = dalloc(&d_nT, nn)) || (st = dalloc(&d_nK, nn)) || (st = dalloc(&d_tasks, nn)))
+        return st;
+    int32_t herr[2] = {-1, -1};
+    CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
+    std::vector<double*> fptr(nn, nullptr);
+    std::vector<double*> level_buf(sc->nlevels, nullptr);
+    std::vector<int> max_parent_h(sc->nlevels, -1);
+    auto height_of = [&](int f) {
+        int h = 0;
+        while (!(sc->lb[h] <= f && f < sc->lb[h + 1])) ++h;
+        return h;
+    };
+    for (int h = 0; h < sc->nlevels; ++h)
+        for (int i = sc->lb[h]; i < sc->lb[h + 1]; ++i)
+            if (sc->fr[i].parent >= 0) max_parent_h[h] = std::max(max_parent_h[h], height_of(sc->fr[i].parent));
+    for (int h = 0; h < sc->nlevels; ++h) {
+        const int f0 = sc->lb[h], f1 = sc->lb[h + 1], nf = f1 - f0;
+        int64_t tot = 0;
+        for (int i = f0; i < f1; ++i) tot += (int64_t)sc->fr[i].nT * sc->fr[i].nT * TILE_ELEMS;
+        if ((st = dalloc(&level_buf[h], tot))) return st;
+        CUDA_TRY(cudaMemsetAsync(level_buf[h], 0, tot * sizeof(double), c->stream));
+        int64_t off = 0;
+        for (int i = f0; i < f1; ++i) {
+            fptr[i] = level_buf[h] + off;
+            off += (int64_t)sc->fr[i].nT * sc->fr[i].nT * TILE_ELEMS;
+        }
+        CUDA_TRY(cudaMemcpyAsync(d_fptr + f0, fptr.data() + f0, nf * sizeof(double*), cudaMemcpyHostToDevice, c->stream));
+        // assemble A_c entries
+        {
+            int32_t *dr = nullptr, *dc = nullptr, *df = nullptr;
+            double* dv = nullptr;
+            if ((st = up(&dr, sc->tr_r[h])) || (st = up(&dc, sc->tr_c[h])) || (st = up(&df, sc->tr_f[h])) ||
+                (st = up(&dv, sc->tr_v[h])))
+                return st;
+            launch_front_scatter(c->stream, (int64_t)sc->tr_v[h].size(), dr, dc, dv, df, sc->d_fr, d_fptr);
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            cudaFree(dr); cudaFree(dc); cudaFree(df); cudaFree(dv);
+        }
+        // extend-add the children's Schur complements (slot by slot: no write conflicts)
+        for (int slot = 0; slot < 2; ++slot) {
+            std::vector<int32_t> tasks;
+            int64_t maxe = 0;
+            for (int i = f0; i < f1; ++i) {
+                const int ch = slot == 0 ? sc->fr[i].child0 : sc->fr[i].child1;
+                if (ch >= 0 && sc->fr[ch].nB > 0) {
+                    tasks.push_back(ch);
+                    maxe = std::max<int64_t>(maxe, (int64_t)sc->fr[ch].nB * sc->fr[ch].nB);
+                }
+            }
+            if (tasks.empty()) continue;
+            CUDA_TRY(cudaMemcpyAsync(d_tasks, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c->stream));
+            launch_front_extend_add(c->stream, (int)tasks.size(), d_tasks, sc->d_fr, d_fptr, sc->d_fmap, maxe);
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+        }
+        // eliminate the S pivots: small fronts batched, big ones grid-wide
+        std::vector<int32_t> ids, nTs, nKs;
+        std::vector<double*> mats;
+        for (int i = f0; i < f1; ++i) {
+            const FrontDesc& f = sc->fr[i];
+            if (f.nT <= 64) {
+                ids.push_back(i);
+                nTs.push_back(f.nT);
+                nKs.push_back(f.nK);
+                mats.push_back(fptr[i]);
+            } else {
+                launch_gj_big(c->stream, f.nT, f.nK, fptr[i], i, d_err);
+            }
+        }
+        if (!ids.empty()) {
+            double** d_m = nullptr;
+            if ((st = dalloc(&d_m, ids.size()))) return st;
+            CUDA_TRY(cudaMemcpyAsync(d_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(d_nT, nTs.data(), ids.size() * 4, cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(d_nK, nKs.data(), ids.size() * 4, cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(d_m, mats.data(), ids.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream));
+            launch_gj_batched(c->stream, (int)ids.size(), d_nT, d_nK, d_m, d_ids, d_err);
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            cudaFree(d_m);
+        }
+        // pack the level's solve operators
+        launch_front_pack(c->stream, sc->g_begin[h], sc->h_end[h], sc->item_base, sc->d_item_front, sc->d_fr,
+                          d_fptr, c->d_items, sc->d_ctiles);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        // release levels whose fronts have all been absorbed by their parents
+        for (int l = 0; l < h; ++l)
+            if (level_buf[l] && max_parent_h[l] <= h) {
+                cudaFree(level_buf[l]);
+                level_buf[l] = nullptr;
+            }
+        if (c->opts.verbose)
+            fprintf(stderr, "[ddg_setup] coarse level %2d: %5d fronts, max front %d\n", h, nf,
+                    [&] { int m = 0; for (int i = f0; i < f1; ++i) m = std::max(m, sc->fr[i].nT * TILE); return m; }());
+    }
+    for (auto* b : level_buf)
+        if (b) cudaFree(b);
+    CUDA_TRY(cudaMemcpy(herr, d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    cudaFree(d_fptr); cudaFree(d_err); cudaFree(d_ids); cudaFree(d_nT); cudaFree(d_nK); cudaFree(d_tasks);
+    if (herr[0] >= 0)
+        return set_err(DDG_E_NOT_SPD, "coarse factor: front %d not positive definite at pivot %d", herr[0], herr[1]);
+    return DDG_OK;
+}
+
+// --------------------------------------------------------------------------
+// solve: y_c = A_c^{-1} b_c
+// --------------------------------------------------------------------------
+double* sparse_coarse_rhs(ddg_ctx* c) { return c->sparse->d_bc; }
+int64_t sparse_coarse_bytes(ddg_ctx* c) { return c->sparse ? c->sparse->factor_bytes : 0; }
+int sparse_coarse_levels(ddg_ctx* c) { return c->sparse ? c->sparse->nlevels : 0; }
+int sparse_coarse_nfront(ddg_ctx* c) { return c->sparse ? c->sparse->nfront : 0; }
+
+int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
+    SparseCoarse* sc = c->sparse;
+    int launches = 0;
+    for (int h = 0; h < sc->nlevels; ++h) {
+        const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
+        launch_front_fwd_assemble(c->stream, f0, nf, sc->d_fr, sc->d_fS, sc->d_fmap, sc->d_bc, sc->d_fvec,
+                                  sc->d_w, done);
+        launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->g_end[h] - sc->g_begin[h],
+                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t);
+        launch_front_reduce(c->stream, sc->d_fwd, sc->fwd_b[h], sc->fwd_b[h + 1] - sc->fwd_b[h], sc->d_contrib,
+                            sc->d_fr, sc->d_fS, c->d_partials, sc->d_w, d_x, done);
+        launches += 1 + (sc->g_end[h] > sc->g_begin[h]) + (sc->fwd_b[h + 1] > sc->fwd_b[h]);
+    }
+    for (int h = sc->nlevels - 1; h >= 0; --h) {
+        const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
+        launch_front_bwd_gather(c->stream, f0, nf, sc->d_fr, sc->d_fB, d_x, sc->d_fvec, done);
+        launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->h_end[h] - sc->g_begin[h],
+                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t);
+        launch_front_reduce(c->stream, sc->d_bwd, sc->bwd_b[h], sc->bwd_b[h + 1] - sc->bwd_b[h], sc->d_contrib,
+                            sc->d_fr, sc->d_fS, c->d_partials, sc->d_w, d_x, done);
+        launches += 3;
+    }
+    return launches;
+}

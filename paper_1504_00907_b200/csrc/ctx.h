@@ -1,0 +1,136 @@
+// ctx.h — the ddg_ctx object shared by setup.cpp and coarse_sparse.cpp (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ddg.h"
+#include "ddg_internal.h"
+
+using namespace ddg;
+
+int set_err(int code, const char* fmt, ...);
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            return set_err(_e == cudaErrorMemoryAllocation ? DDG_E_OOM : DDG_E_CUDA,     \
+                           "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+
+struct SparseCoarse;   // coarse_sparse.cpp
+void sparse_coarse_free(SparseCoarse* sc);
+
+template <typename T>
+static int dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    if (e != cudaSuccess)
+        return set_err(DDG_E_OOM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
+                       cudaGetErrorString(e));
+    return DDG_OK;
+}
+
+struct ddg_ctx {
+    ddg_opts opts{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t n = 0, nnz = 0;
+    int k = 0, nparts = 0;
+    // host structures
+    std::vector<int64_t> bptr;
+    std::vector<int32_t> bidx, bpos, part;
+    std::vector<int64_t> optr;
+    std::vector<int32_t> oidx;
+    std::vector<int32_t> colour, order;
+    int ncolours = 0;
+    std::vector<ColourPlan> plans;
+    std::vector<int32_t> cptr;
+    std::vector<int64_t> qoff;
+    std::vector<double> Q;
+    int64_t nc = 0;
+    int dropped = 0;
+    double min_ratio = INFINITY;
+    std::vector<OpDesc> ops;
+    std::vector<ItemDesc> items;
+    std::vector<RedDesc> red;
+    int coarse_op = -1;
+    int coarse_item_begin = 0, coarse_item_end = 0, coarse_red_begin = 0, coarse_red_end = 0;
+    int coarse_rows_t = 0;
+    int maxmI = 0;
+    int64_t tiles_doubles = 0, s_doubles = 0, part_doubles = 0;
+    // device
+    DevCSR A{};
+    int32_t *d_rp = nullptr, *d_col = nullptr;
+    double* d_val = nullptr;
+    int32_t* d_oidx = nullptr;
+    OpDesc* d_ops = nullptr;
+    ItemDesc* d_items = nullptr;
+    RedDesc* d_red = nullptr;
+    double *d_tiles = nullptr, *d_s = nullptr, *d_partials = nullptr;
+    int64_t* d_bptr = nullptr;
+    int32_t *d_bidx = nullptr, *d_cptr = nullptr;
+    int64_t* d_qoff = nullptr;
+    double *d_Q = nullptr, *d_yc = nullptr;
+    double *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_f = nullptr,
+           *d_u = nullptr, *d_x = nullptr;
+    Scalars* d_sc = nullptr;
+    double* d_hist = nullptr;
+    int hist_cap = 0;
+    double* d_redbuf = nullptr;
+    unsigned* d_ticket = nullptr;
+    int32_t* d_zero = nullptr;  // a device int that stays 0 (`done` for test hooks)
+    Scalars* h_sc = nullptr;    // pinned mirror
+    cudaGraph_t g_iter = nullptr;
+    cudaGraphExec_t ge_iter = nullptr;
+    const double* g_iter_u = nullptr;  // u pointer baked into the captured graph
+    int64_t launches = 0;
+    int64_t launches_per_iter = 0;
+    int64_t local_bytes = 0, coarse_bytes = 0;
+    double t_setup = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // profiling (ddg_set_profiling)
+    bool profiling = false;
+    std::vector<cudaEvent_t> evpool;
+    struct ProfRec { int cat; int e0, e1; double bytes; };
+    std::vector<ProfRec> recs;
+    std::vector<double> colour_alg_bytes;
+    // coarse solver variant: 1 dense packed inverse, 2 sparse supernodal (coarse_sparse.cpp)
+    int coarse_variant = 1;
+    SparseCoarse* sparse = nullptr;
+    std::vector<int32_t> block_coords;  // optional nparts x block_ndim
+    int block_ndim = 0;
+};
+
+enum { PC_SYMV = 0, PC_GATHER, PC_REDUCE, PC_COARSE, PC_VEC, PC_N };
+
+static int prof_event(ddg_ctx* c) {
+    int need = 0;
+    for (auto& r : c->recs) need = std::max(need, std::max(r.e0, r.e1) + 1);
+    if ((int)c->evpool.size() <= need) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->evpool.push_back(e);
+    }
+    return need;
+}
+// bracket the launches issued by fn with an event pair when profiling
+template <typename Fn>
+static void prof(ddg_ctx* c, int cat, double bytes, Fn fn) {
+    if (!c->profiling) { fn(); return; }
+    ddg_ctx::ProfRec r{cat, 0, 0, bytes};
+    r.e0 = prof_event(c);
+    c->recs.push_back(r);
+    cudaEventRecord(c->evpool[r.e0], c->stream);
+    fn();
+    int e1 = prof_event(c);
+    c->recs.back().e1 = e1;
+    cudaEventRecord(c->evpool[e1], c->stream);
+}
+

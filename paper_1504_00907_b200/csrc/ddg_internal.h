@@ -50,6 +50,29 @@ struct RedDesc {
     int32_t b;
 };
 
+// One front of the sparse coarse factorisation (coarse_sparse.cpp): the
+// separator unknowns S of a nested-dissection node, its boundary B (ancestor
+// unknowns coupled to its subtree), stored as a tiled dense [S|B] matrix.
+struct FrontDesc {
+    int32_t nT, nK;          // tiles per side of the [S|B] front, pivot (S) tiles
+    int32_t nS, nSp, nB;     // |S|, |S| padded to TILE, |B|
+    int32_t parent;          // parent front or -1
+    int32_t child0, child1;  // children or -1
+    int32_t op;              // OpDesc index of its solve operator
+    int32_t pad;
+    int64_t fvec_off;        // front vector (nT*TILE doubles)
+    int64_t w_off;           // w_t: contributions passed to the parent (nB doubles)
+    int64_t S_off, B_off;    // coarse index lists
+    int64_t map_off;         // B_t -> position in the parent's front (nB ints), -1 at a root
+};
+
+// Reduction task of the coarse solve: rows [row0, row0+nrows) of a front op.
+struct FRedTask {
+    int32_t front, kind;     // kind 0: w_t += (forward), 1: x[S_t] = (backward)
+    int32_t row0, nrows;
+    int32_t cbeg, cend;      // contributions [cbeg, cend) in the contrib offset list
+};
+
 // Device-side PCG scalars (one struct in device memory).
 struct Scalars {
     double rho, sigma, alpha, beta, gamma;
@@ -116,9 +139,28 @@ void launch_pcg_direction(cudaStream_t st, int64_t n, const double* z, double* p
 void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
                           const int32_t* oidx, DevCSR A, double* scratch,
                           const int64_t* scratch_off);
-void launch_gj_batched(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
-                       double* scratch, const int64_t* scratch_off, int32_t* err);
-void launch_gj_big(cudaStream_t st, int nT, double* M, int32_t* err);
+// Gauss-Jordan exchange on the first nK pivot tiles of nmat tiled dense
+// matrices (nK = nT: full inverse; nK < nT: partial, Schur complement left in
+// the trailing block).  ids[i] is reported in err[0] on a non-positive pivot.
+void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32_t* nK,
+                       double* const* mats, const int32_t* ids, int32_t* err);
+void launch_gj_big(cudaStream_t st, int nT, int nK, double* M, int id, int32_t* err);
+// sparse coarse factorisation / solve
+void launch_front_scatter(cudaStream_t st, int64_t ntrip, const int32_t* frow, const int32_t* fcol,
+                          const double* fval, const int32_t* ffront, const FrontDesc* fronts,
+                          double* const* fptr);
+void launch_front_extend_add(cudaStream_t st, int ntask, const int32_t* child, const FrontDesc* fronts,
+                             double* const* fptr, const int32_t* map, int64_t max_elems);
+void launch_front_pack(cudaStream_t st, int i0, int i1, int item_base, const int32_t* item_front,
+                       const FrontDesc* fronts, double* const* fptr, const ItemDesc* items, double* ctiles);
+void launch_front_fwd_assemble(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
+                               const int32_t* fS, const int32_t* map, const double* bc, double* fvec,
+                               double* w, const int32_t* done);
+void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
+                             const int32_t* fB, const double* x, double* fvec, const int32_t* done);
+void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,
+                         const FrontDesc* fronts, const int32_t* fS, const double* partials, double* w,
+                         double* x, const int32_t* done);
 void launch_scatter_coarse(cudaStream_t st, int64_t nent, const int32_t* row, const int32_t* col,
                            const double* val, int nT, int n_c, double* M);
 void launch_pack(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "ddg_internal.h"
 
 namespace ddg {
@@ -548,19 +550,20 @@ __device__ __forceinline__ void warp_right_mul(double* C, const double* Ps) {
     }
 }
 
-// one CTA (8 warps) inverts one tiled dense matrix in place
+// one CTA (8 warps) runs the exchange over the first nK pivot tiles of one
+// tiled dense matrix in place (nK = nT: full inverse)
 __global__ void __launch_bounds__(256)
-k_gj_batched(const int32_t* __restrict__ op_ids, const OpDesc* __restrict__ ops, double* scratch,
-             const int64_t* __restrict__ scratch_off, int32_t* err) {
+k_gj_batched(const int32_t* __restrict__ nTs, const int32_t* __restrict__ nKs, double* const* mats,
+             const int32_t* __restrict__ ids, int32_t* err) {
     extern __shared__ double gjsm[];
     double* Ps = gjsm;
     double (*Bs)[TILE_ELEMS] = reinterpret_cast<double (*)[TILE_ELEMS]>(gjsm + TILE_ELEMS);
-    const int opid = op_ids[blockIdx.x];
-    const int nT = ops[opid].nT;
-    double* M = scratch + scratch_off[blockIdx.x];
+    const int nT = nTs[blockIdx.x], nK = nKs[blockIdx.x];
+    const int opid = ids[blockIdx.x];
+    double* M = mats[blockIdx.x];
     const int w = threadIdx.x >> 5;
     auto tile = [&](int I, int J) { return M + ((int64_t)J * nT + I) * TILE_ELEMS; };
-    for (int k = 0; k < nT; ++k) {
+    for (int k = 0; k < nK; ++k) {
         for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = tile(k, k)[e];
         __syncthreads();
         tile_exchange_inverse(Ps, err, opid, k * TILE);
@@ -589,12 +592,12 @@ k_gj_batched(const int32_t* __restrict__ op_ids, const OpDesc* __restrict__ ops,
 }
 
 // ---- the same exchange for one big matrix, one launch per phase ---------------
-__global__ void k_gj_pivot(double* M, int nT, int k, int32_t* err) {
+__global__ void k_gj_pivot(double* M, int nT, int k, int id, int32_t* err) {
     __shared__ double Ps[TILE_ELEMS];
     double* T = M + ((int64_t)k * nT + k) * TILE_ELEMS;
     for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = T[e];
     __syncthreads();
-    tile_exchange_inverse(Ps, err, 0, k * TILE);
+    tile_exchange_inverse(Ps, err, id, k * TILE);
     for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) T[e] = Ps[e];
 }
 
@@ -673,6 +676,129 @@ __global__ void k_pack(const int32_t* __restrict__ op_ids, const OpDesc* __restr
                 if (I * TILE + i >= op.m || J * TILE + j >= op.m) v = 0.0;
                 dst[e] = v;
             }
+        }
+    }
+}
+
+// =============================================================================
+// Sparse coarse factorisation and solve (coarse_sparse.cpp)
+// =============================================================================
+
+__global__ void k_front_scatter(int64_t ntrip, const int32_t* __restrict__ frow,
+                                const int32_t* __restrict__ fcol, const double* __restrict__ fval,
+                                const int32_t* __restrict__ ffront, const FrontDesc* __restrict__ fronts,
+                                double* const* fptr) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ntrip;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int f = ffront[e];
+        double* M = fptr[f];
+        const int nT = fronts[f].nT;
+        M[tix(nT, frow[e], fcol[e])] = fval[e];
+        M[tix(nT, fcol[e], frow[e])] = fval[e];
+    }
+}
+
+// parent front += child's Schur complement (its B x B block), through the map
+__global__ void k_front_extend_add(const int32_t* __restrict__ child, const FrontDesc* __restrict__ fronts,
+                                   double* const* fptr, const int32_t* __restrict__ map) {
+    const FrontDesc c = fronts[child[blockIdx.y]];
+    const FrontDesc p = fronts[c.parent];
+    const double* Fc = fptr[child[blockIdx.y]];
+    double* Fp = fptr[c.parent];
+    const int32_t* mp = map + c.map_off;
+    const int64_t tot = (int64_t)c.nB * c.nB;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int a = (int)(e % c.nB), b = (int)(e / c.nB);
+        Fp[tix(p.nT, mp[a], mp[b])] += Fc[tix(c.nT, c.nSp + a, c.nSp + b)];
+    }
+}
+
+// tiles of the front's solve operator K_t = [[A_SS^-1, .], [-A_BS A_SS^-1, 0]]
+__global__ void k_front_pack(int i0, int i1, int item_base, const int32_t* __restrict__ item_front,
+                             const FrontDesc* __restrict__ fronts, double* const* fptr,
+                             const ItemDesc* __restrict__ items, double* __restrict__ ctiles) {
+    for (int itx = i0 + blockIdx.x; itx < i1; itx += gridDim.x) {
+        const ItemDesc it = items[itx];
+        const int fi = item_front[itx - item_base];
+        const FrontDesc fr = fronts[fi];
+        const double* M = fptr[fi];
+        for (int l = 0; l < it.ntiles; ++l) {
+            int I, J;
+            item_tile(it, l, I, J);
+            const double* src = M + ((int64_t)J * fr.nT + I) * TILE_ELEMS;
+            double* dst = ctiles + it.tile_off + (int64_t)l * TILE_ELEMS;
+            for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
+                const int i = e % TILE, j = e / TILE;
+                const int R = I * TILE + i, C = J * TILE + j;
+                double v = src[e];
+                if (I < fr.nK) {                    // H = A_SS^{-1}
+                    if (I == J) v = 0.5 * (v + src[i * TILE + j]);
+                    if (R >= fr.nS || C >= fr.nS) v = 0.0;
+                } else {                             // -G = -A_BS A_SS^{-1}
+                    v = -v;
+                    if (R - fr.nSp >= fr.nB || C >= fr.nS) v = 0.0;
+                }
+                dst[e] = v;
+            }
+        }
+    }
+}
+
+// forward: front vector [b_S ; 0] and w_t = incoming contributions to B
+__global__ void k_front_fwd_assemble(int f0, const FrontDesc* __restrict__ fronts,
+                                     const int32_t* __restrict__ fS, const int32_t* __restrict__ map,
+                                     const double* __restrict__ bc, double* __restrict__ fvec,
+                                     double* __restrict__ w, const int32_t* done) {
+    if (*done) return;
+    const FrontDesc f = fronts[f0 + blockIdx.x];
+    double* fv = fvec + f.fvec_off;
+    double* wt = w + f.w_off;
+    const int ntot = f.nT * TILE;
+    for (int a = threadIdx.x; a < ntot; a += blockDim.x) fv[a] = a < f.nS ? bc[fS[f.S_off + a]] : 0.0;
+    for (int a = threadIdx.x; a < f.nB; a += blockDim.x) wt[a] = 0.0;
+    __syncthreads();
+    for (int s = 0; s < 2; ++s) {
+        const int ci = s == 0 ? f.child0 : f.child1;
+        if (ci < 0) continue;
+        const FrontDesc c = fronts[ci];
+        for (int j = threadIdx.x; j < c.nB; j += blockDim.x) {
+            const int pos = map[c.map_off + j];
+            const double v = w[c.w_off + j];
+            if (pos < f.nSp) fv[pos] += v;
+            else wt[pos - f.nSp] += v;
+        }
+        __syncthreads();
+    }
+}
+
+// backward: B part of the front vector = x[B_t] (solved by ancestors)
+__global__ void k_front_bwd_gather(int f0, const FrontDesc* __restrict__ fronts,
+                                   const int32_t* __restrict__ fB, const double* __restrict__ x,
+                                   double* __restrict__ fvec, const int32_t* done) {
+    if (*done) return;
+    const FrontDesc f = fronts[f0 + blockIdx.x];
+    double* fv = fvec + f.fvec_off + f.nSp;
+    const int nBp = f.nT * TILE - f.nSp;
+    for (int a = threadIdx.x; a < nBp; a += blockDim.x) fv[a] = a < f.nB ? x[fB[f.B_off + a]] : 0.0;
+}
+
+__global__ void k_front_reduce(const FRedTask* __restrict__ tasks, int t0,
+                               const int64_t* __restrict__ contrib, const FrontDesc* __restrict__ fronts,
+                               const int32_t* __restrict__ fS, const double* __restrict__ partials,
+                               double* __restrict__ w, double* __restrict__ x, const int32_t* done) {
+    if (*done) return;
+    const FRedTask t = tasks[t0 + blockIdx.x];
+    const FrontDesc f = fronts[t.front];
+    for (int r = threadIdx.x; r < t.nrows; r += blockDim.x) {
+        double s = 0.0;
+        for (int c = t.cbeg; c < t.cend; ++c) s += partials[contrib[c] + r];
+        const int row = t.row0 + r;
+        if (t.kind == 0) {
+            const int b = row - f.nSp;
+            if (b >= 0 && b < f.nB) w[f.w_off + b] += s;
+        } else if (row < f.nS) {
+            x[fS[f.S_off + row]] = s;
         }
     }
 }
@@ -780,19 +906,19 @@ void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, cons
     k_extract_local<<<nops, 256, 0, st>>>(op_ids, ops, oidx, A, scratch, scratch_off);
 }
 
-void launch_gj_batched(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
-                       double* scratch, const int64_t* scratch_off, int32_t* err) {
-    if (nops <= 0) return;
+void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32_t* nK,
+                       double* const* mats, const int32_t* ids, int32_t* err) {
+    if (nmat <= 0) return;
     const int smem = 9 * TILE_ELEMS * sizeof(double);
     cudaFuncSetAttribute(k_gj_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_gj_batched<<<nops, 256, smem, st>>>(op_ids, ops, scratch, scratch_off, err);
+    k_gj_batched<<<nmat, 256, smem, st>>>(nT, nK, mats, ids, err);
 }
 
-void launch_gj_big(cudaStream_t st, int nT, double* M, int32_t* err) {
+void launch_gj_big(cudaStream_t st, int nT, int nK, double* M, int id, int32_t* err) {
     const int smem = 9 * TILE_ELEMS * sizeof(double);
     cudaFuncSetAttribute(k_gj_rowpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int k = 0; k < nT; ++k) {
-        k_gj_pivot<<<1, 256, 0, st>>>(M, nT, k, err);
+    for (int k = 0; k < nK; ++k) {
+        k_gj_pivot<<<1, 256, 0, st>>>(M, nT, k, id, err);
         k_gj_rowpanel<<<(nT + 7) / 8, 256, smem, st>>>(M, nT, k);
         k_gj_update<<<dim3(nT, (nT + 7) / 8), 256, 0, st>>>(M, nT, k);
         k_gj_colpanel<<<(nT + 7) / 8, 256, 0, st>>>(M, nT, k);
@@ -811,4 +937,42 @@ void launch_pack(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc*
     k_pack<<<dim3(8, nops), 256, 0, st>>>(op_ids, ops, items, scratch, scratch_off, tiles);
 }
 
+}  // namespace ddg
+
+namespace ddg {
+void launch_front_scatter(cudaStream_t st, int64_t ntrip, const int32_t* frow, const int32_t* fcol,
+                          const double* fval, const int32_t* ffront, const FrontDesc* fronts,
+                          double* const* fptr) {
+    if (ntrip <= 0) return;
+    k_front_scatter<<<RED_BLOCKS, 256, 0, st>>>(ntrip, frow, fcol, fval, ffront, fronts, fptr);
+}
+void launch_front_extend_add(cudaStream_t st, int ntask, const int32_t* child, const FrontDesc* fronts,
+                             double* const* fptr, const int32_t* map, int64_t max_elems) {
+    if (ntask <= 0) return;
+    int gx = (int)std::min<int64_t>(std::max<int64_t>(1, (max_elems + 255) / 256), 4096);
+    k_front_extend_add<<<dim3(gx, ntask), 256, 0, st>>>(child, fronts, fptr, map);
+}
+void launch_front_pack(cudaStream_t st, int i0, int i1, int item_base, const int32_t* item_front,
+                       const FrontDesc* fronts, double* const* fptr, const ItemDesc* items, double* ctiles) {
+    if (i1 <= i0) return;
+    k_front_pack<<<std::min(i1 - i0, 4096), 256, 0, st>>>(i0, i1, item_base, item_front, fronts, fptr, items,
+                                                          ctiles);
+}
+void launch_front_fwd_assemble(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
+                               const int32_t* fS, const int32_t* map, const double* bc, double* fvec,
+                               double* w, const int32_t* done) {
+    if (nf <= 0) return;
+    k_front_fwd_assemble<<<nf, 256, 0, st>>>(f0, fronts, fS, map, bc, fvec, w, done);
+}
+void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
+                             const int32_t* fB, const double* x, double* fvec, const int32_t* done) {
+    if (nf <= 0) return;
+    k_front_bwd_gather<<<nf, 256, 0, st>>>(f0, fronts, fB, x, fvec, done);
+}
+void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,
+                         const FrontDesc* fronts, const int32_t* fS, const double* partials, double* w,
+                         double* x, const int32_t* done) {
+    if (nt <= 0) return;
+    k_front_reduce<<<nt, 256, 0, st>>>(tasks, t0, contrib, fronts, fS, partials, w, x, done);
+}
 }  // namespace ddg

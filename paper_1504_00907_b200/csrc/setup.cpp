@@ -33,7 +33,7 @@ using namespace ddg;
 // ---------------------------------------------------------------------------
 static thread_local std::string g_last_error;
 
-static int set_err(int code, const char* fmt, ...) {
+int set_err(int code, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
     va_start(ap, fmt);
@@ -42,14 +42,6 @@ static int set_err(int code, const char* fmt, ...) {
     g_last_error = buf;
     return code;
 }
-
-#define CUDA_TRY(expr)                                                                   \
-    do {                                                                                 \
-        cudaError_t _e = (expr);                                                         \
-        if (_e != cudaSuccess)                                                           \
-            return set_err(_e == cudaErrorMemoryAllocation ? DDG_E_OOM : DDG_E_CUDA,     \
-                           "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
-    } while (0)
 
 extern "C" const char* ddg_last_error(void) { return g_last_error.c_str(); }
 
@@ -150,109 +142,15 @@ static inline DD dd_sqrt(DD a) {
 // ---------------------------------------------------------------------------
 // the context
 // ---------------------------------------------------------------------------
-template <typename T>
-static int dalloc(T** p, size_t count) {
-    *p = nullptr;
-    if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
-    if (e != cudaSuccess)
-        return set_err(DDG_E_OOM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
-                       cudaGetErrorString(e));
-    return DDG_OK;
-}
+#include "ctx.h"
 
-struct ddg_ctx {
-    ddg_opts opts{};
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    int64_t n = 0, nnz = 0;
-    int k = 0, nparts = 0;
-    // host structures
-    std::vector<int64_t> bptr;
-    std::vector<int32_t> bidx, bpos, part;
-    std::vector<int64_t> optr;
-    std::vector<int32_t> oidx;
-    std::vector<int32_t> colour, order;
-    int ncolours = 0;
-    std::vector<ColourPlan> plans;
-    std::vector<int32_t> cptr;
-    std::vector<int64_t> qoff;
-    std::vector<double> Q;
-    int64_t nc = 0;
-    int dropped = 0;
-    double min_ratio = INFINITY;
-    std::vector<OpDesc> ops;
-    std::vector<ItemDesc> items;
-    std::vector<RedDesc> red;
-    int coarse_op = -1;
-    int coarse_item_begin = 0, coarse_item_end = 0, coarse_red_begin = 0, coarse_red_end = 0;
-    int coarse_rows_t = 0;
-    int maxmI = 0;
-    int64_t tiles_doubles = 0, s_doubles = 0, part_doubles = 0;
-    // device
-    DevCSR A{};
-    int32_t *d_rp = nullptr, *d_col = nullptr;
-    double* d_val = nullptr;
-    int32_t* d_oidx = nullptr;
-    OpDesc* d_ops = nullptr;
-    ItemDesc* d_items = nullptr;
-    RedDesc* d_red = nullptr;
-    double *d_tiles = nullptr, *d_s = nullptr, *d_partials = nullptr;
-    int64_t* d_bptr = nullptr;
-    int32_t *d_bidx = nullptr, *d_cptr = nullptr;
-    int64_t* d_qoff = nullptr;
-    double *d_Q = nullptr, *d_yc = nullptr;
-    double *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_f = nullptr,
-           *d_u = nullptr, *d_x = nullptr;
-    Scalars* d_sc = nullptr;
-    double* d_hist = nullptr;
-    int hist_cap = 0;
-    double* d_redbuf = nullptr;
-    unsigned* d_ticket = nullptr;
-    int32_t* d_zero = nullptr;  // a device int that stays 0 (`done` for test hooks)
-    Scalars* h_sc = nullptr;    // pinned mirror
-    cudaGraph_t g_iter = nullptr;
-    cudaGraphExec_t ge_iter = nullptr;
-    const double* g_iter_u = nullptr;  // u pointer baked into the captured graph
-    int64_t launches = 0;
-    int64_t launches_per_iter = 0;
-    int64_t local_bytes = 0, coarse_bytes = 0;
-    double t_setup = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // profiling (ddg_set_profiling)
-    bool profiling = false;
-    std::vector<cudaEvent_t> evpool;
-    struct ProfRec { int cat; int e0, e1; double bytes; };
-    std::vector<ProfRec> recs;
-    std::vector<double> colour_alg_bytes;
-};
-
-enum { PC_SYMV = 0, PC_GATHER, PC_REDUCE, PC_COARSE, PC_VEC, PC_N };
-
-static int prof_event(ddg_ctx* c) {
-    int need = 0;
-    for (auto& r : c->recs) need = std::max(need, std::max(r.e0, r.e1) + 1);
-    if ((int)c->evpool.size() <= need) {
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        c->evpool.push_back(e);
-    }
-    return need;
-}
-// bracket the launches issued by fn with an event pair when profiling
-template <typename Fn>
-static void prof(ddg_ctx* c, int cat, double bytes, Fn fn) {
-    if (!c->profiling) { fn(); return; }
-    ddg_ctx::ProfRec r{cat, 0, 0, bytes};
-    r.e0 = prof_event(c);
-    c->recs.push_back(r);
-    cudaEventRecord(c->evpool[r.e0], c->stream);
-    fn();
-    int e1 = prof_event(c);
-    c->recs.back().e1 = e1;
-    cudaEventRecord(c->evpool[e1], c->stream);
-}
+// coarse_sparse.cpp
+int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col, const std::vector<int32_t>& er,
+                           const std::vector<int32_t>& ec, const std::vector<double>& ev);
+int sparse_coarse_numeric(ddg_ctx* c);
+int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done);
+double* sparse_coarse_rhs(ddg_ctx* c);
+int64_t sparse_coarse_bytes(ddg_ctx* c);
 
 static void free_ctx(ddg_ctx* c) {
     if (!c) return;
@@ -267,6 +165,7 @@ static void free_ctx(ddg_ctx* c) {
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
     for (auto e : c->evpool) cudaEventDestroy(e);
+    if (c->sparse) sparse_coarse_free(c->sparse);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -609,6 +508,7 @@ static int build_plans(ddg_ctx* c) {
             const double m = c->ops[q].m;
             c->colour_alg_bytes[cc] += 8.0 * m * (m + 1) / 2 + 24.0 * m;
         }
+    if (c->coarse_variant != 1) return DDG_OK;
     // dense coarse inverse
     c->coarse_op = (int)c->ops.size();
     c->coarse_item_begin = (int)c->items.size();
@@ -638,32 +538,42 @@ static int invert_locals(ddg_ctx* c) {
     const int64_t cap = std::max<int64_t>(budget / 8, max_single);
     int st = dalloc(&scratch, cap);
     if (st) return st;
-    int32_t *d_ids = nullptr, *d_err = nullptr;
+    int32_t *d_ids = nullptr, *d_err = nullptr, *d_nT = nullptr;
     int64_t* d_soff = nullptr;
-    if ((st = dalloc(&d_ids, np)) || (st = dalloc(&d_soff, np)) || (st = dalloc(&d_err, 2))) {
+    double** d_ptr = nullptr;
+    if ((st = dalloc(&d_ids, np)) || (st = dalloc(&d_soff, np)) || (st = dalloc(&d_err, 2)) ||
+        (st = dalloc(&d_nT, np)) || (st = dalloc(&d_ptr, np))) {
         cudaFree(scratch);
         return st;
     }
     int32_t herr[2] = {-1, -1};
     CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
-    std::vector<int32_t> ids;
+    std::vector<int32_t> ids, nTs;
     std::vector<int64_t> soff;
+    std::vector<double*> ptrs;
     int q = 0;
     while (q < np) {
         ids.clear();
         soff.clear();
+        nTs.clear();
+        ptrs.clear();
         int64_t used = 0;
         while (q < np && (ids.empty() || used + (int64_t)c->ops[q].mp * c->ops[q].mp <= cap)) {
             ids.push_back(q);
             soff.push_back(used);
+            nTs.push_back(c->ops[q].nT);
+            ptrs.push_back(scratch + used);
             used += (int64_t)c->ops[q].mp * c->ops[q].mp;
             ++q;
         }
-        CUDA_TRY(cudaMemcpyAsync(d_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, c->stream));
-        CUDA_TRY(cudaMemcpyAsync(d_soff, soff.data(), soff.size() * 8, cudaMemcpyHostToDevice, c->stream));
-        launch_extract_local(c->stream, (int)ids.size(), d_ids, c->d_ops, c->d_oidx, c->A, scratch, d_soff);
-        launch_gj_batched(c->stream, (int)ids.size(), d_ids, c->d_ops, scratch, d_soff, d_err);
-        launch_pack(c->stream, (int)ids.size(), d_ids, c->d_ops, c->d_items, scratch, d_soff, c->d_tiles);
+        const size_t nb = ids.size();
+        CUDA_TRY(cudaMemcpyAsync(d_ids, ids.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_soff, soff.data(), nb * 8, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_nT, nTs.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_ptr, ptrs.data(), nb * sizeof(double*), cudaMemcpyHostToDevice, c->stream));
+        launch_extract_local(c->stream, (int)nb, d_ids, c->d_ops, c->d_oidx, c->A, scratch, d_soff);
+        launch_gj_batched(c->stream, (int)nb, d_nT, d_nT, d_ptr, d_ids, d_err);
+        launch_pack(c->stream, (int)nb, d_ids, c->d_ops, c->d_items, scratch, d_soff, c->d_tiles);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(c->stream));
     }
@@ -672,6 +582,8 @@ static int invert_locals(ddg_ctx* c) {
     cudaFree(d_ids);
     cudaFree(d_soff);
     cudaFree(d_err);
+    cudaFree(d_nT);
+    cudaFree(d_ptr);
     if (herr[0] >= 0)
         return set_err(DDG_E_NOT_SPD,
                        "local inverse: subdomain %d (sweep position %d) not positive definite at pivot %d",
@@ -684,16 +596,17 @@ static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::
     const OpDesc& op = c->ops[c->coarse_op];
     const int64_t tot = (int64_t)op.mp * op.mp;
     double* M = nullptr;
-    int32_t *d_r = nullptr, *d_c = nullptr, *d_err = nullptr, *d_ids = nullptr;
+    int32_t *d_r = nullptr, *d_c = nullptr, *d_err = nullptr, *d_ids = nullptr, *d_nT = nullptr;
     double* d_v = nullptr;
     int64_t* d_soff = nullptr;
+    double** d_ptr = nullptr;
     int st;
     if ((st = dalloc(&M, tot)) || (st = dalloc(&d_r, er.size())) || (st = dalloc(&d_c, ec.size())) ||
         (st = dalloc(&d_v, ev.size())) || (st = dalloc(&d_err, 2)) || (st = dalloc(&d_ids, 1)) ||
-        (st = dalloc(&d_soff, 1)))
+        (st = dalloc(&d_soff, 1)) || (st = dalloc(&d_nT, 1)) || (st = dalloc(&d_ptr, 1)))
         return st;
     int32_t herr[2] = {-1, -1};
-    int32_t id = c->coarse_op;
+    int32_t id = c->coarse_op, nT = op.nT;
     int64_t zero = 0;
     CUDA_TRY(cudaMemsetAsync(M, 0, tot * sizeof(double), c->stream));
     CUDA_TRY(cudaMemcpy(d_r, er.data(), er.size() * 4, cudaMemcpyHostToDevice));
@@ -702,14 +615,17 @@ static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::
     CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d_ids, &id, 4, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d_soff, &zero, 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_nT, &nT, 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_ptr, &M, sizeof(double*), cudaMemcpyHostToDevice));
     launch_scatter_coarse(c->stream, (int64_t)ev.size(), d_r, d_c, d_v, op.nT, op.m, M);
-    if (op.nT <= 64) launch_gj_batched(c->stream, 1, d_ids, c->d_ops, M, d_soff, d_err);
-    else launch_gj_big(c->stream, op.nT, M, d_err);
+    if (op.nT <= 64) launch_gj_batched(c->stream, 1, d_nT, d_nT, d_ptr, d_ids, d_err);
+    else launch_gj_big(c->stream, op.nT, op.nT, M, id, d_err);
     launch_pack(c->stream, 1, d_ids, c->d_ops, c->d_items, M, d_soff, c->d_tiles);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemcpy(herr, d_err, sizeof herr, cudaMemcpyDeviceToHost));
-    cudaFree(M); cudaFree(d_r); cudaFree(d_c); cudaFree(d_v); cudaFree(d_err); cudaFree(d_ids); cudaFree(d_soff);
+    cudaFree(M); cudaFree(d_r); cudaFree(d_c); cudaFree(d_v); cudaFree(d_err); cudaFree(d_ids);
+    cudaFree(d_soff); cudaFree(d_nT); cudaFree(d_ptr);
     if (herr[0] >= 0)
         return set_err(DDG_E_NOT_SPD, "coarse inverse: A_c not positive definite at pivot %d", herr[1]);
     return DDG_OK;
@@ -816,13 +732,22 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     std::vector<double> ev;
     build_galerkin(c, row_ptr, col, val, er, ec, ev);
     tick("galerkin");
-    if (c->nc > 131072) {
+    c->coarse_variant = c->opts.coarse_variant;
+    if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
+    if (c->coarse_variant == 1 && c->nc > 131072) {
         int64_t nc = c->nc;
         free_ctx(c);
         return set_err(DDG_E_ARG, "n_c = %lld: the dense coarse inverse is limited to 131072 unknowns",
                        (long long)nc);
     }
+    if (c->opts.block_coords && c->opts.block_ndim > 0)
+        c->block_coords.assign(c->opts.block_coords, c->opts.block_coords + (int64_t)nparts * c->opts.block_ndim);
+    c->block_ndim = c->opts.block_ndim;
     build_plans(c);
+    if (c->coarse_variant == 2) {
+        if ((st = sparse_coarse_symbolic(c, row_ptr, col, er, ec, ev))) { free_ctx(c); return st; }
+        tick("coarse symbolic (nested dissection)");
+    }
     // uploads
     std::vector<int32_t> rp32(n + 1);
     for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
@@ -864,14 +789,18 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     tick("upload");
     if ((st = invert_locals(c))) { free_ctx(c); return st; }
     tick("local inverses (GPU)");
-    if ((st = invert_coarse(c, er, ec, ev))) { free_ctx(c); return st; }
+    if (c->coarse_variant == 1) {
+        if ((st = invert_coarse(c, er, ec, ev))) { free_ctx(c); return st; }
+    } else {
+        if ((st = sparse_coarse_numeric(c))) { free_ctx(c); return st; }
+    }
     tick("coarse inverse (GPU)");
     c->local_bytes = 0;
     for (int q = 0; q < nparts; ++q) {
         const OpDesc& op = c->ops[q];
         for (int t = 0; t < op.nitems; ++t) c->local_bytes += (int64_t)c->items[op.item_base + t].ntiles * TILE_ELEMS * 8;
     }
-    c->coarse_bytes = (c->tiles_doubles * 8) - c->local_bytes;
+    c->coarse_bytes = c->coarse_variant == 1 ? (c->tiles_doubles * 8) - c->local_bytes : sparse_coarse_bytes(c);
     c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = c;
     return DDG_OK;
@@ -899,6 +828,17 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
 }
 
 static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
+    if (c->coarse_variant == 2) {
+        prof(c, PC_COARSE, 0, [&] {
+            launch_coarse_restrict(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
+                                   c->A, r, z, sparse_coarse_rhs(c), c->maxmI, done);
+            c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
+            launch_prolong(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc,
+                           z, done);
+        });
+        c->launches += 2;
+        return;
+    }
     const OpDesc& op = c->ops[c->coarse_op];
     prof(c, PC_COARSE, 0, [&] {
         launch_coarse_restrict(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
@@ -1116,7 +1056,7 @@ extern "C" int ddg_get_info(ddg_ctx* c, ddg_info* info) {
     info->min_rank_ratio = c->min_ratio;
     info->local_factor_bytes = c->local_bytes;
     info->coarse_factor_bytes = c->coarse_bytes;
-    info->coarse_variant = 1;
+    info->coarse_variant = c->coarse_variant;
     return DDG_OK;
 }
 

@@ -31,7 +31,8 @@ EXPORTS = ["ddg_default_opts", "ddg_setup", "ddg_pcg_solve", "ddg_pcg_solve_devi
 class ddg_opts(C.Structure):
     _fields_ = [("overlap", C.c_int), ("rank_tol", C.c_double), ("stop_mode", C.c_int),
                 ("max_iter", C.c_int), ("device", C.c_int), ("stream", C.c_void_p),
-                ("use_graphs", C.c_int), ("verbose", C.c_int)]
+                ("use_graphs", C.c_int), ("verbose", C.c_int), ("coarse_variant", C.c_int),
+                ("block_ndim", C.c_int), ("block_coords", C.c_void_p)]
 
 
 class ddg_report(C.Structure):
@@ -122,7 +123,7 @@ class Solver:
 
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
                  stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
-                 verbose=False):
+                 verbose=False, coarse_variant=0, block_coords=None):
         L = load()
         o = default_opts()
         o.overlap, o.rank_tol, o.stop_mode, o.max_iter = overlap, rank_tol, stop_mode, max_iter
@@ -130,6 +131,12 @@ class Solver:
         o.stream = stream
         o.use_graphs = 1 if use_graphs else 0
         o.verbose = 1 if verbose else 0
+        o.coarse_variant = int(coarse_variant)
+        bc = None
+        if block_coords is not None:
+            bc = np.ascontiguousarray(block_coords, np.int32)
+            o.block_ndim = int(bc.shape[1])
+            o.block_coords = bc.ctypes.data
         rp = np.ascontiguousarray(row_ptr, np.int64)
         ci = np.ascontiguousarray(col, np.int32)
         va = np.ascontiguousarray(val, np.float64)
@@ -148,6 +155,7 @@ class Solver:
     @classmethod
     def from_problem(cls, pr, **kw):
         kw.setdefault("overlap", pr.overlap)
+        kw.setdefault("block_coords", pr.block_coords)
         return cls(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts, **kw)
 
     def close(self):

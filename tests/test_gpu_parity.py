@@ -167,3 +167,49 @@ def test_full_c2_properties():
     x, y = rs.standard_normal(pr.n), rs.standard_normal(pr.n)
     Mx, My = s.apply_precond(x), s.apply_precond(y)
     assert abs(x @ My - y @ Mx) <= 1e-11 * np.linalg.norm(x) * np.linalg.norm(My)
+
+
+# ---------------------------------------------------------------- sparse coarse solver
+SPARSE_CASES = {
+    "poisson2d_64_b4_p1": lambda: P.poisson2d(64, 4, 1, 21),      # 256 parts, 2D ND
+    "poisson3d_32_b4_p2": lambda: P.poisson3d(32, 4, 2, 22),      # 512 parts, k=10, 3D ND
+    "lognormal_32_b4": lambda: P.lognormal3d(32, 4, 1, 23),       # C3 shape, 512 parts
+    "biharm_128_b16_p3": lambda: P.biharmonic2d(128, 16, 3, 24),  # C5 shape, 9-point part graph
+    "elasticity_12_be4": lambda: P.elasticity3d(12, 4, 25),       # 27-point part graph
+}
+
+
+@pytest.mark.parametrize("geom", [True, False])
+@pytest.mark.parametrize("name", list(SPARSE_CASES))
+def test_sparse_coarse_parity(name, geom):
+    """coarse_variant=2 (nested dissection + block elimination) vs the oracle's
+    envelope Cholesky: coarse correction and the full PCG solve."""
+    pr = SPARSE_CASES[name]()
+    kw = dict(coarse_variant=2)
+    if not geom:
+        kw["block_coords"] = None
+    from paper_1504_00907_b200 import Solver
+    s = Solver(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts, overlap=pr.overlap,
+               block_coords=pr.block_coords if geom else None, coarse_variant=2)
+    assert s.info.coarse_variant == 2
+    o = oracle.Oracle.from_problem(pr)
+    r = np.random.default_rng(3).standard_normal(pr.n)
+    tol = 1e-9 if "biharm" in name else 1e-12
+    zc, zo = s.coarse_correct(r), o.coarse_correct(r)
+    assert np.linalg.norm(zc - zo) <= tol * np.linalg.norm(zo)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    uo, ito, histo, conv = o.pcg(pr.f, 1e-8)
+    assert rep.converged and abs(it - ito) <= 1
+    m = min(len(hist), len(histo))
+    assert np.max(np.abs(hist[:m] - histo[:m]) / histo[:m]) <= H_TOL
+    assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+
+
+def test_sparse_matches_dense_variant():
+    pr = P.poisson3d(24, 4, 1, 26)
+    from paper_1504_00907_b200 import Solver
+    sd = Solver.from_problem(pr, coarse_variant=1)
+    ss = Solver.from_problem(pr, coarse_variant=2)
+    r = np.random.default_rng(4).standard_normal(pr.n)
+    a, b = sd.coarse_correct(r), ss.coarse_correct(r)
+    assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(a)
