@@ -250,7 +250,7 @@ def bench_ddg(args):
         "config": {"workload": args.config, "desc": P.CONFIG_TEXT[args.config], "n": pr.n,
                    "iterations": it, "rtol": args.rtol, "n_c": int(s.info.n_c),
                    "nparts": int(s.info.nparts), "colours": int(s.info.ncolours),
-                   "coarse": "dense packed inverse", "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                   "coarse": "dense packed inverse" if s.info.coarse_variant == 1 else "sparse nested dissection", "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "l2": "inputs larger than L2 (local inverses %.1f GB)" % (s.info.local_factor_bytes / 1e9),
                    "time_to_rtol_ms": ms_step, "t_setup_s": round(t_setup, 2)},
         "roofline": {"bound": "hbm", "kernel": "k_symv (colour sweep, a4/a8)",

@@ -17,7 +17,9 @@
 // over the operator K_t = [[H_t, .], [-G_t, 0]] plus gather/reduce launches.
 // Bytes per solve: 2|G| + |H| (H packed lower) -- below the 2|L_c| of
 // Cholesky forward/back substitution.
+#include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -517,13 +519,12 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
 }
 
 template <typename T>
-static int up(T** d, const std::vector<T>& h) {
+static int up_s(cudaStream_t s, T** d, const std::vector<T>& h) {
     int st = dalloc(d, h.size());
     if (st) return st;
-    if (!h.empty() && cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
-        return set_err(DDG_E_CUDA, "sparse coarse upload failed");
-    return DDG_OK;
+    return h2d(s, *d, h.data(), h.size() * sizeof(T));
 }
+#define up(d, h) up_s(c->stream, d, h)
 
 // --------------------------------------------------------------------------
 // numeric phase (device)
@@ -545,7 +546,7 @@ int sparse_coarse_numeric(ddg_ctx* c) {
         (st = dalloc(&d_nT, nn)) || (st = dalloc(&d_nK, nn)) || (st = dalloc(&d_tasks, nn)))
         return st;
     int32_t herr[2] = {-1, -1};
-    CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
+    { int _s = h2d(c->stream, d_err, herr, sizeof herr); if (_s) return _s; }
     std::vector<double*> fptr(nn, nullptr);
     std::vector<double*> level_buf(sc->nlevels, nullptr);
     std::vector<int> max_parent_h(sc->nlevels, -1);
@@ -596,6 +597,32 @@ int sparse_coarse_numeric(ddg_ctx* c) {
             launch_front_extend_add(c->stream, (int)tasks.size(), d_tasks, sc->d_fr, d_fptr, sc->d_fmap, maxe);
             CUDA_TRY(cudaStreamSynchronize(c->stream));
         }
+        static const bool dbg = getenv("DDG_DEBUG_CHECK") != nullptr;
+        auto dump = [&](const char* tag) -> int {
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            for (int i = f0; i < f1; ++i) {
+                const FrontDesc& f = sc->fr[i];
+                const int64_t ne = (int64_t)f.nT * f.nT * TILE_ELEMS;
+                std::vector<double> h(ne);
+                { int _s = d2h(c->stream, h.data(), fptr[i], ne * 8); if (_s) return _s; }
+                const int N = f.nT * TILE;
+                auto at = [&](int R, int Cc) {
+                    return h[((int64_t)(Cc / TILE) * f.nT + R / TILE) * TILE_ELEMS + (Cc % TILE) * TILE + R % TILE];
+                };
+                double cs = 0, asym = 0, dmin = 1e300;
+                for (int R = 0; R < N; ++R)
+                    for (int Cc = 0; Cc < N; ++Cc) {
+                        cs += fabs(at(R, Cc)) * (1 + (R * 7 + Cc * 13) % 5);
+                        if (!(R < f.nSp && Cc < f.nSp) && !(R >= f.nSp && Cc >= f.nSp)) continue;
+                        asym = std::max(asym, fabs(at(R, Cc) - at(Cc, R)));
+                    }
+                for (int R = 0; R < f.nS; ++R) dmin = std::min(dmin, at(R, R));
+                fprintf(stderr, "[dbg] %s lvl %d front %d nS %d nB %d nT %d ch %d %d cs %.17g asym %.3g dmin %.3g\n",
+                        tag, h, i, f.nS, f.nB, f.nT, f.child0, f.child1, cs, asym, dmin);
+            }
+            return DDG_OK;
+        };
+        if (dbg && (st = dump("assembled"))) return st;
         // eliminate the S pivots: small fronts batched, big ones grid-wide
         std::vector<int32_t> ids, nTs, nKs;
         std::vector<double*> mats;
@@ -626,6 +653,7 @@ int sparse_coarse_numeric(ddg_ctx* c) {
                           d_fptr, c->d_items, sc->d_ctiles);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (dbg && (st = dump("factored"))) return st;
         // release levels whose fronts have all been absorbed by their parents
         for (int l = 0; l < h; ++l)
             if (level_buf[l] && max_parent_h[l] <= h) {
@@ -638,7 +666,7 @@ int sparse_coarse_numeric(ddg_ctx* c) {
     }
     for (auto* b : level_buf)
         if (b) cudaFree(b);
-    CUDA_TRY(cudaMemcpy(herr, d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    { int _s = d2h(c->stream, herr, d_err, sizeof herr); if (_s) return _s; }
     cudaFree(d_fptr); cudaFree(d_err); cudaFree(d_ids); cudaFree(d_nT); cudaFree(d_nK); cudaFree(d_tasks);
     if (herr[0] >= 0)
         return set_err(DDG_E_NOT_SPD, "coarse factor: front %d not positive definite at pivot %d", herr[0], herr[1]);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <string>
 #include <vector>
@@ -33,6 +34,11 @@ static int dalloc(T** p, size_t count) {
     if (e != cudaSuccess)
         return set_err(DDG_E_OOM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
                        cudaGetErrorString(e));
+    static const int fill = getenv("DDG_DEBUG_FILL") ? atoi(getenv("DDG_DEBUG_FILL")) : -1;
+    if (fill >= 0) {   // debug: 0 zeroes, 255 poisons (NaN)
+        cudaMemset(*p, fill, count * sizeof(T));
+        cudaDeviceSynchronize();
+    }
     return DDG_OK;
 }
 
@@ -134,3 +140,20 @@ static void prof(ddg_ctx* c, int cat, double bytes, Fn fn) {
     cudaEventRecord(c->evpool[e1], c->stream);
 }
 
+
+// Every host<->device transfer of the library is ordered on the context
+// stream (a legacy-stream cudaMemcpy/cudaMemset is NOT ordered with the
+// context's non-blocking stream, and a pageable H2D cudaMemcpy may return
+// before its DMA lands).
+static inline int h2d(cudaStream_t s, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return DDG_OK;
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return DDG_OK;
+}
+static inline int d2h(cudaStream_t s, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return DDG_OK;
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return DDG_OK;
+}

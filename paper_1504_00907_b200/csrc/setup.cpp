@@ -547,7 +547,7 @@ static int invert_locals(ddg_ctx* c) {
         return st;
     }
     int32_t herr[2] = {-1, -1};
-    CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
+    { int _s = h2d(c->stream, d_err, herr, sizeof herr); if (_s) return _s; }
     std::vector<int32_t> ids, nTs;
     std::vector<int64_t> soff;
     std::vector<double*> ptrs;
@@ -577,7 +577,7 @@ static int invert_locals(ddg_ctx* c) {
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(c->stream));
     }
-    CUDA_TRY(cudaMemcpy(herr, d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    { int _s = d2h(c->stream, herr, d_err, sizeof herr); if (_s) return _s; }
     cudaFree(scratch);
     cudaFree(d_ids);
     cudaFree(d_soff);
@@ -609,21 +609,21 @@ static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::
     int32_t id = c->coarse_op, nT = op.nT;
     int64_t zero = 0;
     CUDA_TRY(cudaMemsetAsync(M, 0, tot * sizeof(double), c->stream));
-    CUDA_TRY(cudaMemcpy(d_r, er.data(), er.size() * 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_c, ec.data(), ec.size() * 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_v, ev.data(), ev.size() * 8, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_err, herr, sizeof herr, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_ids, &id, 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_soff, &zero, 8, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_nT, &nT, 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_ptr, &M, sizeof(double*), cudaMemcpyHostToDevice));
+    { int _s = h2d(c->stream, d_r, er.data(), er.size() * 4); if (_s) return _s; }
+    { int _s = h2d(c->stream, d_c, ec.data(), ec.size() * 4); if (_s) return _s; }
+    { int _s = h2d(c->stream, d_v, ev.data(), ev.size() * 8); if (_s) return _s; }
+    { int _s = h2d(c->stream, d_err, herr, sizeof herr); if (_s) return _s; }
+    { int _s = h2d(c->stream, d_ids, &id, 4); if (_s) return _s; }
+    { int _s = h2d(c->stream, d_soff, &zero, 8); if (_s) return _s; }
+    { int _s = h2d(c->stream, d_nT, &nT, 4); if (_s) return _s; }
+    { int _s = h2d(c->stream, d_ptr, &M, sizeof(double*)); if (_s) return _s; }
     launch_scatter_coarse(c->stream, (int64_t)ev.size(), d_r, d_c, d_v, op.nT, op.m, M);
     if (op.nT <= 64) launch_gj_batched(c->stream, 1, d_nT, d_nT, d_ptr, d_ids, d_err);
     else launch_gj_big(c->stream, op.nT, op.nT, M, id, d_err);
     launch_pack(c->stream, 1, d_ids, c->d_ops, c->d_items, M, d_soff, c->d_tiles);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    CUDA_TRY(cudaMemcpy(herr, d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    { int _s = d2h(c->stream, herr, d_err, sizeof herr); if (_s) return _s; }
     cudaFree(M); cudaFree(d_r); cudaFree(d_c); cudaFree(d_v); cudaFree(d_err); cudaFree(d_ids);
     cudaFree(d_soff); cudaFree(d_nT); cudaFree(d_ptr);
     if (herr[0] >= 0)
@@ -632,12 +632,12 @@ static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::
 }
 
 template <typename T>
-static int upload(T** d, const std::vector<T>& h) {
+static int upload_s(cudaStream_t s, T** d, const std::vector<T>& h) {
     int st = dalloc(d, h.size());
     if (st) return st;
-    if (!h.empty()) CUDA_TRY(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
-    return DDG_OK;
+    return h2d(s, *d, h.data(), h.size() * sizeof(T));
 }
+#define upload(d, h) upload_s(c->stream, d, h)
 
 // ---------------------------------------------------------------------------
 // ddg_setup
@@ -755,10 +755,9 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         free_ctx(c);
         return st;
     }
-    if (cudaMemcpy(c->d_col, col, c->nnz * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(c->d_val, val, c->nnz * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if ((st = h2d(c->stream, c->d_col, col, c->nnz * 4)) || (st = h2d(c->stream, c->d_val, val, c->nnz * 8))) {
         free_ctx(c);
-        return set_err(DDG_E_CUDA, "upload of A failed");
+        return st;
     }
     c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val};
     if ((st = upload(&c->d_oidx, c->oidx)) || (st = upload(&c->d_ops, c->ops)) ||
@@ -775,10 +774,11 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         free_ctx(c);
         return st;
     }
-    if (cudaMemset(c->d_s, 0, c->s_doubles * 8) != cudaSuccess ||
-        cudaMemset(c->d_ticket, 0, sizeof(unsigned)) != cudaSuccess ||
-        cudaMemset(c->d_zero, 0, sizeof(int32_t)) != cudaSuccess ||
-        cudaMemset(c->d_sc, 0, sizeof(Scalars)) != cudaSuccess ||
+    if (cudaMemsetAsync(c->d_s, 0, c->s_doubles * 8, c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->d_ticket, 0, sizeof(unsigned), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->d_zero, 0, sizeof(int32_t), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->d_sc, 0, sizeof(Scalars), c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess ||
         cudaMallocHost(&c->h_sc, sizeof(Scalars)) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
         free_ctx(c);
@@ -972,7 +972,7 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     if (iters) *iters = it;
     if (res_hist && cap > 0) {
         int cnt = std::min(cap, it + 1);
-        CUDA_TRY(cudaMemcpy(res_hist, c->d_hist, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+        { int _s = d2h(c->stream, res_hist, c->d_hist, cnt * sizeof(double)); if (_s) return _s; }
     }
     if (rep) {
         rep->converged = s.converged;
@@ -984,7 +984,7 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         rep->frac_iters = (double)it;
         if (it >= 1 && s.converged && s.res > 0) {
             std::vector<double> h(it + 1);
-            if (cudaMemcpy(h.data(), c->d_hist, (it + 1) * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            if (d2h(c->stream, h.data(), c->d_hist, (it + 1) * sizeof(double)) == DDG_OK) {
                 double tol = s.rtol * s.ref;
                 double a = log10(h[it - 1]), b = log10(h[it]), lt = log10(tol);
                 if (a != b) rep->frac_iters = (it - 1) + (a - lt) / (a - b);
