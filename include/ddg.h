@@ -69,6 +69,7 @@ typedef struct {
     int coarse_variant;   /* 0 auto (dense if n_c <= 8192), 1 dense packed inverse of A_c,
                              2 sparse: nested dissection + supernodal block elimination         */
     int block_ndim;       /* 0, or the dimension of block_coords                                    */
+    int fuse_gather;      /* 1 (default): small subdomains compute R~_i(r - A z) inside the SYMV kernel */
     const int32_t* block_coords; /* optional nparts x block_ndim integer coordinates of the parts
                              (host, borrowed): geometric nested dissection of the coarse graph;
                              NULL: BFS level-set bisection                                       */

@@ -426,7 +426,7 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
         op.nT = f.nT;
         op.BT = FRONT_BT;
         op.nblk = (int)rb.size() - 1;
-        op.out_mode = 1;
+        op.out_mode = 2;
         op.idx_off = -1;
         op.s_off = f.fvec_off;
         op.part_off = 0;
@@ -689,7 +689,8 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         launch_front_fwd_assemble(c->stream, f0, nf, sc->d_fr, sc->d_fS, sc->d_fmap, sc->d_bc, sc->d_fvec,
                                   sc->d_w, done);
         launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->g_end[h] - sc->g_begin[h],
-                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t);
+                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
+                    c->d_tickets);
         launch_front_reduce(c->stream, sc->d_fwd, sc->fwd_b[h], sc->fwd_b[h + 1] - sc->fwd_b[h], sc->d_contrib,
                             sc->d_fr, sc->d_fS, c->d_partials, sc->d_w, d_x, done);
         launches += 1 + (sc->g_end[h] > sc->g_begin[h]) + (sc->fwd_b[h + 1] > sc->fwd_b[h]);
@@ -698,7 +699,8 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
         launch_front_bwd_gather(c->stream, f0, nf, sc->d_fr, sc->d_fB, d_x, sc->d_fvec, done);
         launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->h_end[h] - sc->g_begin[h],
-                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t);
+                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
+                    c->d_tickets);
         launch_front_reduce(c->stream, sc->d_bwd, sc->bwd_b[h], sc->bwd_b[h + 1] - sc->bwd_b[h], sc->d_contrib,
                             sc->d_fr, sc->d_fS, c->d_partials, sc->d_w, d_x, done);
         launches += 3;

@@ -92,6 +92,7 @@ struct ddg_ctx {
     double* d_redbuf = nullptr;
     unsigned* d_ticket = nullptr;
     int32_t* d_zero = nullptr;  // a device int that stays 0 (`done` for test hooks)
+    unsigned* d_tickets = nullptr;  // per-operator completion tickets of k_symv
     Scalars* h_sc = nullptr;    // pinned mirror
     cudaGraph_t g_iter = nullptr;
     cudaGraphExec_t ge_iter = nullptr;

@@ -26,7 +26,7 @@ struct OpDesc {
     int32_t nblk;     // item-block rows = ceil(nT / BT)
     int32_t item_base;
     int32_t nitems;   // nblk * (nblk + 1) / 2
-    int32_t out_mode; // 0: z[idx[r]] += y[r]; 1: y_out[r] = y[r] (identity, coarse)
+    int32_t out_mode; // 0: z[idx[r]] += y[r]; 1: y_out[r] = y[r] (identity, coarse); 2: front (external reduce)
     int64_t tile_off; // first double of its tiles
     int64_t idx_off;  // offset of its index list Omega~_i in d_oidx (out_mode 0)
     int64_t s_off;    // offset of its right-hand side (mp entries) in d_s
@@ -100,15 +100,17 @@ struct ColourPlan {
     int32_t red_begin, red_end;     // reduction tasks of multi-item ops
     int32_t max_rows;               // max m over the colour's subdomains
     int32_t max_rows_t;             // max rows touched by one SYMV item (smem sizing)
+    int32_t all_single;             // every operator of the colour is one item: gather fused into SYMV
 };
 
 // ---- kernel launchers (kernels.cu) ----------------------------------------
-void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, const int32_t* oidx,
-                   DevCSR A, const double* r, const double* z, double* s, bool z_is_zero,
-                   const int32_t* done);
+void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, int max_m, bool warp_rows,
+                   const int32_t* oidx, DevCSR A, const double* r, const double* z, double* s,
+                   bool z_is_zero, const int32_t* done);
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
-                 double* y_out, double* partials, const int32_t* done, int max_rows_t);
+                 double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
+                 int gather_mode = 0, DevCSR A = DevCSR{}, const double* r = nullptr);
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
                         const double* partials, double* z, double* y_out, const int32_t* done);

@@ -231,20 +231,39 @@ __global__ void k_spmv(DevCSR A, const double* __restrict__ x, double* __restric
 // Multiplicative Schwarz colour step
 // =============================================================================
 
-// s_i = R~_i (r - A z) for every subdomain i of one colour (pull form, reading R5)
-__global__ void k_gather(const OpDesc* __restrict__ ops, int sub_begin, const int32_t* __restrict__ oidx,
-                         DevCSR A, const double* __restrict__ r, const double* __restrict__ z,
-                         double* __restrict__ s, int z_is_zero, const int32_t* done) {
+// s_i = R~_i (r - A z) for every subdomain i of one colour (pull form, reading R5).
+// Block (q, chunk): rows [chunk*rows_per_cta, ...) of subdomain q; WARP_ROW
+// assigns one warp per row (long CSR rows, e.g. Q1 elasticity's 81).
+template <bool WARP_ROW>
+__global__ void __launch_bounds__(256)
+k_gather(const OpDesc* __restrict__ ops, int sub_begin, int chunks, const int32_t* __restrict__ oidx,
+         DevCSR A, const double* __restrict__ r, const double* __restrict__ z, double* __restrict__ s,
+         int z_is_zero, const int32_t* done) {
     if (*done) return;
-    const OpDesc op = ops[sub_begin + blockIdx.x];
+    const int q = sub_begin + blockIdx.x / chunks;
+    const int chunk = blockIdx.x % chunks;
+    const OpDesc op = ops[q];
     const int32_t* idx = oidx + op.idx_off;
     double* so = s + op.s_off;
-    for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
+    if (!WARP_ROW) {
+        const int a = chunk * blockDim.x + threadIdx.x;
+        if (a >= op.m) return;
         const int v = idx[a];
         double az = 0.0;
         if (!z_is_zero)
             for (int e = A.rp[v]; e < A.rp[v + 1]; e++) az += A.val[e] * z[A.col[e]];
         so[a] = r[v] - az;
+    } else {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int rows_per_cta = (blockDim.x >> 5) * 4;
+        for (int a = chunk * rows_per_cta + w; a < min(op.m, (chunk + 1) * rows_per_cta); a += blockDim.x >> 5) {
+            const int v = idx[a];
+            double az = 0.0;
+            if (!z_is_zero)
+                for (int e = A.rp[v] + lane; e < A.rp[v + 1]; e += 32) az += A.val[e] * z[A.col[e]];
+            az = warp_sum(az);
+            if (lane == 0) so[a] = r[v] - az;
+        }
     }
 }
 
@@ -284,7 +303,8 @@ __global__ void __launch_bounds__(SYMV_WARPS * 32)
 k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
        const double* __restrict__ tiles, const double* __restrict__ s,
        const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
-       double* __restrict__ partials, const int32_t* done) {
+       double* __restrict__ partials, const int32_t* done, unsigned* __restrict__ tickets,
+       int gather_mode, DevCSR A, const double* __restrict__ rvec) {
     if (*done) return;
     extern __shared__ double sm[];
     const ItemDesc it = items[item_begin + blockIdx.x];
@@ -295,10 +315,26 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
     const int rows_t = rows_r + rows_c;
     double* s_sm = sm;                          // [rows_t]: s over row block, then col block
     double* part = sm + rows_t;                 // [SYMV_WARPS][rows_t]
-    const double* sop = s + op.s_off;
-    for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
-        int g = x < rows_r ? it.I0 * TILE + x : it.J0 * TILE + (x - rows_r);
-        s_sm[x] = sop[g];
+    if (gather_mode) {
+        // fused residual restriction (single-item operators): s = R~_i (r - A z)
+        const int32_t* idx = oidx + op.idx_off;
+        for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
+            double v = 0.0;
+            if (x < op.m) {
+                const int node = idx[x];
+                double az = 0.0;
+                if (gather_mode == 1)
+                    for (int e = A.rp[node]; e < A.rp[node + 1]; e++) az += A.val[e] * z[A.col[e]];
+                v = rvec[node] - az;
+            }
+            s_sm[x] = v;
+        }
+    } else {
+        const double* sop = s + op.s_off;
+        for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
+            int g = x < rows_r ? it.I0 * TILE + x : it.J0 * TILE + (x - rows_r);
+            s_sm[x] = sop[g];
+        }
     }
     for (int x = threadIdx.x; x < SYMV_WARPS * rows_t; x += blockDim.x) part[x] = 0.0;
     __syncthreads();
@@ -345,6 +381,32 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
             partials[it.part_off + x] = y;
         }
     }
+    if (single || op.out_mode == 2) return;   // fronts: reduced by k_front_reduce
+    // multi-item operator: the last CTA to finish it sums every row's partial
+    // segments in fixed item order (deterministic) and applies the result
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(&tickets[it.op], 1u) == (unsigned)op.nitems - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int rb = op.BT * TILE;
+    for (int g = threadIdx.x; g < op.m; g += blockDim.x) {
+        const int b = g / rb, x = g % rb;
+        double y = 0.0;
+        for (int j = 0; j <= b; ++j) {
+            const ItemDesc& ij = items[op.item_base + b * (b + 1) / 2 + j];
+            y += __ldcg(partials + ij.part_off + x);
+        }
+        for (int i = b + 1; i < op.nblk; ++i) {
+            const ItemDesc& ii = items[op.item_base + i * (i + 1) / 2 + b];
+            y += __ldcg(partials + ii.part_off + (ii.I1 - ii.I0) * TILE + x);
+        }
+        if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+        else y_out[g] = y;
+    }
+    if (threadIdx.x == 0) tickets[it.op] = 0u;
 }
 
 // Sum the partial segments of multi-item operators for one row block, in
@@ -823,11 +885,16 @@ static inline int vec_grid(int64_t n) {
     return (int)(g < RED_BLOCKS ? (g > 0 ? g : 1) : RED_BLOCKS);
 }
 
-void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, const int32_t* oidx,
-                   DevCSR A, const double* r, const double* z, double* s, bool z_is_zero,
-                   const int32_t* done) {
+void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, int max_m, bool warp_rows,
+                   const int32_t* oidx, DevCSR A, const double* r, const double* z, double* s,
+                   bool z_is_zero, const int32_t* done) {
     if (nsub <= 0) return;
-    k_gather<<<nsub, 128, 0, st>>>(ops, sub_begin, oidx, A, r, z, s, z_is_zero ? 1 : 0, done);
+    const int rows_per_cta = warp_rows ? 32 : 256;
+    const int chunks = (max_m + rows_per_cta - 1) / rows_per_cta;
+    if (warp_rows)
+        k_gather<true><<<nsub * chunks, 256, 0, st>>>(ops, sub_begin, chunks, oidx, A, r, z, s, z_is_zero ? 1 : 0, done);
+    else
+        k_gather<false><<<nsub * chunks, 256, 0, st>>>(ops, sub_begin, chunks, oidx, A, r, z, s, z_is_zero ? 1 : 0, done);
 }
 
 static size_t symv_smem(int max_rows_t) {
@@ -836,12 +903,13 @@ static size_t symv_smem(int max_rows_t) {
 
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
-                 double* y_out, double* partials, const int32_t* done, int max_rows_t) {
+                 double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
+                 int gather_mode, DevCSR A, const double* r) {
     if (nitems <= 0) return;
     const size_t smem = symv_smem(max_rows_t > 0 ? max_rows_t : 2 * MAX_BT * TILE);
     cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_symv<<<nitems, SYMV_WARPS * 32, smem, st>>>(ops, items, item_begin, tiles, s, oidx, z, y_out,
-                                                  partials, done);
+                                                  partials, done, tickets, gather_mode, A, r);
 }
 
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,

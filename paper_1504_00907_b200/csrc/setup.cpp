@@ -72,6 +72,7 @@ extern "C" void ddg_default_opts(ddg_opts* o) {
     o->stream = nullptr;
     o->use_graphs = 1;
     o->verbose = 0;
+    o->fuse_gather = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -160,7 +161,7 @@ static void free_ctx(ddg_ctx* c) {
     void* ptrs[] = {c->d_rp, c->d_col, c->d_val, c->d_oidx, c->d_ops, c->d_items, c->d_red,
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
-                    c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero};
+                    c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -495,6 +496,9 @@ static int build_plans(ddg_ctx* c) {
         pl.sub_end = pos;
         pl.item_end = (int)c->items.size();
         pl.max_rows_t = 0;
+        pl.all_single = 1;
+        for (int q = pl.sub_begin; q < pl.sub_end; ++q)
+            if (c->ops[q].nitems != 1) pl.all_single = 0;
         for (int it = pl.item_begin; it < pl.item_end; ++it) {
             const ItemDesc& d = c->items[it];
             pl.max_rows_t = std::max(pl.max_rows_t, (d.I1 - d.I0 + (d.tri ? 0 : d.J1 - d.J0)) * TILE);
@@ -770,13 +774,14 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         (st = dalloc(&c->d_p, n)) || (st = dalloc(&c->d_q, n)) || (st = dalloc(&c->d_f, n)) ||
         (st = dalloc(&c->d_u, n)) || (st = dalloc(&c->d_x, n)) || (st = dalloc(&c->d_sc, 1)) ||
         (st = dalloc(&c->d_redbuf, RED_BLOCKS)) || (st = dalloc(&c->d_ticket, 1)) ||
-        (st = dalloc(&c->d_zero, 1))) {
+        (st = dalloc(&c->d_zero, 1)) || (st = dalloc(&c->d_tickets, c->ops.size()))) {
         free_ctx(c);
         return st;
     }
     if (cudaMemsetAsync(c->d_s, 0, c->s_doubles * 8, c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->d_ticket, 0, sizeof(unsigned), c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->d_zero, 0, sizeof(int32_t), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->d_tickets, 0, c->ops.size() * sizeof(unsigned), c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->d_sc, 0, sizeof(Scalars), c->stream) != cudaSuccess ||
         cudaStreamSynchronize(c->stream) != cudaSuccess ||
         cudaMallocHost(&c->h_sc, sizeof(Scalars)) != cudaSuccess ||
@@ -811,20 +816,22 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
 // ---------------------------------------------------------------------------
 static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
     const ColourPlan& pl = c->plans[cc];
-    prof(c, PC_GATHER, 0, [&] {
-        launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, c->d_oidx, c->A, r, z,
-                      c->d_s, z_zero, done);
-    });
+    int gmode = 0;
+    if (pl.all_single && c->opts.fuse_gather != 0) {
+        gmode = z_zero ? 2 : 1;
+    } else {
+        prof(c, PC_GATHER, 0, [&] {
+            launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, pl.max_rows,
+                          c->nnz > 24 * c->n, c->d_oidx, c->A, r, z, c->d_s, z_zero, done);
+        });
+        c->launches += 1;
+    }
     prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
         launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
-                    c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done, pl.max_rows_t);
+                    c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done, pl.max_rows_t, c->d_tickets,
+                    gmode, c->A, r);
     });
-    if (pl.red_end > pl.red_begin)
-        prof(c, PC_REDUCE, 0, [&] {
-            launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, pl.red_begin,
-                               pl.red_end - pl.red_begin, c->d_oidx, c->d_partials, z, nullptr, done);
-        });
-    c->launches += 2 + (pl.red_end > pl.red_begin);
+    c->launches += 1;
 }
 
 static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
@@ -845,14 +852,11 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
                                c->A, r, z, c->d_s + op.s_off, c->maxmI, done);
         launch_symv(c->stream, c->d_ops, c->d_items, c->coarse_item_begin,
                     c->coarse_item_end - c->coarse_item_begin, c->d_tiles, c->d_s, c->d_oidx, nullptr,
-                    c->d_yc, c->d_partials, done, c->coarse_rows_t);
-        launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, c->coarse_red_begin,
-                           c->coarse_red_end - c->coarse_red_begin, c->d_oidx, c->d_partials, nullptr,
-                           c->d_yc, done);
+                    c->d_yc, c->d_partials, done, c->coarse_rows_t, c->d_tickets);
         launch_prolong(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc,
                        z, done);
     });
-    c->launches += 3 + (c->coarse_red_end > c->coarse_red_begin);
+    c->launches += 3;
 }
 
 // z = M r: zero guess, forward sweep, coarse, reverse sweep
