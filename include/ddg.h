@@ -69,7 +69,11 @@ typedef struct {
     int coarse_variant;   /* 0 auto (dense if n_c <= 8192), 1 dense packed inverse of A_c,
                              2 sparse: nested dissection + supernodal block elimination         */
     int block_ndim;       /* 0, or the dimension of block_coords                                    */
-    int fuse_gather;      /* 1 (default): small subdomains compute R~_i(r - A z) inside the SYMV kernel */
+    int fuse_gather;      /* R~_i(r - A z) computed inside the SYMV kernel for single-item subdomains:
+                             0 never, 1 (default) when the items are large (>= 32 tiles) or the
+                             colour is small, 2 always                                               */
+    int small_kernel;     /* 1 (default): colours of many (>= 16 per SM) single-item subdomains with
+                             |Omega~_i| <= 256 use the warp-per-subdomain SYMV                    */
     const int32_t* block_coords; /* optional nparts x block_ndim integer coordinates of the parts
                              (host, borrowed): geometric nested dissection of the coarse graph;
                              NULL: BFS level-set bisection                                       */

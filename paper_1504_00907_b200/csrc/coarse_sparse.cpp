@@ -455,7 +455,7 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
         const int h = it.I1 - it.I0, wd = it.J1 - it.J0;
         it.ntiles = it.tri ? h * (h + 1) / 2 : h * wd;
         it.tile_off = sc->ctile_doubles;
-        sc->ctile_doubles += (int64_t)it.ntiles * TILE_ELEMS;
+        sc->ctile_doubles += item_doubles(it.tri, h, it.ntiles);
         it.part_off = c->part_doubles;
         c->part_doubles += (int64_t)(h + (it.tri ? 0 : wd)) * TILE;
         sc->max_rows_t = std::max(sc->max_rows_t, (h + (it.tri ? 0 : wd)) * TILE);

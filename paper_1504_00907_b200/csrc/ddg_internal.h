@@ -11,6 +11,12 @@ namespace ddg {
 
 constexpr int TILE = 32;                 // rows/cols per tile = warp width
 constexpr int TILE_ELEMS = TILE * TILE;  // 1024 doubles = 8 KB per tile
+constexpr int DIAG_ELEMS = TILE * (TILE + 1) / 2;  // 528: packed diagonal tile (4224 B)
+
+// doubles of an item's tiles: diagonal tiles of a triangle item are packed
+inline int64_t item_doubles(int tri, int h, int ntiles) {
+    return tri ? (int64_t)(ntiles - h) * TILE_ELEMS + (int64_t)h * DIAG_ELEMS : (int64_t)ntiles * TILE_ELEMS;
+}
 constexpr int SYMV_WARPS = 8;            // consumer warps per SYMV CTA
 constexpr int MAX_BT = 16;               // max tiles per item side (smem partial sizing)
 
@@ -100,7 +106,8 @@ struct ColourPlan {
     int32_t red_begin, red_end;     // reduction tasks of multi-item ops
     int32_t max_rows;               // max m over the colour's subdomains
     int32_t max_rows_t;             // max rows touched by one SYMV item (smem sizing)
-    int32_t all_single;             // every operator of the colour is one item: gather fused into SYMV
+    int32_t all_single;             // every operator of the colour is one item (gather may be fused)
+    int32_t max_ntiles;             // largest item of the colour (tiles)
 };
 
 // ---- kernel launchers (kernels.cu) ----------------------------------------
@@ -110,7 +117,7 @@ void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, 
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
                  double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
-                 int gather_mode = 0, DevCSR A = DevCSR{}, const double* r = nullptr);
+                 int gather_mode = 0, DevCSR A = DevCSR{}, const double* r = nullptr, bool small_ok = false);
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
                         const double* partials, double* z, double* y_out, const int32_t* done);

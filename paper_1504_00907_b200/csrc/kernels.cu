@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "ddg_internal.h"
@@ -281,6 +283,29 @@ __device__ __forceinline__ void item_tile(const ItemDesc& it, int l, int& I, int
     }
 }
 
+// Diagonal tiles are stored as their lower triangle, column-major packed,
+// with the diagonal halved: D = L' + L'^T, so a diagonal tile is applied
+// exactly like an off-diagonal one (direct + transposed) from half the bytes.
+__device__ __forceinline__ int diag_col_off(int j) { return j * TILE - j * (j - 1) / 2; }
+
+// offset (doubles) of local tile l = (I, J) inside its item
+__device__ __forceinline__ int64_t item_tile_off(const ItemDesc& it, int l, int I) {
+    if (!it.tri) return (int64_t)l * TILE_ELEMS;
+    const int rr = I - it.I0;                  // diagonal tiles of rows 0..rr-1 precede l
+    return (int64_t)(l - rr) * TILE_ELEMS + (int64_t)rr * DIAG_ELEMS;
+}
+
+// lane i loads row i of tile (I, J) (packed form when I == J)
+__device__ __forceinline__ void load_tile_row(double* a, const double* T, bool diag, int lane) {
+    if (!diag) {
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) a[j] = __ldcs(T + j * TILE + lane);
+    } else {
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? __ldcs(T + diag_col_off(j) + lane - j) : 0.0;
+    }
+}
+
 // butterfly reduce-scatter of 32 per-lane values: afterwards v[0] of lane l
 // holds sum over lanes of the original v[l].
 template <int OFF>
@@ -315,6 +340,14 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
     const int rows_t = rows_r + rows_c;
     double* s_sm = sm;                          // [rows_t]: s over row block, then col block
     double* part = sm + rows_t;                 // [SYMV_WARPS][rows_t]
+    const double* tbase = tiles + it.tile_off;
+    // issue this warp's first tile loads now: their latency overlaps the prologue
+    double a[TILE];
+    if (w < it.ntiles) {
+        int I0_, J0_;
+        item_tile(it, w, I0_, J0_);
+        load_tile_row(a, tbase + item_tile_off(it, w, I0_), I0_ == J0_, lane);
+    }
     if (gather_mode) {
         // fused residual restriction (single-item operators): s = R~_i (r - A z)
         const int32_t* idx = oidx + op.idx_off;
@@ -339,30 +372,28 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
     for (int x = threadIdx.x; x < SYMV_WARPS * rows_t; x += blockDim.x) part[x] = 0.0;
     __syncthreads();
     double* pw = part + w * rows_t;
-    const double* tbase = tiles + it.tile_off;
     for (int l = w; l < it.ntiles; l += SYMV_WARPS) {
         int I, J;
         item_tile(it, l, I, J);
-        const double* T = tbase + (int64_t)l * TILE_ELEMS;
-        double a[TILE];
-#pragma unroll
-        for (int j = 0; j < TILE; ++j) a[j] = __ldcs(T + j * TILE + lane);
+        if (l != w) load_tile_row(a, tbase + item_tile_off(it, l, I), I == J, lane);
         const int ri = (I - it.I0) * TILE;                           // row offset in s_sm / pw
         const int cj = it.tri ? (J - it.I0) * TILE : rows_r + (J - it.J0) * TILE;
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < TILE; ++j) acc += a[j] * s_sm[cj + j];
-        pw[ri + lane] += acc;
-        if (I != J) {
-            const double si = s_sm[ri + lane];
+        const double si = s_sm[ri + lane];
 #pragma unroll
-            for (int j = 0; j < TILE; ++j) a[j] *= si;
-            rs_stage<16>(a, lane);
-            rs_stage<8>(a, lane);
-            rs_stage<4>(a, lane);
-            rs_stage<2>(a, lane);
-            rs_stage<1>(a, lane);
+        for (int j = 0; j < TILE; ++j) a[j] *= si;
+        rs_stage<16>(a, lane);
+        rs_stage<8>(a, lane);
+        rs_stage<4>(a, lane);
+        rs_stage<2>(a, lane);
+        rs_stage<1>(a, lane);
+        if (I != J) {
+            pw[ri + lane] += acc;
             pw[cj + lane] += a[0];
+        } else {
+            pw[ri + lane] += acc + a[0];
         }
     }
     __syncthreads();
@@ -407,6 +438,286 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
         else y_out[g] = y;
     }
     if (threadIdx.x == 0) tickets[it.op] = 0u;
+}
+
+// ---- warp-per-subdomain SYMV for small single-item operators (nT <= 8) ----
+// Each warp owns one subdomain end to end: fused residual restriction, all
+// tiles (two in flight: register double buffer), its own shared y, scatter.
+// No CTA barrier anywhere, so warps of a CTA stream independently.
+constexpr int SMALL_MAXROWS = 256;
+
+__device__ __forceinline__ void tile_apply(const double* __restrict__ a_in, double* a, const double* s,
+                                           double* y, int ri, int cj, bool diag, int lane) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) acc += a_in[j] * s[cj + j];
+    const double si = s[ri + lane];
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) a[j] = a_in[j] * si;
+    rs_stage<16>(a, lane);
+    rs_stage<8>(a, lane);
+    rs_stage<4>(a, lane);
+    rs_stage<2>(a, lane);
+    rs_stage<1>(a, lane);
+    if (!diag) {
+        y[ri + lane] += acc;
+        __syncwarp();
+        y[cj + lane] += a[0];
+    } else {
+        y[ri + lane] += acc + a[0];
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(256)
+k_symv_small(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin, int nitems,
+             const double* __restrict__ tiles, const double* __restrict__ s, const int32_t* __restrict__ oidx,
+             double* __restrict__ z, double* __restrict__ y_out, const int32_t* done, int gather_mode, DevCSR A,
+             const double* __restrict__ rvec) {
+    if (*done) return;
+    __shared__ double ssm[8][SMALL_MAXROWS];
+    __shared__ double ysm[8][SMALL_MAXROWS];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ii = blockIdx.x * 8 + w;
+    if (ii >= nitems) return;
+    const ItemDesc it = items[item_begin + ii];
+    const OpDesc op = ops[it.op];
+    const double* tb = tiles + it.tile_off;
+    double a[TILE], b[TILE];
+    int I = 0, J = 0;
+    item_tile(it, 0, I, J);
+    load_tile_row(a, tb + item_tile_off(it, 0, I), I == J, lane);       // first tile in flight
+    double* sw = ssm[w];
+    double* yw = ysm[w];
+    const int32_t* idx = oidx + op.idx_off;
+    for (int x = lane; x < op.mp; x += 32) {
+        double v = 0.0;
+        if (x < op.m) {
+            if (gather_mode) {
+                const int node = idx[x];
+                double az = 0.0;
+                if (gather_mode == 1)
+                    for (int e = A.rp[node]; e < A.rp[node + 1]; e++) az += A.val[e] * z[A.col[e]];
+                v = rvec[node] - az;
+            } else {
+                v = s[op.s_off + x];
+            }
+        }
+        sw[x] = v;
+        yw[x] = 0.0;
+    }
+    __syncwarp();
+    for (int l = 0; l < it.ntiles; l += 2) {
+        int I1 = 0, J1 = 0;
+        const bool has1 = l + 1 < it.ntiles;
+        if (has1) {
+            item_tile(it, l + 1, I1, J1);
+            load_tile_row(b, tb + item_tile_off(it, l + 1, I1), I1 == J1, lane);
+        }
+        tile_apply(a, a, sw, yw, I * TILE, J * TILE, I == J, lane);
+        if (l + 2 < it.ntiles) {
+            item_tile(it, l + 2, I, J);
+            load_tile_row(a, tb + item_tile_off(it, l + 2, I), I == J, lane);
+        }
+        if (has1) tile_apply(b, b, sw, yw, I1 * TILE, J1 * TILE, I1 == J1, lane);
+    }
+    for (int x = lane; x < op.m; x += 32) {
+        if (op.out_mode == 0) z[idx[x]] += yw[x];
+        else y_out[x] = yw[x];
+    }
+}
+
+// ---- persistent warp-specialised SYMV: TMA bulk copies into an smem ring ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// Same arithmetic as k_symv.  Warps 0..7 consume, warp 8 (one lane) produces.
+// Each CTA walks items blockIdx.x, +gridDim.x, ...; tile k of the CTA's
+// stream lands in ring slot k % nst and is consumed by warp k % 8.
+__global__ void __launch_bounds__(288, 1)
+k_symv_tma(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin, int nitems,
+           const double* __restrict__ tiles, const double* __restrict__ s, const int32_t* __restrict__ oidx,
+           double* __restrict__ z, double* __restrict__ y_out, double* __restrict__ partials,
+           const int32_t* done, unsigned* __restrict__ tickets, int gather_mode, DevCSR A,
+           const double* __restrict__ rvec, int nst, int max_rows_t) {
+    if (*done) return;
+    extern __shared__ __align__(128) double tsm[];
+    double* ring = tsm;                                        // nst * 1024 doubles
+    double* s_sm = ring + (size_t)nst * TILE_ELEMS;            // max_rows_t
+    double* part = s_sm + max_rows_t;                          // 8 * max_rows_t
+    uint64_t* full = reinterpret_cast<uint64_t*>(part + SYMV_WARPS * max_rows_t);
+    uint64_t* empty = full + nst;
+    __shared__ bool last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == SYMV_WARPS) {                                  // ---- producer ----
+        if (lane != 0) return;
+        unsigned k = 0;
+        for (int ii = blockIdx.x; ii < nitems; ii += gridDim.x) {
+            const ItemDesc it = items[item_begin + ii];
+            const double* src = tiles + it.tile_off;
+            for (int l = 0; l < it.ntiles; ++l, ++k) {
+                const unsigned slot = k % nst, n = k / nst;
+                int I, J;
+                item_tile(it, l, I, J);
+                const unsigned bytes = (I == J && it.tri ? DIAG_ELEMS : TILE_ELEMS) * sizeof(double);
+                if (n > 0) mbar_wait(&empty[slot], (n - 1) & 1);
+                mbar_expect_tx(&full[slot], bytes);
+                bulk_g2s(ring + (size_t)slot * TILE_ELEMS, src + item_tile_off(it, l, I), bytes, &full[slot]);
+            }
+        }
+        return;
+    }
+    // ---- consumers (256 threads) ----
+    const int tid = threadIdx.x;
+    unsigned kbase = 0;
+    for (int ii = blockIdx.x; ii < nitems; ii += gridDim.x) {
+        const ItemDesc it = items[item_begin + ii];
+        const OpDesc op = ops[it.op];
+        const int rows_r = (it.I1 - it.I0) * TILE;
+        const int rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+        const int rows_t = rows_r + rows_c;
+        const bool single = it.part_off < 0;
+        consumer_sync();                                       // previous item's epilogue done
+        if (gather_mode) {
+            const int32_t* idx = oidx + op.idx_off;
+            for (int x = tid; x < rows_t; x += 256) {
+                double v = 0.0;
+                if (x < op.m) {
+                    const int node = idx[x];
+                    double az = 0.0;
+                    if (gather_mode == 1)
+                        for (int e = A.rp[node]; e < A.rp[node + 1]; e++) az += A.val[e] * z[A.col[e]];
+                    v = rvec[node] - az;
+                }
+                s_sm[x] = v;
+            }
+        } else {
+            const double* sop = s + op.s_off;
+            for (int x = tid; x < rows_t; x += 256) {
+                int g = x < rows_r ? it.I0 * TILE + x : it.J0 * TILE + (x - rows_r);
+                s_sm[x] = sop[g];
+            }
+        }
+        for (int x = tid; x < SYMV_WARPS * rows_t; x += 256) part[x] = 0.0;
+        consumer_sync();
+        double* pw = part + warp * rows_t;
+        // this warp's tiles: local l with (kbase + l) % 8 == warp
+        int l = (int)((warp - (int)(kbase % SYMV_WARPS) + SYMV_WARPS) % SYMV_WARPS);
+        for (; l < it.ntiles; l += SYMV_WARPS) {
+            const unsigned k = kbase + l, slot = k % nst;
+            mbar_wait(&full[slot], (k / nst) & 1);
+            const double* T = ring + (size_t)slot * TILE_ELEMS;
+            int I, J;
+            item_tile(it, l, I, J);
+            double a[TILE];
+            if (I != J) {
+#pragma unroll
+                for (int j = 0; j < TILE; ++j) a[j] = T[j * TILE + lane];
+            } else {
+#pragma unroll
+                for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? T[diag_col_off(j) + lane - j] : 0.0;
+            }
+            const int ri = (I - it.I0) * TILE;
+            const int cj = it.tri ? (J - it.I0) * TILE : rows_r + (J - it.J0) * TILE;
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < TILE; ++j) acc += a[j] * s_sm[cj + j];
+            // every a[j] has been consumed, so the slot's loads are complete
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);          // slot may be refilled
+            const double si = s_sm[ri + lane];
+#pragma unroll
+            for (int j = 0; j < TILE; ++j) a[j] *= si;
+            rs_stage<16>(a, lane);
+            rs_stage<8>(a, lane);
+            rs_stage<4>(a, lane);
+            rs_stage<2>(a, lane);
+            rs_stage<1>(a, lane);
+            if (I != J) {
+                pw[ri + lane] += acc;
+                pw[cj + lane] += a[0];
+            } else {
+                pw[ri + lane] += acc + a[0];
+            }
+        }
+        kbase += it.ntiles;
+        consumer_sync();
+        for (int x = tid; x < rows_t; x += 256) {
+            double y = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < SYMV_WARPS; ++ww) y += part[ww * rows_t + x];
+            if (single) {
+                const int g = it.I0 * TILE + x;
+                if (g < op.m) {
+                    if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+                    else y_out[g] = y;
+                }
+            } else {
+                partials[it.part_off + x] = y;
+            }
+        }
+        if (single || op.out_mode == 2) continue;
+        __threadfence();
+        consumer_sync();
+        if (tid == 0) last = (atomicAdd(&tickets[it.op], 1u) == (unsigned)op.nitems - 1);
+        consumer_sync();
+        if (!last) continue;
+        __threadfence();
+        const int rb = op.BT * TILE;
+        for (int g = tid; g < op.m; g += 256) {
+            const int b = g / rb, x = g % rb;
+            double y = 0.0;
+            for (int j = 0; j <= b; ++j) {
+                const ItemDesc& ij = items[op.item_base + b * (b + 1) / 2 + j];
+                y += __ldcg(partials + ij.part_off + x);
+            }
+            for (int i = b + 1; i < op.nblk; ++i) {
+                const ItemDesc& ii2 = items[op.item_base + i * (i + 1) / 2 + b];
+                y += __ldcg(partials + ii2.part_off + (ii2.I1 - ii2.I0) * TILE + x);
+            }
+            if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+            else y_out[g] = y;
+        }
+        if (tid == 0) tickets[it.op] = 0u;
+    }
 }
 
 // Sum the partial segments of multi-item operators for one row block, in
@@ -730,13 +1041,17 @@ __global__ void k_pack(const int32_t* __restrict__ op_ids, const OpDesc* __restr
             int I, J;
             item_tile(it, l, I, J);
             const double* src = M + ((int64_t)J * op.nT + I) * TILE_ELEMS;
-            double* dst = tiles + it.tile_off + (int64_t)l * TILE_ELEMS;
+            double* dst = tiles + it.tile_off + item_tile_off(it, l, I);
             for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
                 const int i = e % TILE, j = e / TILE;
                 double v = src[e];
-                if (I == J) v = 0.5 * (v + src[i * TILE + j]);
                 if (I * TILE + i >= op.m || J * TILE + j >= op.m) v = 0.0;
-                dst[e] = v;
+                if (I != J) {
+                    dst[e] = v;
+                } else if (i >= j) {           // packed lower, diagonal halved, symmetrised
+                    double vt = (I * TILE + i >= op.m || J * TILE + j >= op.m) ? 0.0 : src[i * TILE + j];
+                    dst[diag_col_off(j) + i - j] = i == j ? 0.5 * v : 0.5 * (v + vt);
+                }
             }
         }
     }
@@ -789,19 +1104,24 @@ __global__ void k_front_pack(int i0, int i1, int item_base, const int32_t* __res
             int I, J;
             item_tile(it, l, I, J);
             const double* src = M + ((int64_t)J * fr.nT + I) * TILE_ELEMS;
-            double* dst = ctiles + it.tile_off + (int64_t)l * TILE_ELEMS;
+            double* dst = ctiles + it.tile_off + item_tile_off(it, l, I);
             for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
                 const int i = e % TILE, j = e / TILE;
                 const int R = I * TILE + i, C = J * TILE + j;
                 double v = src[e];
                 if (I < fr.nK) {                    // H = A_SS^{-1}
-                    if (I == J) v = 0.5 * (v + src[i * TILE + j]);
                     if (R >= fr.nS || C >= fr.nS) v = 0.0;
+                    if (I != J) {
+                        dst[e] = v;
+                    } else if (i >= j) {            // packed lower, diagonal halved, symmetrised
+                        const double vt = (R >= fr.nS || C >= fr.nS) ? 0.0 : src[i * TILE + j];
+                        dst[diag_col_off(j) + i - j] = i == j ? 0.5 * v : 0.5 * (v + vt);
+                    }
                 } else {                             // -G = -A_BS A_SS^{-1}
                     v = -v;
                     if (R - fr.nSp >= fr.nB || C >= fr.nS) v = 0.0;
+                    dst[e] = v;
                 }
-                dst[e] = v;
             }
         }
     }
@@ -904,9 +1224,32 @@ static size_t symv_smem(int max_rows_t) {
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
                  double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
-                 int gather_mode, DevCSR A, const double* r) {
+                 int gather_mode, DevCSR A, const double* r, bool small_ok) {
     if (nitems <= 0) return;
-    const size_t smem = symv_smem(max_rows_t > 0 ? max_rows_t : 2 * MAX_BT * TILE);
+    if (max_rows_t <= 0) max_rows_t = 2 * MAX_BT * TILE;
+    if (small_ok && max_rows_t <= SMALL_MAXROWS) {
+        k_symv_small<<<(nitems + 7) / 8, 256, 0, st>>>(ops, items, item_begin, nitems, tiles, s, oidx, z, y_out,
+                                                      done, gather_mode, A, r);
+        return;
+    }
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("DDG_SYMV");
+        mode = (e && e[0] == 't') ? 1 : 0;   // "tma" selects the persistent TMA-ring kernel
+    }
+    if (mode == 1) {
+        const size_t fixed = (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
+        const size_t budget = 227 * 1024 - 1024;
+        int nst = (int)((budget - fixed) / (TILE_ELEMS * sizeof(double) + 16));
+        nst = std::max(2, std::min(nst, 24));
+        const size_t smem = (size_t)nst * TILE_ELEMS * sizeof(double) + fixed + 2 * nst * sizeof(uint64_t);
+        cudaFuncSetAttribute(k_symv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int grid = std::min(nitems, num_sms());
+        k_symv_tma<<<grid, 288, smem, st>>>(ops, items, item_begin, nitems, tiles, s, oidx, z, y_out, partials,
+                                           done, tickets, gather_mode, A, r, nst, max_rows_t);
+        return;
+    }
+    const size_t smem = symv_smem(max_rows_t);
     cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_symv<<<nitems, SYMV_WARPS * 32, smem, st>>>(ops, items, item_begin, tiles, s, oidx, z, y_out,
                                                   partials, done, tickets, gather_mode, A, r);

@@ -13,6 +13,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -73,6 +74,7 @@ extern "C" void ddg_default_opts(ddg_opts* o) {
     o->use_graphs = 1;
     o->verbose = 0;
     o->fuse_gather = 1;
+    o->small_kernel = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -453,7 +455,7 @@ static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool al
             const int h = it.I1 - it.I0, wd = it.J1 - it.J0;
             it.ntiles = it.tri ? h * (h + 1) / 2 : h * wd;
             it.tile_off = c->tiles_doubles;
-            c->tiles_doubles += (int64_t)it.ntiles * TILE_ELEMS;
+            c->tiles_doubles += item_doubles(it.tri, h, it.ntiles);
             if (op.nitems > 1) {
                 it.part_off = c->part_doubles;
                 c->part_doubles += (int64_t)(h + (it.tri ? 0 : wd)) * TILE;
@@ -497,11 +499,13 @@ static int build_plans(ddg_ctx* c) {
         pl.item_end = (int)c->items.size();
         pl.max_rows_t = 0;
         pl.all_single = 1;
+        pl.max_ntiles = 0;
         for (int q = pl.sub_begin; q < pl.sub_end; ++q)
             if (c->ops[q].nitems != 1) pl.all_single = 0;
         for (int it = pl.item_begin; it < pl.item_end; ++it) {
             const ItemDesc& d = c->items[it];
             pl.max_rows_t = std::max(pl.max_rows_t, (d.I1 - d.I0 + (d.tri ? 0 : d.J1 - d.J0)) * TILE);
+            pl.max_ntiles = std::max(pl.max_ntiles, d.ntiles);
         }
         pl.red_end = (int)c->red.size();
     }
@@ -736,6 +740,9 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     std::vector<double> ev;
     build_galerkin(c, row_ptr, col, val, er, ec, ev);
     tick("galerkin");
+    // environment overrides for experiments (documented in DESIGN.md)
+    if (const char* e = getenv("DDG_FUSE_GATHER")) c->opts.fuse_gather = atoi(e);
+    if (const char* e = getenv("DDG_SMALL_KERNEL")) c->opts.small_kernel = atoi(e);
     c->coarse_variant = c->opts.coarse_variant;
     if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
     if (c->coarse_variant == 1 && c->nc > 131072) {
@@ -803,7 +810,10 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     c->local_bytes = 0;
     for (int q = 0; q < nparts; ++q) {
         const OpDesc& op = c->ops[q];
-        for (int t = 0; t < op.nitems; ++t) c->local_bytes += (int64_t)c->items[op.item_base + t].ntiles * TILE_ELEMS * 8;
+        for (int t = 0; t < op.nitems; ++t) {
+            const ItemDesc& d = c->items[op.item_base + t];
+            c->local_bytes += item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8;
+        }
     }
     c->coarse_bytes = c->coarse_variant == 1 ? (c->tiles_doubles * 8) - c->local_bytes : sparse_coarse_bytes(c);
     c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -817,7 +827,10 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
 static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
     const ColourPlan& pl = c->plans[cc];
     int gmode = 0;
-    if (pl.all_single && c->opts.fuse_gather != 0) {
+    const bool fuse = pl.all_single && (c->opts.fuse_gather == 2 ||
+                                        (c->opts.fuse_gather == 1 &&
+                                         (pl.max_ntiles >= 32 || pl.sub_end - pl.sub_begin <= 2 * num_sms())));
+    if (fuse) {
         gmode = z_zero ? 2 : 1;
     } else {
         prof(c, PC_GATHER, 0, [&] {
@@ -829,7 +842,9 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
     prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
         launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
                     c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done, pl.max_rows_t, c->d_tickets,
-                    gmode, c->A, r);
+                    gmode, c->A, r,
+                    pl.all_single && c->opts.small_kernel != 0 && !fuse &&
+                        pl.sub_end - pl.sub_begin >= 16 * num_sms());
     });
     c->launches += 1;
 }

@@ -32,7 +32,8 @@ class ddg_opts(C.Structure):
     _fields_ = [("overlap", C.c_int), ("rank_tol", C.c_double), ("stop_mode", C.c_int),
                 ("max_iter", C.c_int), ("device", C.c_int), ("stream", C.c_void_p),
                 ("use_graphs", C.c_int), ("verbose", C.c_int), ("coarse_variant", C.c_int),
-                ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("block_coords", C.c_void_p)]
+                ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("small_kernel", C.c_int),
+                ("block_coords", C.c_void_p)]
 
 
 class ddg_report(C.Structure):
