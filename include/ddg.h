@@ -72,6 +72,7 @@ typedef struct {
     int fuse_gather;      /* R~_i(r - A z) computed inside the SYMV kernel for single-item subdomains:
                              0 never, 1 (default) when the items are large (>= 32 tiles) or the
                              colour is small, 2 always                                               */
+    void* comm;           /* ddg_comm* for multi-GPU, or NULL (single GPU)                          */
     int small_kernel;     /* 1 (default): colours of many (>= 16 per SM) single-item subdomains with
                              |Omega~_i| <= 256 use the warp-per-subdomain SYMV                    */
     const int32_t* block_coords; /* optional nparts x block_ndim integer coordinates of the parts
@@ -192,6 +193,38 @@ typedef struct {
 
 int ddg_set_profiling(ddg_ctx* ctx, int on);
 int ddg_get_kernel_stats(ddg_ctx* ctx, ddg_kstats* st);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU.  One process / context per GPU.  Every rank
+ * passes the same GLOBAL A, F and partition to ddg_setup with opts.comm set;
+ * parts are assigned to ranks (boxes of the block grid when block_coords are
+ * given), each rank applies only its own subdomains and exchanges, over NCCL:
+ * p and r halos once per iteration, the z values written by every colour
+ * step, the zero-padded coarse right-hand side (allreduce) and the three CG
+ * scalars (allreduce); the coarse factor is replicated.  f and u stay full
+ * length on every rank (u is assembled on every rank at the end).
+ * ------------------------------------------------------------------------- */
+typedef struct ddg_comm ddg_comm;
+
+/* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */
+int ddg_get_unique_id(void* id128);
+int ddg_comm_init(int rank, int nranks, const void* id128, int device, ddg_comm** out);
+void ddg_comm_destroy(ddg_comm* comm);
+
+/* Host-only decomposition plan (no device needed): the same plan ddg_setup
+ * builds for a communicator of nranks, exposed for tests and tools. */
+typedef struct ddg_plan ddg_plan;
+enum { DDG_PLAN_OWNED_ROWS = 0, DDG_PLAN_OWNED_SUBS = 1, DDG_PLAN_P_SEND = 2, DDG_PLAN_P_RECV = 3,
+       DDG_PLAN_R_SEND = 4, DDG_PLAN_R_RECV = 5, DDG_PLAN_Z_SEND = 6, DDG_PLAN_Z_RECV = 7,
+       DDG_PLAN_PROLONG_PARTS = 8, DDG_PLAN_COLOURS = 9, DDG_PLAN_PART_RANK = 10,
+       DDG_PLAN_OVERLAP = 11 };
+int ddg_plan_create(int64_t n, const int64_t* row_ptr, const int32_t* col, const int32_t* part,
+                    int32_t nparts, int overlap, const int32_t* block_coords, int block_ndim, int rank,
+                    int nranks, ddg_plan** out);
+/* Number of entries of list `what` (for colour / peer / subdomain where it
+ * applies); copies min(count, cap) int32 entries into out when out != NULL. */
+int64_t ddg_plan_query(ddg_plan* plan, int what, int colour, int peer, int32_t* out, int64_t cap);
+void ddg_plan_destroy(ddg_plan* plan);
 
 /* Release every resource of the context (NULL is a no-op). */
 void ddg_destroy(ddg_ctx* ctx);

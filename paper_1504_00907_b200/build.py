@@ -9,10 +9,21 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libddg.so")
-SOURCES = ["kernels.cu", "setup.cpp", "coarse_sparse.cpp"]
-HEADERS = ["ddg_internal.h", "ctx.h", os.path.join("..", "..", "include", "ddg.h")]
+SOURCES = ["kernels.cu", "setup.cpp", "coarse_sparse.cpp", "dist.cpp", "comm.cpp"]
+HEADERS = ["ddg_internal.h", "ctx.h", "dist.h", "comm.h", os.path.join("..", "..", "include", "ddg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    import glob
+    for p in sys.path + ["/opt/prime-rl/.venv/lib/python3.12/site-packages"]:
+        cand = os.path.join(p, "nvidia", "nccl")
+        if os.path.exists(os.path.join(cand, "include", "nccl.h")):
+            return cand
+    if os.path.exists("/usr/include/nccl.h"):
+        return "/usr"
+    raise RuntimeError("nccl.h not found")
 
 
 def _stale() -> bool:
@@ -34,6 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(bdir, s + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
+               "-I", os.path.join(_nccl_dir(), "include"),
+               f'-DDDG_NCCL_DIR="{os.path.join(_nccl_dir(), "lib")}"',
                "-c", src, "-o", obj]
         if s.endswith(".cpp"):
             cmd += ["-x", "cu"] if False else []
@@ -41,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
-                           "-lpthread"])
+                           "-lpthread", "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -8,7 +8,9 @@
 #include <vector>
 
 #include "../../include/ddg.h"
+#include "comm.h"
 #include "ddg_internal.h"
+#include "dist.h"
 
 using namespace ddg;
 
@@ -111,6 +113,21 @@ struct ddg_ctx {
     // coarse solver variant: 1 dense packed inverse, 2 sparse supernodal (coarse_sparse.cpp)
     int coarse_variant = 1;
     SparseCoarse* sparse = nullptr;
+    // multi-GPU (dist.cpp / comm.cpp)
+    ddg_comm* comm = nullptr;
+    bool dist = false;
+    int rank = 0, nranks = 1;
+    int comm_err = 0;
+    ddg::DistPlan plan;
+    int32_t* d_rows = nullptr;          // owned rows (nullptr: all rows)
+    int64_t nrows = 0;
+    ddg::Halo h_p, h_r;
+    std::vector<ddg::Halo> h_z;         // one per colour
+    int32_t* d_restrict_parts = nullptr;
+    int n_restrict = 0;
+    int32_t* d_prolong_parts = nullptr;
+    int n_prolong = 0;
+    std::vector<int32_t> op_sub;        // subdomain id of every local operator
     std::vector<int32_t> block_coords;  // optional nparts x block_ndim
     int block_ndim = 0;
 };

@@ -86,6 +86,8 @@ struct Scalars {
     double rtol;
     int32_t iter, done, status, max_iter;
     int32_t stop_mode, converged, pad0, pad1;
+    double loc[5];   // multi-GPU: rank-local sums (init, rz_first, spmv_dot, update, rz)
+    double glob[5];  // ... and their allreduced totals
 };
 
 // Reduction scratch: per-block partial sums + a ticket counter.
@@ -124,25 +126,34 @@ void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* item
 void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                             const int32_t* cptr, const int64_t* qoff, const double* Q, DevCSR A,
                             const double* r, const double* z, double* bc, int maxmI,
-                            const int32_t* done);
+                            const int32_t* done, const int32_t* parts = nullptr);
 void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                     const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc,
-                    double* z, const int32_t* done);
+                    double* z, const int32_t* done, const int32_t* parts = nullptr);
 void launch_fill(cudaStream_t st, double* x, int64_t n, double v, const int32_t* done);
 void launch_spmv(cudaStream_t st, DevCSR A, const double* x, double* y);
 
-// PCG pieces (all read/write the device Scalars; all exit early once done != 0)
-void launch_pcg_init(cudaStream_t st, int64_t n, const double* f, double* r, double* u,
-                     Scalars* sc, double* hist, double* red, unsigned* ticket);
-void launch_pcg_rz_first(cudaStream_t st, int64_t n, const double* r, const double* z, double* p,
-                         Scalars* sc, double* red, unsigned* ticket);
-void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, Scalars* sc,
-                         double* red, unsigned* ticket);
-void launch_pcg_update(cudaStream_t st, int64_t n, const double* p, const double* q, double* u,
-                       double* r, Scalars* sc, double* hist, double* red, unsigned* ticket);
-void launch_pcg_rz(cudaStream_t st, int64_t n, const double* r, const double* z, Scalars* sc,
-                   double* red, unsigned* ticket);
-void launch_pcg_direction(cudaStream_t st, int64_t n, const double* z, double* p, Scalars* sc);
+// PCG pieces (all read/write the device Scalars; all exit early once done != 0).
+// rows/nrows: the rank's owned rows (rows == nullptr: 0..nrows-1); dist != 0:
+// reductions leave the rank-local sum in sc->loc[slot] (then allreduce +
+// launch_pcg_finalize).
+void launch_pcg_init(cudaStream_t st, int64_t n, const double* f, double* r, double* u, const int32_t* rows,
+                     int64_t nrows, Scalars* sc, double* hist, double* red, unsigned* ticket, int dist);
+void launch_pcg_rz_first(cudaStream_t st, const double* r, const double* z, double* p, const int32_t* rows,
+                         int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist);
+void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, const int32_t* rows,
+                         int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist);
+void launch_pcg_update(cudaStream_t st, const double* p, const double* q, double* u, double* r,
+                       const int32_t* rows, int64_t nrows, Scalars* sc, double* hist, double* red,
+                       unsigned* ticket, int dist);
+void launch_pcg_rz(cudaStream_t st, const double* r, const double* z, const int32_t* rows, int64_t nrows,
+                   Scalars* sc, double* red, unsigned* ticket, int dist);
+void launch_pcg_direction(cudaStream_t st, const double* z, double* p, const int32_t* rows, int64_t nrows,
+                          Scalars* sc);
+void launch_pcg_finalize(cudaStream_t st, int slot, Scalars* sc, double* hist);
+void launch_halo_pack(cudaStream_t st, const double* v, const int32_t* idx, double* buf, int64_t n);
+void launch_halo_unpack(cudaStream_t st, const double* buf, const int32_t* idx, double* v, int64_t n);
+void launch_copy_rows(cudaStream_t st, const double* in, double* out, const int32_t* rows, int64_t nrows);
 
 // setup kernels
 void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,

@@ -76,141 +76,203 @@ __device__ void grid_reduce(double v, double* red, unsigned* ticket, Fin fin) {
 
 // =============================================================================
 // PCG vector kernels
+// Rows: the rank's owned rows (rows == nullptr: rows 0..nrows-1).  Reductions
+// end either in the last block (single rank) or, with `dist`, by storing the
+// rank-local sum in sc->loc[slot] for an NCCL allreduce followed by
+// k_pcg_finalize (multi-GPU).
 // =============================================================================
 
+#define ROW(i) (rows ? (int64_t)rows[i] : (i))
+
+__device__ void fin_init(Scalars* sc, double* hist, double s) {
+    const double r0 = sqrt(s);
+    sc->res0 = r0;
+    sc->ref = r0;
+    sc->res = r0;
+    hist[0] = r0;
+    sc->iter = 0;
+    sc->status = 0;
+    sc->converged = (r0 == 0.0);
+    sc->done = (r0 == 0.0);
+}
+__device__ void fin_rz_first(Scalars* sc, double s) {
+    if (!(s > 0.0)) {
+        sc->status = 7;  // DDG_E_BREAKDOWN
+        sc->done = 1;
+    } else {
+        sc->rho = s;
+        sc->pres0 = sqrt(s);
+    }
+}
+__device__ void fin_spmv_dot(Scalars* sc, double s) {
+    sc->sigma = s;
+    if (!(s > 0.0)) {
+        sc->status = 7;
+        sc->done = 1;
+    } else {
+        sc->alpha = sc->rho / s;
+    }
+}
+__device__ void fin_update(Scalars* sc, double* hist, double s) {
+    const double res = sqrt(s);
+    const int it = sc->iter + 1;
+    sc->iter = it;
+    sc->res = res;
+    hist[it] = res;
+    if (sc->stop_mode == 1 && it == 1) sc->ref = res;
+    bool conv = false;
+    if (sc->stop_mode == 0) conv = res <= sc->rtol * sc->ref;
+    if (sc->stop_mode == 1) conv = (it > 1) && res <= sc->rtol * sc->ref;
+    if (res == 0.0) conv = true;
+    if (conv) {
+        sc->converged = 1;
+        sc->done = 1;
+    } else if (it >= sc->max_iter) {
+        sc->done = 1;
+    }
+}
+__device__ void fin_rz(Scalars* sc, double s) {
+    if (sc->stop_mode == 2 && sqrt(fabs(s)) <= sc->rtol * sc->pres0) {
+        sc->converged = 1;
+        sc->done = 1;
+    } else if (!(s > 0.0)) {
+        sc->status = 7;
+        sc->done = 1;
+    } else {
+        sc->beta = s / sc->rho;
+        sc->rho = s;
+    }
+}
+
 __global__ void k_pcg_init(int64_t n, const double* __restrict__ f, double* __restrict__ r,
-                           double* __restrict__ u, Scalars* sc, double* hist, double* red,
-                           unsigned* ticket) {
+                           double* __restrict__ u, const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc,
+                           double* hist, double* red, unsigned* ticket, int dist) {
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double v = f[i];
-        r[i] = v;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        r[i] = f[i];
         u[i] = 0.0;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = f[ROW(i)];
         acc += v * v;
     }
     grid_reduce(acc, red, ticket, [&](double s) {
-        double r0 = sqrt(s);
-        sc->res0 = r0;
-        sc->ref = r0;
-        sc->res = r0;
-        hist[0] = r0;
-        sc->iter = 0;
-        sc->status = 0;
-        sc->converged = (r0 == 0.0);
-        sc->done = (r0 == 0.0);
+        if (dist) { sc->loc[0] = s; sc->done = 0; return; }
+        fin_init(sc, hist, s);
     });
 }
 
 // rho = r^T z ; p = z  (first direction)
-__global__ void k_pcg_rz_first(int64_t n, const double* __restrict__ r, const double* __restrict__ z,
-                               double* __restrict__ p, Scalars* sc, double* red, unsigned* ticket) {
+__global__ void k_pcg_rz_first(const double* __restrict__ r, const double* __restrict__ z,
+                               double* __restrict__ p, const int32_t* __restrict__ rows, int64_t nrows,
+                               Scalars* sc, double* red, unsigned* ticket, int dist) {
     if (sc->done) return;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double zi = z[i];
-        p[i] = zi;
-        acc += r[i] * zi;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = ROW(i);
+        const double zi = z[v];
+        p[v] = zi;
+        acc += r[v] * zi;
     }
     grid_reduce(acc, red, ticket, [&](double s) {
-        if (!(s > 0.0)) {
-            sc->status = 7;  // DDG_E_BREAKDOWN
-            sc->done = 1;
-        } else {
-            sc->rho = s;
-            sc->pres0 = sqrt(s);
-        }
+        if (dist) { sc->loc[1] = s; return; }
+        fin_rz_first(sc, s);
     });
 }
 
 // q = A p ; sigma = p^T q ; alpha = rho / sigma
 __global__ void k_pcg_spmv_dot(DevCSR A, const double* __restrict__ p, double* __restrict__ q,
-                               Scalars* sc, double* red, unsigned* ticket) {
+                               const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc, double* red,
+                               unsigned* ticket, int dist) {
     if (sc->done) return;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = ROW(i);
         double s = 0.0;
-        for (int e = A.rp[i]; e < A.rp[i + 1]; e++) s += A.val[e] * p[A.col[e]];
-        q[i] = s;
-        acc += p[i] * s;
+        for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * p[A.col[e]];
+        q[v] = s;
+        acc += p[v] * s;
     }
     grid_reduce(acc, red, ticket, [&](double s) {
-        sc->sigma = s;
-        if (!(s > 0.0)) {
-            sc->status = 7;
-            sc->done = 1;
-        } else {
-            sc->alpha = sc->rho / s;
-        }
+        if (dist) { sc->loc[2] = s; return; }
+        fin_spmv_dot(sc, s);
     });
 }
 
 // u += alpha p ; r -= alpha q ; ||r|| ; history ; stopping rule (reading R1)
-__global__ void k_pcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ q,
-                             double* __restrict__ u, double* __restrict__ r, Scalars* sc,
-                             double* hist, double* red, unsigned* ticket) {
+__global__ void k_pcg_update(const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ u,
+                             double* __restrict__ r, const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc,
+                             double* hist, double* red, unsigned* ticket, int dist) {
     if (sc->done) return;
     const double alpha = sc->alpha;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        u[i] += alpha * p[i];
-        double ri = r[i] - alpha * q[i];
-        r[i] = ri;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = ROW(i);
+        u[v] += alpha * p[v];
+        const double ri = r[v] - alpha * q[v];
+        r[v] = ri;
         acc += ri * ri;
     }
     grid_reduce(acc, red, ticket, [&](double s) {
-        double res = sqrt(s);
-        int it = sc->iter + 1;
-        sc->iter = it;
-        sc->res = res;
-        hist[it] = res;
-        if (sc->stop_mode == 1 && it == 1) sc->ref = res;
-        bool conv = false;
-        if (sc->stop_mode == 0) conv = res <= sc->rtol * sc->ref;
-        if (sc->stop_mode == 1) conv = (it > 1) && res <= sc->rtol * sc->ref;
-        if (res == 0.0) conv = true;
-        if (conv) {
-            sc->converged = 1;
-            sc->done = 1;
-        } else if (it >= sc->max_iter) {
-            sc->done = 1;
-        }
+        if (dist) { sc->loc[3] = s; return; }
+        fin_update(sc, hist, s);
     });
 }
 
 // rho' = r^T z ; beta = rho' / rho
-__global__ void k_pcg_rz(int64_t n, const double* __restrict__ r, const double* __restrict__ z,
-                         Scalars* sc, double* red, unsigned* ticket) {
+__global__ void k_pcg_rz(const double* __restrict__ r, const double* __restrict__ z,
+                         const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc, double* red,
+                         unsigned* ticket, int dist) {
     if (sc->done) return;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        acc += r[i] * z[i];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = ROW(i);
+        acc += r[v] * z[v];
+    }
     grid_reduce(acc, red, ticket, [&](double s) {
-        if (sc->stop_mode == 2 && sqrt(fabs(s)) <= sc->rtol * sc->pres0) {
-            sc->converged = 1;
-            sc->done = 1;
-        } else if (!(s > 0.0)) {
-            sc->status = 7;
-            sc->done = 1;
-        } else {
-            sc->beta = s / sc->rho;
-            sc->rho = s;
-        }
+        if (dist) { sc->loc[4] = s; return; }
+        fin_rz(sc, s);
     });
 }
 
 // p = z + beta p
-__global__ void k_pcg_direction(int64_t n, const double* __restrict__ z, double* __restrict__ p,
-                                const Scalars* sc) {
+__global__ void k_pcg_direction(const double* __restrict__ z, double* __restrict__ p,
+                                const int32_t* __restrict__ rows, int64_t nrows, const Scalars* sc) {
     if (sc->done) return;
     const double beta = sc->beta;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = z[i] + beta * p[i];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = ROW(i);
+        p[v] = z[v] + beta * p[v];
+    }
+}
+
+// multi-GPU: apply the stopping / step logic to the allreduced sum
+__global__ void k_pcg_finalize(int slot, Scalars* sc, double* hist) {
+    const double s = sc->glob[slot];
+    if (slot == 0) { fin_init(sc, hist, s); return; }
+    if (sc->done) return;
+    if (slot == 1) fin_rz_first(sc, s);
+    else if (slot == 2) fin_spmv_dot(sc, s);
+    else if (slot == 3) fin_update(sc, hist, s);
+    else fin_rz(sc, s);
+}
+
+// halo exchange pack / unpack
+__global__ void k_halo_pack(const double* __restrict__ v, const int32_t* __restrict__ idx, double* __restrict__ buf,
+                            int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = v[idx[i]];
+}
+__global__ void k_halo_unpack(const double* __restrict__ buf, const int32_t* __restrict__ idx, double* __restrict__ v,
+                              int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[idx[i]] = buf[i];
+}
+// out[rows] = in[rows] (assembly of rank-owned rows before an allreduce)
+__global__ void k_copy_rows(const double* __restrict__ in, double* __restrict__ out,
+                            const int32_t* __restrict__ rows, int64_t nrows) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x)
+        out[rows[i]] = in[rows[i]];
 }
 
 __global__ void k_fill(double* x, int64_t n, double v, const int32_t* done) {
@@ -759,10 +821,10 @@ __global__ void k_coarse_restrict(const int64_t* __restrict__ bptr, const int32_
                                   const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff,
                                   const double* __restrict__ Q, DevCSR A, const double* __restrict__ r,
                                   const double* __restrict__ z, double* __restrict__ bc,
-                                  const int32_t* done) {
+                                  const int32_t* done, const int32_t* __restrict__ parts) {
     if (*done) return;
     extern __shared__ double res[];
-    const int I = blockIdx.x;
+    const int I = parts ? parts[blockIdx.x] : blockIdx.x;
     const int64_t b0 = bptr[I];
     const int mI = (int)(bptr[I + 1] - b0);
     for (int a = threadIdx.x; a < mI; a += blockDim.x) {
@@ -787,10 +849,10 @@ __global__ void k_coarse_restrict(const int64_t* __restrict__ bptr, const int32_
 __global__ void k_prolong(const int64_t* __restrict__ bptr, const int32_t* __restrict__ bidx,
                           const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff,
                           const double* __restrict__ Q, const double* __restrict__ yc,
-                          double* __restrict__ z, const int32_t* done) {
+                          double* __restrict__ z, const int32_t* done, const int32_t* __restrict__ parts) {
     if (*done) return;
     __shared__ double ys[64];
-    const int I = blockIdx.x;
+    const int I = parts ? parts[blockIdx.x] : blockIdx.x;
     const int64_t b0 = bptr[I];
     const int mI = (int)(bptr[I + 1] - b0);
     const int ncI = cptr[I + 1] - cptr[I];
@@ -1265,17 +1327,19 @@ void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* item
 void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                             const int32_t* cptr, const int64_t* qoff, const double* Q, DevCSR A,
                             const double* r, const double* z, double* bc, int maxmI,
-                            const int32_t* done) {
+                            const int32_t* done, const int32_t* parts) {
+    if (nparts <= 0) return;
     const size_t smem = (size_t)maxmI * sizeof(double);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_coarse_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_coarse_restrict<<<nparts, 256, smem, st>>>(bptr, bidx, cptr, qoff, Q, A, r, z, bc, done);
+    k_coarse_restrict<<<nparts, 256, smem, st>>>(bptr, bidx, cptr, qoff, Q, A, r, z, bc, done, parts);
 }
 
 void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                     const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc,
-                    double* z, const int32_t* done) {
-    k_prolong<<<nparts, 128, 0, st>>>(bptr, bidx, cptr, qoff, Q, yc, z, done);
+                    double* z, const int32_t* done, const int32_t* parts) {
+    if (nparts <= 0) return;
+    k_prolong<<<nparts, 128, 0, st>>>(bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
 }
 
 void launch_fill(cudaStream_t st, double* x, int64_t n, double v, const int32_t* done) {
@@ -1286,28 +1350,42 @@ void launch_spmv(cudaStream_t st, DevCSR A, const double* x, double* y) {
     k_spmv<<<vec_grid(A.n), VEC_THREADS, 0, st>>>(A, x, y);
 }
 
-void launch_pcg_init(cudaStream_t st, int64_t n, const double* f, double* r, double* u,
-                     Scalars* sc, double* hist, double* red, unsigned* ticket) {
-    k_pcg_init<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, f, r, u, sc, hist, red, ticket);
+void launch_pcg_init(cudaStream_t st, int64_t n, const double* f, double* r, double* u, const int32_t* rows,
+                     int64_t nrows, Scalars* sc, double* hist, double* red, unsigned* ticket, int dist) {
+    k_pcg_init<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, f, r, u, rows, nrows, sc, hist, red, ticket, dist);
 }
-void launch_pcg_rz_first(cudaStream_t st, int64_t n, const double* r, const double* z, double* p,
-                         Scalars* sc, double* red, unsigned* ticket) {
-    k_pcg_rz_first<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, r, z, p, sc, red, ticket);
+void launch_pcg_rz_first(cudaStream_t st, const double* r, const double* z, double* p, const int32_t* rows,
+                         int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist) {
+    k_pcg_rz_first<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(r, z, p, rows, nrows, sc, red, ticket, dist);
 }
-void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, Scalars* sc,
-                         double* red, unsigned* ticket) {
-    k_pcg_spmv_dot<<<vec_grid(A.n), VEC_THREADS, 0, st>>>(A, p, q, sc, red, ticket);
+void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, const int32_t* rows,
+                         int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist) {
+    k_pcg_spmv_dot<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist);
 }
-void launch_pcg_update(cudaStream_t st, int64_t n, const double* p, const double* q, double* u,
-                       double* r, Scalars* sc, double* hist, double* red, unsigned* ticket) {
-    k_pcg_update<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, p, q, u, r, sc, hist, red, ticket);
+void launch_pcg_update(cudaStream_t st, const double* p, const double* q, double* u, double* r,
+                       const int32_t* rows, int64_t nrows, Scalars* sc, double* hist, double* red,
+                       unsigned* ticket, int dist) {
+    k_pcg_update<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(p, q, u, r, rows, nrows, sc, hist, red, ticket, dist);
 }
-void launch_pcg_rz(cudaStream_t st, int64_t n, const double* r, const double* z, Scalars* sc,
-                   double* red, unsigned* ticket) {
-    k_pcg_rz<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, r, z, sc, red, ticket);
+void launch_pcg_rz(cudaStream_t st, const double* r, const double* z, const int32_t* rows, int64_t nrows,
+                   Scalars* sc, double* red, unsigned* ticket, int dist) {
+    k_pcg_rz<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(r, z, rows, nrows, sc, red, ticket, dist);
 }
-void launch_pcg_direction(cudaStream_t st, int64_t n, const double* z, double* p, Scalars* sc) {
-    k_pcg_direction<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, z, p, sc);
+void launch_pcg_direction(cudaStream_t st, const double* z, double* p, const int32_t* rows, int64_t nrows,
+                          Scalars* sc) {
+    k_pcg_direction<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(z, p, rows, nrows, sc);
+}
+void launch_pcg_finalize(cudaStream_t st, int slot, Scalars* sc, double* hist) {
+    k_pcg_finalize<<<1, 1, 0, st>>>(slot, sc, hist);
+}
+void launch_halo_pack(cudaStream_t st, const double* v, const int32_t* idx, double* buf, int64_t n) {
+    if (n > 0) k_halo_pack<<<vec_grid(n), VEC_THREADS, 0, st>>>(v, idx, buf, n);
+}
+void launch_halo_unpack(cudaStream_t st, const double* buf, const int32_t* idx, double* v, int64_t n) {
+    if (n > 0) k_halo_unpack<<<vec_grid(n), VEC_THREADS, 0, st>>>(buf, idx, v, n);
+}
+void launch_copy_rows(cudaStream_t st, const double* in, double* out, const int32_t* rows, int64_t nrows) {
+    if (nrows > 0) k_copy_rows<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(in, out, rows, nrows);
 }
 
 void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,

@@ -146,6 +146,8 @@ static inline DD dd_sqrt(DD a) {
 // the context
 // ---------------------------------------------------------------------------
 #include "ctx.h"
+#include "comm.h"
+#include "dist.h"
 
 // coarse_sparse.cpp
 int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col, const std::vector<int32_t>& er,
@@ -169,6 +171,19 @@ static void free_ctx(ddg_ctx* c) {
     if (c->h_sc) cudaFreeHost(c->h_sc);
     for (auto e : c->evpool) cudaEventDestroy(e);
     if (c->sparse) sparse_coarse_free(c->sparse);
+    {
+        std::vector<ddg::Halo*> hs{&c->h_p, &c->h_r};
+        for (auto& h : c->h_z) hs.push_back(&h);
+        for (auto* h : hs) {
+            if (h->d_sidx) cudaFree(h->d_sidx);
+            if (h->d_ridx) cudaFree(h->d_ridx);
+            if (h->d_sbuf) cudaFree(h->d_sbuf);
+            if (h->d_rbuf) cudaFree(h->d_rbuf);
+        }
+        if (c->d_rows) cudaFree(c->d_rows);
+        if (c->d_restrict_parts) cudaFree(c->d_restrict_parts);
+        if (c->d_prolong_parts) cudaFree(c->d_prolong_parts);
+    }
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -479,15 +494,18 @@ static int build_plans(ddg_ctx* c) {
     std::vector<int32_t> sorted_idx;
     sorted_idx.reserve(c->oidx.size());
     int pos = 0;
+    c->op_sub.clear();
     for (int cc = 0; cc < c->ncolours; ++cc) {
         ColourPlan& pl = c->plans[cc];
-        pl.sub_begin = pos;
+        pl.sub_begin = (int)c->ops.size();
         pl.item_begin = (int)c->items.size();
         pl.red_begin = (int)c->red.size();
         pl.max_rows = 0;
         while (pos < c->nparts && c->colour[c->order[pos]] == cc) {
             const int i = c->order[pos];
+            if (c->dist && c->plan.part_rank[i] != c->rank) { ++pos; continue; }   // another rank's
             const int64_t m = c->optr[i + 1] - c->optr[i];
+            c->op_sub.push_back(i);
             const int64_t off = (int64_t)sorted_idx.size();
             sorted_idx.insert(sorted_idx.end(), c->oidx.begin() + c->optr[i],
                               c->oidx.begin() + c->optr[i + 1]);
@@ -495,7 +513,7 @@ static int build_plans(ddg_ctx* c) {
             pl.max_rows = std::max<int>(pl.max_rows, (int)m);
             ++pos;
         }
-        pl.sub_end = pos;
+        pl.sub_end = (int)c->ops.size();
         pl.item_end = (int)c->items.size();
         pl.max_rows_t = 0;
         pl.all_single = 1;
@@ -513,7 +531,7 @@ static int build_plans(ddg_ctx* c) {
     c->colour_alg_bytes.assign(c->ncolours, 0.0);
     for (int cc = 0; cc < c->ncolours; ++cc)
         for (int q = c->plans[cc].sub_begin; q < c->plans[cc].sub_end; ++q) {
-            const double m = c->ops[q].m;
+            const double m = c->ops[q].m;   // local operators of this rank
             c->colour_alg_bytes[cc] += 8.0 * m * (m + 1) / 2 + 24.0 * m;
         }
     if (c->coarse_variant != 1) return DDG_OK;
@@ -535,7 +553,8 @@ static int build_plans(ddg_ctx* c) {
 // device setup: local inverses and the coarse inverse
 // ---------------------------------------------------------------------------
 static int invert_locals(ddg_ctx* c) {
-    const int np = c->nparts;
+    const int np = (int)c->op_sub.size();
+    if (np == 0) return DDG_OK;
     size_t freeb = 0, totb = 0;
     CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
     int64_t budget = std::min<int64_t>((int64_t)freeb / 4, (int64_t)8 << 30);
@@ -594,8 +613,8 @@ static int invert_locals(ddg_ctx* c) {
     cudaFree(d_ptr);
     if (herr[0] >= 0)
         return set_err(DDG_E_NOT_SPD,
-                       "local inverse: subdomain %d (sweep position %d) not positive definite at pivot %d",
-                       c->order[herr[0]], herr[0], herr[1]);
+                       "local inverse: subdomain %d not positive definite at pivot %d",
+                       c->op_sub[herr[0]], herr[1]);
     return DDG_OK;
 }
 
@@ -734,6 +753,20 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     tick("overlap");
     build_colours(c, row_ptr, col);
     tick("colours");
+    if (c->opts.block_coords && c->opts.block_ndim > 0)
+        c->block_coords.assign(c->opts.block_coords, c->opts.block_coords + (int64_t)nparts * c->opts.block_ndim);
+    c->block_ndim = c->opts.block_ndim;
+    if (c->opts.comm) {
+        c->comm = (ddg_comm*)c->opts.comm;
+        c->dist = true;
+        c->rank = c->comm->rank;
+        c->nranks = c->comm->nranks;
+        ddg::build_dist_plan(c->plan, n, row_ptr, col, part, nparts, c->bptr.data(), c->bidx.data(),
+                             c->optr.data(), c->oidx.data(), c->colour.data(), c->ncolours,
+                             c->block_coords.empty() ? nullptr : c->block_coords.data(), c->block_ndim, c->rank,
+                             c->nranks);
+        tick("decomposition plan");
+    }
     if ((st = build_basis(c, F))) { free_ctx(c); return st; }
     tick("basis (dd-MGS)");
     std::vector<int32_t> er, ec;
@@ -751,9 +784,6 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         return set_err(DDG_E_ARG, "n_c = %lld: the dense coarse inverse is limited to 131072 unknowns",
                        (long long)nc);
     }
-    if (c->opts.block_coords && c->opts.block_ndim > 0)
-        c->block_coords.assign(c->opts.block_coords, c->opts.block_coords + (int64_t)nparts * c->opts.block_ndim);
-    c->block_ndim = c->opts.block_ndim;
     build_plans(c);
     if (c->coarse_variant == 2) {
         if ((st = sparse_coarse_symbolic(c, row_ptr, col, er, ec, ev))) { free_ctx(c); return st; }
@@ -798,6 +828,52 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     }
     c->maxmI = 0;
     for (int I = 0; I < nparts; ++I) c->maxmI = std::max<int>(c->maxmI, (int)(c->bptr[I + 1] - c->bptr[I]));
+    c->nrows = n;
+    c->n_restrict = nparts;
+    c->n_prolong = nparts;
+    c->h_z.assign(c->ncolours, ddg::Halo{});
+    if (c->dist && c->nranks > 1) {
+        const ddg::DistPlan& P = c->plan;
+        if ((st = upload(&c->d_rows, P.owned_rows)) || (st = upload(&c->d_restrict_parts, P.owned_subs)) ||
+            (st = upload(&c->d_prolong_parts, P.prolong_parts))) {
+            free_ctx(c);
+            return st;
+        }
+        c->nrows = (int64_t)P.owned_rows.size();
+        c->n_restrict = (int)P.owned_subs.size();
+        c->n_prolong = (int)P.prolong_parts.size();
+        auto mk = [&](ddg::Halo& h, const std::vector<std::vector<int32_t>>& snd,
+                      const std::vector<std::vector<int32_t>>& rcv, size_t base) -> int {
+            h.send_off.assign(c->nranks + 1, 0);
+            h.recv_off.assign(c->nranks + 1, 0);
+            std::vector<int32_t> si, ri;
+            for (int p = 0; p < c->nranks; ++p) {
+                const auto& a = snd[base + p];
+                const auto& b = rcv[base + p];
+                si.insert(si.end(), a.begin(), a.end());
+                ri.insert(ri.end(), b.begin(), b.end());
+                h.send_off[p + 1] = (int64_t)si.size();
+                h.recv_off[p + 1] = (int64_t)ri.size();
+            }
+            h.send_total = (int64_t)si.size();
+            h.recv_total = (int64_t)ri.size();
+            int e;
+            if ((e = upload(&h.d_sidx, si)) || (e = upload(&h.d_ridx, ri)) || (e = dalloc(&h.d_sbuf, si.size())) ||
+                (e = dalloc(&h.d_rbuf, ri.size())))
+                return e;
+            return DDG_OK;
+        };
+        if ((st = mk(c->h_p, P.p_send, P.p_recv, 0)) || (st = mk(c->h_r, P.r_send, P.r_recv, 0))) {
+            free_ctx(c);
+            return st;
+        }
+        for (int cc = 0; cc < c->ncolours; ++cc)
+            if ((st = mk(c->h_z[cc], P.z_send, P.z_recv, (size_t)cc * c->nranks))) {
+                free_ctx(c);
+                return st;
+            }
+        tick("halo plans");
+    }
     tick("upload");
     if ((st = invert_locals(c))) { free_ctx(c); return st; }
     tick("local inverses (GPU)");
@@ -808,7 +884,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     }
     tick("coarse inverse (GPU)");
     c->local_bytes = 0;
-    for (int q = 0; q < nparts; ++q) {
+    for (int q = 0; q < (int)c->op_sub.size(); ++q) {
         const OpDesc& op = c->ops[q];
         for (int t = 0; t < op.nitems; ++t) {
             const ItemDesc& d = c->items[op.item_base + t];
@@ -824,54 +900,74 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
 // ---------------------------------------------------------------------------
 // preconditioner and PCG enqueue
 // ---------------------------------------------------------------------------
+// multi-GPU helpers (no-ops on a single GPU) --------------------------------
+static void comm_check(ddg_ctx* c, int st) {
+    if (st && !c->comm_err) c->comm_err = st;
+}
+// after a reduction kernel: allreduce the rank-local sum, then apply its logic
+static void dist_finish(ddg_ctx* c, int slot) {
+    if (!c->dist) return;
+    comm_check(c, comm_allreduce_sum(c->comm, &c->d_sc->loc[slot], &c->d_sc->glob[slot], 1, c->stream));
+    launch_pcg_finalize(c->stream, slot, c->d_sc, c->d_hist);
+    c->launches += 1;
+}
+// send the values this rank wrote to the ranks that read them
+static void halo(ddg_ctx* c, ddg::Halo& h, double* v) {
+    if (!c->dist || c->nranks == 1) return;
+    launch_halo_pack(c->stream, v, h.d_sidx, h.d_sbuf, h.send_total);
+    comm_check(c, comm_exchange(c->comm, h, c->stream));
+    launch_halo_unpack(c->stream, h.d_rbuf, h.d_ridx, v, h.recv_total);
+    c->launches += (h.send_total > 0) + (h.recv_total > 0);
+}
+
 static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
     const ColourPlan& pl = c->plans[cc];
     int gmode = 0;
     const bool fuse = pl.all_single && (c->opts.fuse_gather == 2 ||
                                         (c->opts.fuse_gather == 1 &&
                                          (pl.max_ntiles >= 32 || pl.sub_end - pl.sub_begin <= 2 * num_sms())));
-    if (fuse) {
-        gmode = z_zero ? 2 : 1;
-    } else {
-        prof(c, PC_GATHER, 0, [&] {
-            launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, pl.max_rows,
-                          c->nnz > 24 * c->n, c->d_oidx, c->A, r, z, c->d_s, z_zero, done);
+    if (pl.sub_end > pl.sub_begin) {
+        if (fuse) {
+            gmode = z_zero ? 2 : 1;
+        } else {
+            prof(c, PC_GATHER, 0, [&] {
+                launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, pl.max_rows,
+                              c->nnz > 24 * c->n, c->d_oidx, c->A, r, z, c->d_s, z_zero, done);
+            });
+            c->launches += 1;
+        }
+        prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
+            launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
+                        c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done, pl.max_rows_t,
+                        c->d_tickets, gmode, c->A, r,
+                        pl.all_single && c->opts.small_kernel != 0 && !fuse &&
+                            pl.sub_end - pl.sub_begin >= 16 * num_sms());
         });
         c->launches += 1;
     }
-    prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
-        launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
-                    c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done, pl.max_rows_t, c->d_tickets,
-                    gmode, c->A, r,
-                    pl.all_single && c->opts.small_kernel != 0 && !fuse &&
-                        pl.sub_end - pl.sub_begin >= 16 * num_sms());
-    });
-    c->launches += 1;
+    halo(c, c->h_z[cc], z);
 }
 
 static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
-    if (c->coarse_variant == 2) {
-        prof(c, PC_COARSE, 0, [&] {
-            launch_coarse_restrict(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
-                                   c->A, r, z, sparse_coarse_rhs(c), c->maxmI, done);
-            c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
-            launch_prolong(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc,
-                           z, done);
-        });
-        c->launches += 2;
-        return;
-    }
-    const OpDesc& op = c->ops[c->coarse_op];
+    double* bc = c->coarse_variant == 2 ? sparse_coarse_rhs(c) : c->d_s + c->ops[c->coarse_op].s_off;
+    const bool multi = c->dist && c->nranks > 1;
     prof(c, PC_COARSE, 0, [&] {
-        launch_coarse_restrict(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
-                               c->A, r, z, c->d_s + op.s_off, c->maxmI, done);
-        launch_symv(c->stream, c->d_ops, c->d_items, c->coarse_item_begin,
-                    c->coarse_item_end - c->coarse_item_begin, c->d_tiles, c->d_s, c->d_oidx, nullptr,
-                    c->d_yc, c->d_partials, done, c->coarse_rows_t, c->d_tickets);
-        launch_prolong(c->stream, c->nparts, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc,
-                       z, done);
+        if (multi) cudaMemsetAsync(bc, 0, c->nc * sizeof(double), c->stream);
+        launch_coarse_restrict(c->stream, c->n_restrict, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
+                               c->A, r, z, bc, c->maxmI, done, c->d_restrict_parts);
+        if (multi) comm_check(c, comm_allreduce_sum(c->comm, bc, bc, c->nc, c->stream));
+        if (c->coarse_variant == 2) {
+            c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
+        } else {
+            launch_symv(c->stream, c->d_ops, c->d_items, c->coarse_item_begin,
+                        c->coarse_item_end - c->coarse_item_begin, c->d_tiles, c->d_s, c->d_oidx, nullptr,
+                        c->d_yc, c->d_partials, done, c->coarse_rows_t, c->d_tickets);
+            c->launches += 1;
+        }
+        launch_prolong(c->stream, c->n_prolong, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc, z,
+                       done, c->d_prolong_parts);
     });
-    c->launches += 3;
+    c->launches += 2;
 }
 
 // z = M r: zero guess, forward sweep, coarse, reverse sweep
@@ -883,20 +979,38 @@ static void enqueue_precond(ddg_ctx* c, const double* r, double* z, const int32_
     for (int cc = c->ncolours - 1; cc >= 0; --cc) colour_step(c, cc, r, z, false, done);
 }
 
-static void enqueue_iteration(ddg_ctx* c, double* u) {
+// a1 + a2: q = A p, sigma, alpha; u, r update, ||r||, stop test; r halo
+static void enqueue_step_a(ddg_ctx* c, double* u) {
     Scalars* sc = c->d_sc;
-    const int32_t* done = &sc->done;
+    const int dist = c->dist ? 1 : 0;
     prof(c, PC_VEC, 0, [&] {
-        launch_pcg_spmv_dot(c->stream, c->A, c->d_p, c->d_q, sc, c->d_redbuf, c->d_ticket);
-        launch_pcg_update(c->stream, c->n, c->d_p, c->d_q, u, c->d_r, sc, c->d_hist, c->d_redbuf,
-                          c->d_ticket);
+        launch_pcg_spmv_dot(c->stream, c->A, c->d_p, c->d_q, c->d_rows, c->nrows, sc, c->d_redbuf, c->d_ticket,
+                            dist);
+        dist_finish(c, 2);
+        launch_pcg_update(c->stream, c->d_p, c->d_q, u, c->d_r, c->d_rows, c->nrows, sc, c->d_hist, c->d_redbuf,
+                          c->d_ticket, dist);
+        dist_finish(c, 3);
+        halo(c, c->h_r, c->d_r);
     });
-    enqueue_precond(c, c->d_r, c->d_z, done);
+    c->launches += 2;
+}
+// a9: rho' = r^T z, beta; p = z + beta p; p halo
+static void enqueue_step_b(ddg_ctx* c) {
+    Scalars* sc = c->d_sc;
+    const int dist = c->dist ? 1 : 0;
     prof(c, PC_VEC, 0, [&] {
-        launch_pcg_rz(c->stream, c->n, c->d_r, c->d_z, sc, c->d_redbuf, c->d_ticket);
-        launch_pcg_direction(c->stream, c->n, c->d_z, c->d_p, sc);
+        launch_pcg_rz(c->stream, c->d_r, c->d_z, c->d_rows, c->nrows, sc, c->d_redbuf, c->d_ticket, dist);
+        dist_finish(c, 4);
+        launch_pcg_direction(c->stream, c->d_z, c->d_p, c->d_rows, c->nrows, sc);
+        halo(c, c->h_p, c->d_p);
     });
-    c->launches += 4;
+    c->launches += 2;
+}
+
+static void enqueue_iteration(ddg_ctx* c, double* u) {
+    enqueue_step_a(c, u);
+    enqueue_precond(c, c->d_r, c->d_z, &c->d_sc->done);
+    enqueue_step_b(c);
 }
 
 static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int max_iter,
@@ -909,7 +1023,11 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         int st = dalloc(&c->d_hist, max_iter + 1);
         if (st) return st;
         c->hist_cap = max_iter + 1;
+        if (c->ge_iter) { cudaGraphExecDestroy(c->ge_iter); c->ge_iter = nullptr; }   // d_hist is baked in
+        if (c->g_iter) { cudaGraphDestroy(c->g_iter); c->g_iter = nullptr; }
     }
+    c->comm_err = 0;
+    const int dist = c->dist ? 1 : 0;
     Scalars init{};
     init.rtol = rtol;
     init.max_iter = max_iter;
@@ -917,9 +1035,14 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     *c->h_sc = init;
     CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_sc, c->h_sc, sizeof(Scalars), cudaMemcpyHostToDevice, c->stream));
-    launch_pcg_init(c->stream, c->n, d_f, c->d_r, d_u, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket);
+    launch_pcg_init(c->stream, c->n, d_f, c->d_r, d_u, c->d_rows, c->nrows, c->d_sc, c->d_hist, c->d_redbuf,
+                    c->d_ticket, dist);
+    dist_finish(c, 0);
     enqueue_precond(c, c->d_r, c->d_z, &c->d_sc->done);
-    launch_pcg_rz_first(c->stream, c->n, c->d_r, c->d_z, c->d_p, c->d_sc, c->d_redbuf, c->d_ticket);
+    launch_pcg_rz_first(c->stream, c->d_r, c->d_z, c->d_p, c->d_rows, c->nrows, c->d_sc, c->d_redbuf,
+                        c->d_ticket, dist);
+    dist_finish(c, 1);
+    halo(c, c->h_p, c->d_p);
     c->launches += 2;
     CUDA_TRY(cudaGetLastError());
     // iteration graph (captured once per u pointer)
@@ -944,25 +1067,14 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     if (c->profiling) {
         // profiled solve: step on the host so that no kernel is enqueued after
         // convergence (every timed launch does real work)
-        Scalars* sc = c->d_sc;
         for (int t = 0; t < max_iter; ++t) {
-            CUDA_TRY(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
-            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            { int _s = d2h(c->stream, c->h_sc, c->d_sc, sizeof(Scalars)); if (_s) return _s; }
             if (c->h_sc->done) break;
-            prof(c, PC_VEC, 0, [&] {
-                launch_pcg_spmv_dot(c->stream, c->A, c->d_p, c->d_q, sc, c->d_redbuf, c->d_ticket);
-                launch_pcg_update(c->stream, c->n, c->d_p, c->d_q, d_u, c->d_r, sc, c->d_hist,
-                                  c->d_redbuf, c->d_ticket);
-            });
-            CUDA_TRY(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
-            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            enqueue_step_a(c, d_u);
+            { int _s = d2h(c->stream, c->h_sc, c->d_sc, sizeof(Scalars)); if (_s) return _s; }
             if (c->h_sc->done) break;
-            enqueue_precond(c, c->d_r, c->d_z, &sc->done);
-            prof(c, PC_VEC, 0, [&] {
-                launch_pcg_rz(c->stream, c->n, c->d_r, c->d_z, sc, c->d_redbuf, c->d_ticket);
-                launch_pcg_direction(c->stream, c->n, c->d_z, c->d_p, sc);
-            });
-            c->launches += 4;
+            enqueue_precond(c, c->d_r, c->d_z, &c->d_sc->done);
+            enqueue_step_b(c);
         }
         done_iters = max_iter;
     }
@@ -982,8 +1094,13 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         if (c->h_sc->done) break;
         chunk = std::min(chunk * 2, 8);
     }
+    if (c->dist && c->nranks > 1) {
+        // assemble u on every rank: u is zero outside the owned rows
+        comm_check(c, comm_allreduce_sum(c->comm, d_u, d_u, c->n, c->stream));
+    }
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(cudaEventSynchronize(c->ev1));
+    if (c->comm_err) return set_err(DDG_E_NCCL, "NCCL failure inside the solve");
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     const Scalars s = *c->h_sc;
@@ -1036,6 +1153,7 @@ extern "C" int ddg_pcg_solve(ddg_ctx* c, const double* f, double rtol, int max_i
 static int host_vec_op(ddg_ctx* c, const double* in, double* out, int which) {
     if (!c || !in || !out) return set_err(DDG_E_ARG, "null argument");
     if (cudaSetDevice(c->device) != cudaSuccess) return set_err(DDG_E_CUDA, "cudaSetDevice failed");
+    c->comm_err = 0;
     CUDA_TRY(cudaMemcpyAsync(c->d_x, in, c->n * 8, cudaMemcpyHostToDevice, c->stream));
     if (which == 0) {
         enqueue_precond(c, c->d_x, c->d_z, c->d_zero);
@@ -1046,9 +1164,17 @@ static int host_vec_op(ddg_ctx* c, const double* in, double* out, int which) {
         launch_spmv(c->stream, c->A, c->d_x, c->d_z);
         c->launches += 1;
     }
+    double* res = c->d_z;
+    if (c->dist && c->nranks > 1) {   // assemble: each rank contributes its owned rows
+        launch_fill(c->stream, c->d_q, c->n, 0.0, nullptr);
+        launch_copy_rows(c->stream, c->d_z, c->d_q, c->d_rows, c->nrows);
+        comm_check(c, comm_allreduce_sum(c->comm, c->d_q, c->d_q, c->n, c->stream));
+        res = c->d_q;
+    }
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(out, c->d_z, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(out, res, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->comm_err) return set_err(DDG_E_NCCL, "NCCL failure");
     return DDG_OK;
 }
 
@@ -1064,9 +1190,10 @@ extern "C" int ddg_get_info(ddg_ctx* c, ddg_info* info) {
     info->nparts = c->nparts;
     info->ncolours = c->ncolours;
     int mmin = INT32_MAX, mmax = 0;
-    for (int q = 0; q < c->nparts; ++q) {
-        mmin = std::min(mmin, c->ops[q].m);
-        mmax = std::max(mmax, c->ops[q].m);
+    for (int i = 0; i < c->nparts; ++i) {
+        const int m = (int)(c->optr[i + 1] - c->optr[i]);
+        mmin = std::min(mmin, m);
+        mmax = std::max(mmax, m);
     }
     info->m_min = mmin;
     info->m_max = mmax;
@@ -1087,7 +1214,7 @@ extern "C" int ddg_get_colours(ddg_ctx* c, int32_t* colour) {
 
 extern "C" int ddg_get_subdomain_sizes(ddg_ctx* c, int32_t* m) {
     if (!c || !m) return set_err(DDG_E_ARG, "null argument");
-    for (int q = 0; q < c->nparts; ++q) m[c->order[q]] = c->ops[q].m;
+    for (int i = 0; i < c->nparts; ++i) m[i] = (int32_t)(c->optr[i + 1] - c->optr[i]);
     return DDG_OK;
 }
 
@@ -1124,3 +1251,90 @@ extern "C" int ddg_get_kernel_stats(ddg_ctx* c, ddg_kstats* st) {
     c->recs.clear();
     return DDG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// host-only decomposition plan (tests / tools)
+// ---------------------------------------------------------------------------
+#include "dist.h"
+
+struct ddg_plan {
+    ddg::DistPlan P;
+    std::vector<int32_t> colour;
+    std::vector<int64_t> optr;
+    std::vector<int32_t> oidx;
+};
+
+extern "C" int ddg_plan_create(int64_t n, const int64_t* row_ptr, const int32_t* col, const int32_t* part,
+                               int32_t nparts, int overlap, const int32_t* block_coords, int block_ndim,
+                               int rank, int nranks, ddg_plan** out) {
+    if (!out || n < 1 || !row_ptr || !col || !part || nparts < 1 || nranks < 1 || rank < 0 || rank >= nranks ||
+        overlap < 0)
+        return set_err(DDG_E_ARG, "ddg_plan_create: bad argument");
+    *out = nullptr;
+    ddg_ctx c;
+    ddg_default_opts(&c.opts);
+    c.opts.overlap = overlap;
+    c.n = n;
+    c.nparts = nparts;
+    c.part.assign(part, part + n);
+    c.bptr.assign(nparts + 1, 0);
+    for (int64_t v = 0; v < n; ++v) {
+        if (part[v] < 0 || part[v] >= nparts) return set_err(DDG_E_PART, "part id out of range");
+        c.bptr[part[v] + 1]++;
+    }
+    for (int I = 0; I < nparts; ++I) c.bptr[I + 1] += c.bptr[I];
+    c.bidx.resize(n);
+    c.bpos.resize(n);
+    {
+        std::vector<int64_t> fill(c.bptr.begin(), c.bptr.end() - 1);
+        for (int64_t v = 0; v < n; ++v) {
+            c.bpos[v] = (int32_t)(fill[part[v]] - c.bptr[part[v]]);
+            c.bidx[fill[part[v]]++] = (int32_t)v;
+        }
+    }
+    build_overlap(&c, row_ptr, col);
+    build_colours(&c, row_ptr, col);
+    ddg_plan* p = new ddg_plan();
+    build_dist_plan(p->P, n, row_ptr, col, part, nparts, c.bptr.data(), c.bidx.data(), c.optr.data(),
+                    c.oidx.data(), c.colour.data(), c.ncolours, block_coords, block_ndim, rank, nranks);
+    p->colour = c.colour;
+    p->optr = c.optr;
+    p->oidx = c.oidx;
+    c.device = -1;
+    *out = p;
+    return DDG_OK;
+}
+
+extern "C" int64_t ddg_plan_query(ddg_plan* p, int what, int colour, int peer, int32_t* out, int64_t cap) {
+    if (!p) return -1;
+    const ddg::DistPlan& P = p->P;
+    const std::vector<int32_t>* v = nullptr;
+    std::vector<int32_t> tmp;
+    auto zidx = [&](int c, int q) { return (size_t)c * P.nranks + q; };
+    const bool peer_ok = peer >= 0 && peer < P.nranks;
+    const bool col_ok = colour >= 0 && colour < P.ncolours;
+    switch (what) {
+        case DDG_PLAN_OWNED_ROWS: v = &P.owned_rows; break;
+        case DDG_PLAN_OWNED_SUBS: v = &P.owned_subs; break;
+        case DDG_PLAN_P_SEND: if (!peer_ok) return -1; v = &P.p_send[peer]; break;
+        case DDG_PLAN_P_RECV: if (!peer_ok) return -1; v = &P.p_recv[peer]; break;
+        case DDG_PLAN_R_SEND: if (!peer_ok) return -1; v = &P.r_send[peer]; break;
+        case DDG_PLAN_R_RECV: if (!peer_ok) return -1; v = &P.r_recv[peer]; break;
+        case DDG_PLAN_Z_SEND: if (!peer_ok || !col_ok) return -1; v = &P.z_send[zidx(colour, peer)]; break;
+        case DDG_PLAN_Z_RECV: if (!peer_ok || !col_ok) return -1; v = &P.z_recv[zidx(colour, peer)]; break;
+        case DDG_PLAN_PROLONG_PARTS: v = &P.prolong_parts; break;
+        case DDG_PLAN_COLOURS: v = &p->colour; break;
+        case DDG_PLAN_PART_RANK: v = &P.part_rank; break;
+        case DDG_PLAN_OVERLAP:
+            if (peer < 0 || peer + 1 >= (int64_t)p->optr.size()) return -1;
+            tmp.assign(p->oidx.begin() + p->optr[peer], p->oidx.begin() + p->optr[peer + 1]);
+            v = &tmp;
+            break;
+        default: return -1;
+    }
+    const int64_t cnt = (int64_t)v->size();
+    if (out) std::copy(v->begin(), v->begin() + std::min<int64_t>(cnt, cap), out);
+    return cnt;
+}
+
+extern "C" void ddg_plan_destroy(ddg_plan* p) { delete p; }

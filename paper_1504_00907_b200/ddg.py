@@ -25,15 +25,20 @@ STOP_RES0, STOP_RES1, STOP_PREC = 0, 1, 2
 EXPORTS = ["ddg_default_opts", "ddg_setup", "ddg_pcg_solve", "ddg_pcg_solve_device",
            "ddg_apply_precond", "ddg_coarse_correct", "ddg_spmv", "ddg_get_info",
            "ddg_get_colours", "ddg_get_subdomain_sizes", "ddg_launch_count", "ddg_destroy",
-           "ddg_status_string", "ddg_last_error", "ddg_set_profiling", "ddg_get_kernel_stats"]
+           "ddg_status_string", "ddg_last_error", "ddg_set_profiling", "ddg_get_kernel_stats",
+           "ddg_get_unique_id", "ddg_comm_init", "ddg_comm_destroy", "ddg_plan_create",
+           "ddg_plan_query", "ddg_plan_destroy"]
+
+PLAN = dict(OWNED_ROWS=0, OWNED_SUBS=1, P_SEND=2, P_RECV=3, R_SEND=4, R_RECV=5, Z_SEND=6, Z_RECV=7,
+            PROLONG_PARTS=8, COLOURS=9, PART_RANK=10, OVERLAP=11)
 
 
 class ddg_opts(C.Structure):
     _fields_ = [("overlap", C.c_int), ("rank_tol", C.c_double), ("stop_mode", C.c_int),
                 ("max_iter", C.c_int), ("device", C.c_int), ("stream", C.c_void_p),
                 ("use_graphs", C.c_int), ("verbose", C.c_int), ("coarse_variant", C.c_int),
-                ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("small_kernel", C.c_int),
-                ("block_coords", C.c_void_p)]
+                ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("comm", C.c_void_p),
+                ("small_kernel", C.c_int), ("block_coords", C.c_void_p)]
 
 
 class ddg_report(C.Structure):
@@ -97,6 +102,19 @@ def load(path: str = LIB_PATH):
     L.ddg_set_profiling.restype = C.c_int
     L.ddg_get_kernel_stats.argtypes = [vp, C.POINTER(ddg_kstats)]
     L.ddg_get_kernel_stats.restype = C.c_int
+    L.ddg_get_unique_id.argtypes = [vp]
+    L.ddg_get_unique_id.restype = C.c_int
+    L.ddg_comm_init.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
+    L.ddg_comm_init.restype = C.c_int
+    L.ddg_comm_destroy.argtypes = [vp]
+    L.ddg_comm_destroy.restype = None
+    L.ddg_plan_create.argtypes = [i64, vp, vp, vp, i32, C.c_int, vp, C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(vp)]
+    L.ddg_plan_create.restype = C.c_int
+    L.ddg_plan_query.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, i64]
+    L.ddg_plan_query.restype = i64
+    L.ddg_plan_destroy.argtypes = [vp]
+    L.ddg_plan_destroy.restype = None
     L.ddg_status_string.argtypes = [C.c_int]
     L.ddg_status_string.restype = C.c_char_p
     L.ddg_last_error.restype = C.c_char_p
@@ -124,7 +142,7 @@ class Solver:
 
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
                  stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
-                 verbose=False, coarse_variant=0, block_coords=None):
+                 verbose=False, coarse_variant=0, block_coords=None, comm=None):
         L = load()
         o = default_opts()
         o.overlap, o.rank_tol, o.stop_mode, o.max_iter = overlap, rank_tol, stop_mode, max_iter
@@ -133,6 +151,8 @@ class Solver:
         o.use_graphs = 1 if use_graphs else 0
         o.verbose = 1 if verbose else 0
         o.coarse_variant = int(coarse_variant)
+        o.comm = comm.handle if comm is not None else None
+        self._comm = comm
         bc = None
         if block_coords is not None:
             bc = np.ascontiguousarray(block_coords, np.int32)
@@ -236,3 +256,70 @@ class Solver:
         st = ddg_kstats()
         _check(load().ddg_get_kernel_stats(self._h, C.byref(st)))
         return st
+
+
+def unique_id() -> bytes:
+    """128-byte NCCL unique id (create on rank 0, broadcast, pass to Comm)."""
+    buf = C.create_string_buffer(128)
+    _check(load().ddg_get_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """ddg_comm_init: one NCCL communicator per rank / GPU (include/ddg.h)."""
+
+    def __init__(self, rank, nranks, uid: bytes, device=0):
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        _check(load().ddg_comm_init(int(rank), int(nranks), buf, int(device), C.byref(h)))
+        self.handle = h
+        self.rank, self.nranks = rank, nranks
+
+    def close(self):
+        if getattr(self, "handle", None):
+            load().ddg_comm_destroy(self.handle)
+            self.handle = None
+
+
+class Plan:
+    """Host-only multi-GPU decomposition plan (ddg_plan_create); no device needed."""
+
+    def __init__(self, pr_or_n, row_ptr=None, col=None, part=None, nparts=None, overlap=1,
+                 block_coords=None, rank=0, nranks=1):
+        if row_ptr is None:
+            pr = pr_or_n
+            n, row_ptr, col, part, nparts = pr.n, pr.row_ptr, pr.col, pr.part, pr.nparts
+            overlap = pr.overlap
+            if block_coords is None:
+                block_coords = pr.block_coords
+        else:
+            n = pr_or_n
+        self._keep = [np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
+                      np.ascontiguousarray(part, np.int32)]
+        bc = None if block_coords is None else np.ascontiguousarray(block_coords, np.int32)
+        self._keep.append(bc)
+        h = C.c_void_p()
+        _check(load().ddg_plan_create(int(n), _p(self._keep[0]), _p(self._keep[1]), _p(self._keep[2]),
+                                      int(nparts), int(overlap), None if bc is None else _p(bc),
+                                      0 if bc is None else int(bc.shape[1]), int(rank), int(nranks),
+                                      C.byref(h)))
+        self._h = h
+        self.rank, self.nranks, self.nparts = rank, nranks, int(nparts)
+        self.colours = self.query("COLOURS")
+        self.ncolours = int(self.colours.max()) + 1
+
+    def query(self, what, colour=0, peer=0):
+        L = load()
+        code = PLAN[what]
+        cnt = L.ddg_plan_query(self._h, code, int(colour), int(peer), None, 0)
+        if cnt < 0:
+            raise DDGError(1, f"bad plan query {what}")
+        out = np.empty(cnt, np.int32)
+        if cnt:
+            L.ddg_plan_query(self._h, code, int(colour), int(peer), _p(out), cnt)
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            load().ddg_plan_destroy(self._h)
+            self._h = None
