@@ -213,3 +213,24 @@ def test_sparse_matches_dense_variant():
     r = np.random.default_rng(4).standard_normal(pr.n)
     a, b = sd.coarse_correct(r), ss.coarse_correct(r)
     assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(a)
+
+
+# ---------------------------------------------------------------- communicator path (1 rank)
+@pytest.mark.parametrize("name", ["C1", "poisson3d_24_b8_p2", "biharm_64_b16_p3"])
+def test_comm_path_single_rank(name):
+    """opts.comm set with a 1-rank NCCL communicator: split reductions (local
+    sum -> ncclAllReduce -> finalize kernel) and NCCL inside the iteration
+    graph; must give the same answer as the oracle."""
+    from paper_1504_00907_b200 import Solver, ddg
+    pr = CASES[name]()
+    comm = ddg.Comm(0, 1, ddg.unique_id(), 0)
+    s = Solver.from_problem(pr, comm=comm)
+    o = oracle.Oracle.from_problem(pr)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    uo, ito, histo, conv = o.pcg(pr.f, 1e-8)
+    assert rep.converged and abs(it - ito) <= 1
+    m = min(len(hist), len(histo))
+    assert np.max(np.abs(hist[:m] - histo[:m]) / histo[:m]) <= H_TOL
+    assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+    s.close()
+    comm.close()
