@@ -95,14 +95,14 @@ def dist_env():
 
 
 def model_bytes_per_iter(pr, info, sizes):
-    """Algorithmic bytes of one PCG iteration for THIS implementation (DESIGN.md §Roofline):
-    local operators read once per visit (2 sweeps), the dense coarse inverse once,
+    """Algorithmic bytes of one PCG iteration for THIS implementation (DESIGN.md §6):
+    local operators read once per visit (2 sweeps), the coarse operator bytes one solve reads
+    (ddg_info.coarse_solve_bytes),
     per-visit vectors and the O(n) vector work (SURVEY.md §8(d) formula, a = CSR bytes/row)."""
     m = sizes.astype(np.float64)
     a = 12.0 * pr.nnz / pr.n + 4.0
     local = 2 * np.sum(8.0 * m * (m + 1) / 2)
-    nc = float(info.n_c)
-    coarse = 8.0 * nc * (nc + 1) / 2
+    coarse = float(info.coarse_solve_bytes)     # dense: packed inverse; sparse: 2|G| + |H|
     visits = (64 + 2 * a) * m.sum()
     vec = (144 + 2 * a + 16 * pr.k) * pr.n
     return local + coarse + visits + vec, local
@@ -259,7 +259,9 @@ def bench_ddg(args):
                    "nparts": int(s.info.nparts), "colours": int(s.info.ncolours),
                    "coarse": "dense packed inverse" if s.info.coarse_variant == 1 else "sparse nested dissection", "parallelism": f"subdomain-sharded x{world} (NCCL halos + allreduce, replicated coarse)" if world > 1 else "1gpu",
                    "l2": "inputs larger than L2 (local inverses %.1f GB)" % (s.info.local_factor_bytes / 1e9),
-                   "time_to_rtol_ms": ms_step, "t_setup_s": round(t_setup, 2)},
+                   "time_to_rtol_ms": ms_step, "t_setup_s": round(t_setup, 2),
+                   "local_operator_bytes": int(s.info.local_factor_bytes),
+                   "coarse_solve_bytes": int(s.info.coarse_solve_bytes)},
         "roofline": {"bound": "hbm", "kernel": "k_symv (colour sweep, a4/a8)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"

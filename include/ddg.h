@@ -103,6 +103,9 @@ typedef struct {
     int64_t coarse_factor_bytes;    /* bytes of the stored coarse operator (device)            */
     int32_t coarse_variant;         /* 1 dense packed inverse, 2 sparse supernodal             */
     int32_t pad;
+    int64_t coarse_solve_bytes;     /* operator bytes one coarse solve must read: the packed
+                                       inverse once (dense), or 2|G| + |H| over the fronts
+                                       (sparse: G read forward and backward, H backward)       */
 } ddg_info;
 
 /* Fills *o with the defaults listed above. */

@@ -49,6 +49,7 @@ struct SparseCoarse {
     std::vector<int> lb;                       // fronts of level h: [lb[h], lb[h+1])
     std::vector<int> g_begin, g_end, h_begin, h_end;
     std::vector<int> fwd_b, bwd_b;             // task ranges per level (size nlevels+1)
+    std::vector<int> ring_fwd, ring_bwd;       // k_symv_ring partitions per level (-1: none)
     std::vector<FRedTask> fwd, bwd;
     std::vector<int64_t> contrib;
     std::vector<int32_t> item_front;           // item (relative to item_base) -> front
@@ -515,6 +516,12 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     sc->fwd_b[sc->nlevels] = (int)sc->fwd.size();
     sc->bwd_b[sc->nlevels] = (int)sc->bwd.size();
     sc->factor_bytes = sc->ctile_doubles * 8;
+    sc->ring_fwd.assign(sc->nlevels, -1);
+    sc->ring_bwd.assign(sc->nlevels, -1);
+    for (int h = 0; h < sc->nlevels; ++h) {
+        sc->ring_fwd[h] = ring_partition(c, sc->g_begin[h], sc->g_end[h]);
+        sc->ring_bwd[h] = ring_partition(c, sc->g_begin[h], sc->h_end[h]);
+    }
     return DDG_OK;
 }
 
@@ -660,9 +667,17 @@ int sparse_coarse_numeric(ddg_ctx* c) {
                 cudaFree(level_buf[l]);
                 level_buf[l] = nullptr;
             }
-        if (c->opts.verbose)
-            fprintf(stderr, "[ddg_setup] coarse level %2d: %5d fronts, max front %d\n", h, nf,
-                    [&] { int m = 0; for (int i = f0; i < f1; ++i) m = std::max(m, sc->fr[i].nT * TILE); return m; }());
+        if (c->opts.verbose) {
+            double gb = 0, hb = 0;
+            for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q) {
+                const ItemDesc& d = c->items[q];
+                (q < sc->g_end[h] ? gb : hb) += item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8.0;
+            }
+            fprintf(stderr, "[ddg_setup] coarse level %2d: %5d fronts, max front %d, G items %d (%.1f MB), "
+                    "H items %d (%.1f MB)\n", h, nf,
+                    [&] { int m = 0; for (int i = f0; i < f1; ++i) m = std::max(m, sc->fr[i].nT * TILE); return m; }(),
+                    sc->g_end[h] - sc->g_begin[h], gb / 1e6, sc->h_end[h] - sc->h_begin[h], hb / 1e6);
+        }
     }
     for (auto* b : level_buf)
         if (b) cudaFree(b);
@@ -678,6 +693,18 @@ int sparse_coarse_numeric(ddg_ctx* c) {
 // --------------------------------------------------------------------------
 double* sparse_coarse_rhs(ddg_ctx* c) { return c->sparse->d_bc; }
 int64_t sparse_coarse_bytes(ddg_ctx* c) { return c->sparse ? c->sparse->factor_bytes : 0; }
+// forward reads every G item, backward every G and H item
+int64_t sparse_coarse_solve_bytes(ddg_ctx* c) {
+    if (!c->sparse) return 0;
+    const SparseCoarse* sc = c->sparse;
+    int64_t b = 0;
+    for (int h = 0; h < sc->nlevels; ++h)
+        for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q) {
+            const ItemDesc& d = c->items[q];
+            b += item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8 * (q < sc->g_end[h] ? 2 : 1);
+        }
+    return b;
+}
 int sparse_coarse_levels(ddg_ctx* c) { return c->sparse ? c->sparse->nlevels : 0; }
 int sparse_coarse_nfront(ddg_ctx* c) { return c->sparse ? c->sparse->nfront : 0; }
 
@@ -688,9 +715,13 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
         launch_front_fwd_assemble(c->stream, f0, nf, sc->d_fr, sc->d_fS, sc->d_fmap, sc->d_bc, sc->d_fvec,
                                   sc->d_w, done);
-        launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->g_end[h] - sc->g_begin[h],
-                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
-                    c->d_tickets);
+        if (ring_ok(c, sc->ring_fwd[h]))
+            launch_symv_ring(c->stream, c->d_ops, c->d_items, sc->g_begin[h], c->d_ring + sc->ring_fwd[h], num_sms(),
+                             sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done);
+        else
+            launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->g_end[h] - sc->g_begin[h],
+                        sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
+                        c->d_tickets);
         launch_front_reduce(c->stream, sc->d_fwd, sc->fwd_b[h], sc->fwd_b[h + 1] - sc->fwd_b[h], sc->d_contrib,
                             sc->d_fr, sc->d_fS, c->d_partials, sc->d_w, d_x, done);
         launches += 1 + (sc->g_end[h] > sc->g_begin[h]) + (sc->fwd_b[h + 1] > sc->fwd_b[h]);
@@ -698,9 +729,13 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
     for (int h = sc->nlevels - 1; h >= 0; --h) {
         const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
         launch_front_bwd_gather(c->stream, f0, nf, sc->d_fr, sc->d_fB, d_x, sc->d_fvec, done);
-        launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->h_end[h] - sc->g_begin[h],
-                    sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
-                    c->d_tickets);
+        if (ring_ok(c, sc->ring_bwd[h]))
+            launch_symv_ring(c->stream, c->d_ops, c->d_items, sc->g_begin[h], c->d_ring + sc->ring_bwd[h], num_sms(),
+                             sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done);
+        else
+            launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->h_end[h] - sc->g_begin[h],
+                        sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
+                        c->d_tickets);
         launch_front_reduce(c->stream, sc->d_bwd, sc->bwd_b[h], sc->bwd_b[h + 1] - sc->bwd_b[h], sc->d_contrib,
                             sc->d_fr, sc->d_fS, c->d_partials, sc->d_w, d_x, done);
         launches += 3;

@@ -130,7 +130,19 @@ struct ddg_ctx {
     std::vector<int32_t> op_sub;        // subdomain id of every local operator
     std::vector<int32_t> block_coords;  // optional nparts x block_ndim
     int block_ndim = 0;
+    // SYMV kernel choice (DDG_SYMV: "ring" default, "classic", "tma") and the
+    // byte-balanced CTA partitions of every k_symv_ring launch
+    int symv_mode = 0;                  // 0 ring, 1 classic per-item k_symv, 2 tma (experimental)
+    std::vector<int32_t> h_ring;
+    int32_t* d_ring = nullptr;
+    int coarse_ring_off = -1;
 };
+
+// append the CTA partition of items [b, e) for k_symv_ring; returns its offset
+// in c->h_ring, or -1 when the range is empty or an item exceeds the ring's rows
+int ring_partition(ddg_ctx* c, int b, int e);
+// launch the colour/coarse SYMV over items [b, e) with the context's kernel choice
+bool ring_ok(const ddg_ctx* c, int off);
 
 enum { PC_SYMV = 0, PC_GATHER, PC_REDUCE, PC_COARSE, PC_VEC, PC_N };
 

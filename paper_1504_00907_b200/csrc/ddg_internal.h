@@ -14,7 +14,7 @@ constexpr int TILE_ELEMS = TILE * TILE;  // 1024 doubles = 8 KB per tile
 constexpr int DIAG_ELEMS = TILE * (TILE + 1) / 2;  // 528: packed diagonal tile (4224 B)
 
 // doubles of an item's tiles: diagonal tiles of a triangle item are packed
-inline int64_t item_doubles(int tri, int h, int ntiles) {
+__host__ __device__ inline int64_t item_doubles(int tri, int h, int ntiles) {
     return tri ? (int64_t)(ntiles - h) * TILE_ELEMS + (int64_t)h * DIAG_ELEMS : (int64_t)ntiles * TILE_ELEMS;
 }
 constexpr int SYMV_WARPS = 8;            // consumer warps per SYMV CTA
@@ -110,6 +110,7 @@ struct ColourPlan {
     int32_t max_rows_t;             // max rows touched by one SYMV item (smem sizing)
     int32_t all_single;             // every operator of the colour is one item (gather may be fused)
     int32_t max_ntiles;             // largest item of the colour (tiles)
+    int32_t ring_off;               // its k_symv_ring CTA partition in ctx::h_ring (-1: none)
 };
 
 // ---- kernel launchers (kernels.cu) ----------------------------------------
@@ -120,6 +121,12 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
                  double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
                  int gather_mode = 0, DevCSR A = DevCSR{}, const double* r = nullptr, bool small_ok = false);
+// persistent bulk-copy-ring SYMV (k_symv_ring); cta_part[0..ncta]: item ranges
+// (relative to item_begin) of the CTAs.  Requires every item's rows <= 512.
+constexpr int RING_MAX_ROWS = 512;
+void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
+                      const int32_t* cta_part, int ncta, const double* tiles, const double* s,
+                      const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done);
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
                         const double* partials, double* z, double* y_out, const int32_t* done);

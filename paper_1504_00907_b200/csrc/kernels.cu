@@ -782,6 +782,297 @@ k_symv_tma(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, i
     }
 }
 
+// ---- persistent streaming SYMV: bulk-copy ring, warp-specialised ----------
+// One CTA per SM walks a byte-balanced contiguous range of the launch's items
+// (host partition `cta_part`).  Roles:
+//  * warp 8 lane 0 (producer): streams each item's s segment(s) and its tiles
+//    (RING_TILES tiles per chunk, <= 32 KB) into shared memory with
+//    cp.async.bulk + mbarrier complete_tx, up to RING_NST chunks ahead and
+//    across item boundaries, so HBM never waits on the consumers;
+//  * warps 0-7 (consumers): each owns a fixed set of the item's tiles and
+//    progresses independently of the other consumer warps.  Tile (I, J):
+//    direct part y_I += S_IJ s_J by per-lane dot products into the warp's
+//    partial rows; transposed part y_J += S_IJ^T s_I accumulated per lane in
+//    registers (t[j] += S_IJ[lane][j] s_I[lane]) over the warp's consecutive
+//    tiles of the same column J, then one butterfly reduce-scatter per column
+//    run.  Owner of a tile: l % 8 in rectangular items (= its column for the
+//    8-wide blocks), (J + item counter) % 8 in triangles (one column per warp,
+//    rotated across items so the long columns are spread over the warps);
+//  * warp 9 (epilogue): sums the 8 warps' partial rows in warp order
+//    (deterministic) and applies them -- z[idx] += y with idx and z prefetched
+//    before the item finishes (same-colour subdomains are disjoint), y_out = y,
+//    or the partial segment of a multi-item operator (reduced later).
+// Partial rows are double-buffered by item parity, so consumer warps never
+// wait for each other.  Measured ceiling of this access pattern:
+// tools/bwprobe.cu ("tma ring" rows).
+constexpr int RING_TILES = 4;
+constexpr int RING_SLOT = RING_TILES * TILE_ELEMS;   // doubles per ring slot (32 KB)
+constexpr int RING_NST = 4;                          // ring slots (128 KB)
+constexpr int RING_MAXR = RING_MAX_ROWS;             // max rows_t of an item (512)
+constexpr int RING_THREADS = (SYMV_WARPS + 2) * 32;
+constexpr size_t RING_SMEM = (size_t)RING_NST * RING_SLOT * 8 + 2 * RING_MAXR * 8 +
+                             2 * SYMV_WARPS * RING_MAXR * 8 + 2 * 8 * sizeof(int32_t) + (2 * RING_NST + 8) * 8;
+
+// first double of tile l of item it (l == ntiles: one past the last tile)
+__device__ __forceinline__ int64_t item_tile_off_l(const ItemDesc& it, int l) {
+    if (l >= it.ntiles) return item_doubles(it.tri, it.I1 - it.I0, it.ntiles);
+    int I, J;
+    item_tile(it, l, I, J);
+    return item_tile_off(it, l, I);
+}
+
+// descriptors of the next items, fetched ahead so no role stalls on them
+struct DescPipe {
+    ItemDesc it1, it2;
+    OpDesc op1;
+    __device__ __forceinline__ void init(const ItemDesc* items, const OpDesc* ops, int i0, int i1) {
+        it1 = items[i0];
+        op1 = ops[it1.op];
+        if (i0 + 1 < i1) it2 = items[i0 + 1];
+    }
+    __device__ __forceinline__ void next(const ItemDesc* items, const OpDesc* ops, int ii, int i1, ItemDesc& it,
+                                         OpDesc& op) {
+        it = it1;
+        op = op1;
+        if (ii + 1 < i1) {
+            it1 = it2;
+            op1 = ops[it1.op];
+        }
+        if (ii + 2 < i1) it2 = items[ii + 2];
+    }
+};
+
+__device__ __forceinline__ void flush_column(double* t, double* pw, int cj, int lane) {
+    rs_stage<16>(t, lane);
+    rs_stage<8>(t, lane);
+    rs_stage<4>(t, lane);
+    rs_stage<2>(t, lane);
+    rs_stage<1>(t, lane);
+    pw[cj + lane] += t[0];
+}
+
+__global__ void __launch_bounds__(RING_THREADS, 1)
+k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
+            const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
+            const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
+            double* __restrict__ partials, const int32_t* done) {
+    if (*done) return;
+    extern __shared__ __align__(128) double rsm[];
+    double* ring = rsm;                                          // [RING_NST][RING_SLOT]
+    double* s_sm = ring + (size_t)RING_NST * RING_SLOT;          // [2][RING_MAXR]
+    double* part = s_sm + 2 * RING_MAXR;                         // [2][SYMV_WARPS][RING_MAXR]
+    int32_t* dsc = reinterpret_cast<int32_t*>(part + 2 * SYMV_WARPS * RING_MAXR);   // [2][8]
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsc + 16);
+    uint64_t* empty = full + RING_NST;
+    uint64_t* sfull = empty + RING_NST;   // [2] s + descriptor of the item landed
+    uint64_t* sempty = sfull + 2;         // [2] consumers done with the item's s
+    uint64_t* pdone = sempty + 2;         // [2] consumers' partial rows final
+    uint64_t* pfree = pdone + 2;          // [2] epilogue done with the partial rows
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RING_NST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], SYMV_WARPS);                  // every consumer warp, every chunk
+        }
+        for (int p = 0; p < 2; ++p) {
+            mbar_init(&sfull[p], 1);
+            mbar_init(&sempty[p], SYMV_WARPS);
+            mbar_init(&pdone[p], SYMV_WARPS * 32);
+            mbar_init(&pfree[p], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (i0 >= i1) return;
+    if (warp == SYMV_WARPS) {                                    // ---- producer ----
+        if (lane != 0) return;
+        DescPipe dp;
+        dp.init(items, ops, i0, i1);
+        unsigned kc = 0;
+        for (int ii = i0, ki = 0; ii < i1; ++ii, ++ki) {
+            ItemDesc it;
+            OpDesc op;
+            dp.next(items, ops, ii, i1, it, op);
+            const int p = ki & 1;
+            const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+            if (ki >= 2) mbar_wait(&sempty[p], ((ki >> 1) - 1) & 1);
+            int32_t* d = dsc + p * 8;
+            d[0] = it.I0; d[1] = it.I1; d[2] = it.J0; d[3] = it.J1; d[4] = it.tri; d[5] = it.ntiles;
+            mbar_expect_tx(&sfull[p], (unsigned)(rows_r + rows_c) * 8u);
+            const double* sop = s + op.s_off;
+            bulk_g2s(s_sm + p * RING_MAXR, sop + it.I0 * TILE, rows_r * 8u, &sfull[p]);
+            if (rows_c) bulk_g2s(s_sm + p * RING_MAXR + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[p]);
+            // tile q of a chunk always lands at q * 8 KB of its slot; rectangular
+            // items are contiguous full tiles (one copy per chunk), triangles
+            // copy tile by tile (packed diagonal tiles are 4224 B)
+            const double* src = tiles + it.tile_off;
+            int rr = 0, cc = 0;                                     // triangle walk: row, col
+            for (int l0 = 0; l0 < it.ntiles; l0 += RING_TILES, ++kc) {
+                const unsigned slot = kc % RING_NST, nf = kc / RING_NST;
+                const int nt = min(RING_TILES, it.ntiles - l0);
+                if (nf > 0) mbar_wait(&empty[slot], (nf - 1) & 1);
+                double* dst = ring + (size_t)slot * RING_SLOT;
+                if (!it.tri) {
+                    mbar_expect_tx(&full[slot], (unsigned)nt * TILE_ELEMS * 8u);
+                    bulk_g2s(dst, src, (unsigned)nt * TILE_ELEMS * 8u, &full[slot]);
+                    src += (size_t)nt * TILE_ELEMS;
+                } else {
+                    unsigned bytes = 0;
+                    int r2 = rr, c2 = cc;
+                    for (int q = 0; q < nt; ++q) {
+                        bytes += (c2 == r2 ? DIAG_ELEMS : TILE_ELEMS) * 8u;
+                        if (++c2 > r2) { c2 = 0; ++r2; }
+                    }
+                    mbar_expect_tx(&full[slot], bytes);
+                    for (int q = 0; q < nt; ++q) {
+                        const unsigned tb = (cc == rr ? DIAG_ELEMS : TILE_ELEMS) * 8u;
+                        bulk_g2s(dst + q * TILE_ELEMS, src, tb, &full[slot]);
+                        src += tb / 8;
+                        if (++cc > rr) { cc = 0; ++rr; }
+                    }
+                }
+            }
+        }
+        return;
+    }
+    if (warp == SYMV_WARPS + 1) {                                // ---- epilogue ----
+        DescPipe dp;
+        dp.init(items, ops, i0, i1);
+        for (int ii = i0, ki = 0; ii < i1; ++ii, ++ki) {
+            ItemDesc it;
+            OpDesc op;
+            dp.next(items, ops, ii, i1, it, op);
+            const int p = ki & 1;
+            const int rows_t = (it.I1 - it.I0 + (it.tri ? 0 : it.J1 - it.J0)) * TILE;
+            const int g0 = it.I0 * TILE;
+            const int nr = min(rows_t, op.m - g0);                // single-item ops only
+            const bool scat = it.part_off < 0 && op.out_mode == 0;
+            int ix[RING_MAXR / 32];
+            double zv[RING_MAXR / 32];
+            if (scat) {
+                const int32_t* idx = oidx + op.idx_off + g0;
+#pragma unroll
+                for (int r = 0; r < RING_MAXR / 32; ++r) ix[r] = (lane + 32 * r < nr) ? idx[lane + 32 * r] : 0;
+#pragma unroll
+                for (int r = 0; r < RING_MAXR / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
+            }
+            mbar_wait(&pdone[p], (ki >> 1) & 1);
+            const double* pp = part + (size_t)p * SYMV_WARPS * RING_MAXR;
+#pragma unroll
+            for (int r = 0; r < RING_MAXR / 32; ++r) {
+                const int x = lane + 32 * r;
+                if (x < rows_t) {
+                    double y = 0.0;
+#pragma unroll
+                    for (int ww = 0; ww < SYMV_WARPS; ++ww) y += pp[ww * RING_MAXR + x];
+                    if (it.part_off >= 0) partials[it.part_off + x] = y;
+                    else if (x < nr) {
+                        if (scat) z[ix[r]] = zv[r] + y;
+                        else y_out[g0 + x] = y;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfree[p]);
+        }
+        return;
+    }
+    // ---- consumers (warps 0..7): each walks only its own tiles ----
+    unsigned kc = 0;                                               // first chunk of the item
+    for (int ki = 0; ki < i1 - i0; ++ki) {
+        const int p = ki & 1;
+        mbar_wait(&sfull[p], (ki >> 1) & 1);
+        const int32_t* d = dsc + p * 8;
+        const int I0 = d[0], I1 = d[1], J0 = d[2], J1 = d[3], tri = d[4], ntiles = d[5];
+        const double* ss = s_sm + p * RING_MAXR;
+        const int rows_r = (I1 - I0) * TILE;
+        const int rows_t = rows_r + (tri ? 0 : (J1 - J0) * TILE);
+        double* pw = part + ((size_t)p * SYMV_WARPS + warp) * RING_MAXR;
+        if (ki >= 2) mbar_wait(&pfree[p], ((ki >> 1) - 1) & 1);
+        for (int x = lane; x < rows_t; x += 32) pw[x] = 0.0;
+        __syncwarp();
+        double t[TILE];
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) t[j] = 0.0;
+        int curJ = -1;
+        auto tile = [&](const double* T, int I, int J) {
+            const int ri = (I - I0) * TILE;
+            const int cj = tri ? (J - I0) * TILE : rows_r + (J - J0) * TILE;
+            if (J != curJ) {
+                if (curJ >= 0) {
+                    flush_column(t, pw, tri ? (curJ - I0) * TILE : rows_r + (curJ - J0) * TILE, lane);
+#pragma unroll
+                    for (int j = 0; j < TILE; ++j) t[j] = 0.0;
+                }
+                curJ = J;
+            }
+            double a[TILE];
+            if (I != J) {
+#pragma unroll
+                for (int j = 0; j < TILE; ++j) a[j] = T[j * TILE + lane];
+            } else {
+#pragma unroll
+                for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? T[diag_col_off(j) + lane - j] : 0.0;
+            }
+            const double2* sJ = reinterpret_cast<const double2*>(ss + cj);
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+            for (int j = 0; j < TILE; j += 4) {
+                const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                d0 = fma(a[j], u.x, d0);
+                d1 = fma(a[j + 1], u.y, d1);
+                d2 = fma(a[j + 2], v.x, d2);
+                d3 = fma(a[j + 3], v.y, d3);
+            }
+            pw[ri + lane] += (d0 + d1) + (d2 + d3);
+            const double si = ss[ri + lane];
+#pragma unroll
+            for (int j = 0; j < TILE; ++j) t[j] = fma(a[j], si, t[j]);
+        };
+        // own-tile iterator, in increasing l.  Rectangles: l = warp, warp+8, ...
+        // Triangles: columns c0 = (warp - ki) mod 8, c0+8, ... of rows r >= c.
+        int l = -1, I = 0, J = 0, r = 0, c = 0;
+        const int h = I1 - I0, wd = J1 - J0, c0 = (warp - ki) & (SYMV_WARPS - 1);
+        if (!tri) {
+            if (warp < ntiles) { l = warp; I = I0 + warp / wd; J = J0 + warp % wd; }
+        } else if (c0 < h) {
+            r = c0; c = c0; l = r * (r + 1) / 2 + c; I = I0 + r; J = J0 + c;
+        }
+        auto advance = [&]() {
+            if (!tri) {
+                l += SYMV_WARPS;
+                if (l >= ntiles) { l = -1; return; }
+                J += SYMV_WARPS;
+                while (J >= J1) { J -= wd; ++I; }
+            } else {
+                c += SYMV_WARPS;
+                if (c > r) { ++r; c = c0; }
+                if (r >= h) { l = -1; return; }
+                l = r * (r + 1) / 2 + c; I = I0 + r; J = J0 + c;
+            }
+        };
+        // every warp visits every chunk in order (keeps the mbarrier phases
+        // of each slot in step), consuming only its own tiles
+        const int nch = (ntiles + RING_TILES - 1) / RING_TILES;
+        for (int ch = 0; ch < nch; ++ch, ++kc) {
+            const unsigned slot = kc % RING_NST;
+            mbar_wait(&full[slot], (kc / RING_NST) & 1);
+            const double* C = ring + (size_t)slot * RING_SLOT;
+            while (l >= 0 && l / RING_TILES == ch) {
+                tile(C + (l & (RING_TILES - 1)) * TILE_ELEMS, I, J);
+                advance();
+            }
+            __syncwarp();                                          // every lane has consumed its rows
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+        if (curJ >= 0) flush_column(t, pw, tri ? (curJ - I0) * TILE : rows_r + (curJ - J0) * TILE, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[p]);
+        mbar_arrive(&pdone[p]);                                    // every lane (release its rows)
+    }
+}
+
 // Sum the partial segments of multi-item operators for one row block, in
 // fixed item order, and apply the result.
 __global__ void k_symv_reduce(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
@@ -1294,11 +1585,8 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
                                                       done, gather_mode, A, r);
         return;
     }
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("DDG_SYMV");
-        mode = (e && e[0] == 't') ? 1 : 0;   // "tma" selects the persistent TMA-ring kernel
-    }
+    const char* e = getenv("DDG_SYMV");
+    const int mode = (e && e[0] == 't') ? 1 : 0;   // "tma" selects the persistent TMA-ring kernel
     if (mode == 1) {
         const size_t fixed = (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
         const size_t budget = 227 * 1024 - 1024;
@@ -1315,6 +1603,18 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
     cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_symv<<<nitems, SYMV_WARPS * 32, smem, st>>>(ops, items, item_begin, tiles, s, oidx, z, y_out,
                                                   partials, done, tickets, gather_mode, A, r);
+}
+
+void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
+                      const int32_t* cta_part, int ncta, const double* tiles, const double* s,
+                      const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done) {
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_symv_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+        init = true;
+    }
+    k_symv_ring<<<ncta, RING_THREADS, RING_SMEM, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
+                                                       partials, done);
 }
 
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,

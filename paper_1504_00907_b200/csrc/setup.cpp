@@ -156,6 +156,7 @@ int sparse_coarse_numeric(ddg_ctx* c);
 int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done);
 double* sparse_coarse_rhs(ddg_ctx* c);
 int64_t sparse_coarse_bytes(ddg_ctx* c);
+int64_t sparse_coarse_solve_bytes(ddg_ctx* c);
 
 static void free_ctx(ddg_ctx* c) {
     if (!c) return;
@@ -165,7 +166,8 @@ static void free_ctx(ddg_ctx* c) {
     void* ptrs[] = {c->d_rp, c->d_col, c->d_val, c->d_oidx, c->d_ops, c->d_items, c->d_red,
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
-                    c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets};
+                    c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
+                    c->d_ring};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -485,6 +487,36 @@ static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool al
     c->ops.push_back(op);
 }
 
+// Byte-balanced contiguous partition of items [b, e) over the persistent
+// k_symv_ring CTAs (one per SM): CTA g gets the items whose byte prefix starts
+// nearest to g/G of the total (each item weighted by its bytes plus 8 KB for
+// its fixed per-item work).
+int ring_partition(ddg_ctx* c, int b, int e) {
+    if (e <= b) return -1;
+    const int G = num_sms();
+    std::vector<double> pre(e - b + 1, 0.0);
+    for (int i = b; i < e; ++i) {
+        const ItemDesc& d = c->items[i];
+        const int rows = (d.I1 - d.I0 + (d.tri ? 0 : d.J1 - d.J0)) * TILE;
+        if (rows > RING_MAX_ROWS) return -1;
+        pre[i - b + 1] = pre[i - b] + item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8.0 + 8192.0;
+    }
+    const int off = (int)c->h_ring.size();
+    c->h_ring.push_back(0);
+    int cur = 0;
+    for (int g = 1; g < G; ++g) {
+        const double target = pre.back() * g / G;
+        while (cur < e - b && pre[cur + 1] <= target) ++cur;
+        int pick = cur;
+        if (cur < e - b && target - pre[cur] > pre[cur + 1] - target) pick = cur + 1;
+        pick = std::max(pick, c->h_ring.back());
+        c->h_ring.push_back(pick);
+    }
+    c->h_ring.push_back(e - b);
+    return off;
+}
+bool ring_ok(const ddg_ctx* c, int off) { return c->symv_mode == 0 && off >= 0; }
+
 static int build_plans(ddg_ctx* c) {
     c->ops.clear();
     c->items.clear();
@@ -526,6 +558,7 @@ static int build_plans(ddg_ctx* c) {
             pl.max_ntiles = std::max(pl.max_ntiles, d.ntiles);
         }
         pl.red_end = (int)c->red.size();
+        pl.ring_off = ring_partition(c, pl.item_begin, pl.item_end);
     }
     c->oidx.swap(sorted_idx);  // now in sweep order; optr no longer valid for oidx
     c->colour_alg_bytes.assign(c->ncolours, 0.0);
@@ -546,6 +579,7 @@ static int build_plans(ddg_ctx* c) {
         c->coarse_rows_t = std::max(c->coarse_rows_t, (d.I1 - d.I0 + (d.tri ? 0 : d.J1 - d.J0)) * TILE);
     }
     c->coarse_red_end = (int)c->red.size();
+    c->coarse_ring_off = ring_partition(c, c->coarse_item_begin, c->coarse_item_end);
     return DDG_OK;
 }
 
@@ -776,6 +810,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     // environment overrides for experiments (documented in DESIGN.md)
     if (const char* e = getenv("DDG_FUSE_GATHER")) c->opts.fuse_gather = atoi(e);
     if (const char* e = getenv("DDG_SMALL_KERNEL")) c->opts.small_kernel = atoi(e);
+    if (const char* e = getenv("DDG_SYMV")) c->symv_mode = e[0] == 'c' ? 1 : e[0] == 't' ? 2 : 0;
     c->coarse_variant = c->opts.coarse_variant;
     if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
     if (c->coarse_variant == 1 && c->nc > 131072) {
@@ -811,7 +846,8 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         (st = dalloc(&c->d_p, n)) || (st = dalloc(&c->d_q, n)) || (st = dalloc(&c->d_f, n)) ||
         (st = dalloc(&c->d_u, n)) || (st = dalloc(&c->d_x, n)) || (st = dalloc(&c->d_sc, 1)) ||
         (st = dalloc(&c->d_redbuf, RED_BLOCKS)) || (st = dalloc(&c->d_ticket, 1)) ||
-        (st = dalloc(&c->d_zero, 1)) || (st = dalloc(&c->d_tickets, c->ops.size()))) {
+        (st = dalloc(&c->d_zero, 1)) || (st = dalloc(&c->d_tickets, c->ops.size())) ||
+        (st = upload(&c->d_ring, c->h_ring))) {
         free_ctx(c);
         return st;
     }
@@ -923,7 +959,8 @@ static void halo(ddg_ctx* c, ddg::Halo& h, double* v) {
 static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
     const ColourPlan& pl = c->plans[cc];
     int gmode = 0;
-    const bool fuse = pl.all_single && (c->opts.fuse_gather == 2 ||
+    const bool ring = ring_ok(c, pl.ring_off);
+    const bool fuse = !ring && pl.all_single && (c->opts.fuse_gather == 2 ||
                                         (c->opts.fuse_gather == 1 &&
                                          (pl.max_ntiles >= 32 || pl.sub_end - pl.sub_begin <= 2 * num_sms())));
     if (pl.sub_end > pl.sub_begin) {
@@ -935,6 +972,22 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
                               c->nnz > 24 * c->n, c->d_oidx, c->A, r, z, c->d_s, z_zero, done);
             });
             c->launches += 1;
+        }
+        if (ring) {
+            prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
+                launch_symv_ring(c->stream, c->d_ops, c->d_items, pl.item_begin, c->d_ring + pl.ring_off,
+                                 num_sms(), c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done);
+            });
+            c->launches += 1;
+            if (pl.red_end > pl.red_begin) {
+                prof(c, PC_REDUCE, 0, [&] {
+                    launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, pl.red_begin,
+                                       pl.red_end - pl.red_begin, c->d_oidx, c->d_partials, z, nullptr, done);
+                });
+                c->launches += 1;
+            }
+            halo(c, c->h_z[cc], z);
+            return;
         }
         prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
             launch_symv(c->stream, c->d_ops, c->d_items, pl.item_begin, pl.item_end - pl.item_begin,
@@ -958,6 +1011,16 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
         if (multi) comm_check(c, comm_allreduce_sum(c->comm, bc, bc, c->nc, c->stream));
         if (c->coarse_variant == 2) {
             c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
+        } else if (ring_ok(c, c->coarse_ring_off)) {
+            launch_symv_ring(c->stream, c->d_ops, c->d_items, c->coarse_item_begin, c->d_ring + c->coarse_ring_off,
+                             num_sms(), c->d_tiles, c->d_s, c->d_oidx, nullptr, c->d_yc, c->d_partials, done);
+            c->launches += 1;
+            if (c->coarse_red_end > c->coarse_red_begin) {
+                launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, c->coarse_red_begin,
+                                   c->coarse_red_end - c->coarse_red_begin, c->d_oidx, c->d_partials, nullptr,
+                                   c->d_yc, done);
+                c->launches += 1;
+            }
         } else {
             launch_symv(c->stream, c->d_ops, c->d_items, c->coarse_item_begin,
                         c->coarse_item_end - c->coarse_item_begin, c->d_tiles, c->d_s, c->d_oidx, nullptr,
@@ -1203,6 +1266,7 @@ extern "C" int ddg_get_info(ddg_ctx* c, ddg_info* info) {
     info->local_factor_bytes = c->local_bytes;
     info->coarse_factor_bytes = c->coarse_bytes;
     info->coarse_variant = c->coarse_variant;
+    info->coarse_solve_bytes = c->coarse_variant == 1 ? c->coarse_bytes : sparse_coarse_solve_bytes(c);
     return DDG_OK;
 }
 

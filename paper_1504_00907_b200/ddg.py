@@ -52,7 +52,8 @@ class ddg_info(C.Structure):
                 ("ncolours", C.c_int32), ("m_min", C.c_int32), ("m_max", C.c_int32),
                 ("k", C.c_int32), ("dropped", C.c_int32), ("min_rank_ratio", C.c_double),
                 ("local_factor_bytes", C.c_int64), ("coarse_factor_bytes", C.c_int64),
-                ("coarse_variant", C.c_int32), ("pad", C.c_int32)]
+                ("coarse_variant", C.c_int32), ("pad", C.c_int32),
+                ("coarse_solve_bytes", C.c_int64)]
 
 
 class ddg_kstats(C.Structure):
@@ -142,7 +143,8 @@ class Solver:
 
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
                  stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
-                 verbose=False, coarse_variant=0, block_coords=None, comm=None):
+                 verbose=False, coarse_variant=0, block_coords=None, comm=None, fuse_gather=None,
+                 small_kernel=None):
         L = load()
         o = default_opts()
         o.overlap, o.rank_tol, o.stop_mode, o.max_iter = overlap, rank_tol, stop_mode, max_iter
@@ -151,6 +153,10 @@ class Solver:
         o.use_graphs = 1 if use_graphs else 0
         o.verbose = 1 if verbose else 0
         o.coarse_variant = int(coarse_variant)
+        if fuse_gather is not None:
+            o.fuse_gather = int(fuse_gather)
+        if small_kernel is not None:
+            o.small_kernel = int(small_kernel)
         o.comm = comm.handle if comm is not None else None
         self._comm = comm
         bc = None
