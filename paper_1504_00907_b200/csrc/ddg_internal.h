@@ -124,8 +124,9 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 // persistent bulk-copy-ring SYMV (k_symv_ring); cta_part[0..ncta]: item ranges
 // (relative to item_begin) of the CTAs.  Requires every item's rows <= 512.
 constexpr int RING_MAX_ROWS = 512;
+void symv_ring_init();   // once per device, before any capture
 void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
-                      const int32_t* cta_part, int ncta, const double* tiles, const double* s,
+                      const int32_t* cta_part, int ncta, int max_rows_t, const double* tiles, const double* s,
                       const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done);
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,

@@ -21,6 +21,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "ddg_internal.h"
 
@@ -805,13 +806,17 @@ k_symv_tma(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, i
 // Partial rows are double-buffered by item parity, so consumer warps never
 // wait for each other.  Measured ceiling of this access pattern:
 // tools/bwprobe.cu ("tma ring" rows).
-constexpr int RING_TILES = 4;
-constexpr int RING_SLOT = RING_TILES * TILE_ELEMS;   // doubles per ring slot (32 KB)
-constexpr int RING_NST = 4;                          // ring slots (128 KB)
-constexpr int RING_MAXR = RING_MAX_ROWS;             // max rows_t of an item (512)
-constexpr int RING_THREADS = (SYMV_WARPS + 2) * 32;
-constexpr size_t RING_SMEM = (size_t)RING_NST * RING_SLOT * 8 + 2 * RING_MAXR * 8 +
-                             2 * SYMV_WARPS * RING_MAXR * 8 + 2 * 8 * sizeof(int32_t) + (2 * RING_NST + 8) * 8;
+constexpr int RING_EPI_WARPS = 2;
+constexpr int RING_THREADS = (SYMV_WARPS + 1 + RING_EPI_WARPS) * 32;
+constexpr int RING_MAX_NST = 24;
+constexpr int RING_MAX_NB = 8;
+// shared memory of a launch: nst slots of RT tiles; nb item buffers, each the
+// item's s (maxr rows), the 8 consumer warps' partial rows and a descriptor;
+// barriers
+__host__ __device__ constexpr size_t ring_smem(int RT, int nst, int nb, int maxr) {
+    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * (SYMV_WARPS + 1) * maxr * 8 + (size_t)nb * 8 * 4 +
+           (2 * (size_t)nst + 4 * (size_t)nb) * 8;
+}
 
 // first double of tile l of item it (l == ntiles: one past the last tile)
 __device__ __forceinline__ int64_t item_tile_off_l(const ItemDesc& it, int l) {
@@ -851,35 +856,37 @@ __device__ __forceinline__ void flush_column(double* t, double* pw, int cj, int 
     pw[cj + lane] += t[0];
 }
 
+template <int RT>
 __global__ void __launch_bounds__(RING_THREADS, 1)
 k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
             const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
             const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
-            double* __restrict__ partials, const int32_t* done) {
+            double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr) {
+    constexpr int SLOT = RT * TILE_ELEMS;
     if (*done) return;
     extern __shared__ __align__(128) double rsm[];
-    double* ring = rsm;                                          // [RING_NST][RING_SLOT]
-    double* s_sm = ring + (size_t)RING_NST * RING_SLOT;          // [2][RING_MAXR]
-    double* part = s_sm + 2 * RING_MAXR;                         // [2][SYMV_WARPS][RING_MAXR]
-    int32_t* dsc = reinterpret_cast<int32_t*>(part + 2 * SYMV_WARPS * RING_MAXR);   // [2][8]
-    uint64_t* full = reinterpret_cast<uint64_t*>(dsc + 16);
-    uint64_t* empty = full + RING_NST;
-    uint64_t* sfull = empty + RING_NST;   // [2] s + descriptor of the item landed
-    uint64_t* sempty = sfull + 2;         // [2] consumers done with the item's s
-    uint64_t* pdone = sempty + 2;         // [2] consumers' partial rows final
-    uint64_t* pfree = pdone + 2;          // [2] epilogue done with the partial rows
+    double* ring = rsm;                                          // [nst][SLOT]
+    double* s_sm = ring + (size_t)nst * SLOT;                    // [nb][maxr]
+    double* part = s_sm + (size_t)nb * maxr;                     // [nb][SYMV_WARPS][maxr]
+    int32_t* dsc = reinterpret_cast<int32_t*>(part + (size_t)nb * SYMV_WARPS * maxr);   // [nb][8]
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsc + nb * 8);
+    uint64_t* empty = full + nst;
+    uint64_t* sfull = empty + nst;    // [nb] s + descriptor of the item landed
+    uint64_t* sempty = sfull + nb;    // [nb] consumers done with the item's s
+    uint64_t* pdone = sempty + nb;    // [nb] consumers' partial rows final
+    uint64_t* pfree = pdone + nb;     // [nb] epilogue done with the partial rows
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
     if (threadIdx.x == 0) {
-        for (int i = 0; i < RING_NST; ++i) {
+        for (int i = 0; i < nst; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], SYMV_WARPS);                  // every consumer warp, every chunk
         }
-        for (int p = 0; p < 2; ++p) {
-            mbar_init(&sfull[p], 1);
-            mbar_init(&sempty[p], SYMV_WARPS);
-            mbar_init(&pdone[p], SYMV_WARPS * 32);
-            mbar_init(&pfree[p], 1);
+        for (int b = 0; b < nb; ++b) {
+            mbar_init(&sfull[b], 1);
+            mbar_init(&sempty[b], SYMV_WARPS);
+            mbar_init(&pdone[b], SYMV_WARPS * 32);
+            mbar_init(&pfree[b], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -889,30 +896,32 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
         if (lane != 0) return;
         DescPipe dp;
         dp.init(items, ops, i0, i1);
-        unsigned kc = 0;
-        for (int ii = i0, ki = 0; ii < i1; ++ii, ++ki) {
+        unsigned slot = 0, sph = 0;                                // ring slot and its fill count
+        int bi = 0;
+        unsigned bph = 0;                                          // item buffer and its use count
+        for (int ii = i0; ii < i1; ++ii) {
             ItemDesc it;
             OpDesc op;
             dp.next(items, ops, ii, i1, it, op);
-            const int p = ki & 1;
             const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
-            if (ki >= 2) mbar_wait(&sempty[p], ((ki >> 1) - 1) & 1);
-            int32_t* d = dsc + p * 8;
+            if (bph > 0) mbar_wait(&sempty[bi], (bph - 1) & 1);
+            int32_t* d = dsc + bi * 8;
             d[0] = it.I0; d[1] = it.I1; d[2] = it.J0; d[3] = it.J1; d[4] = it.tri; d[5] = it.ntiles;
-            mbar_expect_tx(&sfull[p], (unsigned)(rows_r + rows_c) * 8u);
+            mbar_expect_tx(&sfull[bi], (unsigned)(rows_r + rows_c) * 8u);
             const double* sop = s + op.s_off;
-            bulk_g2s(s_sm + p * RING_MAXR, sop + it.I0 * TILE, rows_r * 8u, &sfull[p]);
-            if (rows_c) bulk_g2s(s_sm + p * RING_MAXR + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[p]);
+            double* sb = s_sm + (size_t)bi * maxr;
+            bulk_g2s(sb, sop + it.I0 * TILE, rows_r * 8u, &sfull[bi]);
+            if (rows_c) bulk_g2s(sb + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[bi]);
+            if (++bi == nb) { bi = 0; ++bph; }
             // tile q of a chunk always lands at q * 8 KB of its slot; rectangular
             // items are contiguous full tiles (one copy per chunk), triangles
             // copy tile by tile (packed diagonal tiles are 4224 B)
             const double* src = tiles + it.tile_off;
             int rr = 0, cc = 0;                                     // triangle walk: row, col
-            for (int l0 = 0; l0 < it.ntiles; l0 += RING_TILES, ++kc) {
-                const unsigned slot = kc % RING_NST, nf = kc / RING_NST;
-                const int nt = min(RING_TILES, it.ntiles - l0);
-                if (nf > 0) mbar_wait(&empty[slot], (nf - 1) & 1);
-                double* dst = ring + (size_t)slot * RING_SLOT;
+            for (int l0 = 0; l0 < it.ntiles; l0 += RT) {
+                const int nt = min(RT, it.ntiles - l0);
+                if (sph > 0) mbar_wait(&empty[slot], (sph - 1) & 1);
+                double* dst = ring + (size_t)slot * SLOT;
                 if (!it.tri) {
                     mbar_expect_tx(&full[slot], (unsigned)nt * TILE_ELEMS * 8u);
                     bulk_g2s(dst, src, (unsigned)nt * TILE_ELEMS * 8u, &full[slot]);
@@ -932,40 +941,40 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
                         if (++cc > rr) { cc = 0; ++rr; }
                     }
                 }
+                if (++slot == (unsigned)nst) { slot = 0; ++sph; }
             }
         }
         return;
     }
-    if (warp == SYMV_WARPS + 1) {                                // ---- epilogue ----
-        DescPipe dp;
-        dp.init(items, ops, i0, i1);
-        for (int ii = i0, ki = 0; ii < i1; ++ii, ++ki) {
-            ItemDesc it;
-            OpDesc op;
-            dp.next(items, ops, ii, i1, it, op);
-            const int p = ki & 1;
+    if (warp > SYMV_WARPS) {                                     // ---- epilogue warps ----
+        const int e = warp - SYMV_WARPS - 1;                      // handles items ki = e, e+E, ...
+        for (int ii = i0 + e, ki = e; ii < i1; ii += RING_EPI_WARPS, ki += RING_EPI_WARPS) {
+            const ItemDesc it = items[ii];
+            const OpDesc op = ops[it.op];
+            const int b = ki % nb;
+            const unsigned ph = (unsigned)(ki / nb);
             const int rows_t = (it.I1 - it.I0 + (it.tri ? 0 : it.J1 - it.J0)) * TILE;
             const int g0 = it.I0 * TILE;
             const int nr = min(rows_t, op.m - g0);                // single-item ops only
             const bool scat = it.part_off < 0 && op.out_mode == 0;
-            int ix[RING_MAXR / 32];
-            double zv[RING_MAXR / 32];
+            int ix[RING_MAX_ROWS / 32];
+            double zv[RING_MAX_ROWS / 32];
             if (scat) {
                 const int32_t* idx = oidx + op.idx_off + g0;
 #pragma unroll
-                for (int r = 0; r < RING_MAXR / 32; ++r) ix[r] = (lane + 32 * r < nr) ? idx[lane + 32 * r] : 0;
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) ix[r] = (lane + 32 * r < nr) ? idx[lane + 32 * r] : 0;
 #pragma unroll
-                for (int r = 0; r < RING_MAXR / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
             }
-            mbar_wait(&pdone[p], (ki >> 1) & 1);
-            const double* pp = part + (size_t)p * SYMV_WARPS * RING_MAXR;
+            mbar_wait(&pdone[b], ph & 1);
+            const double* pp = part + (size_t)b * SYMV_WARPS * maxr;
 #pragma unroll
-            for (int r = 0; r < RING_MAXR / 32; ++r) {
+            for (int r = 0; r < RING_MAX_ROWS / 32; ++r) {
                 const int x = lane + 32 * r;
                 if (x < rows_t) {
                     double y = 0.0;
 #pragma unroll
-                    for (int ww = 0; ww < SYMV_WARPS; ++ww) y += pp[ww * RING_MAXR + x];
+                    for (int ww = 0; ww < SYMV_WARPS; ++ww) y += pp[ww * maxr + x];
                     if (it.part_off >= 0) partials[it.part_off + x] = y;
                     else if (x < nr) {
                         if (scat) z[ix[r]] = zv[r] + y;
@@ -974,22 +983,23 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&pfree[p]);
+            if (lane == 0) mbar_arrive(&pfree[b]);
         }
         return;
     }
     // ---- consumers (warps 0..7): each walks only its own tiles ----
-    unsigned kc = 0;                                               // first chunk of the item
+    unsigned slot = 0, sph = 0;
+    int bi = 0;
+    unsigned bph = 0;
     for (int ki = 0; ki < i1 - i0; ++ki) {
-        const int p = ki & 1;
-        mbar_wait(&sfull[p], (ki >> 1) & 1);
-        const int32_t* d = dsc + p * 8;
+        mbar_wait(&sfull[bi], bph & 1);
+        const int32_t* d = dsc + bi * 8;
         const int I0 = d[0], I1 = d[1], J0 = d[2], J1 = d[3], tri = d[4], ntiles = d[5];
-        const double* ss = s_sm + p * RING_MAXR;
+        const double* ss = s_sm + (size_t)bi * maxr;
         const int rows_r = (I1 - I0) * TILE;
         const int rows_t = rows_r + (tri ? 0 : (J1 - J0) * TILE);
-        double* pw = part + ((size_t)p * SYMV_WARPS + warp) * RING_MAXR;
-        if (ki >= 2) mbar_wait(&pfree[p], ((ki >> 1) - 1) & 1);
+        double* pw = part + ((size_t)bi * SYMV_WARPS + warp) * maxr;
+        if (bph > 0) mbar_wait(&pfree[bi], (bph - 1) & 1);
         for (int x = lane; x < rows_t; x += 32) pw[x] = 0.0;
         __syncwarp();
         double t[TILE];
@@ -1054,22 +1064,22 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
         };
         // every warp visits every chunk in order (keeps the mbarrier phases
         // of each slot in step), consuming only its own tiles
-        const int nch = (ntiles + RING_TILES - 1) / RING_TILES;
-        for (int ch = 0; ch < nch; ++ch, ++kc) {
-            const unsigned slot = kc % RING_NST;
-            mbar_wait(&full[slot], (kc / RING_NST) & 1);
-            const double* C = ring + (size_t)slot * RING_SLOT;
-            while (l >= 0 && l / RING_TILES == ch) {
-                tile(C + (l & (RING_TILES - 1)) * TILE_ELEMS, I, J);
+        for (int l0 = 0; l0 < ntiles; l0 += RT) {
+            mbar_wait(&full[slot], sph & 1);
+            const double* C = ring + (size_t)slot * SLOT;
+            while (l >= 0 && l < l0 + RT) {
+                tile(C + (l - l0) * TILE_ELEMS, I, J);
                 advance();
             }
             __syncwarp();                                          // every lane has consumed its rows
             if (lane == 0) mbar_arrive(&empty[slot]);
+            if (++slot == (unsigned)nst) { slot = 0; ++sph; }
         }
         if (curJ >= 0) flush_column(t, pw, tri ? (curJ - I0) * TILE : rows_r + (curJ - J0) * TILE, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[p]);
-        mbar_arrive(&pdone[p]);                                    // every lane (release its rows)
+        if (lane == 0) mbar_arrive(&sempty[bi]);
+        mbar_arrive(&pdone[bi]);                                   // every lane (release its rows)
+        if (++bi == nb) { bi = 0; ++bph; }
     }
 }
 
@@ -1605,16 +1615,47 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
                                                   partials, done, tickets, gather_mode, A, r);
 }
 
+static bool g_ring_init[64] = {};
+static int g_ring_rt = 4, g_ring_nb = 0;
+// per device, once, outside any stream capture (called from ddg_setup)
+void symv_ring_init() {
+    g_ring_rt = 4;
+    if (const char* e = getenv("DDG_RING_TILES")) g_ring_rt = atoi(e);
+    if (g_ring_rt != 1 && g_ring_rt != 2) g_ring_rt = 4;
+    g_ring_nb = 0;
+    if (const char* e = getenv("DDG_RING_NB")) g_ring_nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_ring_init[dev & 63]) return;
+    const size_t mx = 227 * 1024;
+    cudaFuncSetAttribute(k_symv_ring<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    g_ring_init[dev & 63] = true;
+}
+
 void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
-                      const int32_t* cta_part, int ncta, const double* tiles, const double* s,
+                      const int32_t* cta_part, int ncta, int max_rows_t, const double* tiles, const double* s,
                       const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done) {
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(k_symv_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
-        init = true;
-    }
-    k_symv_ring<<<ncta, RING_THREADS, RING_SMEM, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                       partials, done);
+    const int RT = g_ring_rt;
+    const int maxr = std::max(TILE, std::min(RING_MAX_ROWS, max_rows_t));
+    const size_t budget = 227 * 1024;
+    // item buffers: deep for small items (s copies and epilogues overlap
+    // several items), two for large ones; the rest of shared memory is ring
+    int nb = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 3 : 2);
+    while (nb > 2 && ring_smem(RT, 4, nb, maxr) > budget) --nb;
+    int nst = 2;
+    while (nst < RING_MAX_NST && ring_smem(RT, nst + 1, nb, maxr) <= budget) ++nst;
+    const size_t smem = ring_smem(RT, nst, nb, maxr);
+    if (RT == 1)
+        k_symv_ring<1><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
+                                                         partials, done, nst, nb, maxr);
+    else if (RT == 2)
+        k_symv_ring<2><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
+                                                         partials, done, nst, nb, maxr);
+    else
+        k_symv_ring<4><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
+                                                         partials, done, nst, nb, maxr);
 }
 
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,

@@ -820,6 +820,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
                        (long long)nc);
     }
     build_plans(c);
+    symv_ring_init();
     if (c->coarse_variant == 2) {
         if ((st = sparse_coarse_symbolic(c, row_ptr, col, er, ec, ev))) { free_ctx(c); return st; }
         tick("coarse symbolic (nested dissection)");
@@ -976,7 +977,7 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
         if (ring) {
             prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
                 launch_symv_ring(c->stream, c->d_ops, c->d_items, pl.item_begin, c->d_ring + pl.ring_off,
-                                 num_sms(), c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done);
+                                 num_sms(), pl.max_rows_t, c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done);
             });
             c->launches += 1;
             if (pl.red_end > pl.red_begin) {
@@ -1013,7 +1014,7 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
             c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
         } else if (ring_ok(c, c->coarse_ring_off)) {
             launch_symv_ring(c->stream, c->d_ops, c->d_items, c->coarse_item_begin, c->d_ring + c->coarse_ring_off,
-                             num_sms(), c->d_tiles, c->d_s, c->d_oidx, nullptr, c->d_yc, c->d_partials, done);
+                             num_sms(), c->coarse_rows_t, c->d_tiles, c->d_s, c->d_oidx, nullptr, c->d_yc, c->d_partials, done);
             c->launches += 1;
             if (c->coarse_red_end > c->coarse_red_begin) {
                 launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, c->coarse_red_begin,
