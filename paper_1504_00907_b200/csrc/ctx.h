@@ -135,7 +135,9 @@ struct ddg_ctx {
     int symv_mode = 0;                  // 0 ring, 1 classic per-item k_symv, 2 tma (experimental)
     std::vector<int32_t> h_ring;
     int32_t* d_ring = nullptr;
+    int32_t* d_gidx = nullptr;          // s position -> fine row (-1: padding)
     int coarse_ring_off = -1;
+    double ring_min_bytes = 16e6;       // launches moving less use the per-item k_symv
 };
 
 // append the CTA partition of items [b, e) for k_symv_ring; returns its offset

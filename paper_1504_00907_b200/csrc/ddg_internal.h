@@ -100,6 +100,8 @@ struct DevCSR {
     const int32_t* rp;   // int32 row offsets (nnz < 2^31 checked)
     const int32_t* col;
     const double* val;
+    int32_t sw;          // lanes per row in the row kernels (1, 4, 8 or 32; by mean row length)
+    int32_t pad;
 };
 
 struct ColourPlan {
@@ -131,13 +133,18 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
                         const double* partials, double* z, double* y_out, const int32_t* done);
+// s[x] = r[g] - (A z)[g] with g = gidx[x] (gidx < 0: padding, left untouched)
+// for x in [x0, x1): the residual restriction of a whole colour, flat over
+// the colour's contiguous s segments
+void launch_gather_flat(cudaStream_t st, int64_t x0, int64_t x1, const int32_t* gidx, DevCSR A, const double* r,
+                        const double* z, double* s, bool z_is_zero, const int32_t* done);
 void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                             const int32_t* cptr, const int64_t* qoff, const double* Q, DevCSR A,
                             const double* r, const double* z, double* bc, int maxmI,
                             const int32_t* done, const int32_t* parts = nullptr);
 void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                     const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc,
-                    double* z, const int32_t* done, const int32_t* parts = nullptr);
+                    double* z, int maxmI, const int32_t* done, const int32_t* parts = nullptr);
 void launch_fill(cudaStream_t st, double* x, int64_t n, double v, const int32_t* done);
 void launch_spmv(cudaStream_t st, DevCSR A, const double* x, double* y);
 

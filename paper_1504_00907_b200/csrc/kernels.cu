@@ -35,6 +35,22 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// (A x)[v] by SW lanes (an aligned group of the warp; sl = lane in group).
+// Every lane of the warp must call it (the group reduction shuffles); rows
+// with valid == false contribute 0.
+template <int SW>
+__device__ __forceinline__ double row_dot(const DevCSR& A, int64_t v, bool valid, const double* __restrict__ x,
+                                          int sl) {
+    double s = 0.0;
+    if (valid) {
+        const int e1 = A.rp[v + 1];
+        for (int e = A.rp[v] + sl; e < e1; e += SW) s += A.val[e] * x[A.col[e]];
+    }
+#pragma unroll
+    for (int o = SW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    return s;
+}
+
 // block-wide sum; result valid in every thread. blockDim.x multiple of 32, <= 1024
 __device__ double block_sum(double v) {
     __shared__ double ws[32];
@@ -182,17 +198,24 @@ __global__ void k_pcg_rz_first(const double* __restrict__ r, const double* __res
 }
 
 // q = A p ; sigma = p^T q ; alpha = rho / sigma
+template <int SW>
 __global__ void k_pcg_spmv_dot(DevCSR A, const double* __restrict__ p, double* __restrict__ q,
                                const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc, double* red,
                                unsigned* ticket, int dist) {
     if (sc->done) return;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = ROW(i);
-        double s = 0.0;
-        for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * p[A.col[e]];
-        q[v] = s;
-        acc += p[v] * s;
+    const int64_t ng = (int64_t)gridDim.x * blockDim.x / SW;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / SW;
+    const int sl = threadIdx.x % SW;
+    for (int64_t base = 0; base < nrows; base += ng) {
+        const int64_t i = base + g;
+        const bool ok = i < nrows;
+        const int64_t v = ok ? ROW(i) : 0;
+        const double s = row_dot<SW>(A, v, ok, p, sl);
+        if (ok && sl == 0) {
+            q[v] = s;
+            acc += p[v] * s;
+        }
     }
     grid_reduce(acc, red, ticket, [&](double s) {
         if (dist) { sc->loc[2] = s; return; }
@@ -329,6 +352,24 @@ k_gather(const OpDesc* __restrict__ ops, int sub_begin, int chunks, const int32_
             az = warp_sum(az);
             if (lane == 0) so[a] = r[v] - az;
         }
+    }
+}
+
+// flat residual restriction of one colour: x over its s segments
+template <int SW>
+__global__ void __launch_bounds__(256)
+k_gather_flat(int64_t x0, int64_t x1, const int32_t* __restrict__ gidx, DevCSR A, const double* __restrict__ r,
+              const double* __restrict__ z, double* __restrict__ s, int z_is_zero, const int32_t* done) {
+    if (*done) return;
+    const int64_t ng = (int64_t)gridDim.x * blockDim.x / SW;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / SW;
+    const int sl = threadIdx.x % SW;
+    for (int64_t base = x0; base < x1; base += ng) {
+        const int64_t x = base + g;
+        const int v = x < x1 ? gidx[x] : -1;
+        const bool ok = v >= 0;
+        const double az = z_is_zero ? 0.0 : row_dot<SW>(A, v, ok, z, sl);
+        if (ok && sl == 0) s[x] = r[v] - az;
     }
 }
 
@@ -1128,11 +1169,14 @@ __global__ void k_coarse_restrict(const int64_t* __restrict__ bptr, const int32_
     const int I = parts ? parts[blockIdx.x] : blockIdx.x;
     const int64_t b0 = bptr[I];
     const int mI = (int)(bptr[I + 1] - b0);
-    for (int a = threadIdx.x; a < mI; a += blockDim.x) {
-        const int v = bidx[b0 + a];
-        double az = 0.0;
-        for (int e = A.rp[v]; e < A.rp[v + 1]; e++) az += A.val[e] * z[A.col[e]];
-        res[a] = r[v] - az;
+    const int sw = A.sw >= 8 ? 8 : 1;                              // lanes per row
+    const int gpb = blockDim.x / sw, g = threadIdx.x / sw, sl = threadIdx.x % sw;
+    for (int base = 0; base < mI; base += gpb) {
+        const int a = base + g;
+        const bool ok = a < mI;
+        const int v = ok ? bidx[b0 + a] : 0;
+        const double az = sw == 8 ? row_dot<8>(A, v, ok, z, sl) : row_dot<1>(A, v, ok, z, sl);
+        if (ok && sl == 0) res[a] = r[v] - az;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1143,6 +1187,80 @@ __global__ void k_coarse_restrict(const int64_t* __restrict__ bptr, const int32_
         for (int a = lane; a < mI; a += 32) acc += QI[(int64_t)i * mI + a] * res[a];
         acc = warp_sum(acc);
         if (lane == 0) bc[cptr[I] + i] = acc;
+    }
+}
+
+// Warp per part (|Omega_I| <= 32 R, short rows): the residual rows live in
+// registers, each coarse column is one warp reduction.
+template <int R>
+__global__ void __launch_bounds__(256)
+k_restrict_warp(int nparts, const int64_t* __restrict__ bptr, const int32_t* __restrict__ bidx,
+                const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff, const double* __restrict__ Q,
+                DevCSR A, const double* __restrict__ r, const double* __restrict__ z, double* __restrict__ bc,
+                const int32_t* done, const int32_t* __restrict__ parts) {
+    if (*done) return;
+    const int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (wg >= nparts) return;                                     // whole warp
+    const int I = parts ? parts[wg] : wg;
+    const int64_t b0 = bptr[I];
+    const int mI = (int)(bptr[I + 1] - b0);
+    double res[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int a = lane + 32 * k;
+        res[k] = 0.0;
+        if (a < mI) {
+            const int v = bidx[b0 + a];
+            double az = 0.0;
+            for (int e = A.rp[v]; e < A.rp[v + 1]; e++) az += A.val[e] * z[A.col[e]];
+            res[k] = r[v] - az;
+        }
+    }
+    const int c0 = cptr[I], ncI = cptr[I + 1] - c0;
+    const double* QI = Q + qoff[I];
+    for (int i = 0; i < ncI; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int a = lane + 32 * k;
+            if (a < mI) acc += QI[(int64_t)i * mI + a] * res[k];
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) bc[c0 + i] = acc;
+    }
+}
+
+// z[Omega_I] += Q_I y_c[I,:], warp per part
+template <int R>
+__global__ void __launch_bounds__(256)
+k_prolong_warp(int nparts, const int64_t* __restrict__ bptr, const int32_t* __restrict__ bidx,
+               const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff, const double* __restrict__ Q,
+               const double* __restrict__ yc, double* __restrict__ z, const int32_t* done,
+               const int32_t* __restrict__ parts) {
+    if (*done) return;
+    const int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (wg >= nparts) return;
+    const int I = parts ? parts[wg] : wg;
+    const int64_t b0 = bptr[I];
+    const int mI = (int)(bptr[I + 1] - b0);
+    const int c0 = cptr[I], ncI = cptr[I + 1] - c0;
+    const double y0 = lane < ncI ? yc[c0 + lane] : 0.0, y1 = lane + 32 < ncI ? yc[c0 + 32 + lane] : 0.0;
+    const double* QI = Q + qoff[I];
+    double acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    for (int i = 0; i < ncI; ++i) {
+        const double yi = __shfl_sync(FULL, i < 32 ? y0 : y1, i & 31);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int a = lane + 32 * k;
+            if (a < mI) acc[k] += QI[(int64_t)i * mI + a] * yi;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int a = lane + 32 * k;
+        if (a < mI) z[bidx[b0 + a]] += acc[k];
     }
 }
 
@@ -1580,6 +1698,21 @@ void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, 
         k_gather<false><<<nsub * chunks, 256, 0, st>>>(ops, sub_begin, chunks, oidx, A, r, z, s, z_is_zero ? 1 : 0, done);
 }
 
+void launch_gather_flat(cudaStream_t st, int64_t x0, int64_t x1, const int32_t* gidx, DevCSR A, const double* r,
+                        const double* z, double* s, bool z_is_zero, const int32_t* done) {
+    if (x1 <= x0) return;
+    const int sw = z_is_zero ? 1 : std::max(1, A.sw);
+    const int64_t want = ((x1 - x0) * sw + 255) / 256;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * 8));
+    const int zz = z_is_zero ? 1 : 0;
+    switch (sw) {
+        case 4: k_gather_flat<4><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
+        case 8: k_gather_flat<8><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
+        case 32: k_gather_flat<32><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
+        default: k_gather_flat<1><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done);
+    }
+}
+
 static size_t symv_smem(int max_rows_t) {
     return (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
 }
@@ -1670,6 +1803,18 @@ void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, co
                             const double* r, const double* z, double* bc, int maxmI,
                             const int32_t* done, const int32_t* parts) {
     if (nparts <= 0) return;
+    if (A.sw <= 1 && maxmI <= 512) {
+        const int g = (nparts + 7) / 8;
+        if (maxmI <= 64)
+            k_restrict_warp<2><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, A, r, z, bc, done, parts);
+        else if (maxmI <= 128)
+            k_restrict_warp<4><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, A, r, z, bc, done, parts);
+        else if (maxmI <= 256)
+            k_restrict_warp<8><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, A, r, z, bc, done, parts);
+        else
+            k_restrict_warp<16><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, A, r, z, bc, done, parts);
+        return;
+    }
     const size_t smem = (size_t)maxmI * sizeof(double);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_coarse_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1678,9 +1823,21 @@ void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, co
 
 void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                     const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc,
-                    double* z, const int32_t* done, const int32_t* parts) {
+                    double* z, int maxmI, const int32_t* done, const int32_t* parts) {
     if (nparts <= 0) return;
-    k_prolong<<<nparts, 128, 0, st>>>(bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
+    if (maxmI <= 512) {
+        const int g = (nparts + 7) / 8;
+        if (maxmI <= 64)
+            k_prolong_warp<2><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
+        else if (maxmI <= 128)
+            k_prolong_warp<4><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
+        else if (maxmI <= 256)
+            k_prolong_warp<8><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
+        else
+            k_prolong_warp<16><<<g, 256, 0, st>>>(nparts, bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
+        return;
+    }
+    k_prolong<<<nparts, 256, 0, st>>>(bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
 }
 
 void launch_fill(cudaStream_t st, double* x, int64_t n, double v, const int32_t* done) {
@@ -1701,7 +1858,13 @@ void launch_pcg_rz_first(cudaStream_t st, const double* r, const double* z, doub
 }
 void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, const int32_t* rows,
                          int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist) {
-    k_pcg_spmv_dot<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist);
+    const int g = vec_grid(nrows * std::max(1, A.sw));
+    switch (A.sw) {
+        case 4: k_pcg_spmv_dot<4><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
+        case 8: k_pcg_spmv_dot<8><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
+        case 32: k_pcg_spmv_dot<32><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
+        default: k_pcg_spmv_dot<1><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist);
+    }
 }
 void launch_pcg_update(cudaStream_t st, const double* p, const double* q, double* u, double* r,
                        const int32_t* rows, int64_t nrows, Scalars* sc, double* hist, double* red,

@@ -167,7 +167,7 @@ static void free_ctx(ddg_ctx* c) {
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
                     c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
-                    c->d_ring};
+                    c->d_ring, c->d_gidx};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -513,6 +513,13 @@ int ring_partition(ddg_ctx* c, int b, int e) {
         c->h_ring.push_back(pick);
     }
     c->h_ring.push_back(e - b);
+    // small launches (C1, the upper coarse levels) stay on the per-item
+    // kernel: the persistent ring's fixed cost (148 CTAs, ~200 KB shared
+    // memory and barrier set-up each) outweighs its streaming advantage
+    if (pre.back() < c->ring_min_bytes) {
+        c->h_ring.resize(off);
+        return -1;
+    }
     return off;
 }
 bool ring_ok(const ddg_ctx* c, int off) { return c->symv_mode == 0 && off >= 0; }
@@ -811,6 +818,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     if (const char* e = getenv("DDG_FUSE_GATHER")) c->opts.fuse_gather = atoi(e);
     if (const char* e = getenv("DDG_SMALL_KERNEL")) c->opts.small_kernel = atoi(e);
     if (const char* e = getenv("DDG_SYMV")) c->symv_mode = e[0] == 'c' ? 1 : e[0] == 't' ? 2 : 0;
+    if (const char* e = getenv("DDG_RING_MIN_MB")) c->ring_min_bytes = atof(e) * 1e6;
     c->coarse_variant = c->opts.coarse_variant;
     if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
     if (c->coarse_variant == 1 && c->nc > 131072) {
@@ -836,7 +844,19 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         free_ctx(c);
         return st;
     }
-    c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val};
+    {
+        const double mean = (double)c->nnz / (double)std::max<int64_t>(1, n);
+        const int sw = mean <= 16 ? 1 : mean <= 48 ? 4 : mean <= 128 ? 8 : 32;
+        c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val, sw, 0};
+    }
+    {   // s position -> fine row (padding -1), for the flat colour gather
+        std::vector<int32_t> g(std::max<int64_t>(1, c->s_doubles), -1);
+        for (size_t q = 0; q < c->op_sub.size(); ++q) {
+            const OpDesc& op = c->ops[q];
+            for (int a = 0; a < op.m; ++a) g[op.s_off + a] = c->oidx[op.idx_off + a];
+        }
+        if ((st = upload(&c->d_gidx, g))) { free_ctx(c); return st; }
+    }
     if ((st = upload(&c->d_oidx, c->oidx)) || (st = upload(&c->d_ops, c->ops)) ||
         (st = upload(&c->d_items, c->items)) || (st = upload(&c->d_red, c->red)) ||
         (st = dalloc(&c->d_tiles, c->tiles_doubles)) || (st = dalloc(&c->d_s, c->s_doubles)) ||
@@ -969,8 +989,10 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
             gmode = z_zero ? 2 : 1;
         } else {
             prof(c, PC_GATHER, 0, [&] {
-                launch_gather(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin, pl.max_rows,
-                              c->nnz > 24 * c->n, c->d_oidx, c->A, r, z, c->d_s, z_zero, done);
+                const OpDesc& lo = c->ops[pl.sub_begin];
+                const OpDesc& hi = c->ops[pl.sub_end - 1];
+                launch_gather_flat(c->stream, lo.s_off, hi.s_off + hi.mp, c->d_gidx, c->A, r, z, c->d_s, z_zero,
+                                   done);
             });
             c->launches += 1;
         }
@@ -1028,7 +1050,7 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
                         c->d_yc, c->d_partials, done, c->coarse_rows_t, c->d_tickets);
             c->launches += 1;
         }
-        launch_prolong(c->stream, c->n_prolong, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc, z,
+        launch_prolong(c->stream, c->n_prolong, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc, z, c->maxmI,
                        done, c->d_prolong_parts);
     });
     c->launches += 2;
