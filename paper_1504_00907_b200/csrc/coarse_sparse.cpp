@@ -31,7 +31,7 @@
 namespace {
 
 constexpr int LEAF_UNKNOWNS = 256;
-constexpr int FRONT_BT = 8;
+int FRONT_BT = 8;   // tiles per item side of the front operators (DDG_FRONT_BT)
 
 struct NDNode {
     std::vector<int32_t> sep;  // blocks eliminated at this node
@@ -50,6 +50,13 @@ struct SparseCoarse {
     std::vector<int> g_begin, g_end, h_begin, h_end;
     std::vector<int> fwd_b, bwd_b;             // task ranges per level (size nlevels+1)
     std::vector<int> ring_fwd, ring_bwd;       // k_symv_ring partitions per level (-1: none)
+    // dataflow solve (k_coarse_dataflow): work queue, per-front schedule, state
+    std::vector<int32_t> dfwork;
+    std::vector<FrontDF> fdf;
+    int32_t *d_dfwork = nullptr, *d_dfstate = nullptr;
+    FrontDF* d_fdf = nullptr;
+    bool dataflow = true;
+    uint64_t* d_trace = nullptr;                // DDG_DF_TRACE: per-entry timestamps (debug)
     std::vector<FRedTask> fwd, bwd;
     std::vector<int64_t> contrib;
     std::vector<int32_t> item_front;           // item (relative to item_base) -> front
@@ -71,7 +78,8 @@ struct SparseCoarse {
 void sparse_coarse_free(SparseCoarse* s) {
     if (!s) return;
     void* p[] = {s->d_fr, s->d_fS, s->d_fB, s->d_fmap, s->d_item_front, s->d_fwd, s->d_bwd,
-                 s->d_contrib, s->d_fvec, s->d_w, s->d_ctiles, s->d_bc};
+                 s->d_contrib, s->d_fvec, s->d_w, s->d_ctiles, s->d_bc, s->d_dfwork, s->d_dfstate, s->d_fdf,
+                 s->d_trace};
     for (void* x : p)
         if (x) cudaFree(x);
     delete s;
@@ -229,6 +237,8 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     const int np = c->nparts;
     SparseCoarse* sc = new SparseCoarse();
     c->sparse = sc;
+    FRONT_BT = 8;
+    if (const char* e = getenv("DDG_FRONT_BT")) FRONT_BT = std::max(1, std::min(8, atoi(e)));
     // part adjacency
     std::vector<std::vector<int32_t>> adj(np);
     for (int I = 0; I < np; ++I) {
@@ -414,18 +424,35 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
         for (int j = 0; j < f.nB; ++j) pos[sc->fB[f.B_off + j]] = -1;
     }
     // solve operators: ops + items (per level: all G items, then all H items)
+    // Item block size per level: the largest of 8, 4, 2 tiles that still gives
+    // the level ~2 work items per SM (upper levels have few, large fronts; in
+    // the dataflow solve each item is one CTA on the critical path).
+    std::vector<int> lvl_bt(sc->nlevels, FRONT_BT);
+    if (!getenv("DDG_FRONT_BT")) {
+        std::vector<double> lvl_tiles(sc->nlevels, 0.0);
+        for (int i = 0; i < nn; ++i) {
+            const FrontDesc& f = sc->fr[i];
+            lvl_tiles[nodes[order[i]].height] += (double)f.nK * f.nT;   // S columns of the [S|B] front
+        }
+        for (int h = 0; h < sc->nlevels; ++h) {
+            int bt = 8;
+            while (bt > 2 && lvl_tiles[h] / ((double)bt * bt) < 2.0 * num_sms()) bt /= 2;
+            lvl_bt[h] = bt;
+        }
+    }
     std::vector<std::vector<int>> rowblk(nn);   // row-block starts (tiles) per front
     for (int i = 0; i < nn; ++i) {
         FrontDesc& f = sc->fr[i];
         auto& rb = rowblk[i];
-        for (int t0 = 0; t0 < f.nK; t0 += FRONT_BT) rb.push_back(t0);
-        for (int t0 = f.nK; t0 < f.nT; t0 += FRONT_BT) rb.push_back(t0);
+        const int bt = lvl_bt[nodes[order[i]].height];
+        for (int t0 = 0; t0 < f.nK; t0 += bt) rb.push_back(t0);
+        for (int t0 = f.nK; t0 < f.nT; t0 += bt) rb.push_back(t0);
         rb.push_back(f.nT);
         OpDesc op{};
         op.m = f.nS;
         op.mp = f.nT * TILE;
         op.nT = f.nT;
-        op.BT = FRONT_BT;
+        op.BT = bt;
         op.nblk = (int)rb.size() - 1;
         op.out_mode = 2;
         op.idx_off = -1;
@@ -486,6 +513,7 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     }
     sc->item_end = (int)c->items.size();
     // reduction tasks
+    sc->fdf.assign(nn, FrontDF{});
     sc->fwd_b.assign(sc->nlevels + 1, 0);
     sc->bwd_b.assign(sc->nlevels + 1, 0);
     for (int h = 0; h < sc->nlevels; ++h) {
@@ -495,6 +523,8 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
             const auto& rb = rowblk[i];
             const int nb = (int)rb.size() - 1, ns = nblkS(i);
             auto idx = [&](int bi, int bj) { return item_of[i][bi * nb + bj]; };
+            sc->fdf[i].ft0 = (int)sc->fwd.size();
+            sc->fdf[i].bt0 = (int)sc->bwd.size();
             for (int bi = ns; bi < nb; ++bi) {       // forward: rows in B
                 FRedTask t{i, 0, rb[bi] * TILE, (rb[bi + 1] - rb[bi]) * TILE, (int)sc->contrib.size(), 0};
                 for (int bj = 0; bj < ns; ++bj) sc->contrib.push_back(c->items[idx(bi, bj)].part_off);
@@ -511,11 +541,39 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
                 t.cend = (int)sc->contrib.size();
                 sc->bwd.push_back(t);
             }
+            sc->fdf[i].ft1 = (int)sc->fwd.size();
+            sc->fdf[i].bt1 = (int)sc->bwd.size();
         }
     }
     sc->fwd_b[sc->nlevels] = (int)sc->fwd.size();
     sc->bwd_b[sc->nlevels] = (int)sc->bwd.size();
     sc->factor_bytes = sc->ctile_doubles * 8;
+    // dataflow work queue: leaf assemblies, forward G items leaves -> root,
+    // backward G + H items root -> leaves
+    for (int h = 0; h < sc->nlevels; ++h)
+        for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q) {
+            FrontDF& d = sc->fdf[sc->item_front[q - sc->item_base]];
+            if (q < sc->g_end[h]) ++d.nG;
+            ++d.nGH;
+        }
+    sc->dfwork.clear();
+    for (int i = 0; i < nn; ++i)
+        if (sc->fr[i].child0 < 0 && sc->fr[i].child1 < 0) sc->dfwork.push_back(DF_ASSEMBLE | i);
+    for (int h = 0; h < sc->nlevels; ++h) {
+        for (int q = sc->g_begin[h]; q < sc->g_end[h]; ++q) sc->dfwork.push_back(q);
+        for (int k = sc->fwd_b[h]; k < sc->fwd_b[h + 1]; ++k) sc->dfwork.push_back(DF_RED | k);
+    }
+    for (int h = sc->nlevels - 1; h >= 0; --h) {
+        for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q) sc->dfwork.push_back(DF_BWD | q);
+        for (int k = sc->bwd_b[h]; k < sc->bwd_b[h + 1]; ++k) sc->dfwork.push_back(DF_BWD | DF_RED | k);
+    }
+    if ((int64_t)c->items.size() >= DF_RED || (int64_t)sc->fwd.size() >= DF_RED || (int64_t)sc->bwd.size() >= DF_RED)
+        sc->dataflow = false;   // entry indices must fit below the flag bits
+    if (const char* e = getenv("DDG_COARSE_DATAFLOW")) sc->dataflow = atoi(e) != 0;
+    if (getenv("DDG_DF_TRACE")) {
+        if (cudaMalloc(&sc->d_trace, sc->dfwork.size() * 4 * sizeof(uint64_t)) != cudaSuccess) sc->d_trace = nullptr;
+        else cudaMemset(sc->d_trace, 0, sc->dfwork.size() * 4 * sizeof(uint64_t));
+    }
     sc->ring_fwd.assign(sc->nlevels, -1);
     sc->ring_bwd.assign(sc->nlevels, -1);
     for (int h = 0; h < sc->nlevels; ++h) {
@@ -542,7 +600,10 @@ int sparse_coarse_numeric(ddg_ctx* c) {
     if ((st = up(&sc->d_fr, sc->fr)) || (st = up(&sc->d_fS, sc->fS)) || (st = up(&sc->d_fB, sc->fB)) ||
         (st = up(&sc->d_fmap, sc->fmap)) || (st = up(&sc->d_item_front, sc->item_front)) ||
         (st = up(&sc->d_fwd, sc->fwd)) || (st = up(&sc->d_bwd, sc->bwd)) ||
-        (st = up(&sc->d_contrib, sc->contrib)) || (st = dalloc(&sc->d_fvec, sc->fvec_doubles)) ||
+        (st = up(&sc->d_contrib, sc->contrib)) || (st = up(&sc->d_dfwork, sc->dfwork)) ||
+        (st = up(&sc->d_fdf, sc->fdf)) ||
+        (st = dalloc(&sc->d_dfstate, 1 + (size_t)DF_STATE_PER_FRONT * sc->nfront)) ||
+        (st = dalloc(&sc->d_fvec, sc->fvec_doubles)) ||
         (st = dalloc(&sc->d_w, sc->w_doubles)) || (st = dalloc(&sc->d_ctiles, sc->ctile_doubles)) ||
         (st = dalloc(&sc->d_bc, c->nc)))
         return st;
@@ -610,11 +671,11 @@ int sparse_coarse_numeric(ddg_ctx* c) {
             for (int i = f0; i < f1; ++i) {
                 const FrontDesc& f = sc->fr[i];
                 const int64_t ne = (int64_t)f.nT * f.nT * TILE_ELEMS;
-                std::vector<double> h(ne);
-                { int _s = d2h(c->stream, h.data(), fptr[i], ne * 8); if (_s) return _s; }
+                std::vector<double> hv(ne);
+                { int _s = d2h(c->stream, hv.data(), fptr[i], ne * 8); if (_s) return _s; }
                 const int N = f.nT * TILE;
                 auto at = [&](int R, int Cc) {
-                    return h[((int64_t)(Cc / TILE) * f.nT + R / TILE) * TILE_ELEMS + (Cc % TILE) * TILE + R % TILE];
+                    return hv[((int64_t)(Cc / TILE) * f.nT + R / TILE) * TILE_ELEMS + (Cc % TILE) * TILE + R % TILE];
                 };
                 double cs = 0, asym = 0, dmin = 1e300;
                 for (int R = 0; R < N; ++R)
@@ -711,6 +772,15 @@ int sparse_coarse_nfront(ddg_ctx* c) { return c->sparse ? c->sparse->nfront : 0;
 int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
     SparseCoarse* sc = c->sparse;
     int launches = 0;
+    if (sc->dataflow) {
+        cudaMemsetAsync(sc->d_dfstate, 0, (1 + (size_t)DF_STATE_PER_FRONT * sc->nfront) * sizeof(int32_t),
+                        c->stream);
+        launch_coarse_dataflow(c->stream, (int)sc->dfwork.size(), sc->d_dfwork, sc->d_fr, sc->d_fdf,
+                               sc->d_item_front, sc->item_base, c->d_ops, c->d_items, sc->d_ctiles, sc->d_fwd,
+                               sc->d_bwd, sc->d_contrib, sc->d_fS, sc->d_fB, sc->d_fmap, sc->d_bc, sc->d_fvec,
+                               sc->d_w, d_x, c->d_partials, sc->d_dfstate, sc->max_rows_t, done, sc->d_trace);
+        return 1;
+    }
     for (int h = 0; h < sc->nlevels; ++h) {
         const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
         launch_front_fwd_assemble(c->stream, f0, nf, sc->d_fr, sc->d_fS, sc->d_fmap, sc->d_bc, sc->d_fvec,
@@ -741,4 +811,18 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         launches += 3;
     }
     return launches;
+}
+
+// debug (not part of include/ddg.h): the dataflow trace of the last coarse
+// solve -- per work entry {start | cta << 52, dependency met, item done,
+// entry finished} in ns -- and the work entries; returns the entry count
+extern "C" int ddg_debug_df_trace(ddg_ctx* c, uint64_t* trace, int32_t* work, int cap) {
+    if (!c || !c->sparse || !c->sparse->d_trace) return -1;
+    SparseCoarse* sc = c->sparse;
+    const int n = (int)sc->dfwork.size();
+    if (cap < n) return -n;
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(trace, sc->d_trace, (size_t)n * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    memcpy(work, sc->dfwork.data(), (size_t)n * sizeof(int32_t));
+    return n;
 }

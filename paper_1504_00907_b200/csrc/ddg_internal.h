@@ -79,6 +79,22 @@ struct FRedTask {
     int32_t cbeg, cend;      // contributions [cbeg, cend) in the contrib offset list
 };
 
+// Per-front schedule of the dataflow coarse solve (k_coarse_dataflow).
+struct FrontDF {
+    int32_t nG, nGH;          // forward (G) and backward (G + H) work items of the front
+    int32_t ft0, ft1;         // its forward reduction tasks [ft0, ft1)
+    int32_t bt0, bt1;         // its backward reduction tasks [bt0, bt1)
+};
+// work-queue entry of the dataflow coarse solve
+constexpr int32_t DF_BWD = 1 << 30;       // backward entry (else forward)
+constexpr int32_t DF_ASSEMBLE = 1 << 29;  // assemble a leaf front (low bits: front)
+constexpr int32_t DF_RED = 1 << 28;       // a reduction task (low bits: task index)
+constexpr int32_t DF_IDX = DF_RED - 1;
+// device state, zeroed before every solve: [0] queue head, then per front
+// fwd_ready, fwd_items_done, fwd_tasks_done, children_done, bwd_ready,
+// bwd_items_done, bwd_tasks_done
+constexpr int DF_STATE_PER_FRONT = 7;
+
 // Device-side PCG scalars (one struct in device memory).
 struct Scalars {
     double rho, sigma, alpha, beta, gamma;
@@ -196,6 +212,13 @@ void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* f
 void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,
                          const FrontDesc* fronts, const int32_t* fS, const double* partials, double* w,
                          double* x, const int32_t* done);
+// whole sparse coarse solve y = A_c^{-1} b_c in one launch (see kernels.cu)
+void launch_coarse_dataflow(cudaStream_t st, int nwork, const int32_t* work, const FrontDesc* fronts,
+                            const FrontDF* fdf, const int32_t* item_front, int item_base, const OpDesc* ops,
+                            const ItemDesc* items, const double* ctiles, const FRedTask* fwd, const FRedTask* bwd,
+                            const int64_t* contrib, const int32_t* fS, const int32_t* fB, const int32_t* map,
+                            const double* bc, double* fvec, double* w, double* x, double* partials,
+                            int32_t* state, int max_rows_t, const int32_t* done, uint64_t* trace = nullptr);
 void launch_scatter_coarse(cudaStream_t st, int64_t nent, const int32_t* row, const int32_t* col,
                            const double* val, int nT, int n_c, double* M);
 void launch_pack(cudaStream_t st, int nops, const int32_t* op_ids, const OpDesc* ops,
