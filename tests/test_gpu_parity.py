@@ -234,3 +234,58 @@ def test_comm_path_single_rank(name):
     assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
     s.close()
     comm.close()
+
+
+# ---------------------------------------------------------------- kernel paths
+# The small parity cases fall below the persistent ring's size threshold, so
+# each path is also forced explicitly (switches are read at ddg_setup).
+PATHS = {
+    "ring_everywhere": {"DDG_RING_MIN_MB": "0"},                 # k_symv_ring for every SYMV launch
+    "ring_2tile_slots": {"DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2"},
+    "classic": {"DDG_SYMV": "classic"},                           # per-item k_symv / k_symv_small
+    "coarse_levels": {"DDG_COARSE_DATAFLOW": "0", "DDG_RING_MIN_MB": "0"},  # level-by-level sparse solve
+}
+PATH_CASES = ["C1", "poisson3d_24_b8_p2", "lognormal_16_b4", "elasticity_8_be4", "biharm_64_b16_p3",
+              "poisson2d_ragged"]
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+@pytest.mark.parametrize("name", PATH_CASES)
+def test_kernel_paths_parity(name, path, monkeypatch):
+    for k, v in PATHS[path].items():
+        monkeypatch.setenv(k, v)
+    compare_solve(CASES[name]())
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+@pytest.mark.parametrize("name", ["lognormal_32_b4", "biharm_128_b16_p3", "elasticity_12_be4"])
+def test_kernel_paths_sparse_coarse(name, path, monkeypatch):
+    """sparse coarse solve (dataflow by default, levels when switched) under every SYMV path"""
+    for k, v in PATHS[path].items():
+        monkeypatch.setenv(k, v)
+    pr = SPARSE_CASES[name]()
+    from paper_1504_00907_b200 import Solver
+    s = Solver.from_problem(pr, coarse_variant=2)
+    o = oracle.Oracle.from_problem(pr)
+    r = np.random.default_rng(5).standard_normal(pr.n)
+    tol = 1e-9 if "biharm" in name else 1e-12
+    zc, zo = s.coarse_correct(r), o.coarse_correct(r)
+    assert np.linalg.norm(zc - zo) <= tol * np.linalg.norm(zo)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    uo, ito, histo, conv = o.pcg(pr.f, 1e-8)
+    assert rep.converged and abs(it - ito) <= 1
+    m = min(len(hist), len(histo))
+    assert np.max(np.abs(hist[:m] - histo[:m]) / histo[:m]) <= H_TOL
+    assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+
+
+def test_ring_bitwise_repeatable(monkeypatch):
+    """k_symv_ring and the dataflow coarse solve are deterministic (fixed
+    reduction orders, no floating-point atomics)."""
+    monkeypatch.setenv("DDG_RING_MIN_MB", "0")
+    pr = P.lognormal3d(32, 4, 1, 23)
+    from paper_1504_00907_b200 import Solver
+    s = Solver.from_problem(pr, coarse_variant=2)
+    u1, it1, h1, _ = s.solve(pr.f)
+    u2, it2, h2, _ = s.solve(pr.f)
+    assert it1 == it2 and np.array_equal(u1, u2) and np.array_equal(h1, h2)
