@@ -42,6 +42,9 @@ class Problem:
     f: np.ndarray              # float64 [n]
     overlap: int = 1
     meta: dict = dataclasses.field(default_factory=dict)
+    # structured-grid description of A for the library's matrix-free row
+    # kernels (include/ddg.h ddg_stencil); the CSR above stays the definition
+    stencil: dict = None
 
     @property
     def k(self) -> int:
@@ -184,8 +187,9 @@ def poisson2d(N=64, b=8, p=1, seed=1001, overlap=1):
     rp, c, v = stencil_csr((N, N), offs, lambda k, m: np.full(m.shape, 4.0 if k == 0 else -1.0))
     h = 1.0 / (N + 1)
     coords = grid_coords((N, N), 1.0, h)
-    return _finish("poisson2d", (N, N), rp, c, v, coords, p, (b, b), seed, overlap,
-                   dict(stencil="5pt"))
+    pr = _finish("poisson2d", (N, N), rp, c, v, coords, p, (b, b), seed, overlap, dict(stencil="5pt"))
+    pr.stencil = dict(kind="const", dims=(N, N, 1), offsets=offs, coef=[4.0, -1, -1, -1, -1])
+    return pr
 
 
 def poisson3d(N=128, b=8, p=2, seed=1002, overlap=1):
@@ -194,8 +198,9 @@ def poisson3d(N=128, b=8, p=2, seed=1002, overlap=1):
     rp, c, v = stencil_csr((N, N, N), offs, lambda k, m: np.full(m.shape, 6.0 if k == 0 else -1.0))
     h = 1.0 / (N + 1)
     coords = grid_coords((N, N, N), 1.0, h)
-    return _finish("poisson3d", (N, N, N), rp, c, v, coords, p, (b, b, b), seed, overlap,
-                   dict(stencil="7pt"))
+    pr = _finish("poisson3d", (N, N, N), rp, c, v, coords, p, (b, b, b), seed, overlap, dict(stencil="7pt"))
+    pr.stencil = dict(kind="const", dims=(N, N, N), offsets=offs, coef=[6.0, -1, -1, -1, -1, -1, -1])
+    return pr
 
 
 def lognormal3d(N=256, b=4, p=1, seed=1003, overlap=1):
@@ -226,8 +231,12 @@ def lognormal3d(N=256, b=4, p=1, seed=1003, overlap=1):
     rp, c, v = stencil_csr(dims, offs, coef)
     h = 1.0 / N
     coords = grid_coords(dims, 0.5, h)                  # cell centres
-    return _finish("lognormal3d", dims, rp, c, v, coords, p, (b, b, b), seed, overlap,
-                   dict(stencil="7pt_harmonic"))
+    pr = _finish("lognormal3d", dims, rp, c, v, coords, p, (b, b, b), seed, overlap,
+                 dict(stencil="7pt_harmonic"))
+    # couplings towards +x, +y, +z (T[0], T[2], T[4]); the -x/-y/-z entries are
+    # the same faces seen from the neighbour (the harmonic mean is symmetric)
+    pr.stencil = dict(kind="face7", dims=dims, coef=np.concatenate([diag, -T[0], -T[2], -T[4]]))
+    return pr
 
 
 def biharmonic2d(N=2048, b=16, p=3, seed=1005, overlap=1):
@@ -239,8 +248,9 @@ def biharmonic2d(N=2048, b=16, p=3, seed=1005, overlap=1):
     rp, c, v = stencil_csr((N, N), offs, lambda k, m: np.full(m.shape, float(cf[k])))
     h = 1.0 / (N + 1)
     coords = grid_coords((N, N), 1.0, h)
-    return _finish("biharmonic2d", (N, N), rp, c, v, coords, p, (b, b), seed, overlap,
-                   dict(stencil="13pt"))
+    pr = _finish("biharmonic2d", (N, N), rp, c, v, coords, p, (b, b), seed, overlap, dict(stencil="13pt"))
+    pr.stencil = dict(kind="const", dims=(N, N, 1), offsets=offs, coef=cf)
+    return pr
 
 
 # --- C4: Q1 elasticity -------------------------------------------------------

@@ -56,6 +56,30 @@ enum { DDG_STOP_RES0 = 0,      /* ||r_k||_2 <= rtol ||r_0||_2 (default)         
        DDG_STOP_RES1 = 1,      /* ||r_k||_2 <= rtol ||r_1||_2           */
        DDG_STOP_PREC = 2 };    /* sqrt(r_k^T z_k) <= rtol sqrt(r_0^T z_0)             */
 
+/* Optional structured-grid description of A (SURVEY.md §8(b) "ddg_stencil"),
+ * used matrix-free by the hot-path row kernels (the SpMV q = A p, the residual
+ * restrictions s = R~_i (r - A z) and b_c = P^T (r - A z)) instead of reading
+ * the CSR.  The CSR passed to ddg_setup stays the definition of A: ddg_setup
+ * checks that the stencil reproduces every entry of every row exactly and
+ * fails with DDG_E_ARG otherwise.  Rows are the grid points, row index
+ * v = x + dims[0] * (y + dims[1] * z); neighbours off the grid are absent
+ * (zero Dirichlet values / zero ghosts: BASELINE configs C1, C2, C3, C5).
+ * All pointers are host pointers, borrowed for the duration of ddg_setup. */
+enum { DDG_STENCIL_NONE = 0,
+       DDG_STENCIL_CONST = 1,   /* constant coefficients: npts points (dx, dy, dz) with values coef */
+       DDG_STENCIL_FACE7 = 2 }; /* 7-point with per-row coefficients: coef = 4 x n, blocks
+                                   diag | cx | cy | cz with cx[v] = A[v, v+1],
+                                   cy[v] = A[v, v+dims[0]], cz[v] = A[v, v+dims[0]*dims[1]]
+                                   (A symmetric: A[v, v-1] = cx[v-1], ...)                     */
+enum { DDG_STENCIL_MAX_PTS = 16 };
+typedef struct {
+    int32_t kind;              /* DDG_STENCIL_*                                                 */
+    int32_t dims[3];           /* grid points per axis (1 for unused axes)                      */
+    int32_t npts;              /* CONST: number of points, <= DDG_STENCIL_MAX_PTS               */
+    const int32_t* offsets;    /* CONST: npts x 3 offsets (dx, dy, dz)                          */
+    const double* coef;        /* CONST: npts values; FACE7: 4 n values                         */
+} ddg_stencil;
+
 typedef struct {
     int overlap;          /* Delta: graph distance in the pattern of A. default 1 */
     double rank_tol;      /* keep column j of a part iff |R_jj| >= rank_tol * max_j ||F_I e_j||
@@ -78,6 +102,7 @@ typedef struct {
     const int32_t* block_coords; /* optional nparts x block_ndim integer coordinates of the parts
                              (host, borrowed): geometric nested dissection of the coarse graph;
                              NULL: BFS level-set bisection                                       */
+    const ddg_stencil* stencil;  /* optional matrix-free description of A (above), or NULL       */
 } ddg_opts;
 
 typedef struct {

@@ -136,6 +136,7 @@ struct ddg_ctx {
     std::vector<int32_t> h_ring;
     int32_t* d_ring = nullptr;
     int32_t* d_gidx = nullptr;          // s position -> fine row (-1: padding)
+    double* d_stencil_coef = nullptr;   // ddg_stencil FACE7 coefficients (device)
     int coarse_ring_off = -1;
     double ring_min_bytes = 16e6;       // launches moving less use the per-item k_symv
 };

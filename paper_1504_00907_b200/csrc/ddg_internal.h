@@ -110,6 +110,20 @@ struct Scalars {
 constexpr int RED_BLOCKS = 148 * 4;
 constexpr int VEC_THREADS = 256;
 
+// Matrix-free description of A for the hot-path row kernels (include/ddg.h
+// ddg_stencil), validated against the CSR at setup.  CONST points are sorted
+// by linear offset, i.e. in the CSR's column order, and FACE7 rows are
+// evaluated in that order too, so stencil and CSR rows round identically.
+constexpr int STENCIL_MAX_PTS = 16;
+struct DevStencil {
+    int32_t kind;        // 0 none (CSR), 1 constant, 2 face7
+    int32_t npts;
+    int32_t nx, ny, nz, pad;
+    int32_t dx[STENCIL_MAX_PTS], dy[STENCIL_MAX_PTS], dz[STENCIL_MAX_PTS];
+    double c[STENCIL_MAX_PTS];
+    const double* coef;  // face7: diag | cx | cy | cz, 4 n doubles (device)
+};
+
 struct DevCSR {
     int64_t n;
     int64_t nnz;
@@ -118,6 +132,7 @@ struct DevCSR {
     const double* val;
     int32_t sw;          // lanes per row in the row kernels (1, 4, 8 or 32; by mean row length)
     int32_t pad;
+    DevStencil st;       // st.kind != 0: rows evaluated matrix-free (sw = 1)
 };
 
 struct ColourPlan {

@@ -35,6 +35,46 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// (A x)[v] from the stencil, in the CSR's column order (see DevStencil)
+__device__ __forceinline__ double stencil_dot(const DevStencil& st, int64_t v, const double* __restrict__ x) {
+    const int nx = st.nx, ny = st.ny;
+    const int ix = (int)(v % nx);
+    const int64_t r = v / nx;
+    const int iy = (int)(r % ny), iz = (int)(r / ny);
+    double s = 0.0;
+    if (st.kind == 1) {
+#pragma unroll
+        for (int k = 0; k < STENCIL_MAX_PTS; ++k) {
+            if (k >= st.npts) break;
+            const int a = ix + st.dx[k], b = iy + st.dy[k], c = iz + st.dz[k];
+            if (a >= 0 && a < nx && b >= 0 && b < ny && c >= 0 && c < st.nz)
+                s = fma(st.c[k], x[v + st.dx[k] + (int64_t)nx * (st.dy[k] + (int64_t)ny * st.dz[k])], s);
+        }
+        return s;
+    }
+    const int64_t n = (int64_t)nx * ny * st.nz, sy = nx, sz = (int64_t)nx * ny;
+    const double* D = st.coef;
+    const double* CX = D + n;
+    const double* CY = CX + n;
+    const double* CZ = CY + n;
+    if (iz > 0) s = fma(CZ[v - sz], x[v - sz], s);
+    if (iy > 0) s = fma(CY[v - sy], x[v - sy], s);
+    if (ix > 0) s = fma(CX[v - 1], x[v - 1], s);
+    s = fma(D[v], x[v], s);
+    if (ix + 1 < nx) s = fma(CX[v], x[v + 1], s);
+    if (iy + 1 < ny) s = fma(CY[v], x[v + sy], s);
+    if (iz + 1 < st.nz) s = fma(CZ[v], x[v + sz], s);
+    return s;
+}
+
+// (A x)[v] by one thread: stencil or CSR row
+__device__ __forceinline__ double row_dot1(const DevCSR& A, int64_t v, const double* __restrict__ x) {
+    if (A.st.kind) return stencil_dot(A.st, v, x);
+    double s = 0.0;
+    for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * x[A.col[e]];
+    return s;
+}
+
 // (A x)[v] by SW lanes (an aligned group of the warp; sl = lane in group).
 // Every lane of the warp must call it (the group reduction shuffles); rows
 // with valid == false contribute 0.
@@ -42,6 +82,7 @@ template <int SW>
 __device__ __forceinline__ double row_dot(const DevCSR& A, int64_t v, bool valid, const double* __restrict__ x,
                                           int sl) {
     double s = 0.0;
+    if (SW == 1) return valid ? row_dot1(A, v, x) : 0.0;
     if (valid) {
         const int e1 = A.rp[v + 1];
         for (int e = A.rp[v] + sl; e < e1; e += SW) s += A.val[e] * x[A.col[e]];
@@ -309,9 +350,7 @@ __global__ void k_fill(double* x, int64_t n, double v, const int32_t* done) {
 __global__ void k_spmv(DevCSR A, const double* __restrict__ x, double* __restrict__ y) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int e = A.rp[i]; e < A.rp[i + 1]; e++) s += A.val[e] * x[A.col[e]];
-        y[i] = s;
+        y[i] = row_dot1(A, i, x);
     }
 }
 
@@ -339,7 +378,7 @@ k_gather(const OpDesc* __restrict__ ops, int sub_begin, int chunks, const int32_
         const int v = idx[a];
         double az = 0.0;
         if (!z_is_zero)
-            for (int e = A.rp[v]; e < A.rp[v + 1]; e++) az += A.val[e] * z[A.col[e]];
+            az = row_dot1(A, v, z);
         so[a] = r[v] - az;
     } else {
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -461,7 +500,7 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
                 const int node = idx[x];
                 double az = 0.0;
                 if (gather_mode == 1)
-                    for (int e = A.rp[node]; e < A.rp[node + 1]; e++) az += A.val[e] * z[A.col[e]];
+                    az = row_dot1(A, node, z);
                 v = rvec[node] - az;
             }
             s_sm[x] = v;
@@ -601,7 +640,7 @@ k_symv_small(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
                 const int node = idx[x];
                 double az = 0.0;
                 if (gather_mode == 1)
-                    for (int e = A.rp[node]; e < A.rp[node + 1]; e++) az += A.val[e] * z[A.col[e]];
+                    az = row_dot1(A, node, z);
                 v = rvec[node] - az;
             } else {
                 v = s[op.s_off + x];
@@ -728,7 +767,7 @@ k_symv_tma(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, i
                     const int node = idx[x];
                     double az = 0.0;
                     if (gather_mode == 1)
-                        for (int e = A.rp[node]; e < A.rp[node + 1]; e++) az += A.val[e] * z[A.col[e]];
+                        az = row_dot1(A, node, z);
                     v = rvec[node] - az;
                 }
                 s_sm[x] = v;
@@ -1212,7 +1251,7 @@ k_restrict_warp(int nparts, const int64_t* __restrict__ bptr, const int32_t* __r
         if (a < mI) {
             const int v = bidx[b0 + a];
             double az = 0.0;
-            for (int e = A.rp[v]; e < A.rp[v + 1]; e++) az += A.val[e] * z[A.col[e]];
+            az = row_dot1(A, v, z);
             res[k] = r[v] - az;
         }
     }

@@ -20,6 +20,7 @@
 #include <atomic>
 #include <chrono>
 #include <functional>
+#include <numeric>
 #include <string>
 #include <thread>
 #include <vector>
@@ -167,7 +168,7 @@ static void free_ctx(ddg_ctx* c) {
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
                     c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
-                    c->d_ring, c->d_gidx};
+                    c->d_ring, c->d_gidx, c->d_stencil_coef};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -485,6 +486,86 @@ static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool al
         for (int b = 0; b < op.nblk; ++b) c->red.push_back(RedDesc{opi, b});
     c->s_doubles += op.mp;
     c->ops.push_back(op);
+}
+
+// ddg_stencil (include/ddg.h): check that it reproduces every CSR row exactly
+// and build the device description (CONST points sorted into column order).
+static int build_stencil(ddg_ctx* c, const ddg_stencil* S, int64_t n, const int64_t* rp, const int32_t* col,
+                         const double* val, DevStencil& D, std::vector<double>& coef) {
+    D = DevStencil{};
+    if (!S || S->kind == DDG_STENCIL_NONE) return DDG_OK;
+    const int64_t nx = S->dims[0], ny = S->dims[1], nz = S->dims[2];
+    if (nx < 1 || ny < 1 || nz < 1 || nx * ny * nz != n)
+        return set_err(DDG_E_ARG, "stencil dims %lld x %lld x %lld do not match n = %lld", (long long)nx,
+                       (long long)ny, (long long)nz, (long long)n);
+    D.nx = (int32_t)nx;
+    D.ny = (int32_t)ny;
+    D.nz = (int32_t)nz;
+    std::vector<int> ord;
+    if (S->kind == DDG_STENCIL_CONST) {
+        if (S->npts < 1 || S->npts > STENCIL_MAX_PTS || !S->offsets || !S->coef)
+            return set_err(DDG_E_ARG, "stencil: npts = %d (1..%d) and offsets/coef required", S->npts,
+                           STENCIL_MAX_PTS);
+        D.kind = 1;
+        D.npts = S->npts;
+        ord.resize(S->npts);
+        std::iota(ord.begin(), ord.end(), 0);
+        auto lin = [&](int k) {
+            return S->offsets[3 * k] + nx * (S->offsets[3 * k + 1] + ny * (int64_t)S->offsets[3 * k + 2]);
+        };
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lin(a) < lin(b); });
+        for (int q = 0; q < S->npts; ++q) {
+            const int k = ord[q];
+            D.dx[q] = S->offsets[3 * k];
+            D.dy[q] = S->offsets[3 * k + 1];
+            D.dz[q] = S->offsets[3 * k + 2];
+            D.c[q] = S->coef[k];
+        }
+    } else if (S->kind == DDG_STENCIL_FACE7) {
+        if (!S->coef) return set_err(DDG_E_ARG, "stencil: coef (4 n values) required");
+        D.kind = 2;
+        coef.assign(S->coef, S->coef + 4 * n);
+    } else {
+        return set_err(DDG_E_ARG, "stencil: unknown kind %d", S->kind);
+    }
+    // exact reproduction of the CSR, row by row
+    std::atomic<int64_t> bad{-1};
+    parallel_for(n, [&](int64_t b, int64_t e, int) {
+        std::vector<std::pair<int64_t, double>> ent;
+        for (int64_t v = b; v < e && bad.load() < 0; ++v) {
+            const int64_t ix = v % nx, iy = (v / nx) % ny, iz = v / (nx * ny);
+            ent.clear();
+            if (D.kind == 1) {
+                for (int q = 0; q < D.npts; ++q) {
+                    const int64_t a = ix + D.dx[q], bb = iy + D.dy[q], cc = iz + D.dz[q];
+                    if (a >= 0 && a < nx && bb >= 0 && bb < ny && cc >= 0 && cc < nz)
+                        ent.push_back({v + D.dx[q] + nx * (D.dy[q] + ny * (int64_t)D.dz[q]), D.c[q]});
+                }
+            } else {
+                const double* Dg = coef.data();
+                const double *CX = Dg + n, *CY = CX + n, *CZ = CY + n;
+                const int64_t sy = nx, sz = nx * ny;
+                if (iz > 0) ent.push_back({v - sz, CZ[v - sz]});
+                if (iy > 0) ent.push_back({v - sy, CY[v - sy]});
+                if (ix > 0) ent.push_back({v - 1, CX[v - 1]});
+                ent.push_back({v, Dg[v]});
+                if (ix + 1 < nx) ent.push_back({v + 1, CX[v]});
+                if (iy + 1 < ny) ent.push_back({v + sy, CY[v]});
+                if (iz + 1 < nz) ent.push_back({v + sz, CZ[v]});
+            }
+            bool ok = (int64_t)ent.size() == rp[v + 1] - rp[v];
+            for (size_t k = 0; ok && k < ent.size(); ++k)
+                ok = col[rp[v] + k] == ent[k].first && val[rp[v] + k] == ent[k].second;
+            if (!ok) {
+                int64_t exp = -1;
+                bad.compare_exchange_strong(exp, v);
+            }
+        }
+    });
+    if (bad.load() >= 0)
+        return set_err(DDG_E_ARG, "stencil does not reproduce row %lld of the CSR matrix", (long long)bad.load());
+    (void)c;
+    return DDG_OK;
 }
 
 // Byte-balanced contiguous partition of items [b, e) over the persistent
@@ -846,8 +927,18 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     }
     {
         const double mean = (double)c->nnz / (double)std::max<int64_t>(1, n);
-        const int sw = mean <= 16 ? 1 : mean <= 48 ? 4 : mean <= 128 ? 8 : 32;
-        c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val, sw, 0};
+        int sw = mean <= 16 ? 1 : mean <= 48 ? 4 : mean <= 128 ? 8 : 32;
+        DevStencil ds;
+        std::vector<double> scoef;
+        if (getenv("DDG_NO_STENCIL")) c->opts.stencil = nullptr;
+        if ((st = build_stencil(c, c->opts.stencil, n, row_ptr, col, val, ds, scoef))) { free_ctx(c); return st; }
+        if (!scoef.empty()) {
+            if ((st = upload(&c->d_stencil_coef, scoef))) { free_ctx(c); return st; }
+            ds.coef = c->d_stencil_coef;
+        }
+        if (ds.kind) sw = 1;
+        c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val, sw, 0, ds};
+        c->opts.stencil = nullptr;   // borrowed for the duration of ddg_setup only
     }
     {   // s position -> fine row (padding -1), for the flat colour gather
         std::vector<int32_t> g(std::max<int64_t>(1, c->s_doubles), -1);

@@ -33,12 +33,21 @@ PLAN = dict(OWNED_ROWS=0, OWNED_SUBS=1, P_SEND=2, P_RECV=3, R_SEND=4, R_RECV=5, 
             PROLONG_PARTS=8, COLOURS=9, PART_RANK=10, OVERLAP=11)
 
 
+class ddg_stencil(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("dims", C.c_int32 * 3), ("npts", C.c_int32),
+                ("offsets", C.c_void_p), ("coef", C.c_void_p)]
+
+
+STENCIL_KIND = {"none": 0, "const": 1, "face7": 2}
+
+
 class ddg_opts(C.Structure):
     _fields_ = [("overlap", C.c_int), ("rank_tol", C.c_double), ("stop_mode", C.c_int),
                 ("max_iter", C.c_int), ("device", C.c_int), ("stream", C.c_void_p),
                 ("use_graphs", C.c_int), ("verbose", C.c_int), ("coarse_variant", C.c_int),
                 ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("comm", C.c_void_p),
-                ("small_kernel", C.c_int), ("block_coords", C.c_void_p)]
+                ("small_kernel", C.c_int), ("block_coords", C.c_void_p),
+                ("stencil", C.POINTER(ddg_stencil))]
 
 
 class ddg_report(C.Structure):
@@ -144,7 +153,7 @@ class Solver:
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
                  stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
                  verbose=False, coarse_variant=0, block_coords=None, comm=None, fuse_gather=None,
-                 small_kernel=None):
+                 small_kernel=None, stencil=None):
         L = load()
         o = default_opts()
         o.overlap, o.rank_tol, o.stop_mode, o.max_iter = overlap, rank_tol, stop_mode, max_iter
@@ -164,6 +173,26 @@ class Solver:
             bc = np.ascontiguousarray(block_coords, np.int32)
             o.block_ndim = int(bc.shape[1])
             o.block_coords = bc.ctypes.data
+        keep = []
+        if stencil is not None:
+            # {"kind": "const", "dims": (nx, ny, nz), "offsets": [(dx, dy, dz), ...], "coef": [...]}
+            # {"kind": "face7", "dims": (nx, ny, nz), "coef": float64[4 n] (diag|cx|cy|cz)}
+            st = ddg_stencil()
+            st.kind = STENCIL_KIND[stencil["kind"]]
+            d = list(stencil["dims"]) + [1] * (3 - len(stencil["dims"]))
+            st.dims = (C.c_int32 * 3)(*d)
+            cf = np.ascontiguousarray(stencil["coef"], np.float64)
+            keep.append(cf)
+            st.coef = cf.ctypes.data
+            if stencil["kind"] == "const":
+                offs = np.zeros((len(stencil["offsets"]), 3), np.int32)
+                for i, off in enumerate(stencil["offsets"]):
+                    offs[i, :len(off)] = off
+                keep.append(offs)
+                st.npts = offs.shape[0]
+                st.offsets = offs.ctypes.data
+            keep.append(st)
+            o.stencil = C.pointer(st)
         rp = np.ascontiguousarray(row_ptr, np.int64)
         ci = np.ascontiguousarray(col, np.int32)
         va = np.ascontiguousarray(val, np.float64)
@@ -183,6 +212,7 @@ class Solver:
     def from_problem(cls, pr, **kw):
         kw.setdefault("overlap", pr.overlap)
         kw.setdefault("block_coords", pr.block_coords)
+        kw.setdefault("stencil", getattr(pr, "stencil", None))
         return cls(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts, **kw)
 
     def close(self):

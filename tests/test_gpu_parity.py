@@ -244,6 +244,7 @@ PATHS = {
     "ring_2tile_slots": {"DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2"},
     "classic": {"DDG_SYMV": "classic"},                           # per-item k_symv / k_symv_small
     "coarse_levels": {"DDG_COARSE_DATAFLOW": "0", "DDG_RING_MIN_MB": "0"},  # level-by-level sparse solve
+    "csr_rows": {"DDG_NO_STENCIL": "1"},                          # row kernels read the CSR
 }
 PATH_CASES = ["C1", "poisson3d_24_b8_p2", "lognormal_16_b4", "elasticity_8_be4", "biharm_64_b16_p3",
               "poisson2d_ragged"]
@@ -289,3 +290,28 @@ def test_ring_bitwise_repeatable(monkeypatch):
     u1, it1, h1, _ = s.solve(pr.f)
     u2, it2, h2, _ = s.solve(pr.f)
     assert it1 == it2 and np.array_equal(u1, u2) and np.array_equal(h1, h2)
+
+
+@pytest.mark.parametrize("name", ["C1", "poisson3d_24_b8_p2", "lognormal_16_b4", "biharm_64_b16_p3"])
+def test_stencil_rows_match_csr_bitwise(name, monkeypatch):
+    """The matrix-free row kernels evaluate each row in the CSR's column order
+    with the same fused multiply-adds, so the whole solve is bitwise identical
+    to the CSR path (DevStencil, ddg_internal.h)."""
+    pr = CASES[name]()
+    assert pr.stencil is not None
+    u1, it1, h1, _ = _solver(pr).solve(pr.f)
+    monkeypatch.setenv("DDG_NO_STENCIL", "1")
+    u2, it2, h2, _ = _solver(pr).solve(pr.f)
+    assert it1 == it2 and np.array_equal(u1, u2) and np.array_equal(h1, h2)
+
+
+def test_stencil_mismatch_rejected():
+    from paper_1504_00907_b200 import DDGError
+    pr = P.poisson2d(16, 4, 1, 9)
+    bad = dict(pr.stencil, coef=[4.0, -1, -1, -1, -0.5])
+    with pytest.raises(DDGError) as e:
+        _solver(pr, stencil=bad)
+    assert e.value.code == 1
+    with pytest.raises(DDGError) as e:
+        _solver(pr, stencil=dict(pr.stencil, dims=(16, 15, 1)))
+    assert e.value.code == 1
