@@ -75,6 +75,14 @@ __device__ __forceinline__ double row_dot1(const DevCSR& A, int64_t v, const dou
     return s;
 }
 
+// CSR row only: the fused gathers of the per-item SYMV kernels (the stencil
+// code would double their register allocation; the CSR rounds identically)
+__device__ __forceinline__ double row_dot_csr(const DevCSR& A, int64_t v, const double* __restrict__ x) {
+    double s = 0.0;
+    for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * x[A.col[e]];
+    return s;
+}
+
 // (A x)[v] by SW lanes (an aligned group of the warp; sl = lane in group).
 // Every lane of the warp must call it (the group reduction shuffles); rows
 // with valid == false contribute 0.
@@ -500,7 +508,7 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
                 const int node = idx[x];
                 double az = 0.0;
                 if (gather_mode == 1)
-                    az = row_dot1(A, node, z);
+                    az = row_dot_csr(A, node, z);
                 v = rvec[node] - az;
             }
             s_sm[x] = v;
@@ -640,7 +648,7 @@ k_symv_small(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
                 const int node = idx[x];
                 double az = 0.0;
                 if (gather_mode == 1)
-                    az = row_dot1(A, node, z);
+                    az = row_dot_csr(A, node, z);
                 v = rvec[node] - az;
             } else {
                 v = s[op.s_off + x];
@@ -767,7 +775,7 @@ k_symv_tma(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, i
                     const int node = idx[x];
                     double az = 0.0;
                     if (gather_mode == 1)
-                        az = row_dot1(A, node, z);
+                        az = row_dot_csr(A, node, z);
                     v = rvec[node] - az;
                 }
                 s_sm[x] = v;

@@ -449,7 +449,8 @@ static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool al
     op.m = m;
     op.mp = ((m + TILE - 1) / TILE) * TILE;
     op.nT = op.mp / TILE;
-    if (allow_single && op.nT <= MAX_BT) op.BT = op.nT;
+    const int single_max = getenv("DDG_SINGLE_MAX_NT") ? atoi(getenv("DDG_SINGLE_MAX_NT")) : MAX_BT;
+    if (allow_single && op.nT <= single_max) op.BT = op.nT;
     else op.BT = (op.nT > 512) ? MAX_BT : 8;
     if (op.BT > op.nT) op.BT = op.nT;
     op.nblk = (op.nT + op.BT - 1) / op.BT;
