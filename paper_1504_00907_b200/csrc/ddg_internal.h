@@ -107,7 +107,7 @@ struct Scalars {
 };
 
 // Reduction scratch: per-block partial sums + a ticket counter.
-constexpr int RED_BLOCKS = 148 * 4;
+constexpr int RED_BLOCKS = 148 * 8;
 constexpr int VEC_THREADS = 256;
 
 // Matrix-free description of A for the hot-path row kernels (include/ddg.h
@@ -120,6 +120,9 @@ struct DevStencil {
     int32_t npts;
     int32_t nx, ny, nz, pad;
     int32_t dx[STENCIL_MAX_PTS], dy[STENCIL_MAX_PTS], dz[STENCIL_MAX_PTS];
+    int32_t off[STENCIL_MAX_PTS];   // linear offsets dx + nx (dy + ny dz)
+    int32_t rx, ry, rz;             // reach per axis: rows farther than that from the faces need no checks
+    int32_t pad2;
     double c[STENCIL_MAX_PTS];
     const double* coef;  // face7: diag | cx | cy | cz, 4 n doubles (device)
 };

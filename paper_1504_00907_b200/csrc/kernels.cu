@@ -43,12 +43,20 @@ __device__ __forceinline__ double stencil_dot(const DevStencil& st, int64_t v, c
     const int iy = (int)(r % ny), iz = (int)(r / ny);
     double s = 0.0;
     if (st.kind == 1) {
+        const double* xv = x + v;
+        if (ix >= st.rx && ix < nx - st.rx && iy >= st.ry && iy < ny - st.ry && iz >= st.rz && iz < st.nz - st.rz) {
+#pragma unroll
+            for (int k = 0; k < STENCIL_MAX_PTS; ++k) {    // interior: every point on the grid
+                if (k >= st.npts) break;
+                s = fma(st.c[k], xv[st.off[k]], s);
+            }
+            return s;
+        }
 #pragma unroll
         for (int k = 0; k < STENCIL_MAX_PTS; ++k) {
             if (k >= st.npts) break;
             const int a = ix + st.dx[k], b = iy + st.dy[k], c = iz + st.dz[k];
-            if (a >= 0 && a < nx && b >= 0 && b < ny && c >= 0 && c < st.nz)
-                s = fma(st.c[k], x[v + st.dx[k] + (int64_t)nx * (st.dy[k] + (int64_t)ny * st.dz[k])], s);
+            if (a >= 0 && a < nx && b >= 0 && b < ny && c >= 0 && c < st.nz) s = fma(st.c[k], xv[st.off[k]], s);
         }
         return s;
     }
@@ -2090,7 +2098,7 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 }
 
 static bool g_ring_init[64] = {};
-static int g_ring_rt = 4, g_ring_nb = 0;
+static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0;
 // per device, once, outside any stream capture (called from ddg_setup)
 void symv_ring_init() {
     g_ring_rt = 4;
@@ -2098,6 +2106,8 @@ void symv_ring_init() {
     if (g_ring_rt != 1 && g_ring_rt != 2) g_ring_rt = 4;
     g_ring_nb = 0;
     if (const char* e = getenv("DDG_RING_NB")) g_ring_nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
+    g_ring_nst = 0;
+    if (const char* e = getenv("DDG_RING_NST")) g_ring_nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
     int dev = 0;
     cudaGetDevice(&dev);
     if (g_ring_init[dev & 63]) return;
@@ -2119,7 +2129,8 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     int nb = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 3 : 2);
     while (nb > 2 && ring_smem(RT, 4, nb, maxr) > budget) --nb;
     int nst = 2;
-    while (nst < RING_MAX_NST && ring_smem(RT, nst + 1, nb, maxr) <= budget) ++nst;
+    const int nst_cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
+    while (nst < nst_cap && ring_smem(RT, nst + 1, nb, maxr) <= budget) ++nst;
     const size_t smem = ring_smem(RT, nst, nb, maxr);
     if (RT == 1)
         k_symv_ring<1><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,

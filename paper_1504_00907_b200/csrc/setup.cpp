@@ -521,6 +521,12 @@ static int build_stencil(ddg_ctx* c, const ddg_stencil* S, int64_t n, const int6
             D.dy[q] = S->offsets[3 * k + 1];
             D.dz[q] = S->offsets[3 * k + 2];
             D.c[q] = S->coef[k];
+            const int64_t lo = lin(k);
+            if (lo < INT32_MIN || lo > INT32_MAX) return set_err(DDG_E_ARG, "stencil offset out of range");
+            D.off[q] = (int32_t)lo;
+            D.rx = std::max(D.rx, std::abs(D.dx[q]));
+            D.ry = std::max(D.ry, std::abs(D.dy[q]));
+            D.rz = std::max(D.rz, std::abs(D.dz[q]));
         }
     } else if (S->kind == DDG_STENCIL_FACE7) {
         if (!S->coef) return set_err(DDG_E_ARG, "stencil: coef (4 n values) required");

@@ -102,6 +102,54 @@ __global__ void __launch_bounds__(288) k_read_tma(const double* __restrict__ p, 
     if (s == 12345.678) out[0] = s;
 }
 
+// K5: 32 KB slots filled by NC copies each (the ring's per-tile copies),
+// optional packed "diagonal" copies of 4224 B every `diag_every` copies
+__global__ void __launch_bounds__(288) k_read_tma_nc(const double* __restrict__ p, size_t nslots, int NC, int S,
+                                                     int diag_every, double* out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = (uint64_t*)smem;
+    uint64_t* empty = full + S;
+    double* ring = (double*)(smem + 1024);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned CH = 32768, cb = CH / NC;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { mb_init(&full[i], 1); mb_init(&empty[i], 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {
+        if (lane) return;
+        unsigned k = 0, cnt = 0;
+        const char* src = (const char*)p + (size_t)blockIdx.x * CH;
+        for (size_t c = blockIdx.x; c < nslots; c += gridDim.x, ++k) {
+            unsigned slot = k % S, n = k / S;
+            if (n) mb_wait(&empty[slot], (n - 1) & 1);
+            unsigned bytes[8], tot = 0;
+            for (int q = 0; q < NC; ++q, ++cnt) {
+                bytes[q] = (diag_every && cnt % diag_every == 0) ? 4224 : cb;
+                tot += bytes[q];
+            }
+            mb_expect(&full[slot], tot);
+            const char* s0 = (const char*)p + c * CH;
+            for (int q = 0; q < NC; ++q)
+                bulk((char*)ring + (size_t)slot * CH + q * cb, s0 + q * cb, bytes[q], &full[slot]);
+        }
+        (void)src;
+        return;
+    }
+    double s = 0;
+    unsigned k = 0;
+    for (size_t c = blockIdx.x; c < nslots; c += gridDim.x, ++k) {
+        unsigned slot = k % S;
+        mb_wait(&full[slot], (k / S) & 1);
+        const double* T = ring + (size_t)slot * 4096;
+        s += T[warp * 512 + lane];
+        __syncwarp();
+        if (lane == 0) mb_arrive(&empty[slot]);
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
 int main() {
     const size_t bytes = 8ull << 30, n = bytes / 8;
     double *p, *out;
@@ -153,5 +201,15 @@ int main() {
                 timeit(nm, [&] { k_read_tma<<<148 * cps, 288, sm>>>(p, bytes / CH, CH, S, out); });
             }
         }
+    for (int S : {4, 6})
+        for (int NC : {1, 2, 4, 8})
+            for (int de : {0, 4}) {
+                const size_t sm = 1024 + (size_t)32768 * S;
+                cudaFuncSetAttribute(k_read_tma_nc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                char nm[96];
+                snprintf(nm, sizeof nm, "tma ring 32K slots S=%d copies/slot=%d diag_every=%d", S, NC, de);
+                // (diag copies move fewer bytes: report the nominal 32 KB/slot rate)
+                timeit(nm, [&] { k_read_tma_nc<<<148, 288, sm>>>(p, bytes / 32768, NC, S, de, out); });
+            }
     return 0;
 }
