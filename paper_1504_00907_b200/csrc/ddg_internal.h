@@ -161,6 +161,7 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 // (relative to item_begin) of the CTAs.  Requires every item's rows <= 512.
 constexpr int RING_MAX_ROWS = 512;
 void symv_ring_init();   // once per device, before any capture
+int symv_ring_trace(unsigned long long* out);   // debug counters (DDG_RING_TRACE)
 void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                       const int32_t* cta_part, int ncta, int max_rows_t, const double* tiles, const double* s,
                       const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done);

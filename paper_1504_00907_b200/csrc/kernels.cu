@@ -957,8 +957,33 @@ __global__ void __launch_bounds__(RING_THREADS, 1)
 k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
             const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
             const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
-            double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr) {
+            double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr,
+            unsigned long long* rtrace) {
     constexpr int SLOT = RT * TILE_ELEMS;
+    // DDG_RING_TRACE: cycles per role and wait (debug; rtrace == nullptr otherwise)
+    unsigned long long tw[4] = {0, 0, 0, 0}, tstart = rtrace ? clock64() : 0, ntile = 0, nflush = 0;
+#define RT_WAIT(k, call)                                        \
+    do {                                                        \
+        if (rtrace) {                                           \
+            const unsigned long long t0_ = clock64();           \
+            call;                                               \
+            tw[k] += clock64() - t0_;                           \
+        } else {                                                \
+            call;                                               \
+        }                                                       \
+    } while (0)
+#define RT_FLUSH(base)                                                                  \
+    do {                                                                                \
+        if (rtrace && lane == 0) {                                                      \
+            atomicAdd(&rtrace[(base)], tw[0]);                                          \
+            atomicAdd(&rtrace[(base) + 1], tw[1]);                                      \
+            atomicAdd(&rtrace[(base) + 2], tw[2]);                                      \
+            atomicAdd(&rtrace[(base) + 3], clock64() - tstart);                         \
+            atomicAdd(&rtrace[(base) + 4], ntile);                                      \
+            atomicAdd(&rtrace[(base) + 5], nflush);                                     \
+            atomicAdd(&rtrace[(base) + 6], tw[3]);                                      \
+        }                                                                               \
+    } while (0)
     if (*done) return;
     extern __shared__ __align__(128) double rsm[];
     double* ring = rsm;                                          // [nst][SLOT]
@@ -988,8 +1013,10 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
     }
     __syncthreads();
     if (i0 >= i1) return;
-    if (warp == SYMV_WARPS) {                                    // ---- producer ----
-        if (lane != 0) return;
+    if (warp == SYMV_WARPS) {                                    // ---- producer warp ----
+        // Lane 0 owns the barriers; the tile copies of a triangle chunk are
+        // issued by lanes 0..nt-1 in one instruction (a bulk-copy issue costs
+        // the issuing thread a few hundred cycles: one per lane overlaps them).
         DescPipe dp;
         dp.init(items, ops, i0, i1);
         unsigned slot = 0, sph = 0;                                // ring slot and its fill count
@@ -998,48 +1025,55 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
         for (int ii = i0; ii < i1; ++ii) {
             ItemDesc it;
             OpDesc op;
-            dp.next(items, ops, ii, i1, it, op);
+            RT_WAIT(2, dp.next(items, ops, ii, i1, it, op); it.tri += 0);
             const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
-            if (bph > 0) mbar_wait(&sempty[bi], (bph - 1) & 1);
-            int32_t* d = dsc + bi * 8;
-            d[0] = it.I0; d[1] = it.I1; d[2] = it.J0; d[3] = it.J1; d[4] = it.tri; d[5] = it.ntiles;
-            mbar_expect_tx(&sfull[bi], (unsigned)(rows_r + rows_c) * 8u);
+            if (bph > 0) RT_WAIT(0, mbar_wait(&sempty[bi], (bph - 1) & 1));
+            if (lane == 0) {
+                int32_t* d = dsc + bi * 8;
+                d[0] = it.I0; d[1] = it.I1; d[2] = it.J0; d[3] = it.J1; d[4] = it.tri; d[5] = it.ntiles;
+                mbar_expect_tx(&sfull[bi], (unsigned)(rows_r + rows_c) * 8u);
+            }
+            __syncwarp();
             const double* sop = s + op.s_off;
             double* sb = s_sm + (size_t)bi * maxr;
-            bulk_g2s(sb, sop + it.I0 * TILE, rows_r * 8u, &sfull[bi]);
-            if (rows_c) bulk_g2s(sb + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[bi]);
+            if (lane == 0) bulk_g2s(sb, sop + it.I0 * TILE, rows_r * 8u, &sfull[bi]);
+            if (lane == 1 && rows_c) bulk_g2s(sb + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[bi]);
             if (++bi == nb) { bi = 0; ++bph; }
             // tile q of a chunk always lands at q * 8 KB of its slot; rectangular
             // items are contiguous full tiles (one copy per chunk), triangles
             // copy tile by tile (packed diagonal tiles are 4224 B)
             const double* src = tiles + it.tile_off;
-            int rr = 0, cc = 0;                                     // triangle walk: row, col
             for (int l0 = 0; l0 < it.ntiles; l0 += RT) {
                 const int nt = min(RT, it.ntiles - l0);
-                if (sph > 0) mbar_wait(&empty[slot], (sph - 1) & 1);
+                if (sph > 0) RT_WAIT(1, mbar_wait(&empty[slot], (sph - 1) & 1));
+                const unsigned long long tc0 = rtrace ? clock64() : 0;
                 double* dst = ring + (size_t)slot * SLOT;
                 if (!it.tri) {
-                    mbar_expect_tx(&full[slot], (unsigned)nt * TILE_ELEMS * 8u);
-                    bulk_g2s(dst, src, (unsigned)nt * TILE_ELEMS * 8u, &full[slot]);
-                    src += (size_t)nt * TILE_ELEMS;
+                    if (lane == 0) {
+                        mbar_expect_tx(&full[slot], (unsigned)nt * TILE_ELEMS * 8u);
+                        bulk_g2s(dst, src + (int64_t)l0 * TILE_ELEMS, (unsigned)nt * TILE_ELEMS * 8u, &full[slot]);
+                    }
                 } else {
-                    unsigned bytes = 0;
-                    int r2 = rr, c2 = cc;
-                    for (int q = 0; q < nt; ++q) {
-                        bytes += (c2 == r2 ? DIAG_ELEMS : TILE_ELEMS) * 8u;
-                        if (++c2 > r2) { c2 = 0; ++r2; }
+                    unsigned tb = 0;
+                    int64_t toff = 0;
+                    if (lane < nt) {
+                        int I_, J_;
+                        item_tile(it, l0 + lane, I_, J_);
+                        tb = (I_ == J_ ? DIAG_ELEMS : TILE_ELEMS) * 8u;
+                        toff = item_tile_off(it, l0 + lane, I_);
                     }
-                    mbar_expect_tx(&full[slot], bytes);
-                    for (int q = 0; q < nt; ++q) {
-                        const unsigned tb = (cc == rr ? DIAG_ELEMS : TILE_ELEMS) * 8u;
-                        bulk_g2s(dst + q * TILE_ELEMS, src, tb, &full[slot]);
-                        src += tb / 8;
-                        if (++cc > rr) { cc = 0; ++rr; }
-                    }
+                    unsigned bytes = tb;
+#pragma unroll
+                    for (int o = 1; o < RT; o <<= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
+                    if (lane == 0) mbar_expect_tx(&full[slot], bytes);
+                    __syncwarp();
+                    if (lane < nt) bulk_g2s(dst + lane * TILE_ELEMS, src + toff, tb, &full[slot]);
                 }
+                if (rtrace) tw[3] += clock64() - tc0;
                 if (++slot == (unsigned)nst) { slot = 0; ++sph; }
             }
         }
+        RT_FLUSH(0);
         return;
     }
     if (warp > SYMV_WARPS) {                                     // ---- epilogue warps ----
@@ -1062,7 +1096,7 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
 #pragma unroll
                 for (int r = 0; r < RING_MAX_ROWS / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
             }
-            mbar_wait(&pdone[b], ph & 1);
+            RT_WAIT(0, mbar_wait(&pdone[b], ph & 1));
             const double* pp = part + (size_t)b * SYMV_WARPS * maxr;
 #pragma unroll
             for (int r = 0; r < RING_MAX_ROWS / 32; ++r) {
@@ -1081,6 +1115,7 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
             __syncwarp();
             if (lane == 0) mbar_arrive(&pfree[b]);
         }
+        RT_FLUSH(8);
         return;
     }
     // ---- consumers (warps 0..7): each walks only its own tiles ----
@@ -1088,14 +1123,14 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
     int bi = 0;
     unsigned bph = 0;
     for (int ki = 0; ki < i1 - i0; ++ki) {
-        mbar_wait(&sfull[bi], bph & 1);
+        RT_WAIT(0, mbar_wait(&sfull[bi], bph & 1));
         const int32_t* d = dsc + bi * 8;
         const int I0 = d[0], I1 = d[1], J0 = d[2], J1 = d[3], tri = d[4], ntiles = d[5];
         const double* ss = s_sm + (size_t)bi * maxr;
         const int rows_r = (I1 - I0) * TILE;
         const int rows_t = rows_r + (tri ? 0 : (J1 - J0) * TILE);
         double* pw = part + ((size_t)bi * SYMV_WARPS + warp) * maxr;
-        if (bph > 0) mbar_wait(&pfree[bi], (bph - 1) & 1);
+        if (bph > 0) RT_WAIT(1, mbar_wait(&pfree[bi], (bph - 1) & 1));
         for (int x = lane; x < rows_t; x += 32) pw[x] = 0.0;
         __syncwarp();
         double t[TILE];
@@ -1105,8 +1140,10 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
         auto tile = [&](const double* T, int I, int J) {
             const int ri = (I - I0) * TILE;
             const int cj = tri ? (J - I0) * TILE : rows_r + (J - J0) * TILE;
+            ++ntile;
             if (J != curJ) {
                 if (curJ >= 0) {
+                    ++nflush;
                     flush_column(t, pw, tri ? (curJ - I0) * TILE : rows_r + (curJ - J0) * TILE, lane);
 #pragma unroll
                     for (int j = 0; j < TILE; ++j) t[j] = 0.0;
@@ -1161,7 +1198,7 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
         // every warp visits every chunk in order (keeps the mbarrier phases
         // of each slot in step), consuming only its own tiles
         for (int l0 = 0; l0 < ntiles; l0 += RT) {
-            mbar_wait(&full[slot], sph & 1);
+            RT_WAIT(2, mbar_wait(&full[slot], sph & 1));
             const double* C = ring + (size_t)slot * SLOT;
             while (l >= 0 && l < l0 + RT) {
                 tile(C + (l - l0) * TILE_ELEMS, I, J);
@@ -1177,6 +1214,9 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
         mbar_arrive(&pdone[bi]);                                   // every lane (release its rows)
         if (++bi == nb) { bi = 0; ++bph; }
     }
+    RT_FLUSH(16);
+#undef RT_WAIT
+#undef RT_FLUSH
 }
 
 // Sum the partial segments of multi-item operators for one row block, in
@@ -2099,6 +2139,7 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 
 static bool g_ring_init[64] = {};
 static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0;
+static unsigned long long* g_ring_trace = nullptr;   // DDG_RING_TRACE (debug)
 // per device, once, outside any stream capture (called from ddg_setup)
 void symv_ring_init() {
     g_ring_rt = 4;
@@ -2108,6 +2149,13 @@ void symv_ring_init() {
     if (const char* e = getenv("DDG_RING_NB")) g_ring_nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
     g_ring_nst = 0;
     if (const char* e = getenv("DDG_RING_NST")) g_ring_nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
+
+    if (getenv("DDG_RING_TRACE") && !g_ring_trace) {
+        if (cudaMalloc(&g_ring_trace, 32 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(g_ring_trace, 0, 32 * sizeof(unsigned long long));
+        else
+            g_ring_trace = nullptr;
+    }
     int dev = 0;
     cudaGetDevice(&dev);
     if (g_ring_init[dev & 63]) return;
@@ -2116,6 +2164,15 @@ void symv_ring_init() {
     cudaFuncSetAttribute(k_symv_ring<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     g_ring_init[dev & 63] = true;
+}
+
+// debug: read and zero the DDG_RING_TRACE counters (24 values; see k_symv_ring)
+int symv_ring_trace(unsigned long long* out) {
+    if (!g_ring_trace) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, g_ring_trace, 24 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemset(g_ring_trace, 0, 32 * sizeof(unsigned long long));
+    return 0;
 }
 
 void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
@@ -2134,13 +2191,13 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     const size_t smem = ring_smem(RT, nst, nb, maxr);
     if (RT == 1)
         k_symv_ring<1><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, maxr);
+                                                         partials, done, nst, nb, maxr, g_ring_trace);
     else if (RT == 2)
         k_symv_ring<2><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, maxr);
+                                                         partials, done, nst, nb, maxr, g_ring_trace);
     else
         k_symv_ring<4><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, maxr);
+                                                         partials, done, nst, nb, maxr, g_ring_trace);
 }
 
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,

@@ -1523,3 +1523,7 @@ extern "C" int64_t ddg_plan_query(ddg_plan* p, int what, int colour, int peer, i
 }
 
 extern "C" void ddg_plan_destroy(ddg_plan* p) { delete p; }
+
+// debug (not part of include/ddg.h): k_symv_ring role/wait cycle counters
+// accumulated since the last call (DDG_RING_TRACE=1); 24 values
+extern "C" int ddg_debug_ring_trace(unsigned long long* out) { return symv_ring_trace(out); }
