@@ -1219,6 +1219,291 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
 #undef RT_FLUSH
 }
 
+// ---- k_symv_ring2: row warps + column warps ----------------------------------
+// Same producer, ring, item buffers and epilogue as k_symv_ring; the 16
+// consumer warps split each tile's two products by role:
+//  * row warps (0-7): own tile rows r (owner (r + item counter) mod 8); lane i
+//    accumulates the direct part y_I[i] += sum_j S_IJ[i][j] s_J[j] in one
+//    register across the row's tiles, then writes pr[row] once;
+//  * column warps (8-15): own tile columns c; lane j accumulates the
+//    transposed part y_J[j] += sum_i S_IJ[i][j] s_I[i] walking the tile along a
+//    rotated diagonal (i = (t + j) mod 32: two wavefronts per load, no bank
+//    conflicts) with s_I rotated by shuffles; one register per owned column,
+//    written to pc[column] at the end of the item.
+// Every row and column has a single owner, so the item's result is
+// y = pr + pc (triangles) or pr | pc (rectangles: row block | column block)
+// -- two partial arrays instead of eight, no butterfly, ~40 registers per
+// consumer thread.
+constexpr int R2_ROWW = 8, R2_COLW = 8, R2_CONS = R2_ROWW + R2_COLW;
+constexpr int RING2_THREADS = (R2_CONS + 1 + RING_EPI_WARPS) * 32;
+__host__ __device__ constexpr size_t ring2_smem(int RT, int nst, int nb, int maxr) {
+    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * 3 * maxr * 8 + (size_t)nb * 8 * 4 +
+           (2 * (size_t)nst + 4 * (size_t)nb) * 8;
+}
+
+template <int RT>
+__global__ void __launch_bounds__(RING2_THREADS, 1)
+k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
+             const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
+             const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
+             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr) {
+    constexpr int SLOT = RT * TILE_ELEMS;
+    if (*done) return;
+    extern __shared__ __align__(128) double rsm[];
+    double* ring = rsm;                                          // [nst][SLOT]
+    double* s_sm = ring + (size_t)nst * SLOT;                    // [nb][maxr]
+    double* pr_sm = s_sm + (size_t)nb * maxr;                    // [nb][maxr]  row (direct) parts
+    double* pc_sm = pr_sm + (size_t)nb * maxr;                   // [nb][maxr]  column (transposed) parts
+    int32_t* dsc = reinterpret_cast<int32_t*>(pc_sm + (size_t)nb * maxr);   // [nb][8]
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsc + nb * 8);
+    uint64_t* empty = full + nst;
+    uint64_t* sfull = empty + nst;
+    uint64_t* sempty = sfull + nb;
+    uint64_t* pdone = sempty + nb;
+    uint64_t* pfree = pdone + nb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], R2_CONS);
+        }
+        for (int b = 0; b < nb; ++b) {
+            mbar_init(&sfull[b], 1);
+            mbar_init(&sempty[b], R2_CONS);
+            mbar_init(&pdone[b], R2_CONS * 32);
+            mbar_init(&pfree[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (i0 >= i1) return;
+    if (warp == R2_CONS) {                                       // ---- producer warp ----
+        DescPipe dp;
+        dp.init(items, ops, i0, i1);
+        unsigned slot = 0, sph = 0;
+        int bi = 0;
+        unsigned bph = 0;
+        for (int ii = i0; ii < i1; ++ii) {
+            ItemDesc it;
+            OpDesc op;
+            dp.next(items, ops, ii, i1, it, op);
+            const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+            if (bph > 0) mbar_wait(&sempty[bi], (bph - 1) & 1);
+            if (lane == 0) {
+                int32_t* d = dsc + bi * 8;
+                d[0] = it.I0; d[1] = it.I1; d[2] = it.J0; d[3] = it.J1; d[4] = it.tri; d[5] = it.ntiles;
+                mbar_expect_tx(&sfull[bi], (unsigned)(rows_r + rows_c) * 8u);
+            }
+            __syncwarp();
+            const double* sop = s + op.s_off;
+            double* sb = s_sm + (size_t)bi * maxr;
+            if (lane == 0) bulk_g2s(sb, sop + it.I0 * TILE, rows_r * 8u, &sfull[bi]);
+            if (lane == 1 && rows_c) bulk_g2s(sb + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[bi]);
+            if (++bi == nb) { bi = 0; ++bph; }
+            const double* src = tiles + it.tile_off;
+            for (int l0 = 0; l0 < it.ntiles; l0 += RT) {
+                const int nt = min(RT, it.ntiles - l0);
+                if (sph > 0) mbar_wait(&empty[slot], (sph - 1) & 1);
+                double* dst = ring + (size_t)slot * SLOT;
+                if (!it.tri) {
+                    if (lane == 0) {
+                        mbar_expect_tx(&full[slot], (unsigned)nt * TILE_ELEMS * 8u);
+                        bulk_g2s(dst, src + (int64_t)l0 * TILE_ELEMS, (unsigned)nt * TILE_ELEMS * 8u, &full[slot]);
+                    }
+                } else {
+                    unsigned tb = 0;
+                    int64_t toff = 0;
+                    if (lane < nt) {
+                        int I_, J_;
+                        item_tile(it, l0 + lane, I_, J_);
+                        tb = (I_ == J_ ? DIAG_ELEMS : TILE_ELEMS) * 8u;
+                        toff = item_tile_off(it, l0 + lane, I_);
+                    }
+                    unsigned bytes = tb;
+#pragma unroll
+                    for (int o = 1; o < RT; o <<= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
+                    if (lane == 0) mbar_expect_tx(&full[slot], bytes);
+                    __syncwarp();
+                    if (lane < nt) bulk_g2s(dst + lane * TILE_ELEMS, src + toff, tb, &full[slot]);
+                }
+                if (++slot == (unsigned)nst) { slot = 0; ++sph; }
+            }
+        }
+        return;
+    }
+    if (warp > R2_CONS) {                                        // ---- epilogue warps ----
+        const int e = warp - R2_CONS - 1;
+        for (int ii = i0 + e, ki = e; ii < i1; ii += RING_EPI_WARPS, ki += RING_EPI_WARPS) {
+            const ItemDesc it = items[ii];
+            const OpDesc op = ops[it.op];
+            const int b = ki % nb;
+            const unsigned ph = (unsigned)(ki / nb);
+            const int rows_r = (it.I1 - it.I0) * TILE;
+            const int rows_t = rows_r + (it.tri ? 0 : (it.J1 - it.J0) * TILE);
+            const int g0 = it.I0 * TILE;
+            const int nr = min(rows_t, op.m - g0);
+            const bool scat = it.part_off < 0 && op.out_mode == 0;
+            int ix[RING_MAX_ROWS / 32];
+            double zv[RING_MAX_ROWS / 32];
+            if (scat) {
+                const int32_t* idx = oidx + op.idx_off + g0;
+#pragma unroll
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) ix[r] = (lane + 32 * r < nr) ? idx[lane + 32 * r] : 0;
+#pragma unroll
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
+            }
+            mbar_wait(&pdone[b], ph & 1);
+            const double* pr = pr_sm + (size_t)b * maxr;
+            const double* pc = pc_sm + (size_t)b * maxr;
+#pragma unroll
+            for (int r = 0; r < RING_MAX_ROWS / 32; ++r) {
+                const int x = lane + 32 * r;
+                if (x < rows_t) {
+                    const double y = it.tri ? pr[x] + pc[x] : (x < rows_r ? pr[x] : pc[x]);
+                    if (it.part_off >= 0) partials[it.part_off + x] = y;
+                    else if (x < nr) {
+                        if (scat) z[ix[r]] = zv[r] + y;
+                        else y_out[g0 + x] = y;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfree[b]);
+        }
+        return;
+    }
+    // ---- consumers: row warps 0..7, column warps 8..15 ----
+    const bool colw = warp >= R2_ROWW;
+    const int wr = colw ? warp - R2_ROWW : warp;
+    unsigned slot = 0, sph = 0;
+    int bi = 0;
+    unsigned bph = 0;
+    for (int ki = 0; ki < i1 - i0; ++ki) {
+        mbar_wait(&sfull[bi], bph & 1);
+        const int32_t* d = dsc + bi * 8;
+        const int I0 = d[0], I1 = d[1], J1 = d[3], tri = d[4], ntiles = d[5];
+        const int J0 = d[2];
+        const double* ss = s_sm + (size_t)bi * maxr;
+        const int h = I1 - I0, wd = tri ? h : J1 - J0;
+        const int rows_r = h * TILE;
+        double* pr = pr_sm + (size_t)bi * maxr;
+        double* pc = pc_sm + (size_t)bi * maxr;
+        if (bph > 0) mbar_wait(&pfree[bi], (bph - 1) & 1);
+        // own tiles in increasing stream index l:
+        //   row warp:    rows a, a + 8 (a = (wr - ki) mod 8), each row's tiles in order
+        //   column warp: columns a, a + 8; per row r both owned columns in order
+        const int a = (wr - ki) & 7;
+        int l = -1, r = 0, c = 0, ccur = 0;
+        double acc = 0.0, acc0 = 0.0, acc1 = 0.0;
+        auto rowstart = [&](int rr) { return tri ? rr * (rr + 1) / 2 : rr * wd; };
+        auto rowlen = [&](int rr) { return tri ? rr + 1 : wd; };
+        if (!colw) {
+            if (a < h) { r = a; c = 0; l = rowstart(r); }
+        } else {
+            if (a < wd) {
+                r = tri ? a : 0;
+                ccur = 0;                                          // 0: column a, 1: column a + 8
+                c = a;
+                l = rowstart(r) + c;
+            }
+        }
+        auto advance = [&]() {
+            if (!colw) {
+                if (++c < rowlen(r)) { ++l; return; }
+                r += 8;
+                if (r >= h) { l = -1; return; }
+                c = 0;
+                l = rowstart(r);
+            } else {
+                const int c1 = a + 8;
+                if (ccur == 0 && c1 < wd && (!tri || c1 <= r)) {
+                    ccur = 1;
+                    c = c1;
+                } else {
+                    ++r;
+                    if (r >= h) { l = -1; return; }
+                    ccur = 0;
+                    c = a;
+                }
+                l = rowstart(r) + c;
+            }
+        };
+        for (int l0 = 0; l0 < ntiles; l0 += RT) {
+            mbar_wait(&full[slot], sph & 1);
+            const double* C = ring + (size_t)slot * SLOT;
+            while (l >= 0 && l < l0 + RT) {
+                const double* T = C + (l - l0) * TILE_ELEMS;
+                const bool diag = tri && r == c;
+                if (!colw) {
+                    // direct part: lane = row, s_J broadcast
+                    const double2* sJ = reinterpret_cast<const double2*>(ss + (tri ? c * TILE : rows_r + c * TILE));
+                    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+                    if (!diag) {
+#pragma unroll
+                        for (int j = 0; j < TILE; j += 4) {
+                            const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                            d0 = fma(T[j * TILE + lane], u.x, d0);
+                            d1 = fma(T[(j + 1) * TILE + lane], u.y, d1);
+                            d2 = fma(T[(j + 2) * TILE + lane], v.x, d2);
+                            d3 = fma(T[(j + 3) * TILE + lane], v.y, d3);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < TILE; j += 4) {
+                            const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                            if (lane >= j) d0 = fma(T[diag_col_off(j) + lane - j], u.x, d0);
+                            if (lane >= j + 1) d1 = fma(T[diag_col_off(j + 1) + lane - j - 1], u.y, d1);
+                            if (lane >= j + 2) d2 = fma(T[diag_col_off(j + 2) + lane - j - 2], v.x, d2);
+                            if (lane >= j + 3) d3 = fma(T[diag_col_off(j + 3) + lane - j - 3], v.y, d3);
+                        }
+                    }
+                    acc += (d0 + d1) + (d2 + d3);
+                    if (c == rowlen(r) - 1) {                      // row complete
+                        pr[r * TILE + lane] = acc;
+                        acc = 0.0;
+                    }
+                } else {
+                    // transposed part: lane = column, rotated walk of the tile
+                    const double sI = ss[r * TILE + lane];
+                    double d0 = 0.0, d1 = 0.0;
+                    if (!diag) {
+#pragma unroll
+                        for (int t = 0; t < TILE; t += 2) {
+                            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31;
+                            d0 = fma(T[lane * TILE + ia], __shfl_sync(FULL, sI, ia), d0);
+                            d1 = fma(T[lane * TILE + ib], __shfl_sync(FULL, sI, ib), d1);
+                        }
+                    } else {
+                        const double* Tc = T + diag_col_off(lane) - lane;   // element (i, lane) at Tc[i], i >= lane
+#pragma unroll
+                        for (int t = 0; t < TILE; t += 2) {
+                            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31;
+                            const double va = __shfl_sync(FULL, sI, ia), vb = __shfl_sync(FULL, sI, ib);
+                            if (ia >= lane) d0 = fma(Tc[ia], va, d0);
+                            if (ib >= lane) d1 = fma(Tc[ib], vb, d1);
+                        }
+                    }
+                    if (ccur == 0) acc0 += d0 + d1;
+                    else acc1 += d0 + d1;
+                }
+                advance();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (++slot == (unsigned)nst) { slot = 0; ++sph; }
+        }
+        if (colw && a < wd) {
+            pc[(tri ? a * TILE : rows_r + a * TILE) + lane] = acc0;
+            if (a + 8 < wd) pc[(tri ? (a + 8) * TILE : rows_r + (a + 8) * TILE) + lane] = acc1;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[bi]);
+        mbar_arrive(&pdone[bi]);                                   // every lane (release its rows)
+        if (++bi == nb) { bi = 0; ++bph; }
+    }
+}
+
 // Sum the partial segments of multi-item operators for one row block, in
 // fixed item order, and apply the result.
 __global__ void k_symv_reduce(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
@@ -2138,7 +2423,7 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 }
 
 static bool g_ring_init[64] = {};
-static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0;
+static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0, g_ring_v2 = 0;
 static unsigned long long* g_ring_trace = nullptr;   // DDG_RING_TRACE (debug)
 // per device, once, outside any stream capture (called from ddg_setup)
 void symv_ring_init() {
@@ -2149,6 +2434,7 @@ void symv_ring_init() {
     if (const char* e = getenv("DDG_RING_NB")) g_ring_nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
     g_ring_nst = 0;
     if (const char* e = getenv("DDG_RING_NST")) g_ring_nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
+    g_ring_v2 = getenv("DDG_RING_V2") ? atoi(getenv("DDG_RING_V2")) : -1;   // -1: auto
 
     if (getenv("DDG_RING_TRACE") && !g_ring_trace) {
         if (cudaMalloc(&g_ring_trace, 32 * sizeof(unsigned long long)) == cudaSuccess)
@@ -2163,6 +2449,8 @@ void symv_ring_init() {
     cudaFuncSetAttribute(k_symv_ring<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     g_ring_init[dev & 63] = true;
 }
 
@@ -2177,7 +2465,8 @@ int symv_ring_trace(unsigned long long* out) {
 
 void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                       const int32_t* cta_part, int ncta, int max_rows_t, const double* tiles, const double* s,
-                      const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done) {
+                      const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done,
+                      bool triangles) {
     const int RT = g_ring_rt;
     const int maxr = std::max(TILE, std::min(RING_MAX_ROWS, max_rows_t));
     const size_t budget = 227 * 1024;
@@ -2188,6 +2477,23 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     int nst = 2;
     const int nst_cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
     while (nst < nst_cap && ring_smem(RT, nst + 1, nb, maxr) <= budget) ++nst;
+    // row/column-warp consumers for launches of whole-subdomain triangles
+    // (measured: C3 +4%, C5 +1%; the 8-warp column consumers win on the
+    // 8-wide rectangles of split operators); DDG_RING_V2=0/1 forces either
+    if (g_ring_v2 == 1 || (g_ring_v2 < 0 && triangles)) {
+        int nb2 = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 4 : 2);
+        int nst2 = 2;
+        const int cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
+        while (nst2 < cap && ring2_smem(RT, nst2 + 1, nb2, maxr) <= budget) ++nst2;
+        const size_t smem2 = ring2_smem(RT, nst2, nb2, maxr);
+        if (RT == 2)
+            k_symv_ring2<2><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
+                                                                 y_out, partials, done, nst2, nb2, maxr);
+        else
+            k_symv_ring2<4><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
+                                                                 y_out, partials, done, nst2, nb2, maxr);
+        return;
+    }
     const size_t smem = ring_smem(RT, nst, nb, maxr);
     if (RT == 1)
         k_symv_ring<1><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,

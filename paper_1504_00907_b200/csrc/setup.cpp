@@ -1097,7 +1097,8 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
         if (ring) {
             prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
                 launch_symv_ring(c->stream, c->d_ops, c->d_items, pl.item_begin, c->d_ring + pl.ring_off,
-                                 num_sms(), pl.max_rows_t, c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done);
+                                 num_sms(), pl.max_rows_t, c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done,
+                                 pl.all_single != 0);
             });
             c->launches += 1;
             if (pl.red_end > pl.red_begin) {

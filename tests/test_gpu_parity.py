@@ -240,8 +240,10 @@ def test_comm_path_single_rank(name):
 # The small parity cases fall below the persistent ring's size threshold, so
 # each path is also forced explicitly (switches are read at ddg_setup).
 PATHS = {
-    "ring_everywhere": {"DDG_RING_MIN_MB": "0"},                 # k_symv_ring for every SYMV launch
+    "ring_everywhere": {"DDG_RING_MIN_MB": "0"},                 # ring for every SYMV launch (auto consumer)
+    "ring1_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "0"},  # 8-warp column consumers only
     "ring_2tile_slots": {"DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2"},
+    "ring2_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1"},  # row/column-warp consumers
     "classic": {"DDG_SYMV": "classic"},                           # per-item k_symv / k_symv_small
     "coarse_levels": {"DDG_COARSE_DATAFLOW": "0", "DDG_RING_MIN_MB": "0"},  # level-by-level sparse solve
     "csr_rows": {"DDG_NO_STENCIL": "1"},                          # row kernels read the CSR

@@ -150,6 +150,90 @@ __global__ void __launch_bounds__(288) k_read_tma_nc(const double* __restrict__ 
     if (s == 12345.678) out[0] = s;
 }
 
+// K6: like K5 with 4 copies per 32 KB slot, the first copy of each slot of
+// `first` bytes (the rest 8 KB): the cost of a short / unaligned-size copy
+__global__ void __launch_bounds__(288) k_read_tma_first(const double* __restrict__ p, size_t nslots, int S,
+                                                        unsigned first, double* out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = (uint64_t*)smem;
+    uint64_t* empty = full + S;
+    double* ring = (double*)(smem + 1024);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned CH = 32768;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { mb_init(&full[i], 1); mb_init(&empty[i], 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {
+        if (lane) return;
+        unsigned k = 0;
+        for (size_t c = blockIdx.x; c < nslots; c += gridDim.x, ++k) {
+            unsigned slot = k % S, n = k / S;
+            if (n) mb_wait(&empty[slot], (n - 1) & 1);
+            mb_expect(&full[slot], first + 3 * 8192);
+            const char* s0 = (const char*)p + c * CH;
+            char* d0 = (char*)ring + (size_t)slot * CH;
+            bulk(d0, s0, first, &full[slot]);
+            for (int q = 1; q < 4; ++q) bulk(d0 + q * 8192, s0 + q * 8192, 8192, &full[slot]);
+        }
+        return;
+    }
+    double sum = 0;
+    unsigned k = 0;
+    for (size_t c = blockIdx.x; c < nslots; c += gridDim.x, ++k) {
+        unsigned slot = k % S;
+        mb_wait(&full[slot], (k / S) & 1);
+        const double* T = ring + (size_t)slot * 4096;
+        sum += T[warp * 512 + lane];
+        __syncwarp();
+        if (lane == 0) mb_arrive(&empty[slot]);
+    }
+    if (sum == 12345.678) out[0] = sum;
+}
+
+// K7: 4 x 8 KB copies per 32 KB slot; source misaligned by `mis` bytes;
+// `contig`: CTA b streams its own contiguous range (the ring's partition)
+// instead of slots strided across the grid
+__global__ void __launch_bounds__(288) k_read_tma_pat(const double* __restrict__ p, size_t nslots, int S,
+                                                      unsigned mis, int contig, double* out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = (uint64_t*)smem;
+    uint64_t* empty = full + S;
+    double* ring = (double*)(smem + 1024);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned CH = 32768;
+    const size_t per = nslots / gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { mb_init(&full[i], 1); mb_init(&empty[i], 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {
+        if (lane) return;
+        for (size_t k = 0; k < per; ++k) {
+            const size_t c = contig ? blockIdx.x * per + k : blockIdx.x + k * gridDim.x;
+            unsigned slot = k % S, n = k / S;
+            if (n) mb_wait(&empty[slot], (n - 1) & 1);
+            mb_expect(&full[slot], 4 * 8192);
+            const char* s0 = (const char*)p + c * CH + mis;
+            char* d0 = (char*)ring + (size_t)slot * CH;
+            for (int q = 0; q < 4; ++q) bulk(d0 + q * 8192, s0 + q * 8192, 8192, &full[slot]);
+        }
+        return;
+    }
+    double sum = 0;
+    for (size_t k = 0; k < per; ++k) {
+        unsigned slot = k % S;
+        mb_wait(&full[slot], (k / S) & 1);
+        const double* T = ring + (size_t)slot * 4096;
+        sum += T[warp * 512 + lane];
+        __syncwarp();
+        if (lane == 0) mb_arrive(&empty[slot]);
+    }
+    if (sum == 12345.678) out[0] = sum;
+}
+
 int main() {
     const size_t bytes = 8ull << 30, n = bytes / 8;
     double *p, *out;
@@ -201,15 +285,25 @@ int main() {
                 timeit(nm, [&] { k_read_tma<<<148 * cps, 288, sm>>>(p, bytes / CH, CH, S, out); });
             }
         }
-    for (int S : {4, 6})
-        for (int NC : {1, 2, 4, 8})
-            for (int de : {0, 4}) {
-                const size_t sm = 1024 + (size_t)32768 * S;
-                cudaFuncSetAttribute(k_read_tma_nc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                char nm[96];
-                snprintf(nm, sizeof nm, "tma ring 32K slots S=%d copies/slot=%d diag_every=%d", S, NC, de);
-                // (diag copies move fewer bytes: report the nominal 32 KB/slot rate)
-                timeit(nm, [&] { k_read_tma_nc<<<148, 288, sm>>>(p, bytes / 32768, NC, S, de, out); });
+    for (int contig : {0, 1})
+        for (unsigned mis : {0u, 128u, 4224u % 8192u}) {
+            const int S = 5;
+            const size_t sm = 1024 + (size_t)32768 * S;
+            cudaFuncSetAttribute(k_read_tma_pat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            const size_t nslots = bytes / 32768 - 1;
+            const double moved = (double)(nslots / 148) * 148 * 32768;
+            float best = 1e9;
+            for (int r = 0; r < 5; ++r) {
+                cudaEventRecord(e0);
+                k_read_tma_pat<<<148, 288, sm>>>(p, nslots, S, mis, contig, out);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (ms < best) best = ms;
             }
+            printf("4x8KB copies/slot, contiguous-per-CTA %d, source offset %4u B: %8.1f GB/s\n", contig, mis,
+                   moved / (best * 1e-3) / 1e9);
+        }
     return 0;
 }
