@@ -691,20 +691,22 @@ int sparse_coarse_numeric(ddg_ctx* c) {
             return DDG_OK;
         };
         if (dbg && (st = dump("assembled"))) return st;
-        // eliminate the S pivots: small fronts batched, big ones grid-wide
+        // eliminate the S pivots: small fronts one CTA each (tile exchange), the
+        // rest with the blocked exchange (fp64 GEMM updates), each as one batch
         std::vector<int32_t> ids, nTs, nKs;
         std::vector<double*> mats;
-        for (int i = f0; i < f1; ++i) {
-            const FrontDesc& f = sc->fr[i];
-            if (f.nT <= 64) {
+        int nsmall = 0, maxT = 0, maxK = 0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int i = f0; i < f1; ++i) {
+                const FrontDesc& f = sc->fr[i];
+                if ((f.nT < GJB_MIN_T) != (pass == 0)) continue;
                 ids.push_back(i);
                 nTs.push_back(f.nT);
                 nKs.push_back(f.nK);
                 mats.push_back(fptr[i]);
-            } else {
-                launch_gj_big(c->stream, f.nT, f.nK, fptr[i], i, d_err);
+                if (pass == 0) ++nsmall;
+                else { maxT = std::max(maxT, f.nT); maxK = std::max(maxK, f.nK); }
             }
-        }
         if (!ids.empty()) {
             double** d_m = nullptr;
             if ((st = dalloc(&d_m, ids.size()))) return st;
@@ -712,7 +714,11 @@ int sparse_coarse_numeric(ddg_ctx* c) {
             CUDA_TRY(cudaMemcpyAsync(d_nT, nTs.data(), ids.size() * 4, cudaMemcpyHostToDevice, c->stream));
             CUDA_TRY(cudaMemcpyAsync(d_nK, nKs.data(), ids.size() * 4, cudaMemcpyHostToDevice, c->stream));
             CUDA_TRY(cudaMemcpyAsync(d_m, mats.data(), ids.size() * sizeof(double*), cudaMemcpyHostToDevice, c->stream));
-            launch_gj_batched(c->stream, (int)ids.size(), d_nT, d_nK, d_m, d_ids, d_err);
+            if (nsmall) launch_gj_batched(c->stream, nsmall, d_nT, d_nK, d_m, d_ids, d_err);
+            const int nbig = (int)ids.size() - nsmall;
+            if (nbig)
+                launch_gj_blocked(c->stream, nbig, maxT, maxK, d_m + nsmall, d_nT + nsmall, d_nK + nsmall,
+                                  d_ids + nsmall, d_err);
             CUDA_TRY(cudaStreamSynchronize(c->stream));
             cudaFree(d_m);
         }

@@ -216,6 +216,12 @@ void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, cons
 void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32_t* nK,
                        double* const* mats, const int32_t* ids, int32_t* err);
 void launch_gj_big(cudaStream_t st, int nT, int nK, double* M, int id, int32_t* err);
+// blocked exchange (128-column pivot blocks, fp64 GEMM updates) over a batch,
+// used for matrices of at least GJB_MIN_T tiles per side;
+// mats/nT/nK/ids are device arrays of nmat entries, maxT/maxK their maxima
+constexpr int GJB_MIN_T = 16;
+void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* const* mats, const int32_t* nT,
+                       const int32_t* nK, const int32_t* ids, int32_t* err);
 // sparse coarse factorisation / solve
 void launch_front_scatter(cudaStream_t st, int64_t ntrip, const int32_t* frow, const int32_t* fcol,
                           const double* fval, const int32_t* ffront, const FrontDesc* fronts,

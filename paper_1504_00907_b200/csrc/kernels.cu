@@ -2166,6 +2166,167 @@ __global__ void __launch_bounds__(256) k_gj_colpanel(double* M, int nT, int k) {
     if (i < nT && i != k) warp_right_mul(M + ((int64_t)k * nT + i) * TILE_ELEMS, Ps);
 }
 
+// ---- blocked Gauss-Jordan exchange (setup) ----------------
+// The same exchange with pivot blocks of GJB_BT tiles (128 columns): per
+// block, P = A_kk^{-1} (tile exchange restricted to the block, one CTA), then
+// A_kj <- -P A_kj, A_ij <- A_ij + A_ik A_kj, A_ik <- A_ik P as register-blocked
+// fp64 GEMMs (k_gjb_gemm): the matrix streams through HBM once per 128
+// columns instead of once per 32, and each pass does 128 FMAs per element.
+// A batch of matrices (tiled layout, possibly different sizes) runs together;
+// matrix b has nT[b] tiles per side and eliminates its first nK[b] tiles.
+constexpr int GJB_BT = 4;                  // pivot block / output block side (tiles)
+constexpr int GJB_N = GJB_BT * TILE;       // 128
+constexpr int GJB_BPAD = GJB_N + 2;        // padded row of the transposed B stage
+
+struct GJBatch {
+    double* const* mats;
+    const int32_t* nT;
+    const int32_t* nK;
+    const int32_t* ids;
+    int32_t* err;
+};
+
+// P = inverse of the pivot block [k0, k0 + nb) (tile exchange inside the block)
+__global__ void __launch_bounds__(256) k_gjb_pivot(GJBatch bt, int k0) {
+    extern __shared__ double gjsm[];
+    double* Ps = gjsm;
+    double (*Bs)[TILE_ELEMS] = reinterpret_cast<double (*)[TILE_ELEMS]>(gjsm + TILE_ELEMS);
+    const int b = blockIdx.x;
+    const int nT = bt.nT[b], nK = bt.nK[b];
+    if (k0 >= nK) return;
+    const int k1 = min(k0 + GJB_BT, nK);
+    double* M = bt.mats[b];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto tile = [&](int I, int J) { return M + ((int64_t)J * nT + I) * TILE_ELEMS; };
+    for (int k = k0; k < k1; ++k) {
+        for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = tile(k, k)[e];
+        __syncthreads();
+        tile_exchange_inverse(Ps, bt.err, bt.ids[b], k * TILE);
+        for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) tile(k, k)[e] = Ps[e];
+        for (int j = k0 + w; j < k1; j += 8)
+            if (j != k) warp_left_mul(Ps, tile(k, j), tile(k, j), Bs[w], -1.0);
+        __syncthreads();
+        for (int j = k0 + w; j < k1; j += 8) {
+            if (j == k) continue;
+            const double* B = tile(k, j);
+            for (int c = 0; c < TILE; ++c) Bs[w][c * TILE + lane] = B[c * TILE + lane];
+            __syncwarp();
+            for (int i = k0; i < k1; ++i)
+                if (i != k) warp_gemm_acc(tile(i, k), Bs[w], tile(i, j));
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int i = k0 + w; i < k1; i += 8)
+            if (i != k) warp_right_mul(tile(i, k), Ps);
+        __syncthreads();
+    }
+}
+
+// mode 0 (row panel):  C(kb, J) = -P C(kb, J)          for tile columns J outside kb
+// mode 1 (trailing):   C(I, J) += C(I, kb) C(kb, J)     for I, J outside kb
+// mode 2 (col panel):  C(I, kb) = C(I, kb) P            for tile rows I outside kb
+// CTA: a 4 x 4-tile (128 x 128) output block; thread: 8 x 8 elements.
+// grid.x: output blocks of one matrix (by 4-tile rows and columns), grid.y: batch
+__global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) {
+    extern __shared__ double gsm[];
+    double* As = gsm;                               // [TILE][GJB_N]   A(row, kk), kk-major
+    double* Bs = gsm + TILE * GJB_N;                // [TILE][GJB_BPAD] B(kk, col), kk-major
+    const int b = blockIdx.y;
+    const int nT = bt.nT[b], nK = bt.nK[b];
+    if (k0 >= nK) return;
+    const int k1 = min(k0 + GJB_BT, nK);
+    const int nb = (nT + GJB_BT - 1) / GJB_BT;      // output blocks per side
+    int bi, bj;
+    if (mode == 1) {
+        if ((int)blockIdx.x >= nb * nb) return;
+        bi = blockIdx.x % nb;
+        bj = blockIdx.x / nb;
+    } else {
+        if ((int)blockIdx.x >= nb) return;
+        bi = mode == 0 ? k0 / GJB_BT : blockIdx.x;
+        bj = mode == 0 ? blockIdx.x : k0 / GJB_BT;
+    }
+    const int i0 = bi * GJB_BT, j0 = bj * GJB_BT;
+    auto in_kb = [&](int t) { return t >= k0 && t < k1; };
+    // does this block own any output tile?
+    {
+        bool any = false;
+        for (int I = i0; I < min(i0 + GJB_BT, nT); ++I)
+            for (int J = j0; J < min(j0 + GJB_BT, nT); ++J) {
+                const bool ok = mode == 0 ? (in_kb(I) && !in_kb(J))
+                              : mode == 1 ? (!in_kb(I) && !in_kb(J)) : (!in_kb(I) && in_kb(J));
+                any |= ok;
+            }
+        if (!any) return;
+    }
+    double* M = bt.mats[b];
+    auto tile = [&](int I, int J) { return M + ((int64_t)J * nT + I) * TILE_ELEMS; };
+    const int tr = (threadIdx.x >> 4) * 8;          // output rows tr..tr+7 (one tile row)
+    const int tc = (threadIdx.x & 15) * 2;          // output cols 32 m + tc, +1 (m = 0..3): consecutive
+                                                    // lanes read consecutive 16 B of a B row
+    double acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+    // inner dimension: the pivot block's tiles q (A's column tile, B's row tile)
+    for (int q = k0; q < k1; ++q) {
+        // A = (rows i0.., tile column q) [mode 0: P = (kb, q)]; B = (tile row q, cols j0..) [mode 2: P]
+        for (int e = threadIdx.x; e < GJB_BT * TILE_ELEMS; e += 256) {
+            const int ti = e / TILE_ELEMS, o = e % TILE_ELEMS;   // o = kk * 32 + r
+            const int I = (mode == 0 ? k0 : i0) + ti;
+            const int kk = o / TILE, r = o % TILE;
+            As[kk * GJB_N + ti * TILE + r] = (I < nT && (mode != 0 || I < k1)) ? tile(I, q)[o] : 0.0;
+        }
+        for (int e = threadIdx.x; e < GJB_BT * TILE_ELEMS; e += 256) {
+            const int tj = e / TILE_ELEMS, o = e % TILE_ELEMS;   // o = c * 32 + kk
+            const int J = (mode == 2 ? k0 : j0) + tj;
+            const int c = o / TILE, kk = o % TILE;
+            Bs[kk * GJB_BPAD + tj * TILE + c] = (J < nT && (mode != 2 || J < k1)) ? tile(q, J)[o] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < TILE; ++kk) {
+            double a[8], bv[8];
+            const double2* ap = reinterpret_cast<const double2*>(As + kk * GJB_N + tr);
+            const double* brow = Bs + kk * GJB_BPAD + tc;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double2 x = ap[u], y = *reinterpret_cast<const double2*>(brow + u * TILE);
+                a[2 * u] = x.x; a[2 * u + 1] = x.y;
+                bv[2 * u] = y.x; bv[2 * u + 1] = y.y;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[r][c] = fma(a[r], bv[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+    // epilogue: rows tr..tr+7 lie in tile row I; columns 2u, 2u+1 of acc are
+    // columns tc, tc+1 of tile column j0 + u
+    const int I = i0 + tr / TILE;
+    if (I >= nT) return;
+    const int rr = tr % TILE;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int J = j0 + u;
+        if (J >= nT) break;
+        const bool ok = mode == 0 ? (in_kb(I) && !in_kb(J)) : mode == 1 ? (!in_kb(I) && !in_kb(J))
+                                                                         : (!in_kb(I) && in_kb(J));
+        if (!ok) continue;
+        double* T = tile(I, J);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double* p = T + (tc + c) * TILE + rr + r;
+                const double v = acc[r][2 * u + c];
+                *p = mode == 1 ? *p + v : (mode == 0 ? -v : v);
+            }
+    }
+}
+
 // Dense tiled A_c from its lower-triangle entries (mirrored => exactly symmetric,
 // reading R9); identity on the padding.
 __global__ void k_scatter_coarse(int64_t nent, const int32_t* __restrict__ row,
@@ -2620,6 +2781,27 @@ void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32
     const int smem = 9 * TILE_ELEMS * sizeof(double);
     cudaFuncSetAttribute(k_gj_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_gj_batched<<<nmat, 256, smem, st>>>(nT, nK, mats, ids, err);
+}
+
+void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* const* mats, const int32_t* nT,
+                       const int32_t* nK, const int32_t* ids, int32_t* err) {
+    if (nmat <= 0) return;
+    static bool init = false;
+    const int smem_p = 9 * TILE_ELEMS * sizeof(double);
+    const int smem_g = (TILE * GJB_N + TILE * GJB_BPAD) * sizeof(double);
+    if (!init) {
+        cudaFuncSetAttribute(k_gjb_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p);
+        cudaFuncSetAttribute(k_gjb_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);
+        init = true;
+    }
+    GJBatch bt{mats, nT, nK, ids, err};
+    const int nb = (maxT + GJB_BT - 1) / GJB_BT;
+    for (int k0 = 0; k0 < maxK; k0 += GJB_BT) {
+        k_gjb_pivot<<<nmat, 256, smem_p, st>>>(bt, k0);
+        k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 0);
+        k_gjb_gemm<<<dim3(nb * nb, nmat), 256, smem_g, st>>>(bt, k0, 1);
+        k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 2);
+    }
 }
 
 void launch_gj_big(cudaStream_t st, int nT, int nK, double* M, int id, int32_t* err) {

@@ -694,11 +694,12 @@ static int invert_locals(ddg_ctx* c) {
     const int64_t cap = std::max<int64_t>(budget / 8, max_single);
     int st = dalloc(&scratch, cap);
     if (st) return st;
-    int32_t *d_ids = nullptr, *d_err = nullptr, *d_nT = nullptr;
+    int32_t *d_ids = nullptr, *d_err = nullptr, *d_nT = nullptr, *d_ids2 = nullptr, *d_nT2 = nullptr;
     int64_t* d_soff = nullptr;
-    double** d_ptr = nullptr;
+    double **d_ptr = nullptr, **d_ptr2 = nullptr;
     if ((st = dalloc(&d_ids, np)) || (st = dalloc(&d_soff, np)) || (st = dalloc(&d_err, 2)) ||
-        (st = dalloc(&d_nT, np)) || (st = dalloc(&d_ptr, np))) {
+        (st = dalloc(&d_nT, np)) || (st = dalloc(&d_ptr, np)) || (st = dalloc(&d_ids2, np)) ||
+        (st = dalloc(&d_nT2, np)) || (st = dalloc(&d_ptr2, np))) {
         cudaFree(scratch);
         return st;
     }
@@ -728,7 +729,30 @@ static int invert_locals(ddg_ctx* c) {
         CUDA_TRY(cudaMemcpyAsync(d_nT, nTs.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
         CUDA_TRY(cudaMemcpyAsync(d_ptr, ptrs.data(), nb * sizeof(double*), cudaMemcpyHostToDevice, c->stream));
         launch_extract_local(c->stream, (int)nb, d_ids, c->d_ops, c->d_oidx, c->A, scratch, d_soff);
-        launch_gj_batched(c->stream, (int)nb, d_nT, d_nT, d_ptr, d_ids, d_err);
+        // small operators: one CTA each (tile exchange); operators of >= GJB_MIN_T
+        // tiles: blocked exchange with fp64 GEMM updates (entries [nsmall, nb))
+        {
+            std::vector<int> order(nb);
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_partition(order.begin(), order.end(), [&](int i) { return nTs[i] < GJB_MIN_T; });
+            std::vector<int32_t> oids(nb), onT(nb);
+            std::vector<double*> optr(nb);
+            int nsmall = 0, maxT = 0;
+            for (size_t i = 0; i < nb; ++i) {
+                oids[i] = ids[order[i]];
+                onT[i] = nTs[order[i]];
+                optr[i] = ptrs[order[i]];
+                if (onT[i] < GJB_MIN_T) ++nsmall;
+                else maxT = std::max(maxT, onT[i]);
+            }
+            CUDA_TRY(cudaMemcpyAsync(d_ids2, oids.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(d_nT2, onT.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(d_ptr2, optr.data(), nb * sizeof(double*), cudaMemcpyHostToDevice, c->stream));
+            if (nsmall) launch_gj_batched(c->stream, nsmall, d_nT2, d_nT2, d_ptr2, d_ids2, d_err);
+            if ((int)nb > nsmall)
+                launch_gj_blocked(c->stream, (int)nb - nsmall, maxT, maxT, d_ptr2 + nsmall, d_nT2 + nsmall,
+                                  d_nT2 + nsmall, d_ids2 + nsmall, d_err);
+        }
         launch_pack(c->stream, (int)nb, d_ids, c->d_ops, c->d_items, scratch, d_soff, c->d_tiles);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -740,6 +764,9 @@ static int invert_locals(ddg_ctx* c) {
     cudaFree(d_err);
     cudaFree(d_nT);
     cudaFree(d_ptr);
+    cudaFree(d_ids2);
+    cudaFree(d_nT2);
+    cudaFree(d_ptr2);
     if (herr[0] >= 0)
         return set_err(DDG_E_NOT_SPD,
                        "local inverse: subdomain %d not positive definite at pivot %d",
@@ -774,8 +801,8 @@ static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::
     { int _s = h2d(c->stream, d_nT, &nT, 4); if (_s) return _s; }
     { int _s = h2d(c->stream, d_ptr, &M, sizeof(double*)); if (_s) return _s; }
     launch_scatter_coarse(c->stream, (int64_t)ev.size(), d_r, d_c, d_v, op.nT, op.m, M);
-    if (op.nT <= 64) launch_gj_batched(c->stream, 1, d_nT, d_nT, d_ptr, d_ids, d_err);
-    else launch_gj_big(c->stream, op.nT, op.nT, M, id, d_err);
+    if (op.nT < GJB_MIN_T) launch_gj_batched(c->stream, 1, d_nT, d_nT, d_ptr, d_ids, d_err);
+    else launch_gj_blocked(c->stream, 1, op.nT, op.nT, d_ptr, d_nT, d_nT, d_ids, d_err);
     launch_pack(c->stream, 1, d_ids, c->d_ops, c->d_items, M, d_soff, c->d_tiles);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(c->stream));
