@@ -49,6 +49,9 @@ def lib():
         L.or_pcg.argtypes = [vp, vp, f64, C.c_int, C.c_int, vp, C.POINTER(C.c_int), vp,
                              C.POINTER(C.c_int)]
         L.or_pcg.restype = C.c_int
+        L.or_pcg_ab.argtypes = [vp, vp, f64, C.c_int, C.c_int, vp, C.POINTER(C.c_int), vp,
+                                C.POINTER(C.c_int), vp, vp]
+        L.or_pcg_ab.restype = C.c_int
         L.or_info.argtypes = [vp, vp]
         L.or_info.restype = None
         L.or_min_rank_ratio.argtypes = [vp]
@@ -143,6 +146,23 @@ class Oracle:
             raise OracleError(st, lib().or_last_error().decode())
         return u, it.value, hist[: it.value + 1].copy(), bool(conv.value)
 
+    def pcg_lanczos(self, f, rtol=1e-8, max_iter=1000, stop_mode=STOP_RES0):
+        """pcg plus the CG coefficients: returns (u, iters, hist, converged,
+        alphas[iters], betas[iters - 1]) (betas of the directions actually used)."""
+        f = np.ascontiguousarray(f, np.float64)
+        u = np.empty(self.n)
+        hist = np.zeros(max_iter + 1)
+        al = np.zeros(max_iter + 1)
+        be = np.zeros(max_iter + 1)
+        it = C.c_int(0)
+        conv = C.c_int(0)
+        st = lib().or_pcg_ab(self._h, _p(f), float(rtol), int(max_iter), int(stop_mode), _p(u),
+                             C.byref(it), _p(hist), C.byref(conv), _p(al), _p(be))
+        if st:
+            raise OracleError(st, lib().or_last_error().decode())
+        k = it.value
+        return u, k, hist[: k + 1].copy(), bool(conv.value), al[:k].copy(), be[: max(k - 1, 0)].copy()
+
     def colours(self):
         c = np.empty(self.nparts, np.int32)
         lib().or_get_colours(self._h, _p(c))
@@ -185,3 +205,32 @@ def fractional_iterations(hist, tol_abs):
             a, b = np.log10(h[k - 1]), np.log10(h[k])
             return (k - 1) + (a - lt) / (a - b)
     return float("inf")
+
+
+def lanczos_tridiagonal(alphas, betas):
+    """The Lanczos tridiagonal of a (P)CG run from its coefficients (the
+    standard CG-Lanczos relation, SPEC.md:383-385): diagonal 1/a_k + b_{k-1}/a_{k-1}
+    (b_{-1}/a_{-1} = 0), off-diagonal sqrt(b_k)/a_k."""
+    a = np.asarray(alphas, float)
+    b = np.asarray(betas, float)[: max(len(a) - 1, 0)]
+    k = len(a)
+    T = np.zeros((k, k))
+    for j in range(k):
+        T[j, j] = 1.0 / a[j] + (b[j - 1] / a[j - 1] if j > 0 else 0.0)
+        if j + 1 < k:
+            T[j, j + 1] = T[j + 1, j] = np.sqrt(b[j]) / a[j]
+    return T
+
+
+def condition_estimate(alphas, betas, tol):
+    """kappa = lambda_max / lambda_min of the Lanczos tridiagonal (an estimate
+    of cond(M A)) and the classical CG iteration bound
+    ln(2/tol) / ln((sqrt(kappa)+1)/(sqrt(kappa)-1)) (SPEC.md:383-387); fewer
+    than 2 coefficients: kappa = 1."""
+    if len(alphas) < 2:
+        return 1.0, 1.0
+    ev = np.linalg.eigvalsh(lanczos_tridiagonal(alphas, betas))
+    kappa = float(ev[-1] / ev[0])
+    sk = np.sqrt(kappa)
+    bound = float(np.log(2.0 / tol) / np.log((sk + 1) / (sk - 1))) if kappa > 1 else 1.0
+    return kappa, bound

@@ -703,8 +703,18 @@ int or_apply_precond(or_ctx* c, const double* r, double* z) {
  * A p products (R16).  stop_mode: 0 ||r_k|| <= rtol ||r_0||; 1 <= rtol ||r_1||
  * (SPEC.md:398); 2 sqrt(r_k^T z_k) <= rtol sqrt(r_0^T z_0)  (reading R1).
  * ------------------------------------------------------------------------- */
+/* PCG as in or_pcg, also recording the CG coefficients alpha_k, beta_k
+ * ("condition number estimates derived from the Lanczos
+ * coefficients computed during CG"); alphas/betas may be NULL. */
+int or_pcg_ab(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode, double* u,
+              int* iters, double* hist, int* converged, double* alphas, double* betas);
 int or_pcg(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode, double* u,
            int* iters, double* hist, int* converged) {
+    return or_pcg_ab(c, f, rtol, max_iter, stop_mode, u, iters, hist, converged, NULL, NULL);
+}
+
+int or_pcg_ab(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode, double* u,
+              int* iters, double* hist, int* converged, double* alphas, double* betas) {
     int64_t n = c->n;
     double *r = malloc(n * sizeof(double)), *z = malloc(n * sizeof(double)),
            *p = malloc(n * sizeof(double)), *q = malloc(n * sizeof(double));
@@ -727,6 +737,7 @@ int or_pcg(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode,
         double sigma = dot(n, p, q);
         if (!(sigma > 0.0)) { st = fail(OR_E_BREAKDOWN, "p^T A p <= 0 at iteration %d", it); goto done; }
         double alpha = rho / sigma;
+        if (alphas) alphas[it] = alpha;
         for (int64_t v = 0; v < n; v++) { u[v] += alpha * p[v]; r[v] -= alpha * q[v]; }
         double res = sqrt(dot(n, r, r));
         hist[it + 1] = res;
@@ -739,6 +750,7 @@ int or_pcg(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode,
         if (stop_mode == 2 && sqrt(fabs(rho1)) <= rtol * pres0) { *converged = 1; break; }
         if (!(rho1 > 0.0)) { st = fail(OR_E_BREAKDOWN, "r^T z <= 0 at iteration %d", it + 1); goto done; }
         double beta = rho1 / rho;
+        if (betas) betas[it] = beta;
         rho = rho1;
         for (int64_t v = 0; v < n; v++) p[v] = z[v] + beta * p[v];
     }

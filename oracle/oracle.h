@@ -34,6 +34,9 @@ int or_coarse_correct(or_ctx* c, const double* r, double* z);
 int or_spmv(or_ctx* c, const double* x, double* y);
 int or_pcg(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode,
            double* u, int* iters, double* hist, int* converged);
+/* the same, recording alpha_k (k < iters) and beta_k (k < iters - 1 or iters) */
+int or_pcg_ab(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode,
+              double* u, int* iters, double* hist, int* converged, double* alphas, double* betas);
 /* info[0..9] = n, n_c, nparts, ncolours, m_min, m_max, k, dropped, (unused), (unused) */
 void or_info(or_ctx* c, int64_t* info);
 double or_min_rank_ratio(or_ctx* c);

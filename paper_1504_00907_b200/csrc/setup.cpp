@@ -970,6 +970,8 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
             if ((st = upload(&c->d_stencil_coef, scoef))) { free_ctx(c); return st; }
             ds.coef = c->d_stencil_coef;
         }
+        if (const char* e = getenv("DDG_ROW_SW")) sw = atoi(e);   // experiment: lanes per CSR row
+        if (sw != 1 && sw != 4 && sw != 8 && sw != 32) sw = 8;
         if (ds.kind) sw = 1;
         c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val, sw, 0, ds};
         c->opts.stencil = nullptr;   // borrowed for the duration of ddg_setup only

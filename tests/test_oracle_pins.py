@@ -433,3 +433,37 @@ def test_spmv_golden():
     g = GOLD["spmv_tridiag"]
     o = make_oracle_dense(laplace1d(3), np.ones((3, 1)), np.zeros(3), 1)
     assert o.spmv(np.array(g["x"], float)).tolist() == g["y"]
+
+
+# ---------------------------------------------------------------- Lanczos condition estimate
+def test_lanczos_condition_estimate_matches_dense_spectrum():
+    """PAPER.md:617-621 (iteration bounds from "condition number estimates
+    derived from the Lanczos coefficients computed during CG"): on a tiny
+    problem run to tight tolerance, the Ritz values of the CG-Lanczos
+    tridiagonal lie in the spectrum of M A, and kappa = lambda_max/lambda_min
+    matches a dense eigensolve of M A (M built column by column)."""
+    pr = P.poisson2d(12, 4, 1, 31)
+    o = oracle.Oracle.from_problem(pr)
+    A = pr.dense()
+    M = np.column_stack([o.apply_precond(e) for e in np.eye(pr.n)])
+    ev = np.sort(np.linalg.eigvals(M @ A).real)
+    u, it, hist, conv, al, be = o.pcg_lanczos(pr.f, 1e-13, 200)
+    assert conv and len(al) == it and len(be) == it - 1
+    T = oracle.lanczos_tridiagonal(al, be)
+    ritz = np.linalg.eigvalsh(T)
+    assert ritz[0] >= ev[0] * (1 - 1e-9) and ritz[-1] <= ev[-1] * (1 + 1e-9)
+    kappa, bound = oracle.condition_estimate(al, be, 1e-13)
+    assert abs(kappa - ev[-1] / ev[0]) <= 0.02 * (ev[-1] / ev[0]), (kappa, ev[-1] / ev[0])
+    # the classical bound ln(2/tol)/ln((sqrt k + 1)/(sqrt k - 1)) is an upper bound on the count
+    assert bound >= it - 1
+
+
+def test_lanczos_trivial_cases():
+    """One subdomain covering everything: M = A^{-1}, one
+    iteration, a single coefficient, kappa = 1; alpha = 1 exactly in theory."""
+    pr = P.poisson2d(10, 10, 1, 32)
+    o = oracle.Oracle.from_problem(pr)
+    u, it, hist, conv, al, be = o.pcg_lanczos(pr.f, 1e-10)
+    assert it == 1 and conv and len(al) == 1
+    assert abs(al[0] - 1.0) <= 1e-10
+    assert oracle.condition_estimate(al, be, 1e-10) == (1.0, 1.0)
