@@ -260,6 +260,8 @@ def bench_ddg(args):
                    "coarse": "dense packed inverse" if s.info.coarse_variant == 1 else "sparse nested dissection", "parallelism": f"subdomain-sharded x{world} (NCCL halos + allreduce, replicated coarse)" if world > 1 else "1gpu",
                    "l2": "inputs larger than L2 (local inverses %.1f GB)" % (s.info.local_factor_bytes / 1e9),
                    "time_to_rtol_ms": ms_step, "t_setup_s": round(t_setup, 2),
+                   "cond_est_lanczos": round(float(rep.cond_est), 3),
+                   "cg_iteration_bound": round(float(rep.iter_bound), 2),
                    "local_operator_bytes": int(s.info.local_factor_bytes),
                    "coarse_solve_bytes": int(s.info.coarse_solve_bytes)},
         "roofline": {"bound": "hbm", "kernel": "k_symv (colour sweep, a4/a8)",

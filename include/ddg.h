@@ -113,6 +113,9 @@ typedef struct {
     double t_setup;       /* seconds spent in ddg_setup (host clock around device work)          */
     double t_solve;       /* seconds of the last solve (CUDA events on the context stream)       */
     double frac_iters;    /* fractional iteration count                       */
+    double cond_est;      /* Lanczos estimate of cond(M A) from the CG coefficients:
+                             lambda_max / lambda_min of the CG-Lanczos tridiagonal; 1 if < 2 steps */
+    double iter_bound;    /* classical CG bound ln(2/rtol) / ln((sqrt k + 1)/(sqrt k - 1)), k = cond_est */
 } ddg_report;
 
 typedef struct {
@@ -192,6 +195,11 @@ int ddg_spmv(ddg_ctx* ctx, const double* x, double* y);
 
 /* Size and diagnostics of a built context. */
 int ddg_get_info(ddg_ctx* ctx, ddg_info* info);
+
+/* CG coefficients of the last solve: alphas[k] for k < iters and betas[k] for
+ * k < iters - 1 (host, out, up to cap entries each; either may be NULL).
+ * Returns iters (the number of alphas), or a negative status. */
+int ddg_get_lanczos(ddg_ctx* ctx, double* alphas, double* betas, int cap);
 
 /* colour[nparts]: colour of every subdomain in the multiplicative sweep (host, out). */
 int ddg_get_colours(ddg_ctx* ctx, int32_t* colour);

@@ -90,6 +90,8 @@ struct ddg_ctx {
            *d_u = nullptr, *d_x = nullptr;
     Scalars* d_sc = nullptr;
     double* d_hist = nullptr;
+    double* d_ab = nullptr;             // CG coefficients of the current solve (Scalars::ab)
+    std::vector<double> last_alpha, last_beta;
     int hist_cap = 0;
     double* d_redbuf = nullptr;
     unsigned* d_ticket = nullptr;

@@ -104,6 +104,7 @@ struct Scalars {
     int32_t stop_mode, converged, pad0, pad1;
     double loc[5];   // multi-GPU: rank-local sums (init, rz_first, spmv_dot, update, rz)
     double glob[5];  // ... and their allreduced totals
+    double* ab;      // CG coefficients: alpha_k at ab[2k], beta_k at ab[2k+1] (Lanczos estimate)
 };
 
 // Reduction scratch: per-block partial sums + a ticket counter.

@@ -185,6 +185,7 @@ __device__ void fin_spmv_dot(Scalars* sc, double s) {
         sc->done = 1;
     } else {
         sc->alpha = sc->rho / s;
+        if (sc->ab) sc->ab[2 * sc->iter] = sc->alpha;
     }
 }
 __device__ void fin_update(Scalars* sc, double* hist, double s) {
@@ -215,6 +216,7 @@ __device__ void fin_rz(Scalars* sc, double s) {
     } else {
         sc->beta = s / sc->rho;
         sc->rho = s;
+        if (sc->ab) sc->ab[2 * (sc->iter - 1) + 1] = sc->beta;
     }
 }
 

@@ -168,7 +168,7 @@ static void free_ctx(ddg_ctx* c) {
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
                     c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
-                    c->d_ring, c->d_gidx, c->d_stencil_coef};
+                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -1227,14 +1227,63 @@ static void enqueue_iteration(ddg_ctx* c, double* u) {
     enqueue_step_b(c);
 }
 
+// Lanczos condition estimate from the CG coefficients:
+// tridiagonal T with T_kk = 1/a_k + b_{k-1}/a_{k-1}, T_{k,k+1} = sqrt(b_k)/a_k;
+// its extreme eigenvalues by Sturm-count bisection; kappa = max/min and the
+// classical CG bound ln(2/tol) / ln((sqrt(kappa)+1)/(sqrt(kappa)-1)).
+static void lanczos_condition(const std::vector<double>& a, const std::vector<double>& b, double tol,
+                              double* kappa, double* bound) {
+    *kappa = 1.0;
+    *bound = 1.0;
+    const int k = (int)a.size();
+    if (k < 2) return;
+    std::vector<double> d(k), e(k, 0.0);
+    for (int j = 0; j < k; ++j) {
+        d[j] = 1.0 / a[j] + (j > 0 ? b[j - 1] / a[j - 1] : 0.0);
+        if (j + 1 < k) e[j] = sqrt(b[j]) / a[j];
+    }
+    double lo = INFINITY, hi = -INFINITY;                     // Gershgorin interval
+    for (int j = 0; j < k; ++j) {
+        const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + fabs(e[j]);
+        lo = std::min(lo, d[j] - r);
+        hi = std::max(hi, d[j] + r);
+    }
+    auto below = [&](double x) {                              // eigenvalues < x (Sturm sequence)
+        int cnt = 0;
+        double q = 1.0;
+        for (int j = 0; j < k; ++j) {
+            q = d[j] - x - (j > 0 ? e[j - 1] * e[j - 1] / q : 0.0);
+            if (q == 0.0) q = -1e-300;
+            if (q < 0.0) ++cnt;
+        }
+        return cnt;
+    };
+    auto kth = [&](int want) {                                // smallest x with below(x) >= want
+        double l = lo, h = hi;
+        for (int it = 0; it < 200; ++it) {
+            const double m = 0.5 * (l + h);
+            if (below(m) >= want) h = m; else l = m;
+        }
+        return 0.5 * (l + h);
+    };
+    const double lmin = kth(1), lmax = kth(k);
+    if (!(lmin > 0.0)) return;
+    *kappa = lmax / lmin;
+    const double sk = sqrt(*kappa);
+    if (*kappa > 1.0) *bound = log(2.0 / tol) / log((sk + 1.0) / (sk - 1.0));
+}
+
 static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int max_iter,
                    int* iters, double* res_hist, int cap, ddg_report* rep) {
     if (!(rtol > 0)) return set_err(DDG_E_ARG, "rtol must be > 0");
     if (max_iter <= 0) max_iter = c->opts.max_iter;
     if (max_iter + 1 > c->hist_cap) {
         if (c->d_hist) cudaFree(c->d_hist);
+        if (c->d_ab) cudaFree(c->d_ab);
         c->d_hist = nullptr;
+        c->d_ab = nullptr;
         int st = dalloc(&c->d_hist, max_iter + 1);
+        if (!st) st = dalloc(&c->d_ab, 2 * (size_t)(max_iter + 1));
         if (st) return st;
         c->hist_cap = max_iter + 1;
         if (c->ge_iter) { cudaGraphExecDestroy(c->ge_iter); c->ge_iter = nullptr; }   // d_hist is baked in
@@ -1246,6 +1295,7 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     init.rtol = rtol;
     init.max_iter = max_iter;
     init.stop_mode = c->opts.stop_mode;
+    init.ab = c->d_ab;
     *c->h_sc = init;
     CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_sc, c->h_sc, sizeof(Scalars), cudaMemcpyHostToDevice, c->stream));
@@ -1332,6 +1382,18 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         rep->t_setup = c->t_setup;
         rep->t_solve = ms * 1e-3;
         rep->frac_iters = (double)it;
+        rep->cond_est = 1.0;
+        rep->iter_bound = 1.0;
+        c->last_alpha.clear();
+        c->last_beta.clear();
+        if (it >= 1) {
+            std::vector<double> ab(2 * (size_t)it);
+            if (d2h(c->stream, ab.data(), c->d_ab, ab.size() * sizeof(double)) == DDG_OK) {
+                for (int k = 0; k < it; ++k) c->last_alpha.push_back(ab[2 * k]);
+                for (int k = 0; k + 1 < it; ++k) c->last_beta.push_back(ab[2 * k + 1]);
+                lanczos_condition(c->last_alpha, c->last_beta, rtol, &rep->cond_est, &rep->iter_bound);
+            }
+        }
         if (it >= 1 && s.converged && s.res > 0) {
             std::vector<double> h(it + 1);
             if (d2h(c->stream, h.data(), c->d_hist, (it + 1) * sizeof(double)) == DDG_OK) {
@@ -1557,3 +1619,14 @@ extern "C" void ddg_plan_destroy(ddg_plan* p) { delete p; }
 // debug (not part of include/ddg.h): k_symv_ring role/wait cycle counters
 // accumulated since the last call (DDG_RING_TRACE=1); 24 values
 extern "C" int ddg_debug_ring_trace(unsigned long long* out) { return symv_ring_trace(out); }
+
+// CG coefficients of the last solve (include/ddg.h)
+extern "C" int ddg_get_lanczos(ddg_ctx* c, double* alphas, double* betas, int cap) {
+    if (!c) return set_err(DDG_E_ARG, "null argument");
+    const int k = (int)c->last_alpha.size();
+    for (int j = 0; j < std::min(k, cap); ++j) {
+        if (alphas) alphas[j] = c->last_alpha[j];
+        if (betas && j + 1 < k) betas[j] = c->last_beta[j];
+    }
+    return k;
+}

@@ -26,7 +26,7 @@ EXPORTS = ["ddg_default_opts", "ddg_setup", "ddg_pcg_solve", "ddg_pcg_solve_devi
            "ddg_apply_precond", "ddg_coarse_correct", "ddg_spmv", "ddg_get_info",
            "ddg_get_colours", "ddg_get_subdomain_sizes", "ddg_launch_count", "ddg_destroy",
            "ddg_status_string", "ddg_last_error", "ddg_set_profiling", "ddg_get_kernel_stats",
-           "ddg_get_unique_id", "ddg_comm_init", "ddg_comm_destroy", "ddg_plan_create",
+           "ddg_get_unique_id", "ddg_comm_init", "ddg_comm_destroy", "ddg_plan_create", "ddg_get_lanczos",
            "ddg_plan_query", "ddg_plan_destroy"]
 
 PLAN = dict(OWNED_ROWS=0, OWNED_SUBS=1, P_SEND=2, P_RECV=3, R_SEND=4, R_RECV=5, Z_SEND=6, Z_RECV=7,
@@ -53,7 +53,7 @@ class ddg_opts(C.Structure):
 class ddg_report(C.Structure):
     _fields_ = [("converged", C.c_int), ("iters", C.c_int), ("res0", C.c_double),
                 ("res_final", C.c_double), ("t_setup", C.c_double), ("t_solve", C.c_double),
-                ("frac_iters", C.c_double)]
+                ("frac_iters", C.c_double), ("cond_est", C.c_double), ("iter_bound", C.c_double)]
 
 
 class ddg_info(C.Structure):
@@ -103,6 +103,8 @@ def load(path: str = LIB_PATH):
     L.ddg_get_info.argtypes = [vp, C.POINTER(ddg_info)]
     L.ddg_get_info.restype = C.c_int
     L.ddg_get_colours.argtypes = [vp, vp]
+    L.ddg_get_lanczos.argtypes = [vp, vp, vp, C.c_int]
+    L.ddg_get_lanczos.restype = C.c_int
     L.ddg_get_subdomain_sizes.argtypes = [vp, vp]
     L.ddg_launch_count.argtypes = [vp, C.c_int]
     L.ddg_launch_count.restype = i64
@@ -271,6 +273,16 @@ class Solver:
 
     def spmv(self, x):
         return self._vec("ddg_spmv", x)
+
+    def lanczos(self):
+        """(alphas[iters], betas[iters - 1]) of the last solve (ddg_get_lanczos)."""
+        k = load().ddg_get_lanczos(self._h, None, None, 0)
+        if k < 0:
+            _check(-k)
+        a = np.zeros(max(k, 1))
+        b = np.zeros(max(k, 1))
+        load().ddg_get_lanczos(self._h, _p(a), _p(b), k)
+        return a[:k].copy(), b[: max(k - 1, 0)].copy()
 
     def colours(self):
         c = np.empty(self.info.nparts, np.int32)

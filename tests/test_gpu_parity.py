@@ -317,3 +317,26 @@ def test_stencil_mismatch_rejected():
     with pytest.raises(DDGError) as e:
         _solver(pr, stencil=dict(pr.stencil, dims=(16, 15, 1)))
     assert e.value.code == 1
+
+
+# ---------------------------------------------------------------- Lanczos condition estimate
+@pytest.mark.parametrize("name", ["C1", "poisson3d_24_b8_p2", "biharm_64_b16_p3"])
+def test_lanczos_coefficients_and_condition_estimate(name):
+    """The CG coefficients recorded on the device match the oracle's, and so
+    does the Lanczos condition estimate of cond(M A) in ddg_report
+    (PAPER.md:617-621; oracle.condition_estimate)."""
+    pr = CASES[name]()
+    s = _solver(pr)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    a, b = s.lanczos()
+    o = oracle.Oracle.from_problem(pr)
+    uo, ito, histo, conv, ao, bo = o.pcg_lanczos(pr.f, 1e-8)
+    m = min(len(a), len(ao))
+    assert len(a) == it and len(b) == it - 1
+    assert np.max(np.abs(a[:m] - ao[:m]) / np.abs(ao[:m])) <= 1e-8
+    mb = min(len(b), len(bo))
+    assert np.max(np.abs(b[:mb] - bo[:mb]) / np.abs(bo[:mb])) <= 1e-8
+    kappa_o, bound_o = oracle.condition_estimate(ao, bo, 1e-8)
+    assert abs(rep.cond_est - kappa_o) <= 1e-6 * kappa_o, (rep.cond_est, kappa_o)
+    assert abs(rep.iter_bound - bound_o) <= 1e-6 * bound_o
+    assert rep.cond_est >= 1.0
