@@ -2592,7 +2592,7 @@ static unsigned long long* g_ring_trace = nullptr;   // DDG_RING_TRACE (debug)
 void symv_ring_init() {
     g_ring_rt = 4;
     if (const char* e = getenv("DDG_RING_TILES")) g_ring_rt = atoi(e);
-    if (g_ring_rt != 1 && g_ring_rt != 2) g_ring_rt = 4;
+    if (g_ring_rt != 1 && g_ring_rt != 2 && g_ring_rt != 8) g_ring_rt = 4;
     g_ring_nb = 0;
     if (const char* e = getenv("DDG_RING_NB")) g_ring_nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
     g_ring_nst = 0;
@@ -2614,6 +2614,7 @@ void symv_ring_init() {
     cudaFuncSetAttribute(k_symv_ring<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     g_ring_init[dev & 63] = true;
 }
 
@@ -2643,7 +2644,7 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     // row/column-warp consumers for launches of whole-subdomain triangles
     // (measured: C3 +4%, C5 +1%; the 8-warp column consumers win on the
     // 8-wide rectangles of split operators); DDG_RING_V2=0/1 forces either
-    if (g_ring_v2 == 1 || (g_ring_v2 < 0 && triangles)) {
+    if (g_ring_v2 == 1 || (g_ring_v2 < 0 && triangles) || RT == 8) {
         int nb2 = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 4 : 2);
         int nst2 = 2;
         const int cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
@@ -2651,6 +2652,9 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
         const size_t smem2 = ring2_smem(RT, nst2, nb2, maxr);
         if (RT == 2)
             k_symv_ring2<2><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
+                                                                 y_out, partials, done, nst2, nb2, maxr);
+        else if (RT == 8)
+            k_symv_ring2<8><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
                                                                  y_out, partials, done, nst2, nb2, maxr);
         else
             k_symv_ring2<4><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
