@@ -169,6 +169,42 @@ def test_full_c2_properties():
     assert abs(x @ My - y @ Mx) <= 1e-11 * np.linalg.norm(x) * np.linalg.norm(My)
 
 
+@pytest.mark.parametrize("cfg,res_tol,poly_tol,sym_tol,cols", [
+    ("C3", 1e-7, 1e-8, 1e-11, (0, 3)),
+    ("C4", 1e-7, 1e-8, 1e-11, (0, 5, 11)),
+    # 13-point biharmonic at 2048^2: fp64 true-residual floor ~1e-7,
+    # cond(A_c) ~1e8 (DESIGN.md tolerances)
+    ("C5", 1e-6, 1e-5, 1e-10, (0, 4, 9)),
+])
+def test_full_size_properties(cfg, res_tol, poly_tol, sym_tol, cols):
+    """BASELINE configs C3, C4, C5 at full size, in the configuration bench.py
+    times (the oracle needs hours there): convergence at rtol 1e-8, the history's
+    first entry is ||f||, the true residual, polynomial reproduction of the
+    coarse correction P A_c^{-1} P^T A F_j = F_j and
+    symmetry of M."""
+    import scipy.sparse as sp
+    pr = P.make(cfg)
+    s = _solver(pr)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    A = sp.csr_matrix((pr.val, pr.col, pr.row_ptr), shape=(pr.n, pr.n))
+    assert rep.converged and 2 <= it <= 40, it
+    assert abs(hist[0] - np.linalg.norm(pr.f)) <= 1e-12 * hist[0]
+    assert hist[-1] <= 1e-8 * hist[0]
+    true_res = np.linalg.norm(pr.f - A @ u) / np.linalg.norm(pr.f)
+    assert true_res <= res_tol, true_res
+    assert 1.0 <= rep.cond_est and it - 1 <= rep.iter_bound
+    for j in cols:
+        Fj = pr.F[:, j]
+        z = s.coarse_correct(A @ Fj)
+        assert np.linalg.norm(z - Fj) <= poly_tol * np.linalg.norm(Fj), j
+    rs = np.random.default_rng(7)
+    x, y = rs.standard_normal(pr.n), rs.standard_normal(pr.n)
+    Mx, My = s.apply_precond(x), s.apply_precond(y)
+    assert abs(x @ My - y @ Mx) <= sym_tol * np.linalg.norm(x) * np.linalg.norm(My)
+    assert x @ Mx > 0
+    s.close()
+
+
 # ---------------------------------------------------------------- sparse coarse solver
 SPARSE_CASES = {
     "poisson2d_64_b4_p1": lambda: P.poisson2d(64, 4, 1, 21),      # 256 parts, 2D ND
