@@ -30,7 +30,7 @@
 
 namespace {
 
-constexpr int LEAF_UNKNOWNS = 256;
+int LEAF_UNKNOWNS = 256;   // nested dissection stops below this many unknowns (DDG_ND_LEAF)
 int FRONT_BT = 8;   // tiles per item side of the front operators (DDG_FRONT_BT)
 
 struct NDNode {
@@ -239,6 +239,10 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     c->sparse = sc;
     FRONT_BT = 8;
     if (const char* e = getenv("DDG_FRONT_BT")) FRONT_BT = std::max(1, std::min(8, atoi(e)));
+    // small coarse systems (C2, C5): bigger leaves, fewer levels on the solve's
+    // critical path; large ones (C3): smaller leaves, fewer bytes (measured)
+    LEAF_UNKNOWNS = c->nc <= 262144 ? 1024 : 256;
+    if (const char* e = getenv("DDG_ND_LEAF")) LEAF_UNKNOWNS = std::max(16, atoi(e));
     // part adjacency
     std::vector<std::vector<int32_t>> adj(np);
     for (int I = 0; I < np; ++I) {

@@ -132,9 +132,9 @@ struct ddg_ctx {
     std::vector<int32_t> op_sub;        // subdomain id of every local operator
     std::vector<int32_t> block_coords;  // optional nparts x block_ndim
     int block_ndim = 0;
-    // SYMV kernel choice (DDG_SYMV: "ring" default, "classic", "tma") and the
+    // SYMV kernel choice (DDG_SYMV: "ring" default, "classic") and the
     // byte-balanced CTA partitions of every k_symv_ring launch
-    int symv_mode = 0;                  // 0 ring, 1 classic per-item k_symv, 2 tma (experimental)
+    int symv_mode = 0;                  // 0 ring, 1 classic per-item k_symv
     std::vector<int32_t> h_ring;
     int32_t* d_ring = nullptr;
     int32_t* d_gidx = nullptr;          // s position -> fine row (-1: padding)

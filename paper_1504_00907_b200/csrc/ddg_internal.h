@@ -151,9 +151,6 @@ struct ColourPlan {
 };
 
 // ---- kernel launchers (kernels.cu) ----------------------------------------
-void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, int max_m, bool warp_rows,
-                   const int32_t* oidx, DevCSR A, const double* r, const double* z, double* s,
-                   bool z_is_zero, const int32_t* done);
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
                  double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
@@ -216,7 +213,6 @@ void launch_extract_local(cudaStream_t st, int nops, const int32_t* op_ids, cons
 // the trailing block).  ids[i] is reported in err[0] on a non-positive pivot.
 void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32_t* nK,
                        double* const* mats, const int32_t* ids, int32_t* err);
-void launch_gj_big(cudaStream_t st, int nT, int nK, double* M, int id, int32_t* err);
 // blocked exchange (128-column pivot blocks, fp64 GEMM updates) over a batch,
 // used for matrices of at least GJB_MIN_T tiles per side;
 // mats/nT/nK/ids are device arrays of nmat entries, maxT/maxK their maxima

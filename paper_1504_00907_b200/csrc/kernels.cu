@@ -376,42 +376,6 @@ __global__ void k_spmv(DevCSR A, const double* __restrict__ x, double* __restric
 // Multiplicative Schwarz colour step
 // =============================================================================
 
-// s_i = R~_i (r - A z) for every subdomain i of one colour (pull form, reading R5).
-// Block (q, chunk): rows [chunk*rows_per_cta, ...) of subdomain q; WARP_ROW
-// assigns one warp per row (long CSR rows, e.g. Q1 elasticity's 81).
-template <bool WARP_ROW>
-__global__ void __launch_bounds__(256)
-k_gather(const OpDesc* __restrict__ ops, int sub_begin, int chunks, const int32_t* __restrict__ oidx,
-         DevCSR A, const double* __restrict__ r, const double* __restrict__ z, double* __restrict__ s,
-         int z_is_zero, const int32_t* done) {
-    if (*done) return;
-    const int q = sub_begin + blockIdx.x / chunks;
-    const int chunk = blockIdx.x % chunks;
-    const OpDesc op = ops[q];
-    const int32_t* idx = oidx + op.idx_off;
-    double* so = s + op.s_off;
-    if (!WARP_ROW) {
-        const int a = chunk * blockDim.x + threadIdx.x;
-        if (a >= op.m) return;
-        const int v = idx[a];
-        double az = 0.0;
-        if (!z_is_zero)
-            az = row_dot1(A, v, z);
-        so[a] = r[v] - az;
-    } else {
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        const int rows_per_cta = (blockDim.x >> 5) * 4;
-        for (int a = chunk * rows_per_cta + w; a < min(op.m, (chunk + 1) * rows_per_cta); a += blockDim.x >> 5) {
-            const int v = idx[a];
-            double az = 0.0;
-            if (!z_is_zero)
-                for (int e = A.rp[v] + lane; e < A.rp[v + 1]; e += 32) az += A.val[e] * z[A.col[e]];
-            az = warp_sum(az);
-            if (lane == 0) so[a] = r[v] - az;
-        }
-    }
-}
-
 // flat residual restriction of one colour: x over its s segments
 template <int SW>
 __global__ void __launch_bounds__(256)
@@ -688,7 +652,7 @@ k_symv_small(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
     }
 }
 
-// ---- persistent warp-specialised SYMV: TMA bulk copies into an smem ring ----
+// ---- mbarrier / bulk-copy helpers (TMA, sm_90+) -----------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -721,165 +685,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         : "memory");
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-// Same arithmetic as k_symv.  Warps 0..7 consume, warp 8 (one lane) produces.
-// Each CTA walks items blockIdx.x, +gridDim.x, ...; tile k of the CTA's
-// stream lands in ring slot k % nst and is consumed by warp k % 8.
-__global__ void __launch_bounds__(288, 1)
-k_symv_tma(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin, int nitems,
-           const double* __restrict__ tiles, const double* __restrict__ s, const int32_t* __restrict__ oidx,
-           double* __restrict__ z, double* __restrict__ y_out, double* __restrict__ partials,
-           const int32_t* done, unsigned* __restrict__ tickets, int gather_mode, DevCSR A,
-           const double* __restrict__ rvec, int nst, int max_rows_t) {
-    if (*done) return;
-    extern __shared__ __align__(128) double tsm[];
-    double* ring = tsm;                                        // nst * 1024 doubles
-    double* s_sm = ring + (size_t)nst * TILE_ELEMS;            // max_rows_t
-    double* part = s_sm + max_rows_t;                          // 8 * max_rows_t
-    uint64_t* full = reinterpret_cast<uint64_t*>(part + SYMV_WARPS * max_rows_t);
-    uint64_t* empty = full + nst;
-    __shared__ bool last;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < nst; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == SYMV_WARPS) {                                  // ---- producer ----
-        if (lane != 0) return;
-        unsigned k = 0;
-        for (int ii = blockIdx.x; ii < nitems; ii += gridDim.x) {
-            const ItemDesc it = items[item_begin + ii];
-            const double* src = tiles + it.tile_off;
-            for (int l = 0; l < it.ntiles; ++l, ++k) {
-                const unsigned slot = k % nst, n = k / nst;
-                int I, J;
-                item_tile(it, l, I, J);
-                const unsigned bytes = (I == J && it.tri ? DIAG_ELEMS : TILE_ELEMS) * sizeof(double);
-                if (n > 0) mbar_wait(&empty[slot], (n - 1) & 1);
-                mbar_expect_tx(&full[slot], bytes);
-                bulk_g2s(ring + (size_t)slot * TILE_ELEMS, src + item_tile_off(it, l, I), bytes, &full[slot]);
-            }
-        }
-        return;
-    }
-    // ---- consumers (256 threads) ----
-    const int tid = threadIdx.x;
-    unsigned kbase = 0;
-    for (int ii = blockIdx.x; ii < nitems; ii += gridDim.x) {
-        const ItemDesc it = items[item_begin + ii];
-        const OpDesc op = ops[it.op];
-        const int rows_r = (it.I1 - it.I0) * TILE;
-        const int rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
-        const int rows_t = rows_r + rows_c;
-        const bool single = it.part_off < 0;
-        consumer_sync();                                       // previous item's epilogue done
-        if (gather_mode) {
-            const int32_t* idx = oidx + op.idx_off;
-            for (int x = tid; x < rows_t; x += 256) {
-                double v = 0.0;
-                if (x < op.m) {
-                    const int node = idx[x];
-                    double az = 0.0;
-                    if (gather_mode == 1)
-                        az = row_dot_csr(A, node, z);
-                    v = rvec[node] - az;
-                }
-                s_sm[x] = v;
-            }
-        } else {
-            const double* sop = s + op.s_off;
-            for (int x = tid; x < rows_t; x += 256) {
-                int g = x < rows_r ? it.I0 * TILE + x : it.J0 * TILE + (x - rows_r);
-                s_sm[x] = sop[g];
-            }
-        }
-        for (int x = tid; x < SYMV_WARPS * rows_t; x += 256) part[x] = 0.0;
-        consumer_sync();
-        double* pw = part + warp * rows_t;
-        // this warp's tiles: local l with (kbase + l) % 8 == warp
-        int l = (int)((warp - (int)(kbase % SYMV_WARPS) + SYMV_WARPS) % SYMV_WARPS);
-        for (; l < it.ntiles; l += SYMV_WARPS) {
-            const unsigned k = kbase + l, slot = k % nst;
-            mbar_wait(&full[slot], (k / nst) & 1);
-            const double* T = ring + (size_t)slot * TILE_ELEMS;
-            int I, J;
-            item_tile(it, l, I, J);
-            double a[TILE];
-            if (I != J) {
-#pragma unroll
-                for (int j = 0; j < TILE; ++j) a[j] = T[j * TILE + lane];
-            } else {
-#pragma unroll
-                for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? T[diag_col_off(j) + lane - j] : 0.0;
-            }
-            const int ri = (I - it.I0) * TILE;
-            const int cj = it.tri ? (J - it.I0) * TILE : rows_r + (J - it.J0) * TILE;
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < TILE; ++j) acc += a[j] * s_sm[cj + j];
-            // every a[j] has been consumed, so the slot's loads are complete
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);          // slot may be refilled
-            const double si = s_sm[ri + lane];
-#pragma unroll
-            for (int j = 0; j < TILE; ++j) a[j] *= si;
-            rs_stage<16>(a, lane);
-            rs_stage<8>(a, lane);
-            rs_stage<4>(a, lane);
-            rs_stage<2>(a, lane);
-            rs_stage<1>(a, lane);
-            if (I != J) {
-                pw[ri + lane] += acc;
-                pw[cj + lane] += a[0];
-            } else {
-                pw[ri + lane] += acc + a[0];
-            }
-        }
-        kbase += it.ntiles;
-        consumer_sync();
-        for (int x = tid; x < rows_t; x += 256) {
-            double y = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < SYMV_WARPS; ++ww) y += part[ww * rows_t + x];
-            if (single) {
-                const int g = it.I0 * TILE + x;
-                if (g < op.m) {
-                    if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
-                    else y_out[g] = y;
-                }
-            } else {
-                partials[it.part_off + x] = y;
-            }
-        }
-        if (single || op.out_mode == 2) continue;
-        __threadfence();
-        consumer_sync();
-        if (tid == 0) last = (atomicAdd(&tickets[it.op], 1u) == (unsigned)op.nitems - 1);
-        consumer_sync();
-        if (!last) continue;
-        __threadfence();
-        const int rb = op.BT * TILE;
-        for (int g = tid; g < op.m; g += 256) {
-            const int b = g / rb, x = g % rb;
-            double y = 0.0;
-            for (int j = 0; j <= b; ++j) {
-                const ItemDesc& ij = items[op.item_base + b * (b + 1) / 2 + j];
-                y += __ldcg(partials + ij.part_off + x);
-            }
-            for (int i = b + 1; i < op.nblk; ++i) {
-                const ItemDesc& ii2 = items[op.item_base + i * (i + 1) / 2 + b];
-                y += __ldcg(partials + ii2.part_off + (ii2.I1 - ii2.I0) * TILE + x);
-            }
-            if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
-            else y_out[g] = y;
-        }
-        if (tid == 0) tickets[it.op] = 0u;
-    }
-}
 
 // ---- persistent streaming SYMV: bulk-copy ring, warp-specialised ----------
 // One CTA per SM walks a byte-balanced contiguous range of the launch's items
@@ -2121,53 +1926,6 @@ k_gj_batched(const int32_t* __restrict__ nTs, const int32_t* __restrict__ nKs, d
     }
 }
 
-// ---- the same exchange for one big matrix, one launch per phase ---------------
-__global__ void k_gj_pivot(double* M, int nT, int k, int id, int32_t* err) {
-    __shared__ double Ps[TILE_ELEMS];
-    double* T = M + ((int64_t)k * nT + k) * TILE_ELEMS;
-    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = T[e];
-    __syncthreads();
-    tile_exchange_inverse(Ps, err, id, k * TILE);
-    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) T[e] = Ps[e];
-}
-
-__global__ void __launch_bounds__(256) k_gj_rowpanel(double* M, int nT, int k) {
-    extern __shared__ double gjsm[];
-    double* Ps = gjsm;
-    double (*Bs)[TILE_ELEMS] = reinterpret_cast<double (*)[TILE_ELEMS]>(gjsm + TILE_ELEMS);
-    const double* P = M + ((int64_t)k * nT + k) * TILE_ELEMS;
-    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = P[e];
-    __syncthreads();
-    const int w = threadIdx.x >> 5;
-    const int j = blockIdx.x * 8 + w;
-    if (j < nT && j != k) {
-        double* T = M + ((int64_t)j * nT + k) * TILE_ELEMS;
-        warp_left_mul(Ps, T, T, Bs[w], -1.0);
-    }
-}
-
-// grid (nT, ceil(nT/8)): CTA stages B_kj once; warp w updates tile (i, j)
-__global__ void __launch_bounds__(256) k_gj_update(double* M, int nT, int k) {
-    __shared__ double Bs[TILE_ELEMS];
-    const int j = blockIdx.x;
-    if (j == k) return;
-    const double* B = M + ((int64_t)j * nT + k) * TILE_ELEMS;
-    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Bs[e] = B[e];
-    __syncthreads();
-    const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
-    if (i >= nT || i == k) return;
-    warp_gemm_acc(M + ((int64_t)k * nT + i) * TILE_ELEMS, Bs, M + ((int64_t)j * nT + i) * TILE_ELEMS);
-}
-
-__global__ void __launch_bounds__(256) k_gj_colpanel(double* M, int nT, int k) {
-    __shared__ double Ps[TILE_ELEMS];
-    const double* P = M + ((int64_t)k * nT + k) * TILE_ELEMS;
-    for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) Ps[e] = P[e];
-    __syncthreads();
-    const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i < nT && i != k) warp_right_mul(M + ((int64_t)k * nT + i) * TILE_ELEMS, Ps);
-}
-
 // ---- blocked Gauss-Jordan exchange (setup) ----------------
 // The same exchange with pivot blocks of GJB_BT tiles (128 columns): per
 // block, P = A_kk^{-1} (tile exchange restricted to the block, one CTA), then
@@ -2523,18 +2281,6 @@ static inline int vec_grid(int64_t n) {
     return (int)(g < RED_BLOCKS ? (g > 0 ? g : 1) : RED_BLOCKS);
 }
 
-void launch_gather(cudaStream_t st, const OpDesc* ops, int sub_begin, int nsub, int max_m, bool warp_rows,
-                   const int32_t* oidx, DevCSR A, const double* r, const double* z, double* s,
-                   bool z_is_zero, const int32_t* done) {
-    if (nsub <= 0) return;
-    const int rows_per_cta = warp_rows ? 32 : 256;
-    const int chunks = (max_m + rows_per_cta - 1) / rows_per_cta;
-    if (warp_rows)
-        k_gather<true><<<nsub * chunks, 256, 0, st>>>(ops, sub_begin, chunks, oidx, A, r, z, s, z_is_zero ? 1 : 0, done);
-    else
-        k_gather<false><<<nsub * chunks, 256, 0, st>>>(ops, sub_begin, chunks, oidx, A, r, z, s, z_is_zero ? 1 : 0, done);
-}
-
 void launch_gather_flat(cudaStream_t st, int64_t x0, int64_t x1, const int32_t* gidx, DevCSR A, const double* r,
                         const double* z, double* s, bool z_is_zero, const int32_t* done) {
     if (x1 <= x0) return;
@@ -2563,20 +2309,6 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
     if (small_ok && max_rows_t <= SMALL_MAXROWS) {
         k_symv_small<<<(nitems + 7) / 8, 256, 0, st>>>(ops, items, item_begin, nitems, tiles, s, oidx, z, y_out,
                                                       done, gather_mode, A, r);
-        return;
-    }
-    const char* e = getenv("DDG_SYMV");
-    const int mode = (e && e[0] == 't') ? 1 : 0;   // "tma" selects the persistent TMA-ring kernel
-    if (mode == 1) {
-        const size_t fixed = (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
-        const size_t budget = 227 * 1024 - 1024;
-        int nst = (int)((budget - fixed) / (TILE_ELEMS * sizeof(double) + 16));
-        nst = std::max(2, std::min(nst, 24));
-        const size_t smem = (size_t)nst * TILE_ELEMS * sizeof(double) + fixed + 2 * nst * sizeof(uint64_t);
-        cudaFuncSetAttribute(k_symv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int grid = std::min(nitems, num_sms());
-        k_symv_tma<<<grid, 288, smem, st>>>(ops, items, item_begin, nitems, tiles, s, oidx, z, y_out, partials,
-                                           done, tickets, gather_mode, A, r, nst, max_rows_t);
         return;
     }
     const size_t smem = symv_smem(max_rows_t);
@@ -2807,17 +2539,6 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
         k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 0);
         k_gjb_gemm<<<dim3(nb * nb, nmat), 256, smem_g, st>>>(bt, k0, 1);
         k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 2);
-    }
-}
-
-void launch_gj_big(cudaStream_t st, int nT, int nK, double* M, int id, int32_t* err) {
-    const int smem = 9 * TILE_ELEMS * sizeof(double);
-    cudaFuncSetAttribute(k_gj_rowpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int k = 0; k < nK; ++k) {
-        k_gj_pivot<<<1, 256, 0, st>>>(M, nT, k, id, err);
-        k_gj_rowpanel<<<(nT + 7) / 8, 256, smem, st>>>(M, nT, k);
-        k_gj_update<<<dim3(nT, (nT + 7) / 8), 256, 0, st>>>(M, nT, k);
-        k_gj_colpanel<<<(nT + 7) / 8, 256, 0, st>>>(M, nT, k);
     }
 }
 

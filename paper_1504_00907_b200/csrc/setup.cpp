@@ -932,7 +932,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     // environment overrides for experiments (documented in DESIGN.md)
     if (const char* e = getenv("DDG_FUSE_GATHER")) c->opts.fuse_gather = atoi(e);
     if (const char* e = getenv("DDG_SMALL_KERNEL")) c->opts.small_kernel = atoi(e);
-    if (const char* e = getenv("DDG_SYMV")) c->symv_mode = e[0] == 'c' ? 1 : e[0] == 't' ? 2 : 0;
+    if (const char* e = getenv("DDG_SYMV")) c->symv_mode = e[0] == 'c' ? 1 : 0;
     if (const char* e = getenv("DDG_RING_MIN_MB")) c->ring_min_bytes = atof(e) * 1e6;
     c->coarse_variant = c->opts.coarse_variant;
     if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
