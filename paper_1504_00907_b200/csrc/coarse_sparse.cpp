@@ -796,9 +796,12 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         launch_front_fwd_assemble(c->stream, f0, nf, sc->d_fr, sc->d_fS, sc->d_fmap, sc->d_bc, sc->d_fvec,
                                   sc->d_w, done);
         if (ring_ok(c, sc->ring_fwd[h]))
-            launch_symv_ring(c->stream, c->d_ops, c->d_items, sc->g_begin[h], c->d_ring + sc->ring_fwd[h], num_sms(), sc->max_rows_t,
+        {
+            int mr, mc;
+            ring_dims(c, sc->ring_fwd[h], &mr, &mc);
+            launch_symv_ring(c->stream, c->d_ops, c->d_items, sc->g_begin[h], c->d_ring + sc->ring_fwd[h], num_sms(), mr, mc,
                              sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done);
-        else
+        } else
             launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->g_end[h] - sc->g_begin[h],
                         sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
                         c->d_tickets);
@@ -810,9 +813,12 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
         launch_front_bwd_gather(c->stream, f0, nf, sc->d_fr, sc->d_fB, d_x, sc->d_fvec, done);
         if (ring_ok(c, sc->ring_bwd[h]))
-            launch_symv_ring(c->stream, c->d_ops, c->d_items, sc->g_begin[h], c->d_ring + sc->ring_bwd[h], num_sms(), sc->max_rows_t,
+        {
+            int mr, mc;
+            ring_dims(c, sc->ring_bwd[h], &mr, &mc);
+            launch_symv_ring(c->stream, c->d_ops, c->d_items, sc->g_begin[h], c->d_ring + sc->ring_bwd[h], num_sms(), mr, mc,
                              sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done);
-        else
+        } else
             launch_symv(c->stream, c->d_ops, c->d_items, sc->g_begin[h], sc->h_end[h] - sc->g_begin[h],
                         sc->d_ctiles, sc->d_fvec, nullptr, nullptr, nullptr, c->d_partials, done, sc->max_rows_t,
                         c->d_tickets);

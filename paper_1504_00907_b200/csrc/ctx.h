@@ -136,6 +136,7 @@ struct ddg_ctx {
     // byte-balanced CTA partitions of every k_symv_ring launch
     int symv_mode = 0;                  // 0 ring, 1 classic per-item k_symv
     std::vector<int32_t> h_ring;
+    std::vector<std::pair<int, std::pair<int, int>>> ring_rc;   // partition offset -> (max rows_r, max rows_c)
     int32_t* d_ring = nullptr;
     int32_t* d_gidx = nullptr;          // s position -> fine row (-1: padding)
     double* d_stencil_coef = nullptr;   // ddg_stencil FACE7 coefficients (device)
@@ -146,6 +147,8 @@ struct ddg_ctx {
 // append the CTA partition of items [b, e) for k_symv_ring; returns its offset
 // in c->h_ring, or -1 when the range is empty or an item exceeds the ring's rows
 int ring_partition(ddg_ctx* c, int b, int e);
+// largest row block and column block (rows) of the items of partition `off`
+void ring_dims(const ddg_ctx* c, int off, int* max_rows_r, int* max_rows_c);
 // launch the colour/coarse SYMV over items [b, e) with the context's kernel choice
 bool ring_ok(const ddg_ctx* c, int off);
 

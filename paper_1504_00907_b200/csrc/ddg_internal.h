@@ -160,10 +160,12 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 constexpr int RING_MAX_ROWS = 512;
 void symv_ring_init();   // once per device, before any capture
 int symv_ring_trace(unsigned long long* out);   // debug counters (DDG_RING_TRACE)
+// max_rows_r / max_rows_c: the launch's largest row block and (rectangles)
+// column block, in rows (ring_dims)
 void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
-                      const int32_t* cta_part, int ncta, int max_rows_t, const double* tiles, const double* s,
-                      const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done,
-                      bool triangles = false);
+                      const int32_t* cta_part, int ncta, int max_rows_r, int max_rows_c, const double* tiles,
+                      const double* s, const int32_t* oidx, double* z, double* y_out, double* partials,
+                      const int32_t* done, bool triangles = false);
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
                         const double* partials, double* z, double* y_out, const int32_t* done);

@@ -716,9 +716,9 @@ constexpr int RING_MAX_NB = 8;
 // shared memory of a launch: nst slots of RT tiles; nb item buffers, each the
 // item's s (maxr rows), the 8 consumer warps' partial rows and a descriptor;
 // barriers
-__host__ __device__ constexpr size_t ring_smem(int RT, int nst, int nb, int maxr) {
-    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * (SYMV_WARPS + 1) * maxr * 8 + (size_t)nb * 8 * 4 +
-           (2 * (size_t)nst + 4 * (size_t)nb) * 8;
+__host__ __device__ constexpr size_t ring_smem(int RT, int nst, int nb, int R, int Cr) {
+    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * (R + Cr) * 8 + (size_t)nb * (SYMV_WARPS * R + Cr) * 8 +
+           (size_t)nb * 8 * 4 + (2 * (size_t)nst + 4 * (size_t)nb) * 8;
 }
 
 // first double of tile l of item it (l == ntiles: one past the last tile)
@@ -764,9 +764,13 @@ __global__ void __launch_bounds__(RING_THREADS, 1)
 k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
             const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
             const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
-            double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr,
+            double* __restrict__ partials, const int32_t* done, int nst, int nb, int R, int Cr,
             unsigned long long* rtrace) {
     constexpr int SLOT = RT * TILE_ELEMS;
+    // item buffers: s over R + Cr rows; partial rows: the row block replicated
+    // per consumer warp ([8][R], every warp adds direct parts to any row) and
+    // the column block of rectangles once ([Cr], each column has one owner)
+    const int maxr = R + Cr, PB = SYMV_WARPS * R + Cr;
     // DDG_RING_TRACE: cycles per role and wait (debug; rtrace == nullptr otherwise)
     unsigned long long tw[4] = {0, 0, 0, 0}, tstart = rtrace ? clock64() : 0, ntile = 0, nflush = 0;
 #define RT_WAIT(k, call)                                        \
@@ -795,8 +799,8 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
     extern __shared__ __align__(128) double rsm[];
     double* ring = rsm;                                          // [nst][SLOT]
     double* s_sm = ring + (size_t)nst * SLOT;                    // [nb][maxr]
-    double* part = s_sm + (size_t)nb * maxr;                     // [nb][SYMV_WARPS][maxr]
-    int32_t* dsc = reinterpret_cast<int32_t*>(part + (size_t)nb * SYMV_WARPS * maxr);   // [nb][8]
+    double* part = s_sm + (size_t)nb * maxr;                     // [nb][PB]
+    int32_t* dsc = reinterpret_cast<int32_t*>(part + (size_t)nb * PB);   // [nb][8]
     uint64_t* full = reinterpret_cast<uint64_t*>(dsc + nb * 8);
     uint64_t* empty = full + nst;
     uint64_t* sfull = empty + nst;    // [nb] s + descriptor of the item landed
@@ -904,14 +908,19 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
                 for (int r = 0; r < RING_MAX_ROWS / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
             }
             RT_WAIT(0, mbar_wait(&pdone[b], ph & 1));
-            const double* pp = part + (size_t)b * SYMV_WARPS * maxr;
+            const double* pp = part + (size_t)b * PB;
+            const int rows_r = (it.I1 - it.I0) * TILE;
 #pragma unroll
             for (int r = 0; r < RING_MAX_ROWS / 32; ++r) {
                 const int x = lane + 32 * r;
                 if (x < rows_t) {
                     double y = 0.0;
+                    if (x < rows_r) {
 #pragma unroll
-                    for (int ww = 0; ww < SYMV_WARPS; ++ww) y += pp[ww * maxr + x];
+                        for (int ww = 0; ww < SYMV_WARPS; ++ww) y += pp[ww * R + x];
+                    } else {
+                        y = pp[SYMV_WARPS * R + x - rows_r];       // column block (one owner)
+                    }
                     if (it.part_off >= 0) partials[it.part_off + x] = y;
                     else if (x < nr) {
                         if (scat) z[ix[r]] = zv[r] + y;
@@ -936,9 +945,10 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
         const double* ss = s_sm + (size_t)bi * maxr;
         const int rows_r = (I1 - I0) * TILE;
         const int rows_t = rows_r + (tri ? 0 : (J1 - J0) * TILE);
-        double* pw = part + ((size_t)bi * SYMV_WARPS + warp) * maxr;
+        double* pw = part + (size_t)bi * PB + (size_t)warp * R;    // this warp's row-block rows
+        double* pcb = part + (size_t)bi * PB + SYMV_WARPS * R;     // column block (rectangles)
         if (bph > 0) RT_WAIT(1, mbar_wait(&pfree[bi], (bph - 1) & 1));
-        for (int x = lane; x < rows_t; x += 32) pw[x] = 0.0;
+        for (int x = lane; x < rows_r; x += 32) pw[x] = 0.0;
         __syncwarp();
         double t[TILE];
 #pragma unroll
@@ -949,9 +959,9 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
             const int cj = tri ? (J - I0) * TILE : rows_r + (J - J0) * TILE;
             ++ntile;
             if (J != curJ) {
-                if (curJ >= 0) {
-                    ++nflush;
-                    flush_column(t, pw, tri ? (curJ - I0) * TILE : rows_r + (curJ - J0) * TILE, lane);
+                if (curJ >= 0) {                                   // (triangles only: one column per
+                    ++nflush;                                      //  warp in a rectangle)
+                    flush_column(t, pw, (curJ - I0) * TILE, lane);
 #pragma unroll
                     for (int j = 0; j < TILE; ++j) t[j] = 0.0;
                 }
@@ -980,21 +990,21 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
 #pragma unroll
             for (int j = 0; j < TILE; ++j) t[j] = fma(a[j], si, t[j]);
         };
-        // own-tile iterator, in increasing l.  Rectangles: l = warp, warp+8, ...
+        // own-tile iterator, in increasing l.  Rectangles: column warp of every
+        // row (l = r * wd + warp; warps >= wd idle); each column has one owner.
         // Triangles: columns c0 = (warp - ki) mod 8, c0+8, ... of rows r >= c.
         int l = -1, I = 0, J = 0, r = 0, c = 0;
         const int h = I1 - I0, wd = J1 - J0, c0 = (warp - ki) & (SYMV_WARPS - 1);
         if (!tri) {
-            if (warp < ntiles) { l = warp; I = I0 + warp / wd; J = J0 + warp % wd; }
+            if (warp < wd) { l = warp; I = I0; J = J0 + warp; }
         } else if (c0 < h) {
             r = c0; c = c0; l = r * (r + 1) / 2 + c; I = I0 + r; J = J0 + c;
         }
         auto advance = [&]() {
             if (!tri) {
-                l += SYMV_WARPS;
-                if (l >= ntiles) { l = -1; return; }
-                J += SYMV_WARPS;
-                while (J >= J1) { J -= wd; ++I; }
+                l += wd;
+                ++I;
+                if (I >= I1) l = -1;
             } else {
                 c += SYMV_WARPS;
                 if (c > r) { ++r; c = c0; }
@@ -1015,7 +1025,18 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == (unsigned)nst) { slot = 0; ++sph; }
         }
-        if (curJ >= 0) flush_column(t, pw, tri ? (curJ - I0) * TILE : rows_r + (curJ - J0) * TILE, lane);
+        if (curJ >= 0) {
+            if (tri) {
+                flush_column(t, pw, (curJ - I0) * TILE, lane);
+            } else {                                               // sole owner of this column
+                rs_stage<16>(t, lane);
+                rs_stage<8>(t, lane);
+                rs_stage<4>(t, lane);
+                rs_stage<2>(t, lane);
+                rs_stage<1>(t, lane);
+                pcb[(curJ - J0) * TILE + lane] = t[0];
+            }
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[bi]);
         mbar_arrive(&pdone[bi]);                                   // every lane (release its rows)
@@ -2360,19 +2381,13 @@ int symv_ring_trace(unsigned long long* out) {
 }
 
 void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
-                      const int32_t* cta_part, int ncta, int max_rows_t, const double* tiles, const double* s,
-                      const int32_t* oidx, double* z, double* y_out, double* partials, const int32_t* done,
-                      bool triangles) {
+                      const int32_t* cta_part, int ncta, int max_rows_r, int max_rows_c, const double* tiles,
+                      const double* s, const int32_t* oidx, double* z, double* y_out, double* partials,
+                      const int32_t* done, bool triangles) {
     const int RT = g_ring_rt;
-    const int maxr = std::max(TILE, std::min(RING_MAX_ROWS, max_rows_t));
+    const int R = std::max(TILE, max_rows_r), Cr = std::max(0, max_rows_c);
+    const int maxr = std::min(RING_MAX_ROWS, R + Cr);
     const size_t budget = 227 * 1024;
-    // item buffers: deep for small items (s copies and epilogues overlap
-    // several items), two for large ones; the rest of shared memory is ring
-    int nb = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 3 : 2);
-    while (nb > 2 && ring_smem(RT, 4, nb, maxr) > budget) --nb;
-    int nst = 2;
-    const int nst_cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
-    while (nst < nst_cap && ring_smem(RT, nst + 1, nb, maxr) <= budget) ++nst;
     // row/column-warp consumers for launches of whole-subdomain triangles
     // (measured: C3 +4%, C5 +1%; the 8-warp column consumers win on the
     // 8-wide rectangles of split operators); DDG_RING_V2=0/1 forces either
@@ -2393,16 +2408,23 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                                                                  y_out, partials, done, nst2, nb2, maxr);
         return;
     }
-    const size_t smem = ring_smem(RT, nst, nb, maxr);
+    // item buffers: deep for small items (s copies and epilogues overlap
+    // several items), two for large ones; the rest of shared memory is ring
+    int nb = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 3 : 2);
+    while (nb > 2 && ring_smem(RT, 4, nb, R, Cr) > budget) --nb;
+    int nst = 2;
+    const int nst_cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
+    while (nst < nst_cap && ring_smem(RT, nst + 1, nb, R, Cr) <= budget) ++nst;
+    const size_t smem = ring_smem(RT, nst, nb, R, Cr);
     if (RT == 1)
         k_symv_ring<1><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, maxr, g_ring_trace);
+                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
     else if (RT == 2)
         k_symv_ring<2><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, maxr, g_ring_trace);
+                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
     else
         k_symv_ring<4><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, maxr, g_ring_trace);
+                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
 }
 
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,

@@ -583,10 +583,13 @@ int ring_partition(ddg_ctx* c, int b, int e) {
     if (e <= b) return -1;
     const int G = num_sms();
     std::vector<double> pre(e - b + 1, 0.0);
+    int mr = 0, mc = 0;
     for (int i = b; i < e; ++i) {
         const ItemDesc& d = c->items[i];
         const int rows = (d.I1 - d.I0 + (d.tri ? 0 : d.J1 - d.J0)) * TILE;
         if (rows > RING_MAX_ROWS) return -1;
+        mr = std::max(mr, (d.I1 - d.I0) * TILE);
+        if (!d.tri) mc = std::max(mc, (d.J1 - d.J0) * TILE);
         pre[i - b + 1] = pre[i - b] + item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8.0 + 8192.0;
     }
     const int off = (int)c->h_ring.size();
@@ -608,7 +611,17 @@ int ring_partition(ddg_ctx* c, int b, int e) {
         c->h_ring.resize(off);
         return -1;
     }
+    c->ring_rc.push_back({off, {mr, mc}});
     return off;
+}
+void ring_dims(const ddg_ctx* c, int off, int* max_rows_r, int* max_rows_c) {
+    *max_rows_r = RING_MAX_ROWS;
+    *max_rows_c = 0;
+    for (const auto& e : c->ring_rc)
+        if (e.first == off) {
+            *max_rows_r = e.second.first;
+            *max_rows_c = e.second.second;
+        }
 }
 bool ring_ok(const ddg_ctx* c, int off) { return c->symv_mode == 0 && off >= 0; }
 
@@ -1125,8 +1138,10 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
         }
         if (ring) {
             prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
+                int mr, mc;
+                ring_dims(c, pl.ring_off, &mr, &mc);
                 launch_symv_ring(c->stream, c->d_ops, c->d_items, pl.item_begin, c->d_ring + pl.ring_off,
-                                 num_sms(), pl.max_rows_t, c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done,
+                                 num_sms(), mr, mc, c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done,
                                  pl.all_single != 0);
             });
             c->launches += 1;
@@ -1163,8 +1178,10 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
         if (c->coarse_variant == 2) {
             c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
         } else if (ring_ok(c, c->coarse_ring_off)) {
+            int mr, mc;
+            ring_dims(c, c->coarse_ring_off, &mr, &mc);
             launch_symv_ring(c->stream, c->d_ops, c->d_items, c->coarse_item_begin, c->d_ring + c->coarse_ring_off,
-                             num_sms(), c->coarse_rows_t, c->d_tiles, c->d_s, c->d_oidx, nullptr, c->d_yc, c->d_partials, done);
+                             num_sms(), mr, mc, c->d_tiles, c->d_s, c->d_oidx, nullptr, c->d_yc, c->d_partials, done);
             c->launches += 1;
             if (c->coarse_red_end > c->coarse_red_begin) {
                 launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, c->coarse_red_begin,
