@@ -1,5 +1,6 @@
 // ddg_internal.h — internal types shared by the host setup (setup.cpp) and the
-// sm_100a kernels (kernels.cu) of libddg.  Not part of the public ABI.
+// sm_100a kernels (pcg.cu, symv.cu, coarse.cu, setup_kernels.cu) of libddg.
+// Not part of the public ABI.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -150,7 +151,7 @@ struct ColourPlan {
     int32_t ring_off;               // its k_symv_ring CTA partition in ctx::h_ring (-1: none)
 };
 
-// ---- kernel launchers (kernels.cu) ----------------------------------------
+// ---- kernel launchers (pcg.cu, symv.cu, coarse.cu, setup_kernels.cu) --------
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
                  double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
@@ -237,7 +238,7 @@ void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* f
 void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,
                          const FrontDesc* fronts, const int32_t* fS, const double* partials, double* w,
                          double* x, const int32_t* done);
-// whole sparse coarse solve y = A_c^{-1} b_c in one launch (see kernels.cu)
+// whole sparse coarse solve y = A_c^{-1} b_c in one launch (see coarse.cu)
 void launch_coarse_dataflow(cudaStream_t st, int nwork, const int32_t* work, const FrontDesc* fronts,
                             const FrontDF* fdf, const int32_t* item_front, int item_base, const OpDesc* ops,
                             const ItemDesc* items, const double* ctiles, const FRedTask* fwd, const FRedTask* bwd,

@@ -1,0 +1,244 @@
+// kernel_common.cuh — device helpers shared by libddg's sm_100a kernels
+// (pcg.cu, symv.cu, coarse.cu, setup_kernels.cu).  Overview of the kernels:
+//
+// Hot path, one PCG iteration:
+//   a1 pcg_spmv_dot      q = A p, sigma = p^T q, alpha = rho / sigma
+//   a2 pcg_update        u += alpha p, r -= alpha q, gamma = r^T r, history, stop test
+//   a4 gather + symv     per colour: s_i = R~_i (r - A z); z[Omega~_i] += A_i^{-1} s_i
+//   a5 coarse_restrict   b_c = P^T (r - A z)
+//   a6 symv (coarse op)  y_c = A_c^{-1} b_c (dense packed inverse, small n_c)
+//   a7 prolong           z += P y_c
+//   a8 gather + symv     reverse colour order
+//   a9 pcg_rz, direction rho' = r^T z, beta, p = z + beta p
+// Setup: extract_local, Gauss-Jordan block inversion (tile / blocked), pack.
+//
+// Every reduction is deterministic (fixed partition, fixed order, last-block
+// finalisation with a ticket; no floating-point atomics), so runs are bitwise
+// repeatable.  Every PCG kernel exits immediately once the device flag
+// `done` is set, so the host can enqueue several iterations without syncing.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ddg_internal.h"
+
+namespace ddg {
+
+#define FULL 0xffffffffu
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// (A x)[v] from the stencil, in the CSR's column order (see DevStencil)
+__device__ __forceinline__ double stencil_dot(const DevStencil& st, int64_t v, const double* __restrict__ x) {
+    const int nx = st.nx, ny = st.ny;
+    const int ix = (int)(v % nx);
+    const int64_t r = v / nx;
+    const int iy = (int)(r % ny), iz = (int)(r / ny);
+    double s = 0.0;
+    if (st.kind == 1) {
+        const double* xv = x + v;
+        if (ix >= st.rx && ix < nx - st.rx && iy >= st.ry && iy < ny - st.ry && iz >= st.rz && iz < st.nz - st.rz) {
+#pragma unroll
+            for (int k = 0; k < STENCIL_MAX_PTS; ++k) {    // interior: every point on the grid
+                if (k >= st.npts) break;
+                s = fma(st.c[k], xv[st.off[k]], s);
+            }
+            return s;
+        }
+#pragma unroll
+        for (int k = 0; k < STENCIL_MAX_PTS; ++k) {
+            if (k >= st.npts) break;
+            const int a = ix + st.dx[k], b = iy + st.dy[k], c = iz + st.dz[k];
+            if (a >= 0 && a < nx && b >= 0 && b < ny && c >= 0 && c < st.nz) s = fma(st.c[k], xv[st.off[k]], s);
+        }
+        return s;
+    }
+    const int64_t n = (int64_t)nx * ny * st.nz, sy = nx, sz = (int64_t)nx * ny;
+    const double* D = st.coef;
+    const double* CX = D + n;
+    const double* CY = CX + n;
+    const double* CZ = CY + n;
+    if (iz > 0) s = fma(CZ[v - sz], x[v - sz], s);
+    if (iy > 0) s = fma(CY[v - sy], x[v - sy], s);
+    if (ix > 0) s = fma(CX[v - 1], x[v - 1], s);
+    s = fma(D[v], x[v], s);
+    if (ix + 1 < nx) s = fma(CX[v], x[v + 1], s);
+    if (iy + 1 < ny) s = fma(CY[v], x[v + sy], s);
+    if (iz + 1 < st.nz) s = fma(CZ[v], x[v + sz], s);
+    return s;
+}
+
+// (A x)[v] by one thread: stencil or CSR row
+__device__ __forceinline__ double row_dot1(const DevCSR& A, int64_t v, const double* __restrict__ x) {
+    if (A.st.kind) return stencil_dot(A.st, v, x);
+    double s = 0.0;
+    for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * x[A.col[e]];
+    return s;
+}
+
+// CSR row only: the fused gathers of the per-item SYMV kernels (the stencil
+// code would double their register allocation; the CSR rounds identically)
+__device__ __forceinline__ double row_dot_csr(const DevCSR& A, int64_t v, const double* __restrict__ x) {
+    double s = 0.0;
+    for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * x[A.col[e]];
+    return s;
+}
+
+// (A x)[v] by SW lanes (an aligned group of the warp; sl = lane in group).
+// Every lane of the warp must call it (the group reduction shuffles); rows
+// with valid == false contribute 0.
+template <int SW>
+__device__ __forceinline__ double row_dot(const DevCSR& A, int64_t v, bool valid, const double* __restrict__ x,
+                                          int sl) {
+    double s = 0.0;
+    if (SW == 1) return valid ? row_dot1(A, v, x) : 0.0;
+    if (valid) {
+        const int e1 = A.rp[v + 1];
+        for (int e = A.rp[v] + sl; e < e1; e += SW) s += A.val[e] * x[A.col[e]];
+    }
+#pragma unroll
+    for (int o = SW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    return s;
+}
+
+// block-wide sum; result valid in every thread. blockDim.x multiple of 32, <= 1024
+static __device__ double block_sum(double v) {
+    __shared__ double ws[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) ws[w] = v;
+    __syncthreads();
+    double t = (threadIdx.x < nw) ? ws[threadIdx.x] : 0.0;
+    if (w == 0) t = warp_sum(t);
+    if (threadIdx.x == 0) ws[0] = t;
+    __syncthreads();
+    return ws[0];
+}
+
+// Grid reduction: every block contributes v; the last block to arrive sums
+// the block partials in index order and calls fin(total) in thread 0.
+template <typename Fin>
+__device__ void grid_reduce(double v, double* red, unsigned* ticket, Fin fin) {
+    __shared__ bool last;
+    double b = block_sum(v);
+    if (threadIdx.x == 0) {
+        red[blockIdx.x] = b;
+        __threadfence();
+        unsigned t = atomicAdd(ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double s = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(red + i);
+        s = block_sum(s);
+        if (threadIdx.x == 0) {
+            fin(s);
+            *ticket = 0u;
+        }
+    }
+}
+
+
+__device__ __forceinline__ void item_tile(const ItemDesc& it, int l, int& I, int& J) {
+    if (!it.tri) {
+        const int wJ = it.J1 - it.J0;
+        I = it.I0 + l / wJ;
+        J = it.J0 + l % wJ;
+    } else {
+        int rr = (int)((sqrtf(8.0f * (float)l + 1.0f) - 1.0f) * 0.5f);
+        while ((rr + 1) * (rr + 2) / 2 <= l) rr++;
+        while (rr * (rr + 1) / 2 > l) rr--;
+        I = it.I0 + rr;
+        J = it.J0 + (l - rr * (rr + 1) / 2);
+    }
+}
+
+// Diagonal tiles are stored as their lower triangle, column-major packed,
+// with the diagonal halved: D = L' + L'^T, so a diagonal tile is applied
+// exactly like an off-diagonal one (direct + transposed) from half the bytes.
+__device__ __forceinline__ int diag_col_off(int j) { return j * TILE - j * (j - 1) / 2; }
+
+// offset (doubles) of local tile l = (I, J) inside its item
+__device__ __forceinline__ int64_t item_tile_off(const ItemDesc& it, int l, int I) {
+    if (!it.tri) return (int64_t)l * TILE_ELEMS;
+    const int rr = I - it.I0;                  // diagonal tiles of rows 0..rr-1 precede l
+    return (int64_t)(l - rr) * TILE_ELEMS + (int64_t)rr * DIAG_ELEMS;
+}
+
+// lane i loads row i of tile (I, J) (packed form when I == J)
+__device__ __forceinline__ void load_tile_row(double* a, const double* T, bool diag, int lane) {
+    if (!diag) {
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) a[j] = __ldcs(T + j * TILE + lane);
+    } else {
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? __ldcs(T + diag_col_off(j) + lane - j) : 0.0;
+    }
+}
+
+// butterfly reduce-scatter of 32 per-lane values: afterwards v[0] of lane l
+// holds sum over lanes of the original v[l].
+template <int OFF>
+__device__ __forceinline__ void rs_stage(double* v, int lane) {
+    const bool upper = (lane & OFF) != 0;
+#pragma unroll
+    for (int j = 0; j < OFF; ++j) {
+        double send = upper ? v[j] : v[j + OFF];
+        double keep = upper ? v[j + OFF] : v[j];
+        v[j] = keep + __shfl_xor_sync(FULL, send, OFF);
+    }
+}
+
+
+// ---- mbarrier / bulk-copy helpers (TMA, sm_90+) -----------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+static inline int vec_grid(int64_t n) {
+    int64_t g = (n + VEC_THREADS - 1) / VEC_THREADS;
+    return (int)(g < RED_BLOCKS ? (g > 0 ? g : 1) : RED_BLOCKS);
+}
+
+}  // namespace ddg

@@ -7,7 +7,7 @@
 //   (host, threaded) -> device: local inverses A_i^{-1} (extract + batched
 //   Gauss-Jordan + pack) and the coarse inverse A_c^{-1}.
 // Solve: PCG whose every vector operation and every
-// preconditioner step runs in kernels.cu; the host only enqueues (one CUDA
+// preconditioner step runs in the .cu kernels; the host only enqueues (one CUDA
 // graph per iteration) and polls the device `done` flag every few iterations.
 #include <cuda_runtime.h>
 #include <math.h>

@@ -1,0 +1,1046 @@
+// symv.cu — colour-sweep kernels (a4, a8): flat residual gather, per-item SYMV, the persistent bulk-copy-ring SYMVs, partial reduction
+// (part of libddg's sm_100a kernels; shared device helpers in kernel_common.cuh)
+#include "kernel_common.cuh"
+
+namespace ddg {
+// =============================================================================
+// Multiplicative Schwarz colour step
+// =============================================================================
+
+// flat residual restriction of one colour: x over its s segments
+template <int SW>
+__global__ void __launch_bounds__(256)
+k_gather_flat(int64_t x0, int64_t x1, const int32_t* __restrict__ gidx, DevCSR A, const double* __restrict__ r,
+              const double* __restrict__ z, double* __restrict__ s, int z_is_zero, const int32_t* done) {
+    if (*done) return;
+    const int64_t ng = (int64_t)gridDim.x * blockDim.x / SW;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / SW;
+    const int sl = threadIdx.x % SW;
+    for (int64_t base = x0; base < x1; base += ng) {
+        const int64_t x = base + g;
+        const int v = x < x1 ? gidx[x] : -1;
+        const bool ok = v >= 0;
+        const double az = z_is_zero ? 0.0 : row_dot<SW>(A, v, ok, z, sl);
+        if (ok && sl == 0) s[x] = r[v] - az;
+    }
+}
+
+// Tiled symmetric matrix-vector product y = S s over one item-block of a
+// packed symmetric operator.  Warp w handles tiles w, w+W, ...; lane i owns
+// row i of each tile: direct part y_I += S_IJ s_J by per-lane dot products,
+// transposed part y_J += S_IJ^T s_I by a butterfly reduce-scatter.  Per-warp
+// partials in shared memory are summed in warp order (deterministic).
+__global__ void __launch_bounds__(SYMV_WARPS * 32)
+k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
+       const double* __restrict__ tiles, const double* __restrict__ s,
+       const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
+       double* __restrict__ partials, const int32_t* done, unsigned* __restrict__ tickets,
+       int gather_mode, DevCSR A, const double* __restrict__ rvec) {
+    if (*done) return;
+    extern __shared__ double sm[];
+    const ItemDesc it = items[item_begin + blockIdx.x];
+    const OpDesc op = ops[it.op];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int rows_r = (it.I1 - it.I0) * TILE;
+    const int rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+    const int rows_t = rows_r + rows_c;
+    double* s_sm = sm;                          // [rows_t]: s over row block, then col block
+    double* part = sm + rows_t;                 // [SYMV_WARPS][rows_t]
+    const double* tbase = tiles + it.tile_off;
+    // issue this warp's first tile loads now: their latency overlaps the prologue
+    double a[TILE];
+    if (w < it.ntiles) {
+        int I0_, J0_;
+        item_tile(it, w, I0_, J0_);
+        load_tile_row(a, tbase + item_tile_off(it, w, I0_), I0_ == J0_, lane);
+    }
+    if (gather_mode) {
+        // fused residual restriction (single-item operators): s = R~_i (r - A z)
+        const int32_t* idx = oidx + op.idx_off;
+        for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
+            double v = 0.0;
+            if (x < op.m) {
+                const int node = idx[x];
+                double az = 0.0;
+                if (gather_mode == 1)
+                    az = row_dot_csr(A, node, z);
+                v = rvec[node] - az;
+            }
+            s_sm[x] = v;
+        }
+    } else {
+        const double* sop = s + op.s_off;
+        for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
+            int g = x < rows_r ? it.I0 * TILE + x : it.J0 * TILE + (x - rows_r);
+            s_sm[x] = sop[g];
+        }
+    }
+    for (int x = threadIdx.x; x < SYMV_WARPS * rows_t; x += blockDim.x) part[x] = 0.0;
+    __syncthreads();
+    double* pw = part + w * rows_t;
+    for (int l = w; l < it.ntiles; l += SYMV_WARPS) {
+        int I, J;
+        item_tile(it, l, I, J);
+        if (l != w) load_tile_row(a, tbase + item_tile_off(it, l, I), I == J, lane);
+        const int ri = (I - it.I0) * TILE;                           // row offset in s_sm / pw
+        const int cj = it.tri ? (J - it.I0) * TILE : rows_r + (J - it.J0) * TILE;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) acc += a[j] * s_sm[cj + j];
+        const double si = s_sm[ri + lane];
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) a[j] *= si;
+        rs_stage<16>(a, lane);
+        rs_stage<8>(a, lane);
+        rs_stage<4>(a, lane);
+        rs_stage<2>(a, lane);
+        rs_stage<1>(a, lane);
+        if (I != J) {
+            pw[ri + lane] += acc;
+            pw[cj + lane] += a[0];
+        } else {
+            pw[ri + lane] += acc + a[0];
+        }
+    }
+    __syncthreads();
+    const bool single = it.part_off < 0;
+    for (int x = threadIdx.x; x < rows_t; x += blockDim.x) {
+        double y = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < SYMV_WARPS; ++ww) y += part[ww * rows_t + x];
+        if (single) {
+            const int g = it.I0 * TILE + x;     // single-item op: one triangle from 0
+            if (g < op.m) {
+                if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+                else y_out[g] = y;
+            }
+        } else {
+            partials[it.part_off + x] = y;
+        }
+    }
+    if (single || op.out_mode == 2) return;   // fronts: reduced by k_front_reduce
+    // multi-item operator: the last CTA to finish it sums every row's partial
+    // segments in fixed item order (deterministic) and applies the result
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(&tickets[it.op], 1u) == (unsigned)op.nitems - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int rb = op.BT * TILE;
+    for (int g = threadIdx.x; g < op.m; g += blockDim.x) {
+        const int b = g / rb, x = g % rb;
+        double y = 0.0;
+        for (int j = 0; j <= b; ++j) {
+            const ItemDesc& ij = items[op.item_base + b * (b + 1) / 2 + j];
+            y += __ldcg(partials + ij.part_off + x);
+        }
+        for (int i = b + 1; i < op.nblk; ++i) {
+            const ItemDesc& ii = items[op.item_base + i * (i + 1) / 2 + b];
+            y += __ldcg(partials + ii.part_off + (ii.I1 - ii.I0) * TILE + x);
+        }
+        if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+        else y_out[g] = y;
+    }
+    if (threadIdx.x == 0) tickets[it.op] = 0u;
+}
+
+// ---- warp-per-subdomain SYMV for small single-item operators (nT <= 8) ----
+// Each warp owns one subdomain end to end: fused residual restriction, all
+// tiles (two in flight: register double buffer), its own shared y, scatter.
+// No CTA barrier anywhere, so warps of a CTA stream independently.
+constexpr int SMALL_MAXROWS = 256;
+
+__device__ __forceinline__ void tile_apply(const double* __restrict__ a_in, double* a, const double* s,
+                                           double* y, int ri, int cj, bool diag, int lane) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) acc += a_in[j] * s[cj + j];
+    const double si = s[ri + lane];
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) a[j] = a_in[j] * si;
+    rs_stage<16>(a, lane);
+    rs_stage<8>(a, lane);
+    rs_stage<4>(a, lane);
+    rs_stage<2>(a, lane);
+    rs_stage<1>(a, lane);
+    if (!diag) {
+        y[ri + lane] += acc;
+        __syncwarp();
+        y[cj + lane] += a[0];
+    } else {
+        y[ri + lane] += acc + a[0];
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(256)
+k_symv_small(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin, int nitems,
+             const double* __restrict__ tiles, const double* __restrict__ s, const int32_t* __restrict__ oidx,
+             double* __restrict__ z, double* __restrict__ y_out, const int32_t* done, int gather_mode, DevCSR A,
+             const double* __restrict__ rvec) {
+    if (*done) return;
+    __shared__ double ssm[8][SMALL_MAXROWS];
+    __shared__ double ysm[8][SMALL_MAXROWS];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ii = blockIdx.x * 8 + w;
+    if (ii >= nitems) return;
+    const ItemDesc it = items[item_begin + ii];
+    const OpDesc op = ops[it.op];
+    const double* tb = tiles + it.tile_off;
+    double a[TILE], b[TILE];
+    int I = 0, J = 0;
+    item_tile(it, 0, I, J);
+    load_tile_row(a, tb + item_tile_off(it, 0, I), I == J, lane);       // first tile in flight
+    double* sw = ssm[w];
+    double* yw = ysm[w];
+    const int32_t* idx = oidx + op.idx_off;
+    for (int x = lane; x < op.mp; x += 32) {
+        double v = 0.0;
+        if (x < op.m) {
+            if (gather_mode) {
+                const int node = idx[x];
+                double az = 0.0;
+                if (gather_mode == 1)
+                    az = row_dot_csr(A, node, z);
+                v = rvec[node] - az;
+            } else {
+                v = s[op.s_off + x];
+            }
+        }
+        sw[x] = v;
+        yw[x] = 0.0;
+    }
+    __syncwarp();
+    for (int l = 0; l < it.ntiles; l += 2) {
+        int I1 = 0, J1 = 0;
+        const bool has1 = l + 1 < it.ntiles;
+        if (has1) {
+            item_tile(it, l + 1, I1, J1);
+            load_tile_row(b, tb + item_tile_off(it, l + 1, I1), I1 == J1, lane);
+        }
+        tile_apply(a, a, sw, yw, I * TILE, J * TILE, I == J, lane);
+        if (l + 2 < it.ntiles) {
+            item_tile(it, l + 2, I, J);
+            load_tile_row(a, tb + item_tile_off(it, l + 2, I), I == J, lane);
+        }
+        if (has1) tile_apply(b, b, sw, yw, I1 * TILE, J1 * TILE, I1 == J1, lane);
+    }
+    for (int x = lane; x < op.m; x += 32) {
+        if (op.out_mode == 0) z[idx[x]] += yw[x];
+        else y_out[x] = yw[x];
+    }
+}
+
+// ---- persistent streaming SYMV: bulk-copy ring, warp-specialised ----------
+// One CTA per SM walks a byte-balanced contiguous range of the launch's items
+// (host partition `cta_part`).  Roles:
+//  * warp 8 lane 0 (producer): streams each item's s segment(s) and its tiles
+//    (RING_TILES tiles per chunk, <= 32 KB) into shared memory with
+//    cp.async.bulk + mbarrier complete_tx, up to RING_NST chunks ahead and
+//    across item boundaries, so HBM never waits on the consumers;
+//  * warps 0-7 (consumers): each owns a fixed set of the item's tiles and
+//    progresses independently of the other consumer warps.  Tile (I, J):
+//    direct part y_I += S_IJ s_J by per-lane dot products into the warp's
+//    partial rows; transposed part y_J += S_IJ^T s_I accumulated per lane in
+//    registers (t[j] += S_IJ[lane][j] s_I[lane]) over the warp's consecutive
+//    tiles of the same column J, then one butterfly reduce-scatter per column
+//    run.  Owner of a tile: l % 8 in rectangular items (= its column for the
+//    8-wide blocks), (J + item counter) % 8 in triangles (one column per warp,
+//    rotated across items so the long columns are spread over the warps);
+//  * warp 9 (epilogue): sums the 8 warps' partial rows in warp order
+//    (deterministic) and applies them -- z[idx] += y with idx and z prefetched
+//    before the item finishes (same-colour subdomains are disjoint), y_out = y,
+//    or the partial segment of a multi-item operator (reduced later).
+// Partial rows are double-buffered by item parity, so consumer warps never
+// wait for each other.  Measured ceiling of this access pattern:
+// tools/bwprobe.cu ("tma ring" rows).
+constexpr int RING_EPI_WARPS = 2;
+constexpr int RING_THREADS = (SYMV_WARPS + 1 + RING_EPI_WARPS) * 32;
+constexpr int RING_MAX_NST = 24;
+constexpr int RING_MAX_NB = 8;
+// shared memory of a launch: nst slots of RT tiles; nb item buffers, each the
+// item's s (maxr rows), the 8 consumer warps' partial rows and a descriptor;
+// barriers
+__host__ __device__ constexpr size_t ring_smem(int RT, int nst, int nb, int R, int Cr) {
+    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * (R + Cr) * 8 + (size_t)nb * (SYMV_WARPS * R + Cr) * 8 +
+           (size_t)nb * 8 * 4 + (2 * (size_t)nst + 4 * (size_t)nb) * 8;
+}
+
+// first double of tile l of item it (l == ntiles: one past the last tile)
+__device__ __forceinline__ int64_t item_tile_off_l(const ItemDesc& it, int l) {
+    if (l >= it.ntiles) return item_doubles(it.tri, it.I1 - it.I0, it.ntiles);
+    int I, J;
+    item_tile(it, l, I, J);
+    return item_tile_off(it, l, I);
+}
+
+// descriptors of the next items, fetched ahead so no role stalls on them
+struct DescPipe {
+    ItemDesc it1, it2;
+    OpDesc op1;
+    __device__ __forceinline__ void init(const ItemDesc* items, const OpDesc* ops, int i0, int i1) {
+        it1 = items[i0];
+        op1 = ops[it1.op];
+        if (i0 + 1 < i1) it2 = items[i0 + 1];
+    }
+    __device__ __forceinline__ void next(const ItemDesc* items, const OpDesc* ops, int ii, int i1, ItemDesc& it,
+                                         OpDesc& op) {
+        it = it1;
+        op = op1;
+        if (ii + 1 < i1) {
+            it1 = it2;
+            op1 = ops[it1.op];
+        }
+        if (ii + 2 < i1) it2 = items[ii + 2];
+    }
+};
+
+__device__ __forceinline__ void flush_column(double* t, double* pw, int cj, int lane) {
+    rs_stage<16>(t, lane);
+    rs_stage<8>(t, lane);
+    rs_stage<4>(t, lane);
+    rs_stage<2>(t, lane);
+    rs_stage<1>(t, lane);
+    pw[cj + lane] += t[0];
+}
+
+template <int RT>
+__global__ void __launch_bounds__(RING_THREADS, 1)
+k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
+            const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
+            const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
+            double* __restrict__ partials, const int32_t* done, int nst, int nb, int R, int Cr,
+            unsigned long long* rtrace) {
+    constexpr int SLOT = RT * TILE_ELEMS;
+    // item buffers: s over R + Cr rows; partial rows: the row block replicated
+    // per consumer warp ([8][R], every warp adds direct parts to any row) and
+    // the column block of rectangles once ([Cr], each column has one owner)
+    const int maxr = R + Cr, PB = SYMV_WARPS * R + Cr;
+    // DDG_RING_TRACE: cycles per role and wait (debug; rtrace == nullptr otherwise)
+    unsigned long long tw[4] = {0, 0, 0, 0}, tstart = rtrace ? clock64() : 0, ntile = 0, nflush = 0;
+#define RT_WAIT(k, call)                                        \
+    do {                                                        \
+        if (rtrace) {                                           \
+            const unsigned long long t0_ = clock64();           \
+            call;                                               \
+            tw[k] += clock64() - t0_;                           \
+        } else {                                                \
+            call;                                               \
+        }                                                       \
+    } while (0)
+#define RT_FLUSH(base)                                                                  \
+    do {                                                                                \
+        if (rtrace && lane == 0) {                                                      \
+            atomicAdd(&rtrace[(base)], tw[0]);                                          \
+            atomicAdd(&rtrace[(base) + 1], tw[1]);                                      \
+            atomicAdd(&rtrace[(base) + 2], tw[2]);                                      \
+            atomicAdd(&rtrace[(base) + 3], clock64() - tstart);                         \
+            atomicAdd(&rtrace[(base) + 4], ntile);                                      \
+            atomicAdd(&rtrace[(base) + 5], nflush);                                     \
+            atomicAdd(&rtrace[(base) + 6], tw[3]);                                      \
+        }                                                                               \
+    } while (0)
+    if (*done) return;
+    extern __shared__ __align__(128) double rsm[];
+    double* ring = rsm;                                          // [nst][SLOT]
+    double* s_sm = ring + (size_t)nst * SLOT;                    // [nb][maxr]
+    double* part = s_sm + (size_t)nb * maxr;                     // [nb][PB]
+    int32_t* dsc = reinterpret_cast<int32_t*>(part + (size_t)nb * PB);   // [nb][8]
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsc + nb * 8);
+    uint64_t* empty = full + nst;
+    uint64_t* sfull = empty + nst;    // [nb] s + descriptor of the item landed
+    uint64_t* sempty = sfull + nb;    // [nb] consumers done with the item's s
+    uint64_t* pdone = sempty + nb;    // [nb] consumers' partial rows final
+    uint64_t* pfree = pdone + nb;     // [nb] epilogue done with the partial rows
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], SYMV_WARPS);                  // every consumer warp, every chunk
+        }
+        for (int b = 0; b < nb; ++b) {
+            mbar_init(&sfull[b], 1);
+            mbar_init(&sempty[b], SYMV_WARPS);
+            mbar_init(&pdone[b], SYMV_WARPS * 32);
+            mbar_init(&pfree[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (i0 >= i1) return;
+    if (warp == SYMV_WARPS) {                                    // ---- producer warp ----
+        // Lane 0 owns the barriers; the tile copies of a triangle chunk are
+        // issued by lanes 0..nt-1 in one instruction (a bulk-copy issue costs
+        // the issuing thread a few hundred cycles: one per lane overlaps them).
+        DescPipe dp;
+        dp.init(items, ops, i0, i1);
+        unsigned slot = 0, sph = 0;                                // ring slot and its fill count
+        int bi = 0;
+        unsigned bph = 0;                                          // item buffer and its use count
+        for (int ii = i0; ii < i1; ++ii) {
+            ItemDesc it;
+            OpDesc op;
+            RT_WAIT(2, dp.next(items, ops, ii, i1, it, op); it.tri += 0);
+            const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+            if (bph > 0) RT_WAIT(0, mbar_wait(&sempty[bi], (bph - 1) & 1));
+            if (lane == 0) {
+                int32_t* d = dsc + bi * 8;
+                d[0] = it.I0; d[1] = it.I1; d[2] = it.J0; d[3] = it.J1; d[4] = it.tri; d[5] = it.ntiles;
+                mbar_expect_tx(&sfull[bi], (unsigned)(rows_r + rows_c) * 8u);
+            }
+            __syncwarp();
+            const double* sop = s + op.s_off;
+            double* sb = s_sm + (size_t)bi * maxr;
+            if (lane == 0) bulk_g2s(sb, sop + it.I0 * TILE, rows_r * 8u, &sfull[bi]);
+            if (lane == 1 && rows_c) bulk_g2s(sb + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[bi]);
+            if (++bi == nb) { bi = 0; ++bph; }
+            // tile q of a chunk always lands at q * 8 KB of its slot; rectangular
+            // items are contiguous full tiles (one copy per chunk), triangles
+            // copy tile by tile (packed diagonal tiles are 4224 B)
+            const double* src = tiles + it.tile_off;
+            for (int l0 = 0; l0 < it.ntiles; l0 += RT) {
+                const int nt = min(RT, it.ntiles - l0);
+                if (sph > 0) RT_WAIT(1, mbar_wait(&empty[slot], (sph - 1) & 1));
+                const unsigned long long tc0 = rtrace ? clock64() : 0;
+                double* dst = ring + (size_t)slot * SLOT;
+                if (!it.tri) {
+                    if (lane == 0) {
+                        mbar_expect_tx(&full[slot], (unsigned)nt * TILE_ELEMS * 8u);
+                        bulk_g2s(dst, src + (int64_t)l0 * TILE_ELEMS, (unsigned)nt * TILE_ELEMS * 8u, &full[slot]);
+                    }
+                } else {
+                    unsigned tb = 0;
+                    int64_t toff = 0;
+                    if (lane < nt) {
+                        int I_, J_;
+                        item_tile(it, l0 + lane, I_, J_);
+                        tb = (I_ == J_ ? DIAG_ELEMS : TILE_ELEMS) * 8u;
+                        toff = item_tile_off(it, l0 + lane, I_);
+                    }
+                    unsigned bytes = tb;
+#pragma unroll
+                    for (int o = 1; o < RT; o <<= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
+                    if (lane == 0) mbar_expect_tx(&full[slot], bytes);
+                    __syncwarp();
+                    if (lane < nt) bulk_g2s(dst + lane * TILE_ELEMS, src + toff, tb, &full[slot]);
+                }
+                if (rtrace) tw[3] += clock64() - tc0;
+                if (++slot == (unsigned)nst) { slot = 0; ++sph; }
+            }
+        }
+        RT_FLUSH(0);
+        return;
+    }
+    if (warp > SYMV_WARPS) {                                     // ---- epilogue warps ----
+        const int e = warp - SYMV_WARPS - 1;                      // handles items ki = e, e+E, ...
+        for (int ii = i0 + e, ki = e; ii < i1; ii += RING_EPI_WARPS, ki += RING_EPI_WARPS) {
+            const ItemDesc it = items[ii];
+            const OpDesc op = ops[it.op];
+            const int b = ki % nb;
+            const unsigned ph = (unsigned)(ki / nb);
+            const int rows_t = (it.I1 - it.I0 + (it.tri ? 0 : it.J1 - it.J0)) * TILE;
+            const int g0 = it.I0 * TILE;
+            const int nr = min(rows_t, op.m - g0);                // single-item ops only
+            const bool scat = it.part_off < 0 && op.out_mode == 0;
+            int ix[RING_MAX_ROWS / 32];
+            double zv[RING_MAX_ROWS / 32];
+            if (scat) {
+                const int32_t* idx = oidx + op.idx_off + g0;
+#pragma unroll
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) ix[r] = (lane + 32 * r < nr) ? idx[lane + 32 * r] : 0;
+#pragma unroll
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
+            }
+            RT_WAIT(0, mbar_wait(&pdone[b], ph & 1));
+            const double* pp = part + (size_t)b * PB;
+            const int rows_r = (it.I1 - it.I0) * TILE;
+#pragma unroll
+            for (int r = 0; r < RING_MAX_ROWS / 32; ++r) {
+                const int x = lane + 32 * r;
+                if (x < rows_t) {
+                    double y = 0.0;
+                    if (x < rows_r) {
+#pragma unroll
+                        for (int ww = 0; ww < SYMV_WARPS; ++ww) y += pp[ww * R + x];
+                    } else {
+                        y = pp[SYMV_WARPS * R + x - rows_r];       // column block (one owner)
+                    }
+                    if (it.part_off >= 0) partials[it.part_off + x] = y;
+                    else if (x < nr) {
+                        if (scat) z[ix[r]] = zv[r] + y;
+                        else y_out[g0 + x] = y;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfree[b]);
+        }
+        RT_FLUSH(8);
+        return;
+    }
+    // ---- consumers (warps 0..7): each walks only its own tiles ----
+    unsigned slot = 0, sph = 0;
+    int bi = 0;
+    unsigned bph = 0;
+    for (int ki = 0; ki < i1 - i0; ++ki) {
+        RT_WAIT(0, mbar_wait(&sfull[bi], bph & 1));
+        const int32_t* d = dsc + bi * 8;
+        const int I0 = d[0], I1 = d[1], J0 = d[2], J1 = d[3], tri = d[4], ntiles = d[5];
+        const double* ss = s_sm + (size_t)bi * maxr;
+        const int rows_r = (I1 - I0) * TILE;
+        double* pw = part + (size_t)bi * PB + (size_t)warp * R;    // this warp's row-block rows
+        double* pcb = part + (size_t)bi * PB + SYMV_WARPS * R;     // column block (rectangles)
+        if (bph > 0) RT_WAIT(1, mbar_wait(&pfree[bi], (bph - 1) & 1));
+        for (int x = lane; x < rows_r; x += 32) pw[x] = 0.0;
+        __syncwarp();
+        double t[TILE];
+#pragma unroll
+        for (int j = 0; j < TILE; ++j) t[j] = 0.0;
+        int curJ = -1;
+        auto tile = [&](const double* T, int I, int J) {
+            const int ri = (I - I0) * TILE;
+            const int cj = tri ? (J - I0) * TILE : rows_r + (J - J0) * TILE;
+            ++ntile;
+            if (J != curJ) {
+                if (curJ >= 0) {                                   // (triangles only: one column per
+                    ++nflush;                                      //  warp in a rectangle)
+                    flush_column(t, pw, (curJ - I0) * TILE, lane);
+#pragma unroll
+                    for (int j = 0; j < TILE; ++j) t[j] = 0.0;
+                }
+                curJ = J;
+            }
+            double a[TILE];
+            if (I != J) {
+#pragma unroll
+                for (int j = 0; j < TILE; ++j) a[j] = T[j * TILE + lane];
+            } else {
+#pragma unroll
+                for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? T[diag_col_off(j) + lane - j] : 0.0;
+            }
+            const double2* sJ = reinterpret_cast<const double2*>(ss + cj);
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+            for (int j = 0; j < TILE; j += 4) {
+                const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                d0 = fma(a[j], u.x, d0);
+                d1 = fma(a[j + 1], u.y, d1);
+                d2 = fma(a[j + 2], v.x, d2);
+                d3 = fma(a[j + 3], v.y, d3);
+            }
+            pw[ri + lane] += (d0 + d1) + (d2 + d3);
+            const double si = ss[ri + lane];
+#pragma unroll
+            for (int j = 0; j < TILE; ++j) t[j] = fma(a[j], si, t[j]);
+        };
+        // own-tile iterator, in increasing l.  Rectangles: column warp of every
+        // row (l = r * wd + warp; warps >= wd idle); each column has one owner.
+        // Triangles: columns c0 = (warp - ki) mod 8, c0+8, ... of rows r >= c.
+        int l = -1, I = 0, J = 0, r = 0, c = 0;
+        const int h = I1 - I0, wd = J1 - J0, c0 = (warp - ki) & (SYMV_WARPS - 1);
+        if (!tri) {
+            if (warp < wd) { l = warp; I = I0; J = J0 + warp; }
+        } else if (c0 < h) {
+            r = c0; c = c0; l = r * (r + 1) / 2 + c; I = I0 + r; J = J0 + c;
+        }
+        auto advance = [&]() {
+            if (!tri) {
+                l += wd;
+                ++I;
+                if (I >= I1) l = -1;
+            } else {
+                c += SYMV_WARPS;
+                if (c > r) { ++r; c = c0; }
+                if (r >= h) { l = -1; return; }
+                l = r * (r + 1) / 2 + c; I = I0 + r; J = J0 + c;
+            }
+        };
+        // every warp visits every chunk in order (keeps the mbarrier phases
+        // of each slot in step), consuming only its own tiles
+        for (int l0 = 0; l0 < ntiles; l0 += RT) {
+            RT_WAIT(2, mbar_wait(&full[slot], sph & 1));
+            const double* C = ring + (size_t)slot * SLOT;
+            while (l >= 0 && l < l0 + RT) {
+                tile(C + (l - l0) * TILE_ELEMS, I, J);
+                advance();
+            }
+            __syncwarp();                                          // every lane has consumed its rows
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (++slot == (unsigned)nst) { slot = 0; ++sph; }
+        }
+        if (curJ >= 0) {
+            if (tri) {
+                flush_column(t, pw, (curJ - I0) * TILE, lane);
+            } else {                                               // sole owner of this column
+                rs_stage<16>(t, lane);
+                rs_stage<8>(t, lane);
+                rs_stage<4>(t, lane);
+                rs_stage<2>(t, lane);
+                rs_stage<1>(t, lane);
+                pcb[(curJ - J0) * TILE + lane] = t[0];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[bi]);
+        mbar_arrive(&pdone[bi]);                                   // every lane (release its rows)
+        if (++bi == nb) { bi = 0; ++bph; }
+    }
+    RT_FLUSH(16);
+#undef RT_WAIT
+#undef RT_FLUSH
+}
+
+// ---- k_symv_ring2: row warps + column warps ----------------------------------
+// Same producer, ring, item buffers and epilogue as k_symv_ring; the 16
+// consumer warps split each tile's two products by role:
+//  * row warps (0-7): own tile rows r (owner (r + item counter) mod 8); lane i
+//    accumulates the direct part y_I[i] += sum_j S_IJ[i][j] s_J[j] in one
+//    register across the row's tiles, then writes pr[row] once;
+//  * column warps (8-15): own tile columns c; lane j accumulates the
+//    transposed part y_J[j] += sum_i S_IJ[i][j] s_I[i] walking the tile along a
+//    rotated diagonal (i = (t + j) mod 32: two wavefronts per load, no bank
+//    conflicts) with s_I rotated by shuffles; one register per owned column,
+//    written to pc[column] at the end of the item.
+// Every row and column has a single owner, so the item's result is
+// y = pr + pc (triangles) or pr | pc (rectangles: row block | column block)
+// -- two partial arrays instead of eight, no butterfly, ~40 registers per
+// consumer thread.
+constexpr int R2_ROWW = 8, R2_COLW = 8, R2_CONS = R2_ROWW + R2_COLW;
+constexpr int RING2_THREADS = (R2_CONS + 1 + RING_EPI_WARPS) * 32;
+__host__ __device__ constexpr size_t ring2_smem(int RT, int nst, int nb, int maxr) {
+    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * 3 * maxr * 8 + (size_t)nb * 8 * 4 +
+           (2 * (size_t)nst + 4 * (size_t)nb) * 8;
+}
+
+template <int RT>
+__global__ void __launch_bounds__(RING2_THREADS, 1)
+k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
+             const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
+             const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
+             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr) {
+    constexpr int SLOT = RT * TILE_ELEMS;
+    if (*done) return;
+    extern __shared__ __align__(128) double rsm[];
+    double* ring = rsm;                                          // [nst][SLOT]
+    double* s_sm = ring + (size_t)nst * SLOT;                    // [nb][maxr]
+    double* pr_sm = s_sm + (size_t)nb * maxr;                    // [nb][maxr]  row (direct) parts
+    double* pc_sm = pr_sm + (size_t)nb * maxr;                   // [nb][maxr]  column (transposed) parts
+    int32_t* dsc = reinterpret_cast<int32_t*>(pc_sm + (size_t)nb * maxr);   // [nb][8]
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsc + nb * 8);
+    uint64_t* empty = full + nst;
+    uint64_t* sfull = empty + nst;
+    uint64_t* sempty = sfull + nb;
+    uint64_t* pdone = sempty + nb;
+    uint64_t* pfree = pdone + nb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], R2_CONS);
+        }
+        for (int b = 0; b < nb; ++b) {
+            mbar_init(&sfull[b], 1);
+            mbar_init(&sempty[b], R2_CONS);
+            mbar_init(&pdone[b], R2_CONS * 32);
+            mbar_init(&pfree[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (i0 >= i1) return;
+    if (warp == R2_CONS) {                                       // ---- producer warp ----
+        DescPipe dp;
+        dp.init(items, ops, i0, i1);
+        unsigned slot = 0, sph = 0;
+        int bi = 0;
+        unsigned bph = 0;
+        for (int ii = i0; ii < i1; ++ii) {
+            ItemDesc it;
+            OpDesc op;
+            dp.next(items, ops, ii, i1, it, op);
+            const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+            if (bph > 0) mbar_wait(&sempty[bi], (bph - 1) & 1);
+            if (lane == 0) {
+                int32_t* d = dsc + bi * 8;
+                d[0] = it.I0; d[1] = it.I1; d[2] = it.J0; d[3] = it.J1; d[4] = it.tri; d[5] = it.ntiles;
+                mbar_expect_tx(&sfull[bi], (unsigned)(rows_r + rows_c) * 8u);
+            }
+            __syncwarp();
+            const double* sop = s + op.s_off;
+            double* sb = s_sm + (size_t)bi * maxr;
+            if (lane == 0) bulk_g2s(sb, sop + it.I0 * TILE, rows_r * 8u, &sfull[bi]);
+            if (lane == 1 && rows_c) bulk_g2s(sb + rows_r, sop + it.J0 * TILE, rows_c * 8u, &sfull[bi]);
+            if (++bi == nb) { bi = 0; ++bph; }
+            const double* src = tiles + it.tile_off;
+            for (int l0 = 0; l0 < it.ntiles; l0 += RT) {
+                const int nt = min(RT, it.ntiles - l0);
+                if (sph > 0) mbar_wait(&empty[slot], (sph - 1) & 1);
+                double* dst = ring + (size_t)slot * SLOT;
+                if (!it.tri) {
+                    if (lane == 0) {
+                        mbar_expect_tx(&full[slot], (unsigned)nt * TILE_ELEMS * 8u);
+                        bulk_g2s(dst, src + (int64_t)l0 * TILE_ELEMS, (unsigned)nt * TILE_ELEMS * 8u, &full[slot]);
+                    }
+                } else {
+                    unsigned tb = 0;
+                    int64_t toff = 0;
+                    if (lane < nt) {
+                        int I_, J_;
+                        item_tile(it, l0 + lane, I_, J_);
+                        tb = (I_ == J_ ? DIAG_ELEMS : TILE_ELEMS) * 8u;
+                        toff = item_tile_off(it, l0 + lane, I_);
+                    }
+                    unsigned bytes = tb;
+#pragma unroll
+                    for (int o = 1; o < RT; o <<= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
+                    if (lane == 0) mbar_expect_tx(&full[slot], bytes);
+                    __syncwarp();
+                    if (lane < nt) bulk_g2s(dst + lane * TILE_ELEMS, src + toff, tb, &full[slot]);
+                }
+                if (++slot == (unsigned)nst) { slot = 0; ++sph; }
+            }
+        }
+        return;
+    }
+    if (warp > R2_CONS) {                                        // ---- epilogue warps ----
+        const int e = warp - R2_CONS - 1;
+        for (int ii = i0 + e, ki = e; ii < i1; ii += RING_EPI_WARPS, ki += RING_EPI_WARPS) {
+            const ItemDesc it = items[ii];
+            const OpDesc op = ops[it.op];
+            const int b = ki % nb;
+            const unsigned ph = (unsigned)(ki / nb);
+            const int rows_r = (it.I1 - it.I0) * TILE;
+            const int rows_t = rows_r + (it.tri ? 0 : (it.J1 - it.J0) * TILE);
+            const int g0 = it.I0 * TILE;
+            const int nr = min(rows_t, op.m - g0);
+            const bool scat = it.part_off < 0 && op.out_mode == 0;
+            int ix[RING_MAX_ROWS / 32];
+            double zv[RING_MAX_ROWS / 32];
+            if (scat) {
+                const int32_t* idx = oidx + op.idx_off + g0;
+#pragma unroll
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) ix[r] = (lane + 32 * r < nr) ? idx[lane + 32 * r] : 0;
+#pragma unroll
+                for (int r = 0; r < RING_MAX_ROWS / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
+            }
+            mbar_wait(&pdone[b], ph & 1);
+            const double* pr = pr_sm + (size_t)b * maxr;
+            const double* pc = pc_sm + (size_t)b * maxr;
+#pragma unroll
+            for (int r = 0; r < RING_MAX_ROWS / 32; ++r) {
+                const int x = lane + 32 * r;
+                if (x < rows_t) {
+                    const double y = it.tri ? pr[x] + pc[x] : (x < rows_r ? pr[x] : pc[x]);
+                    if (it.part_off >= 0) partials[it.part_off + x] = y;
+                    else if (x < nr) {
+                        if (scat) z[ix[r]] = zv[r] + y;
+                        else y_out[g0 + x] = y;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfree[b]);
+        }
+        return;
+    }
+    // ---- consumers: row warps 0..7, column warps 8..15 ----
+    const bool colw = warp >= R2_ROWW;
+    const int wr = colw ? warp - R2_ROWW : warp;
+    unsigned slot = 0, sph = 0;
+    int bi = 0;
+    unsigned bph = 0;
+    for (int ki = 0; ki < i1 - i0; ++ki) {
+        mbar_wait(&sfull[bi], bph & 1);
+        const int32_t* d = dsc + bi * 8;
+        const int I0 = d[0], I1 = d[1], J1 = d[3], tri = d[4], ntiles = d[5];
+        const int J0 = d[2];
+        const double* ss = s_sm + (size_t)bi * maxr;
+        const int h = I1 - I0, wd = tri ? h : J1 - J0;
+        const int rows_r = h * TILE;
+        double* pr = pr_sm + (size_t)bi * maxr;
+        double* pc = pc_sm + (size_t)bi * maxr;
+        if (bph > 0) mbar_wait(&pfree[bi], (bph - 1) & 1);
+        // own tiles in increasing stream index l:
+        //   row warp:    rows a, a + 8 (a = (wr - ki) mod 8), each row's tiles in order
+        //   column warp: columns a, a + 8; per row r both owned columns in order
+        const int a = (wr - ki) & 7;
+        int l = -1, r = 0, c = 0, ccur = 0;
+        double acc = 0.0, acc0 = 0.0, acc1 = 0.0;
+        auto rowstart = [&](int rr) { return tri ? rr * (rr + 1) / 2 : rr * wd; };
+        auto rowlen = [&](int rr) { return tri ? rr + 1 : wd; };
+        if (!colw) {
+            if (a < h) { r = a; c = 0; l = rowstart(r); }
+        } else {
+            if (a < wd) {
+                r = tri ? a : 0;
+                ccur = 0;                                          // 0: column a, 1: column a + 8
+                c = a;
+                l = rowstart(r) + c;
+            }
+        }
+        auto advance = [&]() {
+            if (!colw) {
+                if (++c < rowlen(r)) { ++l; return; }
+                r += 8;
+                if (r >= h) { l = -1; return; }
+                c = 0;
+                l = rowstart(r);
+            } else {
+                const int c1 = a + 8;
+                if (ccur == 0 && c1 < wd && (!tri || c1 <= r)) {
+                    ccur = 1;
+                    c = c1;
+                } else {
+                    ++r;
+                    if (r >= h) { l = -1; return; }
+                    ccur = 0;
+                    c = a;
+                }
+                l = rowstart(r) + c;
+            }
+        };
+        for (int l0 = 0; l0 < ntiles; l0 += RT) {
+            mbar_wait(&full[slot], sph & 1);
+            const double* C = ring + (size_t)slot * SLOT;
+            while (l >= 0 && l < l0 + RT) {
+                const double* T = C + (l - l0) * TILE_ELEMS;
+                const bool diag = tri && r == c;
+                if (!colw) {
+                    // direct part: lane = row, s_J broadcast
+                    const double2* sJ = reinterpret_cast<const double2*>(ss + (tri ? c * TILE : rows_r + c * TILE));
+                    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+                    if (!diag) {
+#pragma unroll
+                        for (int j = 0; j < TILE; j += 4) {
+                            const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                            d0 = fma(T[j * TILE + lane], u.x, d0);
+                            d1 = fma(T[(j + 1) * TILE + lane], u.y, d1);
+                            d2 = fma(T[(j + 2) * TILE + lane], v.x, d2);
+                            d3 = fma(T[(j + 3) * TILE + lane], v.y, d3);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < TILE; j += 4) {
+                            const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                            if (lane >= j) d0 = fma(T[diag_col_off(j) + lane - j], u.x, d0);
+                            if (lane >= j + 1) d1 = fma(T[diag_col_off(j + 1) + lane - j - 1], u.y, d1);
+                            if (lane >= j + 2) d2 = fma(T[diag_col_off(j + 2) + lane - j - 2], v.x, d2);
+                            if (lane >= j + 3) d3 = fma(T[diag_col_off(j + 3) + lane - j - 3], v.y, d3);
+                        }
+                    }
+                    acc += (d0 + d1) + (d2 + d3);
+                    if (c == rowlen(r) - 1) {                      // row complete
+                        pr[r * TILE + lane] = acc;
+                        acc = 0.0;
+                    }
+                } else {
+                    // transposed part: lane = column, rotated walk of the tile
+                    const double sI = ss[r * TILE + lane];
+                    double d0 = 0.0, d1 = 0.0;
+                    if (!diag) {
+#pragma unroll
+                        for (int t = 0; t < TILE; t += 2) {
+                            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31;
+                            d0 = fma(T[lane * TILE + ia], __shfl_sync(FULL, sI, ia), d0);
+                            d1 = fma(T[lane * TILE + ib], __shfl_sync(FULL, sI, ib), d1);
+                        }
+                    } else {
+                        const double* Tc = T + diag_col_off(lane) - lane;   // element (i, lane) at Tc[i], i >= lane
+#pragma unroll
+                        for (int t = 0; t < TILE; t += 2) {
+                            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31;
+                            const double va = __shfl_sync(FULL, sI, ia), vb = __shfl_sync(FULL, sI, ib);
+                            if (ia >= lane) d0 = fma(Tc[ia], va, d0);
+                            if (ib >= lane) d1 = fma(Tc[ib], vb, d1);
+                        }
+                    }
+                    if (ccur == 0) acc0 += d0 + d1;
+                    else acc1 += d0 + d1;
+                }
+                advance();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (++slot == (unsigned)nst) { slot = 0; ++sph; }
+        }
+        if (colw && a < wd) {
+            pc[(tri ? a * TILE : rows_r + a * TILE) + lane] = acc0;
+            if (a + 8 < wd) pc[(tri ? (a + 8) * TILE : rows_r + (a + 8) * TILE) + lane] = acc1;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[bi]);
+        mbar_arrive(&pdone[bi]);                                   // every lane (release its rows)
+        if (++bi == nb) { bi = 0; ++bph; }
+    }
+}
+
+// Sum the partial segments of multi-item operators for one row block, in
+// fixed item order, and apply the result.
+__global__ void k_symv_reduce(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
+                              const RedDesc* __restrict__ red, int red_begin,
+                              const int32_t* __restrict__ oidx, const double* __restrict__ partials,
+                              double* __restrict__ z, double* __restrict__ y_out,
+                              const int32_t* done) {
+    if (*done) return;
+    const RedDesc rd = red[red_begin + blockIdx.x];
+    const OpDesc op = ops[rd.op];
+    const int b = rd.b;
+    const int rows_b = (min(op.nT, (b + 1) * op.BT) - b * op.BT) * TILE;
+    for (int x = threadIdx.x; x < rows_b; x += blockDim.x) {
+        const int g = b * op.BT * TILE + x;
+        double y = 0.0;
+        for (int j = 0; j <= b; ++j) {                       // items (b, j): row segments
+            const ItemDesc& it = items[op.item_base + b * (b + 1) / 2 + j];
+            y += partials[it.part_off + x];
+        }
+        for (int i = b + 1; i < op.nblk; ++i) {              // items (i, b): col segments
+            const ItemDesc& it = items[op.item_base + i * (i + 1) / 2 + b];
+            y += partials[it.part_off + (it.I1 - it.I0) * TILE + x];
+        }
+        if (g < op.m) {
+            if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
+            else y_out[g] = y;
+        }
+    }
+}
+
+
+// ---- launchers ----
+
+void launch_gather_flat(cudaStream_t st, int64_t x0, int64_t x1, const int32_t* gidx, DevCSR A, const double* r,
+                        const double* z, double* s, bool z_is_zero, const int32_t* done) {
+    if (x1 <= x0) return;
+    const int sw = z_is_zero ? 1 : std::max(1, A.sw);
+    const int64_t want = ((x1 - x0) * sw + 255) / 256;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * 8));
+    const int zz = z_is_zero ? 1 : 0;
+    switch (sw) {
+        case 4: k_gather_flat<4><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
+        case 8: k_gather_flat<8><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
+        case 32: k_gather_flat<32><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
+        default: k_gather_flat<1><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done);
+    }
+}
+
+static size_t symv_smem(int max_rows_t) {
+    return (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
+}
+
+void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
+                 int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,
+                 double* y_out, double* partials, const int32_t* done, int max_rows_t, unsigned* tickets,
+                 int gather_mode, DevCSR A, const double* r, bool small_ok) {
+    if (nitems <= 0) return;
+    if (max_rows_t <= 0) max_rows_t = 2 * MAX_BT * TILE;
+    if (small_ok && max_rows_t <= SMALL_MAXROWS) {
+        k_symv_small<<<(nitems + 7) / 8, 256, 0, st>>>(ops, items, item_begin, nitems, tiles, s, oidx, z, y_out,
+                                                      done, gather_mode, A, r);
+        return;
+    }
+    const size_t smem = symv_smem(max_rows_t);
+    cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_symv<<<nitems, SYMV_WARPS * 32, smem, st>>>(ops, items, item_begin, tiles, s, oidx, z, y_out,
+                                                  partials, done, tickets, gather_mode, A, r);
+}
+
+static bool g_ring_init[64] = {};
+static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0, g_ring_v2 = 0;
+static unsigned long long* g_ring_trace = nullptr;   // DDG_RING_TRACE (debug)
+// per device, once, outside any stream capture (called from ddg_setup)
+void symv_ring_init() {
+    g_ring_rt = 4;
+    if (const char* e = getenv("DDG_RING_TILES")) g_ring_rt = atoi(e);
+    if (g_ring_rt != 1 && g_ring_rt != 2 && g_ring_rt != 8) g_ring_rt = 4;
+    g_ring_nb = 0;
+    if (const char* e = getenv("DDG_RING_NB")) g_ring_nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
+    g_ring_nst = 0;
+    if (const char* e = getenv("DDG_RING_NST")) g_ring_nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
+    g_ring_v2 = getenv("DDG_RING_V2") ? atoi(getenv("DDG_RING_V2")) : -1;   // -1: auto
+
+    if (getenv("DDG_RING_TRACE") && !g_ring_trace) {
+        if (cudaMalloc(&g_ring_trace, 32 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(g_ring_trace, 0, 32 * sizeof(unsigned long long));
+        else
+            g_ring_trace = nullptr;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_ring_init[dev & 63]) return;
+    const size_t mx = 227 * 1024;
+    cudaFuncSetAttribute(k_symv_ring<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_ring2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    g_ring_init[dev & 63] = true;
+}
+
+// debug: read and zero the DDG_RING_TRACE counters (24 values; see k_symv_ring)
+int symv_ring_trace(unsigned long long* out) {
+    if (!g_ring_trace) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, g_ring_trace, 24 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemset(g_ring_trace, 0, 32 * sizeof(unsigned long long));
+    return 0;
+}
+
+void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
+                      const int32_t* cta_part, int ncta, int max_rows_r, int max_rows_c, const double* tiles,
+                      const double* s, const int32_t* oidx, double* z, double* y_out, double* partials,
+                      const int32_t* done, bool triangles) {
+    const int RT = g_ring_rt;
+    const int R = std::max(TILE, max_rows_r), Cr = std::max(0, max_rows_c);
+    const int maxr = std::min(RING_MAX_ROWS, R + Cr);
+    const size_t budget = 227 * 1024;
+    // row/column-warp consumers for launches of whole-subdomain triangles
+    // (measured: C3 +4%, C5 +1%; the 8-warp column consumers win on the
+    // 8-wide rectangles of split operators); DDG_RING_V2=0/1 forces either
+    if (g_ring_v2 == 1 || (g_ring_v2 < 0 && triangles) || RT == 8) {
+        int nb2 = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 4 : 2);
+        int nst2 = 2;
+        const int cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
+        while (nst2 < cap && ring2_smem(RT, nst2 + 1, nb2, maxr) <= budget) ++nst2;
+        const size_t smem2 = ring2_smem(RT, nst2, nb2, maxr);
+        if (RT == 2)
+            k_symv_ring2<2><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
+                                                                 y_out, partials, done, nst2, nb2, maxr);
+        else if (RT == 8)
+            k_symv_ring2<8><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
+                                                                 y_out, partials, done, nst2, nb2, maxr);
+        else
+            k_symv_ring2<4><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
+                                                                 y_out, partials, done, nst2, nb2, maxr);
+        return;
+    }
+    // item buffers: deep for small items (s copies and epilogues overlap
+    // several items), two for large ones; the rest of shared memory is ring
+    int nb = g_ring_nb > 0 ? g_ring_nb : (maxr <= 256 ? 3 : 2);
+    while (nb > 2 && ring_smem(RT, 4, nb, R, Cr) > budget) --nb;
+    int nst = 2;
+    const int nst_cap = g_ring_nst > 0 ? g_ring_nst : RING_MAX_NST;
+    while (nst < nst_cap && ring_smem(RT, nst + 1, nb, R, Cr) <= budget) ++nst;
+    const size_t smem = ring_smem(RT, nst, nb, R, Cr);
+    if (RT == 1)
+        k_symv_ring<1><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
+                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
+    else if (RT == 2)
+        k_symv_ring<2><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
+                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
+    else
+        k_symv_ring<4><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
+                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
+}
+
+void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
+                        const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
+                        const double* partials, double* z, double* y_out, const int32_t* done) {
+    if (nred <= 0) return;
+    k_symv_reduce<<<nred, 256, 0, st>>>(ops, items, red, red_begin, oidx, partials, z, y_out, done);
+}
+
+}  // namespace ddg
