@@ -575,6 +575,32 @@ static int build_stencil(ddg_ctx* c, const ddg_stencil* S, int64_t n, const int6
     return DDG_OK;
 }
 
+// Contiguous partition of n weighted items over G parts: out[0] = 0,
+// out[G] = n, non-decreasing; part g starts at the item whose weight prefix
+// pre[] (n + 1 entries, pre[0] = 0) is nearest to g/G of the total.
+static void balanced_partition(const double* pre, int n, int G, int32_t* out) {
+    out[0] = 0;
+    int cur = 0;
+    for (int g = 1; g < G; ++g) {
+        const double target = pre[n] * g / G;
+        while (cur < n && pre[cur + 1] <= target) ++cur;
+        int pick = cur;
+        if (cur < n && target - pre[cur] > pre[cur + 1] - target) pick = cur + 1;
+        out[g] = std::max(pick, out[g - 1]);
+    }
+    out[G] = n;
+}
+
+// debug / test export (not part of include/ddg.h): balanced_partition of
+// weights w[0..n) into G parts, out[0..G]
+extern "C" int ddg_debug_partition(const double* w, int n, int G, int32_t* out) {
+    if (!w || !out || n < 0 || G < 1) return DDG_E_ARG;
+    std::vector<double> pre(n + 1, 0.0);
+    for (int i = 0; i < n; ++i) pre[i + 1] = pre[i] + w[i];
+    balanced_partition(pre.data(), n, G, out);
+    return DDG_OK;
+}
+
 // Byte-balanced contiguous partition of items [b, e) over the persistent
 // k_symv_ring CTAs (one per SM): CTA g gets the items whose byte prefix starts
 // nearest to g/G of the total (each item weighted by its bytes plus 8 KB for
@@ -593,17 +619,8 @@ int ring_partition(ddg_ctx* c, int b, int e) {
         pre[i - b + 1] = pre[i - b] + item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8.0 + 8192.0;
     }
     const int off = (int)c->h_ring.size();
-    c->h_ring.push_back(0);
-    int cur = 0;
-    for (int g = 1; g < G; ++g) {
-        const double target = pre.back() * g / G;
-        while (cur < e - b && pre[cur + 1] <= target) ++cur;
-        int pick = cur;
-        if (cur < e - b && target - pre[cur] > pre[cur + 1] - target) pick = cur + 1;
-        pick = std::max(pick, c->h_ring.back());
-        c->h_ring.push_back(pick);
-    }
-    c->h_ring.push_back(e - b);
+    c->h_ring.resize(off + G + 1);
+    balanced_partition(pre.data(), e - b, G, c->h_ring.data() + off);
     // small launches (C1, the upper coarse levels) stay on the per-item
     // kernel: the persistent ring's fixed cost (148 CTAs, ~200 KB shared
     // memory and barrier set-up each) outweighs its streaming advantage

@@ -85,3 +85,24 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "oracle.h" not in txt and "liboracle" not in txt, f
+
+
+@pytest.mark.parametrize("n,G,seed", [(0, 148, 0), (5, 148, 1), (148, 148, 2), (4096, 148, 3), (32768, 148, 4),
+                                      (1000, 7, 5)])
+def test_ring_partition_properties(lib, n, G, seed):
+    """Host logic of the persistent SYMV: the byte-balanced contiguous partition
+    of a launch's work items over the CTAs (setup.cpp balanced_partition).  It
+    covers every item exactly once in order, and no part exceeds its share of
+    the total by more than one item's weight."""
+    import ctypes as C
+    rs = np.random.default_rng(seed)
+    w = rs.uniform(0.5, 1.5, n) * rs.choice([1.0, 4.0], n)
+    out = np.zeros(G + 1, np.int32)
+    f = lib.ddg_debug_partition
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    assert f(w.ctypes.data, n, G, out.ctypes.data) == 0
+    assert out[0] == 0 and out[-1] == n and np.all(np.diff(out) >= 0)
+    if n:
+        loads = np.array([w[out[g]:out[g + 1]].sum() for g in range(G)])
+        assert loads.sum() == pytest.approx(w.sum())
+        assert loads.max() <= w.sum() / G + 2 * w.max() + 1e-9
