@@ -418,7 +418,10 @@ void launch_coarse_dataflow(cudaStream_t st, int nwork, const int32_t* work, con
     if (nwork <= 0) return;
     DFCtx d{fronts, fdf, fwd, bwd, contrib, fS, fB, map, bc, fvec, w, x, partials, state};
     const size_t smem = (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
-    static bool init = false;
+    static bool init_dev[64] = {};   // function attributes are per device
+    int dev_ = 0;
+    cudaGetDevice(&dev_);
+    bool& init = init_dev[dev_ & 63];
     if (!init) {
         cudaFuncSetAttribute(k_coarse_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         init = true;

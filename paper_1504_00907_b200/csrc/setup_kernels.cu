@@ -461,7 +461,10 @@ void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32
 void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* const* mats, const int32_t* nT,
                        const int32_t* nK, const int32_t* ids, int32_t* err) {
     if (nmat <= 0) return;
-    static bool init = false;
+    static bool init_dev[64] = {};   // function attributes are per device
+    int dev_ = 0;
+    cudaGetDevice(&dev_);
+    bool& init = init_dev[dev_ & 63];
     const int smem_p = 9 * TILE_ELEMS * sizeof(double);
     const int smem_g = (TILE * GJB_N + TILE * GJB_BPAD) * sizeof(double);
     if (!init) {
