@@ -130,6 +130,31 @@ def block_partition(dims, bsize):
     return part, int(np.prod(nb)), bc, tuple(nb)
 
 
+def coarse_parts(pr, factor=None, allow_single=False):
+    """Second-level partition for the three-level method:
+    the parts' block coordinates grouped `factor` per axis (the last group
+    along an axis absorbs a remainder), so that H_1/H_0 = H_0/h when factor is
+    the blocks' size H/h (the default: the first axis of meta['bsize']).
+    Returns (part2 int32[nparts], nparts2).  Fewer than 2 groups means the
+    problem is "too small to use the three-level solver" (Table 3's
+    x entries) and raises ValueError unless allow_single."""
+    if factor is None:
+        factor = int(pr.meta.get("bsize", (2,))[0])
+    nb = list(pr.block_dims)
+    ng = [max(1, b // factor) for b in nb]
+    bc = np.asarray(pr.block_coords, np.int64)
+    g = np.zeros(pr.nparts, np.int64)
+    mult = 1
+    for ax in range(len(nb)):
+        g += np.minimum(bc[:, ax] // factor, ng[ax] - 1) * mult
+        mult *= ng[ax]
+    n2 = int(np.prod(ng))
+    if n2 < 2 and not allow_single:
+        raise ValueError(f"too small for three levels: {pr.nparts} parts grouped {factor} per axis "
+                         f"give {n2} second-level part")
+    return g.astype(np.int32), n2
+
+
 def stencil_csr(dims, offsets, coef_fn):
     """CSR of a structured-grid operator.
 

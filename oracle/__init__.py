@@ -43,6 +43,11 @@ def lib():
         L.or_setup.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64,
                                C.POINTER(vp)]
         L.or_setup.restype = C.c_int
+        L.or_setup3.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64, vp, i32,
+                                C.POINTER(vp)]
+        L.or_setup3.restype = C.c_int
+        L.or_child.argtypes = [vp]
+        L.or_child.restype = vp
         for name in ("or_apply_precond", "or_forward_sweep", "or_coarse_correct", "or_spmv"):
             getattr(L, name).argtypes = [vp, vp, vp]
             getattr(L, name).restype = C.c_int
@@ -82,7 +87,10 @@ def _p(a):
 class Oracle:
     """Plain CPU implementation of setup + M r + PCG (see oracle.c)."""
 
-    def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8):
+    def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
+                 part2=None, nparts2=0):
+        """part2 (int32[nparts], second-level part of every part) selects the
+        three-level method (oracle.c or_setup3)."""
         L = lib()
         self._keep = [np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                       np.ascontiguousarray(val, np.float64),
@@ -92,25 +100,46 @@ class Oracle:
         self.n = int(n)
         self.k = int(Ff.shape[1])
         h = C.c_void_p()
-        st = L.or_setup(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
-                        int(overlap), float(rank_tol), C.byref(h))
+        if part2 is None:
+            st = L.or_setup(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
+                            int(overlap), float(rank_tol), C.byref(h))
+        else:
+            p2 = np.ascontiguousarray(part2, np.int32)
+            st = L.or_setup3(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
+                             int(overlap), float(rank_tol), _p(p2), int(nparts2), C.byref(h))
         if st != 0:
             raise OracleError(st, L.or_last_error().decode())
         self._h = h
+        self._owner = None
         self._keep = None
+        self._read_info()
+
+    def _read_info(self):
         info = np.zeros(10, np.int64)
-        L.or_info(self._h, _p(info))
-        (self.n, self.nc, self.nparts, self.ncolours, self.m_min, self.m_max, _, self.dropped,
-         _, _) = [int(x) for x in info]
+        lib().or_info(self._h, _p(info))
+        (self.n, self.nc, self.nparts, self.ncolours, self.m_min, self.m_max, self.k, self.dropped,
+         self.levels, self.nc2) = [int(x) for x in info]
+
+    def child(self):
+        """The second-level two-level method on A_0 (three levels only), a
+        borrowed view that keeps its parent alive."""
+        h = lib().or_child(self._h)
+        if not h:
+            return None
+        o = Oracle.__new__(Oracle)
+        o._h = C.c_void_p(h)
+        o._owner = self
+        o._read_info()
+        return o
 
     @classmethod
-    def from_problem(cls, pr, overlap=None, rank_tol=1e-8):
+    def from_problem(cls, pr, overlap=None, rank_tol=1e-8, part2=None, nparts2=0):
         return cls(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts,
-                   pr.overlap if overlap is None else overlap, rank_tol)
+                   pr.overlap if overlap is None else overlap, rank_tol, part2, nparts2)
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and getattr(self, "_owner", None) is None:
             lib().or_destroy(h)
             self._h = None
 

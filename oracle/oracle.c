@@ -18,6 +18,8 @@
  *     6. A_0 = R_0 A R_0^T  (A_c = P^T A P)
  *     7. Cholesky of A_0 in envelope storage
  *   apply (or_apply_precond)
+ *   three levels (or_setup3): the two-level method again on
+ *     A_0 with F_0 = R_0 F and a partition of the parts
  *   pcg (or_pcg)
  *
  * Parity status: every function here is pinned by tests/test_oracle_*.py
@@ -75,6 +77,9 @@ struct or_ctx {
     int64_t* eptr;
     double* ea;  /* A_0 (unfactored copy) */
     double* el;  /* its Cholesky factor */
+    /* three-level method: the two-level method applied to
+       A_0 with F_0 = R_0 F; when set, it replaces the exact coarse solve */
+    struct or_ctx* child;
 };
 
 #define ALLOC(p, cnt)                                                        \
@@ -608,8 +613,105 @@ void or_destroy(or_ctx* c) {
     free(c->loff); free(c->L);
     free(c->cptr); free(c->qoff); free(c->Q);
     free(c->efirst); free(c->eptr); free(c->ea); free(c->el);
+    or_destroy(c->child);
     free(c);
 }
+
+/* ---------------------------------------------------------------------------
+ * Three-level method: "taking the two-level algorithm and
+ * applying it again to the coarse matrix A_0 ... a coarsened version of the
+ * generating vectors, which are simply F_0 = R_0 F".
+ *   - A_0 as a sparse matrix: row (I,i) holds every (J,j) with J = I or J
+ *     adjacent to I in the graph of A (reading R20: the structural pattern of
+ *     R_0 A R_0^T, explicit zeros kept, so that the overlap and colouring of
+ *     the second level follow the graph of A_0 and not cancellation).
+ *   - F_0[(I,i), l] = Q_I[:, i]^T F[Omega_I, l]   (R_0 = blockdiag(Q_I^T)).
+ *   - second-level partition: coarse unknown (I,i) belongs to part
+ *     part2[I] (reading R21: whole fine parts are grouped, which keeps
+ *     h/H_0 = H_0/H_1 when part2 groups (H/h)^d neighbouring parts).
+ *   - the same Delta and rank tolerance at both levels.
+ * ------------------------------------------------------------------------- */
+int or_setup3(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+              const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+              double rank_tol, const int32_t* part2, int32_t nparts2, or_ctx** out) {
+    *out = NULL;
+    if (!part2 || nparts2 < 1) return fail(OR_E_ARG, "three levels need a second-level partition");
+    for (int32_t I = 0; I < nparts; I++)
+        if (part2[I] < 0 || part2[I] >= nparts2)
+            return fail(OR_E_PART, "second-level part %d of part %d out of range [0,%d)", part2[I], I, nparts2);
+    or_ctx* c;
+    int st = or_setup(n, row_ptr, col, val, F, k, part, nparts, overlap, rank_tol, &c);
+    if (st) return st;
+    int64_t nc = c->nc;
+    /* part adjacency in the graph of A */
+    char* adj = calloc((size_t)nparts * (size_t)nparts, 1);
+    int64_t* rp0 = calloc((size_t)nc + 1, sizeof(int64_t));
+    double* F0 = calloc((size_t)(nc > 0 ? nc : 1) * (size_t)k, sizeof(double));
+    int32_t* p0 = calloc((size_t)(nc > 0 ? nc : 1), sizeof(int32_t));
+    if (!adj || !rp0 || !F0 || !p0) {
+        free(adj); free(rp0); free(F0); free(p0); or_destroy(c);
+        return fail(OR_E_OOM, "oom");
+    }
+    for (int64_t v = 0; v < n; v++)
+        for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; e++) {
+            int32_t I = part[v], J = part[col[e]];
+            adj[(size_t)I * nparts + J] = adj[(size_t)J * nparts + I] = 1;
+        }
+    for (int32_t I = 0; I < nparts; I++) adj[(size_t)I * nparts + I] = 1;
+    for (int32_t I = 0; I < nparts; I++) {
+        int64_t w = 0;
+        for (int32_t J = 0; J < nparts; J++)
+            if (adj[(size_t)I * nparts + J]) w += c->cptr[J + 1] - c->cptr[J];
+        for (int32_t i = c->cptr[I]; i < c->cptr[I + 1]; i++) rp0[i + 1] = w;
+    }
+    for (int64_t i = 0; i < nc; i++) rp0[i + 1] += rp0[i];
+    int32_t* ci0 = malloc((size_t)(rp0[nc] > 0 ? rp0[nc] : 1) * sizeof(int32_t));
+    double* va0 = malloc((size_t)(rp0[nc] > 0 ? rp0[nc] : 1) * sizeof(double));
+    if (!ci0 || !va0) {
+        free(adj); free(rp0); free(F0); free(p0); free(ci0); free(va0); or_destroy(c);
+        return fail(OR_E_OOM, "oom");
+    }
+    for (int32_t I = 0; I < nparts; I++)
+        for (int32_t i = c->cptr[I]; i < c->cptr[I + 1]; i++) {
+            int64_t e = rp0[i];
+            for (int32_t J = 0; J < nparts; J++) {
+                if (!adj[(size_t)I * nparts + J]) continue;
+                for (int32_t j = c->cptr[J]; j < c->cptr[J + 1]; j++) {
+                    /* A_0 is kept lower in the envelope: (max, min) */
+                    int64_t hi = i > j ? i : j, lo = i > j ? j : i;
+                    ci0[e] = j;
+                    va0[e++] = c->ea[c->eptr[hi] + (lo - c->efirst[hi])];
+                }
+            }
+            p0[i] = part2[I];
+        }
+    /* F_0 = R_0 F (column-major nc x k) */
+    for (int32_t I = 0; I < nparts; I++) {
+        int64_t mI = c->bptr[I + 1] - c->bptr[I];
+        const int32_t* rows = c->bidx + c->bptr[I];
+        for (int32_t i = 0; i < c->cptr[I + 1] - c->cptr[I]; i++) {
+            const double* q = c->Q + c->qoff[I] + (int64_t)i * mI;
+            for (int l = 0; l < k; l++) {
+                double s = 0.0;
+                for (int64_t a = 0; a < mI; a++) s += q[a] * F[(int64_t)l * n + rows[a]];
+                F0[(int64_t)l * nc + c->cptr[I] + i] = s;
+            }
+        }
+    }
+    free(adj);
+    if (nc < 1) {
+        free(rp0); free(F0); free(p0); free(ci0); free(va0); or_destroy(c);
+        return fail(OR_E_ARG, "empty coarse space");
+    }
+    /* every second-level part must own coarse unknowns */
+    st = or_setup(nc, rp0, ci0, va0, F0, k, p0, nparts2, overlap, rank_tol, &c->child);
+    free(rp0); free(F0); free(p0); free(ci0); free(va0);
+    if (st) { or_destroy(c); return st; }
+    *out = c;
+    return OR_OK;
+}
+
+or_ctx* or_child(or_ctx* c) { return c->child; }
 
 /* ---------------------------------------------------------------------------
  * Subdomain update:  u <- u + R~_i^T A_i^{-1} R~_i (f - A u),
@@ -658,7 +760,16 @@ static void coarse_add(or_ctx* c, const double* res, double* z) {
             b[c->cptr[I] + i] = s;
         }
     }
-    coarse_solve(c, b);
+    if (c->child) {
+        /* three levels: one V-cycle of the two-level method on A_0 stands in
+           for A_0^{-1} */
+        double* y = malloc((size_t)(c->nc > 0 ? c->nc : 1) * sizeof(double));
+        or_apply_precond(c->child, b, y);
+        memcpy(b, y, (size_t)c->nc * sizeof(double));
+        free(y);
+    } else {
+        coarse_solve(c, b);
+    }
     for (int32_t I = 0; I < c->nparts; I++) {
         int64_t mI = c->bptr[I + 1] - c->bptr[I];
         const int32_t* rows = c->bidx + c->bptr[I];
@@ -770,7 +881,8 @@ void or_info(or_ctx* c, int64_t* info) {
         if (m > mmax) mmax = m;
     }
     info[0] = c->n; info[1] = c->nc; info[2] = c->nparts; info[3] = c->ncolours;
-    info[4] = mmin; info[5] = mmax; info[6] = c->k; info[7] = c->dropped; info[8] = 0; info[9] = 0;
+    info[4] = mmin; info[5] = mmax; info[6] = c->k; info[7] = c->dropped;
+    info[8] = c->child ? 3 : 2; info[9] = c->child ? c->child->nc : 0;
 }
 double or_min_rank_ratio(or_ctx* c) { return c->min_ratio; }
 int or_get_colours(or_ctx* c, int32_t* colour) {

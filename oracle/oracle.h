@@ -28,6 +28,13 @@ typedef struct or_ctx or_ctx;
 int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
              const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
              double rank_tol, or_ctx** out);
+/* three levels: the two-level method applied again to A_0,
+   with F_0 = R_0 F and second-level part part2[I] for every fine part I */
+int or_setup3(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+              const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+              double rank_tol, const int32_t* part2, int32_t nparts2, or_ctx** out);
+/* the second-level context (borrowed; NULL for two levels) */
+or_ctx* or_child(or_ctx* c);
 int or_apply_precond(or_ctx* c, const double* r, double* z);
 int or_forward_sweep(or_ctx* c, const double* r, double* z);
 int or_coarse_correct(or_ctx* c, const double* r, double* z);
@@ -37,7 +44,7 @@ int or_pcg(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode,
 /* the same, recording alpha_k (k < iters) and beta_k (k < iters - 1 or iters) */
 int or_pcg_ab(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mode,
               double* u, int* iters, double* hist, int* converged, double* alphas, double* betas);
-/* info[0..9] = n, n_c, nparts, ncolours, m_min, m_max, k, dropped, (unused), (unused) */
+/* info[0..9] = n, n_c, nparts, ncolours, m_min, m_max, k, dropped, levels, n_c of level 2 */
 void or_info(or_ctx* c, int64_t* info);
 double or_min_rank_ratio(or_ctx* c);
 int or_get_colours(or_ctx* c, int32_t* colour);
