@@ -174,7 +174,11 @@ def bench_ddg(args):
         dist.broadcast_object_list(obj, src=0)
         comm = ddg.Comm(rank, world, obj[0], local)
     t0 = time.time()
-    s = Solver.from_problem(pr, device=local, stream=stream.cuda_stream, comm=comm)
+    kw = {}
+    if args.levels == 3:   # three-level method: second level on A_c
+        p2, n2, bc2 = P.coarse_parts(pr, args.factor, coords=True)
+        kw = dict(part2=p2, nparts2=n2, block_coords2=bc2)
+    s = Solver.from_problem(pr, device=local, stream=stream.cuda_stream, comm=comm, **kw)
     t_setup = time.time() - t0
     sizes = s.subdomain_sizes()
     f_d = torch.from_numpy(pr.f).cuda()
@@ -254,10 +258,14 @@ def bench_ddg(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "desc": P.CONFIG_TEXT[args.config], "n": pr.n,
+        "config": {"workload": args.config + ("-3level" if args.levels == 3 else ""), "desc": P.CONFIG_TEXT[args.config], "n": pr.n,
                    "iterations": it, "rtol": args.rtol, "n_c": int(s.info.n_c),
                    "nparts": int(s.info.nparts), "colours": int(s.info.ncolours),
-                   "coarse": "dense packed inverse" if s.info.coarse_variant == 1 else "sparse nested dissection", "parallelism": f"subdomain-sharded x{world} (NCCL halos + allreduce, replicated coarse)" if world > 1 else "1gpu",
+                   "coarse": {1: "dense packed inverse", 2: "sparse nested dissection",
+                              3: "three levels: two-level DDG on A_c (second level %s, n_c2=%d, %d parts)" % (
+                                  "dense" if s.info.coarse_variant2 == 1 else "sparse", s.info.n_c2,
+                                  s.info.nparts2)}[s.info.coarse_variant],
+                   "levels": int(s.info.levels), "parallelism": f"subdomain-sharded x{world} (NCCL halos + allreduce, replicated coarse)" if world > 1 else "1gpu",
                    "l2": "inputs larger than L2 (local inverses %.1f GB)" % (s.info.local_factor_bytes / 1e9),
                    "time_to_rtol_ms": ms_step, "t_setup_s": round(t_setup, 2),
                    "cond_est_lanczos": round(float(rep.cond_est), 3),
@@ -302,6 +310,9 @@ def main():
     ap.add_argument("--impl", default="ddg", choices=["ddg", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--rtol", type=float, default=1e-8)
+    ap.add_argument("--levels", type=int, default=2, choices=[2, 3])
+    ap.add_argument("--factor", type=int, default=None,
+                    help="three levels: parts grouped per axis into a second-level part (default H/h)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -130,12 +130,13 @@ def block_partition(dims, bsize):
     return part, int(np.prod(nb)), bc, tuple(nb)
 
 
-def coarse_parts(pr, factor=None, allow_single=False):
+def coarse_parts(pr, factor=None, allow_single=False, coords=False):
     """Second-level partition for the three-level method:
     the parts' block coordinates grouped `factor` per axis (the last group
     along an axis absorbs a remainder), so that H_1/H_0 = H_0/h when factor is
     the blocks' size H/h (the default: the first axis of meta['bsize']).
-    Returns (part2 int32[nparts], nparts2).  Fewer than 2 groups means the
+    Returns (part2 int32[nparts], nparts2) or, with coords=True, also the
+    second-level block coordinates int32[nparts2, ndim].  Fewer than 2 groups means the
     problem is "too small to use the three-level solver" (Table 3's
     x entries) and raises ValueError unless allow_single."""
     if factor is None:
@@ -152,6 +153,9 @@ def coarse_parts(pr, factor=None, allow_single=False):
     if n2 < 2 and not allow_single:
         raise ValueError(f"too small for three levels: {pr.nparts} parts grouped {factor} per axis "
                          f"give {n2} second-level part")
+    if coords:
+        bc2 = np.array(list(itertools.product(*[range(b) for b in reversed(ng)])), dtype=np.int32)
+        return g.astype(np.int32), n2, bc2[:, ::-1].copy()
     return g.astype(np.int32), n2
 
 

@@ -103,6 +103,20 @@ typedef struct {
                              (host, borrowed): geometric nested dissection of the coarse graph;
                              NULL: BFS level-set bisection                                       */
     const ddg_stencil* stencil;  /* optional matrix-free description of A (above), or NULL       */
+    /* Three levels: when part2 is non-NULL the coarse solve
+       A_c^{-1} is replaced by one application of the two-level method built
+       on A_c (same Delta and rank_tol), with coarsened generating vectors
+       F_0 = R_0 F (the coarse coefficients of F) and second-level parts:
+       coarse unknown (I, i) belongs to part2[I].  part2: nparts int32 in
+       [0, nparts2), every second-level part non-empty, nparts2 >= 2
+       (DDG_E_PART "too small for three levels" otherwise); host, borrowed
+       for the duration of ddg_setup.  block_coords2: optional nparts2 x
+       block_ndim coordinates of the second-level parts.  coarse_variant then
+       selects the second level's coarse solve (0 auto, 1 dense, 2 sparse).
+       Single GPU only. */
+    const int32_t* part2;
+    int32_t nparts2;
+    const int32_t* block_coords2;
 } ddg_opts;
 
 typedef struct {
@@ -129,11 +143,18 @@ typedef struct {
     double min_rank_ratio;          /* min over parts and kept j of |R_jj| / max_j ||F_I e_j||  */
     int64_t local_factor_bytes;     /* bytes of the stored local operators (device)            */
     int64_t coarse_factor_bytes;    /* bytes of the stored coarse operator (device)            */
-    int32_t coarse_variant;         /* 1 dense packed inverse, 2 sparse supernodal             */
-    int32_t pad;
+    int32_t coarse_variant;         /* 1 dense packed inverse, 2 sparse supernodal, 3 three
+                                       levels (the second level's own variant in coarse_variant2) */
+    int32_t levels;                 /* 2 or 3                                                   */
     int64_t coarse_solve_bytes;     /* operator bytes one coarse solve must read: the packed
                                        inverse once (dense), or 2|G| + |H| over the fronts
-                                       (sparse: G read forward and backward, H backward)       */
+                                       (sparse: G read forward and backward, H backward);
+                                       three levels: the second level's local operators twice
+                                       (two sweeps) plus its own coarse solve bytes            */
+    int64_t n_c2;                   /* three levels: coarse unknowns of the second level       */
+    int32_t nparts2, ncolours2;     /* three levels: second-level parts and colours            */
+    int32_t coarse_variant2;        /* three levels: the second level's coarse variant (1, 2)  */
+    int32_t pad2;
 } ddg_info;
 
 /* Fills *o with the defaults listed above. */

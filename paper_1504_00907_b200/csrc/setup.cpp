@@ -161,6 +161,7 @@ int64_t sparse_coarse_solve_bytes(ddg_ctx* c);
 
 static void free_ctx(ddg_ctx* c) {
     if (!c) return;
+    if (c->child) free_ctx(c->child);   // borrows this context's stream
     if (c->device >= 0) cudaSetDevice(c->device);
     if (c->ge_iter) cudaGraphExecDestroy(c->ge_iter);
     if (c->g_iter) cudaGraphDestroy(c->g_iter);
@@ -168,7 +169,7 @@ static void free_ctx(ddg_ctx* c) {
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
                     c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
-                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab};
+                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab, c->d_bc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -844,6 +845,87 @@ static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::
     return DDG_OK;
 }
 
+// Three levels: "taking the two-level algorithm and
+// applying it again to the coarse matrix A_0", with "F_0 = R_0 F".  The
+// second level is an ordinary two-level context on A_c (host CSR built from
+// the Galerkin triplets, structural pattern = part adjacency, reading R20),
+// F_0 = blockdiag(Q_I^T) F, coarse unknown (I,i) in part part2[I] (R21), the
+// same Delta and rank tolerance, on this context's device and stream.
+static int build_child(ddg_ctx* c, const double* F, const std::vector<int32_t>& er,
+                       const std::vector<int32_t>& ec, const std::vector<double>& ev) {
+    const int64_t nc = c->nc;
+    const int k = c->k;
+    const int32_t* part2 = c->opts.part2;
+    const int np2 = c->opts.nparts2;
+    // CSR of A_c, both triangles, columns increasing
+    std::vector<int64_t> rp(nc + 1, 0);
+    for (size_t e = 0; e < er.size(); ++e) {
+        rp[er[e] + 1]++;
+        if (er[e] != ec[e]) rp[ec[e] + 1]++;
+    }
+    for (int64_t i = 0; i < nc; ++i) rp[i + 1] += rp[i];
+    if (rp[nc] >= (int64_t)INT32_MAX) return set_err(DDG_E_ARG, "A_c has too many entries for three levels");
+    std::vector<int32_t> col(rp[nc]);
+    std::vector<double> val(rp[nc]);
+    {
+        std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+        for (size_t e = 0; e < er.size(); ++e) {
+            col[fill[er[e]]] = ec[e];
+            val[fill[er[e]]++] = ev[e];
+            if (er[e] != ec[e]) {
+                col[fill[ec[e]]] = er[e];
+                val[fill[ec[e]]++] = ev[e];
+            }
+        }
+        parallel_for(nc, [&](int64_t b, int64_t e, int) {
+            std::vector<std::pair<int32_t, double>> row;
+            for (int64_t i = b; i < e; ++i) {
+                row.clear();
+                for (int64_t x = rp[i]; x < rp[i + 1]; ++x) row.push_back({col[x], val[x]});
+                std::sort(row.begin(), row.end(),
+                          [](const std::pair<int32_t, double>& a, const std::pair<int32_t, double>& b2) {
+                              return a.first < b2.first;
+                          });
+                for (int64_t x = rp[i]; x < rp[i + 1]; ++x) {
+                    col[x] = row[x - rp[i]].first;
+                    val[x] = row[x - rp[i]].second;
+                }
+            }
+        });
+    }
+    // F_0 = R_0 F (column-major nc x k) and the second-level partition
+    std::vector<double> F0((size_t)nc * k);
+    std::vector<int32_t> p0(nc);
+    parallel_for(c->nparts, [&](int64_t b, int64_t e, int) {
+        for (int64_t I = b; I < e; ++I) {
+            const int64_t mI = c->bptr[I + 1] - c->bptr[I];
+            const int32_t* rows = c->bidx.data() + c->bptr[I];
+            for (int i = 0; i < c->cptr[I + 1] - c->cptr[I]; ++i) {
+                const double* q = c->Q.data() + c->qoff[I] + (int64_t)i * mI;
+                for (int l = 0; l < k; ++l) {
+                    double sum = 0;
+                    for (int64_t a = 0; a < mI; ++a) sum += q[a] * F[(int64_t)l * c->n + rows[a]];
+                    F0[(size_t)l * nc + c->cptr[I] + i] = sum;
+                }
+                p0[c->cptr[I] + i] = part2[I];
+            }
+        }
+    });
+    ddg_opts o = c->opts;
+    o.stream = c->stream;
+    o.comm = nullptr;
+    o.stencil = nullptr;
+    o.part2 = nullptr;
+    o.nparts2 = 0;
+    o.block_coords = c->opts.block_coords2;
+    o.block_ndim = c->opts.block_coords2 ? c->opts.block_ndim : 0;
+    o.block_coords2 = nullptr;
+    o.coarse_variant = c->opts.coarse_variant;   // selects the last level's coarse solve
+    int st = ddg_setup(nc, rp.data(), col.data(), val.data(), F0.data(), k, p0.data(), np2, &o, &c->child);
+    if (st) return st;   // the child's message stands
+    return DDG_OK;
+}
+
 template <typename T>
 static int upload_s(cudaStream_t s, T** d, const std::vector<T>& h) {
     int st = dalloc(d, h.size());
@@ -966,6 +1048,27 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     if (const char* e = getenv("DDG_RING_MIN_MB")) c->ring_min_bytes = atof(e) * 1e6;
     c->coarse_variant = c->opts.coarse_variant;
     if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
+    if (c->opts.part2) {   // three levels
+        if (c->dist) { free_ctx(c); return set_err(DDG_E_ARG, "three levels: single GPU only"); }
+        if (c->opts.nparts2 < 2) {
+            int np2 = c->opts.nparts2;
+            free_ctx(c);
+            return set_err(DDG_E_PART, "too small for three levels: %d second-level part(s)", np2);
+        }
+        std::vector<char> seen(c->opts.nparts2, 0);
+        for (int I = 0; I < nparts; ++I) {
+            const int J = c->opts.part2[I];
+            if (J < 0 || J >= c->opts.nparts2) {
+                free_ctx(c);
+                return set_err(DDG_E_PART, "second-level part %d of part %d outside [0,%d)", J, I,
+                               c->opts.nparts2);
+            }
+            if (c->cptr[I + 1] > c->cptr[I]) seen[J] = 1;
+        }
+        for (int J = 0; J < c->opts.nparts2; ++J)
+            if (!seen[J]) { free_ctx(c); return set_err(DDG_E_PART, "second-level part %d is empty", J); }
+        c->coarse_variant = 3;
+    }
     if (c->coarse_variant == 1 && c->nc > 131072) {
         int64_t nc = c->nc;
         free_ctx(c);
@@ -1025,7 +1128,8 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         (st = dalloc(&c->d_u, n)) || (st = dalloc(&c->d_x, n)) || (st = dalloc(&c->d_sc, 1)) ||
         (st = dalloc(&c->d_redbuf, RED_BLOCKS)) || (st = dalloc(&c->d_ticket, 1)) ||
         (st = dalloc(&c->d_zero, 1)) || (st = dalloc(&c->d_tickets, c->ops.size())) ||
-        (st = upload(&c->d_ring, c->h_ring))) {
+        (st = upload(&c->d_ring, c->h_ring)) ||
+        (c->coarse_variant == 3 && (st = dalloc(&c->d_bc, std::max<int64_t>(1, c->nc))))) {
         free_ctx(c);
         return st;
     }
@@ -1093,10 +1197,18 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     tick("local inverses (GPU)");
     if (c->coarse_variant == 1) {
         if ((st = invert_coarse(c, er, ec, ev))) { free_ctx(c); return st; }
-    } else {
+        tick("coarse inverse (GPU)");
+    } else if (c->coarse_variant == 2) {
         if ((st = sparse_coarse_numeric(c))) { free_ctx(c); return st; }
+        tick("coarse inverse (GPU)");
+    } else {
+        if ((st = build_child(c, F, er, ec, ev))) {
+            std::string msg = g_last_error;
+            free_ctx(c);
+            return set_err(st, "second level: %s", msg.c_str());
+        }
+        tick("second level (two-level setup on A_c)");
     }
-    tick("coarse inverse (GPU)");
     c->local_bytes = 0;
     for (int q = 0; q < (int)c->op_sub.size(); ++q) {
         const OpDesc& op = c->ops[q];
@@ -1105,7 +1217,11 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
             c->local_bytes += item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8;
         }
     }
-    c->coarse_bytes = c->coarse_variant == 1 ? (c->tiles_doubles * 8) - c->local_bytes : sparse_coarse_bytes(c);
+    c->coarse_bytes = c->coarse_variant == 1   ? (c->tiles_doubles * 8) - c->local_bytes
+                      : c->coarse_variant == 2 ? sparse_coarse_bytes(c)
+                                               : c->child->local_bytes + c->child->coarse_bytes;
+    c->opts.part2 = nullptr;   // borrowed for the duration of ddg_setup only
+    c->opts.block_coords2 = nullptr;
     c->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = c;
     return DDG_OK;
@@ -1184,15 +1300,24 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
     halo(c, c->h_z[cc], z);
 }
 
+static void enqueue_precond(ddg_ctx* c, const double* r, double* z, const int32_t* done);
+
 static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* done) {
-    double* bc = c->coarse_variant == 2 ? sparse_coarse_rhs(c) : c->d_s + c->ops[c->coarse_op].s_off;
+    double* bc = c->coarse_variant == 2 ? sparse_coarse_rhs(c)
+                 : c->coarse_variant == 3 ? c->d_bc
+                                          : c->d_s + c->ops[c->coarse_op].s_off;
     const bool multi = c->dist && c->nranks > 1;
     prof(c, PC_COARSE, 0, [&] {
         if (multi) cudaMemsetAsync(bc, 0, c->nc * sizeof(double), c->stream);
         launch_coarse_restrict(c->stream, c->n_restrict, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
                                c->A, r, z, bc, c->maxmI, done, c->d_restrict_parts);
         if (multi) comm_check(c, comm_allreduce_sum(c->comm, bc, bc, c->nc, c->stream));
-        if (c->coarse_variant == 2) {
+        if (c->coarse_variant == 3) {
+            // three levels: y_c = M_2 b_c, one V-cycle of the two-level method on A_c
+            const int64_t l0 = c->child->launches;
+            enqueue_precond(c->child, bc, c->d_yc, done);
+            c->launches += c->child->launches - l0;
+        } else if (c->coarse_variant == 2) {
             c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
         } else if (ring_ok(c, c->coarse_ring_off)) {
             int mr, mc;
@@ -1513,7 +1638,18 @@ extern "C" int ddg_get_info(ddg_ctx* c, ddg_info* info) {
     info->local_factor_bytes = c->local_bytes;
     info->coarse_factor_bytes = c->coarse_bytes;
     info->coarse_variant = c->coarse_variant;
-    info->coarse_solve_bytes = c->coarse_variant == 1 ? c->coarse_bytes : sparse_coarse_solve_bytes(c);
+    info->levels = c->child ? 3 : 2;
+    if (c->child) {
+        ddg_info ci;
+        ddg_get_info(c->child, &ci);
+        info->n_c2 = ci.n_c;
+        info->nparts2 = ci.nparts;
+        info->ncolours2 = ci.ncolours;
+        info->coarse_variant2 = ci.coarse_variant;
+        info->coarse_solve_bytes = 2 * ci.local_factor_bytes + ci.coarse_solve_bytes;
+    } else {
+        info->coarse_solve_bytes = c->coarse_variant == 1 ? c->coarse_bytes : sparse_coarse_solve_bytes(c);
+    }
     return DDG_OK;
 }
 

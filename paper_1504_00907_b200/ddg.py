@@ -47,7 +47,8 @@ class ddg_opts(C.Structure):
                 ("use_graphs", C.c_int), ("verbose", C.c_int), ("coarse_variant", C.c_int),
                 ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("comm", C.c_void_p),
                 ("small_kernel", C.c_int), ("block_coords", C.c_void_p),
-                ("stencil", C.POINTER(ddg_stencil))]
+                ("stencil", C.POINTER(ddg_stencil)), ("part2", C.c_void_p),
+                ("nparts2", C.c_int32), ("block_coords2", C.c_void_p)]
 
 
 class ddg_report(C.Structure):
@@ -61,8 +62,9 @@ class ddg_info(C.Structure):
                 ("ncolours", C.c_int32), ("m_min", C.c_int32), ("m_max", C.c_int32),
                 ("k", C.c_int32), ("dropped", C.c_int32), ("min_rank_ratio", C.c_double),
                 ("local_factor_bytes", C.c_int64), ("coarse_factor_bytes", C.c_int64),
-                ("coarse_variant", C.c_int32), ("pad", C.c_int32),
-                ("coarse_solve_bytes", C.c_int64)]
+                ("coarse_variant", C.c_int32), ("levels", C.c_int32),
+                ("coarse_solve_bytes", C.c_int64), ("n_c2", C.c_int64), ("nparts2", C.c_int32),
+                ("ncolours2", C.c_int32), ("coarse_variant2", C.c_int32), ("pad2", C.c_int32)]
 
 
 class ddg_kstats(C.Structure):
@@ -155,7 +157,9 @@ class Solver:
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
                  stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
                  verbose=False, coarse_variant=0, block_coords=None, comm=None, fuse_gather=None,
-                 small_kernel=None, stencil=None):
+                 small_kernel=None, stencil=None, part2=None, nparts2=0, block_coords2=None):
+        """part2 (int32[nparts]: second-level part of every part) selects the
+        three-level method (include/ddg.h ddg_opts.part2)."""
         L = load()
         o = default_opts()
         o.overlap, o.rank_tol, o.stop_mode, o.max_iter = overlap, rank_tol, stop_mode, max_iter
@@ -176,6 +180,15 @@ class Solver:
             o.block_ndim = int(bc.shape[1])
             o.block_coords = bc.ctypes.data
         keep = []
+        if part2 is not None:
+            p2 = np.ascontiguousarray(part2, np.int32)
+            keep.append(p2)
+            o.part2 = p2.ctypes.data
+            o.nparts2 = int(nparts2)
+            if block_coords2 is not None:
+                bc2 = np.ascontiguousarray(block_coords2, np.int32)
+                keep.append(bc2)
+                o.block_coords2 = bc2.ctypes.data
         if stencil is not None:
             # {"kind": "const", "dims": (nx, ny, nz), "offsets": [(dx, dy, dz), ...], "coef": [...]}
             # {"kind": "face7", "dims": (nx, ny, nz), "coef": float64[4 n] (diag|cx|cy|cz)}
