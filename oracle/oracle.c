@@ -622,12 +622,12 @@ void or_destroy(or_ctx* c) {
  * applying it again to the coarse matrix A_0 ... a coarsened version of the
  * generating vectors, which are simply F_0 = R_0 F".
  *   - A_0 as a sparse matrix: row (I,i) holds every (J,j) with J = I or J
- *     adjacent to I in the graph of A (reading R20: the structural pattern of
+ *     adjacent to I in the graph of A (reading R19: the structural pattern of
  *     R_0 A R_0^T, explicit zeros kept, so that the overlap and colouring of
  *     the second level follow the graph of A_0 and not cancellation).
  *   - F_0[(I,i), l] = Q_I[:, i]^T F[Omega_I, l]   (R_0 = blockdiag(Q_I^T)).
  *   - second-level partition: coarse unknown (I,i) belongs to part
- *     part2[I] (reading R21: whole fine parts are grouped, which keeps
+ *     part2[I] (reading R20: whole fine parts are grouped, which keeps
  *     h/H_0 = H_0/H_1 when part2 groups (H/h)^d neighbouring parts).
  *   - the same Delta and rank tolerance at both levels.
  * ------------------------------------------------------------------------- */

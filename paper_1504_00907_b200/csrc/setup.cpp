@@ -848,8 +848,8 @@ static int invert_coarse(ddg_ctx* c, const std::vector<int32_t>& er, const std::
 // Three levels: "taking the two-level algorithm and
 // applying it again to the coarse matrix A_0", with "F_0 = R_0 F".  The
 // second level is an ordinary two-level context on A_c (host CSR built from
-// the Galerkin triplets, structural pattern = part adjacency, reading R20),
-// F_0 = blockdiag(Q_I^T) F, coarse unknown (I,i) in part part2[I] (R21), the
+// the Galerkin triplets, structural pattern = part adjacency, reading R19),
+// F_0 = blockdiag(Q_I^T) F, coarse unknown (I,i) in part part2[I] (R20), the
 // same Delta and rank tolerance, on this context's device and stream.
 static int build_child(ddg_ctx* c, const double* F, const std::vector<int32_t>& er,
                        const std::vector<int32_t>& ec, const std::vector<double>& ev) {

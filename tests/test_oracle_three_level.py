@@ -16,7 +16,7 @@ Each test pins it to something other than itself:
 - the spectrum of M_3 A lies in (0, 1] (each factor of I - M A is an
   A-norm contraction);
 - the second level's matrix is dense P^T A P and its overlap is the graph
-  distance in the structural pattern of A_0 (reading R20).
+  distance in the structural pattern of A_0 (reading R19).
 """
 from __future__ import annotations
 
@@ -98,7 +98,7 @@ def test_second_level_matrix_and_overlap():
         rng = np.random.default_rng(3)
         x = rng.standard_normal(o3.nc)
         assert np.allclose(ch.spmv(x), A0 @ x, rtol=0, atol=1e-12 * np.abs(A0).sum(1).max() * np.abs(x).max())
-        # structural pattern of A_0: parts I, J adjacent in the graph of A (R20)
+        # structural pattern of A_0: parts I, J adjacent in the graph of A (R19)
         cptr = o3.coarse_offsets()
         adj = np.zeros((pr.nparts, pr.nparts), bool)
         rows = np.repeat(np.arange(pr.n), np.diff(pr.row_ptr))
