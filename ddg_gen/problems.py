@@ -130,7 +130,7 @@ def block_partition(dims, bsize):
     return part, int(np.prod(nb)), bc, tuple(nb)
 
 
-def coarse_parts(pr, factor=None, allow_single=False, coords=False):
+def coarse_parts(pr, factor=None, allow_single=False, coords=False, nearest=False):
     """Second-level partition for the three-level method:
     the parts' block coordinates grouped `factor` per axis (the last group
     along an axis absorbs a remainder), so that H_1/H_0 = H_0/h when factor is
@@ -138,16 +138,24 @@ def coarse_parts(pr, factor=None, allow_single=False, coords=False):
     Returns (part2 int32[nparts], nparts2) or, with coords=True, also the
     second-level block coordinates int32[nparts2, ndim].  Fewer than 2 groups means the
     problem is "too small to use the three-level solver" (Table 3's
-    x entries) and raises ValueError unless allow_single."""
+    x entries) and raises ValueError unless allow_single.  nearest=True
+    instead splits each axis's blocks evenly into round(blocks / factor)
+    groups (the paper's grids are not multiples of (H/h)^2 blocks)."""
     if factor is None:
         factor = int(pr.meta.get("bsize", (2,))[0])
     nb = list(pr.block_dims)
-    ng = [max(1, b // factor) for b in nb]
+    if nearest:
+        ng = [max(1, int(np.floor(b / factor + 0.5))) for b in nb]
+    else:
+        ng = [max(1, b // factor) for b in nb]
     bc = np.asarray(pr.block_coords, np.int64)
     g = np.zeros(pr.nparts, np.int64)
     mult = 1
     for ax in range(len(nb)):
-        g += np.minimum(bc[:, ax] // factor, ng[ax] - 1) * mult
+        if nearest:
+            g += (bc[:, ax] * ng[ax] // nb[ax]) * mult
+        else:
+            g += np.minimum(bc[:, ax] // factor, ng[ax] - 1) * mult
         mult *= ng[ax]
     n2 = int(np.prod(ng))
     if n2 < 2 and not allow_single:
@@ -229,6 +237,32 @@ def poisson3d(N=128, b=8, p=2, seed=1002, overlap=1):
     coords = grid_coords((N, N, N), 1.0, h)
     pr = _finish("poisson3d", (N, N, N), rp, c, v, coords, p, (b, b, b), seed, overlap, dict(stencil="7pt"))
     pr.stencil = dict(kind="const", dims=(N, N, N), offsets=offs, coef=[6.0, -1, -1, -1, -1, -1, -1])
+    return pr
+
+
+def poisson3d_mixed(N=40, b=10, p=1, seed=1010, overlap=0):
+    """The paper's problem (A), "Poisson 3D": 7-point FD on an
+    N^3 grid, one face Dirichlet and the other five Neumann.  Reading R21: the
+    graph Laplacian of the grid (off-diagonal -1 to every in-grid neighbour,
+    diagonal = number of in-grid neighbours) plus 1 on the diagonal of the
+    z = 0 layer (the Dirichlet face's ghost).  f ~ N(0, 1) ("random
+    Gaussian-distributed").  Block partition instead of the
+    paper's recursive inertial one (out of scope); Delta = 0
+    by default as in the paper (only the biharmonic uses Delta = 1)."""
+    dims = (N, N, N)
+    idx = np.indices(dims, dtype=np.int64)
+    cnt = np.zeros(dims, np.float64)
+    for a in range(3):
+        cnt += (idx[a] > 0).astype(float) + (idx[a] < N - 1).astype(float)
+    cnt += (idx[2] == 0).astype(float)
+    diag = cnt.ravel(order="F")
+    offs = [(0, 0, 0), (1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]
+    rp, c, v = stencil_csr(dims, offs, lambda k, m: diag.copy() if k == 0 else np.full(m.shape, -1.0))
+    h = 1.0 / N
+    coords = grid_coords(dims, 0.5, h)
+    pr = _finish("poisson3d_mixed", dims, rp, c, v, coords, p, (b, b, b), seed, overlap,
+                 dict(stencil="7pt, Dirichlet z=0 face, Neumann elsewhere"))
+    pr.f = rng.normal(seed, pr.n)
     return pr
 
 

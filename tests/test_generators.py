@@ -141,3 +141,18 @@ def test_stencil_descriptor_reproduces_csr(make):
                     B[v, v + off] = cv[v]
                     B[v + off, v] = cv[v]
     assert np.array_equal(A, B)
+
+
+def test_poisson3d_mixed_boundary_rows():
+    """Problem (A) (reading R21): A 1 is the indicator of the
+    Dirichlet layer z = 0 (Neumann rows sum to zero), and A is SPD."""
+    pr = P.poisson3d_mixed(5, 5, 1)
+    A = pr.dense()
+    assert np.array_equal(A, A.T)
+    z = (np.arange(pr.n) // 25) == 0
+    assert np.array_equal(A @ np.ones(pr.n), z.astype(float))
+    assert np.linalg.eigvalsh(A).min() > 0
+    # the 2x2x2 case by hand: every node has 3 in-grid neighbours, +1 on z = 0
+    B = P.poisson3d_mixed(2, 2, 0).dense()
+    assert np.array_equal(np.diag(B), [4, 4, 4, 4, 3, 3, 3, 3])
+    assert (B[0] == np.array([4, -1, -1, 0, -1, 0, 0, 0])).all()
