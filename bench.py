@@ -270,6 +270,7 @@ def bench_ddg(args):
                    "time_to_rtol_ms": ms_step, "t_setup_s": round(t_setup, 2),
                    "cond_est_lanczos": round(float(rep.cond_est), 3),
                    "cg_iteration_bound": round(float(rep.iter_bound), 2),
+                   "true_residual_rel": float(rep.true_res) / float(np.linalg.norm(pr.f)),
                    "local_operator_bytes": int(s.info.local_factor_bytes),
                    "coarse_solve_bytes": int(s.info.coarse_solve_bytes)},
         "roofline": {"bound": "hbm", "kernel": "k_symv (colour sweep, a4/a8)",

@@ -130,6 +130,8 @@ typedef struct {
     double cond_est;      /* Lanczos estimate of cond(M A) from the CG coefficients:
                              lambda_max / lambda_min of the CG-Lanczos tridiagonal; 1 if < 2 steps */
     double iter_bound;    /* classical CG bound ln(2/rtol) / ln((sqrt k + 1)/(sqrt k - 1)), k = cond_est */
+    double true_res;      /* ||f - A u||_2 of the returned u, computed once after the loop (inside t_solve;
+                             the stopping rule uses the recurrence residual, reading R2)           */
 } ddg_report;
 
 typedef struct {

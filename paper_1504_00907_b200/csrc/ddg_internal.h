@@ -106,6 +106,7 @@ struct Scalars {
     double loc[5];   // multi-GPU: rank-local sums (init, rz_first, spmv_dot, update, rz)
     double glob[5];  // ... and their allreduced totals
     double* ab;      // CG coefficients: alpha_k at ab[2k], beta_k at ab[2k+1] (Lanczos estimate)
+    double tres;     // ||f - A u||_2 after the solve
 };
 
 // Reduction scratch: per-block partial sums + a ticket counter.
@@ -193,6 +194,8 @@ void launch_pcg_init(cudaStream_t st, int64_t n, const double* f, double* r, dou
                      int64_t nrows, Scalars* sc, double* hist, double* red, unsigned* ticket, int dist);
 void launch_pcg_rz_first(cudaStream_t st, const double* r, const double* z, double* p, const int32_t* rows,
                          int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist);
+void launch_true_res(cudaStream_t st, DevCSR A, const double* f, const double* u, int64_t n, Scalars* sc,
+                     double* red, unsigned* ticket);
 void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, const int32_t* rows,
                          int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist);
 void launch_pcg_update(cudaStream_t st, const double* p, const double* q, double* u, double* r,

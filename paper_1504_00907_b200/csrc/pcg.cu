@@ -137,6 +137,27 @@ __global__ void k_pcg_spmv_dot(DevCSR A, const double* __restrict__ p, double* _
     });
 }
 
+// ||f - A u||_2 once after the solve (SURVEY.md §8(c) PCG step 3: the true
+// residual, reported beside the recurrence residual the stopping rule uses)
+template <int SW>
+__global__ void k_true_res(DevCSR A, const double* __restrict__ f, const double* __restrict__ u, int64_t n,
+                           Scalars* sc, double* red, unsigned* ticket) {
+    double acc = 0.0;
+    const int64_t ng = (int64_t)gridDim.x * blockDim.x / SW;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / SW;
+    const int sl = threadIdx.x % SW;
+    for (int64_t base = 0; base < n; base += ng) {
+        const int64_t v = base + g;
+        const bool ok = v < n;
+        const double s = row_dot<SW>(A, ok ? v : 0, ok, u, sl);
+        if (ok && sl == 0) {
+            const double d = f[v] - s;
+            acc += d * d;
+        }
+    }
+    grid_reduce(acc, red, ticket, [&](double t) { sc->tres = sqrt(t); });
+}
+
 // u += alpha p ; r -= alpha q ; ||r|| ; history ; stopping rule (reading R1)
 __global__ void k_pcg_update(const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ u,
                              double* __restrict__ r, const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc,
@@ -267,6 +288,17 @@ void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, 
         case 8: k_pcg_spmv_dot<8><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
         case 32: k_pcg_spmv_dot<32><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
         default: k_pcg_spmv_dot<1><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist);
+    }
+}
+
+void launch_true_res(cudaStream_t st, DevCSR A, const double* f, const double* u, int64_t n, Scalars* sc,
+                     double* red, unsigned* ticket) {
+    const int g = vec_grid(n * std::max(1, A.sw));
+    switch (A.sw) {
+        case 4: k_true_res<4><<<g, VEC_THREADS, 0, st>>>(A, f, u, n, sc, red, ticket); break;
+        case 8: k_true_res<8><<<g, VEC_THREADS, 0, st>>>(A, f, u, n, sc, red, ticket); break;
+        case 32: k_true_res<32><<<g, VEC_THREADS, 0, st>>>(A, f, u, n, sc, red, ticket); break;
+        default: k_true_res<1><<<g, VEC_THREADS, 0, st>>>(A, f, u, n, sc, red, ticket);
     }
 }
 

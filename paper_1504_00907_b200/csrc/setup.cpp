@@ -1521,6 +1521,10 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         // assemble u on every rank: u is zero outside the owned rows
         comm_check(c, comm_allreduce_sum(c->comm, d_u, d_u, c->n, c->stream));
     }
+    // true residual ||f - A u|| once (u is complete on every rank here)
+    launch_true_res(c->stream, c->A, d_f, d_u, c->n, c->d_sc, c->d_redbuf, c->d_ticket);
+    c->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(cudaEventSynchronize(c->ev1));
     if (c->comm_err) return set_err(DDG_E_NCCL, "NCCL failure inside the solve");
@@ -1538,6 +1542,7 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         rep->iters = it;
         rep->res0 = s.res0;
         rep->res_final = s.res;
+        rep->true_res = s.tres;
         rep->t_setup = c->t_setup;
         rep->t_solve = ms * 1e-3;
         rep->frac_iters = (double)it;

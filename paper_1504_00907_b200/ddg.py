@@ -54,7 +54,8 @@ class ddg_opts(C.Structure):
 class ddg_report(C.Structure):
     _fields_ = [("converged", C.c_int), ("iters", C.c_int), ("res0", C.c_double),
                 ("res_final", C.c_double), ("t_setup", C.c_double), ("t_solve", C.c_double),
-                ("frac_iters", C.c_double), ("cond_est", C.c_double), ("iter_bound", C.c_double)]
+                ("frac_iters", C.c_double), ("cond_est", C.c_double), ("iter_bound", C.c_double),
+                ("true_res", C.c_double)]
 
 
 class ddg_info(C.Structure):

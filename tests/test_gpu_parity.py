@@ -376,3 +376,18 @@ def test_lanczos_coefficients_and_condition_estimate(name):
     assert abs(rep.cond_est - kappa_o) <= 1e-6 * kappa_o, (rep.cond_est, kappa_o)
     assert abs(rep.iter_bound - bound_o) <= 1e-6 * bound_o
     assert rep.cond_est >= 1.0
+
+
+@pytest.mark.parametrize("name", ["C1", "lognormal_16_b4", "elasticity_8_be4"])
+def test_true_residual_reported(name):
+    """ddg_report.true_res = ||f - A u||_2 of the returned u (SURVEY.md §8(c)
+    PCG step 3), next to the recurrence residual the stopping rule uses (R2)."""
+    pr = CASES[name]()
+    s = _solver(pr)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    A = pr.scipy()
+    ref = np.linalg.norm(pr.f - A @ u)
+    scale = abs(A).sum(1).max() * np.abs(u).max() * np.sqrt(pr.n) + np.linalg.norm(pr.f)
+    assert abs(rep.true_res - ref) <= 1e-13 * scale, (rep.true_res, ref)
+    assert rep.true_res <= 1e-7 * np.linalg.norm(pr.f)
+    assert abs(rep.res_final - hist[-1]) == 0.0
