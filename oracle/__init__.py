@@ -43,6 +43,9 @@ def lib():
         L.or_setup.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64,
                                C.POINTER(vp)]
         L.or_setup.restype = C.c_int
+        L.or_setup_coloured.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64, vp,
+                                        C.POINTER(vp)]
+        L.or_setup_coloured.restype = C.c_int
         L.or_setup3.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64, vp, i32,
                                 C.POINTER(vp)]
         L.or_setup3.restype = C.c_int
@@ -88,7 +91,7 @@ class Oracle:
     """Plain CPU implementation of setup + M r + PCG (see oracle.c)."""
 
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
-                 part2=None, nparts2=0):
+                 part2=None, nparts2=0, colour=None):
         """part2 (int32[nparts], second-level part of every part) selects the
         three-level method (oracle.c or_setup3)."""
         L = lib()
@@ -100,7 +103,11 @@ class Oracle:
         self.n = int(n)
         self.k = int(Ff.shape[1])
         h = C.c_void_p()
-        if part2 is None:
+        if colour is not None:
+            co = np.ascontiguousarray(colour, np.int32)
+            st = L.or_setup_coloured(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
+                                     int(overlap), float(rank_tol), _p(co), C.byref(h))
+        elif part2 is None:
             st = L.or_setup(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
                             int(overlap), float(rank_tol), C.byref(h))
         else:
@@ -133,9 +140,9 @@ class Oracle:
         return o
 
     @classmethod
-    def from_problem(cls, pr, overlap=None, rank_tol=1e-8, part2=None, nparts2=0):
+    def from_problem(cls, pr, overlap=None, rank_tol=1e-8, part2=None, nparts2=0, colour=None):
         return cls(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts,
-                   pr.overlap if overlap is None else overlap, rank_tol, part2, nparts2)
+                   pr.overlap if overlap is None else overlap, rank_tol, part2, nparts2, colour)
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -80,6 +80,7 @@ struct or_ctx {
     /* three-level method: the two-level method applied to
        A_0 with F_0 = R_0 F; when set, it replaces the exact coarse solve */
     struct or_ctx* child;
+    const int32_t* colour_in;   /* caller's colouring during setup (borrowed), or NULL */
 };
 
 #define ALLOC(p, cnt)                                                        \
@@ -242,6 +243,29 @@ static int build_colours(or_ctx* c) {
     char* used = calloc((size_t)cap, 1);
     for (int32_t i = 0; i < np; i++) {
         memset(used, 0, (size_t)cap);
+        if (c->colour_in) {
+            /* caller's colouring: check it with the same conflict rule
+               (Omega~_i meets Omega~_j or its neighbours, reading R3) */
+            if (c->colour_in[i] < 0 || c->colour_in[i] >= np) {
+                free(used); free(vmark); free(cptr_); free(cidx); free(fill);
+                return fail(OR_E_COLOURING, "colour %d of subdomain %d outside [0,%d)", c->colour_in[i], i, np);
+            }
+            for (int64_t a = c->optr[i]; a < c->optr[i + 1]; a++) {
+                int32_t v = c->oidx[a];
+                for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++)
+                    for (int64_t t = cptr_[c->ci[e]]; t < cptr_[c->ci[e] + 1]; t++) {
+                        int32_t j = cidx[t];
+                        if (j != i && c->colour_in[j] == c->colour_in[i]) {
+                            free(used); free(vmark); free(cptr_); free(cidx); free(fill);
+                            return fail(OR_E_COLOURING, "subdomains %d and %d are coupled but share colour %d",
+                                        i, j, c->colour_in[i]);
+                        }
+                    }
+            }
+            c->colour[i] = c->colour_in[i];
+            if (c->colour[i] + 1 > maxc) maxc = c->colour[i] + 1;
+            continue;
+        }
         /* nodes of Omega~_i and their neighbours */
         for (int64_t a = c->optr[i]; a < c->optr[i + 1]; a++) {
             int32_t v = c->oidx[a];
@@ -540,9 +564,25 @@ static void coarse_solve(or_ctx* c, double* x) {
 /* ---------------------------------------------------------------------------
  * setup
  * ------------------------------------------------------------------------- */
+static int setup_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                      const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+                      double rank_tol, const int32_t* colour, or_ctx** out);
+
 int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
              const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
              double rank_tol, or_ctx** out) {
+    return setup_impl(n, row_ptr, col, val, F, k, part, nparts, overlap, rank_tol, NULL, out);
+}
+
+int or_setup_coloured(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                      const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+                      double rank_tol, const int32_t* colour, or_ctx** out) {
+    return setup_impl(n, row_ptr, col, val, F, k, part, nparts, overlap, rank_tol, colour, out);
+}
+
+static int setup_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                      const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+                      double rank_tol, const int32_t* colour, or_ctx** out) {
     *out = NULL;
     g_err[0] = 0;
     if (n < 1 || !row_ptr || !col || !val || !F || !part || k < 1 || nparts < 1 || overlap < 0)
@@ -561,6 +601,7 @@ int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double
     if (!c) return fail(OR_E_OOM, "oom");
     int st;
     c->n = n; c->k = k; c->nparts = nparts; c->overlap = overlap; c->rank_tol = rank_tol;
+    c->colour_in = colour;
     int64_t nnz = row_ptr[n];
     c->rp = malloc((size_t)(n + 1) * sizeof(int64_t));
     c->ci = malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
@@ -601,6 +642,7 @@ int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double
         or_destroy(c);
         return st;
     }
+    c->colour_in = NULL;
     *out = c;
     return OR_OK;
 }

@@ -22,12 +22,19 @@ typedef struct or_ctx or_ctx;
 #define OR_E_PART 3
 #define OR_E_ZERO_BLOCK 4
 #define OR_E_NOT_SPD 5
+#define OR_E_COLOURING 6
 #define OR_E_BREAKDOWN 7
 #define OR_E_OOM 10
 
 int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
              const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
              double rank_tol, or_ctx** out);
+/* the same with the caller's colouring colour[nparts] (sweep order: by colour,
+   then id); a colouring with two coupled subdomains of one colour fails with
+   OR_E_COLOURING.  colour[i] = i is the paper's plain sequential sweep. */
+int or_setup_coloured(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                      const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+                      double rank_tol, const int32_t* colour, or_ctx** out);
 /* three levels: the two-level method applied again to A_0,
    with F_0 = R_0 F and second-level part part2[I] for every fine part I */
 int or_setup3(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,

@@ -467,3 +467,42 @@ def test_lanczos_trivial_cases():
     assert it == 1 and conv and len(al) == 1
     assert abs(al[0] - 1.0) <= 1e-10
     assert oracle.condition_estimate(al, be, 1e-10) == (1.0, 1.0)
+
+
+# ---------------------------------------------------------------- caller's colouring (reading R3)
+
+@pytest.mark.parametrize("mk", [lambda: P.poisson2d(16, 4, 1), lambda: P.biharmonic2d(16, 4, 2)])
+@pytest.mark.parametrize("kind", ["natural", "permuted"])
+def test_caller_sweep_order_matches_literal_composition(mk, kind):
+    """colour[i] = its sweep position: one subdomain per colour is the paper's
+    plain sequential sweep "iterating over all subdomains" in
+    that order; the oracle's M r equals the literal dense composition."""
+    pr = mk()
+    A = pr.dense()
+    if kind == "natural":
+        colour = np.arange(pr.nparts, dtype=np.int32)
+    else:
+        colour = np.random.default_rng(3).permutation(pr.nparts).astype(np.int32)
+    o = oracle.Oracle.from_problem(pr, colour=colour)
+    assert o.ncolours == pr.nparts and np.array_equal(o.colours(), colour)
+    order = list(np.argsort(colour))
+    sets = [o.overlap_set(i) for i in range(pr.nparts)]
+    r = np.random.default_rng(1).standard_normal(pr.n)
+    ref = dense_two_level(A, r, sets, order, o.P_dense())
+    assert np.linalg.norm(o.apply_precond(r) - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+def test_caller_colouring_validated():
+    pr = P.poisson2d(16, 4, 1)
+    greedy = oracle.Oracle.from_problem(pr)
+    col = greedy.colours()
+    o = oracle.Oracle.from_problem(pr, colour=col)          # the same colouring passed in
+    r = np.random.default_rng(2).standard_normal(pr.n)
+    assert np.array_equal(o.apply_precond(r), greedy.apply_precond(r))
+    bad = col.copy()
+    bad[1] = bad[0]                                          # parts 0 and 1 are neighbours
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.Oracle.from_problem(pr, colour=bad)
+    assert e.value.code == 6
+    with pytest.raises(oracle.OracleError):
+        oracle.Oracle.from_problem(pr, colour=np.full(pr.nparts, -1, np.int32))
