@@ -41,7 +41,7 @@ typedef enum {
     DDG_E_ZERO_BLOCK = 4,  /* F restricted to a part is entirely zero   */
     DDG_E_NOT_SPD = 5,     /* non-positive pivot in a local or the coarse factor
                               (SPEC.md:73); message names stage, block and pivot      */
-    DDG_E_COLOURING = 6,   /* internal colouring check failed                         */
+    DDG_E_COLOURING = 6,   /* ddg_opts.colour has two coupled subdomains in one colour */
     DDG_E_BREAKDOWN = 7,   /* p^T A p <= 0 or r^T z <= 0 inside PCG     */
     DDG_E_CUDA = 8,        /* CUDA runtime error or no device                         */
     DDG_E_NCCL = 9,        /* communicator error                                      */
@@ -117,6 +117,14 @@ typedef struct {
     const int32_t* part2;
     int32_t nparts2;
     const int32_t* block_coords2;
+    /* Optional colouring of the subdomains (nparts int32 in [0, nparts), host,
+       borrowed for ddg_setup): the sweep visits colours in increasing order,
+       subdomains of one colour concurrently (ids increasing within a colour
+       for the record).  Two subdomains of one colour must not be coupled
+       (Omega~_i meets Omega~_j or its neighbours): DDG_E_COLOURING otherwise.
+       colour[i] = i is the paper's plain sequential sweep.
+       NULL: greedy first-fit in id order (reading R3). */
+    const int32_t* colour;
 } ddg_opts;
 
 typedef struct {

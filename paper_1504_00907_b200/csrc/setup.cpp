@@ -259,7 +259,32 @@ static int build_colours(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
     std::vector<int32_t> vmark(n, -1);
     std::vector<char> used;
     int maxc = 0;
-    for (int i = 0; i < np; ++i) {
+    if (const int32_t* uc = c->opts.colour) {
+        // the caller's colouring (ddg_opts.colour), checked with the same
+        // conflict rule: Omega~_i meets Omega~_j or its neighbours (reading R3)
+        for (int i = 0; i < np; ++i)
+            if (uc[i] < 0 || uc[i] >= np)
+                return set_err(DDG_E_COLOURING, "colour %d of subdomain %d outside [0,%d)", uc[i], i, np);
+        for (int i = 0; i < np; ++i) {
+            for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) {
+                const int32_t v = c->oidx[a];
+                for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
+                    const int32_t u = col[x];
+                    if (vmark[u] == i) continue;
+                    vmark[u] = i;
+                    for (int64_t t = cp[u]; t < cp[u + 1]; ++t) {
+                        const int j = cov[t];
+                        if (j != i && uc[j] == uc[i])
+                            return set_err(DDG_E_COLOURING, "subdomains %d and %d are coupled but share colour %d",
+                                           i, j, uc[i]);
+                    }
+                }
+            }
+            c->colour[i] = uc[i];
+            maxc = std::max(maxc, uc[i] + 1);
+        }
+    }
+    for (int i = 0; i < np && !c->opts.colour; ++i) {
         used.assign(maxc + 1, 0);
         for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) {
             const int32_t v = c->oidx[a];
@@ -279,10 +304,10 @@ static int build_colours(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
         maxc = std::max(maxc, cc + 1);
     }
     c->ncolours = maxc;
-    c->order.clear();
-    for (int cc = 0; cc < maxc; ++cc)
-        for (int i = 0; i < np; ++i)
-            if (c->colour[i] == cc) c->order.push_back(i);
+    c->order.resize(np);
+    for (int i = 0; i < np; ++i) c->order[i] = i;
+    std::stable_sort(c->order.begin(), c->order.end(),
+                     [&](int a, int b) { return c->colour[a] < c->colour[b]; });   // (colour, id)
     return DDG_OK;
 }
 
@@ -1019,7 +1044,8 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     };
     build_overlap(c, row_ptr, col);
     tick("overlap");
-    build_colours(c, row_ptr, col);
+    if ((st = build_colours(c, row_ptr, col))) { free_ctx(c); return st; }
+    c->opts.colour = nullptr;   // borrowed for the duration of ddg_setup only
     tick("colours");
     if (c->opts.block_coords && c->opts.block_ndim > 0)
         c->block_coords.assign(c->opts.block_coords, c->opts.block_coords + (int64_t)nparts * c->opts.block_ndim);

@@ -48,7 +48,7 @@ class ddg_opts(C.Structure):
                 ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("comm", C.c_void_p),
                 ("small_kernel", C.c_int), ("block_coords", C.c_void_p),
                 ("stencil", C.POINTER(ddg_stencil)), ("part2", C.c_void_p),
-                ("nparts2", C.c_int32), ("block_coords2", C.c_void_p)]
+                ("nparts2", C.c_int32), ("block_coords2", C.c_void_p), ("colour", C.c_void_p)]
 
 
 class ddg_report(C.Structure):
@@ -158,7 +158,7 @@ class Solver:
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
                  stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
                  verbose=False, coarse_variant=0, block_coords=None, comm=None, fuse_gather=None,
-                 small_kernel=None, stencil=None, part2=None, nparts2=0, block_coords2=None):
+                 small_kernel=None, stencil=None, part2=None, nparts2=0, block_coords2=None, colour=None):
         """part2 (int32[nparts]: second-level part of every part) selects the
         three-level method (include/ddg.h ddg_opts.part2)."""
         L = load()
@@ -181,6 +181,10 @@ class Solver:
             o.block_ndim = int(bc.shape[1])
             o.block_coords = bc.ctypes.data
         keep = []
+        if colour is not None:
+            co = np.ascontiguousarray(colour, np.int32)
+            keep.append(co)
+            o.colour = co.ctypes.data
         if part2 is not None:
             p2 = np.ascontiguousarray(part2, np.int32)
             keep.append(p2)

@@ -391,3 +391,39 @@ def test_true_residual_reported(name):
     assert abs(rep.true_res - ref) <= 1e-13 * scale, (rep.true_res, ref)
     assert rep.true_res <= 1e-7 * np.linalg.norm(pr.f)
     assert abs(rep.res_final - hist[-1]) == 0.0
+
+
+@pytest.mark.parametrize("kind", ["natural", "permuted", "greedy"])
+@pytest.mark.parametrize("name", ["C1", "biharm_64_b16_p3"])
+def test_caller_colouring_parity(name, kind):
+    """ddg_opts.colour: the caller's sweep order (natural = the paper's plain
+    sequential sweep), against the oracle given the same one."""
+    pr = CASES[name]()
+    if kind == "natural":
+        colour = np.arange(pr.nparts, dtype=np.int32)
+    elif kind == "permuted":
+        colour = np.random.default_rng(5).permutation(pr.nparts).astype(np.int32)
+    else:
+        colour = oracle.Oracle.from_problem(pr).colours()
+    s = _solver(pr, colour=colour)
+    o = oracle.Oracle.from_problem(pr, colour=colour)
+    assert np.array_equal(s.colours(), colour) and s.info.ncolours == o.ncolours
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    uo, ito, histo, conv = o.pcg(pr.f, 1e-8)
+    assert abs(it - ito) <= 1
+    m = min(len(hist), len(histo))
+    assert (np.abs(hist[:m] - histo[:m]) / histo[:m]).max() <= H_TOL
+    assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+    if kind == "greedy":
+        u0, it0, _, _ = _solver(pr).solve(pr.f, 1e-8)
+        assert it0 == it and np.array_equal(u0, u)
+
+
+def test_caller_colouring_rejected():
+    from paper_1504_00907_b200.ddg import DDGError
+    pr = CASES["C1"]()
+    col = oracle.Oracle.from_problem(pr).colours()
+    col[1] = col[0]
+    with pytest.raises(DDGError) as e:
+        _solver(pr, colour=col)
+    assert e.value.code == 6
