@@ -160,6 +160,7 @@ __device__ __forceinline__ void st_release(int32_t* p, int v) {
 
 struct DFCtx {
     const FrontDesc* fronts;
+    const int32_t* fchild;
     const FrontDF* fdf;
     const FRedTask* fwd;
     const FRedTask* bwd;
@@ -183,9 +184,8 @@ __device__ void df_assemble(const DFCtx& d, int t) {
     for (int a = threadIdx.x; a < ntot; a += blockDim.x) fv[a] = a < f.nS ? d.bc[d.fS[f.S_off + a]] : 0.0;
     for (int a = threadIdx.x; a < f.nB; a += blockDim.x) wt[a] = 0.0;
     __syncthreads();
-    for (int k = 0; k < 2; ++k) {
-        const int ci = k == 0 ? f.child0 : f.child1;
-        if (ci < 0) continue;
+    for (int k = 0; k < f.nchild; ++k) {                      // children in fixed order
+        const int ci = d.fchild[f.child_off + k];
         const FrontDesc c = d.fronts[ci];
         for (int j = threadIdx.x; j < c.nB; j += blockDim.x) {
             const int pos = d.map[c.map_off + j];
@@ -240,8 +240,7 @@ __device__ void df_forward_complete(const DFCtx& d, int t, int* sh) {
         }
         if (threadIdx.x == 0) {
             const FrontDesc p = d.fronts[f.parent];
-            const int nch = (p.child0 >= 0) + (p.child1 >= 0);
-            sh[0] = atomicAdd(df_flag(d, f.parent, DFF_CHILDREN), 1) == nch - 1;
+            sh[0] = atomicAdd(df_flag(d, f.parent, DFF_CHILDREN), 1) == p.nchild - 1;
         }
         __syncthreads();
         if (!sh[0]) return;
@@ -378,9 +377,8 @@ k_coarse_dataflow(int nwork, const int32_t* __restrict__ work, DFCtx d, const in
                 df_forward_complete(d, t, sh);
             } else {
                 const FrontDesc f = d.fronts[t];
-                for (int k = 0; k < 2; ++k) {                      // children: gather x[B_c]
-                    const int ci = k == 0 ? f.child0 : f.child1;
-                    if (ci < 0) continue;
+                for (int k = 0; k < f.nchild; ++k) {               // children: gather x[B_c]
+                    const int ci = d.fchild[f.child_off + k];
                     const FrontDesc c = d.fronts[ci];
                     double* fv = d.fvec + c.fvec_off + c.nSp;
                     const int nBp = c.nT * TILE - c.nSp;
@@ -410,13 +408,14 @@ k_coarse_dataflow(int nwork, const int32_t* __restrict__ work, DFCtx d, const in
 }
 
 void launch_coarse_dataflow(cudaStream_t st, int nwork, const int32_t* work, const FrontDesc* fronts,
+                            const int32_t* fchild,
                             const FrontDF* fdf, const int32_t* item_front, int item_base, const OpDesc* ops,
                             const ItemDesc* items, const double* ctiles, const FRedTask* fwd, const FRedTask* bwd,
                             const int64_t* contrib, const int32_t* fS, const int32_t* fB, const int32_t* map,
                             const double* bc, double* fvec, double* w, double* x, double* partials,
                             int32_t* state, int max_rows_t, const int32_t* done, uint64_t* trace) {
     if (nwork <= 0) return;
-    DFCtx d{fronts, fdf, fwd, bwd, contrib, fS, fB, map, bc, fvec, w, x, partials, state};
+    DFCtx d{fronts, fchild, fdf, fwd, bwd, contrib, fS, fB, map, bc, fvec, w, x, partials, state};
     const size_t smem = (size_t)max_rows_t * (SYMV_WARPS + 1) * sizeof(double);
     static bool init_dev[64] = {};   // function attributes are per device
     int dev_ = 0;
@@ -432,7 +431,7 @@ void launch_coarse_dataflow(cudaStream_t st, int nwork, const int32_t* work, con
 }
 
 // forward: front vector [b_S ; 0] and w_t = incoming contributions to B
-__global__ void k_front_fwd_assemble(int f0, const FrontDesc* __restrict__ fronts,
+__global__ void k_front_fwd_assemble(int f0, const FrontDesc* __restrict__ fronts, const int32_t* __restrict__ fchild,
                                      const int32_t* __restrict__ fS, const int32_t* __restrict__ map,
                                      const double* __restrict__ bc, double* __restrict__ fvec,
                                      double* __restrict__ w, const int32_t* done) {
@@ -444,9 +443,8 @@ __global__ void k_front_fwd_assemble(int f0, const FrontDesc* __restrict__ front
     for (int a = threadIdx.x; a < ntot; a += blockDim.x) fv[a] = a < f.nS ? bc[fS[f.S_off + a]] : 0.0;
     for (int a = threadIdx.x; a < f.nB; a += blockDim.x) wt[a] = 0.0;
     __syncthreads();
-    for (int s = 0; s < 2; ++s) {
-        const int ci = s == 0 ? f.child0 : f.child1;
-        if (ci < 0) continue;
+    for (int s = 0; s < f.nchild; ++s) {
+        const int ci = fchild[f.child_off + s];
         const FrontDesc c = fronts[ci];
         for (int j = threadIdx.x; j < c.nB; j += blockDim.x) {
             const int pos = map[c.map_off + j];
@@ -534,11 +532,11 @@ void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int3
     k_prolong<<<nparts, 256, 0, st>>>(bptr, bidx, cptr, qoff, Q, yc, z, done, parts);
 }
 
-void launch_front_fwd_assemble(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
+void launch_front_fwd_assemble(cudaStream_t st, int f0, int nf, const FrontDesc* fronts, const int32_t* fchild,
                                const int32_t* fS, const int32_t* map, const double* bc, double* fvec,
                                double* w, const int32_t* done) {
     if (nf <= 0) return;
-    k_front_fwd_assemble<<<nf, 256, 0, st>>>(f0, fronts, fS, map, bc, fvec, w, done);
+    k_front_fwd_assemble<<<nf, 256, 0, st>>>(f0, fronts, fchild, fS, map, bc, fvec, w, done);
 }
 
 void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,

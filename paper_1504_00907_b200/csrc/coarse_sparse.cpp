@@ -31,11 +31,13 @@
 namespace {
 
 int LEAF_UNKNOWNS = 256;   // nested dissection stops below this many unknowns (DDG_ND_LEAF)
+int MERGE_LEVELS = 0;      // top bisection levels merged into the root front (DDG_ND_MERGE)
+int64_t MERGE_MAX = 12288; // ... while the merged separator stays below this many unknowns
 int FRONT_BT = 8;   // tiles per item side of the front operators (DDG_FRONT_BT)
 
 struct NDNode {
     std::vector<int32_t> sep;  // blocks eliminated at this node
-    int child[2] = {-1, -1};
+    std::vector<int> child;    // children in elimination order (2 from a bisection, more when merged)
     int parent = -1;
     int height = 0;
 };
@@ -45,7 +47,7 @@ struct NDNode {
 struct SparseCoarse {
     int nfront = 0, nlevels = 0;
     std::vector<FrontDesc> fr;
-    std::vector<int32_t> fS, fB, fmap;
+    std::vector<int32_t> fS, fB, fmap, fchild;
     std::vector<int> lb;                       // fronts of level h: [lb[h], lb[h+1])
     std::vector<int> g_begin, g_end, h_begin, h_end;
     std::vector<int> fwd_b, bwd_b;             // task ranges per level (size nlevels+1)
@@ -68,7 +70,7 @@ struct SparseCoarse {
     std::vector<std::vector<double>> tr_v;
     // device
     FrontDesc* d_fr = nullptr;
-    int32_t *d_fS = nullptr, *d_fB = nullptr, *d_fmap = nullptr, *d_item_front = nullptr;
+    int32_t *d_fS = nullptr, *d_fB = nullptr, *d_fmap = nullptr, *d_item_front = nullptr, *d_fchild = nullptr;
     FRedTask *d_fwd = nullptr, *d_bwd = nullptr;
     int64_t* d_contrib = nullptr;
     double *d_fvec = nullptr, *d_w = nullptr, *d_ctiles = nullptr, *d_bc = nullptr;
@@ -77,7 +79,7 @@ struct SparseCoarse {
 
 void sparse_coarse_free(SparseCoarse* s) {
     if (!s) return;
-    void* p[] = {s->d_fr, s->d_fS, s->d_fB, s->d_fmap, s->d_item_front, s->d_fwd, s->d_bwd,
+    void* p[] = {s->d_fr, s->d_fchild, s->d_fS, s->d_fB, s->d_fmap, s->d_item_front, s->d_fwd, s->d_bwd,
                  s->d_contrib, s->d_fvec, s->d_w, s->d_ctiles, s->d_bc, s->d_dfwork, s->d_dfstate, s->d_fdf,
                  s->d_trace};
     for (void* x : p)
@@ -215,11 +217,50 @@ struct NDBuilder {
         }
         std::sort(S.begin(), S.end());
         nodes[id].sep = S;
-        int k = 0;
         for (auto* part : {&L, &R}) {
             if (part->empty()) continue;
             int ch = build(std::move(*part));
-            nodes[id].child[k++] = ch;
+            nodes[id].child.push_back(ch);
+            nodes[ch].parent = id;
+        }
+        return id;
+    }
+
+    // The top `levels` bisections merged into one root front: its separator is
+    // the union of theirs and the remaining regions are its children.  One
+    // dense front replaces `levels` sequential steps of the solve's critical
+    // path at the top of the tree, where the fronts are few and small.
+    int build_top(std::vector<int32_t> V, int levels) {
+        if (levels <= 0) return build(std::move(V));
+        const int id = (int)nodes.size();
+        nodes.emplace_back();
+        std::vector<std::vector<int32_t>> frontier, finals;
+        std::vector<int32_t> seps;
+        frontier.push_back(std::move(V));
+        for (int l = 0; l < levels && !frontier.empty(); ++l) {
+            if (l > 0 && unknowns(seps) >= MERGE_MAX) break;
+            std::vector<std::vector<int32_t>> next;
+            for (auto& R0 : frontier) {
+                if (R0.size() <= 1 || unknowns(R0) <= LEAF_UNKNOWNS) { finals.push_back(std::move(R0)); continue; }
+                std::vector<int32_t> L, R, S;
+                if (!split_geom(R0, L, R, S)) split_bfs(R0, L, R, S);
+                if (S.empty() && (L.empty() || R.empty())) { finals.push_back(std::move(R0)); continue; }
+                if (S.empty()) {
+                    S.push_back(R.back());
+                    R.pop_back();
+                }
+                seps.insert(seps.end(), S.begin(), S.end());
+                if (!L.empty()) next.push_back(std::move(L));
+                if (!R.empty()) next.push_back(std::move(R));
+            }
+            frontier.swap(next);
+        }
+        for (auto& R0 : frontier) finals.push_back(std::move(R0));
+        std::sort(seps.begin(), seps.end());
+        nodes[id].sep = seps;
+        for (auto& R0 : finals) {
+            const int ch = build(std::move(R0));
+            nodes[id].child.push_back(ch);
             nodes[ch].parent = id;
         }
         return id;
@@ -243,6 +284,8 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     // critical path; large ones (C3): smaller leaves, fewer bytes (measured)
     LEAF_UNKNOWNS = c->nc <= 262144 ? 1024 : 256;
     if (const char* e = getenv("DDG_ND_LEAF")) LEAF_UNKNOWNS = std::max(16, atoi(e));
+    MERGE_LEVELS = 0;
+    if (const char* e = getenv("DDG_ND_MERGE")) MERGE_LEVELS = std::max(0, atoi(e));
     // part adjacency
     std::vector<std::vector<int32_t>> adj(np);
     for (int I = 0; I < np; ++I) {
@@ -275,7 +318,7 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
                 for (int32_t u : adj[v])
                     if (comp[u] < 0) { comp[u] = s; V.push_back(u); stack.push_back(u); }
             }
-            nd.build(std::move(V));
+            nd.build_top(std::move(V), MERGE_LEVELS);
         }
     }
     auto& nodes = nd.nodes;
@@ -287,11 +330,9 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
         int timer = 0;
         std::function<void(int)> dfs = [&](int t) {
             tin[t] = timer++;
-            for (int k = 0; k < 2; ++k)
-                if (nodes[t].child[k] >= 0) dfs(nodes[t].child[k]);
+            for (int ch : nodes[t].child) dfs(ch);
             int h = 0;
-            for (int k = 0; k < 2; ++k)
-                if (nodes[t].child[k] >= 0) h = std::max(h, nodes[nodes[t].child[k]].height + 1);
+            for (int ch : nodes[t].child) h = std::max(h, nodes[ch].height + 1);
             nodes[t].height = h;
             post.push_back(t);
             tout[t] = timer++;
@@ -310,11 +351,10 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     for (int t : post) {
         std::vector<int32_t> cand;
         for (int32_t b : nodes[t].sep) cand.insert(cand.end(), adj[b].begin(), adj[b].end());
-        for (int k = 0; k < 2; ++k)
-            if (nodes[t].child[k] >= 0) {
-                const auto& cb = Bblk[nodes[t].child[k]];
-                cand.insert(cand.end(), cb.begin(), cb.end());
-            }
+        for (int ch : nodes[t].child) {
+            const auto& cb = Bblk[ch];
+            cand.insert(cand.end(), cb.begin(), cb.end());
+        }
         std::vector<int32_t> keep;
         for (int32_t u : cand) {
             const int su = snode[u];
@@ -344,8 +384,9 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
         const int t = order[i];
         FrontDesc& f = sc->fr[i];
         f.parent = nodes[t].parent >= 0 ? fid[nodes[t].parent] : -1;
-        f.child0 = nodes[t].child[0] >= 0 ? fid[nodes[t].child[0]] : -1;
-        f.child1 = nodes[t].child[1] >= 0 ? fid[nodes[t].child[1]] : -1;
+        f.child_off = (int32_t)sc->fchild.size();
+        f.nchild = (int32_t)nodes[t].child.size();
+        for (int ch : nodes[t].child) sc->fchild.push_back(fid[ch]);
         f.S_off = (int64_t)sc->fS.size();
         for (int32_t b : nodes[t].sep)
             for (int32_t q = c->cptr[b]; q < c->cptr[b + 1]; ++q) sc->fS.push_back(q);
@@ -370,8 +411,8 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
         FrontDesc& p = sc->fr[i];
         for (int a = 0; a < p.nS; ++a) pos[sc->fS[p.S_off + a]] = a;
         for (int j = 0; j < p.nB; ++j) pos[sc->fB[p.B_off + j]] = p.nSp + j;
-        for (int ci : {p.child0, p.child1}) {
-            if (ci < 0) continue;
+        for (int k = 0; k < p.nchild; ++k) {
+            const int ci = sc->fchild[p.child_off + k];
             FrontDesc& ch = sc->fr[ci];
             ch.map_off = (int64_t)sc->fmap.size();
             for (int j = 0; j < ch.nB; ++j) {
@@ -562,7 +603,7 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
         }
     sc->dfwork.clear();
     for (int i = 0; i < nn; ++i)
-        if (sc->fr[i].child0 < 0 && sc->fr[i].child1 < 0) sc->dfwork.push_back(DF_ASSEMBLE | i);
+        if (sc->fr[i].nchild == 0) sc->dfwork.push_back(DF_ASSEMBLE | i);
     for (int h = 0; h < sc->nlevels; ++h) {
         for (int q = sc->g_begin[h]; q < sc->g_end[h]; ++q) sc->dfwork.push_back(q);
         for (int k = sc->fwd_b[h]; k < sc->fwd_b[h + 1]; ++k) sc->dfwork.push_back(DF_RED | k);
@@ -601,7 +642,8 @@ static int up_s(cudaStream_t s, T** d, const std::vector<T>& h) {
 int sparse_coarse_numeric(ddg_ctx* c) {
     SparseCoarse* sc = c->sparse;
     int st;
-    if ((st = up(&sc->d_fr, sc->fr)) || (st = up(&sc->d_fS, sc->fS)) || (st = up(&sc->d_fB, sc->fB)) ||
+    if ((st = up(&sc->d_fr, sc->fr)) || (st = up(&sc->d_fchild, sc->fchild)) || (st = up(&sc->d_fS, sc->fS)) ||
+        (st = up(&sc->d_fB, sc->fB)) ||
         (st = up(&sc->d_fmap, sc->fmap)) || (st = up(&sc->d_item_front, sc->item_front)) ||
         (st = up(&sc->d_fwd, sc->fwd)) || (st = up(&sc->d_bwd, sc->bwd)) ||
         (st = up(&sc->d_contrib, sc->contrib)) || (st = up(&sc->d_dfwork, sc->dfwork)) ||
@@ -654,11 +696,13 @@ int sparse_coarse_numeric(ddg_ctx* c) {
             cudaFree(dr); cudaFree(dc); cudaFree(df); cudaFree(dv);
         }
         // extend-add the children's Schur complements (slot by slot: no write conflicts)
-        for (int slot = 0; slot < 2; ++slot) {
+        int maxch = 0;
+        for (int i = f0; i < f1; ++i) maxch = std::max(maxch, (int)sc->fr[i].nchild);
+        for (int slot = 0; slot < maxch; ++slot) {
             std::vector<int32_t> tasks;
             int64_t maxe = 0;
             for (int i = f0; i < f1; ++i) {
-                const int ch = slot == 0 ? sc->fr[i].child0 : sc->fr[i].child1;
+                const int ch = slot < sc->fr[i].nchild ? sc->fchild[sc->fr[i].child_off + slot] : -1;
                 if (ch >= 0 && sc->fr[ch].nB > 0) {
                     tasks.push_back(ch);
                     maxe = std::max<int64_t>(maxe, (int64_t)sc->fr[ch].nB * sc->fr[ch].nB);
@@ -689,8 +733,8 @@ int sparse_coarse_numeric(ddg_ctx* c) {
                         asym = std::max(asym, fabs(at(R, Cc) - at(Cc, R)));
                     }
                 for (int R = 0; R < f.nS; ++R) dmin = std::min(dmin, at(R, R));
-                fprintf(stderr, "[dbg] %s lvl %d front %d nS %d nB %d nT %d ch %d %d cs %.17g asym %.3g dmin %.3g\n",
-                        tag, h, i, f.nS, f.nB, f.nT, f.child0, f.child1, cs, asym, dmin);
+                fprintf(stderr, "[dbg] %s lvl %d front %d nS %d nB %d nT %d nch %d cs %.17g asym %.3g dmin %.3g\n",
+                        tag, h, i, f.nS, f.nB, f.nT, f.nchild, cs, asym, dmin);
             }
             return DDG_OK;
         };
@@ -785,7 +829,7 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
     if (sc->dataflow) {
         cudaMemsetAsync(sc->d_dfstate, 0, (1 + (size_t)DF_STATE_PER_FRONT * sc->nfront) * sizeof(int32_t),
                         c->stream);
-        launch_coarse_dataflow(c->stream, (int)sc->dfwork.size(), sc->d_dfwork, sc->d_fr, sc->d_fdf,
+        launch_coarse_dataflow(c->stream, (int)sc->dfwork.size(), sc->d_dfwork, sc->d_fr, sc->d_fchild, sc->d_fdf,
                                sc->d_item_front, sc->item_base, c->d_ops, c->d_items, sc->d_ctiles, sc->d_fwd,
                                sc->d_bwd, sc->d_contrib, sc->d_fS, sc->d_fB, sc->d_fmap, sc->d_bc, sc->d_fvec,
                                sc->d_w, d_x, c->d_partials, sc->d_dfstate, sc->max_rows_t, done, sc->d_trace);
@@ -793,7 +837,7 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
     }
     for (int h = 0; h < sc->nlevels; ++h) {
         const int f0 = sc->lb[h], nf = sc->lb[h + 1] - f0;
-        launch_front_fwd_assemble(c->stream, f0, nf, sc->d_fr, sc->d_fS, sc->d_fmap, sc->d_bc, sc->d_fvec,
+        launch_front_fwd_assemble(c->stream, f0, nf, sc->d_fr, sc->d_fchild, sc->d_fS, sc->d_fmap, sc->d_bc, sc->d_fvec,
                                   sc->d_w, done);
         if (ring_ok(c, sc->ring_fwd[h]))
         {

@@ -64,7 +64,7 @@ struct FrontDesc {
     int32_t nT, nK;          // tiles per side of the [S|B] front, pivot (S) tiles
     int32_t nS, nSp, nB;     // |S|, |S| padded to TILE, |B|
     int32_t parent;          // parent front or -1
-    int32_t child0, child1;  // children or -1
+    int32_t child_off, nchild;   // children: fchild[child_off .. child_off + nchild)
     int32_t op;              // OpDesc index of its solve operator
     int32_t pad;
     int64_t fvec_off;        // front vector (nT*TILE doubles)
@@ -233,7 +233,7 @@ void launch_front_extend_add(cudaStream_t st, int ntask, const int32_t* child, c
                              double* const* fptr, const int32_t* map, int64_t max_elems);
 void launch_front_pack(cudaStream_t st, int i0, int i1, int item_base, const int32_t* item_front,
                        const FrontDesc* fronts, double* const* fptr, const ItemDesc* items, double* ctiles);
-void launch_front_fwd_assemble(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
+void launch_front_fwd_assemble(cudaStream_t st, int f0, int nf, const FrontDesc* fronts, const int32_t* fchild,
                                const int32_t* fS, const int32_t* map, const double* bc, double* fvec,
                                double* w, const int32_t* done);
 void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
@@ -243,6 +243,7 @@ void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt,
                          double* x, const int32_t* done);
 // whole sparse coarse solve y = A_c^{-1} b_c in one launch (see coarse.cu)
 void launch_coarse_dataflow(cudaStream_t st, int nwork, const int32_t* work, const FrontDesc* fronts,
+                            const int32_t* fchild,
                             const FrontDF* fdf, const int32_t* item_front, int item_base, const OpDesc* ops,
                             const ItemDesc* items, const double* ctiles, const FRedTask* fwd, const FRedTask* bwd,
                             const int64_t* contrib, const int32_t* fS, const int32_t* fB, const int32_t* map,
