@@ -79,6 +79,76 @@ k_restrict_warp(int nparts, const int64_t* __restrict__ bptr, const int32_t* __r
     }
 }
 
+// Two-stage restriction (single GPU): k_gather_flat first writes the
+// residual res[x] = (r - A z)[bidx[x]] for every position x in part order
+// (one coalesced pass at streaming speed), then b_c[I,:] = Q_I^T res[Omega_I]
+// reads Q_I and res contiguously, warp per part.
+template <int R>
+__global__ void __launch_bounds__(256)
+k_restrict_dot(int nparts, const int64_t* __restrict__ bptr, const int32_t* __restrict__ cptr,
+               const int64_t* __restrict__ qoff, const double* __restrict__ Q, const double* __restrict__ res,
+               double* __restrict__ bc, const int32_t* done) {
+    if (*done) return;
+    const int I = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (I >= nparts) return;
+    const int64_t b0 = bptr[I];
+    const int mI = (int)(bptr[I + 1] - b0);
+    const int c0 = cptr[I], ncI = cptr[I + 1] - c0;
+    const double* QI = Q + qoff[I];
+    double rv[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) rv[k] = lane + 32 * k < mI ? res[b0 + lane + 32 * k] : 0.0;
+    for (int i = 0; i < ncI; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int a = lane + 32 * k;
+            if (a < mI) acc += QI[(int64_t)i * mI + a] * rv[k];
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) bc[c0 + i] = acc;
+    }
+}
+
+// large parts: block per part, one block reduction per coarse column
+__global__ void __launch_bounds__(256)
+k_restrict_dot_block(const int64_t* __restrict__ bptr, const int32_t* __restrict__ cptr,
+                     const int64_t* __restrict__ qoff, const double* __restrict__ Q,
+                     const double* __restrict__ res, double* __restrict__ bc, const int32_t* done) {
+    if (*done) return;
+    const int I = blockIdx.x;
+    const int64_t b0 = bptr[I];
+    const int mI = (int)(bptr[I + 1] - b0);
+    const int c0 = cptr[I], ncI = cptr[I + 1] - c0;
+    const double* QI = Q + qoff[I];
+    for (int i = 0; i < ncI; ++i) {
+        double acc = 0.0;
+        for (int a = threadIdx.x; a < mI; a += blockDim.x) acc += QI[(int64_t)i * mI + a] * res[b0 + a];
+        acc = block_sum(acc);
+        if (threadIdx.x == 0) bc[c0 + i] = acc;
+    }
+}
+
+// Flat prolongation (single GPU): thread per position x of the part order,
+// z[bidx[x]] += sum_i Q_I[a, i] y_c[I, i] with I = xpart[x], a = x - bptr[I].
+__global__ void __launch_bounds__(256)
+k_prolong_flat(int64_t n, const int32_t* __restrict__ xpart, const int64_t* __restrict__ bptr,
+               const int32_t* __restrict__ bidx, const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff,
+               const double* __restrict__ Q, const double* __restrict__ yc, double* __restrict__ z,
+               const int32_t* done) {
+    if (*done) return;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const int I = xpart[x];
+        const int64_t b0 = bptr[I];
+        const int64_t mI = bptr[I + 1] - b0;
+        const int c0 = cptr[I], ncI = cptr[I + 1] - c0;
+        const double* q = Q + qoff[I] + (x - b0);
+        double acc = 0.0;
+        for (int i = 0; i < ncI; ++i) acc += q[i * mI] * yc[c0 + i];
+        z[bidx[x]] += acc;
+    }
+}
+
 // z[Omega_I] += Q_I y_c[I,:], warp per part
 template <int R>
 __global__ void __launch_bounds__(256)
@@ -511,6 +581,24 @@ void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, co
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_coarse_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_coarse_restrict<<<nparts, 256, smem, st>>>(bptr, bidx, cptr, qoff, Q, A, r, z, bc, done, parts);
+}
+
+void launch_restrict_dot(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* cptr, const int64_t* qoff,
+                         const double* Q, const double* res, double* bc, int maxmI, const int32_t* done) {
+    if (nparts <= 0) return;
+    const int g = (nparts + 7) / 8;
+    if (maxmI <= 64) k_restrict_dot<2><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else if (maxmI <= 128) k_restrict_dot<4><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else if (maxmI <= 256) k_restrict_dot<8><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else if (maxmI <= 512) k_restrict_dot<16><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else k_restrict_dot_block<<<nparts, 256, 0, st>>>(bptr, cptr, qoff, Q, res, bc, done);
+}
+
+void launch_prolong_flat(cudaStream_t st, int64_t n, const int32_t* xpart, const int64_t* bptr, const int32_t* bidx,
+                         const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc, double* z,
+                         const int32_t* done) {
+    if (n <= 0) return;
+    k_prolong_flat<<<vec_grid(n), 256, 0, st>>>(n, xpart, bptr, bidx, cptr, qoff, Q, yc, z, done);
 }
 
 void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,

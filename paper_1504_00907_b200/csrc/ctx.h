@@ -114,6 +114,9 @@ struct ddg_ctx {
     std::vector<double> colour_alg_bytes;
     // coarse solver variant: 1 dense packed inverse, 2 sparse supernodal (coarse_sparse.cpp)
     int coarse_variant = 1;   // 1 dense, 2 sparse, 3 three levels (child two-level context on A_c)
+    bool flat_coarse = true;           // two-stage restriction + flat prolongation (single GPU)
+    double* d_res = nullptr;           // r - A z in part order (flat restriction)
+    int32_t* d_xpart = nullptr;        // part of every position of the part order
     struct ddg_ctx* child = nullptr;   // three levels: the two-level method on A_c
     double* d_bc = nullptr;            // three levels: coarse right-hand side R_0 (r - A z)
     SparseCoarse* sparse = nullptr;

@@ -180,6 +180,11 @@ void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, co
                             const int32_t* cptr, const int64_t* qoff, const double* Q, DevCSR A,
                             const double* r, const double* z, double* bc, int maxmI,
                             const int32_t* done, const int32_t* parts = nullptr);
+void launch_restrict_dot(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* cptr, const int64_t* qoff,
+                         const double* Q, const double* res, double* bc, int maxmI, const int32_t* done);
+void launch_prolong_flat(cudaStream_t st, int64_t n, const int32_t* xpart, const int64_t* bptr, const int32_t* bidx,
+                         const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc, double* z,
+                         const int32_t* done);
 void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,
                     const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc,
                     double* z, int maxmI, const int32_t* done, const int32_t* parts = nullptr);

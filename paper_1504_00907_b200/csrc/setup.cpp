@@ -169,7 +169,7 @@ static void free_ctx(ddg_ctx* c) {
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
                     c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
-                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab, c->d_bc};
+                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab, c->d_bc, c->d_res, c->d_xpart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -1072,6 +1072,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     if (const char* e = getenv("DDG_SMALL_KERNEL")) c->opts.small_kernel = atoi(e);
     if (const char* e = getenv("DDG_SYMV")) c->symv_mode = e[0] == 'c' ? 1 : 0;
     if (const char* e = getenv("DDG_RING_MIN_MB")) c->ring_min_bytes = atof(e) * 1e6;
+    if (const char* e = getenv("DDG_FLAT_COARSE")) c->flat_coarse = atoi(e) != 0;
     c->coarse_variant = c->opts.coarse_variant;
     if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
     if (c->opts.part2) {   // three levels
@@ -1158,6 +1159,16 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         (c->coarse_variant == 3 && (st = dalloc(&c->d_bc, std::max<int64_t>(1, c->nc))))) {
         free_ctx(c);
         return st;
+    }
+    if (c->dist) c->flat_coarse = false;
+    if (c->flat_coarse) {
+        std::vector<int32_t> xp(n);
+        for (int I = 0; I < nparts; ++I)
+            for (int64_t x = c->bptr[I]; x < c->bptr[I + 1]; ++x) xp[x] = I;
+        if ((st = dalloc(&c->d_res, n)) || (st = upload(&c->d_xpart, xp))) {
+            free_ctx(c);
+            return st;
+        }
     }
     if (cudaMemsetAsync(c->d_s, 0, c->s_doubles * 8, c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->d_ticket, 0, sizeof(unsigned), c->stream) != cudaSuccess ||
@@ -1335,8 +1346,15 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
     const bool multi = c->dist && c->nranks > 1;
     prof(c, PC_COARSE, 0, [&] {
         if (multi) cudaMemsetAsync(bc, 0, c->nc * sizeof(double), c->stream);
-        launch_coarse_restrict(c->stream, c->n_restrict, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
-                               c->A, r, z, bc, c->maxmI, done, c->d_restrict_parts);
+        if (c->flat_coarse) {   // residual in part order at streaming speed, then Q_I^T res per part
+            launch_gather_flat(c->stream, 0, c->n, c->d_bidx, c->A, r, z, c->d_res, false, done);
+            launch_restrict_dot(c->stream, c->nparts, c->d_bptr, c->d_cptr, c->d_qoff, c->d_Q, c->d_res, bc,
+                                c->maxmI, done);
+            c->launches += 1;
+        } else {
+            launch_coarse_restrict(c->stream, c->n_restrict, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
+                                   c->A, r, z, bc, c->maxmI, done, c->d_restrict_parts);
+        }
         if (multi) comm_check(c, comm_allreduce_sum(c->comm, bc, bc, c->nc, c->stream));
         if (c->coarse_variant == 3) {
             // three levels: y_c = M_2 b_c, one V-cycle of the two-level method on A_c
@@ -1363,8 +1381,12 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
                         c->d_yc, c->d_partials, done, c->coarse_rows_t, c->d_tickets);
             c->launches += 1;
         }
-        launch_prolong(c->stream, c->n_prolong, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc, z, c->maxmI,
-                       done, c->d_prolong_parts);
+        if (c->flat_coarse)
+            launch_prolong_flat(c->stream, c->n, c->d_xpart, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
+                                c->d_yc, z, done);
+        else
+            launch_prolong(c->stream, c->n_prolong, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q, c->d_yc, z,
+                           c->maxmI, done, c->d_prolong_parts);
     });
     c->launches += 2;
 }
