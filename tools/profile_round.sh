@@ -1,6 +1,7 @@
 # round profile: bench lines for every config, per-solve launch lists, C2 bench launch list,
 # full ncu captures of k_symv_ring (C2), k_symv_ring2 (C3), k_coarse_dataflow (C2), k_gjb_gemm (C4 setup)
 set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_round.log 2>&1
 timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
 for c in C3 C5 C4 C1; do
   timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
