@@ -181,6 +181,8 @@ struct GJBatch {
     const int32_t* nK;
     const int32_t* ids;
     int32_t* err;
+    double* strip;          // symmetric variant: the new row panel of matrix b at strip + b * strip_stride
+    int64_t strip_stride;   // (tile (t, J) of the panel at ((J * GJB_BT + t) * TILE_ELEMS)); nullptr: full
 };
 
 // P = inverse of the pivot block [k0, k0 + nb) (tile exchange inside the block)
@@ -224,6 +226,14 @@ __global__ void __launch_bounds__(256) k_gjb_pivot(GJBatch bt, int k0) {
 // mode 2 (col panel):  C(I, kb) = C(I, kb) P            for tile rows I outside kb
 // CTA: a 4 x 4-tile (128 x 128) output block; thread: 8 x 8 elements.
 // grid.x: output blocks of one matrix (by 4-tile rows and columns), grid.y: batch
+// Symmetric variant (bt.strip set, reading R22 in DESIGN.md): the exchange keeps
+// M(X,Y) = s M(Y,X)^T with s = -1 when exactly one of X, Y is pivoted, so only
+// the block-lower tiles (4-tile blocks, diagonal blocks whole) are updated and
+// an upper operand tile is read transposed from its mirror.  The new row
+// panel goes to a strip first (mode 1 still needs the old one), and mode 2
+// copies its block-lower part back.  The same exact algorithm for half the
+// trailing flops; the pivot block's inverse is not bitwise symmetric, so the
+// stored tiles agree with the full variant's to rounding.
 __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) {
     extern __shared__ double gsm[];
     double* As = gsm;                               // [TILE][GJB_N]   A(row, kk), kk-major
@@ -245,6 +255,23 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
     }
     const int i0 = bi * GJB_BT, j0 = bj * GJB_BT;
     auto in_kb = [&](int t) { return t >= k0 && t < k1; };
+    const bool sym = bt.strip != nullptr;
+    const int bk = k0 / GJB_BT;
+    double* strip = sym ? bt.strip + (int64_t)b * bt.strip_stride : nullptr;
+    auto stile = [&](int t, int J) { return strip + ((int64_t)J * GJB_BT + t) * TILE_ELEMS; };
+    if (sym && mode == 1 && bi < bj) return;                     // block-upper: implied by symmetry
+    if (sym && mode == 2 && bi <= bk) {
+        // the new row panel's block-lower tiles (kb, J), J in block bi, back from the strip
+        for (int J = i0; J < min(i0 + GJB_BT, nT); ++J) {
+            if (in_kb(J)) continue;
+            for (int t = 0; t < k1 - k0; ++t) {
+                const double* src = stile(t, J);
+                double* dst = bt.mats[b] + ((int64_t)J * nT + k0 + t) * TILE_ELEMS;
+                for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) dst[e] = src[e];
+            }
+        }
+        if (bi < bk) return;
+    }
     // does this block own any output tile?
     {
         bool any = false;
@@ -273,13 +300,24 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
             const int ti = e / TILE_ELEMS, o = e % TILE_ELEMS;   // o = kk * 32 + r
             const int I = (mode == 0 ? k0 : i0) + ti;
             const int kk = o / TILE, r = o % TILE;
-            As[kk * GJB_N + ti * TILE + r] = (I < nT && (mode != 0 || I < k1)) ? tile(I, q)[o] : 0.0;
+            double v = 0.0;
+            if (I < nT && (mode != 0 || I < k1)) {
+                if (sym && mode == 1 && I / GJB_BT < bk) v = -tile(q, I)[r * TILE + kk];   // pivoted row: s = -1
+                else v = tile(I, q)[o];
+            }
+            As[kk * GJB_N + ti * TILE + r] = v;
         }
         for (int e = threadIdx.x; e < GJB_BT * TILE_ELEMS; e += 256) {
             const int tj = e / TILE_ELEMS, o = e % TILE_ELEMS;   // o = c * 32 + kk
             const int J = (mode == 2 ? k0 : j0) + tj;
             const int c = o / TILE, kk = o % TILE;
-            Bs[kk * GJB_BPAD + tj * TILE + c] = (J < nT && (mode != 2 || J < k1)) ? tile(q, J)[o] : 0.0;
+            double v = 0.0;
+            if (J < nT && (mode != 2 || J < k1)) {
+                if (sym && mode == 1) v = stile(q - k0, J)[o];                           // the new row panel
+                else if (sym && mode == 0 && J / GJB_BT > bk) v = tile(J, q)[kk * TILE + c];   // both unpivoted
+                else v = tile(q, J)[o];
+            }
+            Bs[kk * GJB_BPAD + tj * TILE + c] = v;
         }
         __syncthreads();
 #pragma unroll 4
@@ -312,7 +350,7 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
         const bool ok = mode == 0 ? (in_kb(I) && !in_kb(J)) : mode == 1 ? (!in_kb(I) && !in_kb(J))
                                                                          : (!in_kb(I) && in_kb(J));
         if (!ok) continue;
-        double* T = tile(I, J);
+        double* T = sym && mode == 0 ? stile(I - k0, J) : tile(I, J);
 #pragma unroll
         for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -400,7 +438,8 @@ __global__ void k_front_extend_add(const int32_t* __restrict__ child, const Fron
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int a = (int)(e % c.nB), b = (int)(e / c.nB);
-        Fp[tix(p.nT, mp[a], mp[b])] += Fc[tix(c.nT, c.nSp + a, c.nSp + b)];
+        // the Schur block is symmetric and only its lower part is kept (R22)
+        Fp[tix(p.nT, mp[a], mp[b])] += Fc[tix(c.nT, c.nSp + max(a, b), c.nSp + min(a, b))];
     }
 }
 
@@ -472,14 +511,23 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
         cudaFuncSetAttribute(k_gjb_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);
         init = true;
     }
-    GJBatch bt{mats, nT, nK, ids, err};
+    GJBatch bt{mats, nT, nK, ids, err, nullptr, 0};
     const int nb = (maxT + GJB_BT - 1) / GJB_BT;
+    // symmetric variant: a row-panel strip per matrix (DDG_GJ_SYM=0: full exchange)
+    const bool want_sym = !getenv("DDG_GJ_SYM") || atoi(getenv("DDG_GJ_SYM")) != 0;
+    const int64_t stride = (int64_t)GJB_BT * maxT * TILE_ELEMS;
+    if (want_sym && cudaMallocAsync(&bt.strip, (size_t)nmat * stride * sizeof(double), st) == cudaSuccess)
+        bt.strip_stride = stride;
+    else
+        bt.strip = nullptr;
+    cudaGetLastError();
     for (int k0 = 0; k0 < maxK; k0 += GJB_BT) {
         k_gjb_pivot<<<nmat, 256, smem_p, st>>>(bt, k0);
         k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 0);
         k_gjb_gemm<<<dim3(nb * nb, nmat), 256, smem_g, st>>>(bt, k0, 1);
         k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 2);
     }
+    if (bt.strip) cudaFreeAsync(bt.strip, st);
 }
 
 void launch_scatter_coarse(cudaStream_t st, int64_t nent, const int32_t* row, const int32_t* col,

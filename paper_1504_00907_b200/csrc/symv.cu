@@ -879,32 +879,39 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
 }
 
 // Sum the partial segments of multi-item operators for one row block, in
-// fixed item order, and apply the result.
+// fixed item order, and apply the result.  The block's segment offsets are
+// staged in shared memory first, and each row's index and z value are
+// fetched before its partial sums, so no load waits on a descriptor.
 __global__ void k_symv_reduce(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
                               const RedDesc* __restrict__ red, int red_begin,
                               const int32_t* __restrict__ oidx, const double* __restrict__ partials,
                               double* __restrict__ z, double* __restrict__ y_out,
                               const int32_t* done) {
     if (*done) return;
+    __shared__ int64_t off[64];
     const RedDesc rd = red[red_begin + blockIdx.x];
     const OpDesc op = ops[rd.op];
-    const int b = rd.b;
+    const int b = rd.b, nblk = op.nblk;
+    auto seg = [&](int j) -> int64_t {
+        if (j <= b) return items[op.item_base + b * (b + 1) / 2 + j].part_off;   // items (b, j): row segments
+        const ItemDesc it = items[op.item_base + j * (j + 1) / 2 + b];           // items (j, b): column segments
+        return it.part_off + (int64_t)(it.I1 - it.I0) * TILE;
+    };
+    for (int j = threadIdx.x; j < min(nblk, 64); j += blockDim.x) off[j] = seg(j);
+    __syncthreads();
     const int rows_b = (min(op.nT, (b + 1) * op.BT) - b * op.BT) * TILE;
     for (int x = threadIdx.x; x < rows_b; x += blockDim.x) {
         const int g = b * op.BT * TILE + x;
+        const bool ok = g < op.m;
+        const bool scat = ok && op.out_mode == 0;
+        const int ix = scat ? oidx[op.idx_off + g] : 0;
+        const double zv = scat ? z[ix] : 0.0;
         double y = 0.0;
-        for (int j = 0; j <= b; ++j) {                       // items (b, j): row segments
-            const ItemDesc& it = items[op.item_base + b * (b + 1) / 2 + j];
-            y += partials[it.part_off + x];
-        }
-        for (int i = b + 1; i < op.nblk; ++i) {              // items (i, b): col segments
-            const ItemDesc& it = items[op.item_base + i * (i + 1) / 2 + b];
-            y += partials[it.part_off + (it.I1 - it.I0) * TILE + x];
-        }
-        if (g < op.m) {
-            if (op.out_mode == 0) z[oidx[op.idx_off + g]] += y;
-            else y_out[g] = y;
-        }
+#pragma unroll 8
+        for (int j = 0; j < min(nblk, 64); ++j) y += partials[off[j] + x];
+        for (int j = 64; j < nblk; ++j) y += partials[seg(j) + x];     // very large dense operators
+        if (scat) z[ix] = zv + y;
+        else if (ok) y_out[g] = y;
     }
 }
 

@@ -427,3 +427,22 @@ def test_caller_colouring_rejected():
     with pytest.raises(DDGError) as e:
         _solver(pr, colour=col)
     assert e.value.code == 6
+
+
+@pytest.mark.parametrize("name,kw", [("poisson3d_24_b8_p2", {}), ("elasticity_8_be4", {}),
+                                     ("lognormal_16_b4", {"coarse_variant": 2}),
+                                     ("C1", {"coarse_variant": 1})])
+def test_symmetric_gauss_jordan_bitwise(name, kw, monkeypatch):
+    """The symmetric blocked Gauss-Jordan (reading R22: block-lower tiles only,
+    upper operands read transposed with the exchange's sign) is the same exact
+    algorithm as the full exchange; the pivot block's inverse is not bitwise
+    symmetric, so the two agree to rounding (and each matches the oracle)."""
+    pr = CASES[name]()
+    monkeypatch.setenv("DDG_GJ_SYM", "0")
+    u0, it0, h0, _ = _solver(pr, **kw).solve(pr.f, 1e-8)
+    monkeypatch.setenv("DDG_GJ_SYM", "1")
+    u1, it1, h1, _ = _solver(pr, **kw).solve(pr.f, 1e-8)
+    assert abs(it0 - it1) <= 1
+    assert np.linalg.norm(u1 - u0) <= 1e-11 * np.linalg.norm(u0)
+    m = min(len(h0), len(h1))
+    assert (np.abs(h1[:m] - h0[:m]) / h0[:m]).max() <= 1e-9
