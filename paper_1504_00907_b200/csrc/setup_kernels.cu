@@ -234,10 +234,17 @@ __global__ void __launch_bounds__(256) k_gjb_pivot(GJBatch bt, int k0) {
 // copies its block-lower part back.  The same exact algorithm for half the
 // trailing flops; the pivot block's inverse is not bitwise symmetric, so the
 // stored tiles agree with the full variant's to rounding.
+// MMA: the 128 x 128 block product on the fp64 tensor path (mma.sync m8n8k4,
+// each warp a 32 x 64 tile of 4 x 8 fragments): the fragments are read from
+// shared memory once per 4-deep k step instead of per FMA, which is what
+// bounds the FMA variant (16 B of operands per 8 FMAs).
+constexpr int GJB_LDM = GJB_N + 8;         // MMA stage row: conflict-free 8 x 4 fragment loads
+template <bool MMA>
 __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) {
+    constexpr int LDA = MMA ? GJB_LDM : GJB_N, LDB = MMA ? GJB_LDM : GJB_BPAD;
     extern __shared__ double gsm[];
-    double* As = gsm;                               // [TILE][GJB_N]   A(row, kk), kk-major
-    double* Bs = gsm + TILE * GJB_N;                // [TILE][GJB_BPAD] B(kk, col), kk-major
+    double* As = gsm;                               // [TILE][LDA] A(row, kk), kk-major
+    double* Bs = gsm + TILE * LDA;                  // [TILE][LDB] B(kk, col), kk-major
     const int b = blockIdx.y;
     const int nT = bt.nT[b], nK = bt.nK[b];
     if (k0 >= nK) return;
@@ -288,6 +295,8 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
     const int tr = (threadIdx.x >> 4) * 8;          // output rows tr..tr+7 (one tile row)
     const int tc = (threadIdx.x & 15) * 2;          // output cols 32 m + tc, +1 (m = 0..3): consecutive
                                                     // lanes read consecutive 16 B of a B row
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int wr = (wid & 3) * 32, wc = (wid >> 2) * 64;   // MMA: this warp's 32 x 64 output tile
     double acc[8][8];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -305,7 +314,7 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
                 if (sym && mode == 1 && I / GJB_BT < bk) v = -tile(q, I)[r * TILE + kk];   // pivoted row: s = -1
                 else v = tile(I, q)[o];
             }
-            As[kk * GJB_N + ti * TILE + r] = v;
+            As[kk * LDA + ti * TILE + r] = v;
         }
         for (int e = threadIdx.x; e < GJB_BT * TILE_ELEMS; e += 256) {
             const int tj = e / TILE_ELEMS, o = e % TILE_ELEMS;   // o = c * 32 + kk
@@ -317,14 +326,35 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
                 else if (sym && mode == 0 && J / GJB_BT > bk) v = tile(J, q)[kk * TILE + c];   // both unpivoted
                 else v = tile(q, J)[o];
             }
-            Bs[kk * GJB_BPAD + tj * TILE + c] = v;
+            Bs[kk * LDB + tj * TILE + c] = v;
         }
         __syncthreads();
+        if constexpr (MMA) {
+            // value v = 16 mi + 2 ni + h of acc (acc[v / 8][v % 8]) is
+            // C(wr + 8 mi + lane / 4, wc + 8 ni + 2 (lane % 4) + h)
+#pragma unroll 2
+            for (int kq = 0; kq < TILE; kq += 4) {
+                double af[4], bf[8];
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi) af[mi] = As[(kq + (lane & 3)) * LDA + wr + 8 * mi + (lane >> 2)];
+#pragma unroll
+                for (int ni = 0; ni < 8; ++ni) bf[ni] = Bs[(kq + (lane & 3)) * LDB + wc + 8 * ni + (lane >> 2)];
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 8; ++ni)
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                     : "+d"(acc[2 * mi + ni / 4][(2 * ni) % 8]), "+d"(acc[2 * mi + ni / 4][(2 * ni) % 8 + 1])
+                                     : "d"(af[mi]), "d"(bf[ni]));
+            }
+            __syncthreads();
+            continue;
+        }
 #pragma unroll 4
         for (int kk = 0; kk < TILE; ++kk) {
             double a[8], bv[8];
-            const double2* ap = reinterpret_cast<const double2*>(As + kk * GJB_N + tr);
-            const double* brow = Bs + kk * GJB_BPAD + tc;
+            const double2* ap = reinterpret_cast<const double2*>(As + kk * LDA + tr);
+            const double* brow = Bs + kk * LDB + tc;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const double2 x = ap[u], y = *reinterpret_cast<const double2*>(brow + u * TILE);
@@ -337,6 +367,31 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
                 for (int c = 0; c < 8; ++c) acc[r][c] = fma(a[r], bv[c], acc[r][c]);
         }
         __syncthreads();
+    }
+    if constexpr (MMA) {
+        // rows wr + 8 mi + lane / 4 lie in tile row i0 + wr / 32; columns
+        // wc + 8 ni + 2 (lane % 4) + h in tile column j0 + (wc + 8 ni) / 32
+        const int I = i0 + wr / TILE;
+        if (I >= nT) return;
+#pragma unroll
+        for (int ni = 0; ni < 8; ++ni) {
+            const int J = j0 + (wc + 8 * ni) / TILE;
+            if (J >= nT) continue;
+            const bool ok = mode == 0 ? (in_kb(I) && !in_kb(J)) : mode == 1 ? (!in_kb(I) && !in_kb(J))
+                                                                             : (!in_kb(I) && in_kb(J));
+            if (!ok) continue;
+            double* T = sym && mode == 0 ? stile(I - k0, J) : tile(I, J);
+            const int cc = (wc + 8 * ni) % TILE + 2 * (lane & 3);
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    double* p = T + (cc + h) * TILE + 8 * mi + (lane >> 2);
+                    const double v = acc[2 * mi + ni / 4][(2 * ni) % 8 + h];
+                    *p = mode == 1 ? *p + v : (mode == 0 ? -v : v);
+                }
+        }
+        return;
     }
     // epilogue: rows tr..tr+7 lie in tile row I; columns 2u, 2u+1 of acc are
     // columns tc, tc+1 of tile column j0 + u
@@ -506,9 +561,11 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
     bool& init = init_dev[dev_ & 63];
     const int smem_p = 9 * TILE_ELEMS * sizeof(double);
     const int smem_g = (TILE * GJB_N + TILE * GJB_BPAD) * sizeof(double);
+    const int smem_m = 2 * TILE * GJB_LDM * sizeof(double);
     if (!init) {
         cudaFuncSetAttribute(k_gjb_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p);
-        cudaFuncSetAttribute(k_gjb_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);
+        cudaFuncSetAttribute(k_gjb_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);
+        cudaFuncSetAttribute(k_gjb_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_m);
         init = true;
     }
     GJBatch bt{mats, nT, nK, ids, err, nullptr, 0};
@@ -521,11 +578,18 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
     else
         bt.strip = nullptr;
     cudaGetLastError();
+    const bool use_mma = !getenv("DDG_GJ_MMA") || atoi(getenv("DDG_GJ_MMA")) != 0;   // experiment switch
     for (int k0 = 0; k0 < maxK; k0 += GJB_BT) {
         k_gjb_pivot<<<nmat, 256, smem_p, st>>>(bt, k0);
-        k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 0);
-        k_gjb_gemm<<<dim3(nb * nb, nmat), 256, smem_g, st>>>(bt, k0, 1);
-        k_gjb_gemm<<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 2);
+        if (use_mma) {
+            k_gjb_gemm<true><<<dim3(nb, nmat), 256, smem_m, st>>>(bt, k0, 0);
+            k_gjb_gemm<true><<<dim3(nb * nb, nmat), 256, smem_m, st>>>(bt, k0, 1);
+            k_gjb_gemm<true><<<dim3(nb, nmat), 256, smem_m, st>>>(bt, k0, 2);
+        } else {
+            k_gjb_gemm<false><<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 0);
+            k_gjb_gemm<false><<<dim3(nb * nb, nmat), 256, smem_g, st>>>(bt, k0, 1);
+            k_gjb_gemm<false><<<dim3(nb, nmat), 256, smem_g, st>>>(bt, k0, 2);
+        }
     }
     if (bt.strip) cudaFreeAsync(bt.strip, st);
 }
