@@ -117,6 +117,7 @@ struct ddg_ctx {
     bool flat_coarse = true;           // two-stage restriction + flat prolongation (single GPU)
     double* d_res = nullptr;           // r - A z in part order (flat restriction)
     int32_t* d_xpart = nullptr;        // part of every position of the part order
+    int32_t *d_brp = nullptr, *d_bcol = nullptr;   // node-blocked columns of A (DevCSR::bs)
     struct ddg_ctx* child = nullptr;   // three levels: the two-level method on A_c
     double* d_bc = nullptr;            // three levels: coarse right-hand side R_0 (r - A z)
     SparseCoarse* sparse = nullptr;

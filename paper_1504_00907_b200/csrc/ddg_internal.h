@@ -137,8 +137,15 @@ struct DevCSR {
     const int32_t* col;
     const double* val;
     int32_t sw;          // lanes per row in the row kernels (1, 4, 8 or 32; by mean row length)
-    int32_t pad;
+    int32_t bs;          // 3 or 4: node-blocked columns (bcol/brp below), else 0 (col[] per entry)
     DevStencil st;       // st.kind != 0: rows evaluated matrix-free (sw = 1)
+    // Node-blocked column indices: every row of block-row V = v / bs holds the
+    // same full, aligned bs-column blocks, so entry j of row v sits in column
+    // bcol[brp[V] + j / bs] * bs + j % bs.  val[] keeps the CSR order, so the
+    // row sums are bitwise those of the CSR; only the index traffic shrinks
+    // (4 B per block per block-row instead of 4 B per entry).
+    const int32_t* bcol;
+    const int32_t* brp;
 };
 
 struct ColourPlan {

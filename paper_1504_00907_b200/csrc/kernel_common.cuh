@@ -77,9 +77,24 @@ __device__ __forceinline__ double stencil_dot(const DevStencil& st, int64_t v, c
     return s;
 }
 
+// lane sl of SW: its entries e = rp[v] + sl, + SW, ... in order (node-blocked columns)
+template <int BS, int SW>
+__device__ __forceinline__ double row_dot_nb(const DevCSR& A, int64_t v, const double* __restrict__ x, int sl) {
+    const int e0 = A.rp[v], e1 = A.rp[v + 1];
+    const int32_t* bc = A.bcol + A.brp[v / BS];
+    double s = 0.0;
+    for (int e = e0 + sl; e < e1; e += SW) {
+        const int j = e - e0;
+        s += A.val[e] * x[bc[j / BS] * BS + j % BS];
+    }
+    return s;
+}
+
 // (A x)[v] by one thread: stencil or CSR row
 __device__ __forceinline__ double row_dot1(const DevCSR& A, int64_t v, const double* __restrict__ x) {
     if (A.st.kind) return stencil_dot(A.st, v, x);
+    if (A.bs == 3) return row_dot_nb<3, 1>(A, v, x, 0);
+    if (A.bs == 4) return row_dot_nb<4, 1>(A, v, x, 0);
     double s = 0.0;
     for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * x[A.col[e]];
     return s;
@@ -102,8 +117,14 @@ __device__ __forceinline__ double row_dot(const DevCSR& A, int64_t v, bool valid
     double s = 0.0;
     if (SW == 1) return valid ? row_dot1(A, v, x) : 0.0;
     if (valid) {
-        const int e1 = A.rp[v + 1];
-        for (int e = A.rp[v] + sl; e < e1; e += SW) s += A.val[e] * x[A.col[e]];
+        if (A.bs == 3) {
+            s = row_dot_nb<3, SW>(A, v, x, sl);
+        } else if (A.bs == 4) {
+            s = row_dot_nb<4, SW>(A, v, x, sl);
+        } else {
+            const int e1 = A.rp[v + 1];
+            for (int e = A.rp[v] + sl; e < e1; e += SW) s += A.val[e] * x[A.col[e]];
+        }
     }
 #pragma unroll
     for (int o = SW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);

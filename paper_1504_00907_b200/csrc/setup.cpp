@@ -169,7 +169,7 @@ static void free_ctx(ddg_ctx* c) {
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
                     c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
-                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab, c->d_bc, c->d_res, c->d_xpart};
+                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab, c->d_bc, c->d_res, c->d_xpart, c->d_brp, c->d_bcol};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -951,6 +951,34 @@ static int build_child(ddg_ctx* c, const double* F, const std::vector<int32_t>& 
     return DDG_OK;
 }
 
+// Node-blocked column structure (DevCSR::bs): n % bs == 0 and the bs rows of
+// every block-row share one column list made of whole aligned bs-blocks.
+static bool node_blocks(int64_t n, const int64_t* rp, const int32_t* col, int bs, std::vector<int32_t>& brp,
+                        std::vector<int32_t>& bcol) {
+    if (n % bs) return false;
+    const int64_t nbr = n / bs;
+    brp.assign(nbr + 1, 0);
+    bcol.clear();
+    for (int64_t V = 0; V < nbr; ++V) {
+        const int64_t v0 = V * bs;
+        const int64_t len = rp[v0 + 1] - rp[v0];
+        if (len % bs) return false;
+        for (int64_t j = 0; j < len; j += bs) {
+            const int32_t c0 = col[rp[v0] + j];
+            if (c0 % bs) return false;
+            bcol.push_back(c0 / bs);
+        }
+        for (int r = 0; r < bs; ++r) {
+            const int64_t v = v0 + r;
+            if (rp[v + 1] - rp[v] != len) return false;
+            for (int64_t j = 0; j < len; ++j)
+                if (col[rp[v] + j] != bcol[brp[V] + j / bs] * bs + (int32_t)(j % bs)) return false;
+        }
+        brp[V + 1] = (int32_t)bcol.size();
+    }
+    return true;
+}
+
 template <typename T>
 static int upload_s(cudaStream_t s, T** d, const std::vector<T>& h) {
     int st = dalloc(d, h.size());
@@ -1133,7 +1161,19 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         if (const char* e = getenv("DDG_ROW_SW")) sw = atoi(e);   // experiment: lanes per CSR row
         if (sw != 1 && sw != 4 && sw != 8 && sw != 32) sw = 8;
         if (ds.kind) sw = 1;
-        c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val, sw, 0, ds};
+        c->A = DevCSR{n, c->nnz, c->d_rp, c->d_col, c->d_val, sw, 0, ds, nullptr, nullptr};
+        if (!ds.kind && !getenv("DDG_NO_NODE_BLOCKS")) {
+            // node-blocked columns (C4's 3 DoFs per node, a three-level child's k per part)
+            for (int bs : {4, 3}) {
+                std::vector<int32_t> brp, bcol;
+                if (!node_blocks(n, row_ptr, col, bs, brp, bcol)) continue;
+                if ((st = upload(&c->d_brp, brp)) || (st = upload(&c->d_bcol, bcol))) { free_ctx(c); return st; }
+                c->A.bs = bs;
+                c->A.brp = c->d_brp;
+                c->A.bcol = c->d_bcol;
+                break;
+            }
+        }
         c->opts.stencil = nullptr;   // borrowed for the duration of ddg_setup only
     }
     {   // s position -> fine row (padding -1), for the flat colour gather

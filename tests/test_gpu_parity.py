@@ -446,3 +446,27 @@ def test_symmetric_gauss_jordan_bitwise(name, kw, monkeypatch):
     assert np.linalg.norm(u1 - u0) <= 1e-11 * np.linalg.norm(u0)
     m = min(len(h0), len(h1))
     assert (np.abs(h1[:m] - h0[:m]) / h0[:m]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["elasticity_8_be4", "three_level_child"])
+def test_node_blocked_rows_match_csr_bitwise(name, monkeypatch):
+    """Node-blocked column indices (C4's 3 DoFs per node; a three-level
+    child's k unknowns per part) keep val[] in CSR order and each lane's
+    entries in the same order, so the solve is bitwise the CSR one."""
+    from paper_1504_00907_b200 import Solver
+    if name == "three_level_child":
+        pr = P.poisson3d(24, 4, 1, 1002)
+        p2, n2 = P.coarse_parts(pr, 2)
+        kw = dict(part2=p2, nparts2=n2)
+    else:
+        pr = CASES[name]()
+        kw = {}
+    out = []
+    for off in ("1", None):
+        if off:
+            monkeypatch.setenv("DDG_NO_NODE_BLOCKS", off)
+        else:
+            monkeypatch.delenv("DDG_NO_NODE_BLOCKS", raising=False)
+        out.append(Solver.from_problem(pr, **kw).solve(pr.f, 1e-8))
+    (u0, it0, h0, _), (u1, it1, h1, _) = out
+    assert it0 == it1 and np.array_equal(u0, u1) and np.array_equal(h0, h1)
