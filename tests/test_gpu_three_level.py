@@ -138,3 +138,30 @@ def test_three_level_errors():
         Solver.from_problem(pr, part2=np.full(pr.nparts, 5, np.int32), nparts2=2)
     with pytest.raises(DDGError, match="empty"):
         Solver.from_problem(pr, part2=np.zeros(pr.nparts, np.int32), nparts2=2)
+
+
+def test_three_level_full_c3():
+    """BASELINE C3 at full size with the three-level method as bench.py times
+    it (--levels 3 --factor 2): convergence, the true residual, symmetry and
+    positivity of M_3 and M_3 <= M_2 on a random vector (derived in
+    tests/test_oracle_three_level.py)."""
+    import scipy.sparse as sp
+    from paper_1504_00907_b200 import Solver
+    pr = P.make("C3")
+    p2, n2, bc2 = P.coarse_parts(pr, 2, coords=True)
+    s3 = Solver.from_problem(pr, part2=p2, nparts2=n2, block_coords2=bc2)
+    assert s3.info.levels == 3 and s3.info.nparts2 == n2
+    u, it, hist, rep = s3.solve(pr.f, 1e-8)
+    assert rep.converged and it <= 12, it
+    A = sp.csr_matrix((pr.val, pr.col, pr.row_ptr), shape=(pr.n, pr.n))
+    assert np.linalg.norm(pr.f - A @ u) <= 1e-7 * np.linalg.norm(pr.f)
+    assert abs(rep.true_res - np.linalg.norm(pr.f - A @ u)) <= 1e-3 * rep.true_res
+    rs = np.random.default_rng(8)
+    x, y = rs.standard_normal(pr.n), rs.standard_normal(pr.n)
+    Mx, My = s3.apply_precond(x), s3.apply_precond(y)
+    assert abs(x @ My - y @ Mx) <= 1e-11 * np.linalg.norm(x) * np.linalg.norm(My)
+    assert x @ Mx > 0
+    s3.close()
+    s2 = Solver.from_problem(pr)
+    assert x @ Mx <= (x @ s2.apply_precond(x)) * (1 + 1e-10)
+    s2.close()
