@@ -113,7 +113,9 @@ typedef struct {
        for the duration of ddg_setup.  block_coords2: optional nparts2 x
        block_ndim coordinates of the second-level parts.  coarse_variant then
        selects the second level's coarse solve (0 auto, 1 dense, 2 sparse).
-       Single GPU only. */
+       With opts.comm the second level is distributed over the same ranks
+       (its parts by block_coords2 boxes) and only its coarse factor is
+       replicated; y_c is assembled on every rank by one allreduce. */
     const int32_t* part2;
     int32_t nparts2;
     const int32_t* block_coords2;

@@ -231,7 +231,10 @@ __global__ void k_halo_unpack(const double* __restrict__ buf, const int32_t* __r
 __global__ void k_copy_rows(const double* __restrict__ in, double* __restrict__ out,
                             const int32_t* __restrict__ rows, int64_t nrows) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x)
-        out[rows[i]] = in[rows[i]];
+    {
+        const int64_t v = rows ? (int64_t)rows[i] : i;   // rows == nullptr: every row (one rank)
+        out[v] = in[v];
+    }
 }
 
 __global__ void k_fill(double* x, int64_t n, double v, const int32_t* done) {

@@ -938,7 +938,7 @@ static int build_child(ddg_ctx* c, const double* F, const std::vector<int32_t>& 
     });
     ddg_opts o = c->opts;
     o.stream = c->stream;
-    o.comm = nullptr;
+    o.comm = c->opts.comm;     // multi-GPU: the second level is distributed over the same ranks
     o.stencil = nullptr;
     o.part2 = nullptr;
     o.nparts2 = 0;
@@ -1104,7 +1104,6 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     c->coarse_variant = c->opts.coarse_variant;
     if (c->coarse_variant == 0) c->coarse_variant = c->nc <= 8192 ? 1 : 2;
     if (c->opts.part2) {   // three levels
-        if (c->dist) { free_ctx(c); return set_err(DDG_E_ARG, "three levels: single GPU only"); }
         if (c->opts.nparts2 < 2) {
             int np2 = c->opts.nparts2;
             free_ctx(c);
@@ -1399,8 +1398,18 @@ static void coarse_add(ddg_ctx* c, const double* r, double* z, const int32_t* do
         if (c->coarse_variant == 3) {
             // three levels: y_c = M_2 b_c, one V-cycle of the two-level method on A_c
             const int64_t l0 = c->child->launches;
-            enqueue_precond(c->child, bc, c->d_yc, done);
-            c->launches += c->child->launches - l0;
+            ddg_ctx* ch = c->child;
+            enqueue_precond(ch, bc, c->d_yc, done);
+            if (c->dist) {
+                // each rank holds y_c on the second level's rows it owns (and halos):
+                // assemble it everywhere for this rank's prolongation
+                launch_fill(c->stream, ch->d_q, ch->n, 0.0, done);
+                launch_copy_rows(c->stream, c->d_yc, ch->d_q, ch->d_rows, ch->nrows);
+                comm_check(c, comm_allreduce_sum(c->comm, ch->d_q, c->d_yc, ch->n, c->stream));
+                c->comm_err |= ch->comm_err;
+                ch->launches += 2;
+            }
+            c->launches += ch->launches - l0;
         } else if (c->coarse_variant == 2) {
             c->launches += sparse_coarse_enqueue_solve(c, c->d_yc, done);
         } else if (ring_ok(c, c->coarse_ring_off)) {

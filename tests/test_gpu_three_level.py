@@ -165,3 +165,22 @@ def test_three_level_full_c3():
     s2 = Solver.from_problem(pr)
     assert x @ Mx <= (x @ s2.apply_precond(x)) * (1 + 1e-10)
     s2.close()
+
+
+@pytest.mark.parametrize("name", ["C1_f2", "lognormal_16_b4", "poisson3d_24_b4_p1"])
+def test_three_level_comm_path_single_rank(name):
+    """The distributed three-level path (SURVEY.md §8(f) f2 by the paper's own
+    route: the second level is a two-level method distributed over the same
+    ranks, only the small A_1 factor replicated) at one NCCL rank: split
+    reductions, halo plans and the y_c assembly run, and match the oracle."""
+    from paper_1504_00907_b200 import Solver, ddg
+    mk, f = CASES[name]
+    pr = mk()
+    p2, n2, bc2 = P.coarse_parts(pr, f, coords=True)
+    comm = ddg.Comm(0, 1, ddg.unique_id(), 0)
+    s = Solver.from_problem(pr, comm=comm, part2=p2, nparts2=n2, block_coords2=bc2)
+    o = oracle.Oracle.from_problem(pr, part2=p2, nparts2=n2)
+    assert s.info.levels == 3
+    _check_solve(pr, s, o)
+    s.close()
+    comm.close()
