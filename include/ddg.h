@@ -10,7 +10,9 @@
  * PAPER.md:239-241) restricted to each non-overlapping part Omega_I and
  * orthonormalised per part is one basis function; the
  * coarse matrix is the Galerkin projection A_c = P^T A P (PAPER.md:266,
- * written A_0 = R_0 A R_0^T there; P = R_0^T).
+ * written A_0 = R_0 A R_0^T there; P = R_0^T).  Optionally the coarse solve
+ * is one application of the same two-level method built on A_c (the paper's
+ * three-level V-cycle; ddg_opts.part2).
  *
  * Everything below runs on one CUDA device per context.  All numerics are
  * IEEE fp64.  There is no CPU fallback: with no usable device every entry
