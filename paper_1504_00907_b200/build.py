@@ -17,7 +17,6 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def _nccl_dir():
-    import glob
     for p in sys.path + ["/opt/prime-rl/.venv/lib/python3.12/site-packages"]:
         cand = os.path.join(p, "nvidia", "nccl")
         if os.path.exists(os.path.join(cand, "include", "nccl.h")):

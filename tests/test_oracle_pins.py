@@ -17,8 +17,7 @@ import pytest
 
 import oracle
 from ddg_gen import problems as P
-from tests.helpers import (block_projectors_local, csr_from_dense, dense_two_level,
-                           graph_distance_sets, laplace1d)
+from tests.helpers import csr_from_dense, dense_two_level, graph_distance_sets, laplace1d
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
 
