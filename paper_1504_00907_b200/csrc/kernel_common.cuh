@@ -257,6 +257,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
+// Programmatic dependent launch along the colour-step chain (gather -> ring
+// -> reduce -> gather ...): the next kernel is launched while the previous
+// one drains, and waits in pdl_wait() for it to complete before reading.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+extern int g_pdl;   // 1: chain launches carry the programmatic-serialization attribute (DDG_PDL)
+template <typename... KArgs, typename... Args>
+static inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 static inline int vec_grid(int64_t n) {
     int64_t g = (n + VEC_THREADS - 1) / VEC_THREADS;
     return (int)(g < RED_BLOCKS ? (g > 0 ? g : 1) : RED_BLOCKS);

@@ -3,6 +3,7 @@
 #include "kernel_common.cuh"
 
 namespace ddg {
+int g_pdl = 1;
 // =============================================================================
 // Multiplicative Schwarz colour step
 // =============================================================================
@@ -12,6 +13,7 @@ template <int SW>
 __global__ void __launch_bounds__(256)
 k_gather_flat(int64_t x0, int64_t x1, const int32_t* __restrict__ gidx, DevCSR A, const double* __restrict__ r,
               const double* __restrict__ z, double* __restrict__ s, int z_is_zero, const int32_t* done) {
+    pdl_wait();
     if (*done) return;
     const int64_t ng = (int64_t)gridDim.x * blockDim.x / SW;
     const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / SW;
@@ -313,6 +315,7 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
             const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
             double* __restrict__ partials, const int32_t* done, int nst, int nb, int R, int Cr,
             unsigned long long* rtrace) {
+    pdl_wait();
     constexpr int SLOT = RT * TILE_ELEMS;
     // item buffers: s over R + Cr rows; partial rows: the row block replicated
     // per consumer warp ([8][R], every warp adds direct parts to any row) and
@@ -621,6 +624,7 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
              const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
              const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
              double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr) {
+    pdl_wait();
     constexpr int SLOT = RT * TILE_ELEMS;
     if (*done) return;
     extern __shared__ __align__(128) double rsm[];
@@ -887,6 +891,7 @@ __global__ void k_symv_reduce(const OpDesc* __restrict__ ops, const ItemDesc* __
                               const int32_t* __restrict__ oidx, const double* __restrict__ partials,
                               double* __restrict__ z, double* __restrict__ y_out,
                               const int32_t* done) {
+    pdl_wait();
     if (*done) return;
     __shared__ int64_t off[64];
     const RedDesc rd = red[red_begin + blockIdx.x];
@@ -926,10 +931,10 @@ void launch_gather_flat(cudaStream_t st, int64_t x0, int64_t x1, const int32_t* 
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * 8));
     const int zz = z_is_zero ? 1 : 0;
     switch (sw) {
-        case 4: k_gather_flat<4><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
-        case 8: k_gather_flat<8><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
-        case 32: k_gather_flat<32><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done); break;
-        default: k_gather_flat<1><<<g, 256, 0, st>>>(x0, x1, gidx, A, r, z, s, zz, done);
+        case 4: launch_pdl(k_gather_flat<4>, g, 256, 0, st, x0, x1, gidx, A, r, z, s, zz, done); break;
+        case 8: launch_pdl(k_gather_flat<8>, g, 256, 0, st, x0, x1, gidx, A, r, z, s, zz, done); break;
+        case 32: launch_pdl(k_gather_flat<32>, g, 256, 0, st, x0, x1, gidx, A, r, z, s, zz, done); break;
+        default: launch_pdl(k_gather_flat<1>, g, 256, 0, st, x0, x1, gidx, A, r, z, s, zz, done);
     }
 }
 
@@ -967,6 +972,7 @@ void symv_ring_init() {
     g_ring_nst = 0;
     if (const char* e = getenv("DDG_RING_NST")) g_ring_nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
     g_ring_v2 = getenv("DDG_RING_V2") ? atoi(getenv("DDG_RING_V2")) : -1;   // -1: auto
+    g_pdl = getenv("DDG_PDL") ? (atoi(getenv("DDG_PDL")) != 0) : 1;
 
     if (getenv("DDG_RING_TRACE") && !g_ring_trace) {
         if (cudaMalloc(&g_ring_trace, 32 * sizeof(unsigned long long)) == cudaSuccess)
@@ -1014,14 +1020,14 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
         while (nst2 < cap && ring2_smem(RT, nst2 + 1, nb2, maxr) <= budget) ++nst2;
         const size_t smem2 = ring2_smem(RT, nst2, nb2, maxr);
         if (RT == 2)
-            k_symv_ring2<2><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
-                                                                 y_out, partials, done, nst2, nb2, maxr);
+            launch_pdl(k_symv_ring2<2>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr);
         else if (RT == 8)
-            k_symv_ring2<8><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
-                                                                 y_out, partials, done, nst2, nb2, maxr);
+            launch_pdl(k_symv_ring2<8>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr);
         else
-            k_symv_ring2<4><<<ncta, RING2_THREADS, smem2, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z,
-                                                                 y_out, partials, done, nst2, nb2, maxr);
+            launch_pdl(k_symv_ring2<4>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr);
         return;
     }
     // item buffers: deep for small items (s copies and epilogues overlap
@@ -1033,21 +1039,21 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     while (nst < nst_cap && ring_smem(RT, nst + 1, nb, R, Cr) <= budget) ++nst;
     const size_t smem = ring_smem(RT, nst, nb, R, Cr);
     if (RT == 1)
-        k_symv_ring<1><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
+        launch_pdl(k_symv_ring<1>, ncta, RING_THREADS, smem, st, ops, items, item_begin, cta_part, tiles, s, oidx,
+                   z, y_out, partials, done, nst, nb, R, Cr, g_ring_trace);
     else if (RT == 2)
-        k_symv_ring<2><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
+        launch_pdl(k_symv_ring<2>, ncta, RING_THREADS, smem, st, ops, items, item_begin, cta_part, tiles, s, oidx,
+                   z, y_out, partials, done, nst, nb, R, Cr, g_ring_trace);
     else
-        k_symv_ring<4><<<ncta, RING_THREADS, smem, st>>>(ops, items, item_begin, cta_part, tiles, s, oidx, z, y_out,
-                                                         partials, done, nst, nb, R, Cr, g_ring_trace);
+        launch_pdl(k_symv_ring<4>, ncta, RING_THREADS, smem, st, ops, items, item_begin, cta_part, tiles, s, oidx,
+                   z, y_out, partials, done, nst, nb, R, Cr, g_ring_trace);
 }
 
 void launch_symv_reduce(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
                         const RedDesc* red, int red_begin, int nred, const int32_t* oidx,
                         const double* partials, double* z, double* y_out, const int32_t* done) {
     if (nred <= 0) return;
-    k_symv_reduce<<<nred, 256, 0, st>>>(ops, items, red, red_begin, oidx, partials, z, y_out, done);
+    launch_pdl(k_symv_reduce, nred, 256, 0, st, ops, items, red, red_begin, oidx, partials, z, y_out, done);
 }
 
 }  // namespace ddg
