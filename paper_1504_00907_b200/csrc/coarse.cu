@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(256)
 k_restrict_dot(int nparts, const int64_t* __restrict__ bptr, const int32_t* __restrict__ cptr,
                const int64_t* __restrict__ qoff, const double* __restrict__ Q, const double* __restrict__ res,
                double* __restrict__ bc, const int32_t* done) {
+    pdl_wait();
     if (*done) return;
     const int I = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (I >= nparts) return;
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(256)
 k_restrict_dot_block(const int64_t* __restrict__ bptr, const int32_t* __restrict__ cptr,
                      const int64_t* __restrict__ qoff, const double* __restrict__ Q,
                      const double* __restrict__ res, double* __restrict__ bc, const int32_t* done) {
+    pdl_wait();
     if (*done) return;
     const int I = blockIdx.x;
     const int64_t b0 = bptr[I];
@@ -136,6 +138,7 @@ k_prolong_flat(int64_t n, const int32_t* __restrict__ xpart, const int64_t* __re
                const int32_t* __restrict__ bidx, const int32_t* __restrict__ cptr, const int64_t* __restrict__ qoff,
                const double* __restrict__ Q, const double* __restrict__ yc, double* __restrict__ z,
                const int32_t* done) {
+    pdl_wait();
     if (*done) return;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
         const int I = xpart[x];
@@ -587,18 +590,18 @@ void launch_restrict_dot(cudaStream_t st, int nparts, const int64_t* bptr, const
                          const double* Q, const double* res, double* bc, int maxmI, const int32_t* done) {
     if (nparts <= 0) return;
     const int g = (nparts + 7) / 8;
-    if (maxmI <= 64) k_restrict_dot<2><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
-    else if (maxmI <= 128) k_restrict_dot<4><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
-    else if (maxmI <= 256) k_restrict_dot<8><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
-    else if (maxmI <= 512) k_restrict_dot<16><<<g, 256, 0, st>>>(nparts, bptr, cptr, qoff, Q, res, bc, done);
-    else k_restrict_dot_block<<<nparts, 256, 0, st>>>(bptr, cptr, qoff, Q, res, bc, done);
+    if (maxmI <= 64) launch_pdl(k_restrict_dot<2>, g, 256, 0, st, nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else if (maxmI <= 128) launch_pdl(k_restrict_dot<4>, g, 256, 0, st, nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else if (maxmI <= 256) launch_pdl(k_restrict_dot<8>, g, 256, 0, st, nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else if (maxmI <= 512) launch_pdl(k_restrict_dot<16>, g, 256, 0, st, nparts, bptr, cptr, qoff, Q, res, bc, done);
+    else launch_pdl(k_restrict_dot_block, nparts, 256, 0, st, bptr, cptr, qoff, Q, res, bc, done);
 }
 
 void launch_prolong_flat(cudaStream_t st, int64_t n, const int32_t* xpart, const int64_t* bptr, const int32_t* bidx,
                          const int32_t* cptr, const int64_t* qoff, const double* Q, const double* yc, double* z,
                          const int32_t* done) {
     if (n <= 0) return;
-    k_prolong_flat<<<vec_grid(n), 256, 0, st>>>(n, xpart, bptr, bidx, cptr, qoff, Q, yc, z, done);
+    launch_pdl(k_prolong_flat, vec_grid(n), 256, 0, st, n, xpart, bptr, bidx, cptr, qoff, Q, yc, z, done);
 }
 
 void launch_prolong(cudaStream_t st, int nparts, const int64_t* bptr, const int32_t* bidx,

@@ -116,6 +116,7 @@ template <int SW>
 __global__ void k_pcg_spmv_dot(DevCSR A, const double* __restrict__ p, double* __restrict__ q,
                                const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc, double* red,
                                unsigned* ticket, int dist) {
+    pdl_wait();
     if (sc->done) return;
     double acc = 0.0;
     const int64_t ng = (int64_t)gridDim.x * blockDim.x / SW;
@@ -162,6 +163,7 @@ __global__ void k_true_res(DevCSR A, const double* __restrict__ f, const double*
 __global__ void k_pcg_update(const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ u,
                              double* __restrict__ r, const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc,
                              double* hist, double* red, unsigned* ticket, int dist) {
+    pdl_wait();
     if (sc->done) return;
     const double alpha = sc->alpha;
     double acc = 0.0;
@@ -182,6 +184,7 @@ __global__ void k_pcg_update(const double* __restrict__ p, const double* __restr
 __global__ void k_pcg_rz(const double* __restrict__ r, const double* __restrict__ z,
                          const int32_t* __restrict__ rows, int64_t nrows, Scalars* sc, double* red,
                          unsigned* ticket, int dist) {
+    pdl_wait();
     if (sc->done) return;
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
@@ -197,6 +200,7 @@ __global__ void k_pcg_rz(const double* __restrict__ r, const double* __restrict_
 // p = z + beta p
 __global__ void k_pcg_direction(const double* __restrict__ z, double* __restrict__ p,
                                 const int32_t* __restrict__ rows, int64_t nrows, const Scalars* sc) {
+    pdl_wait();
     if (sc->done) return;
     const double beta = sc->beta;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
@@ -238,6 +242,7 @@ __global__ void k_copy_rows(const double* __restrict__ in, double* __restrict__ 
 }
 
 __global__ void k_fill(double* x, int64_t n, double v, const int32_t* done) {
+    pdl_wait();
     if (done && *done) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -266,7 +271,7 @@ int num_sms() {
 }
 
 void launch_fill(cudaStream_t st, double* x, int64_t n, double v, const int32_t* done) {
-    k_fill<<<vec_grid(n), VEC_THREADS, 0, st>>>(x, n, v, done);
+    launch_pdl(k_fill, vec_grid(n), VEC_THREADS, 0, st, x, n, v, done);
 }
 
 void launch_spmv(cudaStream_t st, DevCSR A, const double* x, double* y) {
@@ -287,10 +292,10 @@ void launch_pcg_spmv_dot(cudaStream_t st, DevCSR A, const double* p, double* q, 
                          int64_t nrows, Scalars* sc, double* red, unsigned* ticket, int dist) {
     const int g = vec_grid(nrows * std::max(1, A.sw));
     switch (A.sw) {
-        case 4: k_pcg_spmv_dot<4><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
-        case 8: k_pcg_spmv_dot<8><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
-        case 32: k_pcg_spmv_dot<32><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist); break;
-        default: k_pcg_spmv_dot<1><<<g, VEC_THREADS, 0, st>>>(A, p, q, rows, nrows, sc, red, ticket, dist);
+        case 4: launch_pdl(k_pcg_spmv_dot<4>, g, VEC_THREADS, 0, st, A, p, q, rows, nrows, sc, red, ticket, dist); break;
+        case 8: launch_pdl(k_pcg_spmv_dot<8>, g, VEC_THREADS, 0, st, A, p, q, rows, nrows, sc, red, ticket, dist); break;
+        case 32: launch_pdl(k_pcg_spmv_dot<32>, g, VEC_THREADS, 0, st, A, p, q, rows, nrows, sc, red, ticket, dist); break;
+        default: launch_pdl(k_pcg_spmv_dot<1>, g, VEC_THREADS, 0, st, A, p, q, rows, nrows, sc, red, ticket, dist);
     }
 }
 
@@ -308,17 +313,17 @@ void launch_true_res(cudaStream_t st, DevCSR A, const double* f, const double* u
 void launch_pcg_update(cudaStream_t st, const double* p, const double* q, double* u, double* r,
                        const int32_t* rows, int64_t nrows, Scalars* sc, double* hist, double* red,
                        unsigned* ticket, int dist) {
-    k_pcg_update<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(p, q, u, r, rows, nrows, sc, hist, red, ticket, dist);
+    launch_pdl(k_pcg_update, vec_grid(nrows), VEC_THREADS, 0, st, p, q, u, r, rows, nrows, sc, hist, red, ticket, dist);
 }
 
 void launch_pcg_rz(cudaStream_t st, const double* r, const double* z, const int32_t* rows, int64_t nrows,
                    Scalars* sc, double* red, unsigned* ticket, int dist) {
-    k_pcg_rz<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(r, z, rows, nrows, sc, red, ticket, dist);
+    launch_pdl(k_pcg_rz, vec_grid(nrows), VEC_THREADS, 0, st, r, z, rows, nrows, sc, red, ticket, dist);
 }
 
 void launch_pcg_direction(cudaStream_t st, const double* z, double* p, const int32_t* rows, int64_t nrows,
                           Scalars* sc) {
-    k_pcg_direction<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(z, p, rows, nrows, sc);
+    launch_pdl(k_pcg_direction, vec_grid(nrows), VEC_THREADS, 0, st, z, p, rows, nrows, sc);
 }
 
 void launch_pcg_finalize(cudaStream_t st, int slot, Scalars* sc, double* hist) {
