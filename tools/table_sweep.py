@@ -72,6 +72,9 @@ def run(prob, m, hh, p, levels):
     except DDGError as e:
         if "too small" in str(e):
             return {"prob": prob, "m": m, "hh": hh, "p": p, "levels": 3, "too_small": True}
+        if "out of memory" in str(e):
+            torch.cuda.empty_cache()
+            return {"prob": prob, "m": m, "hh": hh, "p": p, "levels": levels, "oom": True}
         raise
     ts = time.time() - t0
     f = torch.from_numpy(pr.f).cuda()
@@ -96,6 +99,8 @@ def cell(r):
         return "—"
     if r.get("too_small"):
         return "✕"
+    if r.get("oom"):
+        return "(memory)"
     if not r["converged"]:
         return f"≥1000 ({r['bound']:.0f})"
     return f"{r['iters']}"
@@ -103,13 +108,18 @@ def cell(r):
 
 def main():
     prob = sys.argv[1] if len(sys.argv) > 1 else "A"
+    ps = [int(x) for x in os.environ.get("TABLE_P", "0,1,2,3").split(",")]
+    if os.environ.get("TABLE_FITS"):                # e.g. "10:320" to try a size outside FITS
+        for item in os.environ["TABLE_FITS"].split(";"):
+            hh, ms = item.split(":")
+            FITS[prob][int(hh)] = sorted(set(FITS[prob][int(hh)]) | {int(m) for m in ms.split(",")})
     sizes = [int(x) for x in sys.argv[2:]] or sorted(set(FITS[prob][10]) | set(FITS[prob][20]))
     res = {}
     for m in sizes:
         for hh, lv in ((10, 2), (20, 2), (10, 3)):
             if m not in FITS[prob][hh]:
                 continue
-            for p in range(4):
+            for p in ps:
                 r = run(prob, m, hh, p, lv)
                 res[(m, hh, lv, p)] = r
                 print(json.dumps(r), flush=True)
