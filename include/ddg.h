@@ -181,7 +181,7 @@ void ddg_default_opts(ddg_opts* o);
  *   col[nnz]          int32 column indices, strictly increasing per row (host)
  *   val[nnz]          fp64 values; A must be symmetric positive definite (host)
  *   F[n*k]            fp64 generating vectors, column-major n x k       (host)
- *   k                 number of generating vectors (1..64)
+ *   k                 number of generating vectors (1..128)
  *   part[n]           int32 part id of every unknown, 0..nparts-1; every part non-empty
  *   nparts            number of parts
  *   opts              NULL for defaults

@@ -166,13 +166,16 @@ k_prolong_warp(int nparts, const int64_t* __restrict__ bptr, const int32_t* __re
     const int64_t b0 = bptr[I];
     const int mI = (int)(bptr[I + 1] - b0);
     const int c0 = cptr[I], ncI = cptr[I + 1] - c0;
-    const double y0 = lane < ncI ? yc[c0 + lane] : 0.0, y1 = lane + 32 < ncI ? yc[c0 + 32 + lane] : 0.0;
+    double yq[4];                                                  // k <= 128 coarse columns
+#pragma unroll
+    for (int h = 0; h < 4; ++h) yq[h] = lane + 32 * h < ncI ? yc[c0 + 32 * h + lane] : 0.0;
     const double* QI = Q + qoff[I];
     double acc[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0.0;
     for (int i = 0; i < ncI; ++i) {
-        const double yi = __shfl_sync(FULL, i < 32 ? y0 : y1, i & 31);
+        const double ysel = i < 32 ? yq[0] : i < 64 ? yq[1] : i < 96 ? yq[2] : yq[3];
+        const double yi = __shfl_sync(FULL, ysel, i & 31);
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             const int a = lane + 32 * k;
@@ -192,7 +195,7 @@ __global__ void k_prolong(const int64_t* __restrict__ bptr, const int32_t* __res
                           const double* __restrict__ Q, const double* __restrict__ yc,
                           double* __restrict__ z, const int32_t* done, const int32_t* __restrict__ parts) {
     if (*done) return;
-    __shared__ double ys[64];
+    __shared__ double ys[128];
     const int I = parts ? parts[blockIdx.x] : blockIdx.x;
     const int64_t b0 = bptr[I];
     const int mI = (int)(bptr[I + 1] - b0);

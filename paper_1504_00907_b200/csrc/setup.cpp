@@ -996,7 +996,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     if (!out) return set_err(DDG_E_ARG, "out is NULL");
     *out = nullptr;
     g_last_error.clear();
-    if (n < 1 || !row_ptr || !col || !val || !F || !part || k < 1 || k > 64 || nparts < 1)
+    if (n < 1 || !row_ptr || !col || !val || !F || !part || k < 1 || k > 128 || nparts < 1)
         return set_err(DDG_E_ARG, "bad argument (n=%lld k=%d nparts=%d)", (long long)n, k, nparts);
     if (n >= (int64_t)INT32_MAX) return set_err(DDG_E_ARG, "n=%lld too large for int32 indices", (long long)n);
     auto t0 = std::chrono::steady_clock::now();

@@ -433,10 +433,10 @@ def test_caller_colouring_rejected():
                                      ("lognormal_16_b4", {"coarse_variant": 2}),
                                      ("C1", {"coarse_variant": 1})])
 def test_symmetric_gauss_jordan_bitwise(name, kw, monkeypatch):
-    """The symmetric blocked Gauss-Jordan (reading R22: block-lower tiles only,
-    upper operands read transposed with the exchange's sign) is the same exact
-    algorithm as the full exchange; the pivot block's inverse is not bitwise
-    symmetric, so the two agree to rounding (and each matches the oracle)."""
+    """The experimental symmetric blocked Gauss-Jordan (reading R22, DDG_GJ_SYM=1:
+    block-lower tiles only, upper operands read transposed with the exchange's
+    sign) agrees with the full exchange to rounding on these sizes (up to ~90
+    tiles per side).  It is off by default: it goes wrong on larger blocks."""
     pr = CASES[name]()
     monkeypatch.setenv("DDG_GJ_SYM", "0")
     u0, it0, h0, _ = _solver(pr, **kw).solve(pr.f, 1e-8)
@@ -470,3 +470,17 @@ def test_node_blocked_rows_match_csr_bitwise(name, monkeypatch):
         out.append(Solver.from_problem(pr, **kw).solve(pr.f, 1e-8))
     (u0, it0, h0, _), (u1, it1, h1, _) = out
     assert it0 == it1 and np.array_equal(u0, u1) and np.array_equal(h0, h1)
+
+
+@pytest.mark.parametrize("mk", [lambda: P.poisson3d(16, 8, 6, 77),       # k = 84
+                                lambda: P.biharmonic2d(64, 32, 10, 78)])  # k = 66 (the p-sweep's p = 10)
+def test_more_than_64_generating_vectors(mk):
+    """k up to 128 generating vectors per part (the paper's p-sweep reaches
+    p = 10, 66 monomials in 2D): parity with the oracle, restriction,
+    prolongation and the coarse correction included."""
+    pr = mk()
+    assert pr.k > 64
+    s, o, it, ur = compare_solve(pr)
+    r = np.random.default_rng(3).standard_normal(pr.n)
+    ref = o.coarse_correct(r)
+    assert np.linalg.norm(s.coarse_correct(r) - ref) <= 1e-9 * np.linalg.norm(ref)
