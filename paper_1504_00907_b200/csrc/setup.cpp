@@ -1902,3 +1902,37 @@ extern "C" int ddg_get_lanczos(ddg_ctx* c, double* alphas, double* betas, int ca
     }
     return k;
 }
+
+// Debug: blocked Gauss-Jordan on nmat host matrices (tiled layout, nTs[b] tiles
+// per side, all pivoted, concatenated), in place; sym selects the symmetric
+// variant (tools/gjunit.py only).
+extern "C" int ddg_debug_gj(int nmat, const int32_t* nTs, double* mats, int sym) {
+    std::vector<int64_t> off(nmat + 1, 0);
+    int maxT = 0;
+    for (int b = 0; b < nmat; ++b) {
+        off[b + 1] = off[b] + (int64_t)nTs[b] * nTs[b] * TILE_ELEMS;
+        maxT = std::max(maxT, (int)nTs[b]);
+    }
+    double* d = nullptr;
+    double** dp = nullptr;
+    int32_t *dn = nullptr, *dids = nullptr, *derr = nullptr;
+    if (cudaMalloc(&d, off[nmat] * 8) || cudaMalloc(&dp, nmat * sizeof(double*)) || cudaMalloc(&dn, nmat * 4) ||
+        cudaMalloc(&dids, nmat * 4) || cudaMalloc(&derr, 8))
+        return set_err(DDG_E_OOM, "debug gj alloc");
+    std::vector<double*> ptr(nmat);
+    std::vector<int32_t> ids(nmat);
+    for (int b = 0; b < nmat; ++b) { ptr[b] = d + off[b]; ids[b] = b; }
+    int32_t herr[2] = {-1, -1};
+    cudaMemcpy(d, mats, off[nmat] * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dp, ptr.data(), nmat * sizeof(double*), cudaMemcpyHostToDevice);
+    cudaMemcpy(dn, nTs, nmat * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dids, ids.data(), nmat * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(derr, herr, 8, cudaMemcpyHostToDevice);
+    setenv("DDG_GJ_SYM", sym ? "1" : "0", 1);
+    launch_gj_blocked(nullptr, nmat, maxT, maxT, dp, dn, dn, dids, derr);
+    cudaDeviceSynchronize();
+    cudaMemcpy(mats, d, off[nmat] * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(herr, derr, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d); cudaFree(dp); cudaFree(dn); cudaFree(dids); cudaFree(derr);
+    return herr[0] >= 0 ? DDG_E_NOT_SPD : DDG_OK;
+}

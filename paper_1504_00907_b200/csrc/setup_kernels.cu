@@ -227,13 +227,13 @@ __global__ void __launch_bounds__(256) k_gjb_pivot(GJBatch bt, int k0) {
 // CTA: a 4 x 4-tile (128 x 128) output block; thread: 8 x 8 elements.
 // grid.x: output blocks of one matrix (by 4-tile rows and columns), grid.y: batch
 // Symmetric variant (bt.strip set, reading R22 in DESIGN.md): the exchange keeps
-// M(X,Y) = s M(Y,X)^T with s = -1 when exactly one of X, Y is pivoted, so only
-// the block-lower tiles (4-tile blocks, diagonal blocks whole) are updated and
-// an upper operand tile is read transposed from its mirror.  The new row
-// panel goes to a strip first (mode 1 still needs the old one), and mode 2
-// copies its block-lower part back.  The same exact algorithm for half the
-// trailing flops; the pivot block's inverse is not bitwise symmetric, so the
-// stored tiles agree with the full variant's to rounding.
+// M(X,Y) = s M(Y,X)^T (s = -1 when exactly one of X, Y is pivoted).  The
+// block-upper tiles whose row and column are both pivoted or both unpivoted
+// are not updated; the unpivoted-unpivoted ones are read transposed from
+// their mirror (s = +1) where the row panel needs them.  The mixed tiles
+// (pivoted rows, unpivoted columns) are kept exactly as in the full exchange.
+// The new row panel goes to a strip first (mode 1 still needs the old one),
+// and mode 2 copies it back.  About a third of the trailing flops saved.
 // MMA: the 128 x 128 block product on the fp64 tensor path (mma.sync m8n8k4,
 // each warp a 32 x 64 tile of 4 x 8 fragments): the fragments are read from
 // shared memory once per 4-deep k step instead of per FMA, which is what
@@ -266,9 +266,12 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
     const int bk = k0 / GJB_BT;
     double* strip = sym ? bt.strip + (int64_t)b * bt.strip_stride : nullptr;
     auto stile = [&](int t, int J) { return strip + ((int64_t)J * GJB_BT + t) * TILE_ELEMS; };
-    if (sym && mode == 1 && bi < bj) return;                     // block-upper: implied by symmetry
-    if (sym && mode == 2 && bi <= bk) {
-        // the new row panel's block-lower tiles (kb, J), J in block bi, back from the strip
+    // block-upper tiles with both row and column pivoted, or both unpivoted, follow by
+    // symmetry; the mixed ones (pivoted rows, unpivoted columns) are kept as in the full
+    // exchange, so pivoted rows never take a transposed operand
+    if (sym && mode == 1 && bi < bj && !(bi < bk && bj >= bk)) return;
+    if (sym && mode == 2) {
+        // the new row panel (kb, J), J in block bi, back from the strip
         for (int J = i0; J < min(i0 + GJB_BT, nT); ++J) {
             if (in_kb(J)) continue;
             for (int t = 0; t < k1 - k0; ++t) {
@@ -277,7 +280,6 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
                 for (int e = threadIdx.x; e < TILE_ELEMS; e += 256) dst[e] = src[e];
             }
         }
-        if (bi < bk) return;
     }
     // does this block own any output tile?
     {
@@ -311,8 +313,7 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
             const int kk = o / TILE, r = o % TILE;
             double v = 0.0;
             if (I < nT && (mode != 0 || I < k1)) {
-                if (sym && mode == 1 && I / GJB_BT < bk) v = -tile(q, I)[r * TILE + kk];   // pivoted row: s = -1
-                else v = tile(I, q)[o];
+                v = tile(I, q)[o];
             }
             As[kk * LDA + ti * TILE + r] = v;
         }
