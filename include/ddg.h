@@ -84,7 +84,8 @@ typedef struct {
 
 typedef struct {
     int overlap;          /* Delta: graph distance in the pattern of A. default 1 */
-    double rank_tol;      /* keep column j of a part iff |R_jj| >= rank_tol * max_j ||F_I e_j||
+    double rank_tol;      /* keep column j of a part iff ||v_j|| >= rank_tol * ||F_I e_j||, v_j the
+                             part of column j orthogonal to the kept earlier columns
                              (reading R7). default 1e-8            */
     int stop_mode;        /* DDG_STOP_*, default DDG_STOP_RES0                                   */
     int max_iter;         /* default 1000                                         */
@@ -154,7 +155,7 @@ typedef struct {
     int32_t m_min, m_max; /* min / max |Omega~_i|                                               */
     int32_t k;            /* generating vectors per part before pruning                          */
     int32_t dropped;      /* total columns dropped by the rank test                              */
-    double min_rank_ratio;          /* min over parts and kept j of |R_jj| / max_j ||F_I e_j||  */
+    double min_rank_ratio;          /* min over parts and kept j of ||v_j|| / ||F_I e_j|| (R7)       */
     int64_t local_factor_bytes;     /* bytes of the stored local operators (device)            */
     int64_t coarse_factor_bytes;    /* bytes of the stored coarse operator (device)            */
     int32_t coarse_variant;         /* 1 dense packed inverse, 2 sparse supernodal, 3 three

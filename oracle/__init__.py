@@ -46,6 +46,13 @@ def lib():
         L.or_setup_coloured.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64, vp,
                                         C.POINTER(vp)]
         L.or_setup_coloured.restype = C.c_int
+        L.or_setup_ex.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64, vp,
+                                  C.POINTER(vp)]
+        L.or_setup_ex.restype = C.c_int
+        L.or_set_coarse_solver.argtypes = [vp, vp, vp]
+        L.or_set_coarse_solver.restype = None
+        L.or_get_Ac_csr.argtypes = [vp, vp, vp, vp]
+        L.or_get_Ac_csr.restype = i64
         L.or_setup3.argtypes = [i64, vp, vp, vp, vp, C.c_int, vp, i32, C.c_int, f64, vp, i32,
                                 C.POINTER(vp)]
         L.or_setup3.restype = C.c_int
@@ -77,6 +84,13 @@ def lib():
     return _lib
 
 
+class _Opts(C.Structure):
+    _fields_ = [("colour", C.c_void_p), ("perturb", C.c_int), ("coarse_external", C.c_int)]
+
+
+_COARSE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.POINTER(C.c_double))
+
+
 class OracleError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"oracle error {code}: {msg}")
@@ -91,9 +105,13 @@ class Oracle:
     """Plain CPU implementation of setup + M r + PCG (see oracle.c)."""
 
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
-                 part2=None, nparts2=0, colour=None):
+                 part2=None, nparts2=0, colour=None, coarse="envelope", block_coords=None,
+                 perturb=False, nd_leaf=256, scratch=None):
         """part2 (int32[nparts], second-level part of every part) selects the
-        three-level method (oracle.c or_setup3)."""
+        three-level method (oracle.c or_setup3).
+        coarse="nd" solves A_0 by the nested-dissection multifrontal Cholesky
+        of coarse_nd.py (needs block_coords) instead of oracle.c's envelope
+        Cholesky.  perturb=True is the floor mode (oracle.h or_opts)."""
         L = lib()
         self._keep = [np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                       np.ascontiguousarray(val, np.float64),
@@ -103,7 +121,22 @@ class Oracle:
         self.n = int(n)
         self.k = int(Ff.shape[1])
         h = C.c_void_p()
-        if colour is not None:
+        self._nd = None
+        if coarse not in ("envelope", "nd"):
+            raise ValueError(coarse)
+        if coarse == "nd" or perturb:
+            if part2 is not None:
+                raise ValueError("coarse='nd' / perturb are two-level options")
+            o = _Opts()
+            co = None
+            if colour is not None:
+                co = np.ascontiguousarray(colour, np.int32)
+                o.colour = co.ctypes.data
+            o.perturb = int(bool(perturb))
+            o.coarse_external = int(coarse == "nd")
+            st = L.or_setup_ex(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
+                               int(overlap), float(rank_tol), C.byref(o), C.byref(h))
+        elif colour is not None:
             co = np.ascontiguousarray(colour, np.int32)
             st = L.or_setup_coloured(self.n, _p(rp), _p(ci), _p(va), _p(Ff), self.k, _p(pa), int(nparts),
                                      int(overlap), float(rank_tol), _p(co), C.byref(h))
@@ -120,6 +153,23 @@ class Oracle:
         self._owner = None
         self._keep = None
         self._read_info()
+        if coarse == "nd":
+            from .coarse_nd import NDCholesky
+            if block_coords is None:
+                raise ValueError("coarse='nd' needs block_coords")
+            try:
+                self._nd = NDCholesky(self.Ac_sparse(), self.coarse_offsets(), block_coords,
+                                      leaf=nd_leaf, perturb=perturb, scratch=scratch)
+            except np.linalg.LinAlgError as e:
+                raise OracleError(5, str(e))
+            nd = self._nd
+
+            def _solve(user, nc, x):
+                v = np.ctypeslib.as_array(x, shape=(nc,))
+                v[:] = nd.solve(v.copy())
+
+            self._cb = _COARSE_FN(_solve)
+            L.or_set_coarse_solver(self._h, C.cast(self._cb, C.c_void_p), None)
 
     def _read_info(self):
         info = np.zeros(10, np.int64)
@@ -140,9 +190,12 @@ class Oracle:
         return o
 
     @classmethod
-    def from_problem(cls, pr, overlap=None, rank_tol=1e-8, part2=None, nparts2=0, colour=None):
+    def from_problem(cls, pr, overlap=None, rank_tol=1e-8, part2=None, nparts2=0, colour=None,
+                     coarse="envelope", perturb=False, nd_leaf=256, scratch=None):
         return cls(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts,
-                   pr.overlap if overlap is None else overlap, rank_tol, part2, nparts2, colour)
+                   pr.overlap if overlap is None else overlap, rank_tol, part2, nparts2, colour,
+                   coarse=coarse, block_coords=pr.block_coords, perturb=perturb, nd_leaf=nd_leaf,
+                   scratch=scratch)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -219,6 +272,16 @@ class Oracle:
         A = np.zeros((self.nc, self.nc))
         lib().or_get_Ac_dense(self._h, _p(A))
         return A
+
+    def Ac_sparse(self):
+        """A_0 as a full symmetric scipy CSR matrix in coarse order."""
+        import scipy.sparse as sp
+        nnz = lib().or_get_Ac_csr(self._h, None, None, None)
+        rp = np.zeros(self.nc + 1, np.int64)
+        ci = np.empty(max(nnz, 1), np.int32)
+        va = np.empty(max(nnz, 1))
+        lib().or_get_Ac_csr(self._h, _p(rp), _p(ci), _p(va))
+        return sp.csr_matrix((va[:nnz], ci[:nnz], rp), shape=(self.nc, self.nc))
 
     def coarse_offsets(self):
         c = np.empty(self.nparts + 1, np.int32)

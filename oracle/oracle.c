@@ -15,8 +15,10 @@
  *     5. coarse basis: F restricted to Omega_I,
  *        orthonormalised per part (double-double MGS, R6c),
  *        rank-deficient columns discarded (R7)
- *     6. A_0 = R_0 A R_0^T  (A_c = P^T A P)
+ *     6. A_0 = R_0 A R_0^T  (A_c = P^T A P), block storage
  *     7. Cholesky of A_0 in envelope storage
+ *        (or, for large A_0, the nested-dissection multifrontal
+ *        Cholesky of oracle/coarse_nd.py through or_set_coarse_solver)
  *   apply (or_apply_precond)
  *   three levels (or_setup3): the two-level method again on
  *     A_0 with F_0 = R_0 F and a partition of the parts
@@ -24,6 +26,13 @@
  *
  * Parity status: every function here is pinned by tests/test_oracle_*.py
  * (see DESIGN.md "Oracle pins"); none is "parity unpinned".
+ *
+ * Floor mode (or_opts.perturb, SURVEY.md §8(c) "an unavoidable floor"): the
+ * same method with harmless rounding changes -- dot products summed in
+ * reverse, every local matrix factored with its unknowns in reversed order,
+ * the envelope coarse factor built on the reversed coarse order.  The
+ * distance between the plain and the perturbed solution is the intrinsic
+ * fp64 floor of a configuration.
  */
 #include "oracle.h"
 
@@ -72,11 +81,25 @@ struct or_ctx {
     int dropped;
     double min_ratio;
     int64_t nc;
-    /* coarse matrix, envelope lower storage: row i holds columns efirst[i]..i */
+    int32_t* cpart;  /* part of every coarse unknown (nc) */
+    /* A_0 in block form: for part I, blocks (I,J) with
+       J <= I adjacent to I in the graph of A (or J = I), J ascending in
+       aadj[aptr[I]..aptr[I+1]); block e is r_I x r_J row-major at ablk+aoff[e];
+       in diagonal blocks only i >= j is filled */
+    int64_t* aptr;
+    int32_t* aadj;
+    int64_t* aoff;
+    double* ablk;
+    /* coarse factor, envelope lower storage: row i holds columns efirst[i]..i
+       (in floor mode, of the matrix with the coarse order reversed) */
     int64_t* efirst;
     int64_t* eptr;
-    double* ea;  /* A_0 (unfactored copy) */
-    double* el;  /* its Cholesky factor */
+    double* el;
+    /* external exact coarse solve (oracle/coarse_nd.py), replaces el */
+    int coarse_external;
+    or_coarse_fn ext_fn;
+    void* ext_user;
+    int perturb;
     /* three-level method: the two-level method applied to
        A_0 with F_0 = R_0 F; when set, it replaces the exact coarse solve */
     struct or_ctx* child;
@@ -144,9 +167,13 @@ int or_spmv(or_ctx* c, const double* x, double* y) {
     return OR_OK;
 }
 
-static double dot(int64_t n, const double* a, const double* b) {
+/* a^T b, summed in index order (floor mode: in reverse order) */
+static double dot(const or_ctx* c, int64_t n, const double* a, const double* b) {
     double s = 0.0;
-    for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
+    if (c->perturb)
+        for (int64_t i = n - 1; i >= 0; i--) s += a[i] * b[i];
+    else
+        for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
     return s;
 }
 
@@ -366,7 +393,11 @@ static int build_local(or_ctx* c) {
             int32_t v = idx[a];
             for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
                 int32_t b = pos[c->ci[e]];
-                if (b >= 0 && b <= a) L[a * (a + 1) / 2 + b] = c->va[e];
+                if (c->perturb) {                 /* floor mode: unknowns reversed */
+                    if (b >= 0 && b >= a) L[(m - 1 - a) * (m - a) / 2 + (m - 1 - b)] = c->va[e];
+                } else if (b >= 0 && b <= a) {
+                    L[a * (a + 1) / 2 + b] = c->va[e];
+                }
             }
         }
         int st = chol_packed(L, m, i);
@@ -382,7 +413,9 @@ static int build_local(or_ctx* c) {
  * to part I; orthogonalised per part; columns for which
  * phi_I is not of full rank discarded.  Modified
  * Gram-Schmidt in double-double over the columns in their given (graded-lex)
- * order; column j kept iff ||v_j|| >= rank_tol * max_j ||F_I e_j||  (R7).
+ * order; column j kept iff ||v_j|| >= rank_tol * ||F_I e_j||  (R7: the part
+ * of column j not in the span of the earlier columns, relative to the column
+ * itself, so the test does not depend on how the coordinates are scaled).
  * ------------------------------------------------------------------------- */
 static int build_basis(or_ctx* c, const double* F) {
     int np = c->nparts, k = c->k;
@@ -396,28 +429,31 @@ static int build_basis(or_ctx* c, const double* F) {
         if (c->bptr[I + 1] - c->bptr[I] > mmax) mmax = c->bptr[I + 1] - c->bptr[I];
     dd* V;  /* kept q vectors of this part, dd, column-major mI x k */
     dd* v;
+    double* fnrm;  /* ||F_I e_j|| */
     ALLOC(V, mmax * k);
     ALLOC(v, mmax);
+    ALLOC(fnrm, k);
     c->dropped = 0;
     c->min_ratio = INFINITY;
     int64_t qpos = 0;
     for (int32_t I = 0; I < np; I++) {
         int64_t mI = c->bptr[I + 1] - c->bptr[I];
         const int32_t* rows = c->bidx + c->bptr[I];
-        double ref = 0.0;
+        double fmax = 0.0;
         for (int j = 0; j < k; j++) {
             dd s = {0.0, 0.0};
             for (int64_t a = 0; a < mI; a++) {
                 double x = F[(int64_t)j * c->n + rows[a]];
                 s = dd_add(s, dd_mul((dd){x, 0.0}, (dd){x, 0.0}));
             }
-            double nrm = dd_sqrt(s).hi;
-            if (nrm > ref) ref = nrm;
+            fnrm[j] = dd_sqrt(s).hi;
+            if (fnrm[j] > fmax) fmax = fnrm[j];
         }
-        if (!(ref > 0.0))
+        if (!(fmax > 0.0))
             return fail(OR_E_ZERO_BLOCK, "coarse basis: F restricted to part %d is zero", I);
         int r = 0;
         for (int j = 0; j < k; j++) {
+            const double ref = fnrm[j];
             for (int64_t a = 0; a < mI; a++) v[a] = (dd){F[(int64_t)j * c->n + rows[a]], 0.0};
             for (int t = 0; t < r; t++) { /* MGS: v -= (q_t^T v) q_t */
                 dd* q = V + (int64_t)t * mI;
@@ -428,7 +464,7 @@ static int build_basis(or_ctx* c, const double* F) {
             dd s = {0.0, 0.0};
             for (int64_t a = 0; a < mI; a++) s = dd_add(s, dd_mul(v[a], v[a]));
             dd nrm = dd_sqrt(s);
-            double ratio = nrm.hi / ref;
+            double ratio = ref > 0.0 ? nrm.hi / ref : 0.0;
             if (ratio >= c->rank_tol && nrm.hi > 0.0) {
                 dd* q = V + (int64_t)r * mI;
                 for (int64_t a = 0; a < mI; a++) q[a] = dd_div(v[a], nrm);
@@ -446,35 +482,77 @@ static int build_basis(or_ctx* c, const double* F) {
     }
     c->qoff[np] = qpos;
     c->nc = c->cptr[np];
-    free(V); free(v);
+    ALLOC(c->cpart, c->nc);
+    for (int32_t I = 0; I < np; I++)
+        for (int32_t i = c->cptr[I]; i < c->cptr[I + 1]; i++) c->cpart[i] = I;
+    free(V); free(v); free(fnrm);
     return OR_OK;
 }
 
 /* ---------------------------------------------------------------------------
  * Step 6: A_0 = R_0 A R_0^T.  Column (J,j) of A_0 is
  * P^T (A p_{J,j}); (A p)[u] = sum_c A[u,c] p[c] evaluated for every row u that
- * can be non-zero (rows in Omega_J and its neighbours).  Stored as the lower
- * triangle in envelope form (A_0 is symmetric; only rows >= columns kept).
+ * can be non-zero (rows in Omega_J and its neighbours).  A_0 is stored by
+ * blocks: "the same sparsity pattern as the subdomain adjacency matrix, but
+ * with each non-zero replaced with a small dense block".
+ * A_0 is symmetric: only entries with row >= column are computed (R9).
  * ------------------------------------------------------------------------- */
-static int build_coarse(or_ctx* c) {
+static int64_t blk_find(const or_ctx* c, int32_t I, int32_t J) {
+    int64_t lo = c->aptr[I], hi = c->aptr[I + 1];
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (c->aadj[mid] < J) lo = mid + 1; else hi = mid;
+    }
+    return (lo < c->aptr[I + 1] && c->aadj[lo] == J) ? lo : -1;
+}
+
+/* A_0[ci, cj] for ci >= cj */
+static double a0_entry(const or_ctx* c, int64_t ci, int64_t cj) {
+    int32_t I = c->cpart[ci], J = c->cpart[cj];
+    int64_t e = blk_find(c, I, J);
+    if (e < 0) return 0.0;
+    int64_t rJ = c->cptr[J + 1] - c->cptr[J];
+    return c->ablk[c->aoff[e] + (ci - c->cptr[I]) * rJ + (cj - c->cptr[J])];
+}
+
+static int build_coarse_blocks(or_ctx* c) {
     int np = c->nparts;
-    int64_t n = c->n, nc = c->nc;
-    /* envelope: first column of each coarse row = first coarse index of the
-       lowest-numbered part adjacent to (or equal to) its part */
-    int32_t* minadj;
-    ALLOC(minadj, np);
-    for (int32_t I = 0; I < np; I++) minadj[I] = I;
-    for (int64_t v = 0; v < n; v++)
-        for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
-            int32_t I = c->part[v], J = c->part[c->ci[e]];
-            if (J < minadj[I]) minadj[I] = J;
+    int64_t n = c->n;
+    /* block pattern: parts J <= I coupled to I by an entry of A */
+    int32_t* mark;
+    int32_t* nb;
+    ALLOC(mark, np);
+    ALLOC(nb, np);
+    ALLOC(c->aptr, np + 1);
+    for (int pass = 0; pass < 2; pass++) {
+        for (int32_t I = 0; I < np; I++) mark[I] = -1;
+        for (int32_t I = 0; I < np; I++) {
+            int cnt = 0;
+            for (int64_t a = c->bptr[I]; a < c->bptr[I + 1]; a++) {
+                int32_t v = c->bidx[a];
+                for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) {
+                    int32_t J = c->part[c->ci[e]];
+                    if (J <= I && mark[J] != I) { mark[J] = I; nb[cnt++] = J; }
+                }
+            }
+            if (mark[I] != I) { mark[I] = I; nb[cnt++] = I; }
+            if (pass == 0) {
+                c->aptr[I + 1] = c->aptr[I] + cnt;
+            } else {
+                qsort(nb, (size_t)cnt, sizeof(int32_t), cmp_i32);
+                memcpy(c->aadj + c->aptr[I], nb, (size_t)cnt * sizeof(int32_t));
+            }
         }
-    ALLOC(c->efirst, nc);
-    ALLOC(c->eptr, nc + 1);
+        if (pass == 0) ALLOC(c->aadj, c->aptr[np]);
+    }
+    free(mark); free(nb);
+    ALLOC(c->aoff, c->aptr[np] + 1);
     for (int32_t I = 0; I < np; I++)
-        for (int32_t i = c->cptr[I]; i < c->cptr[I + 1]; i++) c->efirst[i] = c->cptr[minadj[I]];
-    for (int64_t i = 0; i < nc; i++) c->eptr[i + 1] = c->eptr[i] + (i - c->efirst[i] + 1);
-    ALLOC(c->ea, c->eptr[nc]);
+        for (int64_t e = c->aptr[I]; e < c->aptr[I + 1]; e++) {
+            int32_t J = c->aadj[e];
+            c->aoff[e + 1] = c->aoff[e] + (int64_t)(c->cptr[I + 1] - c->cptr[I]) * (c->cptr[J + 1] - c->cptr[J]);
+        }
+    ALLOC(c->ablk, c->aoff[c->aptr[np]]);
     double* w;
     double* p;
     int32_t* touched;
@@ -485,6 +563,7 @@ static int build_coarse(or_ctx* c) {
     ALLOC(tmark, n);
     for (int32_t J = 0; J < np; J++) {
         int64_t mJ = c->bptr[J + 1] - c->bptr[J];
+        int64_t rJ = c->cptr[J + 1] - c->cptr[J];
         const int32_t* rowsJ = c->bidx + c->bptr[J];
         /* rows where A p can be non-zero */
         int64_t nt = 0;
@@ -495,7 +574,7 @@ static int build_coarse(or_ctx* c) {
                 if (!tmark[u]) { tmark[u] = 1; touched[nt++] = u; }
             }
         }
-        for (int32_t j = 0; j < c->cptr[J + 1] - c->cptr[J]; j++) {
+        for (int32_t j = 0; j < rJ; j++) {
             int64_t cj = c->cptr[J] + j;
             const double* qJ = c->Q + c->qoff[J] + (int64_t)j * mJ;
             for (int64_t a = 0; a < mJ; a++) p[rowsJ[a]] = qJ[a];
@@ -509,23 +588,71 @@ static int build_coarse(or_ctx* c) {
             for (int64_t t = 0; t < nt; t++) {
                 int32_t u = touched[t];
                 int32_t I = c->part[u];
-                if (I < 0) continue;
+                if (I < J) continue;
                 int64_t mI = c->bptr[I + 1] - c->bptr[I];
+                int64_t e = blk_find(c, I, J);
+                if (e < 0) return fail(OR_E_ARG, "internal: block (%d,%d) missing", I, J);
+                double* blk = c->ablk + c->aoff[e];
                 for (int32_t i = 0; i < c->cptr[I + 1] - c->cptr[I]; i++) {
                     int64_t ci_ = c->cptr[I] + i;
                     if (ci_ < cj) continue;
                     double qv = c->Q[c->qoff[I] + (int64_t)i * mI + c->bpos[u]];
-                    c->ea[c->eptr[ci_] + (cj - c->efirst[ci_])] += qv * w[u];
+                    blk[(int64_t)i * rJ + j] += qv * w[u];
                 }
             }
             for (int64_t a = 0; a < mJ; a++) p[rowsJ[a]] = 0.0;
         }
         for (int64_t t = 0; t < nt; t++) tmark[touched[t]] = 0;
     }
-    free(w); free(p); free(touched); free(tmark); free(minadj);
-    /* Step 7: Cholesky of A_0 within its envelope (exact: no fill outside it) */
+    free(w); free(p); free(touched); free(tmark);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 7: Cholesky of A_0 within its envelope (exact: no fill outside it;
+ * PAPER.md:267 "A_0 u_0 = R_0 f").  Envelope of row i: from the first coarse
+ * unknown of the lowest-numbered part adjacent to its part.  Floor mode: the
+ * same on the matrix with the coarse order reversed, x'[nc-1-i] = x[i].
+ * ------------------------------------------------------------------------- */
+static int build_envelope(or_ctx* c) {
+    int np = c->nparts;
+    int64_t nc = c->nc;
+    int32_t* minadj;   /* lowest part J <= I adjacent to I */
+    int32_t* maxadj;   /* highest part J >= I adjacent to I */
+    ALLOC(minadj, np);
+    ALLOC(maxadj, np);
+    for (int32_t I = 0; I < np; I++) { minadj[I] = c->aadj[c->aptr[I]]; maxadj[I] = I; }
+    for (int32_t I = 0; I < np; I++)
+        for (int64_t e = c->aptr[I]; e < c->aptr[I + 1]; e++)
+            if (I > maxadj[c->aadj[e]]) maxadj[c->aadj[e]] = I;
+    ALLOC(c->efirst, nc);
+    ALLOC(c->eptr, nc + 1);
+    for (int64_t i = 0; i < nc; i++) {
+        int32_t I = c->cpart[i];
+        if (c->perturb) /* row nc-1-i of the reversed matrix: columns nc-1-j for j >= i */
+            c->efirst[nc - 1 - i] = nc - 1 - (c->cptr[maxadj[I] + 1] - 1);
+        else
+            c->efirst[i] = c->cptr[minadj[I]];
+    }
+    free(minadj); free(maxadj);
+    for (int64_t i = 0; i < nc; i++) c->eptr[i + 1] = c->eptr[i] + (i - c->efirst[i] + 1);
     ALLOC(c->el, c->eptr[nc]);
-    memcpy(c->el, c->ea, (size_t)c->eptr[nc] * sizeof(double));
+    for (int32_t I = 0; I < np; I++) {
+        int64_t rI = c->cptr[I + 1] - c->cptr[I];
+        for (int64_t e = c->aptr[I]; e < c->aptr[I + 1]; e++) {
+            int32_t J = c->aadj[e];
+            int64_t rJ = c->cptr[J + 1] - c->cptr[J];
+            for (int64_t i = 0; i < rI; i++)
+                for (int64_t j = 0; j < rJ; j++) {
+                    int64_t ci_ = c->cptr[I] + i, cj = c->cptr[J] + j;
+                    if (ci_ < cj) continue;
+                    double v = c->ablk[c->aoff[e] + i * rJ + j];
+                    int64_t r = ci_, col = cj;
+                    if (c->perturb) { r = nc - 1 - cj; col = nc - 1 - ci_; }
+                    c->el[c->eptr[r] + (col - c->efirst[r])] = v;
+                }
+        }
+    }
     for (int64_t i = 0; i < nc; i++) {
         double* Li = c->el + c->eptr[i] - c->efirst[i]; /* Li[j] valid for j >= efirst[i] */
         for (int64_t j = c->efirst[i]; j <= i; j++) {
@@ -548,6 +675,8 @@ static int build_coarse(or_ctx* c) {
 
 static void coarse_solve(or_ctx* c, double* x) {
     int64_t nc = c->nc;
+    if (c->perturb)
+        for (int64_t i = 0; i < nc / 2; i++) { double t = x[i]; x[i] = x[nc - 1 - i]; x[nc - 1 - i] = t; }
     for (int64_t i = 0; i < nc; i++) {
         const double* Li = c->el + c->eptr[i] - c->efirst[i];
         double s = x[i];
@@ -559,6 +688,8 @@ static void coarse_solve(or_ctx* c, double* x) {
         x[i] /= Li[i];
         for (int64_t t = c->efirst[i]; t < i; t++) x[t] -= Li[t] * x[i];
     }
+    if (c->perturb)
+        for (int64_t i = 0; i < nc / 2; i++) { double t = x[i]; x[i] = x[nc - 1 - i]; x[nc - 1 - i] = t; }
 }
 
 /* ---------------------------------------------------------------------------
@@ -566,7 +697,7 @@ static void coarse_solve(or_ctx* c, double* x) {
  * ------------------------------------------------------------------------- */
 static int setup_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                       const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
-                      double rank_tol, const int32_t* colour, or_ctx** out);
+                      double rank_tol, const or_opts* o, or_ctx** out);
 
 int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
              const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
@@ -577,12 +708,20 @@ int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double
 int or_setup_coloured(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                       const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
                       double rank_tol, const int32_t* colour, or_ctx** out) {
-    return setup_impl(n, row_ptr, col, val, F, k, part, nparts, overlap, rank_tol, colour, out);
+    or_opts o = {0};
+    o.colour = colour;
+    return setup_impl(n, row_ptr, col, val, F, k, part, nparts, overlap, rank_tol, &o, out);
+}
+
+int or_setup_ex(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+                double rank_tol, const or_opts* o, or_ctx** out) {
+    return setup_impl(n, row_ptr, col, val, F, k, part, nparts, overlap, rank_tol, o, out);
 }
 
 static int setup_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                       const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
-                      double rank_tol, const int32_t* colour, or_ctx** out) {
+                      double rank_tol, const or_opts* o, or_ctx** out) {
     *out = NULL;
     g_err[0] = 0;
     if (n < 1 || !row_ptr || !col || !val || !F || !part || k < 1 || nparts < 1 || overlap < 0)
@@ -601,7 +740,9 @@ static int setup_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     if (!c) return fail(OR_E_OOM, "oom");
     int st;
     c->n = n; c->k = k; c->nparts = nparts; c->overlap = overlap; c->rank_tol = rank_tol;
-    c->colour_in = colour;
+    c->colour_in = o ? o->colour : NULL;
+    c->perturb = o ? o->perturb : 0;
+    c->coarse_external = o ? o->coarse_external : 0;
     int64_t nnz = row_ptr[n];
     c->rp = malloc((size_t)(n + 1) * sizeof(int64_t));
     c->ci = malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
@@ -638,7 +779,8 @@ static int setup_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, con
         free(fillp);
     }
     if ((st = build_overlap(c)) || (st = build_colours(c)) || (st = build_local(c)) ||
-        (st = build_basis(c, F)) || (st = build_coarse(c))) {
+        (st = build_basis(c, F)) || (st = build_coarse_blocks(c)) ||
+        (!c->coarse_external && (st = build_envelope(c)))) {
         or_destroy(c);
         return st;
     }
@@ -653,8 +795,9 @@ void or_destroy(or_ctx* c) {
     free(c->bptr); free(c->bidx); free(c->bpos);
     free(c->optr); free(c->oidx); free(c->colour); free(c->order);
     free(c->loff); free(c->L);
-    free(c->cptr); free(c->qoff); free(c->Q);
-    free(c->efirst); free(c->eptr); free(c->ea); free(c->el);
+    free(c->cptr); free(c->qoff); free(c->Q); free(c->cpart);
+    free(c->aptr); free(c->aadj); free(c->aoff); free(c->ablk);
+    free(c->efirst); free(c->eptr); free(c->el);
     or_destroy(c->child);
     free(c);
 }
@@ -722,7 +865,7 @@ int or_setup3(int64_t n, const int64_t* row_ptr, const int32_t* col, const doubl
                     /* A_0 is kept lower in the envelope: (max, min) */
                     int64_t hi = i > j ? i : j, lo = i > j ? j : i;
                     ci0[e] = j;
-                    va0[e++] = c->ea[c->eptr[hi] + (lo - c->efirst[hi])];
+                    va0[e++] = a0_entry(c, hi, lo);
                 }
             }
             p0[i] = part2[I];
@@ -768,7 +911,13 @@ static void subdomain_update(or_ctx* c, int32_t i, const double* r, double* z, d
         for (int64_t e = c->rp[v]; e < c->rp[v + 1]; e++) az += c->va[e] * z[c->ci[e]];
         s[a] = r[v] - az;
     }
-    chol_solve_packed(c->L + c->loff[i], m, s);
+    if (c->perturb) { /* floor mode: the factor holds the reversed ordering */
+        for (int64_t a = 0; a < m / 2; a++) { double t = s[a]; s[a] = s[m - 1 - a]; s[m - 1 - a] = t; }
+        chol_solve_packed(c->L + c->loff[i], m, s);
+        for (int64_t a = 0; a < m / 2; a++) { double t = s[a]; s[a] = s[m - 1 - a]; s[m - 1 - a] = t; }
+    } else {
+        chol_solve_packed(c->L + c->loff[i], m, s);
+    }
     for (int64_t a = 0; a < m; a++) z[idx[a]] += s[a];
 }
 
@@ -809,6 +958,8 @@ static void coarse_add(or_ctx* c, const double* res, double* z) {
         or_apply_precond(c->child, b, y);
         memcpy(b, y, (size_t)c->nc * sizeof(double));
         free(y);
+    } else if (c->coarse_external) {
+        c->ext_fn(c->ext_user, c->nc, b);
     } else {
         coarse_solve(c, b);
     }
@@ -825,6 +976,7 @@ static void coarse_add(or_ctx* c, const double* res, double* z) {
 }
 
 int or_coarse_correct(or_ctx* c, const double* r, double* z) {
+    if (c->coarse_external && !c->ext_fn) return fail(OR_E_ARG, "external coarse solver not set");
     memset(z, 0, (size_t)c->n * sizeof(double));
     coarse_add(c, r, z);
     return OR_OK;
@@ -837,6 +989,7 @@ int or_coarse_correct(or_ctx* c, const double* r, double* z) {
  * ------------------------------------------------------------------------- */
 int or_apply_precond(or_ctx* c, const double* r, double* z) {
     int64_t n = c->n;
+    if (c->coarse_external && !c->ext_fn) return fail(OR_E_ARG, "external coarse solver not set");
     double* s = malloc((size_t)max_m(c) * sizeof(double));
     double* res = malloc((size_t)n * sizeof(double));
     if (!s || !res) { free(s); free(res); return fail(OR_E_OOM, "oom"); }
@@ -877,29 +1030,29 @@ int or_pcg_ab(or_ctx* c, const double* f, double rtol, int max_iter, int stop_mo
     *iters = 0;
     memset(u, 0, (size_t)n * sizeof(double));
     memcpy(r, f, (size_t)n * sizeof(double));
-    double res0 = sqrt(dot(n, r, r));
+    double res0 = sqrt(dot(c, n, r, r));
     hist[0] = res0;
     if (res0 == 0.0) { *converged = 1; goto done; }
     or_apply_precond(c, r, z);
     memcpy(p, z, (size_t)n * sizeof(double));
-    double rho = dot(n, r, z);
+    double rho = dot(c, n, r, z);
     if (!(rho > 0.0)) { st = fail(OR_E_BREAKDOWN, "r^T z <= 0 at iteration 0"); goto done; }
     double pres0 = sqrt(rho), ref = res0;
     for (int it = 0; it < max_iter; it++) {
         or_spmv(c, p, q);
-        double sigma = dot(n, p, q);
+        double sigma = dot(c, n, p, q);
         if (!(sigma > 0.0)) { st = fail(OR_E_BREAKDOWN, "p^T A p <= 0 at iteration %d", it); goto done; }
         double alpha = rho / sigma;
         if (alphas) alphas[it] = alpha;
         for (int64_t v = 0; v < n; v++) { u[v] += alpha * p[v]; r[v] -= alpha * q[v]; }
-        double res = sqrt(dot(n, r, r));
+        double res = sqrt(dot(c, n, r, r));
         hist[it + 1] = res;
         *iters = it + 1;
         if (stop_mode == 1 && it == 0) ref = res;
         if (stop_mode != 2 && res <= rtol * ref && !(stop_mode == 1 && it == 0)) { *converged = 1; break; }
         if (res == 0.0) { *converged = 1; break; }
         or_apply_precond(c, r, z);
-        double rho1 = dot(n, r, z);
+        double rho1 = dot(c, n, r, z);
         if (stop_mode == 2 && sqrt(fabs(rho1)) <= rtol * pres0) { *converged = 1; break; }
         if (!(rho1 > 0.0)) { st = fail(OR_E_BREAKDOWN, "r^T z <= 0 at iteration %d", it + 1); goto done; }
         double beta = rho1 / rho;
@@ -952,12 +1105,61 @@ int or_get_Ac_dense(or_ctx* c, double* Ac) {
     int64_t nc = c->nc;
     memset(Ac, 0, (size_t)(nc * nc) * sizeof(double));
     for (int64_t i = 0; i < nc; i++)
-        for (int64_t j = c->efirst[i]; j <= i; j++) {
-            double v = c->ea[c->eptr[i] + (j - c->efirst[i])];
+        for (int64_t j = 0; j <= i; j++) {
+            double v = a0_entry(c, i, j);
             Ac[i * nc + j] = v;
             Ac[j * nc + i] = v;
         }
     return OR_OK;
+}
+
+/* A_0 as a full symmetric CSR (rows and columns in coarse order, columns
+   ascending); with rp == NULL only the entry count is returned */
+int64_t or_get_Ac_csr(or_ctx* c, int64_t* rp, int32_t* col, double* val) {
+    int np = c->nparts;
+    /* full block adjacency: lower part from aadj, upper part by symmetry */
+    int64_t* fptr = calloc((size_t)np + 1, sizeof(int64_t));
+    if (!fptr) return -1;
+    for (int32_t I = 0; I < np; I++)
+        for (int64_t e = c->aptr[I]; e < c->aptr[I + 1]; e++) {
+            fptr[I + 1]++;
+            if (c->aadj[e] != I) fptr[c->aadj[e] + 1]++;
+        }
+    for (int32_t I = 0; I < np; I++) fptr[I + 1] += fptr[I];
+    int32_t* fadj = malloc((size_t)(fptr[np] > 0 ? fptr[np] : 1) * sizeof(int32_t));
+    int64_t* fill = calloc((size_t)np, sizeof(int64_t));
+    if (!fadj || !fill) { free(fptr); free(fadj); free(fill); return -1; }
+    for (int32_t I = 0; I < np; I++)   /* I ascending: each list comes out sorted */
+        for (int64_t e = c->aptr[I]; e < c->aptr[I + 1]; e++) {
+            int32_t J = c->aadj[e];
+            fadj[fptr[I] + fill[I]++] = J;
+            if (J != I) fadj[fptr[J] + fill[J]++] = I;
+        }
+    for (int32_t I = 0; I < np; I++)
+        qsort(fadj + fptr[I], (size_t)(fptr[I + 1] - fptr[I]), sizeof(int32_t), cmp_i32);
+    int64_t nnz = 0;
+    if (rp) rp[0] = 0;
+    for (int32_t I = 0; I < np; I++)
+        for (int32_t i = c->cptr[I]; i < c->cptr[I + 1]; i++) {
+            for (int64_t e = fptr[I]; e < fptr[I + 1]; e++) {
+                int32_t J = fadj[e];
+                for (int32_t j = c->cptr[J]; j < c->cptr[J + 1]; j++) {
+                    if (rp) {
+                        col[nnz] = j;
+                        val[nnz] = i >= j ? a0_entry(c, i, j) : a0_entry(c, j, i);
+                    }
+                    nnz++;
+                }
+            }
+            if (rp) rp[i + 1] = nnz;
+        }
+    free(fptr); free(fadj); free(fill);
+    return nnz;
+}
+
+void or_set_coarse_solver(or_ctx* c, or_coarse_fn fn, void* user) {
+    c->ext_fn = fn;
+    c->ext_user = user;
 }
 int or_get_coarse_offsets(or_ctx* c, int32_t* cptr) {
     memcpy(cptr, c->cptr, (size_t)(c->nparts + 1) * sizeof(int32_t));

@@ -15,6 +15,17 @@
 
 typedef struct or_ctx or_ctx;
 
+/* x <- A_0^{-1} x in place (an external exact coarse solve) */
+typedef void (*or_coarse_fn)(void* user, int64_t nc, double* x);
+
+typedef struct {
+    const int32_t* colour; /* caller's colouring (as or_setup_coloured) or NULL */
+    int perturb;           /* floor mode: reversed dot order, reversed local and
+                              coarse elimination order */
+    int coarse_external;   /* 1: no envelope factor of A_0; the caller supplies
+                              A_0^{-1} with or_set_coarse_solver (oracle/coarse_nd.py) */
+} or_opts;
+
 /* return codes (own numbering, mirrors the meaning of the product's statuses) */
 #define OR_OK 0
 #define OR_E_ARG 1
@@ -35,6 +46,12 @@ int or_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, const double
 int or_setup_coloured(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                       const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
                       double rank_tol, const int32_t* colour, or_ctx** out);
+int or_setup_ex(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                const double* F, int k, const int32_t* part, int32_t nparts, int overlap,
+                double rank_tol, const or_opts* o, or_ctx** out);
+void or_set_coarse_solver(or_ctx* c, or_coarse_fn fn, void* user);
+/* A_0 as a full symmetric CSR in coarse order; rp == NULL: returns the entry count */
+int64_t or_get_Ac_csr(or_ctx* c, int64_t* rp, int32_t* col, double* val);
 /* three levels: the two-level method applied again to A_0,
    with F_0 = R_0 F and second-level part part2[I] for every fine part I */
 int or_setup3(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,

@@ -37,10 +37,11 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
     bdir = os.path.join(CSRC, "build")
     os.makedirs(bdir, exist_ok=True)
-    for s in SOURCES:
+
+    def compile_one(s):
         src = os.path.join(CSRC, s)
         obj = os.path.join(bdir, s + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
@@ -48,10 +49,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
                "-I", os.path.join(_nccl_dir(), "include"),
                f'-DDDG_NCCL_DIR="{os.path.join(_nccl_dir(), "lib")}"',
                "-c", src, "-o", obj]
-        if s.endswith(".cpp"):
-            cmd += ["-x", "cu"] if False else []
         subprocess.check_call(cmd)
-        objs.append(obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
                            "-lpthread", "-ldl"])

@@ -313,7 +313,8 @@ static int build_colours(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
 
 // Per-part orthonormal basis of F[Omega_I,:]: modified
 // Gram-Schmidt in double-double, columns in their given order, column j kept
-// iff ||v_j|| >= rank_tol * max_j ||F_I e_j|| (reading R7).
+// iff ||v_j|| >= rank_tol * ||F_I e_j|| (reading R7: relative to the column
+// itself, so the test does not depend on how the coordinates are scaled).
 static int build_basis(ddg_ctx* c, const double* F) {
     const int np = c->nparts, k = c->k;
     const int64_t n = c->n;
@@ -326,16 +327,18 @@ static int build_basis(ddg_ctx* c, const double* F) {
         for (int64_t I = b; I < e; ++I) {
             const int64_t mI = c->bptr[I + 1] - c->bptr[I];
             const int32_t* rows = c->bidx.data() + c->bptr[I];
-            double ref = 0;
+            double fmax = 0;
+            std::vector<double> fnrm(k);
             for (int j = 0; j < k; ++j) {
                 DD s{0, 0};
                 for (int64_t a = 0; a < mI; ++a) {
                     double x = F[(int64_t)j * n + rows[a]];
                     s = s + DD{x, 0} * DD{x, 0};
                 }
-                ref = std::max(ref, dd_sqrt(s).hi);
+                fnrm[j] = dd_sqrt(s).hi;
+                fmax = std::max(fmax, fnrm[j]);
             }
-            if (!(ref > 0)) {
+            if (!(fmax > 0)) {
                 int expect = -1;
                 bad.compare_exchange_strong(expect, (int)I);
                 continue;
@@ -354,7 +357,7 @@ static int build_basis(ddg_ctx* c, const double* F) {
                 DD s{0, 0};
                 for (int64_t a = 0; a < mI; ++a) s = s + v[a] * v[a];
                 DD nrm = dd_sqrt(s);
-                const double rt = nrm.hi / ref;
+                const double rt = fnrm[j] > 0 ? nrm.hi / fnrm[j] : 0.0;
                 if (rt >= c->opts.rank_tol && nrm.hi > 0) {
                     DD* q = V.data() + (size_t)r * mI;
                     for (int64_t a = 0; a < mI; ++a) q[a] = dd_div(v[a], nrm);
