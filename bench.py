@@ -7,9 +7,14 @@ colour sweeps, coarse restrict/solve/prolong, reverse sweeps, r^T z,
 direction), f already resident in HBM.  value = DoF * iterations / s over all
 ranks (time-to-rtol = ms_per_step).  e2e = the same metric through
 ddg_pcg_solve with pinned HOST f/u (H2D of f and D2H of u inside the timed
-region).  Workload at N=1: BASELINE configs[1] (C2, 3D Poisson 128^3, p=2).
+region).  Workload at N=1: C3 (3D lognormal 256^3, 4^3 blocks, p=1) -- the
+largest BASELINE config that fits one GPU and the one BASELINE quotes at
+1/2/4/8 GPUs; --config C1..C5 selects the others.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ddg|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ddg|reference] [--config Cx]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU).
 """
 from __future__ import annotations
 
@@ -108,16 +113,25 @@ def model_bytes_per_iter(pr, info, sizes):
     return local + coarse + visits + vec, local
 
 
-def cpu_sample():
-    """Bounded sample of the C2 workload for the oracle: same stencil, block
-    size and p, 40^3 grid (125 subdomains of 700-1000 unknowns)."""
-    from ddg_gen import problems as P
-    return P.poisson3d(40, 8, 2, 1002), "poisson3d 40^3 (C2 stencil, 8^3 blocks, p=2, overlap 1), solve phase"
+# Bounded CPU samples of each workload for the oracle (the same generator
+# recipe -- stencil, coefficient law, block size, p, overlap -- on a smaller
+# grid, so that the oracle's setup and solve take seconds, not hours)
+CPU_SAMPLES = {
+    "C1": (lambda P: P.poisson2d(64, 8, 1, 1001), "C1 itself: 2D Poisson 64^2, 8^2 blocks, p=1"),
+    "C2": (lambda P: P.poisson3d(40, 8, 2, 1002), "C2 recipe at 40^3: 7-point Poisson, 8^3 blocks, p=2"),
+    "C3": (lambda P: P.lognormal3d(48, 4, 1, 1003), "C3 recipe at 48^3: lognormal 7-point, 4^3 blocks, p=1"),
+    "C4": (lambda P: P.elasticity3d(16, 8, 1004), "C4 recipe at 16^3 elements: Q1 elasticity, 8^3-element blocks"),
+    "C5": (lambda P: P.biharmonic2d(256, 16, 3, 1005), "C5 recipe at 256^2: 13-point biharmonic, 16^2 blocks, p=3"),
+}
 
 
-def run_cpu_baseline(rtol, steps=1):
+def run_cpu_baseline(rtol, config, steps=1):
+    """The oracle as it stands (1 thread) on the bounded sample of `config`:
+    solve phase timed (setup untimed), DoF*it/s = n * iterations / t_solve."""
     import oracle
-    pr, desc = cpu_sample()
+    from ddg_gen import problems as P
+    mk, desc = CPU_SAMPLES[config]
+    pr = mk(P)
     t0 = time.time()
     o = oracle.Oracle.from_problem(pr)
     t_setup = time.time() - t0
@@ -128,9 +142,23 @@ def run_cpu_baseline(rtol, steps=1):
         ts.append(time.perf_counter() - t0)
         its.append(it)
     t = float(np.mean(ts))
-    return {"value": pr.n * its[0] / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{desc}; n={pr.n}, {its[0]} iterations, {t:.2f} s/solve, setup {t_setup:.1f} s (untimed)",
-            "ms_per_step": t * 1e3, "iters": its[0], "n": pr.n}
+    out = {"value": pr.n * its[0] / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"{desc}; n={pr.n}, {its[0]} iterations, {t:.2f} s per solve (solve phase), "
+                     f"setup {t_setup:.1f} s untimed; 1 thread",
+           "ms_per_step": t * 1e3, "iters": its[0], "n": pr.n}
+    # context: the full-size oracle run behind the parity goldens (tools/oracle_ref.py),
+    # timed on the development container's host, not on this box
+    g = os.path.join(ROOT, "tests", "golden", f"oracle_full_{config}.json")
+    if os.path.exists(g):
+        try:
+            gj = json.load(open(g))
+            ts_full = gj["timing"]["solve_s"]
+            out["full_size_offline"] = {"value": gj["info"]["n"] * gj["iters"] / ts_full, "unit": UNIT,
+                                        "solve_s": ts_full, "setup_s": gj["timing"]["setup_s"],
+                                        "iters": gj["iters"], "where": "dev container, 1 thread"}
+        except Exception:
+            pass
+    return out
 
 
 def bench_reference(args):
@@ -139,13 +167,14 @@ def bench_reference(args):
         return 0
     for _ in range(args.warmup if args.warmup < 1 else 1):
         pass
-    cb = run_cpu_baseline(args.rtol, steps=max(1, args.steps))
+    cb = run_cpu_baseline(args.rtol, args.config, steps=max(1, args.steps))
     out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "C2 sample for the CPU oracle", "sample": cb["sample"]},
-           "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "config": {"workload": f"{args.config} (bounded CPU sample of its recipe)", "sample": cb["sample"]},
+           "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "full_size_offline")
+                            if k in cb},
            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -245,8 +274,11 @@ def bench_ddg(args):
     per_launch_bytes = st.symv_alg_bytes / max(1, st.symv_launches)
     per_launch_s = st.symv_ms * 1e-3 / max(1, st.symv_launches)
     achieved = per_launch_bytes / per_launch_s / 1e9
+    # ncu dram bytes per launch of this workload's dominant kernel (one --set full
+    # capture per config, profiles/symv_traffic_<workload>.json), or null
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "symv_traffic.json")
+    workload = args.config + ("-3level" if args.levels == 3 else "")
+    tpath = os.path.join(ROOT, "profiles", f"symv_traffic_{workload}.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("traffic_bytes_per_launch")
@@ -258,7 +290,7 @@ def bench_ddg(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config + ("-3level" if args.levels == 3 else ""), "desc": P.CONFIG_TEXT[args.config], "n": pr.n,
+        "config": {"workload": workload, "desc": P.CONFIG_TEXT[args.config], "n": pr.n,
                    "iterations": it, "rtol": args.rtol, "n_c": int(s.info.n_c),
                    "nparts": int(s.info.nparts), "colours": int(s.info.ncolours),
                    "coarse": {1: "dense packed inverse", 2: "sparse nested dissection",
@@ -291,8 +323,9 @@ def bench_ddg(args):
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = run_cpu_baseline(args.rtol)
-        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb = run_cpu_baseline(args.rtol, args.config)
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "full_size_offline")
+                               if k in cb}
     if rank == 0:
         print(json.dumps(out), flush=True)
     s.close()
@@ -309,13 +342,23 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ddg", choices=["ddg", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--levels", type=int, default=2, choices=[2, 3])
     ap.add_argument("--factor", type=int, default=None,
                     help="three levels: parts grouped per axis into a second-level part (default H/h)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one rank per GPU: re-launch under torchrun (rank 0 prints the line)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return bench_reference(args)
     return bench_ddg(args)
