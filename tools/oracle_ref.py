@@ -4,7 +4,7 @@ For a BASELINE config this runs the CPU oracle (oracle/, PAPER.md:547-564 and
 605-608) from the seeded generator and writes
 
   refcache/<cfg>.u.npy            the oracle's u (fp64, git-ignored, ships with gpurun)
-  refcache/<cfg>.perturb.u.npy    the floor-mode u (--perturb)
+  refcache_perturb/<cfg>.perturb.u.npy   the floor-mode u (--perturb; not shipped)
   tests/golden/oracle_full_<cfg>.json
       iterations, converged, residual history, ||u||, sha256 of u's bytes,
       4096 sampled entries of u at seeded positions (so the GPU test can check
@@ -86,7 +86,7 @@ def main():
         g = json.load(open(gpath))
         gp = json.load(open(os.path.join(GOLD, f"oracle_full_{a.cfg}_perturb.json")))
         u0 = np.load(os.path.join(CACHE, f"{a.cfg}.u.npy"))
-        up = np.load(os.path.join(CACHE, f"{a.cfg}.perturb.u.npy"))
+        up = np.load(os.path.join(CACHE + "_perturb", f"{a.cfg}.perturb.u.npy"))
         h0, hp = np.array(g["hist"]), np.array(gp["hist"])
         m = min(len(h0), len(hp))
         g["floor"] = dict(u_rel=float(np.linalg.norm(u0 - up) / np.linalg.norm(u0)),
@@ -96,7 +96,7 @@ def main():
     else:
         pr, u, it, hist, conv, info, tim = run(a.cfg, a.perturb, a.scratch)
         tag = a.cfg + (".perturb" if a.perturb else "")
-        np.save(os.path.join(CACHE, f"{tag}.u.npy"), u)
+        np.save(os.path.join(CACHE + ("_perturb" if a.perturb else ""), f"{tag}.u.npy"), u)
         g = dict(config=a.cfg, perturb=bool(a.perturb), iters=int(it), converged=bool(conv),
                  hist=[float(x) for x in hist], u_norm=float(np.linalg.norm(u)),
                  u_sha256=hashlib.sha256(u.tobytes()).hexdigest(), info=info, timing=tim,
