@@ -302,6 +302,55 @@ def lognormal3d(N=256, b=4, p=1, seed=1003, overlap=1):
     return pr
 
 
+def material2d(N=256, b=16, p=3, seed=1006, overlap=1, aware=False):
+    """Problem (C) of the paper on a structured grid:
+    div(D grad u) = f with D = S + 100 J, S = exp(1 + sin(pi (x + y))),
+    J = H(0.25 + cos(pi x) cos(2 pi y)) the indicator of a second material.
+    The paper's annulus mesh is replaced by the square [-1,1]^2 (N x N cells,
+    cell-centred 5-point, harmonic face averages T = 2 Da Db / (Da + Db),
+    boundary faces T = Da: Dirichlet at the ghost cell, reading R11's rule in
+    2D); the block partition (b x b cells) does not conform to the material
+    boundary, as the paper's algebraic partitions did not.
+
+    aware=True gives the material-aware generating vectors: "piecewise
+    polynomial with respect to the material domains", [F * (1 - J), F * J]
+    (2k columns; a part inside one material keeps only k -- the rank test R7
+    drops the columns that vanish on it)."""
+    dims = (N, N)
+    n = N * N
+    h = 2.0 / N
+    xc = -1.0 + h * (np.arange(N) + 0.5)
+    X, Y = np.meshgrid(xc, xc, indexing="ij")                # X[ix, iy]
+    S = np.exp(1.0 + np.sin(np.pi * (X + Y)))
+    J = (0.25 + np.cos(np.pi * X) * np.cos(2 * np.pi * Y) > 0).astype(np.float64)
+    D = S + 100.0 * J
+    offs = [(0, 0), (1, 0), (-1, 0), (0, 1), (0, -1)]
+    T = []
+    for o in offs[1:]:
+        Dn = np.roll(D, shift=tuple(-x for x in o), axis=(0, 1))
+        t = 2.0 * D * Dn / (D + Dn)
+        for a in range(2):
+            if o[a] == 1:
+                sl = [slice(None)] * 2; sl[a] = -1; t[tuple(sl)] = D[tuple(sl)]
+            elif o[a] == -1:
+                sl = [slice(None)] * 2; sl[a] = 0; t[tuple(sl)] = D[tuple(sl)]
+        T.append(t.ravel(order="F"))
+    diag = np.sum(T, axis=0)
+
+    def coef(k, m):
+        return diag if k == 0 else -T[k - 1]
+
+    rp, c, v = stencil_csr(dims, offs, coef)
+    coords = np.stack([X.ravel(order="F"), Y.ravel(order="F")], axis=1)
+    pr = _finish("material2d", dims, rp, c, v, coords, p, (b, b), seed, overlap,
+                 dict(stencil="5pt_harmonic", aware=bool(aware)))
+    if aware:
+        j = J.ravel(order="F")[:, None]
+        pr.F = np.asfortranarray(np.concatenate([pr.F * (1.0 - j), pr.F * j], axis=1))
+    pr.meta["material_fraction"] = float(J.mean())
+    return pr
+
+
 def biharmonic2d(N=2048, b=16, p=3, seed=1005, overlap=1):
     """C5: 13-point biharmonic (20; -8 axis; +2 diagonal; +1 at distance 2 on axes),
     restricted to the N x N grid with every off-grid value zero (c13)."""

@@ -145,6 +145,10 @@ typedef struct {
     double iter_bound;    /* classical CG bound ln(2/rtol) / ln((sqrt k + 1)/(sqrt k - 1)), k = cond_est */
     double true_res;      /* ||f - A u||_2 of the returned u, computed once after the loop (inside t_solve;
                              the stopping rule uses the recurrence residual, reading R2)           */
+    double bytes_per_iter_model;  /* algorithmic HBM bytes of one PCG iteration on this rank
+                             (SURVEY.md §8(d)): 2 reads of every local operator, one coarse
+                             solve, (64 + 2a) per subdomain row, (144 + 2a + 16k) per row, a =
+                             matrix bytes per row (0 stencil, 32 face7, 12 nnz/n + 4 CSR)   */
 } ddg_report;
 
 typedef struct {
@@ -282,6 +286,22 @@ typedef struct ddg_comm ddg_comm;
 int ddg_get_unique_id(void* id128);
 int ddg_comm_init(int rank, int nranks, const void* id128, int device, ddg_comm** out);
 void ddg_comm_destroy(ddg_comm* comm);
+
+/* Loopback group: nranks VIRTUAL ranks of one process on one device, so the
+ * multi-rank path (owned rows and subdomains, halo exchanges, split
+ * reductions, the distributed second level) runs and is tested where there
+ * are fewer GPUs than ranks.  Each virtual rank is driven by its own host
+ * thread (ddg_setup / ddg_pcg_solve with opts.comm = its loopback comm); all
+ * of them enqueue on the group's one stream.  A collective is a host
+ * rendezvous of every rank; the last to arrive enqueues the data movement
+ * (device-to-device copies for halos, a fixed-rank-order sum kernel for
+ * allreduces) after all ranks' preceding work -- no kernel waits on another.
+ * Graph capture is off for loopback contexts.  nranks <= 16.  The group must
+ * outlive its comms and their contexts. */
+typedef struct ddg_loop_group ddg_loop_group;
+int ddg_loop_group_create(int nranks, int device, ddg_loop_group** out);
+void ddg_loop_group_destroy(ddg_loop_group* group);
+int ddg_comm_init_loopback(ddg_loop_group* group, int rank, ddg_comm** out);
 
 /* Host-only decomposition plan (no device needed): the same plan ddg_setup
  * builds for a communicator of nranks, exposed for tests and tools. */

@@ -405,7 +405,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 __global__ void __launch_bounds__(SYMV_WARPS * 32)
 k_coarse_dataflow(int nwork, const int32_t* __restrict__ work, DFCtx d, const int32_t* __restrict__ item_front,
                   int item_base, const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
-                  const double* __restrict__ ctiles, const int32_t* done, uint64_t* trace) {
+                  const double* __restrict__ ctiles, const int32_t* done, uint64_t* trace, int pf) {
     if (*done) return;
     extern __shared__ double sm[];
     __shared__ int sh[2];
@@ -416,6 +416,13 @@ k_coarse_dataflow(int nwork, const int32_t* __restrict__ work, DFCtx d, const in
         const int q = sh[0];
         __syncthreads();
         if (q >= nwork) return;
+        if (pf > 0 && threadIdx.x == 0 && q + pf < nwork) {     // L2 prefetch of a later work item's tiles
+            const int32_t ep = work[q + pf];
+            if (!(ep & (DF_ASSEMBLE | DF_RED))) {
+                const ItemDesc ip = items[ep & DF_IDX];
+                bulk_prefetch_l2(ctiles + ip.tile_off, (unsigned)(item_doubles(ip.tri, ip.I1 - ip.I0, ip.ntiles) * 8));
+            }
+        }
         prevq = q;
         if (trace && threadIdx.x == 0) trace[4 * q] = gtimer();
         const int32_t e = work[q];
@@ -502,8 +509,9 @@ void launch_coarse_dataflow(cudaStream_t st, int nwork, const int32_t* work, con
         init = true;
     }
     const int grid = std::min(nwork, num_sms() * 2);
+    static int pfq = getenv("DDG_DF_PF") ? atoi(getenv("DDG_DF_PF")) : 0;   // work entries ahead (0: off)
     k_coarse_dataflow<<<grid, SYMV_WARPS * 32, smem, st>>>(nwork, work, d, item_front, item_base, ops, items,
-                                                           ctiles, done, trace);
+                                                           ctiles, done, trace, pfq);
 }
 
 // forward: front vector [b_S ; 0] and w_t = incoming contributions to B

@@ -103,6 +103,13 @@ struct ddg_ctx {
     const double* g_iter_u = nullptr;  // u pointer baked into the captured graph
     int64_t launches = 0;
     int64_t launches_per_iter = 0;
+    // device-side loop (one graph per solve: WHILE(not done){ a1-a3; IF(not done){ a4-a9 } })
+    cudaGraph_t g_solve = nullptr;
+    cudaGraphExec_t ge_solve = nullptr;
+    const double* g_solve_u = nullptr;
+    int64_t launches_a = 0, launches_b = 0;
+    int device_loop = 1;       // DDG_DEVICE_LOOP=0: host-stepped chunks
+    int loop_graph_used = 0;
     int64_t local_bytes = 0, coarse_bytes = 0;
     double t_setup = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;

@@ -218,6 +218,7 @@ void launch_pcg_rz(cudaStream_t st, const double* r, const double* z, const int3
 void launch_pcg_direction(cudaStream_t st, const double* z, double* p, const int32_t* rows, int64_t nrows,
                           Scalars* sc);
 void launch_pcg_finalize(cudaStream_t st, int slot, Scalars* sc, double* hist);
+void launch_pcg_cond(cudaStream_t st, const Scalars* sc, unsigned long long handle);
 void launch_halo_pack(cudaStream_t st, const double* v, const int32_t* idx, double* buf, int64_t n);
 void launch_halo_unpack(cudaStream_t st, const double* buf, const int32_t* idx, double* v, int64_t n);
 void launch_copy_rows(cudaStream_t st, const double* in, double* out, const int32_t* rows, int64_t nrows);
@@ -235,8 +236,9 @@ void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32
 // used for matrices of at least GJB_MIN_T tiles per side;
 // mats/nT/nK/ids are device arrays of nmat entries, maxT/maxK their maxima
 constexpr int GJB_MIN_T = 16;
+// sym: 1 the experimental symmetric exchange (R22), 0 the full exchange, -1 the DDG_GJ_SYM switch
 void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* const* mats, const int32_t* nT,
-                       const int32_t* nK, const int32_t* ids, int32_t* err);
+                       const int32_t* nK, const int32_t* ids, int32_t* err, int sym = -1);
 // sparse coarse factorisation / solve
 void launch_front_scatter(cudaStream_t st, int64_t ntrip, const int32_t* frow, const int32_t* fcol,
                           const double* fval, const int32_t* ffront, const FrontDesc* fronts,

@@ -338,6 +338,33 @@ void launch_halo_unpack(cudaStream_t st, const double* buf, const int32_t* idx, 
     if (n > 0) k_halo_unpack<<<vec_grid(n), VEC_THREADS, 0, st>>>(buf, idx, v, n);
 }
 
+// device-side iteration control: the condition of a graph IF / WHILE node
+// becomes "not done" (setup.cpp build_solve_graph)
+__global__ void k_pcg_cond(const Scalars* sc, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, sc->done ? 0u : 1u);
+}
+void launch_pcg_cond(cudaStream_t st, const Scalars* sc, unsigned long long h) {
+    k_pcg_cond<<<1, 1, 0, st>>>(sc, (cudaGraphConditionalHandle)h);
+}
+
+// loopback allreduce (comm.cpp): fixed rank order
+struct LoopPtrs {
+    const double* p[16];
+};
+__global__ void k_loop_sum(LoopPtrs P, int n, double* __restrict__ out, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < n; ++r) s += P.p[r][i];
+        out[i] = s;
+    }
+}
+void launch_loop_sum(cudaStream_t st, const double* const* ptrs, int n, double* out, int64_t count) {
+    LoopPtrs P{};
+    for (int r = 0; r < n && r < 16; ++r) P.p[r] = ptrs[r];
+    const int grid = (int)std::min<int64_t>((count + 255) / 256, 4096);
+    if (count > 0) k_loop_sum<<<grid, 256, 0, st>>>(P, n, out, count);
+}
+
 void launch_copy_rows(cudaStream_t st, const double* in, double* out, const int32_t* rows, int64_t nrows) {
     if (nrows > 0) k_copy_rows<<<vec_grid(nrows), VEC_THREADS, 0, st>>>(in, out, rows, nrows);
 }

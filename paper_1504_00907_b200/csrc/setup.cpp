@@ -165,6 +165,8 @@ static void free_ctx(ddg_ctx* c) {
     if (c->device >= 0) cudaSetDevice(c->device);
     if (c->ge_iter) cudaGraphExecDestroy(c->ge_iter);
     if (c->g_iter) cudaGraphDestroy(c->g_iter);
+    if (c->ge_solve) cudaGraphExecDestroy(c->ge_solve);
+    if (c->g_solve) cudaGraphDestroy(c->g_solve);
     void* ptrs[] = {c->d_rp, c->d_col, c->d_val, c->d_oidx, c->d_ops, c->d_items, c->d_red,
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
@@ -1058,7 +1060,12 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         free_ctx(c);
         return set_err(DDG_E_CUDA, "cudaSetDevice(%d) failed", c->opts.device);
     }
-    if (c->opts.stream) {
+    if (c->opts.comm && ((ddg_comm*)c->opts.comm)->loop) {
+        // loopback virtual ranks share the group's stream; no graph capture
+        // (another rank's thread enqueues on the same stream between collectives)
+        c->stream = ddg::loop_stream((ddg_comm*)c->opts.comm);
+        c->opts.use_graphs = 0;
+    } else if (c->opts.stream) {
         c->stream = (cudaStream_t)c->opts.stream;
     } else {
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -1134,6 +1141,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     }
     build_plans(c);
     symv_ring_init();
+    c->device_loop = getenv("DDG_DEVICE_LOOP") ? atoi(getenv("DDG_DEVICE_LOOP")) : 1;
     if (c->coarse_variant == 2) {
         if ((st = sparse_coarse_symbolic(c, row_ptr, col, er, ec, ev))) { free_ctx(c); return st; }
         tick("coarse symbolic (nested dissection)");
@@ -1532,6 +1540,108 @@ static void lanczos_condition(const std::vector<double>& a, const std::vector<do
     if (*kappa > 1.0) *bound = log(2.0 / tol) / log((sk + 1.0) / (sk - 1.0));
 }
 
+// The whole iteration loop as one graph with device-side control (CUDA
+// conditional nodes): no iteration is launched after convergence and the host
+// waits once per solve.
+//   top:  k_pcg_cond(while) -> WHILE { body }
+//   body: a1 spmv+dot, a2 update + a3 test, k_pcg_cond(if) -> IF { a4..a8
+//         preconditioner, a9 r^T z + direction } -> k_pcg_cond(while)
+// Returns false (and leaves no graph) where the driver cannot build it; the
+// caller then steps the loop from the host.
+static bool build_solve_graph(ddg_ctx* c, double* d_u) {
+    if (c->ge_solve) cudaGraphExecDestroy(c->ge_solve);
+    if (c->g_solve) cudaGraphDestroy(c->g_solve);
+    c->ge_solve = nullptr;
+    c->g_solve = nullptr;
+    cudaGraph_t g = nullptr;
+    auto fail = [&]() {
+        cudaStreamCaptureStatus cs;
+        if (cudaStreamIsCapturing(c->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(c->stream, &junk);
+            if (junk && junk != g) cudaGraphDestroy(junk);
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return false;
+    };
+    if (cudaGraphCreate(&g, 0) != cudaSuccess) return fail();
+    cudaGraphConditionalHandle hw;
+    if (cudaGraphConditionalHandleCreate(&hw, g, 0, cudaGraphCondAssignDefault) != cudaSuccess) return fail();
+    // top: the WHILE condition from the state after the prologue
+    if (cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess)
+        return fail();
+    launch_pcg_cond(c->stream, c->d_sc, (unsigned long long)hw);
+    cudaGraph_t tmp = nullptr;
+    if (cudaStreamEndCapture(c->stream, &tmp) != cudaSuccess) return fail();
+    cudaGraphNode_t pre;
+    size_t nn = 1;
+    if (cudaGraphGetNodes(g, &pre, &nn) != cudaSuccess || nn != 1) return fail();
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wn;
+    if (cudaGraphAddNode(&wn, g, &pre, 1, &wp) != cudaSuccess) return fail();
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    cudaGraphConditionalHandle hi;
+    if (cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault) != cudaSuccess) return fail();
+    // body: a1-a3, then the IF condition
+    const int64_t l0 = c->launches;
+    if (cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess)
+        return fail();
+    enqueue_step_a(c, d_u);
+    launch_pcg_cond(c->stream, c->d_sc, (unsigned long long)hi);
+    c->launches_a = c->launches - l0 + 1;
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, nullptr, &deps, &nd) != cudaSuccess) return fail();
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t in;
+    if (cudaGraphAddNode(&in, body, deps, nd, &ip) != cudaSuccess) return fail();
+    if (cudaStreamUpdateCaptureDependencies(c->stream, &in, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+        return fail();
+    launch_pcg_cond(c->stream, c->d_sc, (unsigned long long)hw);
+    if (cudaStreamEndCapture(c->stream, &tmp) != cudaSuccess) return fail();
+    // IF body: a4-a8 (preconditioner) and a9
+    cudaGraph_t ib = ip.conditional.phGraph_out[0];
+    const int64_t l1 = c->launches;
+    if (cudaStreamBeginCaptureToGraph(c->stream, ib, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess)
+        return fail();
+    enqueue_precond(c, c->d_r, c->d_z, &c->d_sc->done);
+    enqueue_step_b(c);
+    if (cudaStreamEndCapture(c->stream, &tmp) != cudaSuccess) return fail();
+    c->launches_b = c->launches - l1 + 1;          // + the WHILE condition kernel
+    c->launches = l0;
+    if (cudaGraphInstantiate(&c->ge_solve, g, 0) != cudaSuccess) return fail();
+    c->g_solve = g;
+    c->g_solve_u = d_u;
+    return true;
+}
+
+// SURVEY.md §8(d) byte model of one PCG iteration on this rank
+static double bytes_per_iter_model(ddg_ctx* c) {
+    const double a = c->A.st.kind == 1 ? 0.0 : c->A.st.kind == 2 ? 32.0 : 12.0 * (double)c->nnz / (double)c->n + 4.0;
+    double local = 0.0, msum = 0.0;
+    for (size_t q = 0; q < c->op_sub.size(); ++q) {      // the subdomain operators come first
+        const double m = c->ops[q].m;
+        local += 2.0 * 8.0 * m * (m + 1) / 2;
+        msum += m;
+    }
+    ddg_info inf;
+    ddg_get_info(c, &inf);
+    return local + (double)inf.coarse_solve_bytes + (64.0 + 2 * a) * msum + (144.0 + 2 * a + 16.0 * c->k) * (double)c->nrows;
+}
+
 static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int max_iter,
                    int* iters, double* res_hist, int cap, ddg_report* rep) {
     if (!(rtol > 0)) return set_err(DDG_E_ARG, "rtol must be > 0");
@@ -1547,8 +1657,11 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         c->hist_cap = max_iter + 1;
         if (c->ge_iter) { cudaGraphExecDestroy(c->ge_iter); c->ge_iter = nullptr; }   // d_hist is baked in
         if (c->g_iter) { cudaGraphDestroy(c->g_iter); c->g_iter = nullptr; }
+        if (c->ge_solve) { cudaGraphExecDestroy(c->ge_solve); c->ge_solve = nullptr; }
+        if (c->g_solve) { cudaGraphDestroy(c->g_solve); c->g_solve = nullptr; }
     }
     c->comm_err = 0;
+    c->loop_graph_used = 0;
     const int dist = c->dist ? 1 : 0;
     Scalars init{};
     init.rtol = rtol;
@@ -1587,6 +1700,19 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     }
     int done_iters = 0;
     int chunk = 2;
+    // device-side loop: one graph launch per solve (single context; the
+    // host-stepped chunks below remain for multi-rank contexts and profiling)
+    if (use_graph && !c->dist && c->device_loop && !c->profiling) {
+        if (!c->ge_solve || c->g_solve_u != d_u) {
+            if (!build_solve_graph(c, d_u)) c->device_loop = 0;
+        }
+        if (c->ge_solve) {
+            CUDA_TRY(cudaGraphLaunch(c->ge_solve, c->stream));
+            c->launches += 1;                          // the WHILE condition before the loop
+            done_iters = max_iter;
+            c->loop_graph_used = 1;
+        }
+    }
     if (c->profiling) {
         // profiled solve: step on the host so that no kernel is enqueued after
         // convergence (every timed launch does real work)
@@ -1632,6 +1758,11 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     const Scalars s = *c->h_sc;
     const int it = s.iter;
+    if (c->loop_graph_used) {     // kernels the device loop ran: every body, the IF bodies taken
+        const int nif = (c->opts.stop_mode != 2 && s.status == 0) ? std::max(0, it - 1) : it;
+        c->launches += (int64_t)it * c->launches_a + (int64_t)nif * c->launches_b;
+        c->loop_graph_used = 0;
+    }
     if (iters) *iters = it;
     if (res_hist && cap > 0) {
         int cnt = std::min(cap, it + 1);
@@ -1646,6 +1777,7 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         rep->t_setup = c->t_setup;
         rep->t_solve = ms * 1e-3;
         rep->frac_iters = (double)it;
+        rep->bytes_per_iter_model = bytes_per_iter_model(c);
         rep->cond_est = 1.0;
         rep->iter_bound = 1.0;
         c->last_alpha.clear();
@@ -1663,7 +1795,10 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
             if (d2h(c->stream, h.data(), c->d_hist, (it + 1) * sizeof(double)) == DDG_OK) {
                 double tol = s.rtol * s.ref;
                 double a = log10(h[it - 1]), b = log10(h[it]), lt = log10(tol);
-                if (a != b) rep->frac_iters = (it - 1) + (a - lt) / (a - b);
+                // SPEC.md:373-377 interpolates the residual history; under stop_mode 2
+                // the rule tests sqrt(r^T z), so the interpolant is kept inside
+                // [it - 1, it] (frac <= iters <= frac + 1 in every mode)
+                if (a != b) rep->frac_iters = std::min((double)it, std::max((double)(it - 1), (it - 1) + (a - lt) / (a - b)));
             }
         }
     }
@@ -1931,8 +2066,7 @@ extern "C" int ddg_debug_gj(int nmat, const int32_t* nTs, double* mats, int sym)
     cudaMemcpy(dn, nTs, nmat * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dids, ids.data(), nmat * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(derr, herr, 8, cudaMemcpyHostToDevice);
-    setenv("DDG_GJ_SYM", sym ? "1" : "0", 1);
-    launch_gj_blocked(nullptr, nmat, maxT, maxT, dp, dn, dn, dids, derr);
+    launch_gj_blocked(nullptr, nmat, maxT, maxT, dp, dn, dn, dids, derr, sym ? 1 : 0);
     cudaDeviceSynchronize();
     cudaMemcpy(mats, d, off[nmat] * 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(herr, derr, 8, cudaMemcpyDeviceToHost);

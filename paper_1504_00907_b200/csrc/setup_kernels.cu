@@ -554,7 +554,7 @@ void launch_gj_batched(cudaStream_t st, int nmat, const int32_t* nT, const int32
 }
 
 void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* const* mats, const int32_t* nT,
-                       const int32_t* nK, const int32_t* ids, int32_t* err) {
+                       const int32_t* nK, const int32_t* ids, int32_t* err, int sym) {
     if (nmat <= 0) return;
     static bool init_dev[64] = {};   // function attributes are per device
     int dev_ = 0;
@@ -574,7 +574,7 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
     // symmetric variant: a row-panel strip per matrix (DDG_GJ_SYM=0: full exchange)
     // off by default: wrong beyond ~100 tiles per side (biharmonic blocks of 5k-16k unknowns;
     // DESIGN.md R22), passes the parity suite below that
-    const bool want_sym = getenv("DDG_GJ_SYM") && atoi(getenv("DDG_GJ_SYM")) != 0;
+    const bool want_sym = sym >= 0 ? sym != 0 : (getenv("DDG_GJ_SYM") && atoi(getenv("DDG_GJ_SYM")) != 0);
     const int64_t stride = (int64_t)GJB_BT * maxT * TILE_ELEMS;
     if (want_sym && cudaMallocAsync(&bt.strip, (size_t)nmat * stride * sizeof(double), st) == cudaSuccess)
         bt.strip_stride = stride;

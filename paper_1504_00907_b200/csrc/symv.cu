@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(RING2_THREADS, 1)
 k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
              const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
              const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
-             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr) {
+             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr, int pf) {
     pdl_wait();
     constexpr int SLOT = RT * TILE_ELEMS;
     if (*done) return;
@@ -666,6 +666,10 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
             ItemDesc it;
             OpDesc op;
             dp.next(items, ops, ii, i1, it, op);
+            if (pf > 0 && lane == 0 && ii + pf < i1) {           // L2 prefetch pf items ahead
+                const ItemDesc ip = items[ii + pf];
+                bulk_prefetch_l2(tiles + ip.tile_off, (unsigned)(item_doubles(ip.tri, ip.I1 - ip.I0, ip.ntiles) * 8));
+            }
             const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
             if (bph > 0) mbar_wait(&sempty[bi], (bph - 1) & 1);
             if (lane == 0) {
@@ -882,6 +886,228 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
     }
 }
 
+// ---- k_symv_whole: whole small triangles, one bulk copy per item -------------
+// For colours whose operators are single small triangles (C3: m <= 160, at most
+// 5 x 5 tiles = 103 KB) the whole item fits in shared memory twice.  Item k of
+// a CTA's byte-balanced range lands in buffer k & 1 by ONE bulk copy of its
+// contiguous tiles plus one of its s segment (one mbarrier); the 16 consumer
+// warps then split the item's (nT + 1) nT contributions -- for output segment
+// g: the direct parts of tiles (g, 0..g), the transposed part of diagonal tile
+// (g, g), the transposed parts of tiles (g+1..nT-1, g) -- two per warp, each a
+// 32-vector written to shared memory.  One named barrier per item; then thread
+// x sums segment x / 32's contributions in that fixed order (deterministic)
+// and applies z[idx[x]] += y, with idx and z fetched before the item's data
+// was waited for (same-colour subdomains are disjoint).  Compared with the
+// chunked ring, the consumers synchronise twice per item instead of once per
+// 4-tile chunk, and the producer issues two copies per item instead of one
+// per tile.
+// consumer warps: 16 (two contributions each at nT = 5) or 30 (one each);
+// + a producer warp and a staging warp
+constexpr int WH_MAX_NT = 5;
+constexpr int WH_MAX_ROWS = WH_MAX_NT * TILE;
+__host__ __device__ constexpr int64_t wh_item_doubles(int nT) {
+    return (int64_t)(nT * (nT + 1) / 2 - nT) * TILE_ELEMS + (int64_t)nT * DIAG_ELEMS;
+}
+// tiles [2][BUFD] | s [2][nT 32] | contributions [2][(nT+1) nT][32] | z values [4][160] |
+// row indices [4][160] | item sizes [4][2] | mbarriers full[2], empty[2], pfull[4], pdone[4]
+__host__ __device__ constexpr size_t wh_smem(int nT) {
+    return 2 * (size_t)((wh_item_doubles(nT) + 15) / 16 * 16) * 8 + 2 * (size_t)nT * TILE * 8 +
+           2 * (size_t)(nT + 1) * nT * TILE * 8 + 4 * (size_t)WH_MAX_ROWS * 12 + 4 * 8 + 12 * 8;
+}
+
+// contribution q = g (nT + 1) + k of a triangle with nT tile rows (see above)
+__device__ __forceinline__ double wh_contrib(const double* __restrict__ T0, const double* __restrict__ ss, int nT, int q,
+                                             int lane) {
+    const int g = q / (nT + 1), k = q % (nT + 1);
+    auto toff = [](int r, int c) { return (r * (r + 1) / 2 + c - r) * TILE_ELEMS + r * DIAG_ELEMS; };
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    if (k < g) {                                           // direct, off-diagonal tile (g, k): lane = row
+        const double* T = T0 + toff(g, k);
+        const double2* sJ = reinterpret_cast<const double2*>(ss + k * TILE);
+#pragma unroll
+        for (int j = 0; j < TILE; j += 4) {
+            const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+            d0 = fma(T[j * TILE + lane], u.x, d0);
+            d1 = fma(T[(j + 1) * TILE + lane], u.y, d1);
+            d2 = fma(T[(j + 2) * TILE + lane], v.x, d2);
+            d3 = fma(T[(j + 3) * TILE + lane], v.y, d3);
+        }
+    } else if (k == g) {                                   // direct, diagonal tile: lower L'
+        const double* T = T0 + toff(g, g);
+        const double* sJ = ss + g * TILE;
+#pragma unroll
+        for (int j = 0; j < TILE; j += 2) {
+            if (lane >= j) d0 = fma(T[diag_col_off(j) + lane - j], sJ[j], d0);
+            if (lane >= j + 1) d1 = fma(T[diag_col_off(j + 1) + lane - j - 1], sJ[j + 1], d1);
+        }
+    } else if (k == g + 1) {                               // transposed, diagonal tile: L'^T
+        const double* Tc = T0 + toff(g, g) + diag_col_off(lane) - lane;   // (i, lane) at Tc[i], i >= lane
+        const double* sI = ss + g * TILE;
+#pragma unroll
+        for (int t = 0; t < TILE; t += 2) {
+            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31;
+            if (ia >= lane) d0 = fma(Tc[ia], sI[ia], d0);
+            if (ib >= lane) d1 = fma(Tc[ib], sI[ib], d1);
+        }
+    } else {                                               // transposed, tile (k - 1, g): lane = column
+        const int r = k - 1;
+        const double* T = T0 + toff(r, g) + lane * TILE;
+        const double* sI = ss + r * TILE;
+#pragma unroll
+        for (int t = 0; t < TILE; t += 4) {
+            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31, ic = (t + 2 + lane) & 31,
+                      id = (t + 3 + lane) & 31;
+            d0 = fma(T[ia], sI[ia], d0);
+            d1 = fma(T[ib], sI[ib], d1);
+            d2 = fma(T[ic], sI[ic], d2);
+            d3 = fma(T[id], sI[id], d3);
+        }
+    }
+    return (d0 + d1) + (d2 + d3);
+}
+
+template <int WH_CONS>
+__global__ void __launch_bounds__((WH_CONS + 2) * 32, 1)
+k_symv_whole(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
+             const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
+             const int32_t* __restrict__ oidx, double* __restrict__ z, const int32_t* done, int nTmax, int split,
+             int pf, int stage) {
+    pdl_wait();
+    if (*done) return;
+    extern __shared__ __align__(128) double wsm[];
+    const int64_t BUFD = (wh_item_doubles(nTmax) + 15) / 16 * 16;
+    double* tbuf = wsm;                                        // [2][BUFD]
+    double* sbuf = tbuf + 2 * BUFD;                            // [2][nTmax * 32]
+    double* cbuf = sbuf + 2 * nTmax * TILE;                    // [2][(nTmax + 1) nTmax][32]
+    double* zbuf = cbuf + 2 * (nTmax + 1) * nTmax * TILE;      // [4][WH_MAX_ROWS]  z[idx[x]] before the item
+    int32_t* ibuf = reinterpret_cast<int32_t*>(zbuf + 4 * WH_MAX_ROWS);   // [4][WH_MAX_ROWS] idx[x]
+    int32_t* dbuf = ibuf + 4 * WH_MAX_ROWS;                    // [4][2]: nT, m
+    uint64_t* full = reinterpret_cast<uint64_t*>(dbuf + 8);    // [2] tiles + s landed
+    uint64_t* empty = full + 2;                                // [2] tiles + s consumed
+    uint64_t* pfull = empty + 2;                               // [4] sizes, idx, z staged
+    uint64_t* pdone = pfull + 4;                               // [4] epilogue done with the slot
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], 1);
+        }
+        for (int b = 0; b < 4; ++b) {
+            mbar_init(&pfull[b], 1);
+            mbar_init(&pdone[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (i0 >= i1) return;
+    if (warp == WH_CONS) {                                     // ---- producer: bulk copies ----
+        if (lane != 0) return;
+        // L2 prefetch of the next pf items: the DRAM stream runs pf items ahead
+        // of the two shared-memory buffers (more bytes in flight per SM than
+        // shared memory holds)
+        for (int k = 0; k < pf && k < i1 - i0; ++k) {
+            const ItemDesc it = items[i0 + k];
+            bulk_prefetch_l2(tiles + it.tile_off, (unsigned)(wh_item_doubles(it.I1 - it.I0) * 8));
+        }
+        for (int k = 0; k < i1 - i0; ++k) {
+            const int b = k & 1;
+            if (pf > 0 && k + pf < i1 - i0) {
+                const ItemDesc itp = items[i0 + k + pf];
+                bulk_prefetch_l2(tiles + itp.tile_off, (unsigned)(wh_item_doubles(itp.I1 - itp.I0) * 8));
+            }
+            if (k >= 2) mbar_wait(&empty[b], ((k - 2) >> 1) & 1);
+            const ItemDesc it = items[i0 + k];
+            const int64_t s_off = ops[it.op].s_off;
+            const int h = it.I1 - it.I0;
+            const unsigned tb = (unsigned)(wh_item_doubles(h) * 8), sb = (unsigned)(h * TILE * 8);
+            mbar_expect_tx(&full[b], tb + sb);
+            bulk_g2s(sbuf + b * nTmax * TILE, s + s_off + it.I0 * TILE, sb, &full[b]);
+            const double* src = tiles + it.tile_off;
+            double* dst = tbuf + b * BUFD;
+            if ((split & 0xff) <= 1) {
+                bulk_g2s(dst, src, tb, &full[b]);
+            } else {                                           // one copy per tile row
+                for (int r = 0; r < h; ++r) {
+                    const int64_t o0 = (int64_t)(r * (r + 1) / 2 - r) * TILE_ELEMS + (int64_t)r * DIAG_ELEMS;
+                    const unsigned rb = (unsigned)((r * TILE_ELEMS + DIAG_ELEMS) * 8);
+                    bulk_g2s(dst + o0, src + o0, rb, &full[b]);
+                }
+            }
+        }
+        return;
+    }
+    if (warp == WH_CONS + 1) {                                 // ---- prefetch: sizes, idx, z ----
+        // runs up to 3 items ahead of the consumers (4 staging slots)
+        if (!stage) return;
+        for (int k = 0; k < i1 - i0; ++k) {
+            const int ps = k & 3;
+            if (k >= 4) mbar_wait(&pdone[ps], ((k - 4) >> 2) & 1);
+            const ItemDesc it = items[i0 + k];
+            const OpDesc op = ops[it.op];
+            const int nT = it.I1 - it.I0, nr = min(nT * TILE, op.m);
+            const int32_t* idx = oidx + op.idx_off;
+            int ix[WH_MAX_ROWS / 32];
+#pragma unroll
+            for (int t = 0; t < WH_MAX_ROWS / 32; ++t) ix[t] = lane + 32 * t < nr ? idx[lane + 32 * t] : 0;
+#pragma unroll
+            for (int t = 0; t < WH_MAX_ROWS / 32; ++t)
+                if (lane + 32 * t < nr) {
+                    zbuf[ps * WH_MAX_ROWS + lane + 32 * t] = z[ix[t]];
+                    ibuf[ps * WH_MAX_ROWS + lane + 32 * t] = ix[t];
+                }
+            if (lane == 0) {
+                dbuf[ps * 2] = nT;
+                dbuf[ps * 2 + 1] = nr;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[ps]);            // release: the warp's shared stores
+        }
+        return;
+    }
+    // ---- consumers: contribution q = warp (+ WH_CONS ...) of each item ----
+    const int tid = threadIdx.x;
+    for (int k = 0; k < i1 - i0; ++k) {
+        const int b = k & 1, ps = k & 3;
+        int nT, nr, ixk = 0;
+        double zvk = 0.0;
+        if (stage) {
+            mbar_wait(&pfull[ps], (k >> 2) & 1);
+            nT = dbuf[ps * 2];
+            nr = dbuf[ps * 2 + 1];
+        } else {                                               // this row's index and z, before the data wait
+            const ItemDesc it = items[i0 + k];
+            const OpDesc op = ops[it.op];
+            nT = it.I1 - it.I0;
+            nr = min(nT * TILE, op.m);
+            if (tid < nr) {
+                ixk = oidx[op.idx_off + tid];
+                zvk = z[ixk];
+            }
+        }
+        mbar_wait(&full[b], (k >> 1) & 1);
+        const double* T0 = tbuf + b * BUFD;
+        const double* ss = sbuf + b * nTmax * TILE;
+        double* cb = cbuf + b * (nTmax + 1) * nTmax * TILE;
+        const int nq = (nT + 1) * nT;
+        if (!(split & 0x100))                                  // DDG_RING_WHOLE bit 8: copy-only probe (debug)
+            for (int q = warp; q < nq; q += WH_CONS) cb[q * TILE + lane] = wh_contrib(T0, ss, nT, q, lane);
+        asm volatile("bar.sync 1, %0;" ::"n"(WH_CONS * 32) : "memory");
+        if (tid == 0) {
+            mbar_arrive(&empty[b]);                            // tiles and s of buffer b consumed
+            if (k >= 1) mbar_arrive(&pdone[(k - 1) & 3]);      // every thread is past item k-1's epilogue
+        }
+        if (tid < nr) {
+            const int g = tid >> 5;
+            const double* c = cb + g * (nT + 1) * TILE + (tid & 31);
+            double y = 0.0;
+            for (int kk = 0; kk <= nT; ++kk) y += c[kk * TILE];
+            if (stage) z[ibuf[ps * WH_MAX_ROWS + tid]] = zbuf[ps * WH_MAX_ROWS + tid] + y;
+            else z[ixk] = zvk + y;
+        }
+    }
+}
+
 // Sum the partial segments of multi-item operators for one row block, in
 // fixed item order, and apply the result.  The block's segment offsets are
 // staged in shared memory first, and each row's index and z value are
@@ -960,7 +1186,8 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 }
 
 static bool g_ring_init[64] = {};
-static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0, g_ring_v2 = 0;
+static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0, g_ring_v2 = 0, g_ring_whole = 1, g_whole_pf = 2,
+           g_ring_pf = 0, g_whole_stage = 0, g_whole_warps = 16;
 static unsigned long long* g_ring_trace = nullptr;   // DDG_RING_TRACE (debug)
 // per device, once, outside any stream capture (called from ddg_setup)
 void symv_ring_init() {
@@ -973,6 +1200,12 @@ void symv_ring_init() {
     if (const char* e = getenv("DDG_RING_NST")) g_ring_nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
     g_ring_v2 = getenv("DDG_RING_V2") ? atoi(getenv("DDG_RING_V2")) : -1;   // -1: auto
     g_pdl = getenv("DDG_PDL") ? (atoi(getenv("DDG_PDL")) != 0) : 1;
+    // DDG_RING_WHOLE: 0 off, 1 (default) one copy per item, n > 1 one copy per tile row
+    g_ring_whole = getenv("DDG_RING_WHOLE") ? atoi(getenv("DDG_RING_WHOLE")) : 1;
+    g_whole_pf = getenv("DDG_WHOLE_PF") ? atoi(getenv("DDG_WHOLE_PF")) : 0;   // items prefetched to L2 ahead
+    g_ring_pf = getenv("DDG_RING_PF") ? atoi(getenv("DDG_RING_PF")) : 0;      // ... by k_symv_ring2
+    g_whole_stage = getenv("DDG_WHOLE_STAGE") ? atoi(getenv("DDG_WHOLE_STAGE")) : 0;   // staging warp
+    g_whole_warps = getenv("DDG_WHOLE_WARPS") ? atoi(getenv("DDG_WHOLE_WARPS")) : 16;  // 16 or 30 consumers
 
     if (getenv("DDG_RING_TRACE") && !g_ring_trace) {
         if (cudaMalloc(&g_ring_trace, 32 * sizeof(unsigned long long)) == cudaSuccess)
@@ -990,6 +1223,8 @@ void symv_ring_init() {
     cudaFuncSetAttribute(k_symv_ring2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_whole<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_whole<30>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     g_ring_init[dev & 63] = true;
 }
 
@@ -1010,6 +1245,17 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     const int R = std::max(TILE, max_rows_r), Cr = std::max(0, max_rows_c);
     const int maxr = std::min(RING_MAX_ROWS, R + Cr);
     const size_t budget = 227 * 1024;
+    // whole small triangles (C3): one bulk copy per item, k_symv_whole
+    const int nTw = (std::max(TILE, max_rows_r) + TILE - 1) / TILE;
+    if (triangles && g_ring_whole && nTw <= WH_MAX_NT && max_rows_c == 0 && wh_smem(nTw) <= budget) {
+        if (g_whole_warps == 30)
+            launch_pdl(k_symv_whole<30>, ncta, 32 * 32, wh_smem(nTw), st, ops, items, item_begin, cta_part, tiles,
+                       s, oidx, z, done, nTw, g_ring_whole, g_whole_pf, g_whole_stage);
+        else
+            launch_pdl(k_symv_whole<16>, ncta, 18 * 32, wh_smem(nTw), st, ops, items, item_begin, cta_part, tiles,
+                       s, oidx, z, done, nTw, g_ring_whole, g_whole_pf, g_whole_stage);
+        return;
+    }
     // row/column-warp consumers for launches of whole-subdomain triangles
     // (measured: C3 +4%, C5 +1%; the 8-warp column consumers win on the
     // 8-wide rectangles of split operators); DDG_RING_V2=0/1 forces either
@@ -1021,13 +1267,13 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
         const size_t smem2 = ring2_smem(RT, nst2, nb2, maxr);
         if (RT == 2)
             launch_pdl(k_symv_ring2<2>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
-                       oidx, z, y_out, partials, done, nst2, nb2, maxr);
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf);
         else if (RT == 8)
             launch_pdl(k_symv_ring2<8>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
-                       oidx, z, y_out, partials, done, nst2, nb2, maxr);
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf);
         else
             launch_pdl(k_symv_ring2<4>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
-                       oidx, z, y_out, partials, done, nst2, nb2, maxr);
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf);
         return;
     }
     // item buffers: deep for small items (s copies and epilogues overlap

@@ -27,7 +27,8 @@ EXPORTS = ["ddg_default_opts", "ddg_setup", "ddg_pcg_solve", "ddg_pcg_solve_devi
            "ddg_get_colours", "ddg_get_subdomain_sizes", "ddg_launch_count", "ddg_destroy",
            "ddg_status_string", "ddg_last_error", "ddg_set_profiling", "ddg_get_kernel_stats",
            "ddg_get_unique_id", "ddg_comm_init", "ddg_comm_destroy", "ddg_plan_create", "ddg_get_lanczos",
-           "ddg_plan_query", "ddg_plan_destroy"]
+           "ddg_plan_query", "ddg_plan_destroy", "ddg_loop_group_create", "ddg_loop_group_destroy",
+           "ddg_comm_init_loopback"]
 
 PLAN = dict(OWNED_ROWS=0, OWNED_SUBS=1, P_SEND=2, P_RECV=3, R_SEND=4, R_RECV=5, Z_SEND=6, Z_RECV=7,
             PROLONG_PARTS=8, COLOURS=9, PART_RANK=10, OVERLAP=11)
@@ -55,7 +56,7 @@ class ddg_report(C.Structure):
     _fields_ = [("converged", C.c_int), ("iters", C.c_int), ("res0", C.c_double),
                 ("res_final", C.c_double), ("t_setup", C.c_double), ("t_solve", C.c_double),
                 ("frac_iters", C.c_double), ("cond_est", C.c_double), ("iter_bound", C.c_double),
-                ("true_res", C.c_double)]
+                ("true_res", C.c_double), ("bytes_per_iter_model", C.c_double)]
 
 
 class ddg_info(C.Structure):
@@ -121,6 +122,12 @@ def load(path: str = LIB_PATH):
     L.ddg_get_unique_id.restype = C.c_int
     L.ddg_comm_init.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
     L.ddg_comm_init.restype = C.c_int
+    L.ddg_loop_group_create.argtypes = [C.c_int, C.c_int, C.POINTER(vp)]
+    L.ddg_loop_group_create.restype = C.c_int
+    L.ddg_loop_group_destroy.argtypes = [vp]
+    L.ddg_loop_group_destroy.restype = None
+    L.ddg_comm_init_loopback.argtypes = [vp, C.c_int, C.POINTER(vp)]
+    L.ddg_comm_init_loopback.restype = C.c_int
     L.ddg_comm_destroy.argtypes = [vp]
     L.ddg_comm_destroy.restype = None
     L.ddg_plan_create.argtypes = [i64, vp, vp, vp, i32, C.c_int, vp, C.c_int, C.c_int, C.c_int,
@@ -344,6 +351,33 @@ class Comm:
     def close(self):
         if getattr(self, "handle", None):
             load().ddg_comm_destroy(self.handle)
+            self.handle = None
+
+
+class LoopGroup:
+    """ddg_loop_group_create: nranks virtual ranks on one device (include/ddg.h).
+    comm(r) is rank r's communicator; drive each rank from its own thread."""
+
+    def __init__(self, nranks, device=0):
+        h = C.c_void_p()
+        _check(load().ddg_loop_group_create(int(nranks), int(device), C.byref(h)))
+        self.handle = h
+        self.nranks = nranks
+        self._comms = []
+
+    def comm(self, rank):
+        h = C.c_void_p()
+        _check(load().ddg_comm_init_loopback(self.handle, int(rank), C.byref(h)))
+        c = Comm.__new__(Comm)
+        c.handle, c.rank, c.nranks = h, rank, self.nranks
+        self._comms.append(c)
+        return c
+
+    def close(self):
+        if getattr(self, "handle", None):
+            for c in self._comms:
+                c.close()
+            load().ddg_loop_group_destroy(self.handle)
             self.handle = None
 
 

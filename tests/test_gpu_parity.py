@@ -276,10 +276,13 @@ def test_comm_path_single_rank(name):
 # The small parity cases fall below the persistent ring's size threshold, so
 # each path is also forced explicitly (switches are read at ddg_setup).
 PATHS = {
-    "ring_everywhere": {"DDG_RING_MIN_MB": "0"},                 # ring for every SYMV launch (auto consumer)
-    "ring1_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "0"},  # 8-warp column consumers only
-    "ring_2tile_slots": {"DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2"},
-    "ring2_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1"},  # row/column-warp consumers
+    "ring_everywhere": {"DDG_RING_MIN_MB": "0"},                 # ring for every SYMV launch (auto: k_symv_whole
+                                                                 # for small whole triangles)
+    "whole_staged": {"DDG_RING_MIN_MB": "0", "DDG_WHOLE_STAGE": "1"},   # k_symv_whole, staging warp
+    "whole_rowcopies": {"DDG_RING_MIN_MB": "0", "DDG_RING_WHOLE": "2"},  # k_symv_whole, one copy per tile row
+    "ring1_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "0", "DDG_RING_WHOLE": "0"},  # 8-warp columns
+    "ring_2tile_slots": {"DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2", "DDG_RING_WHOLE": "0"},
+    "ring2_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0"},  # row/column warps
     "classic": {"DDG_SYMV": "classic"},                           # per-item k_symv / k_symv_small
     "coarse_levels": {"DDG_COARSE_DATAFLOW": "0", "DDG_RING_MIN_MB": "0"},  # level-by-level sparse solve
     "csr_rows": {"DDG_NO_STENCIL": "1"},                          # row kernels read the CSR
@@ -432,11 +435,13 @@ def test_caller_colouring_rejected():
 @pytest.mark.parametrize("name,kw", [("poisson3d_24_b8_p2", {}), ("elasticity_8_be4", {}),
                                      ("lognormal_16_b4", {"coarse_variant": 2}),
                                      ("C1", {"coarse_variant": 1})])
-def test_symmetric_gauss_jordan_bitwise(name, kw, monkeypatch):
+def test_symmetric_gauss_jordan_matches_full(name, kw, monkeypatch):
     """The experimental symmetric blocked Gauss-Jordan (reading R22, DDG_GJ_SYM=1:
-    block-lower tiles only, upper operands read transposed with the exchange's
-    sign) agrees with the full exchange to rounding on these sizes (up to ~90
-    tiles per side).  It is off by default: it goes wrong on larger blocks."""
+    skips the block-upper tiles whose row and column are both pivoted or both
+    unpivoted, keeps the mixed ones as the full exchange does, reads the
+    unpivoted row panel transposed from the lower Schur complement) agrees with
+    the full exchange to rounding on these sizes (up to ~90 tiles per side).
+    It is off by default: it loses accuracy on large ill-conditioned blocks."""
     pr = CASES[name]()
     monkeypatch.setenv("DDG_GJ_SYM", "0")
     u0, it0, h0, _ = _solver(pr, **kw).solve(pr.f, 1e-8)
@@ -484,3 +489,17 @@ def test_more_than_64_generating_vectors(mk):
     r = np.random.default_rng(3).standard_normal(pr.n)
     ref = o.coarse_correct(r)
     assert np.linalg.norm(s.coarse_correct(r) - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("stop_mode", [0, 1, 2])
+def test_fractional_iterations_bracket(stop_mode):
+    """frac <= iters <= frac + 1 in every stop mode, and the
+    report's byte model is the SURVEY §8(d) formula's order of magnitude."""
+    pr = CASES["poisson3d_24_b8_p2"]()
+    s = _solver(pr, stop_mode=stop_mode)
+    u, it, hist, rep = s.solve(pr.f, 1e-8)
+    assert rep.converged
+    assert it - 1 <= rep.frac_iters <= it
+    sizes = s.subdomain_sizes().astype(float)
+    local = 2 * np.sum(8 * sizes * (sizes + 1) / 2)
+    assert local < rep.bytes_per_iter_model < 2 * local + 400 * pr.n
