@@ -478,6 +478,42 @@ def elasticity3d(ne=64, be=8, seed=1004, overlap=1, E=1.0, nu=0.3, clamp=True):
                              stencil="q1_elastic", dof_per_node=3))
 
 
+def grown_partition(pr, nparts, seed=77):
+    """The same problem with an irregular, non-box partition: `nparts` seeds
+    drawn from the SplitMix64 stream `seed`, grown together over the graph of
+    A by breadth-first rounds in which every part claims its unclaimed
+    neighbours (ties: the lowest part id).  Parts are connected, their
+    boundaries follow no grid line, and sizes vary (the paper partitions with
+    SCOTCH or inertial bisection).  Components the
+    seeds do not reach (none for connected A) join part 0.  No block
+    coordinates: the library's nested dissection falls back to its graph
+    bisection, the oracle to the envelope coarse factor."""
+    n = pr.n
+    if not (1 <= nparts <= n):
+        raise ValueError("1 <= nparts <= n")
+    u = rng.uniform01(seed, n)
+    seeds = np.argsort(u, kind="stable")[:nparts]
+    part = np.full(n, -1, np.int64)
+    part[seeds] = np.arange(nparts)
+    rp, col = np.asarray(pr.row_ptr, np.int64), np.asarray(pr.col, np.int64)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    while True:
+        # every claimed node offers its part to its unclaimed neighbours
+        src = part[rows]
+        dst = col
+        m = (src >= 0) & (part[dst] < 0)
+        if not m.any():
+            break
+        best = np.full(n, np.iinfo(np.int64).max)
+        np.minimum.at(best, dst[m], src[m])
+        newly = best < np.iinfo(np.int64).max
+        part[newly] = best[newly]
+    part[part < 0] = 0
+    return dataclasses.replace(pr, name=pr.name + f"_grown{nparts}", part=part.astype(np.int32),
+                               nparts=int(nparts), block_coords=None, block_dims=None,
+                               meta=dict(pr.meta, partition=f"grown({nparts}, seed {seed})"))
+
+
 CONFIGS = {
     "C1": lambda: poisson2d(64, 8, 1, 1001),
     "C2": lambda: poisson3d(128, 8, 2, 1002),

@@ -14,8 +14,21 @@ constexpr int TILE = 32;                 // rows/cols per tile = warp width
 constexpr int TILE_ELEMS = TILE * TILE;  // 1024 doubles = 8 KB per tile
 constexpr int DIAG_ELEMS = TILE * (TILE + 1) / 2;  // 528: packed diagonal tile (4224 B)
 
-// doubles of an item's tiles: diagonal tiles of a triangle item are packed
-__host__ __device__ inline int64_t item_doubles(int tri, int h, int ntiles) {
+// Compact tail (single-triangle operators with m % 32 != 0): the last tile row
+// keeps only its `tail` valid rows -- off-diagonal tiles tail x 32 (element
+// (i, j) at j * tail + i), the diagonal tile its packed tail x tail lower
+// triangle (column j at tail_col_off(tail, j)), padded to an even number of
+// doubles (16-byte bulk copies) -- so no padding row is stored or streamed.
+__host__ __device__ inline int tail_diag_doubles(int tail) { return ((tail * (tail + 1) / 2) + 1) & ~1; }
+__host__ __device__ inline int tail_col_off(int tail, int j) { return j * tail - j * (j - 1) / 2; }
+
+// doubles of an item's tiles: diagonal tiles of a triangle item are packed;
+// tail != 0: its last tile row is compact (above)
+__host__ __device__ inline int64_t item_doubles(int tri, int h, int ntiles, int tail = 0) {
+    if (tri && tail) {
+        const int64_t r = h - 1;    // full rows 0 .. h-2 hold r (r + 1) / 2 tiles, r of them diagonal
+        return (r * (r + 1) / 2 - r) * TILE_ELEMS + r * DIAG_ELEMS + r * tail * TILE + tail_diag_doubles(tail);
+    }
     return tri ? (int64_t)(ntiles - h) * TILE_ELEMS + (int64_t)h * DIAG_ELEMS : (int64_t)ntiles * TILE_ELEMS;
 }
 constexpr int SYMV_WARPS = 8;            // consumer warps per SYMV CTA
@@ -47,6 +60,7 @@ struct ItemDesc {
     int32_t J0, J1;   // tile cols [J0, J1)
     int32_t tri;      // 1: diagonal block (lower triangle incl. diagonal tiles)
     int32_t ntiles;
+    int32_t tail;     // 0, or the valid rows (1..31) of a compact last tile row (whole-operator triangles)
     int64_t tile_off; // first double of this item's tiles
     int64_t part_off; // its partial slot (2 * BT * TILE doubles), -1 if single-item op
 };
@@ -168,6 +182,7 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 // (relative to item_begin) of the CTAs.  Requires every item's rows <= 512.
 constexpr int RING_MAX_ROWS = 512;
 void symv_ring_init();   // once per device, before any capture
+extern int g_compact;    // 1: whole-triangle operators store a compact last tile row (DDG_COMPACT)
 int symv_ring_trace(unsigned long long* out);   // debug counters (DDG_RING_TRACE)
 // max_rows_r / max_rows_c: the launch's largest row block and (rectangles)
 // column block, in rows (ring_dims)

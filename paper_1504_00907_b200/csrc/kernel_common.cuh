@@ -191,21 +191,46 @@ __device__ __forceinline__ void item_tile(const ItemDesc& it, int l, int& I, int
 // exactly like an off-diagonal one (direct + transposed) from half the bytes.
 __device__ __forceinline__ int diag_col_off(int j) { return j * TILE - j * (j - 1) / 2; }
 
-// offset (doubles) of local tile l = (I, J) inside its item
+// offset (doubles) of local tile l = (I, J) inside its item (compact last
+// row when it.tail != 0, ddg_internal.h)
 __device__ __forceinline__ int64_t item_tile_off(const ItemDesc& it, int l, int I) {
     if (!it.tri) return (int64_t)l * TILE_ELEMS;
     const int rr = I - it.I0;                  // diagonal tiles of rows 0..rr-1 precede l
+    if (it.tail && I == it.I1 - 1)
+        return (int64_t)(rr * (rr + 1) / 2 - rr) * TILE_ELEMS + (int64_t)rr * DIAG_ELEMS +
+               (int64_t)(l - rr * (rr + 1) / 2) * it.tail * TILE;
     return (int64_t)(l - rr) * TILE_ELEMS + (int64_t)rr * DIAG_ELEMS;
 }
+// doubles stored for tile (I, J) of an item (packed diagonal, compact tail)
+__device__ __forceinline__ int item_tile_doubles(const ItemDesc& it, int I, int J) {
+    const bool t = it.tail && I == it.I1 - 1;
+    return I == J && it.tri ? (t ? tail_diag_doubles(it.tail) : DIAG_ELEMS) : (t ? it.tail * TILE : TILE_ELEMS);
+}
+// valid rows stored for tile row I of an item: 32, or the compact tail
+__device__ __forceinline__ int item_tile_rows(const ItemDesc& it, int I) {
+    return (it.tail && I == it.I1 - 1) ? it.tail : TILE;
+}
 
-// lane i loads row i of tile (I, J) (packed form when I == J)
-__device__ __forceinline__ void load_tile_row(double* a, const double* T, bool diag, int lane) {
+// lane i loads row i of tile (I, J) (packed form when I == J); th < 32: a
+// compact tail tile (rows >= th are zero)
+__device__ __forceinline__ void load_tile_row(double* a, const double* T, bool diag, int lane, int th = TILE) {
+    if (th == TILE) {
+        if (!diag) {
+#pragma unroll
+            for (int j = 0; j < TILE; ++j) a[j] = __ldcs(T + j * TILE + lane);
+        } else {
+#pragma unroll
+            for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? __ldcs(T + diag_col_off(j) + lane - j) : 0.0;
+        }
+        return;
+    }
     if (!diag) {
 #pragma unroll
-        for (int j = 0; j < TILE; ++j) a[j] = __ldcs(T + j * TILE + lane);
+        for (int j = 0; j < TILE; ++j) a[j] = lane < th ? __ldcs(T + j * th + lane) : 0.0;
     } else {
 #pragma unroll
-        for (int j = 0; j < TILE; ++j) a[j] = lane >= j ? __ldcs(T + diag_col_off(j) + lane - j) : 0.0;
+        for (int j = 0; j < TILE; ++j)
+            a[j] = (lane >= j && lane < th) ? __ldcs(T + tail_col_off(th, j) + lane - j) : 0.0;
     }
 }
 

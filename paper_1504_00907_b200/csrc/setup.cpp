@@ -475,7 +475,7 @@ static void build_galerkin(ddg_ctx* c, const int64_t* rp, const int32_t* col, co
 }
 
 // Operator descriptors, work items and reduction tasks for the tiled SYMV.
-static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool allow_single) {
+static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool allow_single, bool compact = false) {
     OpDesc op{};
     op.m = m;
     op.mp = ((m + TILE - 1) / TILE) * TILE;
@@ -504,8 +504,10 @@ static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool al
             it.tri = (bi == bj);
             const int h = it.I1 - it.I0, wd = it.J1 - it.J0;
             it.ntiles = it.tri ? h * (h + 1) / 2 : h * wd;
+            // compact last tile row (ddg_internal.h) for whole-operator triangles
+            it.tail = (compact && op.nblk == 1 && m % TILE) ? m % TILE : 0;
             it.tile_off = c->tiles_doubles;
-            c->tiles_doubles += item_doubles(it.tri, h, it.ntiles);
+            c->tiles_doubles += item_doubles(it.tri, h, it.ntiles, it.tail);
             if (op.nitems > 1) {
                 it.part_off = c->part_doubles;
                 c->part_doubles += (int64_t)(h + (it.tri ? 0 : wd)) * TILE;
@@ -647,7 +649,7 @@ int ring_partition(ddg_ctx* c, int b, int e) {
         if (rows > RING_MAX_ROWS) return -1;
         mr = std::max(mr, (d.I1 - d.I0) * TILE);
         if (!d.tri) mc = std::max(mc, (d.J1 - d.J0) * TILE);
-        pre[i - b + 1] = pre[i - b] + item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8.0 + 8192.0;
+        pre[i - b + 1] = pre[i - b] + item_doubles(d.tri, d.I1 - d.I0, d.ntiles, d.tail) * 8.0 + 8192.0;
     }
     const int off = (int)c->h_ring.size();
     c->h_ring.resize(off + G + 1);
@@ -689,6 +691,22 @@ static int build_plans(ddg_ctx* c) {
         pl.item_begin = (int)c->items.size();
         pl.red_begin = (int)c->red.size();
         pl.max_rows = 0;
+        // compact last tile rows (ddg_internal.h, DDG_COMPACT) only in colours
+        // whose operators are all whole triangles: the rectangle items of split
+        // operators are read as full tiles
+        bool compact = g_compact != 0;
+        {
+            const int single_max = getenv("DDG_SINGLE_MAX_NT") ? atoi(getenv("DDG_SINGLE_MAX_NT")) : MAX_BT;
+            int64_t max_nt = 0;
+            for (int q = pos; q < c->nparts && c->colour[c->order[q]] == cc; ++q) {
+                const int i = c->order[q];
+                const int64_t m = c->optr[i + 1] - c->optr[i];
+                if ((m + TILE - 1) / TILE > single_max) compact = false;
+                max_nt = std::max<int64_t>(max_nt, (m + TILE - 1) / TILE);
+            }
+            // colours of small triangles (nT <= 5) run k_symv_whole on full tiles
+            if (max_nt <= 5) compact = false;
+        }
         while (pos < c->nparts && c->colour[c->order[pos]] == cc) {
             const int i = c->order[pos];
             if (c->dist && c->plan.part_rank[i] != c->rank) { ++pos; continue; }   // another rank's
@@ -697,7 +715,9 @@ static int build_plans(ddg_ctx* c) {
             const int64_t off = (int64_t)sorted_idx.size();
             sorted_idx.insert(sorted_idx.end(), c->oidx.begin() + c->optr[i],
                               c->oidx.begin() + c->optr[i + 1]);
-            add_op(c, (int32_t)m, 0, off, true);
+            // every list starts 16-byte aligned (k_symv_whole bulk-copies it)
+            while (sorted_idx.size() % 4) sorted_idx.push_back(0);
+            add_op(c, (int32_t)m, 0, off, true, compact);
             pl.max_rows = std::max<int>(pl.max_rows, (int)m);
             ++pos;
         }
@@ -1139,8 +1159,8 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         return set_err(DDG_E_ARG, "n_c = %lld: the dense coarse inverse is limited to 131072 unknowns",
                        (long long)nc);
     }
+    symv_ring_init();          // reads the SYMV switches (g_band) build_plans depends on
     build_plans(c);
-    symv_ring_init();
     c->device_loop = getenv("DDG_DEVICE_LOOP") ? atoi(getenv("DDG_DEVICE_LOOP")) : 1;
     if (c->coarse_variant == 2) {
         if ((st = sparse_coarse_symbolic(c, row_ptr, col, er, ec, ev))) { free_ctx(c); return st; }
@@ -1301,7 +1321,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         const OpDesc& op = c->ops[q];
         for (int t = 0; t < op.nitems; ++t) {
             const ItemDesc& d = c->items[op.item_base + t];
-            c->local_bytes += item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8;
+            c->local_bytes += item_doubles(d.tri, d.I1 - d.I0, d.ntiles, d.tail) * 8;
         }
     }
     c->coarse_bytes = c->coarse_variant == 1   ? (c->tiles_doubles * 8) - c->local_bytes

@@ -449,10 +449,23 @@ __global__ void k_pack(const int32_t* __restrict__ op_ids, const OpDesc* __restr
             item_tile(it, l, I, J);
             const double* src = M + ((int64_t)J * op.nT + I) * TILE_ELEMS;
             double* dst = tiles + it.tile_off + item_tile_off(it, l, I);
+            const int th = item_tile_rows(it, I);     // compact tail: rows >= th are not stored
+            if (th < TILE && I == J && threadIdx.x == 0 && (th * (th + 1) / 2) % 2)
+                dst[tail_diag_doubles(th) - 1] = 0.0;   // the even-size pad of a compact diagonal tile
             for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
                 const int i = e % TILE, j = e / TILE;
                 double v = src[e];
                 if (I * TILE + i >= op.m || J * TILE + j >= op.m) v = 0.0;
+                if (th < TILE) {
+                    if (i >= th) continue;
+                    if (I != J) {
+                        dst[j * th + i] = v;
+                    } else if (i >= j) {
+                        double vt = (I * TILE + i >= op.m || J * TILE + j >= op.m) ? 0.0 : src[i * TILE + j];
+                        dst[tail_col_off(th, j) + i - j] = i == j ? 0.5 * v : 0.5 * (v + vt);
+                    }
+                    continue;
+                }
                 if (I != J) {
                     dst[e] = v;
                 } else if (i >= j) {           // packed lower, diagonal halved, symmetrised

@@ -54,7 +54,7 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
     if (w < it.ntiles) {
         int I0_, J0_;
         item_tile(it, w, I0_, J0_);
-        load_tile_row(a, tbase + item_tile_off(it, w, I0_), I0_ == J0_, lane);
+        load_tile_row(a, tbase + item_tile_off(it, w, I0_), I0_ == J0_, lane, item_tile_rows(it, I0_));
     }
     if (gather_mode) {
         // fused residual restriction (single-item operators): s = R~_i (r - A z)
@@ -83,7 +83,7 @@ k_symv(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int i
     for (int l = w; l < it.ntiles; l += SYMV_WARPS) {
         int I, J;
         item_tile(it, l, I, J);
-        if (l != w) load_tile_row(a, tbase + item_tile_off(it, l, I), I == J, lane);
+        if (l != w) load_tile_row(a, tbase + item_tile_off(it, l, I), I == J, lane, item_tile_rows(it, I));
         const int ri = (I - it.I0) * TILE;                           // row offset in s_sm / pw
         const int cj = it.tri ? (J - it.I0) * TILE : rows_r + (J - it.J0) * TILE;
         double acc = 0.0;
@@ -194,7 +194,7 @@ k_symv_small(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
     double a[TILE], b[TILE];
     int I = 0, J = 0;
     item_tile(it, 0, I, J);
-    load_tile_row(a, tb + item_tile_off(it, 0, I), I == J, lane);       // first tile in flight
+    load_tile_row(a, tb + item_tile_off(it, 0, I), I == J, lane, item_tile_rows(it, I));   // first tile in flight
     double* sw = ssm[w];
     double* yw = ysm[w];
     const int32_t* idx = oidx + op.idx_off;
@@ -220,12 +220,12 @@ k_symv_small(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
         const bool has1 = l + 1 < it.ntiles;
         if (has1) {
             item_tile(it, l + 1, I1, J1);
-            load_tile_row(b, tb + item_tile_off(it, l + 1, I1), I1 == J1, lane);
+            load_tile_row(b, tb + item_tile_off(it, l + 1, I1), I1 == J1, lane, item_tile_rows(it, I1));
         }
         tile_apply(a, a, sw, yw, I * TILE, J * TILE, I == J, lane);
         if (l + 2 < it.ntiles) {
             item_tile(it, l + 2, I, J);
-            load_tile_row(a, tb + item_tile_off(it, l + 2, I), I == J, lane);
+            load_tile_row(a, tb + item_tile_off(it, l + 2, I), I == J, lane, item_tile_rows(it, I));
         }
         if (has1) tile_apply(b, b, sw, yw, I1 * TILE, J1 * TILE, I1 == J1, lane);
     }
@@ -596,26 +596,113 @@ k_symv_ring(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, 
 #undef RT_FLUSH
 }
 
+// ---- tile products of whole-operator triangles (k_symv_whole, k_symv_ring2) --
+// th = 32: a full tile (diagonal tiles packed, kernel_common.cuh); th < 32: a
+// compact last-row tile (ddg_internal.h).
+// direct part of tile (r, c): lane = row i, sum_j T(i, j) s_c[j]
+__device__ __forceinline__ double tile_direct(const double* __restrict__ T, const double* __restrict__ ss, int r,
+                                              int c, int th, int lane) {
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    if (th == TILE) {
+        if (r != c) {
+            const double2* sJ = reinterpret_cast<const double2*>(ss + c * TILE);
+#pragma unroll
+            for (int j = 0; j < TILE; j += 4) {
+                const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                d0 = fma(T[j * TILE + lane], u.x, d0);
+                d1 = fma(T[(j + 1) * TILE + lane], u.y, d1);
+                d2 = fma(T[(j + 2) * TILE + lane], v.x, d2);
+                d3 = fma(T[(j + 3) * TILE + lane], v.y, d3);
+            }
+        } else {
+            const double2* sJ = reinterpret_cast<const double2*>(ss + r * TILE);
+#pragma unroll
+            for (int j = 0; j < TILE; j += 4) {
+                const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                if (lane >= j) d0 = fma(T[diag_col_off(j) + lane - j], u.x, d0);
+                if (lane >= j + 1) d1 = fma(T[diag_col_off(j + 1) + lane - j - 1], u.y, d1);
+                if (lane >= j + 2) d2 = fma(T[diag_col_off(j + 2) + lane - j - 2], v.x, d2);
+                if (lane >= j + 3) d3 = fma(T[diag_col_off(j + 3) + lane - j - 3], v.y, d3);
+            }
+        }
+    } else if (lane < th) {                                // compact tail row
+        if (r != c) {
+            const double* sJ = ss + c * TILE;
+#pragma unroll 8
+            for (int j = 0; j < TILE; j += 2) {
+                d0 = fma(T[j * th + lane], sJ[j], d0);
+                d1 = fma(T[(j + 1) * th + lane], sJ[j + 1], d1);
+            }
+        } else {
+            const double* sJ = ss + r * TILE;
+            for (int j = 0; j <= lane; ++j) d0 = fma(T[tail_col_off(th, j) + lane - j], sJ[j], d0);
+        }
+    }
+    return (d0 + d1) + (d2 + d3);
+}
+
+// transposed part of tile (r, c): lane = column j, sum_i T(i, j) s_r[i]
+__device__ __forceinline__ double tile_trans(const double* __restrict__ T, const double* __restrict__ ss, int r,
+                                             int c, int th, int lane) {
+    const double* sI = ss + r * TILE;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    if (th == TILE) {
+        if (r != c) {
+            // 16-byte pairs along the rotated diagonal: lanes 8p..8p+7 of a
+            // quarter-warp phase hit 8 distinct 16-byte bank groups
+            const double2* Tc = reinterpret_cast<const double2*>(T + lane * TILE);
+            const double2* s2 = reinterpret_cast<const double2*>(sI);
+#pragma unroll
+            for (int t = 0; t < TILE / 2; t += 2) {
+                const int ua = (t + lane) & 15, ub = (t + 1 + lane) & 15;
+                const double2 a = Tc[ua], sa = s2[ua], b = Tc[ub], sb = s2[ub];
+                d0 = fma(a.x, sa.x, d0);
+                d1 = fma(a.y, sa.y, d1);
+                d2 = fma(b.x, sb.x, d2);
+                d3 = fma(b.y, sb.y, d3);
+            }
+        } else {
+            const double* Tc = T + diag_col_off(lane) - lane;   // (i, lane) at Tc[i], i >= lane
+#pragma unroll
+            for (int t = 0; t < TILE; t += 2) {
+                const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31;
+                if (ia >= lane) d0 = fma(Tc[ia], sI[ia], d0);
+                if (ib >= lane) d1 = fma(Tc[ib], sI[ib], d1);
+            }
+        }
+    } else if (r != c) {                                   // compact tail tile: rows i < th
+        const double* Tc = T + lane * th;
+        for (int i = 0; i < th; ++i) d0 = fma(Tc[i], sI[i], d0);
+    } else if (lane < th) {
+        const double* Tc = T + tail_col_off(th, lane) - lane;
+        for (int i = lane; i < th; ++i) d0 = fma(Tc[i], sI[i], d0);
+    }
+    return (d0 + d1) + (d2 + d3);
+}
+
 // ---- k_symv_ring2: row warps + column warps ----------------------------------
 // Same producer, ring, item buffers and epilogue as k_symv_ring; the 16
 // consumer warps split each tile's two products by role:
-//  * row warps (0-7): own tile rows r (owner (r + item counter) mod 8); lane i
-//    accumulates the direct part y_I[i] += sum_j S_IJ[i][j] s_J[j] in one
-//    register across the row's tiles, then writes pr[row] once;
+//  * row warps (0-7): own tile rows r; lane i accumulates the direct part
+//    y_I[i] += sum_j S_IJ[i][j] s_J[j] in one register across the row's
+//    tiles, then writes its partial row once.  split = 2 (default): warps 2p
+//    and 2p + 1 share rows r = (p + item counter) mod 4 (+4, +8, +12), one
+//    taking columns j < 16 of every tile, the other j >= 16 (partials pr, pr2),
+//    so a row streamed as consecutive chunks is consumed by two warps at once;
+//    split = 1: one warp per row (owner (r + item counter) mod 8);
 //  * column warps (8-15): own tile columns c; lane j accumulates the
 //    transposed part y_J[j] += sum_i S_IJ[i][j] s_I[i] walking the tile along a
 //    rotated diagonal (i = (t + j) mod 32: two wavefronts per load, no bank
 //    conflicts) with s_I rotated by shuffles; one register per owned column,
 //    written to pc[column] at the end of the item.
-// Every row and column has a single owner, so the item's result is
-// y = pr + pc (triangles) or pr | pc (rectangles: row block | column block)
-// -- two partial arrays instead of eight, no butterfly, ~40 registers per
-// consumer thread.
+// Every row half and column has a single owner, so the item's result is
+// y = (pr + pr2) + pc (triangles) or pr + pr2 | pc (rectangles: row block |
+// column block) -- three partial arrays instead of eight, no butterfly.
 constexpr int R2_ROWW = 8, R2_COLW = 8, R2_CONS = R2_ROWW + R2_COLW;
 constexpr int RING2_THREADS = (R2_CONS + 1 + RING_EPI_WARPS) * 32;
 __host__ __device__ constexpr size_t ring2_smem(int RT, int nst, int nb, int maxr) {
-    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * 3 * maxr * 8 + (size_t)nb * 8 * 4 +
-           (2 * (size_t)nst + 4 * (size_t)nb) * 8;
+    return (size_t)nst * RT * TILE_ELEMS * 8 + (size_t)nb * 4 * maxr * 8 + (size_t)nb * 8 * 4 +
+           (2 * (size_t)nst + 4 * (size_t)nb) * 8 + (size_t)RING_EPI_WARPS * maxr * 8;
 }
 
 template <int RT>
@@ -623,7 +710,7 @@ __global__ void __launch_bounds__(RING2_THREADS, 1)
 k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
              const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
              const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
-             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr, int pf) {
+             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr, int pf, int split) {
     pdl_wait();
     constexpr int SLOT = RT * TILE_ELEMS;
     if (*done) return;
@@ -632,13 +719,15 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
     double* s_sm = ring + (size_t)nst * SLOT;                    // [nb][maxr]
     double* pr_sm = s_sm + (size_t)nb * maxr;                    // [nb][maxr]  row (direct) parts
     double* pc_sm = pr_sm + (size_t)nb * maxr;                   // [nb][maxr]  column (transposed) parts
-    int32_t* dsc = reinterpret_cast<int32_t*>(pc_sm + (size_t)nb * maxr);   // [nb][8]
+    double* pr2_sm = pc_sm + (size_t)nb * maxr;                  // [nb][maxr]  second row half (split = 2)
+    int32_t* dsc = reinterpret_cast<int32_t*>(pr2_sm + (size_t)nb * maxr);  // [nb][8]
     uint64_t* full = reinterpret_cast<uint64_t*>(dsc + nb * 8);
     uint64_t* empty = full + nst;
     uint64_t* sfull = empty + nst;
     uint64_t* sempty = sfull + nb;
     uint64_t* pdone = sempty + nb;
     uint64_t* pfree = pdone + nb;
+    double* yt_sm = reinterpret_cast<double*>(pfree + nb);      // [RING_EPI_WARPS][maxr] strip transposed parts
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
     if (threadIdx.x == 0) {
@@ -668,9 +757,16 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
             dp.next(items, ops, ii, i1, it, op);
             if (pf > 0 && lane == 0 && ii + pf < i1) {           // L2 prefetch pf items ahead
                 const ItemDesc ip = items[ii + pf];
-                bulk_prefetch_l2(tiles + ip.tile_off, (unsigned)(item_doubles(ip.tri, ip.I1 - ip.I0, ip.ntiles) * 8));
+                bulk_prefetch_l2(tiles + ip.tile_off,
+                                 (unsigned)(item_doubles(ip.tri, ip.I1 - ip.I0, ip.ntiles, ip.tail) * 8));
             }
             const int rows_r = (it.I1 - it.I0) * TILE, rows_c = it.tri ? 0 : (it.J1 - it.J0) * TILE;
+            if (it.tail) {                      // compact last row: the epilogue warp applies it (strip);
+                it.ntiles -= it.I1 - it.I0;     // the ring streams the full rows 0 .. nT-2
+                it.I1 -= 1;
+                it.J1 -= 1;
+                it.tail = 0;
+            }
             if (bph > 0) mbar_wait(&sempty[bi], (bph - 1) & 1);
             if (lane == 0) {
                 int32_t* d = dsc + bi * 8;
@@ -699,7 +795,7 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
                     if (lane < nt) {
                         int I_, J_;
                         item_tile(it, l0 + lane, I_, J_);
-                        tb = (I_ == J_ ? DIAG_ELEMS : TILE_ELEMS) * 8u;
+                        tb = (unsigned)item_tile_doubles(it, I_, J_) * 8u;
                         toff = item_tile_off(it, l0 + lane, I_);
                     }
                     unsigned bytes = tb;
@@ -735,14 +831,54 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
 #pragma unroll
                 for (int r = 0; r < RING_MAX_ROWS / 32; ++r) zv[r] = (lane + 32 * r < nr) ? z[ix[r]] : 0.0;
             }
+            // compact last row (whole-operator triangles): the strip S (th x W,
+            // column-major, W = (nT - 1) 32) and its packed th x th diagonal
+            // tile, read from global memory while the consumers stream the
+            // rest: lane j of column block c adds S(:, 32c + j)^T s_tail to
+            // row 32c + j (a register per block), and the direct parts
+            // S(i, :) s are per-lane partials reduced over the warp
+            double* yT = yt_sm + (size_t)e * maxr;             // row 32 cb + lane: this lane's own entries
+            double ys = 0.0;
+            const int th = it.tail, W = (it.I1 - it.I0 - 1) * TILE;
+            if (th) {
+                const double* S = tiles + it.tile_off + item_tile_off(it, (it.I1 - it.I0 - 1) * (it.I1 - it.I0) / 2,
+                                                                      it.I1 - 1);
+                const double* sv = s + op.s_off + g0;              // s from global (L2): no hold on the s buffer
+                for (int x = lane; x < W; x += TILE) yT[x] = 0.0;
+                for (int i = 0; i < th; ++i) {                    // strip row i (L1 serves the re-reads)
+                    const double si = __ldg(sv + W + i);
+                    double d = 0.0;
+#pragma unroll
+                    for (int cb = 0; cb < RING_MAX_ROWS / 32; ++cb)
+                        if (cb * TILE < W) {
+                            const double v = __ldg(S + (int64_t)(cb * TILE + lane) * th + i);
+                            yT[cb * TILE + lane] = fma(v, si, yT[cb * TILE + lane]);
+                            d = fma(v, __ldg(sv + cb * TILE + lane), d);
+                        }
+                    d = warp_sum(d);
+                    if (lane == i) ys = d;
+                }
+                // diagonal tile: lane i < th, direct L'(i, :) and transposed L'(:, i)^T parts
+                const double* D = S + (int64_t)W * th;
+                if (lane < th) {
+                    double dg = 0.0;
+                    for (int j = 0; j <= lane; ++j) dg = fma(D[tail_col_off(th, j) + lane - j], __ldg(sv + W + j), dg);
+                    for (int i = lane; i < th; ++i)
+                        dg = fma(D[tail_col_off(th, lane) + i - lane], __ldg(sv + W + i), dg);
+                    ys += dg;
+                }
+            }
             mbar_wait(&pdone[b], ph & 1);
             const double* pr = pr_sm + (size_t)b * maxr;
             const double* pc = pc_sm + (size_t)b * maxr;
+            const double* pr2 = pr2_sm + (size_t)b * maxr;
 #pragma unroll
             for (int r = 0; r < RING_MAX_ROWS / 32; ++r) {
                 const int x = lane + 32 * r;
                 if (x < rows_t) {
-                    const double y = it.tri ? pr[x] + pc[x] : (x < rows_r ? pr[x] : pc[x]);
+                    const double pxr = split == 2 ? pr[x] + pr2[x] : pr[x];
+                    const double y = th ? (x < W ? pxr + pc[x] + yT[x] : ys)
+                                        : (it.tri ? pxr + pc[x] : (x < rows_r ? pxr : pc[x]));
                     if (it.part_off >= 0) partials[it.part_off + x] = y;
                     else if (x < nr) {
                         if (scat) z[ix[r]] = zv[r] + y;
@@ -773,9 +909,12 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
         double* pc = pc_sm + (size_t)bi * maxr;
         if (bph > 0) mbar_wait(&pfree[bi], (bph - 1) & 1);
         // own tiles in increasing stream index l:
-        //   row warp:    rows a, a + 8 (a = (wr - ki) mod 8), each row's tiles in order
+        //   row warp:    rows a, a + rstep, ... (split 1: a = (wr - ki) mod 8, rstep 8;
+        //                split 2: a = (wr / 2 - ki) mod 4, rstep 4, column half wr & 1)
         //   column warp: columns a, a + 8; per row r both owned columns in order
-        const int a = (wr - ki) & 7;
+        const int rstep = (!colw && split == 2) ? 4 : 8, hh = (!colw && split == 2) ? (wr & 1) : 0;
+        const int a = (!colw && split == 2) ? ((wr >> 1) - ki) & 3 : (wr - ki) & 7;
+        if (hh) pr = pr2_sm + (size_t)bi * maxr;
         int l = -1, r = 0, c = 0, ccur = 0;
         double acc = 0.0, acc0 = 0.0, acc1 = 0.0;
         auto rowstart = [&](int rr) { return tri ? rr * (rr + 1) / 2 : rr * wd; };
@@ -793,7 +932,7 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
         auto advance = [&]() {
             if (!colw) {
                 if (++c < rowlen(r)) { ++l; return; }
-                r += 8;
+                r += rstep;
                 if (r >= h) { l = -1; return; }
                 c = 0;
                 l = rowstart(r);
@@ -818,21 +957,36 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
                 const double* T = C + (l - l0) * TILE_ELEMS;
                 const bool diag = tri && r == c;
                 if (!colw) {
-                    // direct part: lane = row, s_J broadcast
+                    // direct part: lane = row, s_J broadcast; columns [j0, j0 + jn)
                     const double2* sJ = reinterpret_cast<const double2*>(ss + (tri ? c * TILE : rows_r + c * TILE));
                     double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
                     if (!diag) {
+                        if (split == 2) {
+                            const double* Th = T + hh * 16 * TILE;
+                            const double2* sh = sJ + hh * 8;
 #pragma unroll
-                        for (int j = 0; j < TILE; j += 4) {
-                            const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
-                            d0 = fma(T[j * TILE + lane], u.x, d0);
-                            d1 = fma(T[(j + 1) * TILE + lane], u.y, d1);
-                            d2 = fma(T[(j + 2) * TILE + lane], v.x, d2);
-                            d3 = fma(T[(j + 3) * TILE + lane], v.y, d3);
+                            for (int j = 0; j < 16; j += 4) {
+                                const double2 u = sh[j / 2], v = sh[j / 2 + 1];
+                                d0 = fma(Th[j * TILE + lane], u.x, d0);
+                                d1 = fma(Th[(j + 1) * TILE + lane], u.y, d1);
+                                d2 = fma(Th[(j + 2) * TILE + lane], v.x, d2);
+                                d3 = fma(Th[(j + 3) * TILE + lane], v.y, d3);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < TILE; j += 4) {
+                                const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
+                                d0 = fma(T[j * TILE + lane], u.x, d0);
+                                d1 = fma(T[(j + 1) * TILE + lane], u.y, d1);
+                                d2 = fma(T[(j + 2) * TILE + lane], v.x, d2);
+                                d3 = fma(T[(j + 3) * TILE + lane], v.y, d3);
+                            }
                         }
                     } else {
-#pragma unroll
-                        for (int j = 0; j < TILE; j += 4) {
+                        const int j0 = split == 2 ? hh * 16 : 0, jn = split == 2 ? 16 : TILE;
+#pragma unroll 4
+                        for (int jj = 0; jj < jn; jj += 4) {
+                            const int j = j0 + jj;
                             const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
                             if (lane >= j) d0 = fma(T[diag_col_off(j) + lane - j], u.x, d0);
                             if (lane >= j + 1) d1 = fma(T[diag_col_off(j + 1) + lane - j - 1], u.y, d1);
@@ -889,89 +1043,50 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
 // ---- k_symv_whole: whole small triangles, one bulk copy per item -------------
 // For colours whose operators are single small triangles (C3: m <= 160, at most
 // 5 x 5 tiles = 103 KB) the whole item fits in shared memory twice.  Item k of
-// a CTA's byte-balanced range lands in buffer k & 1 by ONE bulk copy of its
-// contiguous tiles plus one of its s segment (one mbarrier); the 16 consumer
-// warps then split the item's (nT + 1) nT contributions -- for output segment
-// g: the direct parts of tiles (g, 0..g), the transposed part of diagonal tile
-// (g, g), the transposed parts of tiles (g+1..nT-1, g) -- two per warp, each a
-// 32-vector written to shared memory.  One named barrier per item; then thread
-// x sums segment x / 32's contributions in that fixed order (deterministic)
-// and applies z[idx[x]] += y, with idx and z fetched before the item's data
-// was waited for (same-colour subdomains are disjoint).  Compared with the
-// chunked ring, the consumers synchronise twice per item instead of once per
-// 4-tile chunk, and the producer issues two copies per item instead of one
-// per tile.
-// consumer warps: 16 (two contributions each at nT = 5) or 30 (one each);
-// + a producer warp and a staging warp
+// a CTA's byte-balanced range lands in buffer k & 1 by one bulk copy of its
+// contiguous tiles (compact last row) plus its s segment and its index list
+// (one mbarrier); the producer writes the item's sizes next to them.  The 16
+// consumer warps split the item's (nT + 1) nT contributions -- for output
+// segment g: the direct parts of tiles (g, 0..g), the transposed part of
+// diagonal tile (g, g), the transposed parts of tiles (g+1..nT-1, g) -- two per
+// warp, each a 32-vector written to shared memory.  One named barrier per item;
+// then thread x sums segment x / 32's contributions in that fixed order
+// (deterministic) and applies z[idx[x]] += y.  Its z value is loaded as soon
+// as the item lands, so the load overlaps the item's products (same-colour
+// subdomains are disjoint), and no consumer ever waits on a descriptor or
+// index load from global memory.
 constexpr int WH_MAX_NT = 5;
 constexpr int WH_MAX_ROWS = WH_MAX_NT * TILE;
+constexpr int WH_CONS = 16;
 __host__ __device__ constexpr int64_t wh_item_doubles(int nT) {
     return (int64_t)(nT * (nT + 1) / 2 - nT) * TILE_ELEMS + (int64_t)nT * DIAG_ELEMS;
 }
-// tiles [2][BUFD] | s [2][nT 32] | contributions [2][(nT+1) nT][32] | z values [4][160] |
-// row indices [4][160] | item sizes [4][2] | mbarriers full[2], empty[2], pfull[4], pdone[4]
+// tiles [2][BUFD] | s [2][nT 32] | contributions [2][(nT+1) nT][32] | row indices [2][160] |
+// item sizes [2][4] | mbarriers full[2], empty[2]
 __host__ __device__ constexpr size_t wh_smem(int nT) {
     return 2 * (size_t)((wh_item_doubles(nT) + 15) / 16 * 16) * 8 + 2 * (size_t)nT * TILE * 8 +
-           2 * (size_t)(nT + 1) * nT * TILE * 8 + 4 * (size_t)WH_MAX_ROWS * 12 + 4 * 8 + 12 * 8;
+           2 * (size_t)(nT + 1) * nT * TILE * 8 + 2 * (size_t)WH_MAX_ROWS * 4 + 2 * 4 * 4 + 4 * 8;
+}
+// first double of tile (r, c) of a whole-operator triangle (tail: compact last row)
+__device__ __forceinline__ int wh_toff(int r, int c, int nT, int tail) {
+    const int base = (r * (r + 1) / 2 - r) * TILE_ELEMS + r * DIAG_ELEMS;   // rows 0..r-1
+    return base + c * ((tail && r == nT - 1) ? tail * TILE : TILE_ELEMS);
 }
 
-// contribution q = g (nT + 1) + k of a triangle with nT tile rows (see above)
-__device__ __forceinline__ double wh_contrib(const double* __restrict__ T0, const double* __restrict__ ss, int nT, int q,
-                                             int lane) {
-    const int g = q / (nT + 1), k = q % (nT + 1);
-    auto toff = [](int r, int c) { return (r * (r + 1) / 2 + c - r) * TILE_ELEMS + r * DIAG_ELEMS; };
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-    if (k < g) {                                           // direct, off-diagonal tile (g, k): lane = row
-        const double* T = T0 + toff(g, k);
-        const double2* sJ = reinterpret_cast<const double2*>(ss + k * TILE);
-#pragma unroll
-        for (int j = 0; j < TILE; j += 4) {
-            const double2 u = sJ[j / 2], v = sJ[j / 2 + 1];
-            d0 = fma(T[j * TILE + lane], u.x, d0);
-            d1 = fma(T[(j + 1) * TILE + lane], u.y, d1);
-            d2 = fma(T[(j + 2) * TILE + lane], v.x, d2);
-            d3 = fma(T[(j + 3) * TILE + lane], v.y, d3);
-        }
-    } else if (k == g) {                                   // direct, diagonal tile: lower L'
-        const double* T = T0 + toff(g, g);
-        const double* sJ = ss + g * TILE;
-#pragma unroll
-        for (int j = 0; j < TILE; j += 2) {
-            if (lane >= j) d0 = fma(T[diag_col_off(j) + lane - j], sJ[j], d0);
-            if (lane >= j + 1) d1 = fma(T[diag_col_off(j + 1) + lane - j - 1], sJ[j + 1], d1);
-        }
-    } else if (k == g + 1) {                               // transposed, diagonal tile: L'^T
-        const double* Tc = T0 + toff(g, g) + diag_col_off(lane) - lane;   // (i, lane) at Tc[i], i >= lane
-        const double* sI = ss + g * TILE;
-#pragma unroll
-        for (int t = 0; t < TILE; t += 2) {
-            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31;
-            if (ia >= lane) d0 = fma(Tc[ia], sI[ia], d0);
-            if (ib >= lane) d1 = fma(Tc[ib], sI[ib], d1);
-        }
-    } else {                                               // transposed, tile (k - 1, g): lane = column
-        const int r = k - 1;
-        const double* T = T0 + toff(r, g) + lane * TILE;
-        const double* sI = ss + r * TILE;
-#pragma unroll
-        for (int t = 0; t < TILE; t += 4) {
-            const int ia = (t + lane) & 31, ib = (t + 1 + lane) & 31, ic = (t + 2 + lane) & 31,
-                      id = (t + 3 + lane) & 31;
-            d0 = fma(T[ia], sI[ia], d0);
-            d1 = fma(T[ib], sI[ib], d1);
-            d2 = fma(T[ic], sI[ic], d2);
-            d3 = fma(T[id], sI[id], d3);
-        }
-    }
-    return (d0 + d1) + (d2 + d3);
+// contribution (g, k) of a triangle with nT tile rows (see above)
+__device__ __forceinline__ double wh_contrib(const double* __restrict__ T0, const double* __restrict__ ss, int nT,
+                                             int tail, int g, int k, int lane) {
+    const int thg = (tail && g == nT - 1) ? tail : TILE;
+    if (k <= g) return tile_direct(T0 + wh_toff(g, k, nT, tail), ss, g, k, thg, lane);
+    if (k == g + 1) return tile_trans(T0 + wh_toff(g, g, nT, tail), ss, g, g, thg, lane);
+    const int r = k - 1;
+    return tile_trans(T0 + wh_toff(r, g, nT, tail), ss, r, g, (tail && r == nT - 1) ? tail : TILE, lane);
 }
 
-template <int WH_CONS>
-__global__ void __launch_bounds__((WH_CONS + 2) * 32, 1)
+__global__ void __launch_bounds__((WH_CONS + 1) * 32, 1)
 k_symv_whole(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
              const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
-             const int32_t* __restrict__ oidx, double* __restrict__ z, const int32_t* done, int nTmax, int split,
-             int pf, int stage) {
+             const int32_t* __restrict__ oidx, double* __restrict__ z, const int32_t* done, int nTmax, int split) {
     pdl_wait();
     if (*done) return;
     extern __shared__ __align__(128) double wsm[];
@@ -979,13 +1094,10 @@ k_symv_whole(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
     double* tbuf = wsm;                                        // [2][BUFD]
     double* sbuf = tbuf + 2 * BUFD;                            // [2][nTmax * 32]
     double* cbuf = sbuf + 2 * nTmax * TILE;                    // [2][(nTmax + 1) nTmax][32]
-    double* zbuf = cbuf + 2 * (nTmax + 1) * nTmax * TILE;      // [4][WH_MAX_ROWS]  z[idx[x]] before the item
-    int32_t* ibuf = reinterpret_cast<int32_t*>(zbuf + 4 * WH_MAX_ROWS);   // [4][WH_MAX_ROWS] idx[x]
-    int32_t* dbuf = ibuf + 4 * WH_MAX_ROWS;                    // [4][2]: nT, m
-    uint64_t* full = reinterpret_cast<uint64_t*>(dbuf + 8);    // [2] tiles + s landed
-    uint64_t* empty = full + 2;                                // [2] tiles + s consumed
-    uint64_t* pfull = empty + 2;                               // [4] sizes, idx, z staged
-    uint64_t* pdone = pfull + 4;                               // [4] epilogue done with the slot
+    int32_t* ibuf = reinterpret_cast<int32_t*>(cbuf + 2 * (nTmax + 1) * nTmax * TILE);   // [2][WH_MAX_ROWS]
+    int32_t* dbuf = ibuf + 2 * WH_MAX_ROWS;                    // [2][4]: nT, m, tail
+    uint64_t* full = reinterpret_cast<uint64_t*>(dbuf + 8);    // [2] tiles, s, idx landed
+    uint64_t* empty = full + 2;                                // [2] consumed
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = item_begin + cta_part[blockIdx.x], i1 = item_begin + cta_part[blockIdx.x + 1];
     if (threadIdx.x == 0) {
@@ -993,41 +1105,35 @@ k_symv_whole(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], 1);
         }
-        for (int b = 0; b < 4; ++b) {
-            mbar_init(&pfull[b], 1);
-            mbar_init(&pdone[b], 1);
-        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (i0 >= i1) return;
     if (warp == WH_CONS) {                                     // ---- producer: bulk copies ----
         if (lane != 0) return;
-        // L2 prefetch of the next pf items: the DRAM stream runs pf items ahead
-        // of the two shared-memory buffers (more bytes in flight per SM than
-        // shared memory holds)
-        for (int k = 0; k < pf && k < i1 - i0; ++k) {
-            const ItemDesc it = items[i0 + k];
-            bulk_prefetch_l2(tiles + it.tile_off, (unsigned)(wh_item_doubles(it.I1 - it.I0) * 8));
-        }
+        DescPipe dp;
+        dp.init(items, ops, i0, i1);
         for (int k = 0; k < i1 - i0; ++k) {
             const int b = k & 1;
-            if (pf > 0 && k + pf < i1 - i0) {
-                const ItemDesc itp = items[i0 + k + pf];
-                bulk_prefetch_l2(tiles + itp.tile_off, (unsigned)(wh_item_doubles(itp.I1 - itp.I0) * 8));
-            }
+            ItemDesc it;
+            OpDesc op;
+            dp.next(items, ops, i0 + k, i1, it, op);
             if (k >= 2) mbar_wait(&empty[b], ((k - 2) >> 1) & 1);
-            const ItemDesc it = items[i0 + k];
-            const int64_t s_off = ops[it.op].s_off;
             const int h = it.I1 - it.I0;
-            const unsigned tb = (unsigned)(wh_item_doubles(h) * 8), sb = (unsigned)(h * TILE * 8);
-            mbar_expect_tx(&full[b], tb + sb);
-            bulk_g2s(sbuf + b * nTmax * TILE, s + s_off + it.I0 * TILE, sb, &full[b]);
+            int32_t* d = dbuf + b * 4;
+            d[0] = h;
+            d[1] = op.m;
+            d[2] = it.tail;
+            const unsigned tb = (unsigned)(item_doubles(1, h, it.ntiles, it.tail) * 8),
+                           sb = (unsigned)(h * TILE * 8), ib = (unsigned)((op.m + 3) / 4 * 16);
+            mbar_expect_tx(&full[b], tb + sb + ib);            // arrive (release: the sizes)
+            bulk_g2s(sbuf + b * nTmax * TILE, s + op.s_off, sb, &full[b]);
+            bulk_g2s(ibuf + b * WH_MAX_ROWS, oidx + op.idx_off, ib, &full[b]);
             const double* src = tiles + it.tile_off;
             double* dst = tbuf + b * BUFD;
-            if ((split & 0xff) <= 1) {
+            if ((split & 0xff) <= 1 || it.tail) {
                 bulk_g2s(dst, src, tb, &full[b]);
-            } else {                                           // one copy per tile row
+            } else {                                           // one copy per tile row (experiment)
                 for (int r = 0; r < h; ++r) {
                     const int64_t o0 = (int64_t)(r * (r + 1) / 2 - r) * TILE_ELEMS + (int64_t)r * DIAG_ELEMS;
                     const unsigned rb = (unsigned)((r * TILE_ELEMS + DIAG_ELEMS) * 8);
@@ -1037,73 +1143,36 @@ k_symv_whole(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
         }
         return;
     }
-    if (warp == WH_CONS + 1) {                                 // ---- prefetch: sizes, idx, z ----
-        // runs up to 3 items ahead of the consumers (4 staging slots)
-        if (!stage) return;
-        for (int k = 0; k < i1 - i0; ++k) {
-            const int ps = k & 3;
-            if (k >= 4) mbar_wait(&pdone[ps], ((k - 4) >> 2) & 1);
-            const ItemDesc it = items[i0 + k];
-            const OpDesc op = ops[it.op];
-            const int nT = it.I1 - it.I0, nr = min(nT * TILE, op.m);
-            const int32_t* idx = oidx + op.idx_off;
-            int ix[WH_MAX_ROWS / 32];
-#pragma unroll
-            for (int t = 0; t < WH_MAX_ROWS / 32; ++t) ix[t] = lane + 32 * t < nr ? idx[lane + 32 * t] : 0;
-#pragma unroll
-            for (int t = 0; t < WH_MAX_ROWS / 32; ++t)
-                if (lane + 32 * t < nr) {
-                    zbuf[ps * WH_MAX_ROWS + lane + 32 * t] = z[ix[t]];
-                    ibuf[ps * WH_MAX_ROWS + lane + 32 * t] = ix[t];
-                }
-            if (lane == 0) {
-                dbuf[ps * 2] = nT;
-                dbuf[ps * 2 + 1] = nr;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pfull[ps]);            // release: the warp's shared stores
-        }
-        return;
-    }
-    // ---- consumers: contribution q = warp (+ WH_CONS ...) of each item ----
+    // ---- consumers: contributions q = warp, warp + 16 of each item ----
     const int tid = threadIdx.x;
     for (int k = 0; k < i1 - i0; ++k) {
-        const int b = k & 1, ps = k & 3;
-        int nT, nr, ixk = 0;
-        double zvk = 0.0;
-        if (stage) {
-            mbar_wait(&pfull[ps], (k >> 2) & 1);
-            nT = dbuf[ps * 2];
-            nr = dbuf[ps * 2 + 1];
-        } else {                                               // this row's index and z, before the data wait
-            const ItemDesc it = items[i0 + k];
-            const OpDesc op = ops[it.op];
-            nT = it.I1 - it.I0;
-            nr = min(nT * TILE, op.m);
-            if (tid < nr) {
-                ixk = oidx[op.idx_off + tid];
-                zvk = z[ixk];
-            }
-        }
+        const int b = k & 1;
         mbar_wait(&full[b], (k >> 1) & 1);
+        const int32_t* d = dbuf + b * 4;
+        const int nT = d[0], nr = d[1], tail = d[2];
+        int ixk = 0;
+        double zvk = 0.0;
+        if (tid < nr) {                                        // z now, used after the products
+            ixk = ibuf[b * WH_MAX_ROWS + tid];
+            zvk = z[ixk];
+        }
         const double* T0 = tbuf + b * BUFD;
         const double* ss = sbuf + b * nTmax * TILE;
         double* cb = cbuf + b * (nTmax + 1) * nTmax * TILE;
-        const int nq = (nT + 1) * nT;
+        const int nq = (nT + 1) * nT, inv = (256 + nT) / (nT + 1);   // q / (nT + 1) = (q * inv) >> 8, q < 32
         if (!(split & 0x100))                                  // DDG_RING_WHOLE bit 8: copy-only probe (debug)
-            for (int q = warp; q < nq; q += WH_CONS) cb[q * TILE + lane] = wh_contrib(T0, ss, nT, q, lane);
+            for (int q = warp; q < nq; q += WH_CONS) {
+                const int g = (q * inv) >> 8, kk = q - g * (nT + 1);
+                cb[q * TILE + lane] = wh_contrib(T0, ss, nT, tail, g, kk, lane);
+            }
         asm volatile("bar.sync 1, %0;" ::"n"(WH_CONS * 32) : "memory");
-        if (tid == 0) {
-            mbar_arrive(&empty[b]);                            // tiles and s of buffer b consumed
-            if (k >= 1) mbar_arrive(&pdone[(k - 1) & 3]);      // every thread is past item k-1's epilogue
-        }
+        if (tid == 0) mbar_arrive(&empty[b]);                  // tiles, s and idx of buffer b consumed
         if (tid < nr) {
             const int g = tid >> 5;
             const double* c = cb + g * (nT + 1) * TILE + (tid & 31);
             double y = 0.0;
             for (int kk = 0; kk <= nT; ++kk) y += c[kk * TILE];
-            if (stage) z[ibuf[ps * WH_MAX_ROWS + tid]] = zbuf[ps * WH_MAX_ROWS + tid] + y;
-            else z[ixk] = zvk + y;
+            z[ixk] = zvk + y;
         }
     }
 }
@@ -1186,8 +1255,9 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
 }
 
 static bool g_ring_init[64] = {};
-static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0, g_ring_v2 = 0, g_ring_whole = 1, g_whole_pf = 2,
-           g_ring_pf = 0, g_whole_stage = 0, g_whole_warps = 16;
+static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0, g_ring_v2 = 0, g_ring_whole = 1, g_ring_pf = 0,
+           g_ring2_split = 2;
+int g_compact = 1;   // compact tails for whole-triangle colours (DDG_COMPACT)
 static unsigned long long* g_ring_trace = nullptr;   // DDG_RING_TRACE (debug)
 // per device, once, outside any stream capture (called from ddg_setup)
 void symv_ring_init() {
@@ -1202,10 +1272,13 @@ void symv_ring_init() {
     g_pdl = getenv("DDG_PDL") ? (atoi(getenv("DDG_PDL")) != 0) : 1;
     // DDG_RING_WHOLE: 0 off, 1 (default) one copy per item, n > 1 one copy per tile row
     g_ring_whole = getenv("DDG_RING_WHOLE") ? atoi(getenv("DDG_RING_WHOLE")) : 1;
-    g_whole_pf = getenv("DDG_WHOLE_PF") ? atoi(getenv("DDG_WHOLE_PF")) : 0;   // items prefetched to L2 ahead
+    g_ring2_split = (getenv("DDG_RING2_SPLIT") && atoi(getenv("DDG_RING2_SPLIT")) == 1) ? 1 : 2;
     g_ring_pf = getenv("DDG_RING_PF") ? atoi(getenv("DDG_RING_PF")) : 0;      // ... by k_symv_ring2
-    g_whole_stage = getenv("DDG_WHOLE_STAGE") ? atoi(getenv("DDG_WHOLE_STAGE")) : 0;   // staging warp
-    g_whole_warps = getenv("DDG_WHOLE_WARPS") ? atoi(getenv("DDG_WHOLE_WARPS")) : 16;  // 16 or 30 consumers
+    // DDG_COMPACT (default 1): whole-triangle operators store their last tile
+    // row compact (no padding rows streamed); read by every kernel but the
+    // 8-warp ring, which is only chosen for triangles when forced (DDG_RING_V2=0)
+    g_compact = (g_ring_v2 == 0) ? 0 : 1;
+    if (const char* e = getenv("DDG_COMPACT")) g_compact = atoi(e) != 0;
 
     if (getenv("DDG_RING_TRACE") && !g_ring_trace) {
         if (cudaMalloc(&g_ring_trace, 32 * sizeof(unsigned long long)) == cudaSuccess)
@@ -1223,8 +1296,7 @@ void symv_ring_init() {
     cudaFuncSetAttribute(k_symv_ring2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-    cudaFuncSetAttribute(k_symv_whole<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-    cudaFuncSetAttribute(k_symv_whole<30>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(k_symv_whole, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     g_ring_init[dev & 63] = true;
 }
 
@@ -1248,12 +1320,8 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     // whole small triangles (C3): one bulk copy per item, k_symv_whole
     const int nTw = (std::max(TILE, max_rows_r) + TILE - 1) / TILE;
     if (triangles && g_ring_whole && nTw <= WH_MAX_NT && max_rows_c == 0 && wh_smem(nTw) <= budget) {
-        if (g_whole_warps == 30)
-            launch_pdl(k_symv_whole<30>, ncta, 32 * 32, wh_smem(nTw), st, ops, items, item_begin, cta_part, tiles,
-                       s, oidx, z, done, nTw, g_ring_whole, g_whole_pf, g_whole_stage);
-        else
-            launch_pdl(k_symv_whole<16>, ncta, 18 * 32, wh_smem(nTw), st, ops, items, item_begin, cta_part, tiles,
-                       s, oidx, z, done, nTw, g_ring_whole, g_whole_pf, g_whole_stage);
+        launch_pdl(k_symv_whole, ncta, (WH_CONS + 1) * 32, wh_smem(nTw), st, ops, items, item_begin, cta_part, tiles,
+                   s, oidx, z, done, nTw, g_ring_whole);
         return;
     }
     // row/column-warp consumers for launches of whole-subdomain triangles
@@ -1267,13 +1335,13 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
         const size_t smem2 = ring2_smem(RT, nst2, nb2, maxr);
         if (RT == 2)
             launch_pdl(k_symv_ring2<2>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
-                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf);
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf, g_ring2_split);
         else if (RT == 8)
             launch_pdl(k_symv_ring2<8>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
-                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf);
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf, g_ring2_split);
         else
             launch_pdl(k_symv_ring2<4>, ncta, RING2_THREADS, smem2, st, ops, items, item_begin, cta_part, tiles, s,
-                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf);
+                       oidx, z, y_out, partials, done, nst2, nb2, maxr, g_ring_pf, g_ring2_split);
         return;
     }
     // item buffers: deep for small items (s copies and epilogues overlap

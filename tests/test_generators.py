@@ -156,3 +156,26 @@ def test_poisson3d_mixed_boundary_rows():
     B = P.poisson3d_mixed(2, 2, 0).dense()
     assert np.array_equal(np.diag(B), [4, 4, 4, 4, 3, 3, 3, 3])
     assert (B[0] == np.array([4, -1, -1, 0, -1, 0, 0, 0])).all()
+
+
+@pytest.mark.parametrize("mk,nparts", [(lambda: P.lognormal3d(16, 4, 1, 32), 64),
+                                        (lambda: P.biharmonic2d(64, 16, 3, 34), 20),
+                                        (lambda: P.elasticity3d(8, 4, 35), 10)])
+def test_grown_partition_connected_irregular(mk, nparts):
+    """grown_partition: every node in one of nparts non-empty parts, each part
+    connected in the graph of A, sizes not all equal, deterministic in the seed,
+    and the matrix, F and f untouched"""
+    import scipy.sparse.csgraph as cg
+    pr = mk()
+    g = P.grown_partition(pr, nparts, 9)
+    assert g.part.shape == (pr.n,) and g.part.min() == 0 and g.part.max() == nparts - 1
+    sz = np.bincount(g.part, minlength=nparts)
+    assert sz.min() > 0 and sz.min() < sz.max()
+    A = pr.scipy()
+    for q in range(nparts):
+        idx = np.flatnonzero(g.part == q)
+        ncomp, _ = cg.connected_components(A[idx][:, idx], directed=False)
+        assert ncomp == 1, q
+    assert np.array_equal(P.grown_partition(pr, nparts, 9).part, g.part)
+    assert not np.array_equal(P.grown_partition(pr, nparts, 10).part, g.part)
+    assert g.val is pr.val and g.F is pr.F and g.f is pr.f and g.block_coords is None

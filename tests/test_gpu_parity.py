@@ -277,13 +277,17 @@ def test_comm_path_single_rank(name):
 # each path is also forced explicitly (switches are read at ddg_setup).
 PATHS = {
     "ring_everywhere": {"DDG_RING_MIN_MB": "0"},                 # ring for every SYMV launch (auto: k_symv_whole
-                                                                 # for small whole triangles)
-    "whole_staged": {"DDG_RING_MIN_MB": "0", "DDG_WHOLE_STAGE": "1"},   # k_symv_whole, staging warp
+                                                                 # for small whole triangles, compact last rows)
+    "whole_full_tiles": {"DDG_RING_MIN_MB": "0", "DDG_COMPACT": "0"},   # k_symv_whole on padded last rows
     "whole_rowcopies": {"DDG_RING_MIN_MB": "0", "DDG_RING_WHOLE": "2"},  # k_symv_whole, one copy per tile row
+    "ring2_full_tiles": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0", "DDG_COMPACT": "0"},
+    "ring2_split1": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0", "DDG_RING2_SPLIT": "1"},
     "ring1_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "0", "DDG_RING_WHOLE": "0"},  # 8-warp columns
     "ring_2tile_slots": {"DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2", "DDG_RING_WHOLE": "0"},
-    "ring2_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0"},  # row/column warps
+    "ring2_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0"},  # row/column warps,
+                                                                                              # compact last rows
     "classic": {"DDG_SYMV": "classic"},                           # per-item k_symv / k_symv_small
+    "compact_classic": {"DDG_RING_MIN_MB": "1e9"},                # per-item kernels on compact-tail operators
     "coarse_levels": {"DDG_COARSE_DATAFLOW": "0", "DDG_RING_MIN_MB": "0"},  # level-by-level sparse solve
     "csr_rows": {"DDG_NO_STENCIL": "1"},                          # row kernels read the CSR
 }
