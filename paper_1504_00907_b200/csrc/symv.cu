@@ -1,5 +1,7 @@
 // symv.cu — colour-sweep kernels (a4, a8): flat residual gather, per-item SYMV, the persistent bulk-copy-ring SYMVs, partial reduction
 // (part of libddg's sm_100a kernels; shared device helpers in kernel_common.cuh)
+#include <cstring>
+
 #include "kernel_common.cuh"
 
 namespace ddg {
@@ -1073,6 +1075,13 @@ __device__ __forceinline__ int wh_toff(int r, int c, int nT, int tail) {
     return base + c * ((tail && r == nT - 1) ? tail * TILE : TILE_ELEMS);
 }
 
+// Work plan of the 16 consumer warps for a triangle of nT <= 5 tile rows: up
+// to 3 contributions q = g (nT + 1) + k each, balanced by longest-processing-
+// time first over measured-cost weights (host wh_plan_init).
+constexpr int WH_PLAN_U = 3;
+constexpr int WH_PLANS = 2;   // 0: q = warp, warp + 16; 1: LPT
+__constant__ int8_t c_wh_plan[WH_PLANS][WH_MAX_NT + 1][WH_CONS][WH_PLAN_U];
+
 // contribution (g, k) of a triangle with nT tile rows (see above)
 __device__ __forceinline__ double wh_contrib(const double* __restrict__ T0, const double* __restrict__ ss, int nT,
                                              int tail, int g, int k, int lane) {
@@ -1083,10 +1092,11 @@ __device__ __forceinline__ double wh_contrib(const double* __restrict__ T0, cons
     return tile_trans(T0 + wh_toff(r, g, nT, tail), ss, r, g, (tail && r == nT - 1) ? tail : TILE, lane);
 }
 
-__global__ void __launch_bounds__((WH_CONS + 1) * 32, 1)
+__global__ void __launch_bounds__((WH_CONS + 1) * 32, 1)   // 5 warps on one SM sub-partition: 96 registers
 k_symv_whole(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
              const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
-             const int32_t* __restrict__ oidx, double* __restrict__ z, const int32_t* done, int nTmax, int split) {
+             const int32_t* __restrict__ oidx, double* __restrict__ z, const int32_t* done, int nTmax, int split,
+             int plan) {
     pdl_wait();
     if (*done) return;
     extern __shared__ __align__(128) double wsm[];
@@ -1159,9 +1169,12 @@ k_symv_whole(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
         const double* T0 = tbuf + b * BUFD;
         const double* ss = sbuf + b * nTmax * TILE;
         double* cb = cbuf + b * (nTmax + 1) * nTmax * TILE;
-        const int nq = (nT + 1) * nT, inv = (256 + nT) / (nT + 1);   // q / (nT + 1) = (q * inv) >> 8, q < 32
+        const int inv = (256 + nT) / (nT + 1);                 // q / (nT + 1) = (q * inv) >> 8, q < 32
         if (!(split & 0x100))                                  // DDG_RING_WHOLE bit 8: copy-only probe (debug)
-            for (int q = warp; q < nq; q += WH_CONS) {
+#pragma unroll
+            for (int u = 0; u < WH_PLAN_U; ++u) {
+                const int q = c_wh_plan[plan][nT][warp][u];
+                if (q < 0) break;
                 const int g = (q * inv) >> 8, kk = q - g * (nT + 1);
                 cb[q * TILE + lane] = wh_contrib(T0, ss, nT, tail, g, kk, lane);
             }
@@ -1259,6 +1272,8 @@ static int g_ring_rt = 4, g_ring_nb = 0, g_ring_nst = 0, g_ring_v2 = 0, g_ring_w
            g_ring2_split = 2;
 int g_compact = 1;   // compact tails for whole-triangle colours (DDG_COMPACT)
 static unsigned long long* g_ring_trace = nullptr;   // DDG_RING_TRACE (debug)
+static void wh_plan_init();
+static int g_whole_plan = 0;   // DDG_WHOLE_PLAN (WH_PLANS; 0 measured best: C3 0.949 vs LPT 0.914)
 // per device, once, outside any stream capture (called from ddg_setup)
 void symv_ring_init() {
     g_ring_rt = 4;
@@ -1286,6 +1301,7 @@ void symv_ring_init() {
         else
             g_ring_trace = nullptr;
     }
+    g_whole_plan = getenv("DDG_WHOLE_PLAN") ? std::max(0, std::min(WH_PLANS - 1, atoi(getenv("DDG_WHOLE_PLAN")))) : 0;
     int dev = 0;
     cudaGetDevice(&dev);
     if (g_ring_init[dev & 63]) return;
@@ -1297,7 +1313,42 @@ void symv_ring_init() {
     cudaFuncSetAttribute(k_symv_ring2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_ring2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     cudaFuncSetAttribute(k_symv_whole, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    wh_plan_init();
     g_ring_init[dev & 63] = true;
+}
+
+// k_symv_whole work plan (c_wh_plan): longest processing time first.  Unit
+// costs (relative instructions per warp, from the ncu source page): direct
+// full tile 1, direct diagonal 1.2, transposed full tile 1.6, transposed pass
+// over the packed diagonal tile 3.
+static void wh_plan_init() {
+    int8_t plans[WH_PLANS][WH_MAX_NT + 1][WH_CONS][WH_PLAN_U];
+    memset(plans, -1, sizeof plans);
+    for (int mode = 0; mode < WH_PLANS; ++mode)
+    for (int nT = 1; nT <= WH_MAX_NT; ++nT) {
+        auto& plan = plans[mode];
+        if (mode == 0) {
+            for (int q = 0; q < (nT + 1) * nT; ++q) plan[nT][q % WH_CONS][q / WH_CONS] = (int8_t)q;
+            continue;
+        }
+        std::vector<std::pair<double, int>> units;
+        for (int g = 0; g < nT; ++g)
+            for (int k = 0; k <= nT; ++k) {
+                const int q = g * (nT + 1) + k;
+                units.push_back({k < g ? 1.0 : k == g ? 1.2 : k == g + 1 ? 3.0 : 1.6, q});
+            }
+        std::stable_sort(units.begin(), units.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+        double load[WH_CONS] = {};
+        int cnt[WH_CONS] = {};
+        for (const auto& u : units) {
+            int w = 0;
+            for (int v = 1; v < WH_CONS; ++v)
+                if (cnt[v] < WH_PLAN_U && (cnt[w] >= WH_PLAN_U || load[v] < load[w])) w = v;
+            plan[nT][w][cnt[w]++] = (int8_t)u.second;
+            load[w] += u.first;
+        }
+    }
+    cudaMemcpyToSymbol(c_wh_plan, plans, sizeof plans);
 }
 
 // debug: read and zero the DDG_RING_TRACE counters (24 values; see k_symv_ring)
@@ -1321,7 +1372,7 @@ void launch_symv_ring(cudaStream_t st, const OpDesc* ops, const ItemDesc* items,
     const int nTw = (std::max(TILE, max_rows_r) + TILE - 1) / TILE;
     if (triangles && g_ring_whole && nTw <= WH_MAX_NT && max_rows_c == 0 && wh_smem(nTw) <= budget) {
         launch_pdl(k_symv_whole, ncta, (WH_CONS + 1) * 32, wh_smem(nTw), st, ops, items, item_begin, cta_part, tiles,
-                   s, oidx, z, done, nTw, g_ring_whole);
+                   s, oidx, z, done, nTw, g_ring_whole, g_whole_plan);
         return;
     }
     // row/column-warp consumers for launches of whole-subdomain triangles
