@@ -124,6 +124,10 @@ struct ddg_ctx {
     bool flat_coarse = true;           // two-stage restriction + flat prolongation (single GPU)
     double* d_res = nullptr;           // r - A z in part order (flat restriction)
     int32_t* d_xpart = nullptr;        // part of every position of the part order
+    // small problems: the whole solve in one cluster kernel (k_pcg_small, pcg.cu)
+    bool small_ok = false;
+    SmallArgs small{};                 // its shared-memory plan (small_plan)
+    int32_t* d_cops = nullptr;         // [ncolours + 1] operator ranges of the colours
     int32_t *d_brp = nullptr, *d_bcol = nullptr;   // node-blocked columns of A (DevCSR::bs)
     struct ddg_ctx* child = nullptr;   // three levels: the two-level method on A_c
     double* d_bc = nullptr;            // three levels: coarse right-hand side R_0 (r - A z)

@@ -233,6 +233,39 @@ void launch_pcg_rz(cudaStream_t st, const double* r, const double* z, const int3
 void launch_pcg_direction(cudaStream_t st, const double* z, double* p, const int32_t* rows, int64_t nrows,
                           Scalars* sc);
 void launch_pcg_finalize(cudaStream_t st, int slot, Scalars* sc, double* hist);
+// k_pcg_small (pcg.cu): the whole solve of a small problem in one cluster kernel
+struct SmallArgs {
+    DevCSR A;
+    int64_t n;
+    const double* f;
+    double *u, *r, *z, *p, *q;
+    Scalars* sc;
+    double* hist;
+    double* part;                 // [2][SMALL_MAX_G] block sums
+    const OpDesc* ops;
+    const ItemDesc* items;
+    const double* tiles;
+    const int32_t* oidx;
+    const int32_t* cops;          // [ncolours + 1] operator ranges of the colours (sweep order)
+    int ncolours;
+    int nparts;
+    const int64_t* bptr;
+    const int32_t* bidx;
+    const int32_t* cptr;
+    const int64_t* qoff;
+    const double* Q;
+    int coarse_item;
+    double* bc;
+    // shared-memory plan (small_plan, setup.cpp): resident arena (doubles and
+    // ints, the largest over the cluster's CTAs), scratch row length, padded
+    // coarse size, coarse tile rows, bytes; cluster size
+    int ad, ai, pw, ncp, nTc, G;
+    size_t smem;
+    int dbg;                    // DDG_SMALL_TRACE=2: timestamps inside the colour steps too
+};
+bool small_cluster_ok(int G, size_t smem);   // a cluster of G CTAs with smem bytes each fits
+int small_trace(int on, unsigned long long* out, int cap);   // debug (DDG_SMALL_TRACE)
+bool launch_pcg_small(cudaStream_t st, const SmallArgs& args);
 void launch_pcg_cond(cudaStream_t st, const Scalars* sc, unsigned long long handle);
 void launch_halo_pack(cudaStream_t st, const double* v, const int32_t* idx, double* buf, int64_t n);
 void launch_halo_unpack(cudaStream_t st, const double* buf, const int32_t* idx, double* v, int64_t n);

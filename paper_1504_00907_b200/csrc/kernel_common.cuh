@@ -37,29 +37,67 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// x loads of the row kernels: plain, or L2-only (CG: vectors other CTAs of a
+// cluster wrote since this SM last read them; L1 is not coherent)
+template <bool CG>
+__device__ __forceinline__ double ldx(const double* p) {
+    if constexpr (CG) return __ldcg(p);
+    else return *p;
+}
+
 // (A x)[v] from the stencil, in the CSR's column order (see DevStencil)
+template <bool CG = false>
 __device__ __forceinline__ double stencil_dot(const DevStencil& st, int64_t v, const double* __restrict__ x) {
     const int nx = st.nx, ny = st.ny;
-    const int ix = (int)(v % nx);
-    const int64_t r = v / nx;
-    const int iy = (int)(r % ny), iz = (int)(r / ny);
+    // 32-bit index arithmetic (n < 2^31: int32 CSR offsets, checked at setup)
+    const unsigned vv = (unsigned)v, r = vv / (unsigned)nx;
+    const int ix = (int)(vv - r * (unsigned)nx);
+    const unsigned r2 = r / (unsigned)ny;
+    const int iy = (int)(r - r2 * (unsigned)ny), iz = (int)r2;
     double s = 0.0;
     if (st.kind == 1) {
         const double* xv = x + v;
-        if (ix >= st.rx && ix < nx - st.rx && iy >= st.ry && iy < ny - st.ry && iz >= st.rz && iz < st.nz - st.rz) {
+        if constexpr (!CG) {
+            // streaming kernels: enough warps in flight hide each load
+            if (ix >= st.rx && ix < nx - st.rx && iy >= st.ry && iy < ny - st.ry && iz >= st.rz && iz < st.nz - st.rz) {
 #pragma unroll
-            for (int k = 0; k < STENCIL_MAX_PTS; ++k) {    // interior: every point on the grid
+                for (int k = 0; k < STENCIL_MAX_PTS; ++k) {    // interior: every point on the grid
+                    if (k >= st.npts) break;
+                    s = fma(st.c[k], xv[st.off[k]], s);
+                }
+                return s;
+            }
+#pragma unroll
+            for (int k = 0; k < STENCIL_MAX_PTS; ++k) {
                 if (k >= st.npts) break;
-                s = fma(st.c[k], xv[st.off[k]], s);
+                const int a = ix + st.dx[k], b = iy + st.dy[k], c = iz + st.dz[k];
+                if (a >= 0 && a < nx && b >= 0 && b < ny && c >= 0 && c < st.nz) s = fma(st.c[k], xv[st.off[k]], s);
             }
             return s;
         }
+        // k_pcg_small: every load is issued before the first product (a break
+        // between them would make each multiply-add wait out an L2 latency in
+        // turn); the products stay in column order, so the rounding is the CSR's
+        double xk[STENCIL_MAX_PTS];
+        if (ix >= st.rx && ix < nx - st.rx && iy >= st.ry && iy < ny - st.ry && iz >= st.rz && iz < st.nz - st.rz) {
+#pragma unroll
+            for (int k = 0; k < STENCIL_MAX_PTS; ++k)     // interior: every point on the grid
+                xk[k] = k < st.npts ? ldx<CG>(xv + st.off[k]) : 0.0;
+#pragma unroll
+            for (int k = 0; k < STENCIL_MAX_PTS; ++k)
+                if (k < st.npts) s = fma(st.c[k], xk[k], s);
+            return s;
+        }
+        bool in[STENCIL_MAX_PTS];
 #pragma unroll
         for (int k = 0; k < STENCIL_MAX_PTS; ++k) {
-            if (k >= st.npts) break;
             const int a = ix + st.dx[k], b = iy + st.dy[k], c = iz + st.dz[k];
-            if (a >= 0 && a < nx && b >= 0 && b < ny && c >= 0 && c < st.nz) s = fma(st.c[k], xv[st.off[k]], s);
+            in[k] = k < st.npts && a >= 0 && a < nx && b >= 0 && b < ny && c >= 0 && c < st.nz;
+            xk[k] = in[k] ? ldx<CG>(xv + st.off[k]) : 0.0;
         }
+#pragma unroll
+        for (int k = 0; k < STENCIL_MAX_PTS; ++k)
+            if (in[k]) s = fma(st.c[k], xk[k], s);
         return s;
     }
     const int64_t n = (int64_t)nx * ny * st.nz, sy = nx, sz = (int64_t)nx * ny;
@@ -67,36 +105,37 @@ __device__ __forceinline__ double stencil_dot(const DevStencil& st, int64_t v, c
     const double* CX = D + n;
     const double* CY = CX + n;
     const double* CZ = CY + n;
-    if (iz > 0) s = fma(CZ[v - sz], x[v - sz], s);
-    if (iy > 0) s = fma(CY[v - sy], x[v - sy], s);
-    if (ix > 0) s = fma(CX[v - 1], x[v - 1], s);
-    s = fma(D[v], x[v], s);
-    if (ix + 1 < nx) s = fma(CX[v], x[v + 1], s);
-    if (iy + 1 < ny) s = fma(CY[v], x[v + sy], s);
-    if (iz + 1 < st.nz) s = fma(CZ[v], x[v + sz], s);
+    if (iz > 0) s = fma(CZ[v - sz], ldx<CG>(&x[v - sz]), s);
+    if (iy > 0) s = fma(CY[v - sy], ldx<CG>(&x[v - sy]), s);
+    if (ix > 0) s = fma(CX[v - 1], ldx<CG>(&x[v - 1]), s);
+    s = fma(D[v], ldx<CG>(x + v), s);
+    if (ix + 1 < nx) s = fma(CX[v], ldx<CG>(&x[v + 1]), s);
+    if (iy + 1 < ny) s = fma(CY[v], ldx<CG>(&x[v + sy]), s);
+    if (iz + 1 < st.nz) s = fma(CZ[v], ldx<CG>(&x[v + sz]), s);
     return s;
 }
 
 // lane sl of SW: its entries e = rp[v] + sl, + SW, ... in order (node-blocked columns)
-template <int BS, int SW>
+template <int BS, int SW, bool CG = false>
 __device__ __forceinline__ double row_dot_nb(const DevCSR& A, int64_t v, const double* __restrict__ x, int sl) {
     const int e0 = A.rp[v], e1 = A.rp[v + 1];
     const int32_t* bc = A.bcol + A.brp[v / BS];
     double s = 0.0;
     for (int e = e0 + sl; e < e1; e += SW) {
         const int j = e - e0;
-        s += A.val[e] * x[bc[j / BS] * BS + j % BS];
+        s += A.val[e] * ldx<CG>(x + bc[j / BS] * BS + j % BS);
     }
     return s;
 }
 
 // (A x)[v] by one thread: stencil or CSR row
+template <bool CG = false>
 __device__ __forceinline__ double row_dot1(const DevCSR& A, int64_t v, const double* __restrict__ x) {
-    if (A.st.kind) return stencil_dot(A.st, v, x);
-    if (A.bs == 3) return row_dot_nb<3, 1>(A, v, x, 0);
-    if (A.bs == 4) return row_dot_nb<4, 1>(A, v, x, 0);
+    if (A.st.kind) return stencil_dot<CG>(A.st, v, x);
+    if (A.bs == 3) return row_dot_nb<3, 1, CG>(A, v, x, 0);
+    if (A.bs == 4) return row_dot_nb<4, 1, CG>(A, v, x, 0);
     double s = 0.0;
-    for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * x[A.col[e]];
+    for (int e = A.rp[v]; e < A.rp[v + 1]; e++) s += A.val[e] * ldx<CG>(x + A.col[e]);
     return s;
 }
 

@@ -171,7 +171,8 @@ static void free_ctx(ddg_ctx* c) {
                     c->d_tiles, c->d_s, c->d_partials, c->d_bptr, c->d_bidx, c->d_cptr,
                     c->d_qoff, c->d_Q, c->d_yc, c->d_r, c->d_z, c->d_p, c->d_q, c->d_f,
                     c->d_u, c->d_x, c->d_sc, c->d_hist, c->d_redbuf, c->d_ticket, c->d_zero, c->d_tickets,
-                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab, c->d_bc, c->d_res, c->d_xpart, c->d_brp, c->d_bcol};
+                    c->d_ring, c->d_gidx, c->d_stencil_coef, c->d_ab, c->d_bc, c->d_res, c->d_xpart, c->d_brp, c->d_bcol,
+                    c->d_cops};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -1012,6 +1013,76 @@ static int upload_s(cudaStream_t s, T** d, const std::vector<T>& h) {
 }
 #define upload(d, h) upload_s(c->stream, d, h)
 
+// Shared-memory plan of k_pcg_small (pcg.cu), the same walk the kernel makes:
+// CTA g of G keeps its operators t = g, g + G, ... of every colour (tiles and
+// index lists), tile row and column s = G - 1 - g of the coarse inverse
+// (s < nT_c), and the Q_I blocks and row lists of its warps' parts
+// I = g + G w (+ 8 G ...).
+static int small_plan(ddg_ctx* c) {
+    c->small_ok = false;
+    if (c->dist || c->coarse_variant != 1 || c->n > 65536 || c->coarse_op < 0 ||
+        c->coarse_item_end - c->coarse_item_begin != 1 || c->ncolours > 64)
+        return DDG_OK;
+    const int nTc = c->ops[c->coarse_op].nT;
+    int maxmp = 32;
+    for (size_t q = 0; q < c->op_sub.size(); ++q) {
+        if (c->ops[q].nitems != 1 || c->ops[q].mp > 512) return DDG_OK;
+        maxmp = std::max(maxmp, c->ops[q].mp);
+    }
+    for (int cc = 0; cc + 1 < c->ncolours; ++cc)
+        if (c->plans[cc].sub_end != c->plans[cc + 1].sub_begin) return DDG_OK;
+    const int PW = std::max(maxmp, c->maxmI);
+    for (int G : {16, 8}) {
+        if (nTc > G) continue;
+        int64_t ad = 0, ai = 0;
+        bool fits = true;
+        for (int g = 0; g < G; ++g) {
+            int64_t od = 0, oi = 0, nown = 0;
+            for (int cc = 0; cc < c->ncolours; ++cc)
+                for (int t = c->plans[cc].sub_begin + g; t < c->plans[cc].sub_end; t += G) {
+                    const OpDesc& op = c->ops[t];
+                    const ItemDesc& it = c->items[op.item_base];
+                    od += (item_doubles(1, it.I1 - it.I0, it.ntiles, it.tail) + 1) & ~1;
+                    oi += (op.m + 3) & ~3;
+                    ++nown;
+                }
+            if (nown > 32) fits = false;
+            if (G - 1 - g < nTc) od += (int64_t)(nTc - 1) * TILE_ELEMS + DIAG_ELEMS;
+            for (int w = 0; w < 8; ++w)
+                for (int I = g + G * w; I < c->nparts; I += G * 8) {
+                    const int64_t mI = c->bptr[I + 1] - c->bptr[I];
+                    od += (mI * (c->cptr[I + 1] - c->cptr[I]) + 1) & ~1;
+                    oi += (mI + 3) & ~3;
+                }
+            ad = std::max(ad, od);
+            ai = std::max(ai, oi);
+        }
+        const int ncp = nTc * TILE;
+        const size_t smem = 8 * (size_t)(ad + 10 * (int64_t)PW + 2 * ncp) + 4 * (size_t)ai;
+        fits = fits && smem <= 220 * 1024 && small_cluster_ok(G, smem);
+        if (c->opts.verbose)
+            fprintf(stderr, "[ddg_setup] k_pcg_small plan: G %d, %zu bytes of shared memory per CTA%s\n", G, smem,
+                    fits ? "" : " (does not fit)");
+        if (!fits) continue;
+        std::vector<int32_t> cops(c->ncolours + 1);
+        for (int cc = 0; cc < c->ncolours; ++cc) cops[cc] = c->plans[cc].sub_begin;
+        cops[c->ncolours] = c->ncolours ? c->plans[c->ncolours - 1].sub_end : 0;
+        int st = upload(&c->d_cops, cops);
+        if (st) return st;
+        c->small = SmallArgs{};
+        c->small.ad = (int)ad;
+        c->small.ai = (int)ai;
+        c->small.pw = PW;
+        c->small.ncp = ncp;
+        c->small.nTc = nTc;
+        c->small.G = G;
+        c->small.smem = smem;
+        c->small_ok = true;
+        return DDG_OK;
+    }
+    return DDG_OK;
+}
+
 // ---------------------------------------------------------------------------
 // ddg_setup
 // ---------------------------------------------------------------------------
@@ -1298,6 +1369,13 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
                 return st;
             }
         tick("halo plans");
+    }
+    // the whole solve in one cluster kernel (k_pcg_small): one GPU, dense single-item
+    // coarse inverse with at most G tile rows, single-item local operators, n small,
+    // and everything a CTA keeps resident within its shared memory (small_plan)
+    // (DDG_SMALL_FUSED=0: off)
+    if (!(getenv("DDG_SMALL_FUSED") && atoi(getenv("DDG_SMALL_FUSED")) == 0)) {
+        if ((st = small_plan(c))) { free_ctx(c); return st; }
     }
     tick("upload");
     if ((st = invert_locals(c))) { free_ctx(c); return st; }
@@ -1691,6 +1769,45 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     *c->h_sc = init;
     CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_sc, c->h_sc, sizeof(Scalars), cudaMemcpyHostToDevice, c->stream));
+    int done_iters = 0;
+    bool use_graph = c->opts.use_graphs != 0 && !c->profiling;
+    if (c->small_ok && !c->profiling) {
+        SmallArgs a = c->small;
+        a.dbg = getenv("DDG_SMALL_TRACE") ? atoi(getenv("DDG_SMALL_TRACE")) >= 2 : 0;
+        a.A = c->A;
+        a.n = c->n;
+        a.f = d_f;
+        a.u = d_u;
+        a.r = c->d_r;
+        a.z = c->d_z;
+        a.p = c->d_p;
+        a.q = c->d_q;
+        a.sc = c->d_sc;
+        a.hist = c->d_hist;
+        a.part = c->d_redbuf;
+        a.ops = c->d_ops;
+        a.items = c->d_items;
+        a.tiles = c->d_tiles;
+        a.oidx = c->d_oidx;
+        a.cops = c->d_cops;
+        a.ncolours = c->ncolours;
+        a.nparts = c->nparts;
+        a.bptr = c->d_bptr;
+        a.bidx = c->d_bidx;
+        a.cptr = c->d_cptr;
+        a.qoff = c->d_qoff;
+        a.Q = c->d_Q;
+        a.coarse_item = c->coarse_item_begin;
+        a.bc = c->d_s + c->ops[c->coarse_op].s_off;
+        if (!launch_pcg_small(c->stream, a)) {
+            if (c->opts.verbose) fprintf(stderr, "[ddg] k_pcg_small launch failed: multi-kernel iteration\n");
+        } else {
+            c->launches += 1;
+            done_iters = max_iter;
+            use_graph = false;
+            goto solved;
+        }
+    }
     launch_pcg_init(c->stream, c->n, d_f, c->d_r, d_u, c->d_rows, c->nrows, c->d_sc, c->d_hist, c->d_redbuf,
                     c->d_ticket, dist);
     dist_finish(c, 0);
@@ -1702,7 +1819,6 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
     c->launches += 2;
     CUDA_TRY(cudaGetLastError());
     // iteration graph (captured once per u pointer)
-    bool use_graph = c->opts.use_graphs != 0 && !c->profiling;
     if (use_graph && (!c->ge_iter || c->g_iter_u != d_u)) {
         if (c->ge_iter) cudaGraphExecDestroy(c->ge_iter);
         if (c->g_iter) cudaGraphDestroy(c->g_iter);
@@ -1718,7 +1834,7 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         c->launches = l0;
         c->g_iter_u = d_u;
     }
-    int done_iters = 0;
+    {
     int chunk = 2;
     // device-side loop: one graph launch per solve (single context; the
     // host-stepped chunks below remain for multi-rank contexts and profiling)
@@ -1763,6 +1879,8 @@ static int run_pcg(ddg_ctx* c, const double* d_f, double* d_u, double rtol, int 
         if (c->h_sc->done) break;
         chunk = std::min(chunk * 2, 8);
     }
+    }
+solved:
     if (c->dist && c->nranks > 1) {
         // assemble u on every rank: u is zero outside the owned rows
         comm_check(c, comm_allreduce_sum(c->comm, d_u, d_u, c->n, c->stream));
@@ -2049,6 +2167,8 @@ extern "C" void ddg_plan_destroy(ddg_plan* p) { delete p; }
 // debug (not part of include/ddg.h): k_symv_ring role/wait cycle counters
 // accumulated since the last call (DDG_RING_TRACE=1); 24 values
 extern "C" int ddg_debug_ring_trace(unsigned long long* out) { return symv_ring_trace(out); }
+// debug: k_pcg_small barrier timestamps (on = 1: arm; on = 0: read up to cap, returns the count)
+extern "C" int ddg_debug_small_trace(int on, unsigned long long* out, int cap) { return small_trace(on, out, cap); }
 
 // CG coefficients of the last solve (include/ddg.h)
 extern "C" int ddg_get_lanczos(ddg_ctx* c, double* alphas, double* betas, int cap) {

@@ -57,9 +57,15 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("name", list(CASES))
-def test_pcg_parity(name):
-    compare_solve(CASES[name]())
+def test_pcg_parity(name, fused, monkeypatch):
+    """fused = 1: small problems run the whole solve in one cluster kernel
+    (k_pcg_small); 0: the multi-kernel iteration"""
+    monkeypatch.setenv("DDG_SMALL_FUSED", fused)
+    s, o, it, ur = compare_solve(CASES[name]())
+    if name == "C1":                                                                 # eligible: one solve =
+        assert (s.launch_count() <= 3) == (fused == "1")                             # k_pcg_small + true residual
 
 
 @pytest.mark.parametrize("mode", [1, 2])
@@ -276,20 +282,20 @@ def test_comm_path_single_rank(name):
 # The small parity cases fall below the persistent ring's size threshold, so
 # each path is also forced explicitly (switches are read at ddg_setup).
 PATHS = {
-    "ring_everywhere": {"DDG_RING_MIN_MB": "0"},                 # ring for every SYMV launch (auto: k_symv_whole
+    "ring_everywhere": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0"},                 # ring for every SYMV launch (auto: k_symv_whole
                                                                  # for small whole triangles, compact last rows)
-    "whole_full_tiles": {"DDG_RING_MIN_MB": "0", "DDG_COMPACT": "0"},   # k_symv_whole on padded last rows
-    "whole_rowcopies": {"DDG_RING_MIN_MB": "0", "DDG_RING_WHOLE": "2"},  # k_symv_whole, one copy per tile row
-    "ring2_full_tiles": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0", "DDG_COMPACT": "0"},
-    "ring2_split1": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0", "DDG_RING2_SPLIT": "1"},
-    "ring1_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "0", "DDG_RING_WHOLE": "0"},  # 8-warp columns
-    "ring_2tile_slots": {"DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2", "DDG_RING_WHOLE": "0"},
-    "ring2_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0"},  # row/column warps,
+    "whole_full_tiles": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_COMPACT": "0"},   # k_symv_whole on padded last rows
+    "whole_rowcopies": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_RING_WHOLE": "2"},  # k_symv_whole, one copy per tile row
+    "ring2_full_tiles": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0", "DDG_COMPACT": "0"},
+    "ring2_split1": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0", "DDG_RING2_SPLIT": "1"},
+    "ring1_everywhere": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_RING_V2": "0", "DDG_RING_WHOLE": "0"},  # 8-warp columns
+    "ring_2tile_slots": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_RING_TILES": "2", "DDG_RING_WHOLE": "0"},
+    "ring2_everywhere": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0"},  # row/column warps,
                                                                                               # compact last rows
-    "classic": {"DDG_SYMV": "classic"},                           # per-item k_symv / k_symv_small
-    "compact_classic": {"DDG_RING_MIN_MB": "1e9"},                # per-item kernels on compact-tail operators
-    "coarse_levels": {"DDG_COARSE_DATAFLOW": "0", "DDG_RING_MIN_MB": "0"},  # level-by-level sparse solve
-    "csr_rows": {"DDG_NO_STENCIL": "1"},                          # row kernels read the CSR
+    "classic": {"DDG_SMALL_FUSED": "0", "DDG_SYMV": "classic"},                           # per-item k_symv / k_symv_small
+    "compact_classic": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "1e9"},                # per-item kernels on compact-tail operators
+    "coarse_levels": {"DDG_SMALL_FUSED": "0", "DDG_COARSE_DATAFLOW": "0", "DDG_RING_MIN_MB": "0"},  # level-by-level sparse solve
+    "csr_rows": {"DDG_SMALL_FUSED": "0", "DDG_NO_STENCIL": "1"},                          # row kernels read the CSR
 }
 PATH_CASES = ["C1", "poisson3d_24_b8_p2", "lognormal_16_b4", "elasticity_8_be4", "biharm_64_b16_p3",
               "poisson2d_ragged"]

@@ -76,10 +76,10 @@ def test_grown_partition_sparse_coarse(name):
 
 
 PATHS = {
-    "ring_everywhere": {"DDG_RING_MIN_MB": "0"},
-    "whole_full_tiles": {"DDG_RING_MIN_MB": "0", "DDG_COMPACT": "0"},
-    "ring2_everywhere": {"DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0"},
-    "classic": {"DDG_SYMV": "classic"},
+    "ring_everywhere": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0"},
+    "whole_full_tiles": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_COMPACT": "0"},
+    "ring2_everywhere": {"DDG_SMALL_FUSED": "0", "DDG_RING_MIN_MB": "0", "DDG_RING_V2": "1", "DDG_RING_WHOLE": "0"},
+    "classic": {"DDG_SMALL_FUSED": "0", "DDG_SYMV": "classic"},
 }
 
 
