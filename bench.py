@@ -207,6 +207,8 @@ def bench_ddg(args):
     if args.levels == 3:   # three-level method: second level on A_c
         p2, n2, bc2 = P.coarse_parts(pr, args.factor, coords=True)
         kw = dict(part2=p2, nparts2=n2, block_coords2=bc2)
+    if args.local_variant == "cholesky":   # forward + back substitution against Cholesky factors
+        kw["local_variant"] = 1
     s = Solver.from_problem(pr, device=local, stream=stream.cuda_stream, comm=comm, **kw)
     t_setup = time.time() - t0
     sizes = s.subdomain_sizes()
@@ -277,7 +279,8 @@ def bench_ddg(args):
     # ncu dram bytes per launch of this workload's dominant kernel (one --set full
     # capture per config, profiles/symv_traffic_<workload>.json), or null
     traffic = None
-    workload = args.config + ("-3level" if args.levels == 3 else "")
+    workload = args.config + ("-3level" if args.levels == 3 else "") + (
+        "-cholesky" if args.local_variant == "cholesky" else "")
     tpath = os.path.join(ROOT, "profiles", f"symv_traffic_{workload}.json")
     if os.path.exists(tpath):
         try:
@@ -305,7 +308,8 @@ def bench_ddg(args):
                    "true_residual_rel": float(rep.true_res) / float(np.linalg.norm(pr.f)),
                    "local_operator_bytes": int(s.info.local_factor_bytes),
                    "coarse_solve_bytes": int(s.info.coarse_solve_bytes)},
-        "roofline": {"bound": "hbm", "kernel": "k_symv (colour sweep, a4/a8)",
+        "roofline": {"bound": "hbm", "kernel": "k_chol_solve (colour sweep, a4/a8; one factor read per visit "
+                     "counted)" if args.local_variant == "cholesky" else "k_symv (colour sweep, a4/a8)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"
                      if not pk.get("_fallback") else "fallback 6650 GB/s",
@@ -348,6 +352,8 @@ def main():
     ap.add_argument("--factor", type=int, default=None,
                     help="three levels: parts grouped per axis into a second-level part (default H/h)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--local-variant", default="inverse", choices=["inverse", "cholesky"],
+                    help="exact local solves: explicit inverse (default) or Cholesky substitutions")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one rank per GPU: re-launch under torchrun (rank 0 prints the line)

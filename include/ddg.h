@@ -130,7 +130,20 @@ typedef struct {
        colour[i] = i is the paper's plain sequential sweep.
        NULL: greedy first-fit in id order (reading R3). */
     const int32_t* colour;
+    /* How the exact local solves A_i^{-1} s ("we solve these
+       subdomain problems exactly") are realised:
+       DDG_LOCAL_AUTO (0, default) = DDG_LOCAL_INVERSE: the explicit inverse
+       A_i^{-1}, formed once by blocked Gauss-Jordan and applied per visit as one
+       symmetric matrix-vector product (one read of its packed lower triangle);
+       DDG_LOCAL_CHOLESKY (1): the Cholesky factor A_i = L_i L_i^T, applied per
+       visit as a forward and a back substitution over 32 x 32 tiles (the
+       32 x 32 diagonal blocks stored inverted), one CTA per subdomain of a
+       colour.  Both are exact; results agree to rounding (DESIGN.md §7 has
+       the measured comparison).  Other values: DDG_E_ARG. */
+    int local_variant;
 } ddg_opts;
+
+enum { DDG_LOCAL_AUTO = 0, DDG_LOCAL_CHOLESKY = 1, DDG_LOCAL_INVERSE = 2 };
 
 typedef struct {
     int converged;        /* 1 if the stopping rule was met                                     */

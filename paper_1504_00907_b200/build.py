@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libddg.so")
-SOURCES = ["pcg.cu", "symv.cu", "coarse.cu", "setup_kernels.cu", "setup.cpp", "coarse_sparse.cpp", "dist.cpp",
+SOURCES = ["pcg.cu", "symv.cu", "coarse.cu", "setup_kernels.cu", "chol.cu", "basis.cu", "setup.cpp", "coarse_sparse.cpp", "dist.cpp",
            "comm.cpp"]
 HEADERS = ["ddg_internal.h", "kernel_common.cuh", "ctx.h", "dist.h", "comm.h", os.path.join("..", "..", "include", "ddg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

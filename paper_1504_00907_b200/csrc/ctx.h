@@ -152,6 +152,7 @@ struct ddg_ctx {
     // SYMV kernel choice (DDG_SYMV: "ring" default, "classic") and the
     // byte-balanced CTA partitions of every k_symv_ring launch
     int symv_mode = 0;                  // 0 ring, 1 classic per-item k_symv
+    bool chol = false;                  // local_variant DDG_LOCAL_CHOLESKY: factors instead of inverses (chol.cu)
     std::vector<int32_t> h_ring;
     std::vector<std::pair<int, std::pair<int, int>>> ring_rc;   // partition offset -> (max rows_r, max rows_c)
     int32_t* d_ring = nullptr;

@@ -287,6 +287,26 @@ constexpr int GJB_MIN_T = 16;
 // sym: 1 the experimental symmetric exchange (R22), 0 the full exchange, -1 the DDG_GJ_SYM switch
 void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* const* mats, const int32_t* nT,
                        const int32_t* nK, const int32_t* ids, int32_t* err, int sym = -1);
+// coarse space on the device (basis.cu): per-part dd-MGS basis (one warp per
+// part), compaction to Q, and the Galerkin blocks A_c[I, J] (one CTA per block)
+void launch_basis_mgs(cudaStream_t st, int nparts, int k, int64_t n, const double* F, const int64_t* bptr,
+                      const int32_t* bidx, const int64_t* voff, double2* V, double* Qw, int32_t* rank,
+                      double* ratio, double rank_tol, int32_t* err);
+void launch_basis_compact(cudaStream_t st, int nparts, const int64_t* bptr, const int64_t* voff,
+                          const int64_t* qoff, const double* Qw, double* Q);
+void launch_galerkin_blocks(cudaStream_t st, int nblocks, int maxk, const int32_t* bI, const int32_t* bJ,
+                            const int64_t* boff, const int64_t* bptr, const int32_t* bidx, const int32_t* cptr,
+                            const int64_t* qoff, const double* Q, const int32_t* part, const int32_t* bpos,
+                            const int32_t* rp, const int32_t* col, const double* val, double* out);
+// local_variant = DDG_LOCAL_CHOLESKY (chol.cu): tile Cholesky of nmat tiled
+// dense matrices (one CTA each), packing of the lower tiles at each op's
+// tile_off, and one colour's forward + back substitutions (one CTA per op)
+void launch_chol_local(cudaStream_t st, int nmat, const int32_t* nT, double* const* mats, const int32_t* ids,
+                       int32_t* err);
+void launch_chol_pack(cudaStream_t st, int nops, int max_tiles, const int32_t* op_ids, const OpDesc* ops,
+                      const double* scratch, const int64_t* scratch_off, double* out);
+void launch_chol_solve(cudaStream_t st, const OpDesc* ops, int op_begin, int nops, int max_mp, const double* fac,
+                       const double* s, const int32_t* oidx, double* z, const int32_t* done);
 // sparse coarse factorisation / solve
 void launch_front_scatter(cudaStream_t st, int64_t ntrip, const int32_t* frow, const int32_t* fcol,
                           const double* fval, const int32_t* ffront, const FrontDesc* fronts,

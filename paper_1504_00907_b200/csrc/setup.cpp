@@ -103,46 +103,6 @@ static int hw_threads() {
     return (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
 }
 
-// double-double numbers for the per-part orthonormalisation (reading R6c)
-struct DD {
-    double hi, lo;
-};
-static inline DD dd_two_sum(double a, double b) {
-    double s = a + b, v = s - a;
-    return {s, (a - (s - v)) + (b - v)};
-}
-static inline DD dd_fast(double a, double b) {
-    double s = a + b;
-    return {s, b - (s - a)};
-}
-static inline DD operator+(DD x, DD y) {
-    DD s = dd_two_sum(x.hi, y.hi), t = dd_two_sum(x.lo, y.lo);
-    s.lo += t.hi;
-    s = dd_fast(s.hi, s.lo);
-    s.lo += t.lo;
-    return dd_fast(s.hi, s.lo);
-}
-static inline DD operator-(DD x) { return {-x.hi, -x.lo}; }
-static inline DD operator*(DD x, DD y) {
-    double p = x.hi * y.hi;
-    double e = fma(x.hi, y.hi, -p) + (x.hi * y.lo + x.lo * y.hi);
-    return dd_fast(p, e);
-}
-static inline DD dd_div(DD x, DD y) {
-    double q1 = x.hi / y.hi;
-    DD r = x + -(DD{q1, 0} * y);
-    double q2 = r.hi / y.hi;
-    r = r + -(DD{q2, 0} * y);
-    double q3 = r.hi / y.hi;
-    return dd_fast(q1, q2) + DD{q3, 0};
-}
-static inline DD dd_sqrt(DD a) {
-    if (a.hi <= 0) return {0, 0};
-    double x = sqrt(a.hi);
-    DD r = a + -(DD{x, 0} * DD{x, 0});
-    return DD{x, 0} + DD{r.hi / (2 * x), 0};
-}
-
 // ---------------------------------------------------------------------------
 // the context
 // ---------------------------------------------------------------------------
@@ -312,167 +272,6 @@ static int build_colours(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
     std::stable_sort(c->order.begin(), c->order.end(),
                      [&](int a, int b) { return c->colour[a] < c->colour[b]; });   // (colour, id)
     return DDG_OK;
-}
-
-// Per-part orthonormal basis of F[Omega_I,:]: modified
-// Gram-Schmidt in double-double, columns in their given order, column j kept
-// iff ||v_j|| >= rank_tol * ||F_I e_j|| (reading R7: relative to the column
-// itself, so the test does not depend on how the coordinates are scaled).
-static int build_basis(ddg_ctx* c, const double* F) {
-    const int np = c->nparts, k = c->k;
-    const int64_t n = c->n;
-    std::vector<int> rank(np, 0);
-    std::vector<std::vector<double>> QI(np);
-    std::vector<double> ratio(np, INFINITY);
-    std::atomic<int> bad{-1};
-    parallel_for(np, [&](int64_t b, int64_t e, int) {
-        std::vector<DD> V, v;
-        for (int64_t I = b; I < e; ++I) {
-            const int64_t mI = c->bptr[I + 1] - c->bptr[I];
-            const int32_t* rows = c->bidx.data() + c->bptr[I];
-            double fmax = 0;
-            std::vector<double> fnrm(k);
-            for (int j = 0; j < k; ++j) {
-                DD s{0, 0};
-                for (int64_t a = 0; a < mI; ++a) {
-                    double x = F[(int64_t)j * n + rows[a]];
-                    s = s + DD{x, 0} * DD{x, 0};
-                }
-                fnrm[j] = dd_sqrt(s).hi;
-                fmax = std::max(fmax, fnrm[j]);
-            }
-            if (!(fmax > 0)) {
-                int expect = -1;
-                bad.compare_exchange_strong(expect, (int)I);
-                continue;
-            }
-            V.assign((size_t)mI * k, DD{0, 0});
-            v.resize(mI);
-            int r = 0;
-            for (int j = 0; j < k; ++j) {
-                for (int64_t a = 0; a < mI; ++a) v[a] = DD{F[(int64_t)j * n + rows[a]], 0};
-                for (int t = 0; t < r; ++t) {
-                    const DD* q = V.data() + (size_t)t * mI;
-                    DD s{0, 0};
-                    for (int64_t a = 0; a < mI; ++a) s = s + q[a] * v[a];
-                    for (int64_t a = 0; a < mI; ++a) v[a] = v[a] + -(s * q[a]);
-                }
-                DD s{0, 0};
-                for (int64_t a = 0; a < mI; ++a) s = s + v[a] * v[a];
-                DD nrm = dd_sqrt(s);
-                const double rt = fnrm[j] > 0 ? nrm.hi / fnrm[j] : 0.0;
-                if (rt >= c->opts.rank_tol && nrm.hi > 0) {
-                    DD* q = V.data() + (size_t)r * mI;
-                    for (int64_t a = 0; a < mI; ++a) q[a] = dd_div(v[a], nrm);
-                    ratio[I] = std::min(ratio[I], rt);
-                    ++r;
-                }
-            }
-            rank[I] = r;
-            QI[I].resize((size_t)r * mI);
-            for (size_t x = 0; x < (size_t)r * mI; ++x) QI[I][x] = V[x].hi;
-        }
-    });
-    if (bad.load() >= 0)
-        return set_err(DDG_E_ZERO_BLOCK, "coarse basis: F restricted to part %d is zero", bad.load());
-    c->cptr.assign(np + 1, 0);
-    c->qoff.assign(np + 1, 0);
-    c->dropped = 0;
-    for (int I = 0; I < np; ++I) {
-        c->cptr[I + 1] = c->cptr[I] + rank[I];
-        c->qoff[I + 1] = c->qoff[I] + (int64_t)QI[I].size();
-        c->dropped += k - rank[I];
-        c->min_ratio = std::min(c->min_ratio, ratio[I]);
-    }
-    c->nc = c->cptr[np];
-    c->Q.resize(c->qoff[np]);
-    for (int I = 0; I < np; ++I) std::copy(QI[I].begin(), QI[I].end(), c->Q.begin() + c->qoff[I]);
-    return DDG_OK;
-}
-
-// Galerkin product A_c = P^T A P: for every part J and kept
-// column j, w = A p_{J,j} on the rows where it can be non-zero, then
-// A_c[(I,i),(J,j)] = Q_I[:,i]^T w[Omega_I]; only coarse row >= coarse col kept.
-static void build_galerkin(ddg_ctx* c, const int64_t* rp, const int32_t* col, const double* val,
-                           std::vector<int32_t>& er, std::vector<int32_t>& ec,
-                           std::vector<double>& ev) {
-    const int np = c->nparts;
-    const int nt = hw_threads();
-    std::vector<std::vector<int32_t>> tr(np), tc(np);
-    std::vector<std::vector<double>> tv(np);
-    std::vector<std::vector<int32_t>> marks(nt);
-    parallel_for(np, [&](int64_t b, int64_t e, int t) {
-        auto& mark = marks[t];
-        if (mark.empty()) mark.assign(c->n, -1);
-        std::vector<int32_t> touched;
-        std::vector<double> w;
-        std::vector<int32_t> partsI;
-        std::vector<double> acc;
-        for (int64_t J = b; J < e; ++J) {
-            const int64_t mJ = c->bptr[J + 1] - c->bptr[J];
-            const int32_t* rowsJ = c->bidx.data() + c->bptr[J];
-            touched.clear();
-            for (int64_t a = 0; a < mJ; ++a) {
-                const int32_t v = rowsJ[a];
-                for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
-                    const int32_t u = col[x];
-                    if (mark[u] != (int32_t)J) {
-                        mark[u] = (int32_t)J;
-                        touched.push_back(u);
-                    }
-                }
-            }
-            std::sort(touched.begin(), touched.end());
-            partsI.clear();
-            for (int32_t u : touched) partsI.push_back(c->part[u]);
-            std::sort(partsI.begin(), partsI.end());
-            partsI.erase(std::unique(partsI.begin(), partsI.end()), partsI.end());
-            const int ncJ = c->cptr[J + 1] - c->cptr[J];
-            w.resize(touched.size());
-            for (int j = 0; j < ncJ; ++j) {
-                const double* qJ = c->Q.data() + c->qoff[J] + (int64_t)j * mJ;
-                for (size_t t2 = 0; t2 < touched.size(); ++t2) {
-                    const int32_t u = touched[t2];
-                    double s = 0;
-                    for (int64_t x = rp[u]; x < rp[u + 1]; ++x) {
-                        const int32_t cc = col[x];
-                        if (c->part[cc] == (int32_t)J) s += val[x] * qJ[c->bpos[cc]];
-                    }
-                    w[t2] = s;
-                }
-                const int64_t cj = c->cptr[J] + j;
-                for (int32_t I : partsI) {
-                    const int ncI = c->cptr[I + 1] - c->cptr[I];
-                    const int64_t mI = c->bptr[I + 1] - c->bptr[I];
-                    acc.assign(ncI, 0.0);
-                    for (size_t t2 = 0; t2 < touched.size(); ++t2) {
-                        const int32_t u = touched[t2];
-                        if (c->part[u] != I) continue;
-                        const double wu = w[t2];
-                        for (int i = 0; i < ncI; ++i)
-                            acc[i] += c->Q[c->qoff[I] + (int64_t)i * mI + c->bpos[u]] * wu;
-                    }
-                    for (int i = 0; i < ncI; ++i) {
-                        const int64_t ci = c->cptr[I] + i;
-                        if (ci < cj) continue;
-                        tr[J].push_back((int32_t)ci);
-                        tc[J].push_back((int32_t)cj);
-                        tv[J].push_back(acc[i]);
-                    }
-                }
-            }
-        }
-    });
-    size_t tot = 0;
-    for (int J = 0; J < np; ++J) tot += tv[J].size();
-    er.reserve(tot);
-    ec.reserve(tot);
-    ev.reserve(tot);
-    for (int J = 0; J < np; ++J) {
-        er.insert(er.end(), tr[J].begin(), tr[J].end());
-        ec.insert(ec.end(), tc[J].begin(), tc[J].end());
-        ev.insert(ev.end(), tv[J].begin(), tv[J].end());
-    }
 }
 
 // Operator descriptors, work items and reduction tasks for the tiled SYMV.
@@ -718,7 +517,18 @@ static int build_plans(ddg_ctx* c) {
                               c->oidx.begin() + c->optr[i + 1]);
             // every list starts 16-byte aligned (k_symv_whole bulk-copies it)
             while (sorted_idx.size() % 4) sorted_idx.push_back(0);
-            add_op(c, (int32_t)m, 0, off, true, compact);
+            if (c->chol) {
+                // Cholesky factor (chol.cu): nT (nT + 1) / 2 full tiles at tile_off,
+                // no SYMV items read, no partial segments
+                const int64_t t0 = c->tiles_doubles, p0 = c->part_doubles;
+                add_op(c, (int32_t)m, 0, off, true, false);
+                OpDesc& op = c->ops.back();
+                op.tile_off = t0;
+                c->tiles_doubles = t0 + (int64_t)op.nT * (op.nT + 1) / 2 * TILE_ELEMS;
+                c->part_doubles = p0;
+            } else {
+                add_op(c, (int32_t)m, 0, off, true, compact);
+            }
             pl.max_rows = std::max<int>(pl.max_rows, (int)m);
             ++pos;
         }
@@ -830,12 +640,23 @@ static int invert_locals(ddg_ctx* c) {
             CUDA_TRY(cudaMemcpyAsync(d_ids2, oids.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
             CUDA_TRY(cudaMemcpyAsync(d_nT2, onT.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
             CUDA_TRY(cudaMemcpyAsync(d_ptr2, optr.data(), nb * sizeof(double*), cudaMemcpyHostToDevice, c->stream));
-            if (nsmall) launch_gj_batched(c->stream, nsmall, d_nT2, d_nT2, d_ptr2, d_ids2, d_err);
+            if (c->chol) {
+                launch_chol_local(c->stream, (int)nb, d_nT2, d_ptr2, d_ids2, d_err);
+                nsmall = (int)nb;
+            } else if (nsmall) {
+                launch_gj_batched(c->stream, nsmall, d_nT2, d_nT2, d_ptr2, d_ids2, d_err);
+            }
             if ((int)nb > nsmall)
                 launch_gj_blocked(c->stream, (int)nb - nsmall, maxT, maxT, d_ptr2 + nsmall, d_nT2 + nsmall,
                                   d_nT2 + nsmall, d_ids2 + nsmall, d_err);
         }
-        launch_pack(c->stream, (int)nb, d_ids, c->d_ops, c->d_items, scratch, d_soff, c->d_tiles);
+        if (c->chol) {
+            int maxT = 0;
+            for (int32_t t : nTs) maxT = std::max(maxT, (int)t);
+            launch_chol_pack(c->stream, (int)nb, maxT * (maxT + 1) / 2, d_ids, c->d_ops, scratch, d_soff, c->d_tiles);
+        } else {
+            launch_pack(c->stream, (int)nb, d_ids, c->d_ops, c->d_items, scratch, d_soff, c->d_tiles);
+        }
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(c->stream));
     }
@@ -851,7 +672,8 @@ static int invert_locals(ddg_ctx* c) {
     cudaFree(d_ptr2);
     if (herr[0] >= 0)
         return set_err(DDG_E_NOT_SPD,
-                       "local inverse: subdomain %d not positive definite at pivot %d",
+                       c->chol ? "local Cholesky: subdomain %d not positive definite at pivot %d"
+                               : "local inverse: subdomain %d not positive definite at pivot %d",
                        c->op_sub[herr[0]], herr[1]);
     return DDG_OK;
 }
@@ -1013,6 +835,143 @@ static int upload_s(cudaStream_t s, T** d, const std::vector<T>& h) {
 }
 #define upload(d, h) upload_s(c->stream, d, h)
 
+// Per-part orthonormal basis of F[Omega_I,:] on the device (basis.cu,
+// PAPER.md:253-264; readings R6c, R7): cptr, qoff, d_Q, and the host copy of
+// Q when the three-level child needs it (build_child).
+static int device_basis(ddg_ctx* c, const double* F, int32_t* d_part) {
+    (void)d_part;
+    const int np = c->nparts, k = c->k;
+    const int64_t n = c->n;
+    std::vector<int64_t> voff(np + 1, 0);
+    for (int I = 0; I < np; ++I) voff[I + 1] = voff[I] + (c->bptr[I + 1] - c->bptr[I]) * k;
+    double *dF = nullptr, *dQw = nullptr, *dratio = nullptr;
+    double2* dV = nullptr;
+    int64_t* dvoff = nullptr;
+    int32_t *drank = nullptr, *derr = nullptr;
+    auto done = [&](int st) {
+        cudaFree(dF); cudaFree(dQw); cudaFree(dratio); cudaFree(dV); cudaFree(dvoff); cudaFree(drank);
+        cudaFree(derr);
+        return st;
+    };
+    int st;
+    if ((st = dalloc(&dF, (size_t)n * k)) || (st = h2d(c->stream, dF, F, (size_t)n * k * 8)) ||
+        (st = upload(&dvoff, voff)) || (st = dalloc(&dV, (size_t)voff[np])) || (st = dalloc(&dQw, (size_t)voff[np])) ||
+        (st = dalloc(&drank, np)) || (st = dalloc(&dratio, np)) || (st = dalloc(&derr, 1)))
+        return done(st);
+    const int32_t neg = -1;
+    if ((st = h2d(c->stream, derr, &neg, 4))) return done(st);
+    launch_basis_mgs(c->stream, np, k, n, dF, c->d_bptr, c->d_bidx, dvoff, dV, dQw, drank, dratio,
+                     c->opts.rank_tol, derr);
+    std::vector<int32_t> rank(np);
+    std::vector<double> ratio(np);
+    int32_t bad = -1;
+    if ((st = d2h(c->stream, rank.data(), drank, np * 4)) || (st = d2h(c->stream, ratio.data(), dratio, np * 8)) ||
+        (st = d2h(c->stream, &bad, derr, 4)))
+        return done(st);
+    if (bad >= 0) return done(set_err(DDG_E_ZERO_BLOCK, "coarse basis: F restricted to part %d is zero", bad));
+    c->cptr.assign(np + 1, 0);
+    c->qoff.assign(np + 1, 0);
+    c->dropped = 0;
+    for (int I = 0; I < np; ++I) {
+        c->cptr[I + 1] = c->cptr[I] + rank[I];
+        c->qoff[I + 1] = c->qoff[I] + (int64_t)rank[I] * (c->bptr[I + 1] - c->bptr[I]);
+        c->dropped += k - rank[I];
+        c->min_ratio = std::min(c->min_ratio, ratio[I]);
+    }
+    c->nc = c->cptr[np];
+    if ((st = upload(&c->d_cptr, c->cptr)) || (st = upload(&c->d_qoff, c->qoff)) ||
+        (st = dalloc(&c->d_Q, std::max<int64_t>(1, c->qoff[np]))))
+        return done(st);
+    launch_basis_compact(c->stream, np, c->d_bptr, dvoff, c->d_qoff, dQw, c->d_Q);
+    CUDA_TRY(cudaGetLastError());
+    if (c->opts.part2) {
+        c->Q.resize(c->qoff[np]);
+        if ((st = d2h(c->stream, c->Q.data(), c->d_Q, c->qoff[np] * 8))) return done(st);
+    }
+    return done(DDG_OK);
+}
+
+// Galerkin product A_c = P^T A P on the device (basis.cu), one
+// block A_c[I, J] = Q_I^T A[Omega_I, Omega_J] Q_J per adjacent pair I >= J;
+// triplets (row >= col only, reading R9) in (J, j, I, i) order for the coarse
+// factorisation.
+static int device_galerkin(ddg_ctx* c, const int64_t* rp, const int32_t* col, const int32_t* d_part,
+                           const int32_t* d_bpos, std::vector<int32_t>& er, std::vector<int32_t>& ec,
+                           std::vector<double>& ev) {
+    const int np = c->nparts;
+    // adjacent parts I >= J of every J (structural pattern of A)
+    std::vector<std::vector<int32_t>> adj(np);
+    const int nt = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
+    std::vector<std::vector<int32_t>> marks(nt);
+    parallel_for(np, [&](int64_t b, int64_t e, int t) {
+        auto& mark = marks[t];
+        if (mark.empty()) mark.assign(np, -1);
+        for (int64_t J = b; J < e; ++J) {
+            auto& L = adj[J];
+            for (int64_t a = c->bptr[J]; a < c->bptr[J + 1]; ++a) {
+                const int32_t v = c->bidx[a];
+                for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
+                    const int32_t I = c->part[col[x]];
+                    if (I >= J && mark[I] != (int32_t)J) {
+                        mark[I] = (int32_t)J;
+                        L.push_back(I);
+                    }
+                }
+            }
+            std::sort(L.begin(), L.end());
+        }
+    });
+    std::vector<int32_t> bI, bJ;
+    std::vector<int64_t> boff(1, 0);
+    int maxk = 1;
+    for (int J = 0; J < np; ++J)
+        for (int32_t I : adj[J]) {
+            bI.push_back(I);
+            bJ.push_back(J);
+            boff.push_back(boff.back() + (int64_t)(c->cptr[I + 1] - c->cptr[I]) * (c->cptr[J + 1] - c->cptr[J]));
+        }
+    for (int I = 0; I < np; ++I) maxk = std::max(maxk, c->cptr[I + 1] - c->cptr[I]);
+    const int nb = (int)bI.size();
+    int32_t *dbI = nullptr, *dbJ = nullptr;
+    int64_t* dboff = nullptr;
+    double* dout = nullptr;
+    auto done = [&](int st) {
+        cudaFree(dbI); cudaFree(dbJ); cudaFree(dboff); cudaFree(dout);
+        return st;
+    };
+    int st;
+    if ((st = upload(&dbI, bI)) || (st = upload(&dbJ, bJ)) || (st = upload(&dboff, boff)) ||
+        (st = dalloc(&dout, std::max<int64_t>(1, boff.back()))))
+        return done(st);
+    launch_galerkin_blocks(c->stream, nb, maxk, dbI, dbJ, dboff, c->d_bptr, c->d_bidx, c->d_cptr, c->d_qoff, c->d_Q,
+                           d_part, d_bpos, c->d_rp, c->d_col, c->d_val, dout);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<double> hb(boff.back());
+    if ((st = d2h(c->stream, hb.data(), dout, hb.size() * 8))) return done(st);
+    er.clear(); ec.clear(); ev.clear();
+    er.reserve(hb.size()); ec.reserve(hb.size()); ev.reserve(hb.size());
+    int64_t b0 = 0;
+    for (int J = 0; J < np; ++J) {
+        const int rJ = c->cptr[J + 1] - c->cptr[J];
+        const int64_t nbJ = (int64_t)adj[J].size();
+        for (int j = 0; j < rJ; ++j) {
+            const int32_t cj = c->cptr[J] + j;
+            for (int64_t q = 0; q < nbJ; ++q) {
+                const int I = bI[b0 + q];
+                const int rI = c->cptr[I + 1] - c->cptr[I];
+                const double* blk = hb.data() + boff[b0 + q];
+                for (int i = (I == J ? j : 0); i < rI; ++i) {
+                    er.push_back(c->cptr[I] + i);
+                    ec.push_back(cj);
+                    ev.push_back(blk[(int64_t)i * rJ + j]);
+                }
+            }
+        }
+        b0 += nbJ;
+    }
+    return done(DDG_OK);
+}
+
 // Shared-memory plan of k_pcg_small (pcg.cu), the same walk the kernel makes:
 // CTA g of G keeps its operators t = g, g + G, ... of every colour (tiles and
 // index lists), tile row and column s = G - 1 - g of the coarse inverse
@@ -1101,6 +1060,12 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     else ddg_default_opts(&c->opts);
     if (c->opts.overlap < 0) { free_ctx(c); return set_err(DDG_E_ARG, "overlap < 0"); }
     if (c->opts.max_iter <= 0) c->opts.max_iter = 1000;
+    if (c->opts.local_variant < DDG_LOCAL_AUTO || c->opts.local_variant > DDG_LOCAL_INVERSE) {
+        int lv = c->opts.local_variant;
+        free_ctx(c);
+        return set_err(DDG_E_ARG, "local_variant %d not one of DDG_LOCAL_*", lv);
+    }
+    c->chol = c->opts.local_variant == DDG_LOCAL_CHOLESKY;
     c->n = n;
     c->k = k;
     c->nparts = nparts;
@@ -1190,12 +1155,34 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
                              c->nranks);
         tick("decomposition plan");
     }
-    if ((st = build_basis(c, F))) { free_ctx(c); return st; }
-    tick("basis (dd-MGS)");
+    // A, the parts and the row positions on the device: the coarse space is
+    // built there (basis.cu), and the hot path keeps A, bptr and bidx
+    {
+        std::vector<int32_t> rp32(n + 1);
+        for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
+        if ((st = upload(&c->d_rp, rp32)) || (st = dalloc(&c->d_col, c->nnz)) || (st = dalloc(&c->d_val, c->nnz)) ||
+            (st = h2d(c->stream, c->d_col, col, c->nnz * 4)) || (st = h2d(c->stream, c->d_val, val, c->nnz * 8)) ||
+            (st = upload(&c->d_bptr, c->bptr)) || (st = upload(&c->d_bidx, c->bidx))) {
+            free_ctx(c);
+            return st;
+        }
+    }
+    int32_t *d_part = nullptr, *d_bpos = nullptr;
+    if ((st = upload(&d_part, c->part)) || (st = upload(&d_bpos, c->bpos))) {
+        cudaFree(d_part);
+        free_ctx(c);
+        return st;
+    }
+    tick("upload A");
     std::vector<int32_t> er, ec;
     std::vector<double> ev;
-    build_galerkin(c, row_ptr, col, val, er, ec, ev);
-    tick("galerkin");
+    if ((st = device_basis(c, F, d_part))) { cudaFree(d_part); cudaFree(d_bpos); free_ctx(c); return st; }
+    tick("basis (dd-MGS, GPU)");
+    st = device_galerkin(c, row_ptr, col, d_part, d_bpos, er, ec, ev);
+    cudaFree(d_part);
+    cudaFree(d_bpos);
+    if (st) { free_ctx(c); return st; }
+    tick("galerkin (GPU)");
     // environment overrides for experiments (documented in DESIGN.md)
     if (const char* e = getenv("DDG_FUSE_GATHER")) c->opts.fuse_gather = atoi(e);
     if (const char* e = getenv("DDG_SMALL_KERNEL")) c->opts.small_kernel = atoi(e);
@@ -1238,16 +1225,6 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
         tick("coarse symbolic (nested dissection)");
     }
     // uploads
-    std::vector<int32_t> rp32(n + 1);
-    for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
-    if ((st = upload(&c->d_rp, rp32)) || (st = dalloc(&c->d_col, c->nnz)) || (st = dalloc(&c->d_val, c->nnz))) {
-        free_ctx(c);
-        return st;
-    }
-    if ((st = h2d(c->stream, c->d_col, col, c->nnz * 4)) || (st = h2d(c->stream, c->d_val, val, c->nnz * 8))) {
-        free_ctx(c);
-        return st;
-    }
     {
         const double mean = (double)c->nnz / (double)std::max<int64_t>(1, n);
         int sw = mean <= 16 ? 1 : mean <= 48 ? 4 : mean <= 128 ? 8 : 32;
@@ -1288,9 +1265,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     if ((st = upload(&c->d_oidx, c->oidx)) || (st = upload(&c->d_ops, c->ops)) ||
         (st = upload(&c->d_items, c->items)) || (st = upload(&c->d_red, c->red)) ||
         (st = dalloc(&c->d_tiles, c->tiles_doubles)) || (st = dalloc(&c->d_s, c->s_doubles)) ||
-        (st = dalloc(&c->d_partials, c->part_doubles)) || (st = upload(&c->d_bptr, c->bptr)) ||
-        (st = upload(&c->d_bidx, c->bidx)) || (st = upload(&c->d_cptr, c->cptr)) ||
-        (st = upload(&c->d_qoff, c->qoff)) || (st = upload(&c->d_Q, c->Q)) ||
+        (st = dalloc(&c->d_partials, c->part_doubles)) ||
         (st = dalloc(&c->d_yc, c->nc)) || (st = dalloc(&c->d_r, n)) || (st = dalloc(&c->d_z, n)) ||
         (st = dalloc(&c->d_p, n)) || (st = dalloc(&c->d_q, n)) || (st = dalloc(&c->d_f, n)) ||
         (st = dalloc(&c->d_u, n)) || (st = dalloc(&c->d_x, n)) || (st = dalloc(&c->d_sc, 1)) ||
@@ -1374,7 +1349,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     // coarse inverse with at most G tile rows, single-item local operators, n small,
     // and everything a CTA keeps resident within its shared memory (small_plan)
     // (DDG_SMALL_FUSED=0: off)
-    if (!(getenv("DDG_SMALL_FUSED") && atoi(getenv("DDG_SMALL_FUSED")) == 0)) {
+    if (!c->chol && !(getenv("DDG_SMALL_FUSED") && atoi(getenv("DDG_SMALL_FUSED")) == 0)) {
         if ((st = small_plan(c))) { free_ctx(c); return st; }
     }
     tick("upload");
@@ -1397,6 +1372,10 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     c->local_bytes = 0;
     for (int q = 0; q < (int)c->op_sub.size(); ++q) {
         const OpDesc& op = c->ops[q];
+        if (c->chol) {
+            c->local_bytes += (int64_t)op.nT * (op.nT + 1) / 2 * TILE_ELEMS * 8;
+            continue;
+        }
         for (int t = 0; t < op.nitems; ++t) {
             const ItemDesc& d = c->items[op.item_base + t];
             c->local_bytes += item_doubles(d.tri, d.I1 - d.I0, d.ntiles, d.tail) * 8;
@@ -1437,6 +1416,23 @@ static void halo(ddg_ctx* c, ddg::Halo& h, double* v) {
 
 static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
     const ColourPlan& pl = c->plans[cc];
+    if (c->chol) {   // DDG_LOCAL_CHOLESKY: gather s, then forward + back substitution per subdomain
+        if (pl.sub_end > pl.sub_begin) {
+            const OpDesc& lo = c->ops[pl.sub_begin];
+            const OpDesc& hi = c->ops[pl.sub_end - 1];
+            prof(c, PC_GATHER, 0, [&] {
+                launch_gather_flat(c->stream, lo.s_off, hi.s_off + hi.mp, c->d_gidx, c->A, r, z, c->d_s, z_zero,
+                                   done);
+            });
+            prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
+                launch_chol_solve(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin,
+                                  (pl.max_rows + TILE - 1) / TILE * TILE, c->d_tiles, c->d_s, c->d_oidx, z, done);
+            });
+            c->launches += 2;
+        }
+        halo(c, c->h_z[cc], z);
+        return;
+    }
     int gmode = 0;
     const bool ring = ring_ok(c, pl.ring_off);
     const bool fuse = !ring && pl.all_single && (c->opts.fuse_gather == 2 ||

@@ -49,7 +49,8 @@ class ddg_opts(C.Structure):
                 ("block_ndim", C.c_int), ("fuse_gather", C.c_int), ("comm", C.c_void_p),
                 ("small_kernel", C.c_int), ("block_coords", C.c_void_p),
                 ("stencil", C.POINTER(ddg_stencil)), ("part2", C.c_void_p),
-                ("nparts2", C.c_int32), ("block_coords2", C.c_void_p), ("colour", C.c_void_p)]
+                ("nparts2", C.c_int32), ("block_coords2", C.c_void_p), ("colour", C.c_void_p),
+                ("local_variant", C.c_int)]
 
 
 class ddg_report(C.Structure):
@@ -165,7 +166,8 @@ class Solver:
     def __init__(self, n, row_ptr, col, val, F, part, nparts, overlap=1, rank_tol=1e-8,
                  stop_mode=STOP_RES0, max_iter=1000, device=0, stream=None, use_graphs=True,
                  verbose=False, coarse_variant=0, block_coords=None, comm=None, fuse_gather=None,
-                 small_kernel=None, stencil=None, part2=None, nparts2=0, block_coords2=None, colour=None):
+                 small_kernel=None, stencil=None, part2=None, nparts2=0, block_coords2=None, colour=None,
+                 local_variant=0):
         """part2 (int32[nparts]: second-level part of every part) selects the
         three-level method (include/ddg.h ddg_opts.part2)."""
         L = load()
@@ -176,6 +178,7 @@ class Solver:
         o.use_graphs = 1 if use_graphs else 0
         o.verbose = 1 if verbose else 0
         o.coarse_variant = int(coarse_variant)
+        o.local_variant = int(local_variant)
         if fuse_gather is not None:
             o.fuse_gather = int(fuse_gather)
         if small_kernel is not None:

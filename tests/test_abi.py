@@ -59,6 +59,9 @@ def test_argument_errors_before_device(lib):
     with pytest.raises(ddg.DDGError) as e:
         ddg.Solver(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, bad, pr.nparts)
     assert e.value.code == 3
+    with pytest.raises(ddg.DDGError) as e:     # local_variant outside DDG_LOCAL_*
+        ddg.Solver(pr.n, pr.row_ptr, pr.col, pr.val, pr.F, pr.part, pr.nparts, local_variant=5)
+    assert e.value.code == 1
     col = pr.col.copy(); col[1], col[2] = col[2], col[1]
     with pytest.raises(ddg.DDGError) as e:
         ddg.Solver(pr.n, pr.row_ptr, col, pr.val, pr.F, pr.part, pr.nparts)

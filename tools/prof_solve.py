@@ -27,6 +27,7 @@ kw = {}
 if levels == 3:
     p2, n2, bc2 = P.coarse_parts(pr, factor, coords=True)
     kw = dict(part2=p2, nparts2=n2, block_coords2=bc2)
+kw["local_variant"] = int(os.environ.get("LOCAL_VARIANT", "0"))   # 1: Cholesky substitutions
 s = Solver.from_problem(pr, device=0, stream=stream.cuda_stream, verbose=int(os.environ.get("VERBOSE", "0")), **kw)
 inf = s.info
 print(f"levels={inf.levels} n_c={inf.n_c} colours={inf.ncolours} n_c2={inf.n_c2} parts2={inf.nparts2} "
