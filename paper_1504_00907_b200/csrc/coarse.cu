@@ -647,6 +647,28 @@ void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* f
     k_front_bwd_gather<<<nf, 256, 0, st>>>(f0, fronts, fB, x, fvec, done);
 }
 
+// distributed coarse solve (coarse_sparse.cpp) --------------
+// dst[k] = mask[k] ? src[idx ? idx[k] : k] : 0  (a rank's share of an allreduce)
+__global__ void k_gather_masked(int64_t n, const int32_t* __restrict__ idx, const uint8_t* __restrict__ mask,
+                                const double* __restrict__ src, double* __restrict__ dst) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = mask[k] ? src[idx ? idx[k] : k] : 0.0;
+}
+// next dataflow phase: queue head back to 0, the children counters of the
+// replicated top fronts preset to their children solved by the ranks
+__global__ void k_df_preset(int n, const int32_t* __restrict__ slot, const int32_t* __restrict__ val,
+                            int32_t* __restrict__ state) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) state[slot[k]] = val[k];
+    if (blockIdx.x == 0 && threadIdx.x == 0) state[0] = 0;
+}
+void launch_gather_masked(cudaStream_t st, int64_t n, const int32_t* idx, const uint8_t* mask, const double* src,
+                          double* dst) {
+    if (n > 0) k_gather_masked<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, idx, mask, src, dst);
+}
+void launch_df_preset(cudaStream_t st, int n, const int32_t* slot, const int32_t* val, int32_t* state) {
+    k_df_preset<<<std::max(1, std::min((n + 255) / 256, 64)), 256, 0, st>>>(n, slot, val, state);
+}
+
 void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,
                          const FrontDesc* fronts, const int32_t* fS, const double* partials, double* w,
                          double* x, const int32_t* done) {

@@ -27,6 +27,7 @@
 #include <numeric>
 
 #include "ctx.h"
+#include "comm.h"
 
 namespace {
 
@@ -75,13 +76,27 @@ struct SparseCoarse {
     int64_t* d_contrib = nullptr;
     double *d_fvec = nullptr, *d_w = nullptr, *d_ctiles = nullptr, *d_bc = nullptr;
     int64_t factor_bytes = 0;
+    // distributed solve (sparse_coarse_dist_setup): the top fronts replicated,
+    // every subtree below them solved by one rank
+    bool dist = false;
+    int nw1 = 0, nw2 = 0, nw3 = 0, npreset = 0;
+    int64_t nwx = 0, rank_solve_bytes = 0;
+    int32_t *d_work1 = nullptr, *d_work2 = nullptr, *d_work3 = nullptr;
+    int32_t *d_preset_slot = nullptr, *d_preset_val = nullptr, *d_wx_idx = nullptr;
+    uint8_t *d_wx_mask = nullptr, *d_y_mask = nullptr;
+    FrontDesc* d_fr1 = nullptr;
+    double *d_wx_buf = nullptr, *d_y_buf = nullptr;
+    int ntop = 0, nsub = 0;
 };
+
+int64_t sparse_coarse_solve_bytes(ddg_ctx* c);
 
 void sparse_coarse_free(SparseCoarse* s) {
     if (!s) return;
     void* p[] = {s->d_fr, s->d_fchild, s->d_fS, s->d_fB, s->d_fmap, s->d_item_front, s->d_fwd, s->d_bwd,
                  s->d_contrib, s->d_fvec, s->d_w, s->d_ctiles, s->d_bc, s->d_dfwork, s->d_dfstate, s->d_fdf,
-                 s->d_trace};
+                 s->d_trace, s->d_work1, s->d_work2, s->d_work3, s->d_preset_slot, s->d_preset_val,
+                 s->d_wx_idx, s->d_wx_mask, s->d_y_mask, s->d_fr1, s->d_wx_buf, s->d_y_buf};
     for (void* x : p)
         if (x) cudaFree(x);
     delete s;
@@ -637,6 +652,159 @@ static int up_s(cudaStream_t s, T** d, const std::vector<T>& h) {
 #define up(d, h) up_s(c->stream, d, h)
 
 // --------------------------------------------------------------------------
+// distributed solve plan
+// --------------------------------------------------------------------------
+// The nested-dissection tree is cut at depth D = ceil(log2 P): the fronts
+// above the cut (the top separators) are solved redundantly by every rank,
+// every subtree below it by one rank (greedy by solve bytes).  One solve:
+//   phase 1  forward elimination over this rank's subtrees (dataflow kernel;
+//            the subtree roots stop there, as if they were roots)
+//   exchange the subtree roots' contributions w_t to their top ancestors:
+//            one allreduce of their concatenation (zeros from non-owners)
+//   phase 2  forward + backward over the top fronts (replicated); their
+//            children counters preset to the subtrees already eliminated
+//   phase 3  backward substitution over this rank's subtrees
+//   y_c      one allreduce: each unknown contributed by exactly one rank (a
+//            subtree's owner, rank 0 for the top), so every rank holds the
+//            same y_c bitwise.
+// The factor stays replicated in memory (the top fronts need every subtree's
+// Schur complement at setup); each rank READS only the top fronts and its
+// own subtrees per solve, which is what bounds the coarse step's time.
+struct DistSplit {
+    std::vector<char> top, sroot;
+    std::vector<int> owner, roots;
+    std::vector<double> fbytes;
+};
+static void dist_split(ddg_ctx* c, int P, DistSplit& ds) {
+    SparseCoarse* sc = c->sparse;
+    const int nn = sc->nfront;
+    std::vector<char>& top = ds.top;
+    std::vector<char>& sroot = ds.sroot;
+    std::vector<int>& owner = ds.owner;
+    std::vector<int>& roots = ds.roots;
+    std::vector<double>& fbytes = ds.fbytes;
+    top.assign(nn, 0);
+    sroot.assign(nn, 0);
+    roots.clear();
+    int D = 0;
+    while ((1 << D) < P) ++D;
+    std::vector<int> depth(nn, 0);
+    for (int i = nn - 1; i >= 0; --i) depth[i] = sc->fr[i].parent < 0 ? 0 : depth[sc->fr[i].parent] + 1;
+    for (int i = 0; i < nn; ++i) top[i] = depth[i] < D;
+    // solve bytes per front (G twice, H once)
+    fbytes.assign(nn, 0.0);
+    for (int h = 0; h < sc->nlevels; ++h)
+        for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q) {
+            const ItemDesc& d = c->items[q];
+            fbytes[sc->item_front[q - sc->item_base]] +=
+                item_doubles(d.tri, d.I1 - d.I0, d.ntiles) * 8.0 * (q < sc->g_end[h] ? 2 : 1);
+        }
+    std::vector<double> sub(nn, 0.0);   // subtree bytes (children have lower indices)
+    for (int i = 0; i < nn; ++i) {
+        sub[i] += fbytes[i];
+        if (sc->fr[i].parent >= 0) sub[sc->fr[i].parent] += sub[i];
+    }
+    for (int i = 0; i < nn; ++i)
+        if (!top[i] && (sc->fr[i].parent < 0 || top[sc->fr[i].parent])) {
+            sroot[i] = 1;
+            roots.push_back(i);
+        }
+    owner.assign(nn, -1);
+    std::vector<int> sorted = roots;
+    std::stable_sort(sorted.begin(), sorted.end(), [&](int a, int b) { return sub[a] > sub[b]; });
+    std::vector<double> load(P, 0.0);
+    for (int r : sorted) {
+        const int k = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        owner[r] = k;
+        load[k] += sub[r];
+    }
+    for (int i = nn - 1; i >= 0; --i)
+        if (!top[i] && !sroot[i]) owner[i] = owner[sc->fr[i].parent];
+}
+
+static int sparse_coarse_dist_setup(ddg_ctx* c) {
+    SparseCoarse* sc = c->sparse;
+    const int nn = sc->nfront, P = c->nranks, me = c->rank;
+    DistSplit ds;
+    dist_split(c, P, ds);
+    const std::vector<char>& top = ds.top;
+    const std::vector<int>& owner = ds.owner;
+    const std::vector<int>& roots = ds.roots;
+    const std::vector<double>& fbytes = ds.fbytes;
+    if (roots.empty()) return DDG_OK;   // the whole tree is above the cut: replicated solve
+    int D = 0;
+    while ((1 << D) < P) ++D;
+    auto mine = [&](int f) { return !top[f] && owner[f] == me; };
+    auto entry_front = [&](int32_t e) {
+        const int idx = e & DF_IDX;
+        if (e & DF_ASSEMBLE) return idx;
+        if (e & DF_RED) return (e & DF_BWD) ? sc->bwd[idx].front : sc->fwd[idx].front;
+        return (int)sc->item_front[idx - sc->item_base];
+    };
+    std::vector<int32_t> w1, w2, w3;
+    std::vector<int32_t> pslot, pval;
+    for (int i = 0; i < nn; ++i) {
+        if (!top[i] || sc->fr[i].nchild == 0) continue;
+        int nsubch = 0;
+        for (int k = 0; k < sc->fr[i].nchild; ++k) nsubch += !top[sc->fchild[sc->fr[i].child_off + k]];
+        if (nsubch == sc->fr[i].nchild) {
+            w2.push_back(DF_ASSEMBLE | i);                   // all children eliminated by the ranks
+        } else if (nsubch > 0) {
+            pslot.push_back(1 + DF_STATE_PER_FRONT * i + 3);   // DFF_CHILDREN (coarse.cu)
+            pval.push_back(nsubch);
+        }
+    }
+    for (int32_t e : sc->dfwork) {
+        const int f = entry_front(e);
+        if (top[f]) w2.push_back(e);
+        else if (mine(f)) (e & DF_BWD ? w3 : w1).push_back(e);
+    }
+    // phase-1 fronts: subtree roots end the forward elimination like roots
+    std::vector<FrontDesc> fr1 = sc->fr;
+    for (int r : roots) fr1[r].parent = -1;
+    // w exchange: the subtree roots' w, concatenated (zero slot for non-owners)
+    std::vector<int32_t> wx;
+    std::vector<uint8_t> wm;
+    for (int r : roots)
+        for (int j = 0; j < sc->fr[r].nB; ++j) {
+            wx.push_back((int32_t)(sc->fr[r].w_off + j));
+            wm.push_back(owner[r] == me);
+        }
+    // y_c: who contributes each coarse unknown
+    std::vector<uint8_t> ym(c->nc, 0);
+    for (int i = 0; i < nn; ++i) {
+        const bool contrib = top[i] ? me == 0 : owner[i] == me;
+        if (!contrib) continue;
+        for (int a = 0; a < sc->fr[i].nS; ++a) ym[sc->fS[sc->fr[i].S_off + a]] = 1;
+    }
+    int st;
+    if ((st = up(&sc->d_work1, w1)) || (st = up(&sc->d_work2, w2)) || (st = up(&sc->d_work3, w3)) ||
+        (st = up(&sc->d_fr1, fr1)) || (st = up(&sc->d_wx_idx, wx)) || (st = up(&sc->d_wx_mask, wm)) ||
+        (st = dalloc(&sc->d_wx_buf, std::max<size_t>(1, wx.size()))) || (st = up(&sc->d_y_mask, ym)) ||
+        (st = dalloc(&sc->d_y_buf, std::max<int64_t>(1, c->nc))))
+        return st;
+    if (!pslot.empty() && ((st = up(&sc->d_preset_slot, pslot)) || (st = up(&sc->d_preset_val, pval)))) return st;
+    sc->nw1 = (int)w1.size();
+    sc->nw2 = (int)w2.size();
+    sc->nw3 = (int)w3.size();
+    sc->npreset = (int)pslot.size();
+    sc->nwx = (int64_t)wx.size();
+    sc->ntop = 0;
+    for (int i = 0; i < nn; ++i) sc->ntop += top[i];
+    sc->nsub = (int)roots.size();
+    double rb = 0;
+    for (int i = 0; i < nn; ++i)
+        if (top[i] || owner[i] == me) rb += fbytes[i];
+    sc->rank_solve_bytes = (int64_t)rb;
+    sc->dist = true;
+    if (c->opts.verbose)
+        fprintf(stderr, "[ddg_setup] distributed coarse solve: depth %d cut, %d top fronts, %d subtrees; rank %d "
+                "reads %.2f of %.2f GB per solve\n", D, sc->ntop, sc->nsub, me, rb / 1e9,
+                (double)sparse_coarse_solve_bytes(c) / 1e9);
+    return DDG_OK;
+}
+
+// --------------------------------------------------------------------------
 // numeric phase (device)
 // --------------------------------------------------------------------------
 int sparse_coarse_numeric(ddg_ctx* c) {
@@ -800,6 +968,9 @@ int sparse_coarse_numeric(ddg_ctx* c) {
     cudaFree(d_fptr); cudaFree(d_err); cudaFree(d_ids); cudaFree(d_nT); cudaFree(d_nK); cudaFree(d_tasks);
     if (herr[0] >= 0)
         return set_err(DDG_E_NOT_SPD, "coarse factor: front %d not positive definite at pivot %d", herr[0], herr[1]);
+    if (c->dist && c->nranks > 1 && sc->dataflow && !(getenv("DDG_COARSE_REPLICATED") &&
+                                                      atoi(getenv("DDG_COARSE_REPLICATED")) != 0))
+        return sparse_coarse_dist_setup(c);
     return DDG_OK;
 }
 
@@ -812,6 +983,7 @@ int64_t sparse_coarse_bytes(ddg_ctx* c) { return c->sparse ? c->sparse->factor_b
 int64_t sparse_coarse_solve_bytes(ddg_ctx* c) {
     if (!c->sparse) return 0;
     const SparseCoarse* sc = c->sparse;
+    if (sc->dist) return sc->rank_solve_bytes;
     int64_t b = 0;
     for (int h = 0; h < sc->nlevels; ++h)
         for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q) {
@@ -826,6 +998,28 @@ int sparse_coarse_nfront(ddg_ctx* c) { return c->sparse ? c->sparse->nfront : 0;
 int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
     SparseCoarse* sc = c->sparse;
     int launches = 0;
+    if (sc->dist) {
+        auto df = [&](int nw, const int32_t* work, const FrontDesc* fr) {
+            launch_coarse_dataflow(c->stream, nw, work, fr, sc->d_fchild, sc->d_fdf, sc->d_item_front, sc->item_base,
+                                   c->d_ops, c->d_items, sc->d_ctiles, sc->d_fwd, sc->d_bwd, sc->d_contrib, sc->d_fS,
+                                   sc->d_fB, sc->d_fmap, sc->d_bc, sc->d_fvec, sc->d_w, d_x, c->d_partials,
+                                   sc->d_dfstate, sc->max_rows_t, done, nullptr);
+        };
+        int err = 0;
+        cudaMemsetAsync(sc->d_dfstate, 0, (1 + (size_t)DF_STATE_PER_FRONT * sc->nfront) * sizeof(int32_t), c->stream);
+        df(sc->nw1, sc->d_work1, sc->d_fr1);                                       // phase 1: own subtrees, forward
+        launch_gather_masked(c->stream, sc->nwx, sc->d_wx_idx, sc->d_wx_mask, sc->d_w, sc->d_wx_buf);
+        err |= ddg::comm_allreduce_sum(c->comm, sc->d_wx_buf, sc->d_wx_buf, (size_t)sc->nwx, c->stream);
+        launch_halo_unpack(c->stream, sc->d_wx_buf, sc->d_wx_idx, sc->d_w, sc->nwx);
+        launch_df_preset(c->stream, sc->npreset, sc->d_preset_slot, sc->d_preset_val, sc->d_dfstate);
+        df(sc->nw2, sc->d_work2, sc->d_fr);                                        // phase 2: top fronts
+        cudaMemsetAsync(sc->d_dfstate, 0, sizeof(int32_t), c->stream);
+        df(sc->nw3, sc->d_work3, sc->d_fr);                                        // phase 3: own subtrees, back
+        launch_gather_masked(c->stream, c->nc, nullptr, sc->d_y_mask, d_x, sc->d_y_buf);
+        err |= ddg::comm_allreduce_sum(c->comm, sc->d_y_buf, d_x, (size_t)c->nc, c->stream);
+        if (err && !c->comm_err) c->comm_err = err;
+        return 8;
+    }
     if (sc->dataflow) {
         cudaMemsetAsync(sc->d_dfstate, 0, (1 + (size_t)DF_STATE_PER_FRONT * sc->nfront) * sizeof(int32_t),
                         c->stream);
@@ -871,6 +1065,26 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         launches += 3;
     }
     return launches;
+}
+
+// debug (not part of include/ddg.h): the distributed coarse solve's split for
+// P ranks on this context's tree (the plan sparse_coarse_dist_setup makes):
+// coarse solve bytes read per rank (top fronts + its subtrees) into
+// bytes[0 .. P), the top fronts' share into *top; returns the number of
+// subtrees (0: the whole tree lies above the cut), -1 without a sparse coarse
+extern "C" int ddg_debug_coarse_split(ddg_ctx* c, int P, double* bytes, double* top) {
+    if (!c || !c->sparse || P < 1) return -1;
+    DistSplit ds;
+    dist_split(c, P, ds);
+    double tb = 0;
+    for (int p = 0; p < P; ++p) bytes[p] = 0;
+    for (size_t i = 0; i < ds.top.size(); ++i) {
+        if (ds.top[i]) tb += ds.fbytes[i];
+        else bytes[ds.owner[i]] += ds.fbytes[i];
+    }
+    for (int p = 0; p < P; ++p) bytes[p] += tb;
+    *top = tb;
+    return (int)ds.roots.size();
 }
 
 // debug (not part of include/ddg.h): the dataflow trace of the last coarse

@@ -418,6 +418,131 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
     }
 }
 
+// Pipelined full-exchange block product (the default for the blocked exchange):
+// the same three modes as k_gjb_gemm<true> with the operand tiles streamed by
+// 16-byte cp.async into GJP_STAGES shared-memory stages (stage q + 2 in flight
+// while q computes), B stored column-major per output column so both fragment
+// loads are conflict-free; the trailing mode's C tiles are bulk-prefetched into
+// L2 at the start, so the epilogue's C + A B read-modify-write hits L2.  (Adding
+// the products onto C inside the accumulators instead was measured: the same
+// speed, but 1e-14 instead of 3e-15 against numpy's inverse in tools/gjunit.py.)
+constexpr int GJP_LDA = GJB_N + 8;                          // As[kk][row]
+constexpr int GJP_LDK = TILE + 4;                           // Bs[col][kk]
+constexpr int GJP_STAGE = TILE * GJP_LDA + GJB_N * GJP_LDK; // doubles per stage (71.7 KB)
+constexpr int GJP_STAGES = 3;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+__global__ void __launch_bounds__(256) k_gjb_gemm_pipe(GJBatch bt, int k0, int mode) {
+    extern __shared__ __align__(16) double psm[];
+    const int b = blockIdx.y;
+    const int nT = bt.nT[b], nK = bt.nK[b];
+    if (k0 >= nK) return;
+    const int k1 = min(k0 + GJB_BT, nK);
+    const int nb = (nT + GJB_BT - 1) / GJB_BT;
+    int bi, bj;
+    if (mode == 1) {
+        if ((int)blockIdx.x >= nb * nb) return;
+        bi = blockIdx.x % nb;
+        bj = blockIdx.x / nb;
+    } else {
+        if ((int)blockIdx.x >= nb) return;
+        bi = mode == 0 ? k0 / GJB_BT : blockIdx.x;
+        bj = mode == 0 ? blockIdx.x : k0 / GJB_BT;
+    }
+    const int i0 = bi * GJB_BT, j0 = bj * GJB_BT;
+    auto in_kb = [&](int t) { return t >= k0 && t < k1; };
+    auto owns = [&](int I, int J) {
+        return mode == 0 ? (in_kb(I) && !in_kb(J)) : mode == 1 ? (!in_kb(I) && !in_kb(J)) : (!in_kb(I) && in_kb(J));
+    };
+    {
+        bool any = false;
+        for (int I = i0; I < min(i0 + GJB_BT, nT); ++I)
+            for (int J = j0; J < min(j0 + GJB_BT, nT); ++J) any |= owns(I, J);
+        if (!any) return;
+    }
+    double* M = bt.mats[b];
+    auto tile = [&](int I, int J) { return M + ((int64_t)J * nT + I) * TILE_ELEMS; };
+    const int nq = k1 - k0;
+    auto load_stage = [&](int q, int slot) {
+        double* As = psm + slot * GJP_STAGE;
+        double* Bs = As + TILE * GJP_LDA;
+        constexpr int CH = TILE * TILE / 2;   // 16-byte chunks per tile
+        for (int e = threadIdx.x; e < GJB_BT * CH; e += 256) {
+            const int t = e / CH, rem = e % CH;
+            const int kk = rem / (TILE / 2), r2 = (rem % (TILE / 2)) * 2;
+            // A: tile (I, q), element (r, kk) at kk * 32 + r  ->  As[kk][t * 32 + r]
+            const int I = (mode == 0 ? k0 : i0) + t;
+            const bool oka = I < nT && (mode != 0 || I < k1);
+            cp_async16(As + kk * GJP_LDA + t * TILE + r2, oka ? tile(I, q) + kk * TILE + r2 : M, oka);
+            // B: tile (q, J), element (kk, c) at c * 32 + kk  ->  Bs[t * 32 + c][kk]
+            const int c = kk, k2 = r2;
+            const int J = (mode == 2 ? k0 : j0) + t;
+            const bool okb = J < nT && (mode != 2 || J < k1);
+            cp_async16(Bs + (t * TILE + c) * GJP_LDK + k2, okb ? tile(q, J) + c * TILE + k2 : M, okb);
+        }
+    };
+#pragma unroll
+    for (int sg = 0; sg < GJP_STAGES - 1; ++sg) {
+        if (sg < nq) load_stage(k0 + sg, sg);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int wr = (wid & 3) * 32, wc = (wid >> 2) * 64;   // this warp's 32 x 64 output tile
+    const int I = i0 + wr / TILE;
+    // value v = 16 mi + 2 ni + h of acc (acc[v / 8][v % 8]) is
+    // C(wr + 8 mi + lane / 4, wc + 8 ni + 2 (lane % 4) + h)
+    if (mode == 1 && threadIdx.x < GJB_BT * GJB_BT) {
+        const int Ip = i0 + threadIdx.x / GJB_BT, Jp = j0 + threadIdx.x % GJB_BT;
+        if (Ip < nT && Jp < nT && owns(Ip, Jp)) bulk_prefetch_l2(tile(Ip, Jp), TILE_ELEMS * sizeof(double));
+    }
+    double acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c2 = 0; c2 < 8; ++c2) acc[r][c2] = 0.0;
+    for (int qi = 0; qi < nq; ++qi) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(GJP_STAGES - 2) : "memory");
+        __syncthreads();
+        if (qi + GJP_STAGES - 1 < nq) load_stage(k0 + qi + GJP_STAGES - 1, (qi + GJP_STAGES - 1) % GJP_STAGES);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const double* As = psm + (qi % GJP_STAGES) * GJP_STAGE;
+        const double* Bs = As + TILE * GJP_LDA;
+#pragma unroll 2
+        for (int kq = 0; kq < TILE; kq += 4) {
+            double af[4], bf[8];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) af[mi] = As[(kq + (lane & 3)) * GJP_LDA + wr + 8 * mi + (lane >> 2)];
+#pragma unroll
+            for (int ni = 0; ni < 8; ++ni) bf[ni] = Bs[(wc + 8 * ni + (lane >> 2)) * GJP_LDK + kq + (lane & 3)];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 8; ++ni)
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                 : "+d"(acc[2 * mi + ni / 4][(2 * ni) % 8]), "+d"(acc[2 * mi + ni / 4][(2 * ni) % 8 + 1])
+                                 : "d"(af[mi]), "d"(bf[ni]));
+        }
+    }
+    if (I >= nT) return;
+#pragma unroll
+    for (int ni = 0; ni < 8; ++ni) {
+        const int J = j0 + (wc + 8 * ni) / TILE;
+        if (J >= nT || !owns(I, J)) continue;
+        double* T = tile(I, J);
+        const int cc = (wc + 8 * ni) % TILE + 2 * (lane & 3);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double v = acc[2 * mi + ni / 4][(2 * ni) % 8 + h];
+                double* p = T + (cc + h) * TILE + 8 * mi + (lane >> 2);
+                *p = mode == 1 ? *p + v : (mode == 0 ? -v : v);
+            }
+    }
+}
+
 // Dense tiled A_c from its lower-triangle entries (mirrored => exactly symmetric,
 // reading R9); identity on the padding.
 __global__ void k_scatter_coarse(int64_t nent, const int32_t* __restrict__ row,
@@ -576,10 +701,12 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
     const int smem_p = 9 * TILE_ELEMS * sizeof(double);
     const int smem_g = (TILE * GJB_N + TILE * GJB_BPAD) * sizeof(double);
     const int smem_m = 2 * TILE * GJB_LDM * sizeof(double);
+    const int smem_pp = GJP_STAGES * GJP_STAGE * sizeof(double);
     if (!init) {
         cudaFuncSetAttribute(k_gjb_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p);
         cudaFuncSetAttribute(k_gjb_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);
         cudaFuncSetAttribute(k_gjb_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_m);
+        cudaFuncSetAttribute(k_gjb_gemm_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
         init = true;
     }
     GJBatch bt{mats, nT, nK, ids, err, nullptr, 0};
@@ -595,9 +722,15 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
         bt.strip = nullptr;
     cudaGetLastError();
     const bool use_mma = !getenv("DDG_GJ_MMA") || atoi(getenv("DDG_GJ_MMA")) != 0;   // experiment switch
+    // the pipelined MMA product for the full exchange (DDG_GJ_PIPE=0: the single-stage one)
+    const bool use_pipe = use_mma && !bt.strip && !(getenv("DDG_GJ_PIPE") && atoi(getenv("DDG_GJ_PIPE")) == 0);
     for (int k0 = 0; k0 < maxK; k0 += GJB_BT) {
         k_gjb_pivot<<<nmat, 256, smem_p, st>>>(bt, k0);
-        if (use_mma) {
+        if (use_pipe) {
+            k_gjb_gemm_pipe<<<dim3(nb, nmat), 256, smem_pp, st>>>(bt, k0, 0);
+            k_gjb_gemm_pipe<<<dim3(nb * nb, nmat), 256, smem_pp, st>>>(bt, k0, 1);
+            k_gjb_gemm_pipe<<<dim3(nb, nmat), 256, smem_pp, st>>>(bt, k0, 2);
+        } else if (use_mma) {
             k_gjb_gemm<true><<<dim3(nb, nmat), 256, smem_m, st>>>(bt, k0, 0);
             k_gjb_gemm<true><<<dim3(nb * nb, nmat), 256, smem_m, st>>>(bt, k0, 1);
             k_gjb_gemm<true><<<dim3(nb, nmat), 256, smem_m, st>>>(bt, k0, 2);

@@ -149,3 +149,45 @@ def test_loopback_rejects_mismatched_collectives():
 
     codes = run_ranks(2, rank)
     assert 9 in codes
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+@pytest.mark.parametrize("name", ["lognormal_32_b4", "biharm_128_b16_p3", "poisson3d_32_b8_p2"])
+def test_loopback_distributed_coarse_solve(name, nranks, monkeypatch):
+    """the sparse coarse solve distributed over the ranks --
+    the nested-dissection tree cut at depth ceil(log2 P), the top fronts solved
+    by every rank, each subtree below by one rank (forward, an allreduce of
+    the subtree roots' contributions, the top fronts, backward), y_c assembled
+    by one allreduce.  Against the oracle (north-star bar), bitwise equal to
+    the replicated solve (DDG_COARSE_REPLICATED=1: every rank the whole tree),
+    and each rank reads fewer coarse bytes per solve."""
+    from paper_1504_00907_b200 import Solver
+    monkeypatch.setenv("DDG_ND_LEAF", "64")       # a deep tree on a test-sized A_c
+    pr = CASES[name]()
+    o = oracle.Oracle.from_problem(pr)
+    uo, ito, histo, conv = o.pcg(pr.f, 1e-8)
+    r = np.random.default_rng(6).standard_normal(pr.n)
+
+    def rank(rk, comm):
+        s = Solver.from_problem(pr, comm=comm, coarse_variant=2)
+        zc = s.coarse_correct(r)
+        u, it, hist, rep = s.solve(pr.f, 1e-8)
+        nb = s.info.coarse_solve_bytes
+        s.close()
+        return zc, u, it, hist, nb
+
+    res = run_ranks(nranks, rank)
+    monkeypatch.setenv("DDG_COARSE_REPLICATED", "1")
+    rep_ = run_ranks(nranks, rank)
+    s1 = Solver.from_problem(pr, coarse_variant=2)
+    full = s1.info.coarse_solve_bytes
+    zc1 = s1.coarse_correct(r)
+    s1.close()
+    for (zc, u, it, hist, nb), (zr, ur, itr, histr, nbr) in zip(res, rep_):
+        assert abs(it - ito) <= 1, (it, ito)
+        m = min(len(hist), len(histo))
+        assert np.max(np.abs(hist[:m] - histo[:m]) / histo[:m]) <= H_TOL
+        assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+        assert np.array_equal(zc, zr) and np.array_equal(u, ur) and np.array_equal(hist, histr)
+        assert np.linalg.norm(zc - zc1) <= 1e-13 * np.linalg.norm(zc1)
+        assert nbr == full and nb < full
