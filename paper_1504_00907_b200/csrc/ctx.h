@@ -113,6 +113,10 @@ struct ddg_ctx {
     int64_t local_bytes = 0, coarse_bytes = 0;
     double t_setup = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // multi-GPU (NCCL): the z halo of a colour's boundary subdomains runs on a side
+    // stream while the interior subdomains compute (colour_step)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // profiling (ddg_set_profiling)
     bool profiling = false;
     std::vector<cudaEvent_t> evpool;

@@ -171,6 +171,11 @@ struct ColourPlan {
     int32_t all_single;             // every operator of the colour is one item (gather may be fused)
     int32_t max_ntiles;             // largest item of the colour (tiles)
     int32_t ring_off;               // its k_symv_ring CTA partition in ctx::h_ring (-1: none)
+    // multi-GPU boundary-first split: ops [sub_begin, sub_mid) write
+    // z values another rank reads, [sub_mid, sub_end) do not; their items, reduction
+    // tasks and ring partitions ([*_begin, *_mid) / [*_mid, *_end)); sub_mid = sub_end: no split
+    int32_t sub_mid, item_mid, red_mid;
+    int32_t ring_b, ring_i;
 };
 
 // ---- kernel launchers (pcg.cu, symv.cu, coarse.cu, setup_kernels.cu) --------

@@ -154,6 +154,9 @@ static void free_ctx(ddg_ctx* c) {
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     delete c;
 }
 
@@ -507,9 +510,34 @@ static int build_plans(ddg_ctx* c) {
             // colours of small triangles (nT <= 5) run k_symv_whole on full tiles
             if (max_nt <= 5) compact = false;
         }
+        // this rank's subdomains of the colour; with several ranks, those whose
+        // writes another rank reads (the colour's z halo) first
+        std::vector<int> subs;
         while (pos < c->nparts && c->colour[c->order[pos]] == cc) {
-            const int i = c->order[pos];
-            if (c->dist && c->plan.part_rank[i] != c->rank) { ++pos; continue; }   // another rank's
+            const int i = c->order[pos++];
+            if (c->dist && c->plan.part_rank[i] != c->rank) continue;   // another rank's
+            subs.push_back(i);
+        }
+        int nbound = (int)subs.size();
+        if (c->dist && c->nranks > 1) {
+            std::vector<char> sent(c->n, 0);
+            for (int h = 0; h < c->nranks; ++h)
+                for (int32_t v : c->plan.z_send[(size_t)cc * c->nranks + h]) sent[v] = 1;
+            auto is_b = [&](int i) {
+                for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a)
+                    if (sent[c->oidx[a]]) return true;
+                return false;
+            };
+            auto mid = std::stable_partition(subs.begin(), subs.end(), is_b);
+            nbound = (int)(mid - subs.begin());
+        }
+        for (size_t qq = 0; qq < subs.size(); ++qq) {
+            if ((int)qq == nbound) {
+                pl.sub_mid = (int)c->ops.size();
+                pl.item_mid = (int)c->items.size();
+                pl.red_mid = (int)c->red.size();
+            }
+            const int i = subs[qq];
             const int64_t m = c->optr[i + 1] - c->optr[i];
             c->op_sub.push_back(i);
             const int64_t off = (int64_t)sorted_idx.size();
@@ -530,10 +558,14 @@ static int build_plans(ddg_ctx* c) {
                 add_op(c, (int32_t)m, 0, off, true, compact);
             }
             pl.max_rows = std::max<int>(pl.max_rows, (int)m);
-            ++pos;
         }
         pl.sub_end = (int)c->ops.size();
         pl.item_end = (int)c->items.size();
+        if (nbound >= (int)subs.size() || nbound == 0) {   // nothing to overlap
+            pl.sub_mid = pl.sub_end;
+            pl.item_mid = pl.item_end;
+            pl.red_mid = -1;
+        }
         pl.max_rows_t = 0;
         pl.all_single = 1;
         pl.max_ntiles = 0;
@@ -545,7 +577,13 @@ static int build_plans(ddg_ctx* c) {
             pl.max_ntiles = std::max(pl.max_ntiles, d.ntiles);
         }
         pl.red_end = (int)c->red.size();
+        if (pl.red_mid < 0) pl.red_mid = pl.red_end;
         pl.ring_off = ring_partition(c, pl.item_begin, pl.item_end);
+        pl.ring_b = pl.ring_i = -1;
+        if (pl.sub_mid < pl.sub_end) {
+            pl.ring_b = ring_partition(c, pl.item_begin, pl.item_mid);
+            pl.ring_i = ring_partition(c, pl.item_mid, pl.item_end);
+        }
     }
     c->oidx.swap(sorted_idx);  // now in sweep order; optr no longer valid for oidx
     c->colour_alg_bytes.assign(c->ncolours, 0.0);
@@ -1303,6 +1341,14 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     c->n_restrict = nparts;
     c->n_prolong = nparts;
     c->h_z.assign(c->ncolours, ddg::Halo{});
+    if (c->dist && c->nranks > 1 && !c->comm->loop && !getenv("DDG_NO_HALO_OVERLAP")) {
+        if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            free_ctx(c);
+            return set_err(DDG_E_CUDA, "side stream creation failed");
+        }
+    }
     if (c->dist && c->nranks > 1) {
         const ddg::DistPlan& P = c->plan;
         if ((st = upload(&c->d_rows, P.owned_rows)) || (st = upload(&c->d_restrict_parts, P.owned_subs)) ||
@@ -1406,12 +1452,26 @@ static void dist_finish(ddg_ctx* c, int slot) {
     c->launches += 1;
 }
 // send the values this rank wrote to the ranks that read them
-static void halo(ddg_ctx* c, ddg::Halo& h, double* v) {
+static void halo_on(ddg_ctx* c, ddg::Halo& h, double* v, cudaStream_t st) {
     if (!c->dist || c->nranks == 1) return;
-    launch_halo_pack(c->stream, v, h.d_sidx, h.d_sbuf, h.send_total);
-    comm_check(c, comm_exchange(c->comm, h, c->stream));
-    launch_halo_unpack(c->stream, h.d_rbuf, h.d_ridx, v, h.recv_total);
+    launch_halo_pack(st, v, h.d_sidx, h.d_sbuf, h.send_total);
+    comm_check(c, comm_exchange(c->comm, h, st));
+    launch_halo_unpack(st, h.d_rbuf, h.d_ridx, v, h.recv_total);
     c->launches += (h.send_total > 0) + (h.recv_total > 0);
+}
+static void halo(ddg_ctx* c, ddg::Halo& h, double* v) { halo_on(c, h, v, c->stream); }
+// boundary-first colour step: the z halo of the boundary
+// subdomains goes out on the side stream while the interior ones compute
+// (loopback ranks share one stream: in order there)
+static void halo_fork(ddg_ctx* c, ddg::Halo& h, double* v) {
+    if (!c->side) { halo(c, h, v); return; }
+    cudaEventRecord(c->ev_fork, c->stream);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    halo_on(c, h, v, c->side);
+    cudaEventRecord(c->ev_join, c->side);
+}
+static void halo_join(ddg_ctx* c) {
+    if (c->side) cudaStreamWaitEvent(c->stream, c->ev_join, 0);
 }
 
 static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_zero, const int32_t* done) {
@@ -1424,13 +1484,53 @@ static void colour_step(ddg_ctx* c, int cc, const double* r, double* z, bool z_z
                 launch_gather_flat(c->stream, lo.s_off, hi.s_off + hi.mp, c->d_gidx, c->A, r, z, c->d_s, z_zero,
                                    done);
             });
+            const int mp = (pl.max_rows + TILE - 1) / TILE * TILE;
             prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
-                launch_chol_solve(c->stream, c->d_ops, pl.sub_begin, pl.sub_end - pl.sub_begin,
-                                  (pl.max_rows + TILE - 1) / TILE * TILE, c->d_tiles, c->d_s, c->d_oidx, z, done);
+                launch_chol_solve(c->stream, c->d_ops, pl.sub_begin, pl.sub_mid - pl.sub_begin, mp, c->d_tiles,
+                                  c->d_s, c->d_oidx, z, done);
+                if (pl.sub_mid < pl.sub_end) {
+                    halo_fork(c, c->h_z[cc], z);
+                    launch_chol_solve(c->stream, c->d_ops, pl.sub_mid, pl.sub_end - pl.sub_mid, mp, c->d_tiles,
+                                      c->d_s, c->d_oidx, z, done);
+                    halo_join(c);
+                }
             });
-            c->launches += 2;
+            c->launches += 2 + (pl.sub_mid < pl.sub_end);
+            if (pl.sub_mid < pl.sub_end) return;
         }
         halo(c, c->h_z[cc], z);
+        return;
+    }
+    if (pl.sub_mid < pl.sub_end) {   // several ranks: boundary subdomains, halo out, interior ones
+        const OpDesc& lo = c->ops[pl.sub_begin];
+        const OpDesc& hi = c->ops[pl.sub_end - 1];
+        prof(c, PC_GATHER, 0, [&] {
+            launch_gather_flat(c->stream, lo.s_off, hi.s_off + hi.mp, c->d_gidx, c->A, r, z, c->d_s, z_zero, done);
+        });
+        c->launches += 1;
+        auto run = [&](int ib, int ie, int rb, int re, int roff) {
+            if (ie <= ib) return;
+            if (ring_ok(c, roff)) {
+                int mr, mc;
+                ring_dims(c, roff, &mr, &mc);
+                launch_symv_ring(c->stream, c->d_ops, c->d_items, ib, c->d_ring + roff, num_sms(), mr, mc,
+                                 c->d_tiles, c->d_s, c->d_oidx, z, nullptr, c->d_partials, done, pl.all_single != 0);
+                if (re > rb)
+                    launch_symv_reduce(c->stream, c->d_ops, c->d_items, c->d_red, rb, re - rb, c->d_oidx,
+                                       c->d_partials, z, nullptr, done);
+                c->launches += 1 + (re > rb);
+            } else {
+                launch_symv(c->stream, c->d_ops, c->d_items, ib, ie - ib, c->d_tiles, c->d_s, c->d_oidx, z, nullptr,
+                            c->d_partials, done, pl.max_rows_t, c->d_tickets);
+                c->launches += 1;
+            }
+        };
+        prof(c, PC_SYMV, c->colour_alg_bytes[cc], [&] {
+            run(pl.item_begin, pl.item_mid, pl.red_begin, pl.red_mid, pl.ring_b);
+            halo_fork(c, c->h_z[cc], z);
+            run(pl.item_mid, pl.item_end, pl.red_mid, pl.red_end, pl.ring_i);
+            halo_join(c);
+        });
         return;
     }
     int gmode = 0;
