@@ -559,8 +559,17 @@ __global__ void k_front_reduce(const FRedTask* __restrict__ tasks, int t0,
     const FRedTask t = tasks[t0 + blockIdx.x];
     const FrontDesc f = fronts[t.front];
     for (int r = threadIdx.x; r < t.nrows; r += blockDim.x) {
+        // df_reduce's combine order (k_coarse_dataflow), so the level-by-level and the
+        // distributed top-front steps give the dataflow solve's values bitwise
         double s = 0.0;
-        for (int c = t.cbeg; c < t.cend; ++c) s += partials[contrib[c] + r];
+        int c = t.cbeg;
+        for (; c + 8 <= t.cend; c += 8) {
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = partials[contrib[c + k] + r];
+            s += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+        }
+        for (; c < t.cend; ++c) s += partials[contrib[c] + r];
         const int row = t.row0 + r;
         if (t.kind == 0) {
             const int b = row - f.nSp;
@@ -654,19 +663,9 @@ __global__ void k_gather_masked(int64_t n, const int32_t* __restrict__ idx, cons
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
         dst[k] = mask[k] ? src[idx ? idx[k] : k] : 0.0;
 }
-// next dataflow phase: queue head back to 0, the children counters of the
-// replicated top fronts preset to their children solved by the ranks
-__global__ void k_df_preset(int n, const int32_t* __restrict__ slot, const int32_t* __restrict__ val,
-                            int32_t* __restrict__ state) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) state[slot[k]] = val[k];
-    if (blockIdx.x == 0 && threadIdx.x == 0) state[0] = 0;
-}
 void launch_gather_masked(cudaStream_t st, int64_t n, const int32_t* idx, const uint8_t* mask, const double* src,
                           double* dst) {
     if (n > 0) k_gather_masked<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, idx, mask, src, dst);
-}
-void launch_df_preset(cudaStream_t st, int n, const int32_t* slot, const int32_t* val, int32_t* state) {
-    k_df_preset<<<std::max(1, std::min((n + 255) / 256, 64)), 256, 0, st>>>(n, slot, val, state);
 }
 
 void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,

@@ -79,14 +79,20 @@ struct SparseCoarse {
     // distributed solve (sparse_coarse_dist_setup): the top fronts replicated,
     // every subtree below them solved by one rank
     bool dist = false;
-    int nw1 = 0, nw2 = 0, nw3 = 0, npreset = 0;
+    int nw1 = 0, nw3 = 0;
     int64_t nwx = 0, rank_solve_bytes = 0;
-    int32_t *d_work1 = nullptr, *d_work2 = nullptr, *d_work3 = nullptr;
-    int32_t *d_preset_slot = nullptr, *d_preset_val = nullptr, *d_wx_idx = nullptr;
+    int32_t *d_work1 = nullptr, *d_work3 = nullptr, *d_wx_idx = nullptr;
     uint8_t *d_wx_mask = nullptr, *d_y_mask = nullptr;
     FrontDesc* d_fr1 = nullptr;
     double *d_wx_buf = nullptr, *d_y_buf = nullptr;
     int ntop = 0, nsub = 0;
+    // the top fronts' work split over the ranks (phase 2):
+    // per front its G and H item ranges and reduction tasks; a rank computes its
+    // share of every range, the partial segments are allreduced, the reductions
+    // run everywhere
+    struct Top { int f, depth, g0, g1, h0, h1, ft0, ft1, bt0, bt1; };
+    std::vector<Top> tops;          // deepest first
+    std::vector<int> own_roots;     // this rank's subtree roots
 };
 
 int64_t sparse_coarse_solve_bytes(ddg_ctx* c);
@@ -95,7 +101,7 @@ void sparse_coarse_free(SparseCoarse* s) {
     if (!s) return;
     void* p[] = {s->d_fr, s->d_fchild, s->d_fS, s->d_fB, s->d_fmap, s->d_item_front, s->d_fwd, s->d_bwd,
                  s->d_contrib, s->d_fvec, s->d_w, s->d_ctiles, s->d_bc, s->d_dfwork, s->d_dfstate, s->d_fdf,
-                 s->d_trace, s->d_work1, s->d_work2, s->d_work3, s->d_preset_slot, s->d_preset_val,
+                 s->d_trace, s->d_work1, s->d_work3,
                  s->d_wx_idx, s->d_wx_mask, s->d_y_mask, s->d_fr1, s->d_wx_buf, s->d_y_buf};
     for (void* x : p)
         if (x) cudaFree(x);
@@ -661,15 +667,19 @@ static int up_s(cudaStream_t s, T** d, const std::vector<T>& h) {
 //            the subtree roots stop there, as if they were roots)
 //   exchange the subtree roots' contributions w_t to their top ancestors:
 //            one allreduce of their concatenation (zeros from non-owners)
-//   phase 2  forward + backward over the top fronts (replicated); their
-//            children counters preset to the subtrees already eliminated
+//   phase 2  forward + backward over the top fronts, front by front, each
+//            front's G and H item ranges split over the ranks: a rank zeroes
+//            the range's partial segments, computes its share (k_symv), the
+//            segments are allreduced, the front's reductions run everywhere
 //   phase 3  backward substitution over this rank's subtrees
 //   y_c      one allreduce: each unknown contributed by exactly one rank (a
 //            subtree's owner, rank 0 for the top), so every rank holds the
 //            same y_c bitwise.
-// The factor stays replicated in memory (the top fronts need every subtree's
-// Schur complement at setup); each rank READS only the top fronts and its
-// own subtrees per solve, which is what bounds the coarse step's time.
+// Every partial segment and every y_c entry is computed by exactly one rank
+// and the allreduces only add zeros, so the result equals the replicated
+// solve bitwise.  The factor stays replicated in memory (the top fronts need
+// every subtree's Schur complement at setup); each rank READS its subtrees and
+// 1/P of the top fronts per solve, which is what bounds the coarse step.
 struct DistSplit {
     std::vector<char> top, sroot;
     std::vector<int> owner, roots;
@@ -741,23 +751,10 @@ static int sparse_coarse_dist_setup(ddg_ctx* c) {
         if (e & DF_RED) return (e & DF_BWD) ? sc->bwd[idx].front : sc->fwd[idx].front;
         return (int)sc->item_front[idx - sc->item_base];
     };
-    std::vector<int32_t> w1, w2, w3;
-    std::vector<int32_t> pslot, pval;
-    for (int i = 0; i < nn; ++i) {
-        if (!top[i] || sc->fr[i].nchild == 0) continue;
-        int nsubch = 0;
-        for (int k = 0; k < sc->fr[i].nchild; ++k) nsubch += !top[sc->fchild[sc->fr[i].child_off + k]];
-        if (nsubch == sc->fr[i].nchild) {
-            w2.push_back(DF_ASSEMBLE | i);                   // all children eliminated by the ranks
-        } else if (nsubch > 0) {
-            pslot.push_back(1 + DF_STATE_PER_FRONT * i + 3);   // DFF_CHILDREN (coarse.cu)
-            pval.push_back(nsubch);
-        }
-    }
+    std::vector<int32_t> w1, w3;
     for (int32_t e : sc->dfwork) {
         const int f = entry_front(e);
-        if (top[f]) w2.push_back(e);
-        else if (mine(f)) (e & DF_BWD ? w3 : w1).push_back(e);
+        if (mine(f)) (e & DF_BWD ? w3 : w1).push_back(e);
     }
     // phase-1 fronts: subtree roots end the forward elimination like roots
     std::vector<FrontDesc> fr1 = sc->fr;
@@ -778,23 +775,48 @@ static int sparse_coarse_dist_setup(ddg_ctx* c) {
         for (int a = 0; a < sc->fr[i].nS; ++a) ym[sc->fS[sc->fr[i].S_off + a]] = 1;
     }
     int st;
-    if ((st = up(&sc->d_work1, w1)) || (st = up(&sc->d_work2, w2)) || (st = up(&sc->d_work3, w3)) ||
+    if ((st = up(&sc->d_work1, w1)) || (st = up(&sc->d_work3, w3)) ||
         (st = up(&sc->d_fr1, fr1)) || (st = up(&sc->d_wx_idx, wx)) || (st = up(&sc->d_wx_mask, wm)) ||
         (st = dalloc(&sc->d_wx_buf, std::max<size_t>(1, wx.size()))) || (st = up(&sc->d_y_mask, ym)) ||
         (st = dalloc(&sc->d_y_buf, std::max<int64_t>(1, c->nc))))
         return st;
-    if (!pslot.empty() && ((st = up(&sc->d_preset_slot, pslot)) || (st = up(&sc->d_preset_val, pval)))) return st;
     sc->nw1 = (int)w1.size();
-    sc->nw2 = (int)w2.size();
     sc->nw3 = (int)w3.size();
-    sc->npreset = (int)pslot.size();
     sc->nwx = (int64_t)wx.size();
     sc->ntop = 0;
     for (int i = 0; i < nn; ++i) sc->ntop += top[i];
     sc->nsub = (int)roots.size();
-    double rb = 0;
-    for (int i = 0; i < nn; ++i)
-        if (top[i] || owner[i] == me) rb += fbytes[i];
+    // top fronts: item ranges per front (a front's G items, and its H items, are
+    // contiguous in c->items, and so are their partial segments)
+    sc->tops.clear();
+    sc->own_roots.clear();
+    for (int r : roots)
+        if (owner[r] == me) sc->own_roots.push_back(r);
+    {
+        std::vector<int> dep(nn, 0);
+        for (int i = nn - 1; i >= 0; --i) dep[i] = sc->fr[i].parent < 0 ? 0 : dep[sc->fr[i].parent] + 1;
+        std::vector<int> g0(nn, INT32_MAX), g1(nn, -1), h0(nn, INT32_MAX), h1(nn, -1);
+        for (int h = 0; h < sc->nlevels; ++h)
+            for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q) {
+                const int f = sc->item_front[q - sc->item_base];
+                if (q < sc->g_end[h]) { g0[f] = std::min(g0[f], q); g1[f] = std::max(g1[f], q + 1); }
+                else { h0[f] = std::min(h0[f], q); h1[f] = std::max(h1[f], q + 1); }
+            }
+        for (int i = 0; i < nn; ++i) {
+            if (!top[i]) continue;
+            SparseCoarse::Top t{i, dep[i], g1[i] < 0 ? 0 : g0[i], g1[i] < 0 ? 0 : g1[i], h1[i] < 0 ? 0 : h0[i],
+                                h1[i] < 0 ? 0 : h1[i], sc->fdf[i].ft0, sc->fdf[i].ft1, sc->fdf[i].bt0, sc->fdf[i].bt1};
+            sc->tops.push_back(t);
+        }
+        std::stable_sort(sc->tops.begin(), sc->tops.end(),
+                         [](const SparseCoarse::Top& a, const SparseCoarse::Top& b) { return a.depth > b.depth; });
+    }
+    double rb = 0, tb = 0;
+    for (int i = 0; i < nn; ++i) {
+        if (top[i]) tb += fbytes[i];
+        else if (owner[i] == me) rb += fbytes[i];
+    }
+    rb += tb / P;    // the top fronts' item ranges are split evenly by item count
     sc->rank_solve_bytes = (int64_t)rb;
     sc->dist = true;
     if (c->opts.verbose)
@@ -1011,14 +1033,52 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
         launch_gather_masked(c->stream, sc->nwx, sc->d_wx_idx, sc->d_wx_mask, sc->d_w, sc->d_wx_buf);
         err |= ddg::comm_allreduce_sum(c->comm, sc->d_wx_buf, sc->d_wx_buf, (size_t)sc->nwx, c->stream);
         launch_halo_unpack(c->stream, sc->d_wx_buf, sc->d_wx_idx, sc->d_w, sc->nwx);
-        launch_df_preset(c->stream, sc->npreset, sc->d_preset_slot, sc->d_preset_val, sc->d_dfstate);
-        df(sc->nw2, sc->d_work2, sc->d_fr);                                        // phase 2: top fronts
+        {
+            // phase 2, the top fronts' items split over the ranks: per item range
+            // zero its partial segments, compute this rank's share, allreduce
+            const int P = c->nranks, me = c->rank;
+            auto sym_range = [&](int q0, int q1) {
+                if (q1 <= q0) return;
+                const ItemDesc& a = c->items[q0];
+                const ItemDesc& b = c->items[q1 - 1];
+                const int64_t lo = a.part_off;
+                const int64_t hi = b.part_off + (int64_t)(b.I1 - b.I0 + (b.tri ? 0 : b.J1 - b.J0)) * TILE;
+                cudaMemsetAsync(c->d_partials + lo, 0, (size_t)(hi - lo) * sizeof(double), c->stream);
+                const int64_t len = q1 - q0;
+                const int m0 = q0 + (int)(len * me / P), m1 = q0 + (int)(len * (me + 1) / P);
+                if (m1 > m0)
+                    launch_symv(c->stream, c->d_ops, c->d_items, m0, m1 - m0, sc->d_ctiles, sc->d_fvec, nullptr,
+                                nullptr, nullptr, c->d_partials, done, sc->max_rows_t, c->d_tickets);
+                err |= ddg::comm_allreduce_sum(c->comm, c->d_partials + lo, c->d_partials + lo, (size_t)(hi - lo),
+                                               c->stream);
+                launches += 2;
+            };
+            for (const auto& t : sc->tops) {                                       // forward, deepest first
+                launch_front_fwd_assemble(c->stream, t.f, 1, sc->d_fr, sc->d_fchild, sc->d_fS, sc->d_fmap, sc->d_bc,
+                                          sc->d_fvec, sc->d_w, done);
+                sym_range(t.g0, t.g1);
+                launch_front_reduce(c->stream, sc->d_fwd, t.ft0, t.ft1 - t.ft0, sc->d_contrib, sc->d_fr, sc->d_fS,
+                                    c->d_partials, sc->d_w, d_x, done);
+                launches += 2;
+            }
+            for (auto it = sc->tops.rbegin(); it != sc->tops.rend(); ++it) {        // backward, root first
+                launch_front_bwd_gather(c->stream, it->f, 1, sc->d_fr, sc->d_fB, d_x, sc->d_fvec, done);
+                sym_range(it->g0, it->g1);
+                sym_range(it->h0, it->h1);
+                launch_front_reduce(c->stream, sc->d_bwd, it->bt0, it->bt1 - it->bt0, sc->d_contrib, sc->d_fr,
+                                    sc->d_fS, c->d_partials, sc->d_w, d_x, done);
+                launches += 2;
+            }
+            for (int r : sc->own_roots)                                            // x[B] of the subtree roots
+                launch_front_bwd_gather(c->stream, r, 1, sc->d_fr, sc->d_fB, d_x, sc->d_fvec, done);
+            launches += (int)sc->own_roots.size();
+        }
         cudaMemsetAsync(sc->d_dfstate, 0, sizeof(int32_t), c->stream);
         df(sc->nw3, sc->d_work3, sc->d_fr);                                        // phase 3: own subtrees, back
         launch_gather_masked(c->stream, c->nc, nullptr, sc->d_y_mask, d_x, sc->d_y_buf);
         err |= ddg::comm_allreduce_sum(c->comm, sc->d_y_buf, d_x, (size_t)c->nc, c->stream);
         if (err && !c->comm_err) c->comm_err = err;
-        return 8;
+        return launches + 8;
     }
     if (sc->dataflow) {
         cudaMemsetAsync(sc->d_dfstate, 0, (1 + (size_t)DF_STATE_PER_FRONT * sc->nfront) * sizeof(int32_t),
@@ -1069,8 +1129,9 @@ int sparse_coarse_enqueue_solve(ddg_ctx* c, double* d_x, const int32_t* done) {
 
 // debug (not part of include/ddg.h): the distributed coarse solve's split for
 // P ranks on this context's tree (the plan sparse_coarse_dist_setup makes):
-// coarse solve bytes read per rank (top fronts + its subtrees) into
-// bytes[0 .. P), the top fronts' share into *top; returns the number of
+// coarse solve bytes of each rank's own subtrees into bytes[0 .. P), the
+// top fronts' total into *top (read by every rank when replicated, 1/P of it
+// per rank when split, the default); returns the number of
 // subtrees (0: the whole tree lies above the cut), -1 without a sparse coarse
 extern "C" int ddg_debug_coarse_split(ddg_ctx* c, int P, double* bytes, double* top) {
     if (!c || !c->sparse || P < 1) return -1;
@@ -1082,7 +1143,6 @@ extern "C" int ddg_debug_coarse_split(ddg_ctx* c, int P, double* bytes, double* 
         if (ds.top[i]) tb += ds.fbytes[i];
         else bytes[ds.owner[i]] += ds.fbytes[i];
     }
-    for (int p = 0; p < P; ++p) bytes[p] += tb;
     *top = tb;
     return (int)ds.roots.size();
 }

@@ -327,7 +327,6 @@ void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* f
                              const int32_t* fB, const double* x, double* fvec, const int32_t* done);
 void launch_gather_masked(cudaStream_t st, int64_t n, const int32_t* idx, const uint8_t* mask, const double* src,
                           double* dst);
-void launch_df_preset(cudaStream_t st, int n, const int32_t* slot, const int32_t* val, int32_t* state);
 void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,
                          const FrontDesc* fronts, const int32_t* fS, const double* partials, double* w,
                          double* x, const int32_t* done);

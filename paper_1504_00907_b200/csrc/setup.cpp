@@ -519,7 +519,8 @@ static int build_plans(ddg_ctx* c) {
             subs.push_back(i);
         }
         int nbound = (int)subs.size();
-        if (c->dist && c->nranks > 1) {
+        static const bool no_split = getenv("DDG_NO_BOUNDARY_FIRST") && atoi(getenv("DDG_NO_BOUNDARY_FIRST")) != 0;
+        if (c->dist && c->nranks > 1 && !no_split) {
             std::vector<char> sent(c->n, 0);
             for (int h = 0; h < c->nranks; ++h)
                 for (int32_t v : c->plan.z_send[(size_t)cc * c->nranks + h]) sent[v] = 1;

@@ -160,7 +160,9 @@ def test_loopback_distributed_coarse_solve(name, nranks, monkeypatch):
     the subtree roots' contributions, the top fronts, backward), y_c assembled
     by one allreduce.  Against the oracle (north-star bar), bitwise equal to
     the replicated solve (DDG_COARSE_REPLICATED=1: every rank the whole tree),
-    and each rank reads fewer coarse bytes per solve."""
+    and each rank reads fewer coarse bytes per solve.  The top fronts' items are
+    split over the ranks too (their partial segments allreduced, the reductions
+    run by every rank)."""
     from paper_1504_00907_b200 import Solver
     monkeypatch.setenv("DDG_ND_LEAF", "64")       # a deep tree on a test-sized A_c
     pr = CASES[name]()
