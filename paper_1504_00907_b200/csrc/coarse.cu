@@ -252,22 +252,56 @@ __device__ __forceinline__ int32_t* df_flag(const DFCtx& d, int t, int k) {
 }
 
 // front vector and w of front t from b_c and its children's w (children in order)
+// The index loads of one CTA over a front of up to ~25k rows are a chain of
+// dependent global round trips per element (index, then value): each thread
+// keeps DF_U independent elements in flight (measured: a 24k-row assembly took
+// ~150 us one element at a time, on the coarse solve's critical path).
+constexpr int DF_U = 8;
+__device__ void df_gather_idx(double* __restrict__ out, int n, int ntot, const int32_t* __restrict__ idx,
+                              const double* __restrict__ src, bool cg) {
+    for (int a0 = threadIdx.x; a0 < ntot; a0 += blockDim.x * DF_U) {
+        int ix[DF_U];
+#pragma unroll
+        for (int u = 0; u < DF_U; ++u) {
+            const int a = a0 + u * blockDim.x;
+            ix[u] = a < n ? idx[a] : -1;
+        }
+        double v[DF_U];
+#pragma unroll
+        for (int u = 0; u < DF_U; ++u) v[u] = ix[u] >= 0 ? (cg ? __ldcg(src + ix[u]) : src[ix[u]]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < DF_U; ++u) {
+            const int a = a0 + u * blockDim.x;
+            if (a < ntot) out[a] = v[u];
+        }
+    }
+}
 __device__ void df_assemble(const DFCtx& d, int t) {
     const FrontDesc f = d.fronts[t];
     double* fv = d.fvec + f.fvec_off;
     double* wt = d.w + f.w_off;
     const int ntot = f.nT * TILE;
-    for (int a = threadIdx.x; a < ntot; a += blockDim.x) fv[a] = a < f.nS ? d.bc[d.fS[f.S_off + a]] : 0.0;
+    df_gather_idx(fv, f.nS, ntot, d.fS + f.S_off, d.bc, false);
     for (int a = threadIdx.x; a < f.nB; a += blockDim.x) wt[a] = 0.0;
     __syncthreads();
     for (int k = 0; k < f.nchild; ++k) {                      // children in fixed order
         const int ci = d.fchild[f.child_off + k];
         const FrontDesc c = d.fronts[ci];
-        for (int j = threadIdx.x; j < c.nB; j += blockDim.x) {
-            const int pos = d.map[c.map_off + j];
-            const double v = __ldcg(d.w + c.w_off + j);
-            if (pos < f.nSp) fv[pos] += v;
-            else wt[pos - f.nSp] += v;
+        for (int j0 = threadIdx.x; j0 < c.nB; j0 += blockDim.x * DF_U) {
+            int pos[DF_U];
+            double v[DF_U];
+#pragma unroll
+            for (int u = 0; u < DF_U; ++u) {
+                const int j = j0 + u * blockDim.x;
+                pos[u] = j < c.nB ? d.map[c.map_off + j] : -1;
+                v[u] = j < c.nB ? __ldcg(d.w + c.w_off + j) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < DF_U; ++u) {   // positions are distinct within a child
+                if (pos[u] < 0) continue;
+                if (pos[u] < f.nSp) fv[pos[u]] += v[u];
+                else wt[pos[u] - f.nSp] += v[u];
+            }
         }
         __syncthreads();
     }
@@ -464,9 +498,7 @@ k_coarse_dataflow(int nwork, const int32_t* __restrict__ work, DFCtx d, const in
                     const int ci = d.fchild[f.child_off + k];
                     const FrontDesc c = d.fronts[ci];
                     double* fv = d.fvec + c.fvec_off + c.nSp;
-                    const int nBp = c.nT * TILE - c.nSp;
-                    for (int a = threadIdx.x; a < nBp; a += blockDim.x)
-                        fv[a] = a < c.nB ? __ldcg(d.x + d.fB[c.B_off + a]) : 0.0;
+                    df_gather_idx(fv, c.nB, c.nT * TILE - c.nSp, d.fB + c.B_off, d.x, true);
                     __threadfence();
                     __syncthreads();
                     if (threadIdx.x == 0) st_release(df_flag(d, ci, DFB_READY), 1);
@@ -524,7 +556,7 @@ __global__ void k_front_fwd_assemble(int f0, const FrontDesc* __restrict__ front
     double* fv = fvec + f.fvec_off;
     double* wt = w + f.w_off;
     const int ntot = f.nT * TILE;
-    for (int a = threadIdx.x; a < ntot; a += blockDim.x) fv[a] = a < f.nS ? bc[fS[f.S_off + a]] : 0.0;
+    df_gather_idx(fv, f.nS, ntot, fS + f.S_off, bc, false);
     for (int a = threadIdx.x; a < f.nB; a += blockDim.x) wt[a] = 0.0;
     __syncthreads();
     for (int s = 0; s < f.nchild; ++s) {
@@ -547,8 +579,7 @@ __global__ void k_front_bwd_gather(int f0, const FrontDesc* __restrict__ fronts,
     if (*done) return;
     const FrontDesc f = fronts[f0 + blockIdx.x];
     double* fv = fvec + f.fvec_off + f.nSp;
-    const int nBp = f.nT * TILE - f.nSp;
-    for (int a = threadIdx.x; a < nBp; a += blockDim.x) fv[a] = a < f.nB ? x[fB[f.B_off + a]] : 0.0;
+    df_gather_idx(fv, f.nB, f.nT * TILE - f.nSp, fB + f.B_off, x, false);
 }
 
 __global__ void k_front_reduce(const FRedTask* __restrict__ tasks, int t0,

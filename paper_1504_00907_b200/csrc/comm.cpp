@@ -171,6 +171,7 @@ extern "C" int ddg_loop_group_create(int nranks, int device, ddg_loop_group** ou
         delete g;
         return set_err(DDG_E_CUDA, "loop group stream");
     }
+    ddg::register_no_pdl_stream(g->stream);
     *out = g;
     return DDG_OK;
 }

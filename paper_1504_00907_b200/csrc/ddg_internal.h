@@ -178,6 +178,9 @@ struct ColourPlan {
     int32_t ring_b, ring_i;
 };
 
+// streams on which chain kernels launch without programmatic dependent launch
+// (the loopback group's stream, shared by several host threads; symv.cu)
+void register_no_pdl_stream(cudaStream_t st);
 // ---- kernel launchers (pcg.cu, symv.cu, coarse.cu, setup_kernels.cu) --------
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,

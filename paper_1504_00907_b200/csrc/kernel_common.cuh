@@ -331,6 +331,9 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 extern int g_pdl;   // 1: chain launches carry the programmatic-serialization attribute (DDG_PDL)
+// streams shared by several host threads (the loopback group's stream): launched
+// without the attribute (comm.cpp registers them)
+bool no_pdl_stream(cudaStream_t st);
 template <typename... KArgs, typename... Args>
 static inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args... args) {
@@ -341,7 +344,7 @@ static inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = g_pdl;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl && !no_pdl_stream(st);
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k, args...);

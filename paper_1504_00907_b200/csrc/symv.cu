@@ -2,10 +2,30 @@
 // (part of libddg's sm_100a kernels; shared device helpers in kernel_common.cuh)
 #include <cstring>
 
+#include <atomic>
+#include <mutex>
+
 #include "kernel_common.cuh"
 
 namespace ddg {
 int g_pdl = 1;
+static cudaStream_t g_nopdl[64];
+static std::atomic<int> g_nnopdl{0};
+bool no_pdl_stream(cudaStream_t st) {
+    const int n = g_nnopdl.load(std::memory_order_acquire);
+    for (int i = 0; i < n; ++i)
+        if (g_nopdl[i] == st) return true;
+    return false;
+}
+void register_no_pdl_stream(cudaStream_t st) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    const int n = g_nnopdl.load();
+    if (n < 64) {
+        g_nopdl[n] = st;
+        g_nnopdl.store(n + 1, std::memory_order_release);
+    }
+}
 // =============================================================================
 // Multiplicative Schwarz colour step
 // =============================================================================

@@ -46,7 +46,20 @@ for k, nm in enumerate(["assemble", "fwd item", "bwd item", "fwd red", "bwd red"
 # busy fraction over time
 busy = np.sum(np.where(t[2] > 0, t[2] - np.maximum(t[1], t[0]), 0))
 print(f"  item-busy CTA-time {busy/1e3:.0f} us of {nct*end/1e3:.0f} us CTA-time ({busy/(nct*end):.1%})")
-# per forward/backward level: first start, last item done
-lvl = {}
-
+# occupancy timeline: CTAs busy on items / reductions per 100 us bucket
+B = 100_000
+nb = int(end // B) + 1
+occ_item = np.zeros(nb)
+occ_red = np.zeros(nb)
+for k in range(n):
+    a, b = max(t[1][k], t[0][k]), t[2][k]
+    if b <= 0:
+        continue
+    tgt = occ_red if kind[k] >= 3 else occ_item
+    for q in range(int(a // B), int(b // B) + 1):
+        lo, hi = max(a, q * B), min(b, (q + 1) * B)
+        if hi > lo:
+            tgt[q] += (hi - lo) / B
+print("  busy CTAs per 100 us (items + reductions, of %d):" % nct)
+print("  " + " ".join("%d" % (occ_item[q] + occ_red[q]) for q in range(nb)))
 s.close()

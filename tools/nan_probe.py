@@ -18,6 +18,11 @@ nr = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 pr = {"biharm": lambda: P.biharmonic2d(128, 16, 3, 1005), "lognormal": lambda: P.lognormal3d(32, 4, 1, 1003),
       "poisson": lambda: P.poisson3d(32, 8, 2, 1002)}[cfg]()
 r = np.random.default_rng(4).standard_normal(pr.n)
+if os.environ.get("SINGLE_FIRST"):          # a single-GPU context first, as the parity test does
+    s1 = Solver.from_problem(pr)
+    z1 = s1.apply_precond(r)
+    print("single", int(np.isnan(z1).sum()), flush=True)
+    s1.close()
 g = LoopGroup(nr)
 out = [None] * nr
 
@@ -25,7 +30,9 @@ out = [None] * nr
 def body(k):
     s = Solver.from_problem(pr, comm=g.comm(k))
     res = {}
-    for nm, fn in (("spmv", s.spmv), ("coarse", s.coarse_correct), ("precond", s.apply_precond)):
+    steps = (("precond", s.apply_precond),) if os.environ.get("PRECOND_ONLY") else (
+        ("spmv", s.spmv), ("coarse", s.coarse_correct), ("precond", s.apply_precond))
+    for nm, fn in steps:
         v = fn(r)
         res[nm] = (int(np.isnan(v).sum()), np.nonzero(np.isnan(v))[0][:8].tolist())
     u, it, hist, rep = s.solve(pr.f, 1e-8)
