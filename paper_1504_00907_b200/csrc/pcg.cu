@@ -403,6 +403,11 @@ __global__ void __launch_bounds__(256) k_pcg_small(SmallArgs a) {
     }
     __syncthreads();
     // ---- load the resident data once ----
+    // b_c and y_c: the restriction writes only the n_c real entries, while the
+    // coarse tile products read whole tiles, so the padding must hold zeros (not
+    // stale shared memory: 0 * NaN is NaN); zeroed before the first cluster
+    // barrier, i.e. before any CTA stores into another's copy
+    for (int x = tid; x < 2 * a.ncp; x += blockDim.x) bcv[x] = 0.0;
     for (int e = 0; e < own_col[a.ncolours]; ++e) {
         const ItemDesc& it = own[e].it;
         const OpDesc op = a.ops[it.op];
