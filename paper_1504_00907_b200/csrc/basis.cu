@@ -221,8 +221,7 @@ void launch_galerkin_blocks(cudaStream_t st, int nblocks, int maxk, const int32_
                             const int32_t* rp, const int32_t* col, const double* val, double* out) {
     if (nblocks <= 0) return;
     const size_t smem = (size_t)GAL_RB * 2 * maxk * sizeof(double);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_galerkin_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) DDG_MAX_DYN_SMEM(k_galerkin_blocks);
     for (int b0 = 0; b0 < nblocks; b0 += 1 << 30)
         k_galerkin_blocks<<<std::min(nblocks - b0, 1 << 30), GAL_THREADS, smem, st>>>(
             bI + b0, bJ + b0, boff + b0, bptr, bidx, cptr, qoff, Q, part, bpos, rp, col, val, out);

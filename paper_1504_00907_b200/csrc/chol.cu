@@ -285,11 +285,9 @@ void launch_chol_solve(cudaStream_t st, const OpDesc* ops, int op_begin, int nop
     const bool staged = maxT <= CHOL_STAGE_T && !getenv("DDG_CHOL_GLOBAL");
     const size_t smem = (size_t)(max_mp + CHOL_WARPS * TILE) * sizeof(double) +
                         (staged ? (size_t)maxT * (maxT + 1) / 2 * TILE_ELEMS * sizeof(double) : 0);
-    static size_t set[2] = {0, 0};
-    if (smem > 48 * 1024 && smem > set[staged]) {
-        if (staged) cudaFuncSetAttribute(k_chol_solve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        else cudaFuncSetAttribute(k_chol_solve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        set[staged] = smem;
+    if (smem > 48 * 1024) {
+        if (staged) DDG_MAX_DYN_SMEM(k_chol_solve<true>);
+        else DDG_MAX_DYN_SMEM(k_chol_solve<false>);
     }
     if (staged) launch_pdl(k_chol_solve<true>, nops, CHOL_WARPS * 32, smem, st, ops, op_begin, fac, s, oidx, z, done);
     else launch_pdl(k_chol_solve<false>, nops, CHOL_WARPS * 32, smem, st, ops, op_begin, fac, s, oidx, z, done);

@@ -632,8 +632,7 @@ void launch_coarse_restrict(cudaStream_t st, int nparts, const int64_t* bptr, co
         return;
     }
     const size_t smem = (size_t)maxmI * sizeof(double);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_coarse_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) DDG_MAX_DYN_SMEM(k_coarse_restrict);
     k_coarse_restrict<<<nparts, 256, smem, st>>>(bptr, bidx, cptr, qoff, Q, A, r, z, bc, done, parts);
 }
 

@@ -350,6 +350,27 @@ static inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
     cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+// Raise a kernel's dynamic shared-memory limit to the device maximum once per
+// device.  Setting it to each launch's own size races when several host
+// threads launch the same kernel with different sizes (the loopback ranks):
+// one thread's smaller value lands between another's set and launch, and that
+// launch fails with an invalid argument.  A single maximal value cannot race.
+#define DDG_MAX_DYN_SMEM(kern)                                                                        \
+    do {                                                                                              \
+        static bool done_[64] = {};                                                                   \
+        int d_ = 0;                                                                                   \
+        cudaGetDevice(&d_);                                                                           \
+        if (!done_[d_ & 63]) {                                                                        \
+            cudaFuncAttributes fa_{};                                                                 \
+            cudaFuncGetAttributes(&fa_, (const void*)(kern));                                         \
+            int optin_ = 0;                                                                           \
+            cudaDeviceGetAttribute(&optin_, cudaDevAttrMaxSharedMemoryPerBlockOptin, d_);             \
+            cudaFuncSetAttribute((const void*)(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                 optin_ - (int)fa_.sharedSizeBytes);                                  \
+            done_[d_ & 63] = true;                                                                    \
+        }                                                                                             \
+    } while (0)
+
 static inline int vec_grid(int64_t n) {
     int64_t g = (n + VEC_THREADS - 1) / VEC_THREADS;
     return (int)(g < RED_BLOCKS ? (g > 0 ? g : 1) : RED_BLOCKS);

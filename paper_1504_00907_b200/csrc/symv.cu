@@ -1282,7 +1282,7 @@ void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int 
         return;
     }
     const size_t smem = symv_smem(max_rows_t);
-    cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    DDG_MAX_DYN_SMEM(k_symv);
     k_symv<<<nitems, SYMV_WARPS * 32, smem, st>>>(ops, items, item_begin, tiles, s, oidx, z, y_out,
                                                   partials, done, tickets, gather_mode, A, r);
 }
