@@ -1988,6 +1988,7 @@ solved:
     CUDA_TRY(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(cudaEventSynchronize(c->ev1));
+    CUDA_TRY(cudaGetLastError());   // a launch that failed (bad configuration) must not pass silently
     if (c->comm_err) return set_err(DDG_E_NCCL, "NCCL failure inside the solve");
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);

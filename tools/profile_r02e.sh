@@ -17,3 +17,6 @@ for c in C3 C5 C2 C4; do
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 30000 --csv --log-file gpurun_out/launches_${T}_C3.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_${T}.log 2>&1
 echo done
+if [ -n "$RING2_CAPTURE" ]; then
+  timeout 600 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:k_symv_ring2 --launch-skip 5 -c 1 -o gpurun_out/ring2_full_C5_${T} -f python tools/prof_solve.py C5 > gpurun_out/ncu_ring2_${T}.log 2>&1
+fi
