@@ -31,10 +31,10 @@
 
 namespace {
 
-int LEAF_UNKNOWNS = 256;   // nested dissection stops below this many unknowns (DDG_ND_LEAF)
-int MERGE_LEVELS = 0;      // top bisection levels merged into the root front (DDG_ND_MERGE)
-int64_t MERGE_MAX = 12288; // ... while the merged separator stays below this many unknowns
-int FRONT_BT = 8;   // tiles per item side of the front operators (DDG_FRONT_BT)
+// Tunables of one symbolic phase, per call (not globals: contexts are set up
+// concurrently by the loopback ranks' threads, and a global reset to its default
+// in one thread was seen by another's tree builder -- different trees per rank)
+constexpr int64_t MERGE_MAX = 12288; // merged top separators stay below this many unknowns
 
 struct NDNode {
     std::vector<int32_t> sep;  // blocks eliminated at this node
@@ -122,9 +122,11 @@ struct NDBuilder {
     std::vector<int32_t> mark;   // 0 none, 1 L, 2 R, 3 S, 4 in V (scratch)
     std::vector<int32_t> lev;
 
+    int64_t leaf_unknowns = 256;   // nested dissection stops below this many unknowns (DDG_ND_LEAF)
+
     NDBuilder(const std::vector<std::vector<int32_t>>& a, const std::vector<int32_t>& r,
-              const int32_t* co, int nd)
-        : adj(a), rank(r), coords(co), ndim(nd), mark(a.size(), 0), lev(a.size(), -1) {}
+              const int32_t* co, int nd, int64_t leaf)
+        : adj(a), rank(r), coords(co), ndim(nd), mark(a.size(), 0), lev(a.size(), -1), leaf_unknowns(leaf) {}
 
     int64_t unknowns(const std::vector<int32_t>& V) const {
         int64_t s = 0;
@@ -220,7 +222,7 @@ struct NDBuilder {
     int build(std::vector<int32_t> V) {
         const int id = (int)nodes.size();
         nodes.emplace_back();
-        if (V.size() <= 1 || unknowns(V) <= LEAF_UNKNOWNS) {
+        if (V.size() <= 1 || unknowns(V) <= leaf_unknowns) {
             std::sort(V.begin(), V.end());
             nodes[id].sep = std::move(V);
             return id;
@@ -262,7 +264,7 @@ struct NDBuilder {
             if (l > 0 && unknowns(seps) >= MERGE_MAX) break;
             std::vector<std::vector<int32_t>> next;
             for (auto& R0 : frontier) {
-                if (R0.size() <= 1 || unknowns(R0) <= LEAF_UNKNOWNS) { finals.push_back(std::move(R0)); continue; }
+                if (R0.size() <= 1 || unknowns(R0) <= leaf_unknowns) { finals.push_back(std::move(R0)); continue; }
                 std::vector<int32_t> L, R, S;
                 if (!split_geom(R0, L, R, S)) split_bfs(R0, L, R, S);
                 if (S.empty() && (L.empty() || R.empty())) { finals.push_back(std::move(R0)); continue; }
@@ -299,13 +301,13 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     const int np = c->nparts;
     SparseCoarse* sc = new SparseCoarse();
     c->sparse = sc;
-    FRONT_BT = 8;
+    int FRONT_BT = 8;   // tiles per item side of the front operators (DDG_FRONT_BT)
     if (const char* e = getenv("DDG_FRONT_BT")) FRONT_BT = std::max(1, std::min(8, atoi(e)));
     // small coarse systems (C2, C5): bigger leaves, fewer levels on the solve's
     // critical path; large ones (C3): smaller leaves, fewer bytes (measured)
-    LEAF_UNKNOWNS = c->nc <= 262144 ? 1024 : 256;
-    if (const char* e = getenv("DDG_ND_LEAF")) LEAF_UNKNOWNS = std::max(16, atoi(e));
-    MERGE_LEVELS = 0;
+    int64_t leaf = c->nc <= 262144 ? 1024 : 256;
+    if (const char* e = getenv("DDG_ND_LEAF")) leaf = std::max(16, atoi(e));
+    int MERGE_LEVELS = 0;   // top bisection levels merged into the root front (DDG_ND_MERGE)
     if (const char* e = getenv("DDG_ND_MERGE")) MERGE_LEVELS = std::max(0, atoi(e));
     // part adjacency
     std::vector<std::vector<int32_t>> adj(np);
@@ -323,7 +325,7 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     }
     std::vector<int32_t> rank(np);
     for (int I = 0; I < np; ++I) rank[I] = c->cptr[I + 1] - c->cptr[I];
-    NDBuilder nd(adj, rank, c->block_coords.empty() ? nullptr : c->block_coords.data(), c->block_ndim);
+    NDBuilder nd(adj, rank, c->block_coords.empty() ? nullptr : c->block_coords.data(), c->block_ndim, leaf);
     // one tree per connected component of the part graph
     {
         std::vector<int32_t> comp(np, -1);

@@ -1296,24 +1296,32 @@ static void wh_plan_init();
 static int g_whole_plan = 0;   // DDG_WHOLE_PLAN (WH_PLANS; 0 measured best: C3 0.949 vs LPT 0.914)
 // per device, once, outside any stream capture (called from ddg_setup)
 void symv_ring_init() {
-    g_ring_rt = 4;
-    if (const char* e = getenv("DDG_RING_TILES")) g_ring_rt = atoi(e);
-    if (g_ring_rt != 1 && g_ring_rt != 2 && g_ring_rt != 8) g_ring_rt = 4;
-    g_ring_nb = 0;
-    if (const char* e = getenv("DDG_RING_NB")) g_ring_nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
-    g_ring_nst = 0;
-    if (const char* e = getenv("DDG_RING_NST")) g_ring_nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
-    g_ring_v2 = getenv("DDG_RING_V2") ? atoi(getenv("DDG_RING_V2")) : -1;   // -1: auto
+    // every switch computed in locals and stored once: ddg_setup may run in several
+    // host threads at a time (loopback ranks), so no global may pass through a
+    // transient value another thread could read
+    int rt = 4;
+    if (const char* e = getenv("DDG_RING_TILES")) rt = atoi(e);
+    if (rt != 1 && rt != 2 && rt != 8) rt = 4;
+    int nb = 0;
+    if (const char* e = getenv("DDG_RING_NB")) nb = std::max(2, std::min(RING_MAX_NB, atoi(e)));
+    int nst = 0;
+    if (const char* e = getenv("DDG_RING_NST")) nst = std::max(2, std::min(RING_MAX_NST, atoi(e)));
+    const int v2 = getenv("DDG_RING_V2") ? atoi(getenv("DDG_RING_V2")) : -1;   // -1: auto
+    // DDG_COMPACT (default 1): whole-triangle operators store their last tile
+    // row compact (no padding rows streamed); read by every kernel but the
+    // 8-warp ring, which is only chosen for triangles when forced (DDG_RING_V2=0)
+    int compact = (v2 == 0) ? 0 : 1;
+    if (const char* e = getenv("DDG_COMPACT")) compact = atoi(e) != 0;
+    g_ring_rt = rt;
+    g_ring_nb = nb;
+    g_ring_nst = nst;
+    g_ring_v2 = v2;
     g_pdl = getenv("DDG_PDL") ? (atoi(getenv("DDG_PDL")) != 0) : 1;
     // DDG_RING_WHOLE: 0 off, 1 (default) one copy per item, n > 1 one copy per tile row
     g_ring_whole = getenv("DDG_RING_WHOLE") ? atoi(getenv("DDG_RING_WHOLE")) : 1;
     g_ring2_split = (getenv("DDG_RING2_SPLIT") && atoi(getenv("DDG_RING2_SPLIT")) == 1) ? 1 : 2;
     g_ring_pf = getenv("DDG_RING_PF") ? atoi(getenv("DDG_RING_PF")) : 0;      // ... by k_symv_ring2
-    // DDG_COMPACT (default 1): whole-triangle operators store their last tile
-    // row compact (no padding rows streamed); read by every kernel but the
-    // 8-warp ring, which is only chosen for triangles when forced (DDG_RING_V2=0)
-    g_compact = (g_ring_v2 == 0) ? 0 : 1;
-    if (const char* e = getenv("DDG_COMPACT")) g_compact = atoi(e) != 0;
+    g_compact = compact;
 
     if (getenv("DDG_RING_TRACE") && !g_ring_trace) {
         if (cudaMalloc(&g_ring_trace, 32 * sizeof(unsigned long long)) == cudaSuccess)
