@@ -311,18 +311,20 @@ int sparse_coarse_symbolic(ddg_ctx* c, const int64_t* rp, const int32_t* col,
     if (const char* e = getenv("DDG_ND_MERGE")) MERGE_LEVELS = std::max(0, atoi(e));
     // part adjacency
     std::vector<std::vector<int32_t>> adj(np);
-    for (int I = 0; I < np; ++I) {
-        auto& a = adj[I];
-        for (int64_t x = c->bptr[I]; x < c->bptr[I + 1]; ++x) {
-            const int32_t v = c->bidx[x];
-            for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
-                const int32_t J = c->part[col[e]];
-                if (J != I) a.push_back(J);
+    parallel_for(np, [&](int64_t b, int64_t e2, int) {
+        for (int64_t I = b; I < e2; ++I) {
+            auto& a = adj[I];
+            for (int64_t x = c->bptr[I]; x < c->bptr[I + 1]; ++x) {
+                const int32_t v = c->bidx[x];
+                for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+                    const int32_t J = c->part[col[e]];
+                    if (J != (int32_t)I) a.push_back(J);
+                }
             }
+            std::sort(a.begin(), a.end());
+            a.erase(std::unique(a.begin(), a.end()), a.end());
         }
-        std::sort(a.begin(), a.end());
-        a.erase(std::unique(a.begin(), a.end()), a.end());
-    }
+    });
     std::vector<int32_t> rank(np);
     for (int I = 0; I < np; ++I) rank[I] = c->cptr[I + 1] - c->cptr[I];
     NDBuilder nd(adj, rank, c->block_coords.empty() ? nullptr : c->block_coords.data(), c->block_ndim, leaf);

@@ -5,6 +5,7 @@
 #include <stdlib.h>
 
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/ddg.h"
@@ -24,6 +25,9 @@ int set_err(int code, const char* fmt, ...);
                            "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
     } while (0)
 
+
+// host work split over the hardware threads: fn(begin, end, thread) on chunks of [0, n)
+void parallel_for(int64_t n, const std::function<void(int64_t, int64_t, int)>& fn);
 
 struct SparseCoarse;   // coarse_sparse.cpp
 void sparse_coarse_free(SparseCoarse* sc);

@@ -81,7 +81,7 @@ extern "C" void ddg_default_opts(ddg_opts* o) {
 // ---------------------------------------------------------------------------
 // small host helpers
 // ---------------------------------------------------------------------------
-static void parallel_for(int64_t n, const std::function<void(int64_t, int64_t, int)>& fn) {
+void parallel_for(int64_t n, const std::function<void(int64_t, int64_t, int)>& fn) {
     int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 32);
     if (n < 64 || nt == 1) { fn(0, n, 0); return; }
     nt = (int)std::min<int64_t>(nt, n);
@@ -221,8 +221,35 @@ static int build_colours(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
         for (int i = 0; i < np; ++i)
             for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) cov[fill[c->oidx[a]]++] = i;
     }
+    // the conflict graph, in parallel: j conflicts with i iff some row of
+    // Omega~_i or one of its neighbours lies in Omega~_j (sorted, j != i)
+    std::vector<std::vector<int32_t>> conf(np);
+    {
+        const int nt = hw_threads();
+        std::vector<std::vector<int32_t>> marks(nt);
+        parallel_for(np, [&](int64_t b, int64_t e, int t) {
+            auto& mark = marks[t];
+            if (mark.empty()) mark.assign(np, -1);
+            for (int64_t i = b; i < e; ++i) {
+                auto& L = conf[i];
+                for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) {
+                    const int32_t v = c->oidx[a];
+                    for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
+                        const int32_t u = col[x];
+                        for (int64_t q = cp[u]; q < cp[u + 1]; ++q) {
+                            const int j = cov[q];
+                            if (j != (int)i && mark[j] != (int32_t)i) {
+                                mark[j] = (int32_t)i;
+                                L.push_back(j);
+                            }
+                        }
+                    }
+                }
+                std::sort(L.begin(), L.end());
+            }
+        });
+    }
     c->colour.assign(np, -1);
-    std::vector<int32_t> vmark(n, -1);
     std::vector<char> used;
     int maxc = 0;
     if (const int32_t* uc = c->opts.colour) {
@@ -232,38 +259,20 @@ static int build_colours(ddg_ctx* c, const int64_t* rp, const int32_t* col) {
             if (uc[i] < 0 || uc[i] >= np)
                 return set_err(DDG_E_COLOURING, "colour %d of subdomain %d outside [0,%d)", uc[i], i, np);
         for (int i = 0; i < np; ++i) {
-            for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) {
-                const int32_t v = c->oidx[a];
-                for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
-                    const int32_t u = col[x];
-                    if (vmark[u] == i) continue;
-                    vmark[u] = i;
-                    for (int64_t t = cp[u]; t < cp[u + 1]; ++t) {
-                        const int j = cov[t];
-                        if (j != i && uc[j] == uc[i])
-                            return set_err(DDG_E_COLOURING, "subdomains %d and %d are coupled but share colour %d",
-                                           i, j, uc[i]);
-                    }
-                }
-            }
+            for (int32_t j : conf[i])
+                if (uc[j] == uc[i])
+                    return set_err(DDG_E_COLOURING, "subdomains %d and %d are coupled but share colour %d",
+                                   std::min(i, j), std::max(i, j), uc[i]);
             c->colour[i] = uc[i];
             maxc = std::max(maxc, uc[i] + 1);
         }
     }
+    // greedy first-fit over increasing id (reading R3): the smallest colour no
+    // already-coloured conflicting subdomain has
     for (int i = 0; i < np && !c->opts.colour; ++i) {
         used.assign(maxc + 1, 0);
-        for (int64_t a = c->optr[i]; a < c->optr[i + 1]; ++a) {
-            const int32_t v = c->oidx[a];
-            for (int64_t x = rp[v]; x < rp[v + 1]; ++x) {
-                const int32_t u = col[x];
-                if (vmark[u] == i) continue;
-                vmark[u] = i;
-                for (int64_t t = cp[u]; t < cp[u + 1]; ++t) {
-                    const int j = cov[t];
-                    if (j != i && c->colour[j] >= 0) used[c->colour[j]] = 1;
-                }
-            }
-        }
+        for (int32_t j : conf[i])
+            if (c->colour[j] >= 0) used[c->colour[j]] = 1;
         int cc = 0;
         while (cc <= maxc && used[cc]) ++cc;
         c->colour[i] = cc;
