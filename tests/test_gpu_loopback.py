@@ -151,7 +151,7 @@ def test_loopback_rejects_mismatched_collectives():
     assert 9 in codes
 
 
-@pytest.mark.parametrize("nranks", [2, 4, 8])
+@pytest.mark.parametrize("nranks", [2, 3, 4, 5, 8])
 @pytest.mark.parametrize("name", ["lognormal_32_b4", "biharm_128_b16_p3", "poisson3d_32_b8_p2"])
 def test_loopback_distributed_coarse_solve(name, nranks, monkeypatch):
     """the sparse coarse solve distributed over the ranks --
@@ -193,3 +193,30 @@ def test_loopback_distributed_coarse_solve(name, nranks, monkeypatch):
         assert np.array_equal(zc, zr) and np.array_equal(u, ur) and np.array_equal(hist, histr)
         assert np.linalg.norm(zc - zc1) <= 1e-13 * np.linalg.norm(zc1)
         assert nbr == full and nb < full
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_loopback_three_level_with_distributed_sparse_coarse(nranks, monkeypatch):
+    """three levels over the ranks with the second level's own coarse problem
+    solved by the distributed sparse solve (coarse_variant 2 on A_1)"""
+    from paper_1504_00907_b200 import Solver
+    monkeypatch.setenv("DDG_ND_LEAF", "32")
+    pr = CASES["lognormal_32_b4"]()
+    p2, n2, bc2 = P.coarse_parts(pr, 2, coords=True)
+    o = oracle.Oracle.from_problem(pr, part2=p2, nparts2=n2)
+    uo, ito, histo, conv = o.pcg(pr.f, 1e-8)
+
+    def rank(rk, comm):
+        s = Solver.from_problem(pr, comm=comm, part2=p2, nparts2=n2, block_coords2=bc2, coarse_variant=2)
+        u, it, hist, rep = s.solve(pr.f, 1e-8)
+        s.close()
+        return u, it, hist
+
+    res = run_ranks(nranks, rank)
+    for u, it, hist in res:
+        assert abs(it - ito) <= 1
+        m = min(len(hist), len(histo))
+        assert np.max(np.abs(hist[:m] - histo[:m]) / histo[:m]) <= H_TOL
+        assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+    for u, it, hist in res[1:]:
+        assert np.array_equal(u, res[0][0])
