@@ -428,30 +428,41 @@ __global__ void __launch_bounds__(256) k_gjb_gemm(GJBatch bt, int k0, int mode) 
 // speed, but 1e-14 instead of 3e-15 against numpy's inverse in tools/gjunit.py.)
 constexpr int GJP_LDA = GJB_N + 8;                          // As[kk][row]
 constexpr int GJP_LDK = TILE + 4;                           // Bs[col][kk]
-constexpr int GJP_STAGE = TILE * GJP_LDA + GJB_N * GJP_LDK; // doubles per stage (71.7 KB)
-constexpr int GJP_STAGES = 3;
+// BNT: output block width in tiles (4: 128 x 128 per CTA, 8 warps, 3 stages,
+// one CTA per SM; 2: 128 x 64 per CTA, 4 warps, 2 stages of 53 KB, two CTAs per
+// SM, so one CTA's prologue and epilogue overlap the other's products)
+template <int BNT> struct GJP {
+    static constexpr int W = 2 * BNT;                                    // warps (32 x 64 outputs each)
+    static constexpr int STAGE = TILE * GJP_LDA + BNT * TILE * GJP_LDK;  // doubles per stage
+    static constexpr int STAGES = BNT == 4 ? 3 : 2;
+};
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
                  : "memory");
 }
-__global__ void __launch_bounds__(256) k_gjb_gemm_pipe(GJBatch bt, int k0, int mode) {
+template <int BNT>
+__global__ void __launch_bounds__(GJP<BNT>::W * 32) k_gjb_gemm_pipe(GJBatch bt, int k0, int mode) {
+    constexpr int W = GJP<BNT>::W, NTH = W * 32, STAGE = GJP<BNT>::STAGE, STAGES = GJP<BNT>::STAGES;
     extern __shared__ __align__(16) double psm[];
     const int b = blockIdx.y;
     const int nT = bt.nT[b], nK = bt.nK[b];
     if (k0 >= nK) return;
     const int k1 = min(k0 + GJB_BT, nK);
-    const int nb = (nT + GJB_BT - 1) / GJB_BT;
-    int bi, bj;
+    const int nbr = (nT + GJB_BT - 1) / GJB_BT, nbc = (nT + BNT - 1) / BNT;   // row / column blocks
+    int i0, j0;
     if (mode == 1) {
-        if ((int)blockIdx.x >= nb * nb) return;
-        bi = blockIdx.x % nb;
-        bj = blockIdx.x / nb;
-    } else {
-        if ((int)blockIdx.x >= nb) return;
-        bi = mode == 0 ? k0 / GJB_BT : blockIdx.x;
-        bj = mode == 0 ? blockIdx.x : k0 / GJB_BT;
+        if ((int)blockIdx.x >= nbr * nbc) return;
+        i0 = (blockIdx.x % nbr) * GJB_BT;
+        j0 = (blockIdx.x / nbr) * BNT;
+    } else if (mode == 0) {                 // the pivot rows, every column block
+        if ((int)blockIdx.x >= nbc) return;
+        i0 = k0;
+        j0 = blockIdx.x * BNT;
+    } else {                                // every row block, the pivot columns
+        if ((int)blockIdx.x >= nbr * (GJB_BT / BNT)) return;
+        i0 = (blockIdx.x % nbr) * GJB_BT;
+        j0 = k0 + (blockIdx.x / nbr) * BNT;
     }
-    const int i0 = bi * GJB_BT, j0 = bj * GJB_BT;
     auto in_kb = [&](int t) { return t >= k0 && t < k1; };
     auto owns = [&](int I, int J) {
         return mode == 0 ? (in_kb(I) && !in_kb(J)) : mode == 1 ? (!in_kb(I) && !in_kb(J)) : (!in_kb(I) && in_kb(J));
@@ -459,42 +470,43 @@ __global__ void __launch_bounds__(256) k_gjb_gemm_pipe(GJBatch bt, int k0, int m
     {
         bool any = false;
         for (int I = i0; I < min(i0 + GJB_BT, nT); ++I)
-            for (int J = j0; J < min(j0 + GJB_BT, nT); ++J) any |= owns(I, J);
+            for (int J = j0; J < min(j0 + BNT, nT); ++J) any |= owns(I, J);
         if (!any) return;
     }
     double* M = bt.mats[b];
     auto tile = [&](int I, int J) { return M + ((int64_t)J * nT + I) * TILE_ELEMS; };
     const int nq = k1 - k0;
     auto load_stage = [&](int q, int slot) {
-        double* As = psm + slot * GJP_STAGE;
+        double* As = psm + slot * STAGE;
         double* Bs = As + TILE * GJP_LDA;
         constexpr int CH = TILE * TILE / 2;   // 16-byte chunks per tile
-        for (int e = threadIdx.x; e < GJB_BT * CH; e += 256) {
+        for (int e = threadIdx.x; e < GJB_BT * CH; e += NTH) {
             const int t = e / CH, rem = e % CH;
             const int kk = rem / (TILE / 2), r2 = (rem % (TILE / 2)) * 2;
             // A: tile (I, q), element (r, kk) at kk * 32 + r  ->  As[kk][t * 32 + r]
-            const int I = (mode == 0 ? k0 : i0) + t;
+            const int I = i0 + t;
             const bool oka = I < nT && (mode != 0 || I < k1);
             cp_async16(As + kk * GJP_LDA + t * TILE + r2, oka ? tile(I, q) + kk * TILE + r2 : M, oka);
+        }
+        for (int e = threadIdx.x; e < BNT * CH; e += NTH) {
+            const int t = e / CH, rem = e % CH;
+            const int c = rem / (TILE / 2), k2 = (rem % (TILE / 2)) * 2;
             // B: tile (q, J), element (kk, c) at c * 32 + kk  ->  Bs[t * 32 + c][kk]
-            const int c = kk, k2 = r2;
-            const int J = (mode == 2 ? k0 : j0) + t;
+            const int J = j0 + t;
             const bool okb = J < nT && (mode != 2 || J < k1);
             cp_async16(Bs + (t * TILE + c) * GJP_LDK + k2, okb ? tile(q, J) + c * TILE + k2 : M, okb);
         }
     };
 #pragma unroll
-    for (int sg = 0; sg < GJP_STAGES - 1; ++sg) {
+    for (int sg = 0; sg < STAGES - 1; ++sg) {
         if (sg < nq) load_stage(k0 + sg, sg);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int wr = (wid & 3) * 32, wc = (wid >> 2) * 64;   // this warp's 32 x 64 output tile
     const int I = i0 + wr / TILE;
-    // value v = 16 mi + 2 ni + h of acc (acc[v / 8][v % 8]) is
-    // C(wr + 8 mi + lane / 4, wc + 8 ni + 2 (lane % 4) + h)
-    if (mode == 1 && threadIdx.x < GJB_BT * GJB_BT) {
-        const int Ip = i0 + threadIdx.x / GJB_BT, Jp = j0 + threadIdx.x % GJB_BT;
+    if (mode == 1 && (int)threadIdx.x < GJB_BT * BNT) {
+        const int Ip = i0 + threadIdx.x / BNT, Jp = j0 + threadIdx.x % BNT;
         if (Ip < nT && Jp < nT && owns(Ip, Jp)) bulk_prefetch_l2(tile(Ip, Jp), TILE_ELEMS * sizeof(double));
     }
     double acc[8][8];
@@ -503,11 +515,11 @@ __global__ void __launch_bounds__(256) k_gjb_gemm_pipe(GJBatch bt, int k0, int m
 #pragma unroll
         for (int c2 = 0; c2 < 8; ++c2) acc[r][c2] = 0.0;
     for (int qi = 0; qi < nq; ++qi) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(GJP_STAGES - 2) : "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
         __syncthreads();
-        if (qi + GJP_STAGES - 1 < nq) load_stage(k0 + qi + GJP_STAGES - 1, (qi + GJP_STAGES - 1) % GJP_STAGES);
+        if (qi + STAGES - 1 < nq) load_stage(k0 + qi + STAGES - 1, (qi + STAGES - 1) % STAGES);
         asm volatile("cp.async.commit_group;" ::: "memory");
-        const double* As = psm + (qi % GJP_STAGES) * GJP_STAGE;
+        const double* As = psm + (qi % STAGES) * STAGE;
         const double* Bs = As + TILE * GJP_LDA;
 #pragma unroll 2
         for (int kq = 0; kq < TILE; kq += 4) {
@@ -524,6 +536,7 @@ __global__ void __launch_bounds__(256) k_gjb_gemm_pipe(GJBatch bt, int k0, int m
                                  : "+d"(acc[2 * mi + ni / 4][(2 * ni) % 8]), "+d"(acc[2 * mi + ni / 4][(2 * ni) % 8 + 1])
                                  : "d"(af[mi]), "d"(bf[ni]));
         }
+        if (STAGES == 2) __syncthreads();   // two stages: the next prefetch overwrites this one
     }
     if (I >= nT) return;
 #pragma unroll
@@ -701,12 +714,14 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
     const int smem_p = 9 * TILE_ELEMS * sizeof(double);
     const int smem_g = (TILE * GJB_N + TILE * GJB_BPAD) * sizeof(double);
     const int smem_m = 2 * TILE * GJB_LDM * sizeof(double);
-    const int smem_pp = GJP_STAGES * GJP_STAGE * sizeof(double);
+    const int smem_pp = GJP<4>::STAGES * GJP<4>::STAGE * sizeof(double);
+    const int smem_p2 = GJP<2>::STAGES * GJP<2>::STAGE * sizeof(double);
     if (!init) {
         cudaFuncSetAttribute(k_gjb_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p);
         cudaFuncSetAttribute(k_gjb_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);
         cudaFuncSetAttribute(k_gjb_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_m);
-        cudaFuncSetAttribute(k_gjb_gemm_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
+        cudaFuncSetAttribute(k_gjb_gemm_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
+        cudaFuncSetAttribute(k_gjb_gemm_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p2);
         init = true;
     }
     GJBatch bt{mats, nT, nK, ids, err, nullptr, 0};
@@ -724,12 +739,19 @@ void launch_gj_blocked(cudaStream_t st, int nmat, int maxT, int maxK, double* co
     const bool use_mma = !getenv("DDG_GJ_MMA") || atoi(getenv("DDG_GJ_MMA")) != 0;   // experiment switch
     // the pipelined MMA product for the full exchange (DDG_GJ_PIPE=0: the single-stage one)
     const bool use_pipe = use_mma && !bt.strip && !(getenv("DDG_GJ_PIPE") && atoi(getenv("DDG_GJ_PIPE")) == 0);
+    // DDG_GJ_BNT = 2: the 128 x 64 two-CTAs-per-SM product, 4 (default): 128 x 128
+    const int pipe_bnt = getenv("DDG_GJ_BNT") && atoi(getenv("DDG_GJ_BNT")) == 2 ? 2 : 4;
     for (int k0 = 0; k0 < maxK; k0 += GJB_BT) {
         k_gjb_pivot<<<nmat, 256, smem_p, st>>>(bt, k0);
-        if (use_pipe) {
-            k_gjb_gemm_pipe<<<dim3(nb, nmat), 256, smem_pp, st>>>(bt, k0, 0);
-            k_gjb_gemm_pipe<<<dim3(nb * nb, nmat), 256, smem_pp, st>>>(bt, k0, 1);
-            k_gjb_gemm_pipe<<<dim3(nb, nmat), 256, smem_pp, st>>>(bt, k0, 2);
+        if (use_pipe && pipe_bnt == 2) {
+            const int nbc = (maxT + 1) / 2;
+            k_gjb_gemm_pipe<2><<<dim3(nbc, nmat), 128, smem_p2, st>>>(bt, k0, 0);
+            k_gjb_gemm_pipe<2><<<dim3(nb * nbc, nmat), 128, smem_p2, st>>>(bt, k0, 1);
+            k_gjb_gemm_pipe<2><<<dim3(nb * 2, nmat), 128, smem_p2, st>>>(bt, k0, 2);
+        } else if (use_pipe) {
+            k_gjb_gemm_pipe<4><<<dim3(nb, nmat), 256, smem_pp, st>>>(bt, k0, 0);
+            k_gjb_gemm_pipe<4><<<dim3(nb * nb, nmat), 256, smem_pp, st>>>(bt, k0, 1);
+            k_gjb_gemm_pipe<4><<<dim3(nb, nmat), 256, smem_pp, st>>>(bt, k0, 2);
         } else if (use_mma) {
             k_gjb_gemm<true><<<dim3(nb, nmat), 256, smem_m, st>>>(bt, k0, 0);
             k_gjb_gemm<true><<<dim3(nb * nb, nmat), 256, smem_m, st>>>(bt, k0, 1);
