@@ -693,6 +693,16 @@ __global__ void k_gather_masked(int64_t n, const int32_t* __restrict__ idx, cons
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
         dst[k] = mask[k] ? src[idx ? idx[k] : k] : 0.0;
 }
+// copy segments [src_off, src_off + len) -> [dst_off, ...), one CTA per segment
+__global__ void k_copy_segments(const int64_t* __restrict__ seg, const double* __restrict__ src,
+                                double* __restrict__ dst) {
+    const int64_t so = seg[3 * blockIdx.x], doff = seg[3 * blockIdx.x + 1], len = seg[3 * blockIdx.x + 2];
+    for (int64_t x = threadIdx.x; x < len; x += blockDim.x) dst[doff + x] = src[so + x];
+}
+void launch_copy_segments(cudaStream_t st, int nseg, const int64_t* seg, const double* src, double* dst) {
+    for (int s0 = 0; s0 < nseg; s0 += 65535)
+        k_copy_segments<<<std::min(65535, nseg - s0), 256, 0, st>>>(seg + 3 * (int64_t)s0, src, dst);
+}
 void launch_gather_masked(cudaStream_t st, int64_t n, const int32_t* idx, const uint8_t* mask, const double* src,
                           double* dst) {
     if (n > 0) k_gather_masked<<<vec_grid(n), VEC_THREADS, 0, st>>>(n, idx, mask, src, dst);

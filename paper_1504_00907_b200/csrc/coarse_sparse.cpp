@@ -822,6 +822,50 @@ static int sparse_coarse_dist_setup(ddg_ctx* c) {
     }
     rb += tb / P;    // the top fronts' item ranges are split evenly by item count
     sc->rank_solve_bytes = (int64_t)rb;
+    // keep only the front operators this rank reads (its subtrees, its chunk of every
+    // top range): the factor was built replicated (the top fronts need every
+    // subtree's Schur complement), the solve needs a 1/P share of it
+    if (!(getenv("DDG_COARSE_KEEP_ALL") && atoi(getenv("DDG_COARSE_KEEP_ALL")) != 0)) {
+        std::vector<char> keep(c->items.size(), 0);
+        for (int h = 0; h < sc->nlevels; ++h)
+            for (int q = sc->g_begin[h]; q < sc->h_end[h]; ++q)
+                if (mine(sc->item_front[q - sc->item_base])) keep[q] = 1;
+        auto chunk = [&](int q0, int q1) {
+            const int64_t len = q1 - q0;
+            for (int q = q0 + (int)(len * me / P); q < q0 + (int)(len * (me + 1) / P); ++q) keep[q] = 1;
+        };
+        for (const auto& t : sc->tops) {
+            chunk(t.g0, t.g1);
+            chunk(t.h0, t.h1);
+        }
+        std::vector<int64_t> seg;
+        int64_t nd = 0;
+        for (int q = sc->item_base; q < sc->item_end; ++q) {
+            if (!keep[q]) continue;
+            ItemDesc& it = c->items[q];
+            const int64_t len = item_doubles(it.tri, it.I1 - it.I0, it.ntiles);
+            seg.push_back(it.tile_off);
+            seg.push_back(nd);
+            seg.push_back(len);
+            it.tile_off = nd;
+            nd += len;
+        }
+        double* d_new = nullptr;
+        int64_t* d_seg = nullptr;
+        if ((st = dalloc(&d_new, std::max<int64_t>(1, nd))) || (st = up(&d_seg, seg))) return st;
+        launch_copy_segments(c->stream, (int)(seg.size() / 3), d_seg, sc->d_ctiles, d_new);
+        for (int q = sc->item_base; q < sc->item_end; ++q)
+            if (!keep[q]) c->items[q].tile_off = -1;   // never read on this rank
+        CUDA_TRY(cudaMemcpyAsync(c->d_items + sc->item_base, c->items.data() + sc->item_base,
+                                 (size_t)(sc->item_end - sc->item_base) * sizeof(ItemDesc), cudaMemcpyHostToDevice,
+                                 c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        CUDA_TRY(cudaGetLastError());
+        cudaFree(d_seg);
+        cudaFree(sc->d_ctiles);
+        sc->d_ctiles = d_new;
+        sc->factor_bytes = nd * 8;
+    }
     sc->dist = true;
     if (c->opts.verbose)
         fprintf(stderr, "[ddg_setup] distributed coarse solve: depth %d cut, %d top fronts, %d subtrees; rank %d "

@@ -328,6 +328,7 @@ void launch_front_fwd_assemble(cudaStream_t st, int f0, int nf, const FrontDesc*
                                double* w, const int32_t* done);
 void launch_front_bwd_gather(cudaStream_t st, int f0, int nf, const FrontDesc* fronts,
                              const int32_t* fB, const double* x, double* fvec, const int32_t* done);
+void launch_copy_segments(cudaStream_t st, int nseg, const int64_t* seg, const double* src, double* dst);
 void launch_gather_masked(cudaStream_t st, int64_t n, const int32_t* idx, const uint8_t* mask, const double* src,
                           double* dst);
 void launch_front_reduce(cudaStream_t st, const FRedTask* tasks, int t0, int nt, const int64_t* contrib,

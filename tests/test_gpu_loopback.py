@@ -174,7 +174,7 @@ def test_loopback_distributed_coarse_solve(name, nranks, monkeypatch):
         s = Solver.from_problem(pr, comm=comm, coarse_variant=2)
         zc = s.coarse_correct(r)
         u, it, hist, rep = s.solve(pr.f, 1e-8)
-        nb = s.info.coarse_solve_bytes
+        nb = (s.info.coarse_solve_bytes, s.info.coarse_factor_bytes)
         s.close()
         return zc, u, it, hist, nb
 
@@ -182,7 +182,7 @@ def test_loopback_distributed_coarse_solve(name, nranks, monkeypatch):
     monkeypatch.setenv("DDG_COARSE_REPLICATED", "1")
     rep_ = run_ranks(nranks, rank)
     s1 = Solver.from_problem(pr, coarse_variant=2)
-    full = s1.info.coarse_solve_bytes
+    full = (s1.info.coarse_solve_bytes, s1.info.coarse_factor_bytes)
     zc1 = s1.coarse_correct(r)
     s1.close()
     for (zc, u, it, hist, nb), (zr, ur, itr, histr, nbr) in zip(res, rep_):
@@ -192,7 +192,9 @@ def test_loopback_distributed_coarse_solve(name, nranks, monkeypatch):
         assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
         assert np.array_equal(zc, zr) and np.array_equal(u, ur) and np.array_equal(hist, histr)
         assert np.linalg.norm(zc - zc1) <= 1e-13 * np.linalg.norm(zc1)
-        assert nbr == full and nb < full
+        assert nbr == full
+        assert nb[0] < full[0] and nb[1] < full[1]      # reads and stores a share of the factor
+    assert sum(r[4][1] for r in res) == full[1]          # the shares partition it: each operator on one rank
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
