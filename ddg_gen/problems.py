@@ -471,11 +471,16 @@ def elasticity3d(ne=64, be=8, seed=1004, overlap=1, E=1.0, nu=0.3, clamp=True):
                   dtype=np.int32)
     part = np.repeat(npart, 3)
     f = rng.uniform_pm1(seed, n)
-    return Problem(name="elasticity3d", n=n, row_ptr=row_ptr, col=col, val=val, F=F,
-                   part=part, nparts=nparts, block_coords=bc, block_dims=(nbx,) * 3, f=f,
-                   overlap=overlap,
-                   meta=dict(dims=dims, p=1, be=be, ne=ne, lam=lam, mu=mu, seed=seed,
-                             stencil="q1_elastic", dof_per_node=3))
+    pr = Problem(name="elasticity3d", n=n, row_ptr=row_ptr, col=col, val=val, F=F,
+                 part=part, nparts=nparts, block_coords=bc, block_dims=(nbx,) * 3, f=f,
+                 overlap=overlap,
+                 meta=dict(dims=dims, p=1, be=be, ne=ne, lam=lam, mu=mu, seed=seed,
+                           stencil="q1_elastic", dof_per_node=3))
+    # node-blocked 27-point rows, constant per boundary class (include/ddg.h
+    # DDG_STENCIL_NODE27): the library reads the values from the CSR and checks
+    # every row against them
+    pr.stencil = dict(kind="node27", dims=dims, dof=3)
+    return pr
 
 
 def grown_partition(pr, nparts, seed=77):

@@ -69,10 +69,18 @@ enum { DDG_STOP_RES0 = 0,      /* ||r_k||_2 <= rtol ||r_0||_2 (default)         
  * All pointers are host pointers, borrowed for the duration of ddg_setup. */
 enum { DDG_STENCIL_NONE = 0,
        DDG_STENCIL_CONST = 1,   /* constant coefficients: npts points (dx, dy, dz) with values coef */
-       DDG_STENCIL_FACE7 = 2 }; /* 7-point with per-row coefficients: coef = 4 x n, blocks
+       DDG_STENCIL_FACE7 = 2,   /* 7-point with per-row coefficients: coef = 4 x n, blocks
                                    diag | cx | cy | cz with cx[v] = A[v, v+1],
                                    cy[v] = A[v, v+dims[0]], cz[v] = A[v, v+dims[0]*dims[1]]
                                    (A symmetric: A[v, v-1] = cx[v-1], ...)                     */
+       DDG_STENCIL_NODE27 = 3 };/* node-blocked 27-point operator with constant rows per boundary
+                                   class (Q1 elements on a uniform grid, BASELINE C4): dims =
+                                   nodes per axis, npts = unknowns per node (1..4), row
+                                   dof * node + d, node = x + dims[0] (y + dims[1] z); every row
+                                   couples to all in-grid nodes at distance <= 1 per axis.  The
+                                   values are read from the CSR: all nodes of one class (first /
+                                   interior / last per axis, 27 classes) must have identical rows;
+                                   offsets and coef are unused                                   */
 enum { DDG_STENCIL_MAX_PTS = 16 };
 typedef struct {
     int32_t kind;              /* DDG_STENCIL_*                                                 */

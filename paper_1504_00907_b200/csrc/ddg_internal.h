@@ -133,15 +133,15 @@ constexpr int VEC_THREADS = 256;
 // evaluated in that order too, so stencil and CSR rows round identically.
 constexpr int STENCIL_MAX_PTS = 16;
 struct DevStencil {
-    int32_t kind;        // 0 none (CSR), 1 constant, 2 face7
+    int32_t kind;        // 0 none (CSR), 1 constant, 2 face7, 3 node27 (class table in coef)
     int32_t npts;
     int32_t nx, ny, nz, pad;
     int32_t dx[STENCIL_MAX_PTS], dy[STENCIL_MAX_PTS], dz[STENCIL_MAX_PTS];
     int32_t off[STENCIL_MAX_PTS];   // linear offsets dx + nx (dy + ny dz)
     int32_t rx, ry, rz;             // reach per axis: rows farther than that from the faces need no checks
-    int32_t pad2;
+    int32_t dof;                    // node27: unknowns per node
     double c[STENCIL_MAX_PTS];
-    const double* coef;  // face7: diag | cx | cy | cz, 4 n doubles (device)
+    const double* coef;  // face7: diag | cx | cy | cz, 4 n doubles; node27: table[class][offset][d][e] (device)
 };
 
 struct DevCSR {

@@ -100,6 +100,34 @@ __device__ __forceinline__ double stencil_dot(const DevStencil& st, int64_t v, c
             if (in[k]) s = fma(st.c[k], xk[k], s);
         return s;
     }
+    if (st.kind == 3) {
+        // node27: row v = dof * node + d; the node's class (first / interior / last per
+        // axis) selects its table rows; neighbours in ascending node order, then e --
+        // the CSR's column order, so the multiply-adds round as the CSR row does
+        const int dof = st.dof;
+        const unsigned node = vv / (unsigned)dof, d = vv - node * (unsigned)dof;
+        const unsigned q = node / (unsigned)nx;
+        const int jx = (int)(node - q * (unsigned)nx);
+        const unsigned q2 = q / (unsigned)ny;
+        const int jy = (int)(q - q2 * (unsigned)ny), jz = (int)q2;
+        const int cls = (jx == 0 ? 0 : jx == nx - 1 ? 2 : 1) + 3 * (jy == 0 ? 0 : jy == ny - 1 ? 2 : 1) +
+                        9 * (jz == 0 ? 0 : jz == st.nz - 1 ? 2 : 1);
+        const double* T = st.coef + ((size_t)cls * 27 * dof + d) * dof;   // [offset][d][e], offset-major
+        for (int dz = -1; dz <= 1; ++dz) {
+            if (jz + dz < 0 || jz + dz >= st.nz) continue;
+            for (int dy = -1; dy <= 1; ++dy) {
+                if (jy + dy < 0 || jy + dy >= ny) continue;
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (jx + dx < 0 || jx + dx >= nx) continue;
+                    const int o = (dx + 1) + 3 * ((dy + 1) + 3 * (dz + 1));
+                    const int64_t nb = (int64_t)node + dx + (int64_t)nx * (dy + (int64_t)ny * dz);
+                    const double* Te = T + (size_t)o * dof * dof;
+                    for (int e = 0; e < dof; ++e) s = fma(__ldg(Te + e), ldx<CG>(x + nb * dof + e), s);
+                }
+            }
+        }
+        return s;
+    }
     const int64_t n = (int64_t)nx * ny * st.nz, sy = nx, sz = (int64_t)nx * ny;
     const double* D = st.coef;
     const double* CX = D + n;

@@ -336,11 +336,88 @@ static void add_op(ddg_ctx* c, int32_t m, int out_mode, int64_t idx_off, bool al
 
 // ddg_stencil (include/ddg.h): check that it reproduces every CSR row exactly
 // and build the device description (CONST points sorted into column order).
+// DDG_STENCIL_NODE27: the class table from the CSR, every row checked against it
+static int build_node27(const ddg_stencil* S, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
+                        DevStencil& D, std::vector<double>& table) {
+    const int64_t nx = S->dims[0], ny = S->dims[1], nz = S->dims[2], dof = S->npts;
+    if (dof < 1 || dof > 4 || nx < 1 || ny < 1 || nz < 1 || nx * ny * nz * dof != n)
+        return set_err(DDG_E_ARG, "node27 stencil: dims %lld x %lld x %lld x %lld unknowns per node != n = %lld",
+                       (long long)nx, (long long)ny, (long long)nz, (long long)dof, (long long)n);
+    D.kind = 3;
+    D.nx = (int32_t)nx;
+    D.ny = (int32_t)ny;
+    D.nz = (int32_t)nz;
+    D.dof = (int32_t)dof;
+    const size_t per_class = 27 * (size_t)dof * dof;
+    table.assign(27 * per_class, 0.0);
+    std::vector<int64_t> rep(27, -1);               // the node whose rows define each class
+    auto cls_of = [&](int64_t ix, int64_t iy, int64_t iz) {
+        return (int)((ix == 0 ? 0 : ix == nx - 1 ? 2 : 1) + 3 * (iy == 0 ? 0 : iy == ny - 1 ? 2 : 1) +
+                     9 * (iz == 0 ? 0 : iz == nz - 1 ? 2 : 1));
+    };
+    // expected columns of row (node, d) and the table slot of each, in CSR order
+    auto walk = [&](int64_t node, const std::function<bool(int64_t colv, size_t slot)>& f) {
+        const int64_t ix = node % nx, iy = (node / nx) % ny, iz = node / (nx * ny);
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (ix + dx < 0 || ix + dx >= nx || iy + dy < 0 || iy + dy >= ny || iz + dz < 0 || iz + dz >= nz)
+                        continue;
+                    const int o = (dx + 1) + 3 * ((dy + 1) + 3 * (dz + 1));
+                    const int64_t nb = node + dx + nx * (dy + ny * (int64_t)dz);
+                    for (int e = 0; e < dof; ++e)
+                        if (!f(nb * dof + e, (size_t)o * dof * dof + e)) return false;
+                }
+        return true;
+    };
+    const int64_t nnode = nx * ny * nz;
+    for (int64_t node = 0; node < nnode; ++node) {   // first node of each class fills its table rows
+        const int cl = cls_of(node % nx, (node / nx) % ny, node / (nx * ny));
+        if (rep[cl] >= 0) continue;
+        rep[cl] = node;
+        for (int d = 0; d < dof; ++d) {
+            const int64_t v = node * dof + d;
+            int64_t k = rp[v];
+            const bool ok = walk(node, [&](int64_t colv, size_t slot) {
+                if (k >= rp[v + 1] || col[k] != colv) return false;
+                table[cl * per_class + slot + (size_t)d * dof] = val[k++];
+                return true;
+            });
+            if (!ok || k != rp[v + 1])
+                return set_err(DDG_E_ARG, "node27 stencil: row %lld is not a full 27-point node row", (long long)v);
+        }
+    }
+    std::atomic<int64_t> bad{-1};
+    parallel_for(nnode, [&](int64_t b, int64_t e, int) {
+        for (int64_t node = b; node < e && bad.load() < 0; ++node) {
+            const int cl = cls_of(node % nx, (node / nx) % ny, node / (nx * ny));
+            for (int d = 0; d < dof; ++d) {
+                const int64_t v = node * dof + d;
+                int64_t k = rp[v];
+                const bool ok = walk(node, [&](int64_t colv, size_t slot) {
+                    const bool same = k < rp[v + 1] && col[k] == colv &&
+                                      val[k] == table[cl * per_class + slot + (size_t)d * dof];
+                    ++k;
+                    return same;
+                });
+                if (!ok || k != rp[v + 1]) {
+                    int64_t exp = -1;
+                    bad.compare_exchange_strong(exp, v);
+                }
+            }
+        }
+    });
+    if (bad.load() >= 0)
+        return set_err(DDG_E_ARG, "node27 stencil does not reproduce row %lld of the CSR matrix", (long long)bad.load());
+    return DDG_OK;
+}
+
 static int build_stencil(ddg_ctx* c, const ddg_stencil* S, int64_t n, const int64_t* rp, const int32_t* col,
                          const double* val, DevStencil& D, std::vector<double>& coef) {
     D = DevStencil{};
     if (!S || S->kind == DDG_STENCIL_NONE) return DDG_OK;
     const int64_t nx = S->dims[0], ny = S->dims[1], nz = S->dims[2];
+    if (S->kind == DDG_STENCIL_NODE27) return build_node27(S, n, rp, col, val, D, coef);
     if (nx < 1 || ny < 1 || nz < 1 || nx * ny * nz != n)
         return set_err(DDG_E_ARG, "stencil dims %lld x %lld x %lld do not match n = %lld", (long long)nx,
                        (long long)ny, (long long)nz, (long long)n);
@@ -1834,7 +1911,8 @@ static bool build_solve_graph(ddg_ctx* c, double* d_u) {
 
 // SURVEY.md §8(d) byte model of one PCG iteration on this rank
 static double bytes_per_iter_model(ddg_ctx* c) {
-    const double a = c->A.st.kind == 1 ? 0.0 : c->A.st.kind == 2 ? 32.0 : 12.0 * (double)c->nnz / (double)c->n + 4.0;
+    const double a = (c->A.st.kind == 1 || c->A.st.kind == 3) ? 0.0
+                     : c->A.st.kind == 2 ? 32.0 : 12.0 * (double)c->nnz / (double)c->n + 4.0;
     double local = 0.0, msum = 0.0;
     for (size_t q = 0; q < c->op_sub.size(); ++q) {      // the subdomain operators come first
         const double m = c->ops[q].m;

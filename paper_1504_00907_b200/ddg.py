@@ -39,7 +39,7 @@ class ddg_stencil(C.Structure):
                 ("offsets", C.c_void_p), ("coef", C.c_void_p)]
 
 
-STENCIL_KIND = {"none": 0, "const": 1, "face7": 2}
+STENCIL_KIND = {"none": 0, "const": 1, "face7": 2, "node27": 3}
 
 
 class ddg_opts(C.Structure):
@@ -207,13 +207,17 @@ class Solver:
         if stencil is not None:
             # {"kind": "const", "dims": (nx, ny, nz), "offsets": [(dx, dy, dz), ...], "coef": [...]}
             # {"kind": "face7", "dims": (nx, ny, nz), "coef": float64[4 n] (diag|cx|cy|cz)}
+            # {"kind": "node27", "dims": (nx, ny, nz) nodes, "dof": unknowns per node}
             st = ddg_stencil()
             st.kind = STENCIL_KIND[stencil["kind"]]
             d = list(stencil["dims"]) + [1] * (3 - len(stencil["dims"]))
             st.dims = (C.c_int32 * 3)(*d)
-            cf = np.ascontiguousarray(stencil["coef"], np.float64)
-            keep.append(cf)
-            st.coef = cf.ctypes.data
+            if stencil["kind"] == "node27":        # values read from the CSR by the library
+                st.npts = int(stencil["dof"])
+            else:
+                cf = np.ascontiguousarray(stencil["coef"], np.float64)
+                keep.append(cf)
+                st.coef = cf.ctypes.data
             if stencil["kind"] == "const":
                 offs = np.zeros((len(stencil["offsets"]), 3), np.int32)
                 for i, off in enumerate(stencil["offsets"]):

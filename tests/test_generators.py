@@ -179,3 +179,38 @@ def test_grown_partition_connected_irregular(mk, nparts):
     assert np.array_equal(P.grown_partition(pr, nparts, 9).part, g.part)
     assert not np.array_equal(P.grown_partition(pr, nparts, 10).part, g.part)
     assert g.val is pr.val and g.F is pr.F and g.f is pr.f and g.block_coords is None
+
+
+def test_node27_descriptor_classes_reproduce_csr():
+    """C4's node27 descriptor (include/ddg.h DDG_STENCIL_NODE27): every row is a
+    full 27-point node row in ascending column order, and all nodes of one
+    boundary class (first / interior / last per axis) have identical rows, so
+    the class table the library reads from the CSR reproduces A exactly."""
+    pr = P.elasticity3d(4, 2, 5)
+    st = pr.stencil
+    assert st["kind"] == "node27" and st["dof"] == 3
+    nx, ny, nz = st["dims"]
+    dof = st["dof"]
+    assert nx * ny * nz * dof == pr.n
+    table = {}
+    for node in range(nx * ny * nz):
+        ix, iy, iz = node % nx, (node // nx) % ny, node // (nx * ny)
+        cls = tuple(0 if a == 0 else 2 if a == m - 1 else 1 for a, m in ((ix, nx), (iy, ny), (iz, nz)))
+        for d in range(dof):
+            v = node * dof + d
+            cols, vals = [], []
+            for dz in (-1, 0, 1):
+                for dy in (-1, 0, 1):
+                    for dx in (-1, 0, 1):
+                        a, b, c = ix + dx, iy + dy, iz + dz
+                        if 0 <= a < nx and 0 <= b < ny and 0 <= c < nz:
+                            nb = a + nx * (b + ny * c)
+                            cols += [nb * dof + e for e in range(dof)]
+            row = slice(pr.row_ptr[v], pr.row_ptr[v + 1])
+            assert np.array_equal(pr.col[row], np.array(cols))
+            key = (cls, d)
+            if key in table:
+                assert np.array_equal(table[key], pr.val[row])
+            else:
+                table[key] = pr.val[row].copy()
+    assert len(table) == 27 * dof

@@ -476,6 +476,7 @@ def test_node_blocked_rows_match_csr_bitwise(name, monkeypatch):
     else:
         pr = CASES[name]()
         kw = {}
+    monkeypatch.setenv("DDG_NO_STENCIL", "1")      # the CSR rows (C4 has a node27 stencil too)
     out = []
     for off in ("1", None):
         if off:
@@ -513,3 +514,36 @@ def test_fractional_iterations_bracket(stop_mode):
     sizes = s.subdomain_sizes().astype(float)
     local = 2 * np.sum(8 * sizes * (sizes + 1) / 2)
     assert local < rep.bytes_per_iter_model < 2 * local + 400 * pr.n
+
+
+@pytest.mark.parametrize("name", ["elasticity_8_be4"])
+def test_node27_stencil_matches_csr_path(name, monkeypatch):
+    """C4's node27 class stencil (include/ddg.h DDG_STENCIL_NODE27: rows read
+    from the CSR per boundary class, every row checked) against the CSR rows:
+    the same matrix, one lane per row instead of the CSR path's eight, so the
+    solves agree to rounding; both at the oracle bar (test_pcg_parity)."""
+    pr = CASES[name]()
+    assert pr.stencil["kind"] == "node27"
+    s1 = _solver(pr)
+    r = np.random.default_rng(9).standard_normal(pr.n)
+    y1 = s1.spmv(r)
+    u1, it1, h1, _ = s1.solve(pr.f)
+    monkeypatch.setenv("DDG_NO_STENCIL", "1")
+    s2 = _solver(pr)
+    y2 = s2.spmv(r)
+    u2, it2, h2, _ = s2.solve(pr.f)
+    assert np.linalg.norm(y1 - y2) <= 1e-14 * np.linalg.norm(y2)
+    assert it1 == it2 and np.linalg.norm(u1 - u2) <= 1e-12 * np.linalg.norm(u2)
+    assert s1.info.m_max == s2.info.m_max
+
+
+def test_node27_stencil_rejected_when_wrong():
+    from paper_1504_00907_b200 import DDGError
+    pr = P.elasticity3d(4, 2, 5)
+    nx, ny, nz = pr.stencil["dims"]
+    with pytest.raises(DDGError) as e:            # dims do not match n
+        _solver(pr, stencil=dict(pr.stencil, dims=(nx, ny, nz - 1)))
+    assert e.value.code == 1
+    with pytest.raises(DDGError) as e:            # rows are not 1-dof 27-point rows
+        _solver(pr, stencil=dict(kind="node27", dims=(nx * 3, ny, nz), dof=1))
+    assert e.value.code == 1
