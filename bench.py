@@ -300,7 +300,8 @@ def bench_ddg(args):
                               3: "three levels: two-level DDG on A_c (second level %s, n_c2=%d, %d parts)" % (
                                   "dense" if s.info.coarse_variant2 == 1 else "sparse", s.info.n_c2,
                                   s.info.nparts2)}[s.info.coarse_variant],
-                   "levels": int(s.info.levels), "parallelism": f"subdomain-sharded x{world} (NCCL halos + allreduce, replicated coarse)" if world > 1 else "1gpu",
+                   "levels": int(s.info.levels), "parallelism": f"subdomain-sharded x{world} (NCCL halos, boundary subdomains first; "
+                                  f"split reductions; coarse solve {'distributed over the ranks' if s.info.coarse_variant == 2 else 'replicated (dense)'})" if world > 1 else "1gpu",
                    "l2": "inputs larger than L2 (local inverses %.1f GB)" % (s.info.local_factor_bytes / 1e9),
                    "time_to_rtol_ms": ms_step, "t_setup_s": round(t_setup, 2),
                    "cond_est_lanczos": round(float(rep.cond_est), 3),
