@@ -181,7 +181,10 @@ extern "C" void ddg_loop_group_destroy(ddg_loop_group* g) {
     cudaSetDevice(g->device);
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->d_tmp) cudaFree(g->d_tmp);
-    if (g->stream) cudaStreamDestroy(g->stream);
+    if (g->stream) {
+        ddg::release_no_pdl_stream(g->stream);
+        cudaStreamDestroy(g->stream);
+    }
     delete g;
 }
 

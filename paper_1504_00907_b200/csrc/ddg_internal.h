@@ -181,6 +181,7 @@ struct ColourPlan {
 // streams on which chain kernels launch without programmatic dependent launch
 // (the loopback group's stream, shared by several host threads; symv.cu)
 void register_no_pdl_stream(cudaStream_t st);
+void release_no_pdl_stream(cudaStream_t st);
 // ---- kernel launchers (pcg.cu, symv.cu, coarse.cu, setup_kernels.cu) --------
 void launch_symv(cudaStream_t st, const OpDesc* ops, const ItemDesc* items, int item_begin,
                  int nitems, const double* tiles, const double* s, const int32_t* oidx, double* z,

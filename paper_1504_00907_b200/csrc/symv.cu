@@ -9,22 +9,30 @@
 
 namespace ddg {
 int g_pdl = 1;
-static cudaStream_t g_nopdl[64];
-static std::atomic<int> g_nnopdl{0};
+static std::mutex g_nopdl_mu;
+static std::vector<cudaStream_t> g_nopdl;   // live loopback streams (registered / released by comm.cpp)
+static std::atomic<int> g_nopdl_n{0};
 bool no_pdl_stream(cudaStream_t st) {
-    const int n = g_nnopdl.load(std::memory_order_acquire);
-    for (int i = 0; i < n; ++i)
-        if (g_nopdl[i] == st) return true;
+    if (g_nopdl_n.load(std::memory_order_acquire) == 0) return false;   // no loopback group alive
+    std::lock_guard<std::mutex> lk(g_nopdl_mu);
+    for (cudaStream_t x : g_nopdl)
+        if (x == st) return true;
     return false;
 }
 void register_no_pdl_stream(cudaStream_t st) {
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
-    const int n = g_nnopdl.load();
-    if (n < 64) {
-        g_nopdl[n] = st;
-        g_nnopdl.store(n + 1, std::memory_order_release);
-    }
+    std::lock_guard<std::mutex> lk(g_nopdl_mu);
+    g_nopdl.push_back(st);
+    g_nopdl_n.store((int)g_nopdl.size(), std::memory_order_release);
+}
+void release_no_pdl_stream(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_nopdl_mu);
+    for (size_t i = 0; i < g_nopdl.size(); ++i)
+        if (g_nopdl[i] == st) {
+            g_nopdl[i] = g_nopdl.back();
+            g_nopdl.pop_back();
+            g_nopdl_n.store((int)g_nopdl.size(), std::memory_order_release);
+            return;
+        }
 }
 // =============================================================================
 // Multiplicative Schwarz colour step
