@@ -182,7 +182,8 @@ typedef struct {
     int32_t dropped;      /* total columns dropped by the rank test                              */
     double min_rank_ratio;          /* min over parts and kept j of ||v_j|| / ||F_I e_j|| (R7)       */
     int64_t local_factor_bytes;     /* bytes of the stored local operators (device)            */
-    int64_t coarse_factor_bytes;    /* bytes of the stored coarse operator (device)            */
+    int64_t coarse_factor_bytes;    /* bytes of the stored coarse operator (device); with several
+                                       ranks and the sparse coarse solve, this rank's share     */
     int32_t coarse_variant;         /* 1 dense packed inverse, 2 sparse supernodal, 3 three
                                        levels (the second level's own variant in coarse_variant2) */
     int32_t levels;                 /* 2 or 3                                                   */
@@ -190,7 +191,8 @@ typedef struct {
                                        inverse once (dense), or 2|G| + |H| over the fronts
                                        (sparse: G read forward and backward, H backward);
                                        three levels: the second level's local operators twice
-                                       (two sweeps) plus its own coarse solve bytes            */
+                                       (two sweeps) plus its own coarse solve bytes; with several
+                                       ranks (sparse), the bytes this rank reads per solve     */
     int64_t n_c2;                   /* three levels: coarse unknowns of the second level       */
     int32_t nparts2, ncolours2;     /* three levels: second-level parts and colours            */
     int32_t coarse_variant2;        /* three levels: the second level's coarse variant (1, 2)  */

@@ -6,12 +6,12 @@
 // substitution over 32 x 32 tiles.
 //
 // Factor storage (one factor after another in ddg_ctx::d_tiles at the local
-// op's tile_off): tile rows I = 0 .. nT-1, tiles J = 0 .. I, row-major over the
-// lower triangle -- tile (I, J) at tile_off + (I (I + 1) / 2 + J) * 1024, each
-// tile column-major like the SYMV tiles (element (i, j) at j * 32 + i).
-// Off-diagonal tiles hold L_IJ.  The diagonal tile I holds T_I with
-//     lower(T_I) (diagonal included) = L_II^{-1},  strict upper(T_I) = L_II^{-T},
-// so both substitutions are row-wise dot products within a warp:
+// op's tile_off): tile rows I = 0 .. nT-1 at chol_row_off(I) (ddg_internal.h),
+// each row the I full tiles L_IJ (J < I, tile (I, J) at + J * 1024, column-major
+// like the SYMV tiles: element (i, j) at j * 32 + i) and then D_I = L_II^{-1}
+// as a packed lower triangle (element (i, j), i >= j, at diag_col_off(j) + i - j;
+// 4224 B instead of 8 KB, so a 5-tile-row factor (C3) fits twice per SM when
+// staged).  Both substitutions are dot products within a warp:
 //     forward  y_I = L_II^{-1} (s_I - sum_{J<I} L_IJ y_J)
 //     back     x_J = L_JJ^{-T} (y_J - sum_{I>J} L_IJ^T x_I)
 // (the inverted 32 x 32 diagonal blocks remove the scalar recurrence inside a
@@ -153,11 +153,20 @@ __global__ void k_chol_pack(const int32_t* __restrict__ op_ids, const OpDesc* __
         while ((I + 1) * (I + 2) / 2 <= t) ++I;
         const int J = t - I * (I + 1) / 2;
         const double* src = M + ((int64_t)J * op.nT + I) * TILE_ELEMS;
-        double* dst = out + op.tile_off + (int64_t)t * TILE_ELEMS;
-        for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
-            const int i = e % TILE, j = e / TILE;
-            const bool ok = I * TILE + i < op.m && J * TILE + j < op.m;
-            dst[e] = ok ? src[e] : 0.0;
+        double* dst = out + op.tile_off + chol_row_off(I) + (int64_t)J * TILE_ELEMS;
+        if (J < I) {
+            for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
+                const int i = e % TILE, j = e / TILE;
+                const bool ok = I * TILE + i < op.m && J * TILE + j < op.m;
+                dst[e] = ok ? src[e] : 0.0;
+            }
+        } else {                       // D_I packed lower (the lower part of T_I)
+            for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
+                const int i = e % TILE, j = e / TILE;
+                if (i < j) continue;
+                const bool ok = I * TILE + i < op.m;
+                dst[diag_col_off(j) + i - j] = ok ? src[e] : 0.0;
+            }
         }
     }
 }
@@ -171,7 +180,7 @@ __global__ void k_chol_pack(const int32_t* __restrict__ op_ids, const OpDesc* __
 // Otherwise the tiles are read from global memory by both passes (the back
 // pass mostly from L2).
 constexpr int CHOL_WARPS = 8;
-constexpr int CHOL_STAGE_T = 6;    // 21 tiles = 168 KB
+constexpr int CHOL_STAGE_T = 6;    // 15 full tiles + 6 packed diagonals = 148 KB (C3, 5 rows: 103 KB, two CTAs per SM)
 template <bool STAGED>
 __device__ __forceinline__ double ldt(const double* p) {
     if constexpr (STAGED) return *p;
@@ -188,20 +197,20 @@ k_chol_solve(const OpDesc* __restrict__ ops, int op_begin, const double* __restr
     if (*done) return;
     const OpDesc op = ops[op_begin + blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ntl = op.nT * (op.nT + 1) / 2;
-    double* tiles = sm;                                  // STAGED: ntl tiles
-    double* y = sm + (STAGED ? (int64_t)ntl * TILE_ELEMS : 0);   // mp: s, then y, then x (in place)
+    double* tiles = sm;                                  // STAGED: the whole factor
+    double* y = sm + (STAGED ? chol_doubles(op.nT) : 0); // mp: s, then y, then x (in place)
     double* part = y + op.mp;                            // CHOL_WARPS x 32 partial rows
+    double* dsm = part + CHOL_WARPS * TILE;              // !STAGED: a packed diagonal block, for the
+                                                         // back pass's column walk (coalesced load)
     const double* L = STAGED ? tiles : fac + op.tile_off;
     if constexpr (STAGED) {
         if (threadIdx.x == 0) {
             for (int I = 0; I < op.nT; ++I) mbar_init(&bar[I], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             for (int I = 0; I < op.nT; ++I) {
-                const unsigned bytes = (unsigned)(I + 1) * TILE_ELEMS * 8;
+                const unsigned bytes = (unsigned)(chol_row_off(I + 1) - chol_row_off(I)) * 8;
                 mbar_expect_tx(&bar[I], bytes);
-                bulk_g2s(tiles + (int64_t)(I * (I + 1) / 2) * TILE_ELEMS,
-                         fac + op.tile_off + (int64_t)(I * (I + 1) / 2) * TILE_ELEMS, bytes, &bar[I]);
+                bulk_g2s(tiles + chol_row_off(I), fac + op.tile_off + chol_row_off(I), bytes, &bar[I]);
             }
         }
     }
@@ -210,7 +219,7 @@ k_chol_solve(const OpDesc* __restrict__ ops, int op_begin, const double* __restr
     // forward: L y = s
     for (int I = 0; I < op.nT; ++I) {
         if constexpr (STAGED) mbar_wait(&bar[I], 0);
-        const double* row = L + (int64_t)(I * (I + 1) / 2) * TILE_ELEMS;
+        const double* row = L + chol_row_off(I);
         double acc = 0.0;
         for (int J = warp; J < I; J += CHOL_WARPS) {
             const double* T = row + (int64_t)J * TILE_ELEMS;
@@ -223,12 +232,12 @@ k_chol_solve(const OpDesc* __restrict__ ops, int op_begin, const double* __restr
         if (warp == 0) {
             double t = y[I * TILE + lane];
             for (int w = 0; w < CHOL_WARPS; ++w) t -= part[w * TILE + lane];
-            const double* D = row + (int64_t)I * TILE_ELEMS;
+            const double* D = row + (int64_t)I * TILE_ELEMS;     // packed lower D_I
             double yi = 0.0;
 #pragma unroll
             for (int j = 0; j < TILE; ++j) {
                 const double tj = __shfl_sync(FULL, t, j);
-                if (j <= lane) yi += ldt<STAGED>(D + j * TILE + lane) * tj;
+                if (j <= lane) yi += ldt<STAGED>(D + diag_col_off(j) + lane - j) * tj;
             }
             y[I * TILE + lane] = yi;
         }
@@ -240,7 +249,7 @@ k_chol_solve(const OpDesc* __restrict__ ops, int op_begin, const double* __restr
 #pragma unroll
         for (int j = 0; j < TILE; ++j) v[j] = 0.0;
         for (int I = J + 1 + warp; I < op.nT; I += CHOL_WARPS) {
-            const double* T = L + ((int64_t)(I * (I + 1) / 2) + J) * TILE_ELEMS;
+            const double* T = L + chol_row_off(I) + (int64_t)J * TILE_ELEMS;
             const double xi = y[I * TILE + lane];
 #pragma unroll
             for (int j = 0; j < TILE; ++j) v[j] += ldt<STAGED>(T + j * TILE + lane) * xi;
@@ -255,12 +264,17 @@ k_chol_solve(const OpDesc* __restrict__ ops, int op_begin, const double* __restr
         if (warp == 0) {
             double t = y[J * TILE + lane];
             for (int w = 0; w < CHOL_WARPS; ++w) t -= part[w * TILE + lane];
-            const double* D = L + ((int64_t)(J * (J + 1) / 2) + J) * TILE_ELEMS;
+            const double* D = L + chol_row_off(J) + (int64_t)J * TILE_ELEMS;   // packed lower D_J
+            if constexpr (!STAGED) {      // lane j reads column j of D_J: stage it in shared memory
+                for (int k = lane; k < DIAG_ELEMS; k += TILE) dsm[k] = __ldg(D + k);
+                __syncwarp();
+                D = dsm;
+            }
             double xj = 0.0;
 #pragma unroll
             for (int j = 0; j < TILE; ++j) {
                 const double tj = __shfl_sync(FULL, t, j);
-                if (j >= lane) xj += ldt<STAGED>(D + j * TILE + lane) * tj;
+                if (j >= lane) xj += D[diag_col_off(lane) + j - lane] * tj;   // D_J(j, lane), shared memory
             }
             y[J * TILE + lane] = xj;
         }
@@ -284,7 +298,7 @@ void launch_chol_solve(cudaStream_t st, const OpDesc* ops, int op_begin, int nop
     const int maxT = max_mp / TILE;
     const bool staged = maxT <= CHOL_STAGE_T && !getenv("DDG_CHOL_GLOBAL");
     const size_t smem = (size_t)(max_mp + CHOL_WARPS * TILE) * sizeof(double) +
-                        (staged ? (size_t)maxT * (maxT + 1) / 2 * TILE_ELEMS * sizeof(double) : 0);
+                        (staged ? (size_t)chol_doubles(maxT) : (size_t)DIAG_ELEMS) * sizeof(double);
     if (smem > 48 * 1024) {
         if (staged) DDG_MAX_DYN_SMEM(k_chol_solve<true>);
         else DDG_MAX_DYN_SMEM(k_chol_solve<false>);

@@ -307,6 +307,12 @@ void launch_galerkin_blocks(cudaStream_t st, int nblocks, int maxk, const int32_
                             const int64_t* boff, const int64_t* bptr, const int32_t* bidx, const int32_t* cptr,
                             const int64_t* qoff, const double* Q, const int32_t* part, const int32_t* bpos,
                             const int32_t* rp, const int32_t* col, const double* val, double* out);
+// Cholesky factor storage (chol.cu): tile row I holds I full 32 x 32 tiles L_IJ
+// (J < I) and then the packed lower triangle of L_II^{-1} (DIAG_ELEMS doubles)
+__host__ __device__ inline int64_t chol_row_off(int I) {
+    return (int64_t)TILE_ELEMS * I * (I - 1) / 2 + (int64_t)DIAG_ELEMS * I;
+}
+__host__ __device__ inline int64_t chol_doubles(int nT) { return chol_row_off(nT); }
 // local_variant = DDG_LOCAL_CHOLESKY (chol.cu): tile Cholesky of nmat tiled
 // dense matrices (one CTA each), packing of the lower tiles at each op's
 // tile_off, and one colour's forward + back substitutions (one CTA per op)

@@ -639,7 +639,7 @@ static int build_plans(ddg_ctx* c) {
                 add_op(c, (int32_t)m, 0, off, true, false);
                 OpDesc& op = c->ops.back();
                 op.tile_off = t0;
-                c->tiles_doubles = t0 + (int64_t)op.nT * (op.nT + 1) / 2 * TILE_ELEMS;
+                c->tiles_doubles = t0 + chol_doubles(op.nT);
                 c->part_doubles = p0;
             } else {
                 add_op(c, (int32_t)m, 0, off, true, compact);
@@ -778,7 +778,7 @@ static int invert_locals(ddg_ctx* c) {
         if (c->chol) {
             int maxT = 0;
             for (int32_t t : nTs) maxT = std::max(maxT, (int)t);
-            launch_chol_pack(c->stream, (int)nb, maxT * (maxT + 1) / 2, d_ids, c->d_ops, scratch, d_soff, c->d_tiles);
+            launch_chol_pack(c->stream, (int)nb, maxT * (maxT + 1) / 2, d_ids, c->d_ops, scratch, d_soff, c->d_tiles);   // tiles of the largest
         } else {
             launch_pack(c->stream, (int)nb, d_ids, c->d_ops, c->d_items, scratch, d_soff, c->d_tiles);
         }
@@ -1506,7 +1506,7 @@ extern "C" int ddg_setup(int64_t n, const int64_t* row_ptr, const int32_t* col, 
     for (int q = 0; q < (int)c->op_sub.size(); ++q) {
         const OpDesc& op = c->ops[q];
         if (c->chol) {
-            c->local_bytes += (int64_t)op.nT * (op.nT + 1) / 2 * TILE_ELEMS * 8;
+            c->local_bytes += chol_doubles(op.nT) * 8;
             continue;
         }
         for (int t = 0; t < op.nitems; ++t) {

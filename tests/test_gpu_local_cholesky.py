@@ -64,9 +64,9 @@ def test_cholesky_pcg_parity(name, path, monkeypatch):
     m = min(len(hist), len(histo))
     assert np.max(np.abs(hist[:m] - histo[:m]) / histo[:m]) <= H_TOL
     assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
-    # factor storage: nT (nT + 1) / 2 full tiles per subdomain
+    # factor storage: nT (nT - 1) / 2 full tiles and nT packed diagonal blocks per subdomain
     nT = (s.subdomain_sizes() + 31) // 32
-    assert s.info.local_factor_bytes == int(np.sum(nT * (nT + 1) // 2)) * 8192
+    assert s.info.local_factor_bytes == int(np.sum(nT * (nT - 1) // 2 * 8192 + nT * 528 * 8))
 
 
 @pytest.mark.parametrize("name", list(CASES))
