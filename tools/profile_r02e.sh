@@ -20,3 +20,6 @@ echo done
 if [ -n "$RING2_CAPTURE" ]; then
   timeout 600 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:k_symv_ring2 --launch-skip 5 -c 1 -o gpurun_out/ring2_full_C5_${T} -f python tools/prof_solve.py C5 > gpurun_out/ncu_ring2_${T}.log 2>&1
 fi
+if [ -n "$CHOL_BENCH" ]; then
+  for c in C2 C4; do timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --local-variant cholesky > gpurun_out/bench_${T}_chol_$c.json 2> gpurun_out/bench_${T}_chol_$c.err; done
+fi
