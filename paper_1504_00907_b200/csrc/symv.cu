@@ -740,9 +740,14 @@ __global__ void __launch_bounds__(RING2_THREADS, 1)
 k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items, int item_begin,
              const int32_t* __restrict__ cta_part, const double* __restrict__ tiles, const double* __restrict__ s,
              const int32_t* __restrict__ oidx, double* __restrict__ z, double* __restrict__ y_out,
-             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr, int pf, int split) {
+             double* __restrict__ partials, const int32_t* done, int nst, int nb, int maxr, int pf, int split_) {
     pdl_wait();
     constexpr int SLOT = RT * TILE_ELEMS;
+    const bool copy_only = split_ & 0x100;                       // DDG_RING2_COPYONLY: bandwidth probe (debug)
+    const bool merge = split_ & 0x200;                           // DDG_RING2_MERGE=1: one copy per contiguous run (measured no gain)
+    // DDG_RING2_BARE_EPI (probes): 1 the epilogue only hands buffers back; 2 it skips the tail strip only
+    const bool bare_epi = split_ & 0x400, no_strip = split_ & 0xC00;
+    const int split = split_ & 0xff;
     if (*done) return;
     extern __shared__ __align__(128) double rsm[];
     double* ring = rsm;                                          // [nst][SLOT]
@@ -833,7 +838,26 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
                     for (int o = 1; o < RT; o <<= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
                     if (lane == 0) mbar_expect_tx(&full[slot], bytes);
                     __syncwarp();
-                    if (lane < nt) bulk_g2s(dst + lane * TILE_ELEMS, src + toff, tb, &full[slot]);
+                    if (merge) {
+                        // one copy per run of stream-contiguous tiles: full tiles
+                        // of a row are adjacent in the packed operator and in the
+                        // slot; a (shorter, packed) diagonal tile ends a run
+                        const unsigned ptb = __shfl_up_sync(FULL, tb, 1);
+                        const bool start = lane < nt && (lane == 0 || ptb != (unsigned)TILE_ELEMS * 8u);
+                        unsigned rb = 0;
+                        bool open = true;
+#pragma unroll
+                        for (int k = 0; k < RT; ++k) {              // run bytes from this lane on
+                            const unsigned tk = __shfl_sync(FULL, tb, k);
+                            if (k >= lane && k < nt && open) {
+                                rb += tk;
+                                open = tk == (unsigned)TILE_ELEMS * 8u;
+                            }
+                        }
+                        if (start) bulk_g2s(dst + lane * TILE_ELEMS, src + toff, rb, &full[slot]);
+                    } else if (lane < nt) {
+                        bulk_g2s(dst + lane * TILE_ELEMS, src + toff, tb, &full[slot]);
+                    }
                 }
                 if (++slot == (unsigned)nst) { slot = 0; ++sph; }
             }
@@ -851,7 +875,7 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
             const int rows_t = rows_r + (it.tri ? 0 : (it.J1 - it.J0) * TILE);
             const int g0 = it.I0 * TILE;
             const int nr = min(rows_t, op.m - g0);
-            const bool scat = it.part_off < 0 && op.out_mode == 0;
+            const bool scat = it.part_off < 0 && op.out_mode == 0 && !bare_epi;
             int ix[RING_MAX_ROWS / 32];
             double zv[RING_MAX_ROWS / 32];
             if (scat) {
@@ -869,7 +893,7 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
             // S(i, :) s are per-lane partials reduced over the warp
             double* yT = yt_sm + (size_t)e * maxr;             // row 32 cb + lane: this lane's own entries
             double ys = 0.0;
-            const int th = it.tail, W = (it.I1 - it.I0 - 1) * TILE;
+            const int th = no_strip ? 0 : it.tail, W = (it.I1 - it.I0 - 1) * TILE;
             if (th) {
                 const double* S = tiles + it.tile_off + item_tile_off(it, (it.I1 - it.I0 - 1) * (it.I1 - it.I0) / 2,
                                                                       it.I1 - 1);
@@ -899,6 +923,11 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
                 }
             }
             mbar_wait(&pdone[b], ph & 1);
+            if (bare_epi) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pfree[b]);
+                continue;
+            }
             const double* pr = pr_sm + (size_t)b * maxr;
             const double* pc = pc_sm + (size_t)b * maxr;
             const double* pr2 = pr2_sm + (size_t)b * maxr;
@@ -983,7 +1012,7 @@ k_symv_ring2(const OpDesc* __restrict__ ops, const ItemDesc* __restrict__ items,
         for (int l0 = 0; l0 < ntiles; l0 += RT) {
             mbar_wait(&full[slot], sph & 1);
             const double* C = ring + (size_t)slot * SLOT;
-            while (l >= 0 && l < l0 + RT) {
+            while (!copy_only && l >= 0 && l < l0 + RT) {
                 const double* T = C + (l - l0) * TILE_ELEMS;
                 const bool diag = tri && r == c;
                 if (!colw) {
@@ -1327,7 +1356,11 @@ void symv_ring_init() {
     g_pdl = getenv("DDG_PDL") ? (atoi(getenv("DDG_PDL")) != 0) : 1;
     // DDG_RING_WHOLE: 0 off, 1 (default) one copy per item, n > 1 one copy per tile row
     g_ring_whole = getenv("DDG_RING_WHOLE") ? atoi(getenv("DDG_RING_WHOLE")) : 1;
-    g_ring2_split = (getenv("DDG_RING2_SPLIT") && atoi(getenv("DDG_RING2_SPLIT")) == 1) ? 1 : 2;
+    g_ring2_split = ((getenv("DDG_RING2_SPLIT") && atoi(getenv("DDG_RING2_SPLIT")) == 1) ? 1 : 2) |
+                    ((getenv("DDG_RING2_COPYONLY") && atoi(getenv("DDG_RING2_COPYONLY")) != 0) ? 0x100 : 0) |
+                    ((getenv("DDG_RING2_MERGE") && atoi(getenv("DDG_RING2_MERGE")) != 0) ? 0x200 : 0) |
+                    (!getenv("DDG_RING2_BARE_EPI") ? 0 : atoi(getenv("DDG_RING2_BARE_EPI")) == 1 ? 0x400
+                     : atoi(getenv("DDG_RING2_BARE_EPI")) == 2 ? 0x800 : 0);
     g_ring_pf = getenv("DDG_RING_PF") ? atoi(getenv("DDG_RING_PF")) : 0;      // ... by k_symv_ring2
     g_compact = compact;
 
